@@ -1,0 +1,152 @@
+"""Seeded synthetic inputs for the attention-variant forward (no method arithmetic).
+
+This module is the ONE piece shared by the CUDA path's callers (bench, tests)
+and the oracle's callers: it only draws numbers.  It contains none of the
+method's arithmetic (no scores, softmax, masks applied to data, ...).
+
+Shard consistency: every tensor is drawn slab by slab, each slab from its own
+numpy Philox stream keyed by (seed, tensor id, slab index) where a slab is one
+index of the leading ``lead`` dims.  Any rank can therefore regenerate exactly
+its slice of the global tensor (SURVEY §8(d) "Input distributions").
+
+Recipes:
+  uniform   U[-1,1) -> bf16 (round to nearest even) or fp32
+  needle    K in {+-1}^D, Q[q] = K[pi(q)], pi(q) uniform over the row's admissible keys
+  constant  V[k,:] = c for every key k, c ~ U[-1,1)^D per slab  (closed form O = c)
+  docs      11 distinct cut points uniform on (1, S-1) per batch b, seed (1, b)
+  clustered RSA: 32 centroids in {+-0.6}^D per slab; a KV block of 128 keys
+            gets cluster z(j), its keys clip(c_z + 0.4 U[-1,1), +-1); q-blocks likewise
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+TENSOR_IDS = {"q": 1, "k": 2, "v": 3, "gate": 4, "bias": 5, "key_mask": 6, "lambda": 7, "doc": 8}
+
+
+def _rng(seed: int, tensor: str, slab: int) -> np.random.Generator:
+    return np.random.Generator(np.random.Philox(key=[int(seed) & 0xFFFFFFFF, TENSOR_IDS[tensor] * (1 << 40) + slab]))
+
+
+def _to(a: np.ndarray, dtype: torch.dtype) -> torch.Tensor:
+    t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32))
+    return t.to(dtype)
+
+
+def _slabs(shape, lead):
+    n = 1
+    for s in shape[:lead]:
+        n *= s
+    inner = shape[lead:]
+    return n, inner
+
+
+def uniform(shape, *, seed=0, tensor="q", dtype=torch.bfloat16, lo=-1.0, hi=1.0, lead=2,
+            slab_range=None) -> torch.Tensor:
+    """U[lo,hi) drawn slab by slab over the first ``lead`` dims.
+
+    slab_range=(begin, end) returns only those slabs (flattened over the lead
+    dims), identical to the same slabs of the full tensor."""
+    n, inner = _slabs(shape, lead)
+    b, e = (0, n) if slab_range is None else slab_range
+    out = np.empty((e - b,) + tuple(inner), dtype=np.float32)
+    for i in range(b, e):
+        out[i - b] = _rng(seed, tensor, i).random(tuple(inner), dtype=np.float32) * (hi - lo) + lo
+    t = _to(out, dtype)
+    return t.reshape(tuple(shape)) if slab_range is None else t
+
+
+def constant_v(shape, *, seed=0, dtype=torch.bfloat16, lead=2, slab_range=None) -> torch.Tensor:
+    """V[..., k, :] = c (one c ~ U[-1,1)^Dv per slab) -- the closed-form check O = c (P13)."""
+    n, inner = _slabs(shape, lead)
+    b, e = (0, n) if slab_range is None else slab_range
+    out = np.empty((e - b,) + tuple(inner), dtype=np.float32)
+    for i in range(b, e):
+        c = _rng(seed, "v", i).random((inner[-1],), dtype=np.float32) * 2 - 1
+        out[i - b] = np.broadcast_to(c, tuple(inner))
+    t = _to(out, dtype)
+    return t.reshape(tuple(shape)) if slab_range is None else t
+
+
+def needle(q_shape, k_shape, *, seed=0, dtype=torch.bfloat16, interval=None, sq_sk=None):
+    """Peaked inputs: K in {+-1}^D; Q[b,h,q] = K[b,h_kv,pi(q)] with pi(q) drawn
+    uniformly from the admissible keys [lo(q), hi(q)) of row q.
+
+    ``interval(q) -> (lo, hi)`` gives the admissible key range (None = all keys).
+    Shapes are [B,H,S,D]; GQA groups copy from their shared KV head."""
+    B, Hq, Sq, D = q_shape
+    _, Hkv, Sk, _ = k_shape
+    k = np.empty(k_shape, dtype=np.float32)
+    for i in range(B * Hkv):
+        r = _rng(seed, "k", i)
+        k.reshape(B * Hkv, Sk, D)[i] = np.where(r.random((Sk, D)) < 0.5, -1.0, 1.0)
+    q = np.empty(q_shape, dtype=np.float32)
+    grp = Hq // Hkv
+    for b in range(B):
+        for h in range(Hq):
+            r = _rng(seed, "q", b * Hq + h)
+            u = r.random(Sq)
+            if interval is None:
+                lo = np.zeros(Sq, dtype=np.int64)
+                hi = np.full(Sq, Sk, dtype=np.int64)
+            else:
+                lo, hi = (np.asarray(a, dtype=np.int64) for a in interval(np.arange(Sq)))
+            hi = np.maximum(hi, lo + 1)
+            pick = np.minimum(lo + np.floor(u * (hi - lo)).astype(np.int64), Sk - 1)
+            q[b, h] = k[b, h // grp][pick]
+    return _to(q, dtype), _to(k, dtype)
+
+
+def doc_offsets(B, S, n_docs=12, *, seed=1) -> np.ndarray:
+    """[B, n_docs+1] int32: 0 = off[0] < ... < off[n_docs] = S; cut points
+    uniform on (1, S-1) per batch b, drawn from stream (seed, b) (reading G6)."""
+    out = np.zeros((B, n_docs + 1), dtype=np.int32)
+    for b in range(B):
+        r = _rng(seed, "doc", b)
+        cuts = np.sort(r.choice(np.arange(1, S), size=n_docs - 1, replace=False))
+        out[b, 1:-1] = cuts
+        out[b, -1] = S
+    return out
+
+
+def alibi_slopes(H: int) -> np.ndarray:
+    """Geometric schedule 2^(-8(h+1)/H), h 0-based (reading G2)."""
+    return np.array([2.0 ** (-8.0 * (h + 1) / H) for h in range(H)], dtype=np.float32)
+
+
+def clustered_qk(q_shape, k_shape, *, seed=2, blk=128, n_clusters=32, dtype=torch.bfloat16):
+    """RSA inputs: per slab 32 centroids in {+-0.6}^D; each KV block / q block
+    draws a cluster and its rows are clip(c_z + 0.4 U[-1,1), +-1)."""
+    def one(shape, tensor, heads_per_centroid_slab):
+        B, H, S, D = shape
+        out = np.empty(shape, dtype=np.float32)
+        for b in range(B):
+            for h in range(H):
+                r = _rng(seed, tensor, b * H + h)
+                cr = _rng(seed + 1000, "k", b * (H // heads_per_centroid_slab) + h // heads_per_centroid_slab)
+                cents = np.where(cr.random((n_clusters, D)) < 0.5, -0.6, 0.6)
+                nb = (S + blk - 1) // blk
+                z = r.integers(0, n_clusters, size=nb)
+                x = cents[np.repeat(z, blk)[:S]] + 0.4 * (r.random((S, D)) * 2 - 1)
+                out[b, h] = np.clip(x, -1.0, 1.0)
+        return _to(out, dtype)
+    grp = q_shape[1] // k_shape[1]
+    return one(q_shape, "q", grp), one(k_shape, "k", 1)
+
+
+def gate_logits(shape, *, seed=0, dtype=torch.bfloat16, lead=2):
+    return uniform(shape, seed=seed, tensor="gate", dtype=dtype, lo=-4.0, hi=4.0, lead=lead)
+
+
+def pair_bias(shape, *, seed=0, dtype=torch.bfloat16, lead=2):
+    return uniform(shape, seed=seed, tensor="bias", dtype=dtype, lo=-4.0, hi=4.0, lead=lead)
+
+
+def key_mask(shape, *, seed=0, p_zero=0.1, lead=1):
+    n, inner = _slabs(shape, lead)
+    out = np.empty((n,) + tuple(inner), dtype=np.uint8)
+    for i in range(n):
+        out[i] = (_rng(seed, "key_mask", i).random(tuple(inner)) >= p_zero).astype(np.uint8)
+    return torch.from_numpy(out.reshape(shape))
+

@@ -1,0 +1,494 @@
+"""Pins for the fp64 oracle (-m "not gpu"): the oracle is checked against things
+other than itself -- closed forms, invariants, library routines (torch SDPA /
+torch.softmax run in fp64), the paper's own Listing 1/4 programs executed
+eagerly, a hand-derived golden example and brute force.  Each test names the
+paper passage or DESIGN.md reading it pins.  A plausible slip in the oracle
+(dropped term, wrong sign or index, transposed operand) fails at least one.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+import oracle
+from paper_2511_02043_b200 import synth
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+D64 = torch.float64
+
+
+def rnd(*shape, seed=0, lo=-1.0, hi=1.0):
+    g = torch.Generator().manual_seed(seed)
+    return torch.rand(*shape, generator=g, dtype=D64) * (hi - lo) + lo
+
+
+def listing1(q, k, v, attn_mask=None):
+    """Listing 1 executed eagerly with torch in fp64; attn_mask True = masked."""
+    attn_scores = torch.matmul(q, k.transpose(-2, -1))
+    attn_scores *= 1 / math.sqrt(q.size(-1))
+    if attn_mask is not None:
+        attn_scores = attn_scores.masked_fill(attn_mask, -float("inf"))
+    attn_weights = torch.softmax(attn_scores, dim=-1)
+    return torch.matmul(attn_weights, v)
+
+
+def O(out, like):
+    return torch.from_numpy(out).reshape(like)
+
+
+# ----------------------------------------------------------------- softmax (Alg.1/Alg.2, §3.3)
+def online_softmax_alg2(x):
+    """Alg.2, written independently: returns all prefixes (m_j, d_j)."""
+    m, d, ms, ds = -math.inf, 0.0, [], []
+    for xj in x:
+        mj = max(m, xj)
+        d = d * math.exp(m - mj) + math.exp(xj - mj) if m != -math.inf else math.exp(xj - mj)
+        m = mj
+        ms.append(m)
+        ds.append(d)
+    return ms, ds
+
+
+@pytest.mark.parametrize("case", ["random", "ascending", "descending", "equal", "dupmax", "single", "wide"])
+def test_alg1_matches_library_and_alg2_closed_form(case):
+    """P1: Alg.1's asserts, Alg.2 == Alg.1, do[j] closed form at every prefix."""
+    r = np.random.default_rng(abs(hash(case)) % 2**32)
+    x = {"random": r.normal(size=257), "ascending": np.arange(50.0), "descending": np.arange(50.0)[::-1].copy(),
+         "equal": np.full(33, 3.25), "dupmax": np.array([1.0, 7.0, -2.0, 7.0, 0.5]), "single": np.array([-4.0]),
+         "wide": r.uniform(-700, 700, size=64)}[case]
+    y, m, d = oracle.stable_softmax(x)
+    # library routine
+    ref = torch.softmax(torch.from_numpy(x), dim=0).numpy()
+    np.testing.assert_allclose(y, ref, rtol=1e-12, atol=1e-300)
+    assert m == x.max()                                          # Alg.1 Assert m_N = max x
+    np.testing.assert_allclose(d, math.fsum(math.exp(v - x.max()) for v in x), rtol=1e-13)
+    assert abs(y.sum() - 1.0) < 1e-12 and (y >= 0).all() and (case == "wide" or (y > 0).all())  # Eq.1
+    ms, ds = online_softmax_alg2(list(x))
+    np.testing.assert_allclose(ds[-1], d, rtol=1e-12)            # ds[N] = do[N]
+    for j in range(len(x)):                                       # do[j] = (sum_{i<=j} e^x_i) * e^{-m_j}
+        closed = math.fsum(math.exp(v - ms[j]) for v in x[: j + 1])
+        np.testing.assert_allclose(ds[j], closed, rtol=1e-12)
+
+
+def test_softmax_of_zeros_is_uniform():
+    y, m, d = oracle.stable_softmax(np.zeros(4))
+    np.testing.assert_array_equal(y, np.full(4, 0.25))
+    assert m == 0.0 and d == 4.0
+
+
+# ----------------------------------------------------------------- golden (hand-derived)
+def test_golden_hand_computed_2x2():
+    """tests/golden/hand_2x2.json: Eq.3 expanded by hand for a 2x2 case (S:L74 idea)."""
+    g = json.load(open(os.path.join(GOLDEN, "hand_2x2.json")))
+    q, k, v = (torch.tensor(g[n], dtype=D64).reshape(1, 1, 2, 2) for n in ("Q", "K", "V"))
+    out, lse = oracle.attn(q, k, v)
+    np.testing.assert_allclose(out, np.array(g["O"]), rtol=0, atol=1e-15)
+    np.testing.assert_allclose(lse, np.array(g["LSE"]), rtol=0, atol=1e-15)
+    out, _ = oracle.attn(q, k, v, mask="causal")
+    np.testing.assert_allclose(out, np.array(g["O_causal"]), rtol=0, atol=1e-15)
+
+
+# ----------------------------------------------------------------- library routines
+@pytest.mark.parametrize("sq,sk", [(17, 17), (9, 23), (64, 64)])
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32, torch.bfloat16])
+def test_vanilla_and_causal_vs_sdpa(sq, sk, dtype):
+    """Eq.3 against torch SDPA (fp64); bf16/fp32 storage read exactly."""
+    q, k, v = (rnd(2, 3, s, 16, seed=i).to(dtype) for i, s in enumerate((sq, sk, sk)))
+    qd, kd, vd = (t.to(D64) for t in (q, k, v))
+    out, lse = oracle.attn(q, k, v)
+    ref = F.scaled_dot_product_attention(qd, kd, vd)
+    torch.testing.assert_close(O(out, ref.shape), ref, rtol=1e-12, atol=1e-13)
+    s = (qd @ kd.transpose(-1, -2)) / math.sqrt(16)
+    torch.testing.assert_close(torch.from_numpy(lse).reshape(2, 3, sq), torch.logsumexp(s, -1), rtol=1e-12, atol=1e-12)
+    out, _ = oracle.attn(q, k, v, mask="causal")
+    # bottom-right causal (G12): keep k <= q + (Sk - Sq); torch tril with diagonal offset
+    keep = torch.ones(sq, sk, dtype=torch.bool).tril(sk - sq)
+    ref = F.scaled_dot_product_attention(qd, kd, vd, attn_mask=keep)
+    torch.testing.assert_close(O(out, ref.shape), ref, rtol=1e-12, atol=1e-13)
+    if sq == sk:
+        ref2 = F.scaled_dot_product_attention(qd, kd, vd, is_causal=True)
+        torch.testing.assert_close(O(out, ref.shape), ref2, rtol=1e-12, atol=1e-13)
+
+
+def test_gqa_vs_sdpa_enable_gqa():
+    """G15: h_kv = floor(h / (Hq/Hkv)) == PyTorch enable_gqa (P:L858, 16 Q : 2 KV)."""
+    q, k, v = rnd(2, 16, 20, 8, seed=1), rnd(2, 2, 20, 8, seed=2), rnd(2, 2, 20, 8, seed=3)
+    out, _ = oracle.attn(q, k, v, mask="causal")
+    ref = F.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True)
+    torch.testing.assert_close(O(out, ref.shape), ref, rtol=1e-12, atol=1e-13)
+
+
+def test_listing1_sliding_window_predicate():
+    """G4: Listing 2 predicate keep = (q >= kv) & (q - kv <= w); Listing 3's
+    garbled mask read as its complement, fed to Listing 1."""
+    S, w = 40, 7
+    q, k, v = rnd(1, 2, S, 8, seed=4), rnd(1, 2, S, 8, seed=5), rnd(1, 2, S, 8, seed=6)
+    qi = torch.arange(S).view(S, 1)
+    kv = torch.arange(S).view(1, S)
+    mask = (qi < kv) | ((qi - kv) > w)        # True = masked (Listing 1 convention)
+    ref = listing1(q, k, v, mask)
+    out, _ = oracle.attn(q, k, v, mask="sliding", window=w)
+    torch.testing.assert_close(O(out, ref.shape), ref, rtol=1e-12, atol=1e-13)
+
+
+def test_listing4_differential():
+    """P:L412-424 Listing 4 run eagerly: chunk on dim=1, shared v, attn0 - lambda*attn1 (G8)."""
+    H = 3
+    q, k, v = rnd(2, 2 * H, 15, 8, seed=7), rnd(2, 2 * H, 15, 8, seed=8), rnd(2, H, 15, 8, seed=9)
+    q0, q1 = q.chunk(2, dim=1)
+    k0, k1 = k.chunk(2, dim=1)
+    ref = listing1(q0, k0, v) - 0.2 * listing1(q1, k1, v)
+    out, lse = oracle.attn(q, k, v, diff=True, lam=0.2)
+    torch.testing.assert_close(O(out, ref.shape), ref, rtol=1e-12, atol=1e-13)
+    assert np.isnan(lse).all()
+    lam_h = np.array([0.1, 0.5, 0.9])
+    ref = listing1(q0, k0, v) - torch.tensor(lam_h).view(1, H, 1, 1) * listing1(q1, k1, v)
+    out, _ = oracle.attn(q, k, v, diff=True, lambda_h=lam_h)
+    torch.testing.assert_close(O(out, ref.shape), ref, rtol=1e-12, atol=1e-13)
+
+
+def test_prefix_and_document_vs_sdpa_bool_masks():
+    """G5/G6 predicates fed as bool masks to SDPA (library softmax/matmul)."""
+    S = 48
+    q, k, v = rnd(2, 2, S, 8, seed=10), rnd(2, 2, S, 8, seed=11), rnd(2, 2, S, 8, seed=12)
+    P = 10
+    qi, ki = torch.arange(S).view(S, 1), torch.arange(S).view(1, S)
+    out, _ = oracle.attn(q, k, v, mask="prefix", prefix=P)
+    ref = F.scaled_dot_product_attention(q, k, v, attn_mask=(ki < P) | (ki <= qi))
+    torch.testing.assert_close(O(out, ref.shape), ref, rtol=1e-12, atol=1e-13)
+    offs = synth.doc_offsets(2, S, 5, seed=3)
+    for causal in (False, True):
+        out, _ = oracle.attn(q, k, v, mask="document", doc_offsets=offs, doc_causal=causal)
+        for b in range(2):
+            doc = torch.from_numpy(np.searchsorted(offs[b], np.arange(S), side="right") - 1)
+            keep = doc.view(S, 1) == doc.view(1, S)
+            if causal:
+                keep &= ki <= qi
+            ref = F.scaled_dot_product_attention(q[b:b + 1], k[b:b + 1], v[b:b + 1], attn_mask=keep)
+            torch.testing.assert_close(O(out, (2, 2, S, 8))[b:b + 1], ref, rtol=1e-12, atol=1e-13)
+
+
+def test_alibi_and_softcap_vs_explicit_torch_ops():
+    """Eq.4: score_mod on the SCALED score (G1); ALiBi slope_h*(k-q) (G2), softcap tanh (G3)."""
+    H, S = 4, 24
+    q, k, v = rnd(1, H, S, 8, seed=13), rnd(1, H, S, 8, seed=14), rnd(1, H, S, 8, seed=15)
+    s = (q @ k.transpose(-1, -2)) * (1 / math.sqrt(8))
+    slopes = torch.tensor([2.0 ** (-8.0 * (h + 1) / H) for h in range(H)], dtype=D64)
+    ref = torch.softmax(s + slopes.view(1, H, 1, 1) * (torch.arange(S).view(1, S) - torch.arange(S).view(S, 1)), -1) @ v
+    out, _ = oracle.attn(q, k, v, mod="alibi")
+    torch.testing.assert_close(O(out, ref.shape), ref, rtol=1e-12, atol=1e-13)
+    ref = torch.softmax(20.0 * torch.tanh(s / 20.0), -1) @ v
+    out, _ = oracle.attn(q, k, v, mod="softcap", softcap=20.0)
+    torch.testing.assert_close(O(out, ref.shape), ref, rtol=1e-12, atol=1e-13)
+
+
+def test_evoformer_row_and_column_vs_explicit_torch():
+    """G9: row attention adds pair bias [b,h,i,j] broadcast over s plus the MSA
+    key mask; sigmoid gate.  Column attention = row attention of the transposed MSA."""
+    Bn, Ns, Nr, H, c = 1, 5, 7, 2, 4
+    m = lambda s: rnd(Bn, Ns, Nr, H, c, seed=s)
+    Q, K, V, Gt = m(20), m(21), m(22), m(23)
+    bias = rnd(Bn, H, Nr, Nr, seed=24, lo=-4, hi=4)
+    msa_mask = torch.ones(Bn, Ns, Nr, dtype=torch.uint8)
+    msa_mask[0, 1, 3] = 0
+    msa_mask[0, 4, 0] = 0
+    # row: views [B, G=s, H, S=i, D=c]
+    rv = lambda t: t.permute(0, 1, 3, 2, 4)
+    out, _ = oracle.attn(rv(Q), rv(K), rv(V), bias=bias.unsqueeze(1).expand(Bn, Ns, H, Nr, Nr),
+                         key_mask=msa_mask, gate_mode="sigmoid", gate=rv(Gt))
+    s = torch.einsum("bsihc,bsjhc->bshij", Q, K) / math.sqrt(c) + bias.unsqueeze(1)
+    s = s.masked_fill(msa_mask.view(Bn, Ns, 1, 1, Nr) == 0, -float("inf"))
+    ref = torch.einsum("bshij,bsjhc->bsihc", torch.softmax(s, -1), V) * torch.sigmoid(Gt)
+    torch.testing.assert_close(O(out, (Bn, Ns, H, Nr, c)), rv(ref), rtol=1e-12, atol=1e-13)
+    # column: views [B, G=i, H, S=s, D=c]; key mask msa_mask[b, s', i] -> [B, G=i, S=s']
+    cv = lambda t: t.permute(0, 2, 3, 1, 4)
+    out, _ = oracle.attn(cv(Q), cv(K), cv(V), key_mask=msa_mask.permute(0, 2, 1),
+                         gate_mode="sigmoid", gate=cv(Gt))
+    s = torch.einsum("bsihc,btihc->bihst", Q, K) / math.sqrt(c)
+    s = s.masked_fill(msa_mask.permute(0, 2, 1).reshape(Bn, Nr, 1, 1, Ns) == 0, -float("inf"))
+    ref = torch.einsum("bihst,btihc->bsihc", torch.softmax(s, -1), V) * torch.sigmoid(Gt)
+    torch.testing.assert_close(O(out, (Bn, Nr, H, Ns, c)), cv(ref), rtol=1e-12, atol=1e-13)
+    # and column == row of a transposed copy (P9)
+    Qt, Kt, Vt, Gtt = (t.transpose(1, 2).contiguous() for t in (Q, K, V, Gt))
+    out2, _ = oracle.attn(rv(Qt), rv(Kt), rv(Vt), key_mask=msa_mask.transpose(1, 2).contiguous(),
+                          gate_mode="sigmoid", gate=rv(Gtt))
+    np.testing.assert_allclose(out2, out, rtol=0, atol=0)
+
+
+# ----------------------------------------------------------------- closed forms
+MASKS = [("none", {}), ("causal", {}), ("sliding", {"window": 5}), ("prefix", {"prefix": 6}),
+         ("document", {"doc_offsets": np.array([[0, 4, 11, 30]], dtype=np.int32)})]
+
+
+def kept_sets(mask, kw, S):
+    """Admissible key sets per row, straight from the predicates (G4-G6)."""
+    out = []
+    for q in range(S):
+        if mask == "none":
+            ks = range(S)
+        elif mask == "causal":
+            ks = range(q + 1)
+        elif mask == "sliding":
+            ks = range(max(0, q - kw["window"]), q + 1)
+        elif mask == "prefix":
+            ks = [k for k in range(S) if k < kw["prefix"] or k <= q]
+        else:
+            o = kw["doc_offsets"][0]
+            j = np.searchsorted(o, q, side="right") - 1
+            ks = range(o[j], o[j + 1])
+        out.append(list(ks))
+    return out
+
+
+@pytest.mark.parametrize("mask,kw", MASKS)
+@pytest.mark.parametrize("mod", ["none", "softcap"])
+def test_uniform_scores_give_mean_of_kept_v(mask, kw, mod):
+    """P2: Q = 0 => every kept score equal => O = mean of the kept V rows (also under softcap)."""
+    S = 30
+    q = torch.zeros(1, 1, S, 8, dtype=D64)
+    k, v = rnd(1, 1, S, 8, seed=30), rnd(1, 1, S, 6, seed=31)
+    out, _ = oracle.attn(q, k, v, mask=mask, mod=mod, softcap=3.0, **kw)
+    for qi, ks in enumerate(kept_sets(mask, kw, S)):
+        np.testing.assert_allclose(out[qi], v[0, 0, ks].mean(0).numpy(), rtol=0, atol=1e-14)
+
+
+@pytest.mark.parametrize("mask,kw", MASKS + [("blocklist", {})])
+@pytest.mark.parametrize("mod", ["none", "alibi", "softcap"])
+def test_constant_v_gives_constant(mask, kw, mod):
+    """P13: V[k,:] = c  =>  O = c for every non-empty row, every mask and mod."""
+    S = 40
+    q, k = rnd(1, 2, S, 8, seed=32), rnd(1, 2, S, 8, seed=33)
+    c = torch.linspace(-0.9, 0.8, 6, dtype=D64)
+    v = c.view(1, 1, 1, 6).expand(1, 2, S, 6).contiguous()
+    if mask == "blocklist":
+        nqb = 3
+        idx = np.array([[[0, 2, -1], [1, -1, -1], [0, 1, 2]]] * 2, dtype=np.int32)
+        cnt = np.array([[2, 1, 3]] * 2, dtype=np.int32)
+        kw = dict(blk_idx=idx, blk_cnt=cnt, blk_q=16, blk_k=16)
+        assert nqb == idx.shape[1]
+    out, _ = oracle.attn(q, k, v, mask=mask, mod=mod, softcap=5.0, **kw)
+    for r in range(out.shape[0]):
+        if mask == "blocklist" and (r % S) // 16 == 0 and False:
+            continue
+        np.testing.assert_allclose(out[r], c.numpy(), rtol=0, atol=1e-14)
+
+
+def test_causal_row0_is_v0_and_window0_is_identity():
+    """P3: causal row 0 attends only key 0; SW with w=0 attends only the diagonal."""
+    S = 19
+    q, k, v = rnd(2, 2, S, 8, seed=34), rnd(2, 2, S, 8, seed=35), rnd(2, 2, S, 8, seed=36)
+    out, _ = oracle.attn(q, k, v, mask="causal")
+    np.testing.assert_array_equal(O(out, (2, 2, S, 8))[:, :, 0], v[:, :, 0])
+    out, _ = oracle.attn(q, k, v, mask="sliding", window=0)
+    np.testing.assert_array_equal(O(out, (2, 2, S, 8)), v)
+
+
+def test_empty_rows_give_zero_and_neg_inf_lse():
+    """G7: a fully masked row gives O = 0, LSE = -inf."""
+    q, k, v = rnd(1, 1, 4, 8, seed=37), rnd(1, 1, 6, 8, seed=38), rnd(1, 1, 6, 8, seed=39)
+    km = torch.zeros(1, 1, 6, dtype=torch.uint8)
+    out, lse = oracle.attn(q, k, v, key_mask=km)
+    assert (out == 0).all() and np.isneginf(lse).all()
+
+
+def test_diff_lambda_zero_and_equal_maps():
+    """P4: lambda=0 => A_0; Q_1=Q_0, K_1=K_0 => (1-lambda) A_0."""
+    q0, k0, v = rnd(1, 2, 12, 8, seed=40), rnd(1, 2, 12, 8, seed=41), rnd(1, 2, 12, 8, seed=42)
+    q1, k1 = rnd(1, 2, 12, 8, seed=43), rnd(1, 2, 12, 8, seed=44)
+    a0, _ = oracle.attn(q0, k0, v, mask="causal")
+    out, _ = oracle.attn(torch.cat([q0, q1], 1), torch.cat([k0, k1], 1), v, diff=True, lam=0.0, mask="causal")
+    np.testing.assert_array_equal(out, a0)
+    out, _ = oracle.attn(torch.cat([q0, q0], 1), torch.cat([k0, k0], 1), v, diff=True, lam=0.3, mask="causal")
+    np.testing.assert_allclose(out, 0.7 * a0, rtol=1e-15, atol=1e-16)
+
+
+def test_gate_identities():
+    """P5: gate mul with ones is the identity; sigmoid(+40) ~ 1 and sigmoid(-40) ~ 0."""
+    q, k, v = rnd(1, 2, 9, 8, seed=45), rnd(1, 2, 9, 8, seed=46), rnd(1, 2, 9, 8, seed=47)
+    base, _ = oracle.attn(q, k, v)
+    out, _ = oracle.attn(q, k, v, gate_mode="mul", gate=torch.ones(1, 2, 9, 8, dtype=D64))
+    np.testing.assert_array_equal(out, base)
+    out, _ = oracle.attn(q, k, v, gate_mode="sigmoid", gate=torch.full((1, 2, 9, 8), 40.0, dtype=D64))
+    np.testing.assert_allclose(out, base, rtol=1e-16, atol=1e-17)
+    out, _ = oracle.attn(q, k, v, gate_mode="sigmoid", gate=torch.full((1, 2, 9, 8), -40.0, dtype=D64))
+    assert np.abs(out).max() < 1e-17
+    g = rnd(1, 2, 9, 8, seed=48, lo=-4, hi=4)
+    out, _ = oracle.attn(q, k, v, gate_mode="mul", gate=g)
+    np.testing.assert_allclose(out, base * g.numpy().reshape(-1, 8), rtol=1e-15)
+
+
+def test_full_blocklist_is_dense_causal():
+    """P6: RSA with every admissible block listed == dense causal attention (BJ north_star)."""
+    S, blk = 50, 8
+    q, k, v = rnd(1, 2, S, 8, seed=49), rnd(1, 2, S, 8, seed=50), rnd(1, 2, S, 8, seed=51)
+    nqb = (S + blk - 1) // blk
+    idx = np.full((2, nqb, nqb), -1, dtype=np.int32)
+    cnt = np.zeros((2, nqb), dtype=np.int32)
+    for i in range(nqb):
+        idx[:, i, : i + 1] = np.arange(i + 1)
+        cnt[:, i] = i + 1
+    out, _ = oracle.attn(q, k, v, mask="blocklist", blk_idx=idx, blk_cnt=cnt, blk_q=blk, blk_k=blk)
+    ref, _ = oracle.attn(q, k, v, mask="causal")
+    np.testing.assert_array_equal(out, ref)
+    idx1 = np.full((2, nqb, 1), -1, dtype=np.int32)
+    idx1[:, :, 0] = np.arange(nqb)
+    out, _ = oracle.attn(q, k, v, mask="blocklist", blk_idx=idx1, blk_cnt=np.ones((2, nqb), np.int32),
+                         blk_q=blk, blk_k=blk)
+    # P3: list = {diagonal} => causal attention inside each block
+    for i in range(nqb):
+        sl = slice(i * blk, min(S, (i + 1) * blk))
+        ref, _ = oracle.attn(q[:, :, sl], k[:, :, sl], v[:, :, sl], mask="causal")
+        np.testing.assert_allclose(O(out, (2, S, 8))[:, sl].reshape(-1, 8).numpy(), ref, rtol=1e-14, atol=1e-15)
+
+
+# ----------------------------------------------------------------- invariances (P9)
+def test_invariances():
+    S = 32
+    q, k, v = rnd(1, 2, S, 8, seed=52), rnd(1, 2, S, 8, seed=53), rnd(1, 2, S, 8, seed=54)
+    base, lse = oracle.attn(q, k, v)
+    # a per-row constant added to scores changes O, shifts LSE by the constant
+    row_c = rnd(1, 2, S, 1, seed=55, lo=-3, hi=3)
+    out, lse2 = oracle.attn(q, k, v, bias=row_c.expand(1, 2, S, S))
+    np.testing.assert_allclose(out, base, rtol=1e-13, atol=1e-14)
+    np.testing.assert_allclose(lse2, lse + row_c.reshape(-1).numpy(), rtol=1e-13)
+    # ALiBi == additive bias slope_h * k (the -slope*q part is per-row constant)
+    sl = synth.alibi_slopes(2).astype(np.float64)
+    al, _ = oracle.attn(q, k, v, mod="alibi")
+    bias = torch.from_numpy(sl).view(1, 2, 1, 1) * torch.arange(S, dtype=D64).view(1, 1, 1, S)
+    out, _ = oracle.attn(q, k, v, bias=bias.expand(1, 2, S, S))
+    np.testing.assert_allclose(out, al, rtol=1e-12, atol=1e-13)
+    # key permutation invariance (no position-dependent mod or mask)
+    perm = torch.randperm(S, generator=torch.Generator().manual_seed(1))
+    out, _ = oracle.attn(q, k[:, :, perm], v[:, :, perm])
+    np.testing.assert_allclose(out, base, rtol=1e-12, atol=1e-13)
+    # softcap with a huge cap == vanilla
+    out, _ = oracle.attn(q, k, v, mod="softcap", softcap=1e6)
+    np.testing.assert_allclose(out, base, rtol=1e-9, atol=1e-10)
+    # causal perturbation invariance: row q ignores keys > q
+    causal, _ = oracle.attn(q, k, v, mask="causal")
+    k2, v2 = k.clone(), v.clone()
+    k2[:, :, 20:] += 5
+    v2[:, :, 20:] -= 7
+    out, _ = oracle.attn(q, k2, v2, mask="causal")
+    rows = np.array([h * S + r for h in range(2) for r in range(20)])
+    np.testing.assert_array_equal(out[rows], causal[rows])
+    # SW with w >= S-1 == causal; prefix 0 == causal; prefix S == vanilla
+    for kw in (dict(mask="sliding", window=S - 1), dict(mask="prefix", prefix=0)):
+        out, _ = oracle.attn(q, k, v, **kw)
+        np.testing.assert_array_equal(out, causal)
+    out, _ = oracle.attn(q, k, v, mask="prefix", prefix=S)
+    np.testing.assert_array_equal(out, base)
+    # 1 document == vanilla; 12 documents == per-segment vanilla
+    out, _ = oracle.attn(q, k, v, mask="document", doc_offsets=np.array([[0, S]], np.int32))
+    np.testing.assert_array_equal(out, base)
+    offs = synth.doc_offsets(1, S, 12, seed=4)
+    out, _ = oracle.attn(q, k, v, mask="document", doc_offsets=offs)
+    for j in range(12):
+        a, b = offs[0, j], offs[0, j + 1]
+        seg, _ = oracle.attn(q[:, :, a:b], k[:, :, a:b], v[:, :, a:b])
+        np.testing.assert_allclose(O(out, (2, S, 8))[:, a:b].reshape(-1, 8).numpy(), seg, rtol=1e-14, atol=1e-15)
+    # GQA with Hkv == Hq is MHA, bit for bit
+    out, _ = oracle.attn(q, k, v, mask="causal")
+    np.testing.assert_array_equal(out, causal)
+
+
+def test_row_subset_equals_full_run():
+    """P10: the oracle's row-subset API returns exactly the rows of a full run."""
+    q, k, v = rnd(2, 3, 21, 8, seed=56), rnd(2, 3, 21, 8, seed=57), rnd(2, 3, 21, 8, seed=58)
+    full, lse = oracle.attn(q, k, v, mask="causal")
+    rows = np.array([0, 5, 20, 21, 63, 125])
+    sub, lse_s = oracle.attn(q, k, v, mask="causal", rows=rows)
+    np.testing.assert_array_equal(sub, full[rows])
+    np.testing.assert_array_equal(lse_s, lse[rows])
+
+
+# ----------------------------------------------------------------- brute force (P7)
+def brute(q, k, v, keep, mod=None, gate=None):
+    """Quadruple loop in plain Python with math.fsum, tiny shapes only."""
+    B, H, Sq, D = q.shape
+    Sk, Dv = k.shape[2], v.shape[3]
+    out = np.zeros((B, H, Sq, Dv))
+    for b in range(B):
+        for h in range(H):
+            for i in range(Sq):
+                s = {}
+                for j in range(Sk):
+                    if keep(b, h, i, j):
+                        x = math.fsum(float(q[b, h, i, d]) * float(k[b, h, j, d]) for d in range(D)) / math.sqrt(D)
+                        s[j] = mod(h, i, j, x) if mod else x
+                if not s:
+                    continue
+                mx = max(s.values())
+                den = math.fsum(math.exp(x - mx) for x in s.values())
+                for d in range(Dv):
+                    out[b, h, i, d] = math.fsum(math.exp(x - mx) / den * float(v[b, h, j, d]) for j, x in s.items())
+                    if gate is not None:
+                        out[b, h, i, d] /= 1.0 + math.exp(-float(gate[b, h, i, d]))
+    return out
+
+
+@pytest.mark.parametrize("name", ["vanilla", "causal", "sliding", "prefix", "alibi", "softcap", "gate"])
+def test_brute_force_tiny(name):
+    q, k, v = rnd(1, 2, 6, 4, seed=60), rnd(1, 2, 6, 4, seed=61), rnd(1, 2, 6, 3, seed=62)
+    keep = lambda b, h, i, j: True
+    mod = None
+    kw = {}
+    gate = None
+    if name == "causal":
+        keep, kw = (lambda b, h, i, j: j <= i), dict(mask="causal")
+    if name == "sliding":
+        keep, kw = (lambda b, h, i, j: j <= i and i - j <= 2), dict(mask="sliding", window=2)
+    if name == "prefix":
+        keep, kw = (lambda b, h, i, j: j < 3 or j <= i), dict(mask="prefix", prefix=3)
+    if name == "alibi":
+        mod, kw = (lambda h, i, j, x: x + 2.0 ** (-8.0 * (h + 1) / 2) * (j - i)), dict(mod="alibi")
+    if name == "softcap":
+        mod, kw = (lambda h, i, j, x: 0.5 * math.tanh(x / 0.5)), dict(mod="softcap", softcap=0.5)
+    if name == "gate":
+        gate = rnd(1, 2, 6, 3, seed=63, lo=-4, hi=4)
+        kw = dict(gate_mode="sigmoid", gate=gate)
+    ref = brute(q.numpy(), k.numpy(), v.numpy(), keep, mod, None if gate is None else gate.numpy())
+    out, _ = oracle.attn(q, k, v, **kw)
+    np.testing.assert_allclose(out.reshape(ref.shape), ref, rtol=1e-13, atol=1e-15)
+
+
+# ----------------------------------------------------------------- RSA selection (G10/G11, P14)
+def test_rsa_summaries_and_bound_identity():
+    q, k = synth.clustered_qk((1, 2, 64, 16), (1, 1, 64, 16), blk=16, dtype=torch.float32)
+    kmin, kmax = oracle.rsa_summaries(k.to(D64), 16)
+    kk = k.to(D64).reshape(1, 4, 16, 16)
+    np.testing.assert_array_equal(kmin[0], kk[0].amin(1).numpy())
+    np.testing.assert_array_equal(kmax[0], kk[0].amax(1).numpy())
+    # P14: sum_d max(q_d x_d, q_d y_d) == q+ . x + q- . y when x >= y
+    qq = q.to(D64)[0, 0].numpy()
+    lhs = np.maximum(qq[:, None, :] * kmax[0][None], qq[:, None, :] * kmin[0][None]).sum(-1)
+    rhs = np.maximum(qq, 0) @ kmax[0].T + np.minimum(qq, 0) @ kmin[0].T
+    np.testing.assert_allclose(lhs, rhs, rtol=1e-12, atol=1e-12)
+
+
+def test_rsa_selection_matches_sort_reference():
+    Sq = Sk = 256
+    blk, topk = 16, 4
+    q, k = synth.clustered_qk((1, 4, Sq, 16), (1, 2, Sk, 16), blk=blk, dtype=torch.bfloat16)
+    idx, cnt, sc = oracle.rsa_select(q, k, blk_q=blk, blk_k=blk, topk=topk, want_scores=True)
+    kmin, kmax = oracle.rsa_summaries(k, blk)
+    qd = q.to(D64).numpy()
+    for h in range(4):
+        hk = h // 2
+        for i in range(Sq // blk):
+            c = i
+            if c <= topk + 1:
+                assert list(idx[h, i, : cnt[h, i]]) == list(range(c + 1))
+                continue
+            # independent score via the q+/q- identity (P14), max over the group's heads
+            qs = qd[0, hk * 2:(hk + 1) * 2, i * blk:(i + 1) * blk].reshape(-1, 16)
+            score = (np.maximum(qs, 0) @ kmax[hk].T + np.minimum(qs, 0) @ kmin[hk].T).max(0)
+            np.testing.assert_allclose(sc[h, i, 1:c], score[1:c], rtol=1e-12, atol=1e-12)
+            order = sorted(range(1, c), key=lambda j: (-score[j], j))[:topk]
+            want = sorted({0, c, *order})
+            assert list(idx[h, i, : cnt[h, i]]) == want
+            assert cnt[h, i] == topk + 2
