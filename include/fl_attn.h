@@ -1,0 +1,176 @@
+/*
+ * fl_attn.h -- C ABI of the B200-native (sm_100a) fused attention-variant
+ * forward: the data-parallel hot path of Flashlight (arXiv 2511.02043).
+ *
+ * "P:Lnnn" cites /root/reference/PAPER.md line nnn (section / equation /
+ * listing named beside it); "Gnn" is a reading of an ambiguous passage listed
+ * in DESIGN.md §Readings.
+ *
+ * What one call computes (per output row b, g, h, q; the kernel fuses all of
+ * it, one pass over K/V with the online softmax of Alg.2):
+ *   s_k  = scale * <Q[b,g,h,q,:], K[b,g,h_kv,k,:]>      Eq.3, Listing 1
+ *   s_k  = score_mod(s_k)                              Eq.4 P:L251-257 (ALiBi, softcap, bias)
+ *   s_k  = -inf where masked                           Listing 1, Listing 2
+ *   P    = softmax_k(s)   ;   O = P V                  Eq.2/Eq.3
+ *   diff : O = A_0 - lambda_h A_1                      Listing 4 P:L412-424 (G8)
+ *   gate : O = O * sigmoid(G)  |  O * G                Evoformer P:L865 (G9)
+ *
+ * Conventions (all functions):
+ *  - All symbols are extern "C"; structs are POD; no exception crosses the ABI.
+ *  - OWNERSHIP: the caller owns every buffer.  The library never allocates or
+ *    frees device memory, never synchronises, never changes the current device.
+ *    Device pointers must be on the current device.
+ *  - ASYNCHRONY: work is enqueued on `stream` (a cudaStream_t; NULL = legacy
+ *    default stream) and the call returns.  Launch failures return FL_ERR_CUDA
+ *    with the CUDA error text in fl_last_error(); device faults surface at the
+ *    caller's next synchronisation.
+ *  - VALIDATION is all-or-nothing: on any non-OK status nothing is enqueued and
+ *    no output is touched.  Unsupported combinations return FL_ERR_UNSUPPORTED
+ *    and a reason in fl_last_error().  There is NO fallback path of any kind
+ *    (no CPU path, no second backend).
+ *  - Thread safety: every call is re-entrant; the only global state is the
+ *    once-resolved driver entry point (cuTensorMapEncodeTiled) and the
+ *    thread-local error string.
+ */
+#ifndef FL_ATTN_H
+#define FL_ATTN_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FL_ABI_VERSION 1
+
+typedef enum {
+  FL_OK = 0,
+  FL_ERR_INVALID_ARGUMENT = 1, /* null/inconsistent descriptor, bad enum, pointer not on device */
+  FL_ERR_UNSUPPORTED = 2,      /* valid but not implemented (reason in fl_last_error) */
+  FL_ERR_MISALIGNED = 3,       /* TMA needs 16-B aligned base and 16-B multiple strides */
+  FL_ERR_SHAPE_MISMATCH = 4,   /* q/k/v/o/bias/gate/lse shapes disagree */
+  FL_ERR_WORKSPACE = 5,        /* workspace too small */
+  FL_ERR_CUDA = 6,             /* CUDA runtime/driver error (text in fl_last_error) */
+  FL_ERR_ABI_VERSION = 7       /* abi_version != FL_ABI_VERSION */
+} fl_status;
+
+typedef enum { FL_BF16 = 0, FL_F32 = 1, FL_U8 = 2, FL_I32 = 3 } fl_dtype;
+
+/* A strided view.  rank <= 5, sizes/strides in ELEMENTS, stride 0 broadcasts a
+ * dim.  data == NULL means "absent".  The last dim of q/k/v/o/gate must be
+ * contiguous (stride 1). */
+typedef struct {
+  void* data;
+  int32_t dtype;     /* fl_dtype */
+  int32_t rank;
+  int64_t size[5];
+  int64_t stride[5];
+} fl_tensor;
+
+typedef enum { FL_MOD_NONE = 0, FL_MOD_ALIBI = 1, FL_MOD_SOFTCAP = 2 } fl_mod;
+typedef enum {
+  FL_MASK_NONE = 0,
+  FL_MASK_CAUSAL = 1,    /* keep k <= q_abs                                  */
+  FL_MASK_SLIDING = 2,   /* keep k <= q_abs && q_abs - k <= window  (G4) */
+  FL_MASK_PREFIX = 3,    /* keep k < prefix_len || k <= q_abs       (G5)       */
+  FL_MASK_DOCUMENT = 4,  /* keep doc(k) == doc(q_abs) [&& k <= q_abs]  (G6)    */
+  FL_MASK_BLOCKLIST = 5  /* keep floor(k/blk_k) in list[b,h,floor(q/blk_q)] && k <= q_abs (RSA, G10) */
+} fl_mask;
+typedef enum { FL_GATE_NONE = 0, FL_GATE_MUL = 1, FL_GATE_SIGMOID = 2 } fl_gate;
+
+/* The variant descriptor (BASELINE.json north_star: "mod type, mask,
+ * bias/gate tensors, diff-lambda, sparse block list").  Zero-initialise it
+ * and set abi_version; every field's zero value means "off". */
+typedef struct {
+  uint32_t abi_version;      /* must equal FL_ABI_VERSION */
+  float scale;               /* 0 -> 1/sqrt(D_qk)  (Listing 1, G1) */
+  int32_t mod;               /* fl_mod; acts on the SCALED score (Eq.4) */
+  float softcap;             /* FL_MOD_SOFTCAP: s <- softcap * tanh(s / softcap)   (G3) */
+  fl_tensor alibi_slopes;    /* FL_MOD_ALIBI: f32 [Hq]; absent -> 2^(-8(h+1)/Hq); s += slope_h (k - q_abs) (G2) */
+  int32_t mask;              /* fl_mask */
+  int32_t window;            /* FL_MASK_SLIDING window w (inclusive: w+1 keys incl. the diagonal) */
+  int32_t prefix_len;        /* FL_MASK_PREFIX P */
+  fl_tensor doc_offsets;     /* FL_MASK_DOCUMENT: i32 [B, n_docs+1], 0 = off[0] < ... < off[n_docs] = S_k */
+  int32_t doc_causal;        /* FL_MASK_DOCUMENT: also require k <= q_abs */
+  int32_t causal_align;      /* 0: bottom-right q_abs = q + S_k - S_q (G12); 1: top-left q_abs = q */
+  fl_tensor bias;            /* optional additive score bias, same rank as q: [B,Hq,S_q,S_k] or [B,G,Hq,S_q,S_k],
+                                bf16 or f32, broadcast by stride 0 (Evoformer pair bias [b,h,i,j] broadcast over
+                                G = s) */
+  fl_tensor key_mask;        /* optional u8, rank(q)-2: [B,S_k] or [B,G,S_k]; 1 = keep (Evoformer MSA mask, G9) */
+  int32_t gate_mode;         /* fl_gate */
+  fl_tensor gate;            /* gate logits/values, same logical shape as o */
+  int32_t diff;              /* differential attention: q,k carry 2*H heads, map i = heads [iH,(i+1)H) (G8) */
+  float lambda;              /* diff: lambda_full (Listing 4 P:L431 uses 0.2) */
+  fl_tensor lambda_h;        /* diff: optional f32 [Hq] per-head lambda (overrides lambda) */
+  fl_tensor blk_idx;         /* FL_MASK_BLOCKLIST: i32 [B*(G)*Hq, n_qblk, max_sel], ascending, -1 padded */
+  fl_tensor blk_cnt;         /* FL_MASK_BLOCKLIST: i32 [B*(G)*Hq, n_qblk] */
+  int32_t blk_q;             /* FL_MASK_BLOCKLIST query block (must be 128) */
+  int32_t blk_k;             /* FL_MASK_BLOCKLIST key block (must be 128) */
+} fl_variant;
+
+typedef struct {
+  /* rank 4 [B,H,S,D] or rank 5 [B,G,H,S,D]; any strides with a contiguous last dim.
+   * q [..,Hq(x2 if diff),S_q,D_qk]; k [..,Hkv(x2 if diff),S_k,D_qk]; v [..,Hkv,S_k,D_v];
+   * o [..,Hq,S_q,D_v].  Hq % Hkv == 0; query head h reads KV head floor(h/(Hq/Hkv)) (G15). */
+  fl_tensor q, k, v, o;
+  fl_tensor lse;             /* optional f32 [B,(G,)Hq,S_q]: natural-log LSE of the scaled, modified scores (G19) */
+  fl_variant var;
+  void* stream;              /* cudaStream_t */
+  void* workspace;           /* device scratch (see fl_attn_workspace_size); never allocated here */
+  size_t workspace_bytes;
+} fl_attn_args;
+
+/* Supported set (ABI v1):
+ *   f32 q/k/v/o  : exact-fp32 SIMT path, every variant, D_qk, D_v <= 128.
+ *   bf16 q/k/v/o : tcgen05/TMEM/TMA path, D_qk == D_v in {32, 64, 128}; every mask, mod,
+ *                  bias, key_mask, gate; diff (lse must be absent with diff).
+ * Empty work (B*G*Hq*S_q == 0) returns FL_OK without a launch; S_k == 0 gives O = 0,
+ * lse = -inf (G7); a fully masked row likewise gives O = 0, lse = -inf. */
+fl_status fl_attn_fwd(const fl_attn_args* args);
+
+/* Bytes of device workspace fl_attn_fwd needs for these args: the key mask packed to one bit per
+ * key (ceil(S_k/128)*16 bytes per (b, g)) when key_mask is present, else 0. */
+fl_status fl_attn_workspace_size(const fl_attn_args* args, size_t* bytes);
+
+/* Host-buffer entry (the end-to-end path): same as fl_attn_fwd, but q/k/v (and
+ * bias/gate/key_mask/doc_offsets/blk_* if present) and o/lse point to HOST
+ * memory (pinned for overlap).  `device_scratch` holds device copies laid out
+ * by the library: size from fl_attn_host_scratch_size.  The call enqueues
+ * H2D copies, the kernel and the D2H copy of o (and lse) on `stream`, and
+ * returns without synchronising.  Host tensors must be contiguous. */
+fl_status fl_attn_host_scratch_size(const fl_attn_args* args, size_t* bytes);
+fl_status fl_attn_fwd_host(const fl_attn_args* host_args, void* device_scratch, size_t scratch_bytes);
+
+/* RSA block summaries (reading G10): kmin/kmax [B*(G)*Hkv, n_kblk, D] bf16 = exact
+ * element-wise min / max of the keys of each KV block of blk_k keys. */
+fl_status fl_rsa_build_summaries(const fl_tensor* k, fl_tensor* kmin, fl_tensor* kmax,
+                                 int32_t blk_k, void* stream);
+
+/* RSA selection (reading G10/G11): for each (b, h, q-block i) with diagonal block c,
+ * score_j = max_{q in block i, h' in h's KV group} sum_d max(q_d kmax_jd, q_d kmin_jd),
+ * 0 < j < c; list = {0} U {c} U top-k(score) (ties to lower j), ascending, -1 padded.
+ * blk_idx i32 [B*(G)*Hq, n_qblk, max_sel >= topk+2], blk_cnt i32 [B*(G)*Hq, n_qblk]. */
+fl_status fl_rsa_select(const fl_tensor* q, const fl_tensor* kmin, const fl_tensor* kmax,
+                        int32_t topk, int32_t blk_q, int32_t blk_k, int32_t causal_align,
+                        fl_tensor* blk_idx, fl_tensor* blk_cnt, void* stream);
+
+/* Contiguous range [begin, end) of `units` independent work units owned by
+ * `rank` of `world` (multi-GPU batch x head sharding; no collective). */
+void fl_shard_range(int64_t units, int32_t world, int32_t rank, int64_t* begin, int64_t* end);
+
+/* Diagnostic: one bf16 tcgen05 GEMM C[M,N] (f32) = A[M,K] B[N,K]^T (or B[K,N] when
+ * b_mn_major), M = 128, N in {32,64,128}, K in {32,64,128}, through the same
+ * TMA/UMMA descriptor helpers the attention kernels use; `a_from_tmem` routes
+ * A through TMEM (the P operand path).  For bring-up tests only. */
+fl_status fl_diag_umma_gemm(const void* a, const void* b, float* c, int32_t n, int32_t k,
+                            int32_t b_mn_major, int32_t a_from_tmem, void* stream);
+
+const char* fl_status_string(fl_status s);
+const char* fl_last_error(void);   /* thread-local detail of the last non-OK status */
+int32_t fl_abi_version(void);
+/* Number of kernel launches enqueued by the calling thread since the last reset. */
+int64_t fl_launch_count(int32_t reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FL_ATTN_H */

@@ -1,0 +1,99 @@
+"""ctypes mirror of include/fl_attn.h (argument marshalling only).
+
+Loading is lazy; if libfl_attn.so is missing the first call raises -- there is
+no CPU or library fallback anywhere in this package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(HERE, "libfl_attn.so")
+
+FL_BF16, FL_F32, FL_U8, FL_I32 = 0, 1, 2, 3
+ABI_VERSION = 1
+
+EXPORTS = ["fl_attn_fwd", "fl_attn_workspace_size", "fl_attn_host_scratch_size", "fl_attn_fwd_host",
+           "fl_rsa_build_summaries", "fl_rsa_select", "fl_shard_range", "fl_diag_umma_gemm",
+           "fl_status_string", "fl_last_error", "fl_abi_version", "fl_launch_count"]
+
+
+class Tensor(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("dtype", C.c_int32), ("rank", C.c_int32),
+                ("size", C.c_int64 * 5), ("stride", C.c_int64 * 5)]
+
+
+class Variant(C.Structure):
+    _fields_ = [
+        ("abi_version", C.c_uint32), ("scale", C.c_float), ("mod", C.c_int32), ("softcap", C.c_float),
+        ("alibi_slopes", Tensor), ("mask", C.c_int32), ("window", C.c_int32), ("prefix_len", C.c_int32),
+        ("doc_offsets", Tensor), ("doc_causal", C.c_int32), ("causal_align", C.c_int32),
+        ("bias", Tensor), ("key_mask", Tensor), ("gate_mode", C.c_int32), ("gate", Tensor),
+        ("diff", C.c_int32), ("lambda_", C.c_float), ("lambda_h", Tensor),
+        ("blk_idx", Tensor), ("blk_cnt", Tensor), ("blk_q", C.c_int32), ("blk_k", C.c_int32),
+    ]
+
+
+class AttnArgs(C.Structure):
+    _fields_ = [("q", Tensor), ("k", Tensor), ("v", Tensor), ("o", Tensor), ("lse", Tensor),
+                ("var", Variant), ("stream", C.c_void_p), ("workspace", C.c_void_p),
+                ("workspace_bytes", C.c_size_t)]
+
+
+class FlError(RuntimeError):
+    def __init__(self, status: int, detail: str):
+        super().__init__(f"{status_string(status)}: {detail}")
+        self.status = status
+        self.detail = detail
+
+
+_lib = None
+
+
+def lib():
+    """Load libfl_attn.so (raises if it was never built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(SO_PATH):
+            raise FileNotFoundError(
+                f"{SO_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(there is no CPU fallback)")
+        L = C.CDLL(SO_PATH)
+        L.fl_attn_fwd.argtypes = [C.POINTER(AttnArgs)]
+        L.fl_attn_workspace_size.argtypes = [C.POINTER(AttnArgs), C.POINTER(C.c_size_t)]
+        L.fl_attn_host_scratch_size.argtypes = [C.POINTER(AttnArgs), C.POINTER(C.c_size_t)]
+        L.fl_attn_fwd_host.argtypes = [C.POINTER(AttnArgs), C.c_void_p, C.c_size_t]
+        L.fl_rsa_build_summaries.argtypes = [C.POINTER(Tensor), C.POINTER(Tensor), C.POINTER(Tensor), C.c_int32,
+                                             C.c_void_p]
+        L.fl_rsa_select.argtypes = [C.POINTER(Tensor), C.POINTER(Tensor), C.POINTER(Tensor), C.c_int32, C.c_int32,
+                                    C.c_int32, C.c_int32, C.POINTER(Tensor), C.POINTER(Tensor), C.c_void_p]
+        L.fl_shard_range.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.fl_shard_range.restype = None
+        L.fl_diag_umma_gemm.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                        C.c_int32, C.c_void_p]
+        L.fl_status_string.argtypes = [C.c_int]
+        L.fl_status_string.restype = C.c_char_p
+        L.fl_last_error.restype = C.c_char_p
+        L.fl_abi_version.restype = C.c_int32
+        L.fl_launch_count.argtypes = [C.c_int32]
+        L.fl_launch_count.restype = C.c_int64
+        for name in ("fl_attn_fwd", "fl_attn_workspace_size", "fl_attn_host_scratch_size", "fl_attn_fwd_host",
+                     "fl_rsa_build_summaries", "fl_rsa_select", "fl_diag_umma_gemm"):
+            getattr(L, name).restype = C.c_int
+        if L.fl_abi_version() != ABI_VERSION:
+            raise RuntimeError("libfl_attn.so ABI version mismatch")
+        _lib = L
+    return _lib
+
+
+def status_string(s: int) -> str:
+    try:
+        return lib().fl_status_string(s).decode()
+    except Exception:  # pragma: no cover
+        return f"status {s}"
+
+
+def check(status: int) -> None:
+    if status != 0:
+        raise FlError(status, lib().fl_last_error().decode())

@@ -1,0 +1,547 @@
+// attn_tc.cu -- bf16 fused attention forward on the 5th-generation tensor cores
+// (sm_100a): TMA -> mbarrier ring -> tcgen05.mma (accumulators in TMEM) ->
+// tcgen05.ld -> online softmax in registers -> P back into TMEM -> tcgen05.mma.
+//
+// This is the single monolithic kernel Flashlight's compiler emits per
+// attention program: "each thread block computes tiles of the
+// dot-product S = QK^T/sqrt(d), applies the online softmax to each tile via a
+// fused max-reduction and rescaled accumulation, and multiplies the resulting
+// softmax output with the corresponding tiles of V".  Re-designed for B200:
+//
+//  * CTA = 384 threads, one CTA per SM (TMEM: all 512 columns).
+//      warps 0-3  softmax WG0: query tile 0 (thread = row = TMEM lane)
+//      warps 4-7  softmax WG1: query tile 1 (differential attention: map 1)
+//      warp  8    TMA producer (one elected lane)
+//      warp  9    MMA issuer (one elected lane) + TMEM allocator
+//  * TMEM columns: S0 [0,128) S1 [128,256) O0 [256,256+D) O1 [256+D,256+2D);
+//    P_i (bf16, 64 columns) aliases the upper half of S_i (the
+//    whole D_v lives in one accumulator -- "tiling-aware dimension elimination").
+//  * MMA issue order S0(0) S1(0) | PV0(j) S0(j+1) PV1(j) S1(j+1) | ... so the two
+//    softmax warpgroups ping-pong against the tensor pipe; tcgen05 ops issued by
+//    one thread execute in order, so S_i(j+1) may overwrite P_i(j) after PV_i(j).
+//  * Online softmax (Alg.2, semantic fusion P:L685-697) in the log2
+//    domain with CONDITIONAL rescaling: the running reference m_ref only moves
+//    when the row max grows by more than TAU = 8 (p <= 2^8 stays exact in fp32
+//    and representable in bf16).  Licensed by the closed form of do[j]
+//     whose proof never uses m[j] = max.
+//  * Masks are per-row key intervals (masks.cuh): KV tiles outside the union
+//    are never loaded, tiles inside every row's interval run mask-free, only
+//    boundary tiles pay two compares per element.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "masks.cuh"
+#include "params.h"
+#include "ptx.cuh"
+
+namespace fl {
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kTau = 8.0f;
+constexpr int kThreadsTc = 384;
+
+template <int D, bool DIFF>
+struct TcCfg {
+  static constexpr int BM = 128;                     // query rows per tile (= TMEM lanes)
+  static constexpr int BN = 128;                     // keys per KV tile
+  static constexpr int CH = D >= 64 ? 64 : 32;       // elements per swizzle row
+  static constexpr int SWB = CH * 2;                 // swizzle bytes: 128 or 64
+  static constexpr int NCH = D / CH;                 // swizzle chunks per row
+  static constexpr int CHUNK_BYTES = BM * SWB;
+  static constexpr int TILE_BYTES = BM * D * 2;
+  static constexpr int NSLOT = D == 128 ? 4 : (D == 64 ? 6 : 8);
+  static constexpr uint32_t LAYOUT = SWB == 128 ? kLayoutSW128 : kLayoutSW64;
+  static constexpr int SBO = 8 * SWB;                // 8-row (K-major) / 8-key (MN-major) group stride
+  static constexpr uint32_t COL_S0 = 0, COL_S1 = 128, COL_O0 = 256, COL_O1 = 256 + D;
+  static constexpr uint32_t P_OFF = 64;              // P_i at S_i + 64
+  static constexpr int SMEM_Q = 0;
+  static constexpr int SMEM_RING = 2 * TILE_BYTES;
+  static constexpr int SMEM_BAR = SMEM_RING + NSLOT * TILE_BYTES;
+  static constexpr int NBAR = 1 + 2 * NSLOT + 6;
+  static constexpr int SMEM_TOTAL = SMEM_BAR + NBAR * 8 + 16 + 1024;  // + alignment slack
+  static constexpr uint32_t IDESC_S = idesc_bf16_f32(128, BN, 0);   // Q (K-major) x K (K-major)
+  static constexpr uint32_t IDESC_O = idesc_bf16_f32(128, D, 1);    // P (TMEM) x V (MN-major)
+  static constexpr int ENTRIES_PER_TILE = DIFF ? 3 : 2;              // K0 [K1] V
+};
+
+struct Work {
+  int b, g, h;
+  int q0[2];            // first query row of each warpgroup's tile
+  int lo[2], hi[2];     // KV tile range [lo, hi) each warpgroup needs
+  int lo_cta, hi_cta;
+};
+
+template <int D, bool DIFF>
+__device__ __forceinline__ Work decode_work(const AttnParams& p) {
+  Work w;
+  const int rows_per_unit = DIFF ? 128 : 256;
+  const int nqb = (p.Sq + rows_per_unit - 1) / rows_per_unit;
+  const int nbgh = p.B * p.G * p.Hq;
+  const int u = blockIdx.x;
+  const int qb = nqb - 1 - u / nbgh;                 // heaviest (latest) query blocks first
+  const int bgh = u % nbgh;
+  w.h = bgh % p.Hq;
+  w.g = (bgh / p.Hq) % p.G;
+  w.b = bgh / (p.Hq * p.G);
+  w.lo_cta = 1 << 30;
+  w.hi_cta = 0;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    w.q0[i] = DIFF ? qb * 128 : qb * 256 + i * 128;
+    w.lo[i] = w.hi[i] = 0;
+    if (w.q0[i] < p.Sq) {
+      const int q_last = min(p.Sq, w.q0[i] + 128) - 1;
+      Interval iv = rows_union(p, w.b, w.q0[i], q_last);
+      if (iv.hi > iv.lo) {
+        w.lo[i] = iv.lo / 128;
+        w.hi[i] = (iv.hi + 127) / 128;
+      }
+    }
+    if (w.hi[i] > w.lo[i]) {
+      w.lo_cta = min(w.lo_cta, w.lo[i]);
+      w.hi_cta = max(w.hi_cta, w.hi[i]);
+    }
+  }
+  if (w.hi_cta <= w.lo_cta) w.lo_cta = w.hi_cta = 0;
+  return w;
+}
+
+__device__ __forceinline__ bool needs(const Work& w, int i, int j) { return j >= w.lo[i] && j < w.hi[i]; }
+__device__ __forceinline__ int next_tile(const Work& w, int j) {
+  for (++j; j < w.hi_cta; ++j)
+    if (needs(w, 0, j) || needs(w, 1, j)) return j;
+  return -1;
+}
+
+template <int D, bool DIFF, int MOD, bool BIAS>
+__global__ void __launch_bounds__(kThreadsTc, 1)
+    attn_tc_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ TmaMaps maps) {
+  using C = TcCfg<D, DIFF>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem + C::SMEM_Q;
+  uint8_t* sRing = smem + C::SMEM_RING;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::SMEM_BAR);
+  uint64_t* q_full = bars;
+  uint64_t* full = bars + 1;
+  uint64_t* empty = full + C::NSLOT;
+  uint64_t* s_full = empty + C::NSLOT;
+  uint64_t* p_full = s_full + 2;
+  uint64_t* o_full = p_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const Work w = decode_work<D, DIFF>(p);
+
+  if (warp == 8 && lane == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < C::NSLOT; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 128);
+      mbar_init(&o_full[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 9) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int hkv = w.h / p.grp;
+  const int gq = maps.q_bcast_g ? 0 : w.g, bq = maps.q_bcast_b ? 0 : w.b;
+  const int gk = maps.k_bcast_g ? 0 : w.g, bk = maps.k_bcast_b ? 0 : w.b;
+  const int gv = maps.v_bcast_g ? 0 : w.g, bv = maps.v_bcast_b ? 0 : w.b;
+
+  if (warp >= 8) {
+   regs_dec<96>();
+   if (warp == 8) {
+    // ============================== TMA producer ==============================
+    if (lane == 0) {
+      tma_prefetch_desc(&maps.q);
+      tma_prefetch_desc(&maps.k);
+      tma_prefetch_desc(&maps.v);
+      mbar_arrive_expect_tx(q_full, 2 * C::TILE_BYTES);
+      for (int i = 0; i < 2; ++i) {
+        const int qh = DIFF ? w.h + i * p.Hq : w.h;
+        for (int c = 0; c < C::NCH; ++c)
+          tma_load_5d(sQ + i * C::TILE_BYTES + c * C::CHUNK_BYTES, &maps.q, q_full, c * C::CH, w.q0[i], qh, gq, bq);
+      }
+      int e = 0;
+      for (int j = next_tile(w, w.lo_cta - 1); j >= 0; j = next_tile(w, j)) {
+        for (int t = 0; t < C::ENTRIES_PER_TILE; ++t, ++e) {
+          const int slot = e % C::NSLOT;
+          if (e >= C::NSLOT) mbar_wait(&empty[slot], ((e / C::NSLOT) - 1) & 1);
+          mbar_arrive_expect_tx(&full[slot], C::TILE_BYTES);
+          uint8_t* dst = sRing + slot * C::TILE_BYTES;
+          const bool is_v = t == C::ENTRIES_PER_TILE - 1;
+          const CUtensorMap* m = is_v ? &maps.v : &maps.k;
+          const int head = is_v ? hkv : hkv + t * p.Hkv;
+          const int gg = is_v ? gv : gk, bb = is_v ? bv : bk;
+          for (int c = 0; c < C::NCH; ++c)
+            tma_load_5d(dst + c * C::CHUNK_BYTES, m, &full[slot], c * C::CH, j * C::BN, head, gg, bb);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    // ============================== MMA issuer ==============================
+    if (lane == 0) {
+      const uint32_t sq_addr = smem_u32(sQ), ring_addr = smem_u32(sRing);
+      int e = 0;
+      auto acquire = [&]() -> int {
+        const int slot = e % C::NSLOT;
+        mbar_wait(&full[slot], (e / C::NSLOT) & 1);
+        ++e;
+        return slot;
+      };
+      auto issue_s = [&](int i, int kslot) {
+        const uint32_t qa = sq_addr + i * C::TILE_BYTES, ka = ring_addr + kslot * C::TILE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk * 16 / C::CH) * C::CHUNK_BYTES + (kk * 16 % C::CH) * 2;
+          umma_ss(tmem + (i ? C::COL_S1 : C::COL_S0), smem_desc(qa + off, 16, C::SBO, C::LAYOUT),
+                  smem_desc(ka + off, 16, C::SBO, C::LAYOUT), C::IDESC_S, kk > 0);
+        }
+        umma_commit(&s_full[i]);
+      };
+      int pv_cnt[2] = {0, 0};
+      auto issue_pv = [&](int i, int vslot) {
+        mbar_wait(&p_full[i], pv_cnt[i] & 1);
+        tc_fence_after();
+        const uint32_t va = ring_addr + vslot * C::TILE_BYTES;
+        const uint32_t pcol = (i ? C::COL_S1 : C::COL_S0) + C::P_OFF;
+#pragma unroll
+        for (int kk = 0; kk < C::BN / 16; ++kk) {
+          umma_ts(tmem + (i ? C::COL_O1 : C::COL_O0), tmem + pcol + kk * 8,
+                  smem_desc(va + kk * 16 * C::SWB, C::CHUNK_BYTES, C::SBO, C::LAYOUT), C::IDESC_O,
+                  (pv_cnt[i] > 0 || kk > 0) ? 1u : 0u);
+        }
+        ++pv_cnt[i];
+      };
+      int j = next_tile(w, w.lo_cta - 1);
+      mbar_wait(q_full, 0);                          // always: no CTA exits with Q's TMA in flight
+      tc_fence_after();
+      if (j >= 0) {
+        int ks0 = acquire();
+        int ks1 = DIFF ? acquire() : ks0;
+        if (needs(w, 0, j)) issue_s(0, ks0);
+        if (needs(w, 1, j)) issue_s(1, ks1);
+        umma_commit(&empty[ks0]);
+        if (DIFF) umma_commit(&empty[ks1]);
+        while (j >= 0) {
+          const int vs = acquire();
+          const int jn = next_tile(w, j);
+          int kn0 = -1, kn1 = -1;
+          if (jn >= 0) {
+            kn0 = acquire();
+            kn1 = DIFF ? acquire() : kn0;
+          }
+          if (needs(w, 0, j)) {
+            issue_pv(0, vs);
+            if (j == w.hi[0] - 1) umma_commit(&o_full[0]);
+          }
+          if (jn >= 0 && needs(w, 0, jn)) issue_s(0, kn0);
+          if (needs(w, 1, j)) {
+            issue_pv(1, vs);
+            if (j == w.hi[1] - 1) umma_commit(&o_full[1]);
+          }
+          umma_commit(&empty[vs]);
+          if (jn >= 0) {
+            if (needs(w, 1, jn)) issue_s(1, kn1);
+            umma_commit(&empty[kn0]);
+            if (DIFF) umma_commit(&empty[kn1]);
+          }
+          j = jn;
+        }
+      }
+    }
+   }
+  } else {
+    regs_inc<208>();
+    // ============================== softmax warpgroups ==============================
+    const int wg = warp >> 2;
+    const int r = threadIdx.x & 127;                 // row within the tile == TMEM lane
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    const int q = w.q0[wg] + r;
+    const bool row_valid = q < p.Sq;
+    const int q_abs = q + p.q_off;
+    const Interval iv = row_interval(p, w.b, q);
+    const int lo_i = w.lo[wg], hi_i = w.hi[wg];
+    const uint32_t col_s = wg ? C::COL_S1 : C::COL_S0;
+    const uint32_t col_o = wg ? C::COL_O1 : C::COL_O0;
+    float slope_l2 = 0.f;
+    if (MOD == MOD_ALIBI)
+      slope_l2 = kLog2e * (p.alibi ? p.alibi[w.h] : exp2f(-8.f * (float)(w.h + 1) / (float)p.Hq));
+    const float sc_l2 = p.scale * kLog2e;
+    const float cap_in = MOD == MOD_SOFTCAP ? p.scale / p.softcap : 0.f;   // s*scale/cap
+    const float cap_out = MOD == MOD_SOFTCAP ? p.softcap * kLog2e : 0.f;
+    const uint32_t* kbits = p.keybits ? p.keybits + ((int64_t)w.b * p.G + w.g) * p.keybits_words : nullptr;
+    const unsigned char* bias_row = nullptr;
+    if (BIAS)
+      bias_row = static_cast<const unsigned char*>(p.bias) +
+                 (w.b * p.bs.b + w.g * p.bs.g + (int64_t)w.h * p.bs.h + (int64_t)(row_valid ? q : 0) * p.bs.s) *
+                     (p.bias_dtype == 1 ? 4 : 2);
+
+    float m_ref = -INFINITY, l = 0.f;
+    int n_done = 0;
+    for (int j = next_tile(w, w.lo_cta - 1); j >= 0; j = next_tile(w, j)) {
+      if (j < lo_i || j >= hi_i) continue;
+      const int k0 = j * 128;
+      mbar_wait(&s_full[wg], n_done & 1);
+      tc_fence_after();
+      uint32_t s[128];
+      tmem_ld32(tmem + lane_base + col_s + 0, &s[0]);
+      tmem_ld32(tmem + lane_base + col_s + 32, &s[32]);
+      tmem_ld32(tmem + lane_base + col_s + 64, &s[64]);
+      tmem_ld32(tmem + lane_base + col_s + 96, &s[96]);
+      tmem_wait_ld();
+      // ---- score modification (Eq.4) in the log2 domain: x = log2(e) * mod(scale * s)
+      float x[128];
+      const float alibi_base = slope_l2 * (float)(k0 - q_abs);
+#pragma unroll
+      for (int c = 0; c < 128; ++c) {
+        float v = __uint_as_float(s[c]);
+        if (MOD == MOD_SOFTCAP && !BIAS) {
+          v = cap_out * tanh_approx(v * cap_in);
+        } else {
+          v *= sc_l2;
+          if (MOD == MOD_ALIBI) v += fmaf(slope_l2, (float)c, alibi_base);
+        }
+        x[c] = v;
+      }
+      if (BIAS) {  // additive bias (Evoformer pair bias), then softcap if any (order G16)
+        if (p.bias_vec) {
+          const uint4* br = reinterpret_cast<const uint4*>(bias_row + (int64_t)k0 * 2);
+#pragma unroll
+          for (int c8 = 0; c8 < 16; ++c8) {
+            if (k0 + c8 * 8 + 8 <= p.Sk) {
+              const uint4 u = __ldg(br + c8);
+              const uint32_t ww[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                x[c8 * 8 + 2 * t] = fmaf(bf16_lo(ww[t]), kLog2e, x[c8 * 8 + 2 * t]);
+                x[c8 * 8 + 2 * t + 1] = fmaf(bf16_hi(ww[t]), kLog2e, x[c8 * 8 + 2 * t + 1]);
+              }
+            } else {  // ragged tail: element loads, predicated
+#pragma unroll
+              for (int t = 0; t < 8; ++t) {
+                const int k = k0 + c8 * 8 + t;
+                const unsigned short u = k < p.Sk ? reinterpret_cast<const unsigned short*>(bias_row)[k] : 0;
+                x[c8 * 8 + t] = fmaf(__uint_as_float((uint32_t)u << 16), kLog2e, x[c8 * 8 + t]);
+              }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 128; ++c) {
+            const int k = min(k0 + c, p.Sk - 1);
+            const float bv =
+                p.bias_dtype == 1
+                    ? reinterpret_cast<const float*>(bias_row)[(int64_t)k * p.bs.d]
+                    : __uint_as_float((uint32_t)reinterpret_cast<const unsigned short*>(bias_row)[(int64_t)k * p.bs.d]
+                                      << 16);
+            x[c] = fmaf(bv, kLog2e, x[c]);
+          }
+        }
+        if (MOD == MOD_SOFTCAP) {
+#pragma unroll
+          for (int c = 0; c < 128; ++c) x[c] = cap_out * tanh_approx(x[c] * (kLn2 / p.softcap));
+        }
+      }
+      // ---- masking: only tiles that are not inside every row's interval
+      const bool full_tile = k0 >= iv.lo && k0 + 128 <= iv.hi && k0 + 128 <= p.Sk;
+      if (__any_sync(0xffffffffu, !full_tile)) {
+#pragma unroll
+        for (int c = 0; c < 128; ++c) {
+          const int k = k0 + c;
+          x[c] = (k >= iv.lo && k < iv.hi) ? x[c] : -INFINITY;
+        }
+      }
+      if (kbits) {
+        uint32_t kw[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) kw[t] = __ldg(kbits + (k0 >> 5) + t);
+#pragma unroll
+        for (int c = 0; c < 128; ++c) x[c] = ((kw[c >> 5] >> (c & 31)) & 1u) ? x[c] : -INFINITY;
+      }
+      // ---- online softmax with conditional rescale (threshold kTau, log2 units)
+      float mt0 = -INFINITY, mt1 = -INFINITY, mt2 = -INFINITY, mt3 = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 128; c += 4) {
+        mt0 = fmaxf(mt0, x[c]);
+        mt1 = fmaxf(mt1, x[c + 1]);
+        mt2 = fmaxf(mt2, x[c + 2]);
+        mt3 = fmaxf(mt3, x[c + 3]);
+      }
+      const float mt = fmaxf(fmaxf(mt0, mt1), fmaxf(mt2, mt3));
+      const bool rescale = mt > m_ref + kTau;          // also true for the first finite tile (m_ref = -inf)
+      const float factor = rescale ? ex2(m_ref - mt) : 1.f;
+      if (n_done > 0 && __any_sync(0xffffffffu, rescale)) {
+        // O_i is quiescent: PV_i(j-1) completed before S_i(j)'s commit arrived.
+#pragma unroll
+        for (int c = 0; c < D; c += 32) {
+          uint32_t o[32];
+          tmem_ld32(tmem + lane_base + col_o + c, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * factor);
+          tmem_st32(tmem + lane_base + col_o + c, o);
+        }
+      }
+      if (rescale) {
+        l *= factor;
+        m_ref = mt;
+      }
+      const float m_use = m_ref == -INFINITY ? 0.f : m_ref;
+      float ls0 = 0.f, ls1 = 0.f;
+      uint32_t pk[64];
+#pragma unroll
+      for (int c = 0; c < 128; c += 2) {
+        const float p0 = ex2(x[c] - m_use), p1 = ex2(x[c + 1] - m_use);
+        ls0 += p0;
+        ls1 += p1;
+        pk[c >> 1] = pack_bf16(p0, p1);
+      }
+      l += ls0 + ls1;
+      tmem_st32(tmem + lane_base + col_s + C::P_OFF, &pk[0]);
+      tmem_st32(tmem + lane_base + col_s + C::P_OFF + 32, &pk[32]);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&p_full[wg]);
+      ++n_done;
+    }
+
+    // ============================== epilogue ==============================
+    if (n_done > 0) {
+      mbar_wait(&o_full[wg], 0);
+      tc_fence_after();
+    }
+    const float inv_l = l > 0.f ? 1.f / l : 0.f;
+    const float lam = DIFF ? (p.lambda_h ? p.lambda_h[w.h] : p.lambda) : 0.f;
+    float* xbuf = reinterpret_cast<float*>(sQ);      // diff: map-1 rows handed to WG0 (Q is dead now)
+    if (DIFF && wg == 1) {
+      if (n_done == 0) mbar_wait(q_full, 0);         // never overwrite Q while its TMA may be in flight
+#pragma unroll
+      for (int c = 0; c < D; c += 32) {
+        uint32_t o[32];
+        if (n_done > 0) {
+          tmem_ld32(tmem + lane_base + col_o + c, o);
+          tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int t = 0; t < 32; ++t) o[t] = 0u;
+        }
+#pragma unroll
+        for (int t4 = 0; t4 < 8; ++t4) {
+          const int chunk = (c >> 2) + t4;           // 16-byte chunk index within the row
+          float4 v = make_float4(__uint_as_float(o[4 * t4]) * inv_l, __uint_as_float(o[4 * t4 + 1]) * inv_l,
+                                 __uint_as_float(o[4 * t4 + 2]) * inv_l, __uint_as_float(o[4 * t4 + 3]) * inv_l);
+          reinterpret_cast<float4*>(xbuf + r * D)[chunk ^ (r & 7)] = v;
+        }
+      }
+      named_bar_sync(1, 256);
+    } else {
+      if (DIFF) named_bar_sync(1, 256);
+      const int64_t obase = w.b * p.os.b + w.g * p.os.g + (int64_t)w.h * p.os.h + (int64_t)q * p.os.s;
+      const int64_t gbase = w.b * p.gs.b + w.g * p.gs.g + (int64_t)w.h * p.gs.h + (int64_t)q * p.gs.s;
+#pragma unroll
+      for (int c = 0; c < D; c += 32) {
+        uint32_t o[32];
+        if (n_done > 0) {
+          tmem_ld32(tmem + lane_base + col_o + c, o);
+          tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int t = 0; t < 32; ++t) o[t] = 0u;
+        }
+        float f[32];
+#pragma unroll
+        for (int t = 0; t < 32; ++t) f[t] = __uint_as_float(o[t]) * inv_l;
+        if (DIFF) {
+#pragma unroll
+          for (int t4 = 0; t4 < 8; ++t4) {
+            const float4 v = reinterpret_cast<const float4*>(xbuf + r * D)[((c >> 2) + t4) ^ (r & 7)];
+            f[4 * t4] -= lam * v.x;
+            f[4 * t4 + 1] -= lam * v.y;
+            f[4 * t4 + 2] -= lam * v.z;
+            f[4 * t4 + 3] -= lam * v.w;
+          }
+        }
+        if (p.gate_mode != GATE_NONE && row_valid) {
+          const uint4* gp = reinterpret_cast<const uint4*>(static_cast<const unsigned short*>(p.gate) + gbase + c);
+#pragma unroll
+          for (int t8 = 0; t8 < 4; ++t8) {
+            const uint4 u = __ldg(gp + t8);
+            const uint32_t ww[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              float g0 = bf16_lo(ww[t]), g1 = bf16_hi(ww[t]);
+              if (p.gate_mode == GATE_SIGMOID) {
+                g0 = 1.f / (1.f + ex2(-g0 * kLog2e));
+                g1 = 1.f / (1.f + ex2(-g1 * kLog2e));
+              }
+              f[t8 * 8 + 2 * t] *= g0;
+              f[t8 * 8 + 2 * t + 1] *= g1;
+            }
+          }
+        }
+        if (row_valid) {
+          uint4* op = reinterpret_cast<uint4*>(static_cast<unsigned short*>(p.o) + obase + c);
+#pragma unroll
+          for (int t8 = 0; t8 < 4; ++t8)
+            op[t8] = make_uint4(pack_bf16(f[t8 * 8 + 0], f[t8 * 8 + 1]), pack_bf16(f[t8 * 8 + 2], f[t8 * 8 + 3]),
+                                pack_bf16(f[t8 * 8 + 4], f[t8 * 8 + 5]), pack_bf16(f[t8 * 8 + 6], f[t8 * 8 + 7]));
+        }
+      }
+      if (p.lse && row_valid)
+        p.lse[w.b * p.lses.b + w.g * p.lses.g + (int64_t)w.h * p.lses.h + (int64_t)q * p.lses.s] =
+            l > 0.f ? (m_ref + __log2f(l)) * kLn2 : -INFINITY;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 9) tmem_dealloc<512>(tmem);
+}
+
+template <int D, bool DIFF, int MOD>
+static cudaError_t launch_one(const AttnParams& p, const TmaMaps& maps, cudaStream_t stream) {
+  using C = TcCfg<D, DIFF>;
+  auto kern = p.bias ? attn_tc_kernel<D, DIFF, MOD, true> : attn_tc_kernel<D, DIFF, MOD, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_TOTAL);
+  if (e != cudaSuccess) return e;
+  const int rows_per_unit = DIFF ? 128 : 256;
+  const long long units = (long long)p.B * p.G * p.Hq * ((p.Sq + rows_per_unit - 1) / rows_per_unit);
+  kern<<<(unsigned)units, kThreadsTc, C::SMEM_TOTAL, stream>>>(p, maps);
+  return cudaGetLastError();
+}
+
+template <int D, bool DIFF>
+static cudaError_t launch_mod(const AttnParams& p, const TmaMaps& maps, cudaStream_t stream) {
+  switch (p.mod) {
+    case MOD_ALIBI: return launch_one<D, DIFF, MOD_ALIBI>(p, maps, stream);
+    case MOD_SOFTCAP: return launch_one<D, DIFF, MOD_SOFTCAP>(p, maps, stream);
+    default: return launch_one<D, DIFF, MOD_NONE>(p, maps, stream);
+  }
+}
+
+cudaError_t launch_attn_tc(const AttnParams& p, const TmaMaps& maps, cudaStream_t stream) {
+  const bool diff = p.maps == 2;
+  switch (p.Dqk) {
+    case 128: return diff ? launch_mod<128, true>(p, maps, stream) : launch_mod<128, false>(p, maps, stream);
+    case 64: return diff ? launch_mod<64, true>(p, maps, stream) : launch_mod<64, false>(p, maps, stream);
+    case 32: return diff ? launch_mod<32, true>(p, maps, stream) : launch_mod<32, false>(p, maps, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+int tc_chunk_elems(int D) { return D >= 64 ? 64 : 32; }
+
+}  // namespace fl

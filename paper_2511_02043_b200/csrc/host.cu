@@ -1,0 +1,617 @@
+// host.cu -- the C ABI of include/fl_attn.h: validation, descriptor -> device
+// params, TMA tensor-map encoding, kernel selection and launch.  No device
+// memory is ever allocated here and nothing synchronises; there is no fallback:
+// anything the kernels do not implement returns FL_ERR_UNSUPPORTED.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <initializer_list>
+#include <mutex>
+#include <string>
+
+#include "../../include/fl_attn.h"
+#include "params.h"
+
+namespace fl {
+cudaError_t launch_attn_simt(const AttnParams& p, cudaStream_t stream);
+cudaError_t launch_attn_tc(const AttnParams& p, const TmaMaps& maps, cudaStream_t stream);
+cudaError_t launch_pack_keymask(const unsigned char* km, int64_t sb, int64_t sg, int64_t sk, int B, int G, int Sk,
+                                int words, uint32_t* out, cudaStream_t stream);
+cudaError_t launch_fill_empty(const AttnParams& p, cudaStream_t stream);
+cudaError_t launch_diag_gemm(int n, int k, const CUtensorMap& ta, const CUtensorMap& tb, const void* a, float* c,
+                             bool bmn, bool atmem, cudaStream_t s);
+int tc_chunk_elems(int D);
+}  // namespace fl
+
+using namespace fl;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_launches = 0;
+
+fl_status fail(fl_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+fl_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(FL_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------- driver entry point
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn g_encode = nullptr;
+std::once_flag g_encode_once;
+
+EncodeTiledFn encode_fn() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<EncodeTiledFn>(fn);
+  });
+  return g_encode;
+}
+
+// ---------------------------------------------------------------- tensor views
+// Every tensor is normalised to a 5-D view [B, G, H, S, X]; rank-(4-r) inputs
+// get G = 1.  X is D for q/k/v/o/gate, S_k for bias, 1 for lse.
+struct View5 {
+  bool present = false;
+  void* data = nullptr;
+  int dtype = 0;
+  int64_t size[5] = {1, 1, 1, 1, 1};
+  int64_t stride[5] = {0, 0, 0, 0, 0};
+};
+
+int elem_bytes(int dtype) { return dtype == FL_F32 || dtype == FL_I32 ? 4 : dtype == FL_U8 ? 1 : 2; }
+
+// Map a rank-(base) or rank-(base+1) tensor onto slots; `slots` lists the View5
+// slot of each dim of the rank-(base+1) form (the G dim is slot 1).
+bool to_view(const fl_tensor& t, int q_rank, int rank_delta, View5& v) {
+  v = View5();
+  if (!t.data) return true;
+  if (t.rank != q_rank + rank_delta) return false;
+  v.present = true;
+  v.data = t.data;
+  v.dtype = t.dtype;
+  // full 5-slot order is B,G,H,S,X; rank_delta removes trailing slots (lse: X; key_mask: H... handled by caller)
+  const int n5 = 5 + rank_delta;              // number of slots used in the rank-5 (with G) form
+  int slot[5];
+  if (q_rank == 5) {
+    for (int i = 0; i < n5; ++i) slot[i] = i;
+  } else {
+    slot[0] = 0;
+    for (int i = 1; i < t.rank; ++i) slot[i] = i + 1;
+  }
+  for (int i = 0; i < t.rank; ++i) {
+    if (t.size[i] < 0) return false;
+    v.size[slot[i]] = t.size[i];
+    v.stride[slot[i]] = t.stride[i];
+  }
+  return true;
+}
+
+void byte_range(const View5& v, uintptr_t& lo, uintptr_t& hi) {
+  int64_t mn = 0, mx = 0;
+  for (int i = 0; i < 5; ++i) {
+    if (v.size[i] == 0) {
+      lo = hi = 0;
+      return;
+    }
+    const int64_t e = (v.size[i] - 1) * v.stride[i];
+    if (e < 0) mn += e; else mx += e;
+  }
+  const int eb = elem_bytes(v.dtype);
+  lo = reinterpret_cast<uintptr_t>(v.data) + mn * eb;
+  hi = reinterpret_cast<uintptr_t>(v.data) + (mx + 1) * eb;
+}
+
+bool overlaps(const View5& a, const View5& b) {
+  if (!a.present || !b.present) return false;
+  uintptr_t al, ah, bl, bh;
+  byte_range(a, al, ah);
+  byte_range(b, bl, bh);
+  return al < bh && bl < ah;
+}
+
+Strided5 strides_of(const View5& v) {
+  return Strided5{v.size[0] > 1 ? v.stride[0] : 0, v.size[1] > 1 ? v.stride[1] : 0, v.size[2] > 1 ? v.stride[2] : 0,
+                  v.size[3] > 1 ? v.stride[3] : 0, v.size[4] > 1 ? v.stride[4] : 1};
+}
+
+bool on_device(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+bool aligned16(const View5& v) {
+  if (reinterpret_cast<uintptr_t>(v.data) % 16) return false;
+  for (int i = 0; i < 4; ++i)
+    if (v.size[i] > 1 && (v.stride[i] * elem_bytes(v.dtype)) % 16) return false;
+  return true;
+}
+
+// Encode a 5-D bf16 tensor map (D, S, H, G, B) with box {CH, 128, 1, 1, 1}.
+fl_status encode_map(const View5& v, int ch, CUtensorMap* out, int* bcast_g, int* bcast_b, int box_rows = 128) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(FL_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable (driver too old?)");
+  cuuint64_t dim[5] = {(cuuint64_t)v.size[4], (cuuint64_t)v.size[3], (cuuint64_t)v.size[2], (cuuint64_t)v.size[1],
+                       (cuuint64_t)v.size[0]};
+  const int64_t st[5] = {1, v.stride[3], v.stride[2], v.stride[1], v.stride[0]};
+  *bcast_g = 0;
+  *bcast_b = 0;
+  cuuint64_t gstride[4];
+  int64_t span = (int64_t)dim[0] * 2;
+  for (int i = 1; i < 5; ++i) {
+    int64_t bytes = st[i] * 2;
+    if (dim[i] <= 1 || st[i] == 0) {
+      if (dim[i] > 1) {
+        if (i == 3) *bcast_g = 1;
+        else if (i == 4) *bcast_b = 1;
+        else return fail(FL_ERR_UNSUPPORTED, "stride-0 broadcast of the S or H dim is not supported on the bf16 path");
+      }
+      dim[i] = 1;
+      bytes = (span + 15) / 16 * 16;
+    }
+    if (bytes <= 0 || bytes % 16 != 0 || bytes >= (1ll << 40))
+      return fail(FL_ERR_MISALIGNED, "TMA needs 16-byte multiple strides (dim %d: %lld bytes)", i, (long long)bytes);
+    gstride[i - 1] = (cuuint64_t)bytes;
+    span = std::max<int64_t>(span, bytes * (int64_t)dim[i]);
+  }
+  if (reinterpret_cast<uintptr_t>(v.data) % 16 != 0) return fail(FL_ERR_MISALIGNED, "TMA needs 16-byte aligned data");
+  cuuint32_t box[5] = {(cuuint32_t)ch, (cuuint32_t)box_rows, 1, 1, 1};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, v.data, dim, gstride, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, ch == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(FL_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)r);
+  return FL_OK;
+}
+
+struct Prepared {
+  AttnParams p{};
+  View5 q, k, v, o, lse, bias, gate, km;
+  int q_rank = 4;
+  size_t keybits_bytes = 0;
+  bool empty_work = false;
+  bool no_keys = false;
+  bool bf16 = false;
+};
+
+fl_status check_vec(const fl_tensor& t, int dtype, int64_t n, const char* what) {
+  if (!t.data) return FL_OK;
+  if (t.dtype != dtype || t.rank != 1 || t.size[0] != n || (n > 1 && t.stride[0] != 1))
+    return fail(FL_ERR_INVALID_ARGUMENT, "%s: expected contiguous 1-D tensor of %lld elements", what, (long long)n);
+  return FL_OK;
+}
+
+fl_status prepare(const fl_attn_args* a, Prepared& P, bool device_ptrs) {
+  if (!a) return fail(FL_ERR_INVALID_ARGUMENT, "args is NULL");
+  const fl_variant& var = a->var;
+  if (var.abi_version != FL_ABI_VERSION)
+    return fail(FL_ERR_ABI_VERSION, "abi_version %u != %d", var.abi_version, FL_ABI_VERSION);
+  if (!a->q.data || !a->k.data || !a->v.data || !a->o.data)
+    return fail(FL_ERR_INVALID_ARGUMENT, "q, k, v and o are required");
+  const int R = a->q.rank;
+  if (R != 4 && R != 5) return fail(FL_ERR_INVALID_ARGUMENT, "q rank must be 4 or 5");
+  P.q_rank = R;
+  if (!to_view(a->q, R, 0, P.q) || !to_view(a->k, R, 0, P.k) || !to_view(a->v, R, 0, P.v) ||
+      !to_view(a->o, R, 0, P.o))
+    return fail(FL_ERR_SHAPE_MISMATCH, "q/k/v/o must share one rank (4 or 5) with non-negative sizes");
+  const int dt = a->q.dtype;
+  if (dt != FL_BF16 && dt != FL_F32) return fail(FL_ERR_UNSUPPORTED, "q dtype must be bf16 or f32");
+  if (a->k.dtype != dt || a->v.dtype != dt || a->o.dtype != dt)
+    return fail(FL_ERR_INVALID_ARGUMENT, "q, k, v and o must share one dtype");
+  P.bf16 = dt == FL_BF16;
+  for (const View5* t : {&P.q, &P.k, &P.v, &P.o})
+    if (t->size[4] > 1 && t->stride[4] != 1)
+      return fail(FL_ERR_UNSUPPORTED, "the last dim of q/k/v/o must be contiguous");
+  const int maps = var.diff ? 2 : 1;
+  const int64_t B = P.q.size[0], G = P.q.size[1];
+  for (const View5* t : {&P.k, &P.v, &P.o})
+    if (t->size[0] != B || t->size[1] != G) return fail(FL_ERR_SHAPE_MISMATCH, "batch dims of q/k/v/o differ");
+  if (P.q.size[2] % maps || P.k.size[2] % maps) return fail(FL_ERR_SHAPE_MISMATCH, "diff: q, k carry 2*H heads");
+  const int64_t Hq = P.q.size[2] / maps, Hkv = P.k.size[2] / maps;
+  if (P.v.size[2] != Hkv || P.o.size[2] != Hq || Hkv == 0 || Hq % Hkv)
+    return fail(FL_ERR_SHAPE_MISMATCH, "heads: need v.H == k.H/maps, o.H == q.H/maps, Hq %% Hkv == 0");
+  const int64_t Sq = P.q.size[3], Sk = P.k.size[3], Dqk = P.q.size[4], Dv = P.v.size[4];
+  if (P.o.size[3] != Sq || P.v.size[3] != Sk || P.k.size[4] != Dqk || P.o.size[4] != Dv)
+    return fail(FL_ERR_SHAPE_MISMATCH, "q/k/v/o sequence or head-dim sizes disagree");
+  if (Sq >= (1ll << 30) || Sk >= (1ll << 30) || B * G * Hq >= (1ll << 30))
+    return fail(FL_ERR_UNSUPPORTED, "sizes beyond 2^30");
+  if (P.bf16) {
+    if (Dqk != Dv || (Dqk != 32 && Dqk != 64 && Dqk != 128))
+      return fail(FL_ERR_UNSUPPORTED, "bf16 path: D_qk == D_v in {32, 64, 128} (got %lld, %lld)", (long long)Dqk,
+                  (long long)Dv);
+  } else if (Dqk < 1 || Dqk > 128 || Dv < 1 || Dv > 128) {
+    return fail(FL_ERR_UNSUPPORTED, "f32 path: D_qk, D_v in [1, 128]");
+  }
+  if (var.mod < FL_MOD_NONE || var.mod > FL_MOD_SOFTCAP) return fail(FL_ERR_INVALID_ARGUMENT, "bad mod");
+  if (var.mask < FL_MASK_NONE || var.mask > FL_MASK_BLOCKLIST) return fail(FL_ERR_INVALID_ARGUMENT, "bad mask");
+  if (var.gate_mode < FL_GATE_NONE || var.gate_mode > FL_GATE_SIGMOID)
+    return fail(FL_ERR_INVALID_ARGUMENT, "bad gate_mode");
+  if (var.mod == FL_MOD_SOFTCAP && !(var.softcap > 0.f)) return fail(FL_ERR_INVALID_ARGUMENT, "softcap must be > 0");
+  if (var.mod == FL_MOD_ALIBI && check_vec(var.alibi_slopes, FL_F32, Hq, "alibi_slopes")) return FL_ERR_INVALID_ARGUMENT;
+  if (var.diff && check_vec(var.lambda_h, FL_F32, Hq, "lambda_h")) return FL_ERR_INVALID_ARGUMENT;
+  if (var.causal_align != 0 && var.causal_align != 1) return fail(FL_ERR_INVALID_ARGUMENT, "causal_align is 0 or 1");
+  if (var.mask == FL_MASK_SLIDING && var.window < 0) return fail(FL_ERR_INVALID_ARGUMENT, "window must be >= 0");
+  if (var.mask == FL_MASK_PREFIX && var.prefix_len < 0) return fail(FL_ERR_INVALID_ARGUMENT, "prefix_len >= 0");
+  int n_docs = 0;
+  if (var.mask == FL_MASK_DOCUMENT) {
+    const fl_tensor& d = var.doc_offsets;
+    if (!d.data || d.dtype != FL_I32 || d.rank != 2 || d.size[0] != B || d.size[1] < 2 || d.stride[1] != 1)
+      return fail(FL_ERR_INVALID_ARGUMENT, "doc_offsets: i32 [B, n_docs+1] with contiguous rows");
+    n_docs = (int)d.size[1] - 1;
+  }
+  if (var.mask == FL_MASK_BLOCKLIST) {
+    if (var.blk_q <= 0 || var.blk_k <= 0 || var.blk_q % 16 || var.blk_k % 32)
+      return fail(FL_ERR_INVALID_ARGUMENT, "blocklist: blk_q % 16 == 0, blk_k % 32 == 0");
+    if (P.bf16 && (var.blk_q != 128 || var.blk_k != 128))
+      return fail(FL_ERR_UNSUPPORTED, "bf16 blocklist path needs blk_q == blk_k == 128");
+    const int64_t nqb = (Sq + var.blk_q - 1) / var.blk_q;
+    const fl_tensor &bi = var.blk_idx, &bc = var.blk_cnt;
+    if (!bi.data || !bc.data || bi.dtype != FL_I32 || bc.dtype != FL_I32 || bi.rank != 3 || bc.rank != 2 ||
+        bi.size[0] != B * G * Hq || bi.size[1] != nqb || bc.size[0] != B * G * Hq || bc.size[1] != nqb ||
+        bi.stride[2] != 1 || bi.stride[1] != bi.size[2] || bi.stride[0] != nqb * bi.size[2] || bc.stride[1] != 1 ||
+        bc.stride[0] != nqb)
+      return fail(FL_ERR_INVALID_ARGUMENT, "blk_idx i32 [B*G*Hq, n_qblk, max_sel], blk_cnt i32 [B*G*Hq, n_qblk], contiguous");
+  }
+  // optional tensors -------------------------------------------------------
+  if (a->lse.data) {
+    if (a->lse.dtype != FL_F32) return fail(FL_ERR_INVALID_ARGUMENT, "lse must be f32");
+    if (!to_view(a->lse, R, -1, P.lse)) return fail(FL_ERR_SHAPE_MISMATCH, "lse rank must be rank(q)-1");
+    if (P.lse.size[0] != B || P.lse.size[1] != G || P.lse.size[2] != Hq || P.lse.size[3] != Sq)
+      return fail(FL_ERR_SHAPE_MISMATCH, "lse shape must be [B,(G,)Hq,Sq]");
+    if (var.diff) return fail(FL_ERR_INVALID_ARGUMENT, "lse must be absent with diff (two softmax maps)");
+  }
+  if (var.bias.data) {
+    if (var.bias.dtype != FL_BF16 && var.bias.dtype != FL_F32) return fail(FL_ERR_INVALID_ARGUMENT, "bias: bf16 or f32");
+    if (!to_view(var.bias, R, 0, P.bias)) return fail(FL_ERR_SHAPE_MISMATCH, "bias rank must equal rank(q)");
+    const int64_t want[5] = {B, G, Hq, Sq, Sk};
+    for (int i = 0; i < 5; ++i)
+      if (P.bias.size[i] != want[i] && !(P.bias.size[i] == 1))
+        return fail(FL_ERR_SHAPE_MISMATCH, "bias must broadcast to [B,(G,)Hq,Sq,Sk]");
+    for (int i = 0; i < 5; ++i)
+      if (P.bias.size[i] == 1 && want[i] > 1) {
+        P.bias.size[i] = want[i];
+        P.bias.stride[i] = 0;
+      }
+  }
+  if (var.key_mask.data) {
+    if (var.key_mask.dtype != FL_U8) return fail(FL_ERR_INVALID_ARGUMENT, "key_mask must be u8");
+    if (var.key_mask.rank != R - 2) return fail(FL_ERR_SHAPE_MISMATCH, "key_mask rank must be rank(q)-2");
+    P.km.present = true;
+    P.km.data = var.key_mask.data;
+    P.km.dtype = FL_U8;
+    if (R == 5) {
+      P.km.size[0] = var.key_mask.size[0]; P.km.stride[0] = var.key_mask.stride[0];
+      P.km.size[1] = var.key_mask.size[1]; P.km.stride[1] = var.key_mask.stride[1];
+      P.km.size[4] = var.key_mask.size[2]; P.km.stride[4] = var.key_mask.stride[2];
+    } else {
+      P.km.size[0] = var.key_mask.size[0]; P.km.stride[0] = var.key_mask.stride[0];
+      P.km.size[4] = var.key_mask.size[1]; P.km.stride[4] = var.key_mask.stride[1];
+    }
+    if ((P.km.size[0] != B && P.km.size[0] != 1) || (P.km.size[1] != G && P.km.size[1] != 1) || P.km.size[4] != Sk)
+      return fail(FL_ERR_SHAPE_MISMATCH, "key_mask must be [B,(G,)Sk]");
+    P.keybits_bytes = (size_t)B * G * ((Sk + 127) / 128) * 16;
+  }
+  if (var.gate_mode != FL_GATE_NONE) {
+    if (!var.gate.data) return fail(FL_ERR_INVALID_ARGUMENT, "gate_mode set but gate absent");
+    if (!to_view(var.gate, R, 0, P.gate)) return fail(FL_ERR_SHAPE_MISMATCH, "gate rank must equal rank(q)");
+    for (int i = 0; i < 5; ++i)
+      if (P.gate.size[i] != P.o.size[i]) return fail(FL_ERR_SHAPE_MISMATCH, "gate shape must equal o's");
+    if (P.gate.size[4] > 1 && P.gate.stride[4] != 1) return fail(FL_ERR_UNSUPPORTED, "gate last dim must be contiguous");
+    if (P.bf16 && var.gate.dtype != FL_BF16) return fail(FL_ERR_UNSUPPORTED, "bf16 path: gate must be bf16");
+    if (!P.bf16 && var.gate.dtype != FL_BF16 && var.gate.dtype != FL_F32)
+      return fail(FL_ERR_INVALID_ARGUMENT, "gate must be bf16 or f32");
+  }
+  // alignment (bf16 path: TMA + 16-byte vector epilogue) -----------------------
+  if (P.bf16) {
+    for (const View5* t : {&P.q, &P.k, &P.v, &P.o})
+      if (!aligned16(*t)) return fail(FL_ERR_MISALIGNED, "bf16 path: q/k/v/o need 16-byte aligned base and strides");
+    if (P.gate.present && !aligned16(P.gate)) return fail(FL_ERR_MISALIGNED, "bf16 path: gate needs 16-byte alignment");
+  }
+  // aliasing: o must not overlap any input
+  for (const View5* t : {&P.q, &P.k, &P.v, &P.gate, &P.bias})
+    if (overlaps(P.o, *t)) return fail(FL_ERR_INVALID_ARGUMENT, "o overlaps an input tensor");
+  if (P.lse.present && (overlaps(P.lse, P.o) || overlaps(P.lse, P.q) || overlaps(P.lse, P.k) || overlaps(P.lse, P.v)))
+    return fail(FL_ERR_INVALID_ARGUMENT, "lse overlaps another tensor");
+  if (device_ptrs) {
+    const void* ptrs[] = {a->q.data, a->k.data, a->v.data, a->o.data, a->lse.data, var.bias.data, var.key_mask.data,
+                          var.gate.data, var.alibi_slopes.data, var.lambda_h.data, var.doc_offsets.data,
+                          var.blk_idx.data, var.blk_cnt.data};
+    for (const void* p : ptrs)
+      if (!on_device(p)) return fail(FL_ERR_INVALID_ARGUMENT, "a tensor pointer is not device memory on this device");
+  }
+
+  // device params ------------------------------------------------------------
+  AttnParams& p = P.p;
+  p.B = (int)B; p.G = (int)G; p.Hq = (int)Hq; p.Hkv = (int)Hkv; p.Sq = (int)Sq; p.Sk = (int)Sk;
+  p.Dqk = (int)Dqk; p.Dv = (int)Dv; p.maps = maps; p.grp = (int)(Hq / Hkv);
+  p.q_off = var.causal_align ? 0 : (int)(Sk - Sq);
+  p.q = P.q.data; p.k = P.k.data; p.v = P.v.data; p.o = P.o.data;
+  p.qs = strides_of(P.q); p.ks = strides_of(P.k); p.vs = strides_of(P.v); p.os = strides_of(P.o);
+  p.lse = static_cast<float*>(P.lse.data); p.lses = strides_of(P.lse);
+  p.scale = var.scale != 0.f ? var.scale : 1.f / std::sqrt((float)Dqk);
+  p.scale_log2 = p.scale * 1.4426950408889634f;
+  p.mod = var.mod; p.softcap = var.softcap;
+  p.alibi = static_cast<const float*>(var.alibi_slopes.data);
+  p.mask = var.mask; p.window = var.window; p.prefix = var.prefix_len;
+  p.doc_offsets = static_cast<const int32_t*>(var.doc_offsets.data); p.n_docs = n_docs;
+  p.doc_stride_b = var.mask == FL_MASK_DOCUMENT ? var.doc_offsets.stride[0] : 0;
+  p.doc_causal = var.doc_causal;
+  p.bias = P.bias.data; p.bias_dtype = P.bias.present ? (P.bias.dtype == FL_F32 ? 1 : 0) : 0;
+  p.bs = strides_of(P.bias);
+  p.bias_vec = P.bias.present && P.bias.dtype == FL_BF16 && P.bias.stride[4] == 1 &&
+               reinterpret_cast<uintptr_t>(P.bias.data) % 16 == 0 && (p.bs.b * 2) % 16 == 0 &&
+               (p.bs.g * 2) % 16 == 0 && (p.bs.h * 2) % 16 == 0 && (p.bs.s * 2) % 16 == 0;
+  p.keybits = nullptr; p.keybits_words = (int)((Sk + 127) / 128) * 4;
+  p.gate_mode = var.gate_mode; p.gate = P.gate.data; p.gs = strides_of(P.gate);
+  p.gate_dtype = P.gate.present ? (P.gate.dtype == FL_F32 ? 1 : 0) : 0;
+  p.lambda = var.lambda; p.lambda_h = static_cast<const float*>(var.lambda_h.data);
+  p.blk_idx = static_cast<const int32_t*>(var.blk_idx.data); p.blk_cnt = static_cast<const int32_t*>(var.blk_cnt.data);
+  p.blk_q = var.blk_q; p.blk_k = var.blk_k;
+  p.max_sel = var.mask == FL_MASK_BLOCKLIST ? (int)var.blk_idx.size[2] : 0;
+  p.n_qblk = var.mask == FL_MASK_BLOCKLIST ? (int)((Sq + var.blk_q - 1) / var.blk_q) : 0;
+  p.in_dtype = P.bf16 ? 0 : 1;
+  P.empty_work = B * G * Hq * Sq == 0 || Dv == 0;
+  P.no_keys = Sk == 0;
+  return FL_OK;
+}
+
+fl_status launch_prepared(Prepared& P, const fl_attn_args* a) {
+  cudaStream_t stream = static_cast<cudaStream_t>(a->stream);
+  if (P.empty_work) return FL_OK;
+  cudaError_t e;
+  if (P.no_keys) {
+    e = launch_fill_empty(P.p, stream);
+    ++g_launches;
+    return e == cudaSuccess ? FL_OK : cuda_fail(e, "fill_empty launch");
+  }
+  TmaMaps maps;
+  memset(&maps, 0, sizeof maps);
+  if (P.bf16) {
+    const int ch = tc_chunk_elems(P.p.Dqk);
+    fl_status s;
+    if ((s = encode_map(P.q, ch, &maps.q, &maps.q_bcast_g, &maps.q_bcast_b)) != FL_OK) return s;
+    if ((s = encode_map(P.k, ch, &maps.k, &maps.k_bcast_g, &maps.k_bcast_b)) != FL_OK) return s;
+    if ((s = encode_map(P.v, ch, &maps.v, &maps.v_bcast_g, &maps.v_bcast_b)) != FL_OK) return s;
+  }
+  if (P.km.present) {
+    if (!a->workspace || a->workspace_bytes < P.keybits_bytes)
+      return fail(FL_ERR_WORKSPACE, "key_mask needs %zu bytes of workspace", P.keybits_bytes);
+    uint32_t* bits = static_cast<uint32_t*>(a->workspace);
+    e = launch_pack_keymask(static_cast<const unsigned char*>(P.km.data), P.km.size[0] > 1 ? P.km.stride[0] : 0,
+                            P.km.size[1] > 1 ? P.km.stride[1] : 0, P.km.stride[4], P.p.B, P.p.G, P.p.Sk,
+                            P.p.keybits_words, bits, stream);
+    ++g_launches;
+    if (e != cudaSuccess) return cuda_fail(e, "pack_keymask launch");
+    P.p.keybits = bits;
+  }
+  if (P.bf16) {
+    if (P.p.mask == MASK_BLOCKLIST) return fail(FL_ERR_UNSUPPORTED, "bf16 blocklist kernel not built in this ABI revision");
+    e = launch_attn_tc(P.p, maps, stream);
+  } else {
+    e = launch_attn_simt(P.p, stream);
+  }
+  ++g_launches;
+  return e == cudaSuccess ? FL_OK : cuda_fail(e, "attention launch");
+}
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace
+
+// =============================================================================== C ABI
+extern "C" {
+
+fl_status fl_attn_fwd(const fl_attn_args* args) {
+  Prepared P;
+  fl_status s = prepare(args, P, true);
+  if (s != FL_OK) return s;
+  return launch_prepared(P, args);
+}
+
+fl_status fl_attn_workspace_size(const fl_attn_args* args, size_t* bytes) {
+  if (!bytes) return fail(FL_ERR_INVALID_ARGUMENT, "bytes is NULL");
+  Prepared P;
+  fl_status s = prepare(args, P, false);
+  if (s != FL_OK) return s;
+  *bytes = P.keybits_bytes;
+  return FL_OK;
+}
+
+// ---- host-buffer (end-to-end) entry --------------------------------------------
+namespace {
+struct HostPlan {
+  struct Item {
+    fl_tensor* t;       // tensor in the device copy of the args
+    size_t bytes;
+    size_t off;
+    bool out;
+  };
+  Item items[16];
+  int n = 0;
+  size_t total = 0;
+  size_t ws_off = 0, ws_bytes = 0;
+};
+
+size_t dense_bytes(const fl_tensor& t) {
+  size_t n = 1;
+  for (int i = 0; i < t.rank; ++i) n *= (size_t)t.size[i];
+  return n * elem_bytes(t.dtype);
+}
+
+bool is_contiguous(const fl_tensor& t) {
+  int64_t expect = 1;
+  for (int i = t.rank - 1; i >= 0; --i) {
+    if (t.size[i] > 1 && t.stride[i] != expect) return false;
+    expect *= t.size[i];
+  }
+  return true;
+}
+
+fl_status plan_host(fl_attn_args& d, HostPlan& hp) {
+  fl_tensor* ins[] = {&d.q, &d.k, &d.v, &d.var.bias, &d.var.key_mask, &d.var.gate, &d.var.alibi_slopes,
+                      &d.var.lambda_h, &d.var.doc_offsets, &d.var.blk_idx, &d.var.blk_cnt};
+  for (fl_tensor* t : ins) {
+    if (!t->data) continue;
+    if (!is_contiguous(*t)) return fail(FL_ERR_UNSUPPORTED, "fl_attn_fwd_host: host tensors must be contiguous");
+    hp.items[hp.n++] = {t, dense_bytes(*t), hp.total, false};
+    hp.total = align256(hp.total + dense_bytes(*t));
+  }
+  fl_tensor* outs[] = {&d.o, &d.lse};
+  for (fl_tensor* t : outs) {
+    if (!t->data) continue;
+    if (!is_contiguous(*t)) return fail(FL_ERR_UNSUPPORTED, "fl_attn_fwd_host: host tensors must be contiguous");
+    hp.items[hp.n++] = {t, dense_bytes(*t), hp.total, true};
+    hp.total = align256(hp.total + dense_bytes(*t));
+  }
+  return FL_OK;
+}
+}  // namespace
+
+fl_status fl_attn_host_scratch_size(const fl_attn_args* args, size_t* bytes) {
+  if (!args || !bytes) return fail(FL_ERR_INVALID_ARGUMENT, "NULL argument");
+  fl_attn_args d = *args;
+  HostPlan hp;
+  fl_status s = plan_host(d, hp);
+  if (s != FL_OK) return s;
+  Prepared P;
+  if ((s = prepare(args, P, false)) != FL_OK) return s;
+  *bytes = hp.total + align256(P.keybits_bytes);
+  return FL_OK;
+}
+
+fl_status fl_attn_fwd_host(const fl_attn_args* host_args, void* scratch, size_t scratch_bytes) {
+  if (!host_args) return fail(FL_ERR_INVALID_ARGUMENT, "args is NULL");
+  fl_attn_args d = *host_args;
+  HostPlan hp;
+  fl_status s = plan_host(d, hp);
+  if (s != FL_OK) return s;
+  Prepared P0;
+  if ((s = prepare(host_args, P0, false)) != FL_OK) return s;
+  const size_t need = hp.total + align256(P0.keybits_bytes);
+  if (!scratch || scratch_bytes < need) return fail(FL_ERR_WORKSPACE, "fl_attn_fwd_host needs %zu scratch bytes", need);
+  if (!on_device(scratch)) return fail(FL_ERR_INVALID_ARGUMENT, "scratch must be device memory");
+  cudaStream_t stream = static_cast<cudaStream_t>(host_args->stream);
+  char* base = static_cast<char*>(scratch);
+  void* host_ptr[16];
+  for (int i = 0; i < hp.n; ++i) {
+    host_ptr[i] = hp.items[i].t->data;
+    hp.items[i].t->data = base + hp.items[i].off;
+    // re-stride as dense row-major (same layout as the contiguous host tensor)
+  }
+  d.workspace = base + hp.total;
+  d.workspace_bytes = align256(P0.keybits_bytes);
+  Prepared P;
+  if ((s = prepare(&d, P, true)) != FL_OK) return s;
+  for (int i = 0; i < hp.n; ++i) {
+    if (hp.items[i].out) continue;
+    cudaError_t e = cudaMemcpyAsync(hp.items[i].t->data, host_ptr[i], hp.items[i].bytes, cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+  }
+  if ((s = launch_prepared(P, &d)) != FL_OK) return s;
+  for (int i = 0; i < hp.n; ++i) {
+    if (!hp.items[i].out) continue;
+    cudaError_t e = cudaMemcpyAsync(host_ptr[i], hp.items[i].t->data, hp.items[i].bytes, cudaMemcpyDeviceToHost, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+  }
+  return FL_OK;
+}
+
+void fl_shard_range(int64_t units, int32_t world, int32_t rank, int64_t* begin, int64_t* end) {
+  if (world <= 0 || rank < 0 || rank >= world || units <= 0) {
+    if (begin) *begin = 0;
+    if (end) *end = 0;
+    return;
+  }
+  const int64_t base = units / world, rem = units % world;
+  const int64_t b = rank * base + std::min<int64_t>(rank, rem);
+  if (begin) *begin = b;
+  if (end) *end = b + base + (rank < rem ? 1 : 0);
+}
+
+fl_status fl_diag_umma_gemm(const void* a, const void* b, float* c, int32_t n, int32_t k, int32_t b_mn_major,
+                            int32_t a_from_tmem, void* stream) {
+  if (!a || !b || !c) return fail(FL_ERR_INVALID_ARGUMENT, "NULL pointer");
+  if ((n != 32 && n != 64 && n != 128) || (k != 32 && k != 64 && k != 128))
+    return fail(FL_ERR_UNSUPPORTED, "n, k in {32, 64, 128}");
+  View5 va, vb;
+  va.present = vb.present = true;
+  va.data = const_cast<void*>(a);
+  vb.data = const_cast<void*>(b);
+  va.dtype = vb.dtype = FL_BF16;
+  // A [128, K] row-major
+  va.size[3] = 128; va.size[4] = k; va.stride[3] = k; va.stride[4] = 1;
+  // B [N, K] (K-major) or [K, N] (MN-major); box rows = 128 covers N or K (OOB rows zero-filled, unused)
+  if (b_mn_major) { vb.size[3] = k; vb.size[4] = n; vb.stride[3] = n; }
+  else { vb.size[3] = n; vb.size[4] = k; vb.stride[3] = k; }
+  vb.stride[4] = 1;
+  CUtensorMap ta, tb;
+  int g0, b0;
+  fl_status s;
+  if ((s = encode_map(va, k >= 64 ? 64 : 32, &ta, &g0, &b0)) != FL_OK) return s;
+  if ((s = encode_map(vb, b_mn_major ? (n >= 64 ? 64 : 32) : (k >= 64 ? 64 : 32), &tb, &g0, &b0,
+                      b_mn_major ? k : n)) != FL_OK)
+    return s;
+  cudaError_t e = launch_diag_gemm(n, k, ta, tb, a, c, b_mn_major != 0, a_from_tmem != 0, static_cast<cudaStream_t>(stream));
+  ++g_launches;
+  return e == cudaSuccess ? FL_OK : cuda_fail(e, "diag gemm launch");
+}
+
+fl_status fl_rsa_build_summaries(const fl_tensor* k, fl_tensor* kmin, fl_tensor* kmax, int32_t blk_k, void* stream) {
+  (void)k; (void)kmin; (void)kmax; (void)blk_k; (void)stream;
+  return fail(FL_ERR_UNSUPPORTED, "fl_rsa_build_summaries: not built in this revision");
+}
+
+fl_status fl_rsa_select(const fl_tensor* q, const fl_tensor* kmin, const fl_tensor* kmax, int32_t topk, int32_t blk_q,
+                        int32_t blk_k, int32_t causal_align, fl_tensor* blk_idx, fl_tensor* blk_cnt, void* stream) {
+  (void)q; (void)kmin; (void)kmax; (void)topk; (void)blk_q; (void)blk_k; (void)causal_align; (void)blk_idx;
+  (void)blk_cnt; (void)stream;
+  return fail(FL_ERR_UNSUPPORTED, "fl_rsa_select: not built in this revision");
+}
+
+const char* fl_status_string(fl_status s) {
+  switch (s) {
+    case FL_OK: return "FL_OK";
+    case FL_ERR_INVALID_ARGUMENT: return "FL_ERR_INVALID_ARGUMENT";
+    case FL_ERR_UNSUPPORTED: return "FL_ERR_UNSUPPORTED";
+    case FL_ERR_MISALIGNED: return "FL_ERR_MISALIGNED";
+    case FL_ERR_SHAPE_MISMATCH: return "FL_ERR_SHAPE_MISMATCH";
+    case FL_ERR_WORKSPACE: return "FL_ERR_WORKSPACE";
+    case FL_ERR_CUDA: return "FL_ERR_CUDA";
+    case FL_ERR_ABI_VERSION: return "FL_ERR_ABI_VERSION";
+  }
+  return "FL_ERR_UNKNOWN";
+}
+
+const char* fl_last_error(void) { return g_err.c_str(); }
+int32_t fl_abi_version(void) { return FL_ABI_VERSION; }
+int64_t fl_launch_count(int32_t reset) {
+  int64_t n = g_launches;
+  if (reset) g_launches = 0;
+  return n;
+}
+
+}  // extern "C"

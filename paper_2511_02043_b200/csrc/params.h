@@ -1,0 +1,57 @@
+// params.h -- device-side problem description built by host.cu from fl_attn_args
+// (include/fl_attn.h).  One struct for every kernel of the attention family; it is
+// passed by value as a __grid_constant__ kernel parameter.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+
+namespace fl {
+
+enum Mod : int32_t { MOD_NONE = 0, MOD_ALIBI = 1, MOD_SOFTCAP = 2 };
+enum Mask : int32_t { MASK_NONE = 0, MASK_CAUSAL = 1, MASK_SLIDING = 2, MASK_PREFIX = 3, MASK_DOCUMENT = 4,
+                      MASK_BLOCKLIST = 5 };
+enum Gate : int32_t { GATE_NONE = 0, GATE_MUL = 1, GATE_SIGMOID = 2 };
+
+struct Strided5 {          // element strides of a [B,G,H,S,D] view
+  int64_t b, g, h, s, d;
+};
+
+struct AttnParams {
+  // ---- shape (rank-4 inputs have G = 1)
+  int32_t B, G, Hq, Hkv, Sq, Sk, Dqk, Dv;
+  int32_t maps;            // 2 for differential attention, else 1
+  int32_t grp;             // Hq / Hkv (G15)
+  int32_t q_off;           // Sk - Sq for bottom-right alignment (G12), 0 for top-left
+  // ---- data (device pointers) and strides
+  const void* q; const void* k; const void* v; void* o;
+  Strided5 qs, ks, vs, os;
+  float* lse; Strided5 lses;       // lse [B,G,H,S] (d unused)
+  // ---- score modification (Eq.4), in the log2 domain where noted
+  float scale;             // softmax scale (G1)
+  float scale_log2;        // scale * log2(e)
+  int32_t mod;
+  float softcap;           // cap
+  const float* alibi;      // [Hq] slopes or nullptr (default 2^(-8(h+1)/Hq))
+  // ---- masking
+  int32_t mask, window, prefix;
+  const int32_t* doc_offsets; int32_t n_docs; int64_t doc_stride_b; int32_t doc_causal;
+  const void* bias; int32_t bias_dtype; int32_t bias_vec; Strided5 bs;  // bias [B,G,H,Sq,Sk] (d = key stride);
+                                                               // bias_vec: bf16, key-contiguous, 16-B aligned rows
+  const uint32_t* keybits; int32_t keybits_words;              // packed key mask [B*G][words] (workspace)
+  // ---- gate / diff
+  int32_t gate_mode; const void* gate; Strided5 gs; int32_t gate_dtype;
+  float lambda; const float* lambda_h;
+  // ---- block list (RSA)
+  const int32_t* blk_idx; const int32_t* blk_cnt; int32_t blk_q, blk_k, max_sel, n_qblk;
+  int32_t in_dtype;        // 0 bf16, 1 f32
+};
+
+// TMA tensor maps for the tcgen05 kernel family (5-D: D, S, H, G, B).
+struct TmaMaps {
+  CUtensorMap q, k, v;
+  // dims whose tensor-map extent was collapsed to 1 because the view broadcasts
+  // them (stride 0): the kernel passes coordinate 0 there.
+  int32_t q_bcast_g, q_bcast_b, k_bcast_g, k_bcast_b, v_bcast_g, v_bcast_b;
+};
+
+}  // namespace fl

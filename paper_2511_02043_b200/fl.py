@@ -1,0 +1,169 @@
+"""Python binding of the C ABI (include/fl_attn.h) -- argument marshalling only.
+
+Every step of the attention path runs in the CUDA kernels behind
+``libfl_attn.so``; this module turns torch tensors (device memory, streams) into
+``fl_tensor`` views and raises :class:`FlError` on any non-OK status.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import torch
+
+from . import _lib
+from ._lib import AttnArgs, FlError, Tensor, Variant  # noqa: F401  (re-export)
+
+MOD = {"none": 0, "alibi": 1, "softcap": 2}
+MASK = {"none": 0, "causal": 1, "sliding": 2, "prefix": 3, "document": 4, "blocklist": 5}
+GATE = {"none": 0, "mul": 1, "sigmoid": 2}
+_DT = {torch.bfloat16: _lib.FL_BF16, torch.float32: _lib.FL_F32, torch.uint8: _lib.FL_U8,
+       torch.int32: _lib.FL_I32, torch.bool: _lib.FL_U8}
+
+
+def tensor(t: Optional[torch.Tensor]) -> Tensor:
+    out = Tensor()
+    if t is None:
+        return out
+    if t.dim() > 5:
+        raise ValueError("rank > 5")
+    if t.dtype not in _DT:
+        raise TypeError(f"unsupported dtype {t.dtype}")
+    out.data = t.data_ptr()
+    out.dtype = _DT[t.dtype]
+    out.rank = t.dim()
+    for i, (s, st) in enumerate(zip(t.shape, t.stride())):
+        out.size[i] = s
+        out.stride[i] = st
+    return out
+
+
+def _f32vec(x, device):
+    if x is None:
+        return None
+    if not torch.is_tensor(x):
+        x = torch.tensor(x, dtype=torch.float32)
+    return x.to(device=device, dtype=torch.float32).contiguous()
+
+
+def make_args(q, k, v, o, lse=None, *, scale=0.0, mod="none", softcap=0.0, alibi_slopes=None, mask="none",
+              window=0, prefix=0, doc_offsets=None, doc_causal=False, causal_align=0, bias=None, key_mask=None,
+              gate_mode="none", gate=None, diff=False, lam=0.0, lambda_h=None, blk_idx=None, blk_cnt=None,
+              blk_q=128, blk_k=128, stream=None, keep=None):
+    """Fill an fl_attn_args.  ``keep`` collects temporaries that must outlive the call."""
+    keep = [] if keep is None else keep
+    dev = q.device
+    a = AttnArgs()
+    a.q, a.k, a.v, a.o, a.lse = tensor(q), tensor(k), tensor(v), tensor(o), tensor(lse)
+    var = a.var
+    var.abi_version = _lib.ABI_VERSION
+    var.scale = float(scale)
+    var.mod = MOD[mod]
+    var.softcap = float(softcap)
+    sl = _f32vec(alibi_slopes, dev)
+    keep.append(sl)
+    var.alibi_slopes = tensor(sl)
+    var.mask = MASK[mask]
+    var.window = int(window)
+    var.prefix_len = int(prefix)
+    if doc_offsets is not None:
+        do = doc_offsets if torch.is_tensor(doc_offsets) else torch.as_tensor(doc_offsets)
+        do = do.to(device=dev, dtype=torch.int32).contiguous()
+        keep.append(do)
+        var.doc_offsets = tensor(do)
+    var.doc_causal = int(bool(doc_causal))
+    var.causal_align = int(causal_align)
+    var.bias = tensor(bias)
+    if key_mask is not None and key_mask.dtype == torch.bool:
+        key_mask = key_mask.to(torch.uint8)
+        keep.append(key_mask)
+    var.key_mask = tensor(key_mask)
+    var.gate_mode = GATE[gate_mode]
+    var.gate = tensor(gate)
+    var.diff = int(bool(diff))
+    var.lambda_ = float(lam)
+    lh = _f32vec(lambda_h, dev)
+    keep.append(lh)
+    var.lambda_h = tensor(lh)
+    for name, t in (("blk_idx", blk_idx), ("blk_cnt", blk_cnt)):
+        if t is not None:
+            t = (t if torch.is_tensor(t) else torch.as_tensor(t)).to(device=dev, dtype=torch.int32).contiguous()
+            keep.append(t)
+            setattr(var, name, tensor(t))
+    var.blk_q, var.blk_k = int(blk_q), int(blk_k)
+    if stream is None and q.is_cuda:
+        stream = torch.cuda.current_stream(q.device)
+    a.stream = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+    return a
+
+
+def out_shape(q, v, diff):
+    shp = list(q.shape)
+    if diff:
+        shp[-3] //= 2
+    shp[-1] = v.shape[-1]
+    return shp
+
+
+def attn_fwd(q, k, v, *, out=None, return_lse=False, lse=None, workspace=None, **variant):
+    """Fused attention forward on the current CUDA stream.
+
+    q/k/v: CUDA tensors [B,H,S,D] or [B,G,H,S,D] (bf16 -> tcgen05 path, f32 ->
+    exact SIMT path).  Variant keywords follow fl_variant (see make_args).
+    Returns ``out`` (and ``lse`` when ``return_lse``)."""
+    diff = variant.get("diff", False)
+    if out is None:
+        out = torch.empty(out_shape(q, v, diff), device=q.device, dtype=q.dtype)
+    if return_lse and lse is None:
+        lse = torch.empty(out_shape(q, v, diff)[:-1], device=q.device, dtype=torch.float32)
+    keep: list = []
+    a = make_args(q, k, v, out, lse, keep=keep, **variant)
+    need = C.c_size_t(0)
+    _lib.check(_lib.lib().fl_attn_workspace_size(C.byref(a), C.byref(need)))
+    if need.value:
+        if workspace is None or workspace.numel() * workspace.element_size() < need.value:
+            workspace = torch.empty(need.value, dtype=torch.uint8, device=q.device)
+        keep.append(workspace)
+        a.workspace = workspace.data_ptr()
+        a.workspace_bytes = need.value
+    _lib.check(_lib.lib().fl_attn_fwd(C.byref(a)))
+    return (out, lse) if return_lse else out
+
+
+class HostRunner:
+    """End-to-end entry over HOST buffers (fl_attn_fwd_host): H2D copies of the
+    inputs, the kernel and the D2H copy of the output, all enqueued by the C ABI
+    on one stream.  Device scratch is allocated once and reused."""
+
+    def __init__(self, device="cuda"):
+        self.device = torch.device(device)
+        self.scratch = None
+
+    def __call__(self, q, k, v, out, lse=None, stream=None, **variant):
+        keep: list = []
+        a = make_args(q, k, v, out, lse, keep=keep, stream=stream or torch.cuda.current_stream(self.device),
+                      **variant)
+        need = C.c_size_t(0)
+        _lib.check(_lib.lib().fl_attn_host_scratch_size(C.byref(a), C.byref(need)))
+        if self.scratch is None or self.scratch.numel() < need.value:
+            self.scratch = torch.empty(max(need.value, 1), dtype=torch.uint8, device=self.device)
+        _lib.check(_lib.lib().fl_attn_fwd_host(C.byref(a), self.scratch.data_ptr(), self.scratch.numel()))
+        return out
+
+
+def diag_umma_gemm(a: torch.Tensor, b: torch.Tensor, n: int, k: int, b_mn_major=False, a_from_tmem=False):
+    c = torch.empty(128, n, device=a.device, dtype=torch.float32)
+    s = torch.cuda.current_stream(a.device).cuda_stream
+    _lib.check(_lib.lib().fl_diag_umma_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), n, k, int(b_mn_major),
+                                            int(a_from_tmem), s))
+    return c
+
+
+def shard_range(units: int, world: int, rank: int):
+    b, e = C.c_int64(), C.c_int64()
+    _lib.lib().fl_shard_range(units, world, rank, C.byref(b), C.byref(e))
+    return b.value, e.value
+
+
+def launch_count(reset=False) -> int:
+    return int(_lib.lib().fl_launch_count(int(reset)))
