@@ -47,6 +47,8 @@ def _compile(src, extra):
 
 def build(verbose: bool = False, extra=None) -> str:
     extra = list(extra or [])
+    if os.environ.get("FL_DEBUG_HANG"):
+        extra.append("-DFL_DEBUG_HANG")
     os.makedirs(BUILD, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:

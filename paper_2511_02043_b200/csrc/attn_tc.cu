@@ -40,6 +40,12 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kTau = 8.0f;
 constexpr int kThreadsTc = 384;
+// Register split via setmaxnreg: the CTA launches with 168 regs/thread (launch
+// bounds 384 x 1); the control warpgroup gives registers back and the two softmax
+// warpgroups take them.  inc blocks until the CTA's pool can pay, so the split
+// must fit in what the CTA owns or the second softmax WG deadlocks.
+constexpr uint32_t kRegsLaunch = 168, kRegsCtl = 88, kRegsSoftmax = 208;
+static_assert(2 * 128 * kRegsSoftmax + 128 * kRegsCtl <= kThreadsTc * kRegsLaunch, "setmaxnreg split exceeds CTA pool");
 
 template <int D, bool DIFF>
 struct TcCfg {
@@ -160,7 +166,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   const int gv = maps.v_bcast_g ? 0 : w.g, bv = maps.v_bcast_b ? 0 : w.b;
 
   if (warp >= 8) {
-   regs_dec<96>();
+   regs_dec<kRegsCtl>();
    if (warp == 8) {
     // ============================== TMA producer ==============================
     if (lane == 0) {
@@ -263,7 +269,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     }
    }
   } else {
-    regs_inc<208>();
+    regs_inc<kRegsSoftmax>();
     // ============================== softmax warpgroups ==============================
     const int wg = warp >> 2;
     const int r = threadIdx.x & 127;                 // row within the tile == TMEM lane

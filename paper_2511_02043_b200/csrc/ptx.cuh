@@ -6,6 +6,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cstdio>
 
 #define FL_DEVICE __device__ __forceinline__
 
@@ -43,7 +44,7 @@ FL_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
 #ifdef FL_DEBUG_HANG
   long long spins = 0;
   while (!mbar_try_wait(bar, parity)) {
-    if (++spins > (1ll << 26)) {
+    if (++spins > (1ll << 22)) {
       printf("fl: mbarrier hang block %d thread %d bar %p parity %u\n", blockIdx.x, threadIdx.x, bar, parity);
       asm volatile("trap;");
     }
