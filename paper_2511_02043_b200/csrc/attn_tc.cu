@@ -85,8 +85,11 @@ __device__ __forceinline__ Work decode_work(const AttnParams& p) {
   const int nqb = (p.Sq + rows_per_unit - 1) / rows_per_unit;
   const int nbgh = p.B * p.G * p.Hq;
   const int u = blockIdx.x;
-  const int qb = nqb - 1 - u / nbgh;                 // heaviest (latest) query blocks first
-  const int bgh = u % nbgh;
+  // (b,h)-major so the ~148 co-resident CTAs share a few heads' K/V in L2;
+  // inside a head the heaviest (latest, for causal) query blocks go first.
+  const int bgh = u / nqb;
+  const int qb = nqb - 1 - u % nqb;
+  (void)nbgh;
   w.h = bgh % p.Hq;
   w.g = (bgh / p.Hq) % p.G;
   w.b = bgh / (p.Hq * p.G);
@@ -279,6 +282,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     const int q_abs = q + p.q_off;
     const Interval iv = row_interval(p, w.b, q);
     const int lo_i = w.lo[wg], hi_i = w.hi[wg];
+    const int c_lo = max(w.lo[0], w.lo[1]), c_hi = min(w.hi[0], w.hi[1]);  // tiles both warpgroups need
     const uint32_t col_s = wg ? C::COL_S1 : C::COL_S0;
     const uint32_t col_o = wg ? C::COL_O1 : C::COL_O0;
     float slope_l2 = 0.f;
@@ -309,13 +313,14 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       tmem_wait_ld();
       // ---- score modification (Eq.4) in the log2 domain: x = log2(e) * mod(scale * s)
       float x[128];
+      constexpr bool kRaw = MOD == MOD_NONE && !BIAS;  // keep raw s; scale folds into the exp FFMA
       const float alibi_base = slope_l2 * (float)(k0 - q_abs);
 #pragma unroll
       for (int c = 0; c < 128; ++c) {
         float v = __uint_as_float(s[c]);
         if (MOD == MOD_SOFTCAP && !BIAS) {
           v = cap_out * tanh_approx(v * cap_in);
-        } else {
+        } else if (!kRaw) {
           v *= sc_l2;
           if (MOD == MOD_ALIBI) v += fmaf(slope_l2, (float)c, alibi_base);
         }
@@ -379,13 +384,14 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       // ---- online softmax with conditional rescale (threshold kTau, log2 units)
       float mt0 = -INFINITY, mt1 = -INFINITY, mt2 = -INFINITY, mt3 = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 128; c += 4) {
-        mt0 = fmaxf(mt0, x[c]);
-        mt1 = fmaxf(mt1, x[c + 1]);
-        mt2 = fmaxf(mt2, x[c + 2]);
-        mt3 = fmaxf(mt3, x[c + 3]);
+      for (int c = 0; c < 128; c += 8) {
+        mt0 = fmax3(mt0, x[c], x[c + 1]);
+        mt1 = fmax3(mt1, x[c + 2], x[c + 3]);
+        mt2 = fmax3(mt2, x[c + 4], x[c + 5]);
+        mt3 = fmax3(mt3, x[c + 6], x[c + 7]);
       }
-      const float mt = fmaxf(fmaxf(mt0, mt1), fmaxf(mt2, mt3));
+      const float xscale = kRaw ? sc_l2 : 1.f;        // x * xscale is the log2-domain score
+      const float mt = fmaxf(fmaxf(mt0, mt1), fmaxf(mt2, mt3)) * xscale;
       const bool rescale = mt > m_ref + kTau;          // also true for the first finite tile (m_ref = -inf)
       const float factor = rescale ? ex2(m_ref - mt) : 1.f;
       if (n_done > 0 && __any_sync(0xffffffffu, rescale)) {
@@ -404,17 +410,36 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         l *= factor;
         m_ref = mt;
       }
-      const float m_use = m_ref == -INFINITY ? 0.f : m_ref;
-      float ls0 = 0.f, ls1 = 0.f;
+      const float neg_m = m_ref == -INFINITY ? 0.f : -m_ref;
+      // Ping-pong: the two warpgroups take turns on the MUFU (exp) pipe for the
+      // tiles both need, so each exp loop runs at full rate while the tensor
+      // pipe works for the other warpgroup (CTA-local named barriers 2 and 3).
+      const bool common = j >= c_lo && j < c_hi;
+      if (common) {
+        if (wg == 0 && j > c_lo) named_bar_sync(2, 256);
+        if (wg == 1) named_bar_sync(3, 256);
+      }
+      float ls0 = 0.f, ls1 = 0.f, ls2 = 0.f, ls3 = 0.f;
       uint32_t pk[64];
 #pragma unroll
-      for (int c = 0; c < 128; c += 2) {
-        const float p0 = ex2(x[c] - m_use), p1 = ex2(x[c + 1] - m_use);
-        ls0 += p0;
-        ls1 += p1;
-        pk[c >> 1] = pack_bf16(p0, p1);
+      for (int c = 0; c < 128; c += 4) {
+        float a0, a1, a2, a3;
+        ffma2(a0, a1, x[c], x[c + 1], xscale, xscale, neg_m, neg_m);
+        ffma2(a2, a3, x[c + 2], x[c + 3], xscale, xscale, neg_m, neg_m);
+        a0 = ex2(a0);
+        a1 = ex2(a1);
+        a2 = ex2(a2);
+        a3 = ex2(a3);
+        fadd2(ls0, ls1, ls0, ls1, a0, a1);
+        fadd2(ls2, ls3, ls2, ls3, a2, a3);
+        pk[c >> 1] = pack_bf16(a0, a1);
+        pk[(c >> 1) + 1] = pack_bf16(a2, a3);
       }
-      l += ls0 + ls1;
+      if (common) {
+        if (wg == 0) named_bar_arrive(3, 256);
+        if (wg == 1 && j < c_hi - 1) named_bar_arrive(2, 256);
+      }
+      l += (ls0 + ls1) + (ls2 + ls3);
       tmem_st32(tmem + lane_base + col_s + C::P_OFF, &pk[0]);
       tmem_st32(tmem + lane_base + col_s + C::P_OFF + 32, &pk[32]);
       tmem_wait_st();

@@ -204,6 +204,24 @@ FL_DEVICE void regs_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" :
 template <uint32_t N>
 FL_DEVICE void regs_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
 
+FL_DEVICE float fmax3(float a, float b, float c) { return fmaxf(a, fmaxf(b, c)); }
+// packed fp32x2 FMA / ADD (sm_100 FFMA2 / FADD2): two lanes per instruction
+FL_DEVICE void ffma2(float& dx, float& dy, float ax, float ay, float bx, float by, float cx, float cy) {
+  asm("{.reg .b64 a, b, c, d;\n\tmov.b64 a, {%2,%3};\n\tmov.b64 b, {%4,%5};\n\tmov.b64 c, {%6,%7};\n\t"
+      "fma.rn.f32x2 d, a, b, c;\n\tmov.b64 {%0,%1}, d;}"
+      : "=f"(dx), "=f"(dy)
+      : "f"(ax), "f"(ay), "f"(bx), "f"(by), "f"(cx), "f"(cy));
+}
+FL_DEVICE void fadd2(float& dx, float& dy, float ax, float ay, float bx, float by) {
+  asm("{.reg .b64 a, b, d;\n\tmov.b64 a, {%2,%3};\n\tmov.b64 b, {%4,%5};\n\tadd.rn.f32x2 d, a, b;\n\t"
+      "mov.b64 {%0,%1}, d;}"
+      : "=f"(dx), "=f"(dy)
+      : "f"(ax), "f"(ay), "f"(bx), "f"(by));
+}
+FL_DEVICE void named_bar_arrive(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 FL_DEVICE void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
