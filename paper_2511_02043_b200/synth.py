@@ -135,12 +135,12 @@ def clustered_qk(q_shape, k_shape, *, seed=2, blk=128, n_clusters=32, dtype=torc
     return one(q_shape, "q", grp), one(k_shape, "k", 1)
 
 
-def gate_logits(shape, *, seed=0, dtype=torch.bfloat16, lead=2):
-    return uniform(shape, seed=seed, tensor="gate", dtype=dtype, lo=-4.0, hi=4.0, lead=lead)
+def gate_logits(shape, *, seed=0, dtype=torch.bfloat16, lead=2, slab_range=None):
+    return uniform(shape, seed=seed, tensor="gate", dtype=dtype, lo=-4.0, hi=4.0, lead=lead, slab_range=slab_range)
 
 
-def pair_bias(shape, *, seed=0, dtype=torch.bfloat16, lead=2):
-    return uniform(shape, seed=seed, tensor="bias", dtype=dtype, lo=-4.0, hi=4.0, lead=lead)
+def pair_bias(shape, *, seed=0, dtype=torch.bfloat16, lead=2, slab_range=None):
+    return uniform(shape, seed=seed, tensor="bias", dtype=dtype, lo=-4.0, hi=4.0, lead=lead, slab_range=slab_range)
 
 
 def key_mask(shape, *, seed=0, p_zero=0.1, lead=1):
