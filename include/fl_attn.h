@@ -140,16 +140,27 @@ fl_status fl_attn_workspace_size(const fl_attn_args* args, size_t* bytes);
 fl_status fl_attn_host_scratch_size(const fl_attn_args* args, size_t* bytes);
 fl_status fl_attn_fwd_host(const fl_attn_args* host_args, void* device_scratch, size_t scratch_bytes);
 
-/* RSA block summaries (reading G10): kmin/kmax [B*(G)*Hkv, n_kblk, D] bf16 = exact
- * element-wise min / max of the keys of each KV block of blk_k keys. */
+/* RSA block summaries (reading G10; the paper only names RSA).
+ *   k    : bf16 [B,Hkv,S_k,D] or [B,G,Hkv,S_k,D], contiguous last dim, 16-byte aligned rows, D % 8 == 0, D <= 1024.
+ *   kmin, kmax : bf16 [B*G*Hkv, n_kblk, D] contiguous, n_kblk = ceil(S_k / blk_k); device memory owned by
+ *          the caller.  kmin[bh, j, d] = min over the keys of block j (keys [j*blk_k, min((j+1)*blk_k, S_k)))
+ *          of K[bh, key, d]; kmax likewise.  Exact (min/max of bf16 values).
+ *   blk_k > 0.  One launch, HBM-bound (one pass over K). */
 fl_status fl_rsa_build_summaries(const fl_tensor* k, fl_tensor* kmin, fl_tensor* kmax,
                                  int32_t blk_k, void* stream);
 
-/* RSA selection (reading G10/G11): for each (b, h, q-block i) with diagonal block c,
- * score_j = max_{q in block i, h' in h's KV group} sum_d max(q_d kmax_jd, q_d kmin_jd),
- * 0 < j < c; list = {0} U {c} U top-k(score) (ties to lower j), ascending, -1 padded.
- * blk_idx i32 [B*(G)*Hq, n_qblk, max_sel >= topk+2], blk_cnt i32 [B*(G)*Hq, n_qblk]. */
-fl_status fl_rsa_select(const fl_tensor* q, const fl_tensor* kmin, const fl_tensor* kmax,
+/* RSA selection (reading G10/G11): for each (b, g, h, q-block i of blk_q rows) with diagonal block
+ *   c = min(floor(q_abs(last row of block i) / blk_k), n_kblk - 1)   (q_abs per causal_align, G12),
+ *   score_j = max_{q in block i, h' in h's KV group} sum_d max(q_d kmax_jd, q_d kmin_jd),  0 < j < c;
+ *   list = {0} U {c} U top-k(score) (ties to the lower j), ascending, -1 padded (all of 0..c if c <= topk+1).
+ *   q    : bf16 [B,(G,)Hq,S_q,D], D in {64, 128}, TMA-aligned as for fl_attn_fwd.
+ *   kmin, kmax : as written by fl_rsa_build_summaries for the same K (Hkv = kmin.size[0] / (B*G)).
+ *   s_k  : number of keys the summaries cover (n_kblk == ceil(s_k / blk_k)); n_kblk <= 256 (D=128) / 512 (D=64).
+ *   blk_q == blk_k == 128; 0 <= topk; topk + 2 <= max_sel <= 512.
+ *   blk_idx : i32 [B*G*Hq, n_qblk, max_sel] contiguous; blk_cnt : i32 [B*G*Hq, n_qblk] contiguous.
+ *   The scores are one tcgen05 GEMM per (b, h) over K = 2D (q+ . kmax + q- . kmin, exact identity for
+ *   kmax >= kmin), fp32 accumulation; near-ties may resolve differently from an fp64 evaluation (G11). */
+fl_status fl_rsa_select(const fl_tensor* q, const fl_tensor* kmin, const fl_tensor* kmax, int32_t s_k,
                         int32_t topk, int32_t blk_q, int32_t blk_k, int32_t causal_align,
                         fl_tensor* blk_idx, fl_tensor* blk_cnt, void* stream);
 

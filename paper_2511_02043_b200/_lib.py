@@ -67,7 +67,8 @@ def lib():
         L.fl_rsa_build_summaries.argtypes = [C.POINTER(Tensor), C.POINTER(Tensor), C.POINTER(Tensor), C.c_int32,
                                              C.c_void_p]
         L.fl_rsa_select.argtypes = [C.POINTER(Tensor), C.POINTER(Tensor), C.POINTER(Tensor), C.c_int32, C.c_int32,
-                                    C.c_int32, C.c_int32, C.POINTER(Tensor), C.POINTER(Tensor), C.c_void_p]
+                                    C.c_int32, C.c_int32, C.c_int32, C.POINTER(Tensor), C.POINTER(Tensor),
+                                    C.c_void_p]
         L.fl_shard_range.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.fl_shard_range.restype = None
         L.fl_diag_umma_gemm.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,

@@ -45,6 +45,8 @@ constexpr int kThreadsTc = 384;
 // warpgroups take them.  inc blocks until the CTA's pool can pay, so the split
 // must fit in what the CTA owns or the second softmax WG deadlocks.
 constexpr uint32_t kRegsLaunch = 168, kRegsCtl = 88, kRegsSoftmax = 208;
+// FL_MASK_BLOCKLIST: at most this many listed KV blocks per query block on the bf16 path.
+constexpr int kMaxSelTc = 256;
 static_assert(2 * 128 * kRegsSoftmax + 128 * kRegsCtl <= kThreadsTc * kRegsLaunch, "setmaxnreg split exceeds CTA pool");
 
 template <int D, bool DIFF>
@@ -65,17 +67,24 @@ struct TcCfg {
   static constexpr int SMEM_RING = 2 * TILE_BYTES;
   static constexpr int SMEM_BAR = SMEM_RING + NSLOT * TILE_BYTES;
   static constexpr int NBAR = 1 + 2 * NSLOT + 6;
-  static constexpr int SMEM_TOTAL = SMEM_BAR + NBAR * 8 + 16 + 1024;  // + alignment slack
+  static constexpr int SMEM_SCHED = SMEM_BAR + NBAR * 8 + 16;       // blocklist schedule (RSA)
+  static constexpr int SMEM_TOTAL = SMEM_SCHED + (2 * kMaxSelTc + 8) * 4 + 1024;  // + alignment slack
   static constexpr uint32_t IDESC_S = idesc_bf16_f32(128, BN, 0);   // Q (K-major) x K (K-major)
   static constexpr uint32_t IDESC_O = idesc_bf16_f32(128, D, 1);    // P (TMEM) x V (MN-major)
   static constexpr int ENTRIES_PER_TILE = DIFF ? 3 : 2;              // K0 [K1] V
 };
 
+// The KV tiles a CTA walks form a "schedule" indexed by t.  For every interval
+// mask (masks.cuh) t IS the KV tile index and warpgroup i needs t in [lo[i], hi[i]).
+// For the RSA block list (FL_MASK_BLOCKLIST) the two warpgroups' sorted lists are
+// merged in shared memory: sched[t] = kv tile | need0 << 30 | need1 << 31, and
+// lo/hi are the first / one-past-last schedule steps each warpgroup needs.
 struct Work {
   int b, g, h;
   int q0[2];            // first query row of each warpgroup's tile
-  int lo[2], hi[2];     // KV tile range [lo, hi) each warpgroup needs
+  int lo[2], hi[2];     // schedule range [lo, hi) each warpgroup needs
   int lo_cta, hi_cta;
+  const uint32_t* sched;  // blocklist schedule (nullptr for interval masks)
 };
 
 template <int D, bool DIFF>
@@ -113,10 +122,73 @@ __device__ __forceinline__ Work decode_work(const AttnParams& p) {
     }
   }
   if (w.hi_cta <= w.lo_cta) w.lo_cta = w.hi_cta = 0;
+  w.sched = nullptr;
   return w;
 }
 
-__device__ __forceinline__ bool needs(const Work& w, int i, int j) { return j >= w.lo[i] && j < w.hi[i]; }
+// Blocklist mode: one thread merges the two warpgroups' sorted lists into `sched`
+// (kv tile | need bits) and stores [n, lo0, hi0, lo1, hi1] after it.  Entries
+// outside the valid key range or duplicated are dropped.
+__device__ __forceinline__ void build_sched(const AttnParams& p, const Work& w, uint32_t* sched) {
+  const int nkb = (p.Sk + 127) / 128;
+  const int32_t* li[2];
+  int cnt[2];
+  const int64_t bgh = ((int64_t)w.b * p.G + w.g) * p.Hq + w.h;
+  for (int i = 0; i < 2; ++i) {
+    cnt[i] = 0;
+    li[i] = nullptr;
+    if (w.q0[i] < p.Sq) {
+      const int64_t row = bgh * p.n_qblk + w.q0[i] / 128;
+      li[i] = p.blk_idx + row * p.max_sel;
+      cnt[i] = min(p.blk_cnt[row], p.max_sel);
+    }
+  }
+  int a = 0, z = 0, n = 0, last = -1;
+  int lo[2] = {1 << 30, 1 << 30}, hi[2] = {0, 0};
+  while (a < cnt[0] || z < cnt[1]) {
+    const int ja = a < cnt[0] ? li[0][a] : (1 << 30), jz = z < cnt[1] ? li[1][z] : (1 << 30);
+    const int j = min(ja, jz);
+    uint32_t need = 0;
+    if (ja == j) { need |= 1u; ++a; }
+    if (jz == j) { need |= 2u; ++z; }
+    if (j < 0 || j >= nkb) continue;
+    if (j == last) {                                   // duplicate entry: merge its bits
+      sched[n - 1] |= need << 30;
+      for (int i = 0; i < 2; ++i) if (need >> i & 1u) hi[i] = n;
+      continue;
+    }
+    if (n >= 2 * kMaxSelTc) break;
+    sched[n] = (uint32_t)j | (need << 30);
+    for (int i = 0; i < 2; ++i)
+      if (need >> i & 1u) {
+        lo[i] = min(lo[i], n);
+        hi[i] = n + 1;
+      }
+    last = j;
+    ++n;
+  }
+  int* meta = reinterpret_cast<int*>(sched + 2 * kMaxSelTc);
+  meta[0] = n;
+  for (int i = 0; i < 2; ++i) {
+    meta[1 + 2 * i] = hi[i] > 0 ? lo[i] : 0;
+    meta[2 + 2 * i] = hi[i];
+  }
+}
+
+__device__ __forceinline__ void load_sched(Work& w, const uint32_t* sched) {
+  const int* meta = reinterpret_cast<const int*>(sched + 2 * kMaxSelTc);
+  w.sched = sched;
+  w.lo[0] = meta[1]; w.hi[0] = meta[2];
+  w.lo[1] = meta[3]; w.hi[1] = meta[4];
+  w.lo_cta = 0;
+  w.hi_cta = meta[0];
+}
+
+__device__ __forceinline__ bool needs(const Work& w, int i, int j) {
+  if (w.sched) return (w.sched[j] >> (30 + i)) & 1u;
+  return j >= w.lo[i] && j < w.hi[i];
+}
+__device__ __forceinline__ int kv_tile(const Work& w, int j) { return w.sched ? (int)(w.sched[j] & 0x3FFFFFFFu) : j; }
 __device__ __forceinline__ int next_tile(const Work& w, int j) {
   for (++j; j < w.hi_cta; ++j)
     if (needs(w, 0, j) || needs(w, 1, j)) return j;
@@ -142,8 +214,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const Work w = decode_work<D, DIFF>(p);
+  Work w = decode_work<D, DIFF>(p);
+  uint32_t* sched = reinterpret_cast<uint32_t*>(smem + C::SMEM_SCHED);
+  const bool blocklist = p.mask == MASK_BLOCKLIST;
 
+  if (blocklist && warp == 9 && lane == 0) build_sched(p, w, sched);
   if (warp == 8 && lane == 0) {
     mbar_init(q_full, 1);
     for (int s = 0; s < C::NSLOT; ++s) {
@@ -162,6 +237,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (blocklist) load_sched(w, sched);
 
   const int hkv = w.h / p.grp;
   const int gq = maps.q_bcast_g ? 0 : w.g, bq = maps.q_bcast_b ? 0 : w.b;
@@ -194,7 +270,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           const int head = is_v ? hkv : hkv + t * p.Hkv;
           const int gg = is_v ? gv : gk, bb = is_v ? bv : bk;
           for (int c = 0; c < C::NCH; ++c)
-            tma_load_5d(dst + c * C::CHUNK_BYTES, m, &full[slot], c * C::CH, j * C::BN, head, gg, bb);
+            tma_load_5d(dst + c * C::CHUNK_BYTES, m, &full[slot], c * C::CH, kv_tile(w, j) * C::BN, head, gg, bb);
         }
       }
     }
@@ -281,8 +357,17 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     const bool row_valid = q < p.Sq;
     const int q_abs = q + p.q_off;
     const Interval iv = row_interval(p, w.b, q);
-    const int lo_i = w.lo[wg], hi_i = w.hi[wg];
-    const int c_lo = max(w.lo[0], w.lo[1]), c_hi = min(w.hi[0], w.hi[1]);  // tiles both warpgroups need
+    // first / one-past-last schedule steps both warpgroups need (ping-pong range)
+    int c_lo = max(w.lo[0], w.lo[1]), c_hi = min(w.hi[0], w.hi[1]);
+    if (w.sched) {
+      c_lo = 1 << 30;
+      c_hi = 0;
+      for (int t = w.lo_cta; t < w.hi_cta; ++t)
+        if (needs(w, 0, t) && needs(w, 1, t)) {
+          c_lo = min(c_lo, t);
+          c_hi = t + 1;
+        }
+    }
     const uint32_t col_s = wg ? C::COL_S1 : C::COL_S0;
     const uint32_t col_o = wg ? C::COL_O1 : C::COL_O0;
     float slope_l2 = 0.f;
@@ -301,8 +386,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     float m_ref = -INFINITY, l = 0.f;
     int n_done = 0;
     for (int j = next_tile(w, w.lo_cta - 1); j >= 0; j = next_tile(w, j)) {
-      if (j < lo_i || j >= hi_i) continue;
-      const int k0 = j * 128;
+      if (!needs(w, wg, j)) continue;
+      const int k0 = kv_tile(w, j) * 128;
       mbar_wait(&s_full[wg], n_done & 1);
       tc_fence_after();
       uint32_t s[128];
@@ -414,7 +499,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       // Ping-pong: the two warpgroups take turns on the MUFU (exp) pipe for the
       // tiles both need, so each exp loop runs at full rate while the tensor
       // pipe works for the other warpgroup (CTA-local named barriers 2 and 3).
-      const bool common = j >= c_lo && j < c_hi;
+      const bool common = needs(w, 0, j) && needs(w, 1, j);
       if (common) {
         if (wg == 0 && j > c_lo) named_bar_sync(2, 256);
         if (wg == 1) named_bar_sync(3, 256);

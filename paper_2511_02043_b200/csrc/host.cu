@@ -26,6 +26,11 @@ cudaError_t launch_fill_empty(const AttnParams& p, cudaStream_t stream);
 cudaError_t launch_diag_gemm(int n, int k, const CUtensorMap& ta, const CUtensorMap& tb, const void* a, float* c,
                              bool bmn, bool atmem, cudaStream_t s);
 int tc_chunk_elems(int D);
+cudaError_t launch_rsa_summaries(const void* k, int64_t sb, int64_t sg, int64_t sh, int64_t ss, int B, int G, int H,
+                                 int Sk, int D, int blk, void* kmin, void* kmax, cudaStream_t stream);
+cudaError_t launch_rsa_select(const RsaSelParams& p, const CUtensorMap& tq, const CUtensorMap& tmin,
+                              const CUtensorMap& tmax, cudaStream_t stream);
+int rsa_select_max_blocks(int D);
 }  // namespace fl
 
 using namespace fl;
@@ -268,6 +273,8 @@ fl_status prepare(const fl_attn_args* a, Prepared& P, bool device_ptrs) {
       return fail(FL_ERR_INVALID_ARGUMENT, "blocklist: blk_q % 16 == 0, blk_k % 32 == 0");
     if (P.bf16 && (var.blk_q != 128 || var.blk_k != 128))
       return fail(FL_ERR_UNSUPPORTED, "bf16 blocklist path needs blk_q == blk_k == 128");
+    if (P.bf16 && var.blk_idx.data && var.blk_idx.rank == 3 && var.blk_idx.size[2] > 256)
+      return fail(FL_ERR_UNSUPPORTED, "bf16 blocklist path: max_sel <= 256");
     const int64_t nqb = (Sq + var.blk_q - 1) / var.blk_q;
     const fl_tensor &bi = var.blk_idx, &bc = var.blk_cnt;
     if (!bi.data || !bc.data || bi.dtype != FL_I32 || bc.dtype != FL_I32 || bi.rank != 3 || bc.rank != 2 ||
@@ -409,7 +416,6 @@ fl_status launch_prepared(Prepared& P, const fl_attn_args* a) {
     P.p.keybits = bits;
   }
   if (P.bf16) {
-    if (P.p.mask == MASK_BLOCKLIST) return fail(FL_ERR_UNSUPPORTED, "bf16 blocklist kernel not built in this ABI revision");
     e = launch_attn_tc(P.p, maps, stream);
   } else {
     e = launch_attn_simt(P.p, stream);
@@ -581,15 +587,97 @@ fl_status fl_diag_umma_gemm(const void* a, const void* b, float* c, int32_t n, i
 }
 
 fl_status fl_rsa_build_summaries(const fl_tensor* k, fl_tensor* kmin, fl_tensor* kmax, int32_t blk_k, void* stream) {
-  (void)k; (void)kmin; (void)kmax; (void)blk_k; (void)stream;
-  return fail(FL_ERR_UNSUPPORTED, "fl_rsa_build_summaries: not built in this revision");
+  if (!k || !kmin || !kmax || !k->data || !kmin->data || !kmax->data)
+    return fail(FL_ERR_INVALID_ARGUMENT, "rsa_build_summaries: k, kmin, kmax are required");
+  if (blk_k <= 0) return fail(FL_ERR_INVALID_ARGUMENT, "rsa_build_summaries: blk_k must be > 0");
+  if (k->dtype != FL_BF16 || kmin->dtype != FL_BF16 || kmax->dtype != FL_BF16)
+    return fail(FL_ERR_UNSUPPORTED, "rsa_build_summaries: bf16 only");
+  if (k->rank != 4 && k->rank != 5) return fail(FL_ERR_INVALID_ARGUMENT, "rsa_build_summaries: k rank 4 or 5");
+  View5 kv;
+  if (!to_view(*k, k->rank, 0, kv)) return fail(FL_ERR_SHAPE_MISMATCH, "rsa_build_summaries: bad k view");
+  const int64_t B = kv.size[0], G = kv.size[1], H = kv.size[2], Sk = kv.size[3], D = kv.size[4];
+  if (D % 8 || D > 1024 || D < 8) return fail(FL_ERR_UNSUPPORTED, "rsa_build_summaries: D %% 8 == 0, 8 <= D <= 1024");
+  if (D > 1 && kv.stride[4] != 1) return fail(FL_ERR_UNSUPPORTED, "rsa_build_summaries: k last dim must be contiguous");
+  if (!aligned16(kv)) return fail(FL_ERR_MISALIGNED, "rsa_build_summaries: k needs 16-byte aligned rows");
+  const int64_t nkb = (Sk + blk_k - 1) / blk_k;
+  for (const fl_tensor* t : {static_cast<const fl_tensor*>(kmin), static_cast<const fl_tensor*>(kmax)})
+    if (t->rank != 3 || t->size[0] != B * G * H || t->size[1] != nkb || t->size[2] != D || t->stride[2] != 1 ||
+        t->stride[1] != D || t->stride[0] != nkb * D || reinterpret_cast<uintptr_t>(t->data) % 16)
+      return fail(FL_ERR_SHAPE_MISMATCH, "rsa_build_summaries: kmin/kmax must be contiguous bf16 [B*G*Hkv, n_kblk, D]");
+  for (const void* ptr : {k->data, kmin->data, kmax->data})
+    if (!on_device(ptr)) return fail(FL_ERR_INVALID_ARGUMENT, "rsa_build_summaries: pointers must be device memory");
+  if (B * G * H == 0 || nkb == 0) return FL_OK;
+  if (B * G * H > 65535) return fail(FL_ERR_UNSUPPORTED, "rsa_build_summaries: B*G*H > 65535");
+  cudaError_t e = launch_rsa_summaries(kv.data, kv.size[0] > 1 ? kv.stride[0] : 0, kv.size[1] > 1 ? kv.stride[1] : 0,
+                                       kv.size[2] > 1 ? kv.stride[2] : 0, kv.stride[3], (int)B, (int)G, (int)H, (int)Sk,
+                                       (int)D, blk_k, kmin->data, kmax->data, static_cast<cudaStream_t>(stream));
+  ++g_launches;
+  return e == cudaSuccess ? FL_OK : cuda_fail(e, "rsa_summaries launch");
 }
 
-fl_status fl_rsa_select(const fl_tensor* q, const fl_tensor* kmin, const fl_tensor* kmax, int32_t topk, int32_t blk_q,
-                        int32_t blk_k, int32_t causal_align, fl_tensor* blk_idx, fl_tensor* blk_cnt, void* stream) {
-  (void)q; (void)kmin; (void)kmax; (void)topk; (void)blk_q; (void)blk_k; (void)causal_align; (void)blk_idx;
-  (void)blk_cnt; (void)stream;
-  return fail(FL_ERR_UNSUPPORTED, "fl_rsa_select: not built in this revision");
+fl_status fl_rsa_select(const fl_tensor* q, const fl_tensor* kmin, const fl_tensor* kmax, int32_t s_k, int32_t topk,
+                        int32_t blk_q, int32_t blk_k, int32_t causal_align, fl_tensor* blk_idx, fl_tensor* blk_cnt,
+                        void* stream) {
+  if (!q || !kmin || !kmax || !blk_idx || !blk_cnt || !q->data || !kmin->data || !kmax->data || !blk_idx->data ||
+      !blk_cnt->data)
+    return fail(FL_ERR_INVALID_ARGUMENT, "rsa_select: q, kmin, kmax, blk_idx, blk_cnt are required");
+  if (blk_q != 128 || blk_k != 128) return fail(FL_ERR_UNSUPPORTED, "rsa_select: blk_q == blk_k == 128");
+  if (causal_align != 0 && causal_align != 1) return fail(FL_ERR_INVALID_ARGUMENT, "rsa_select: causal_align 0 or 1");
+  if (q->dtype != FL_BF16 || kmin->dtype != FL_BF16 || kmax->dtype != FL_BF16)
+    return fail(FL_ERR_UNSUPPORTED, "rsa_select: bf16 only");
+  if (q->rank != 4 && q->rank != 5) return fail(FL_ERR_INVALID_ARGUMENT, "rsa_select: q rank 4 or 5");
+  View5 qv;
+  if (!to_view(*q, q->rank, 0, qv)) return fail(FL_ERR_SHAPE_MISMATCH, "rsa_select: bad q view");
+  const int64_t B = qv.size[0], G = qv.size[1], Hq = qv.size[2], Sq = qv.size[3], D = qv.size[4];
+  if (D != 64 && D != 128) return fail(FL_ERR_UNSUPPORTED, "rsa_select: D in {64, 128}");
+  if (qv.stride[4] != 1) return fail(FL_ERR_UNSUPPORTED, "rsa_select: q last dim must be contiguous");
+  if (s_k <= 0) return fail(FL_ERR_INVALID_ARGUMENT, "rsa_select: s_k must be > 0");
+  const int64_t nkb = (s_k + blk_k - 1) / blk_k, nqb = (Sq + blk_q - 1) / blk_q;
+  if (B * G == 0 || kmin->rank != 3 || kmin->size[0] % (B * G)) return fail(FL_ERR_SHAPE_MISMATCH, "rsa_select: kmin rank 3 [B*G*Hkv, n_kblk, D]");
+  const int64_t Hkv = kmin->size[0] / (B * G);
+  if (Hkv == 0 || Hq % Hkv) return fail(FL_ERR_SHAPE_MISMATCH, "rsa_select: Hq %% Hkv != 0");
+  for (const fl_tensor* t : {kmin, kmax})
+    if (t->rank != 3 || t->size[0] != B * G * Hkv || t->size[1] != nkb || t->size[2] != D || t->stride[2] != 1 ||
+        t->stride[1] != D || t->stride[0] != nkb * D)
+      return fail(FL_ERR_SHAPE_MISMATCH, "rsa_select: kmin/kmax must be contiguous [B*G*Hkv, ceil(s_k/blk_k), D]");
+  if (nkb > rsa_select_max_blocks((int)D))
+    return fail(FL_ERR_UNSUPPORTED, "rsa_select: n_kblk %lld exceeds %d at D=%lld", (long long)nkb,
+                rsa_select_max_blocks((int)D), (long long)D);
+  if (topk < 0) return fail(FL_ERR_INVALID_ARGUMENT, "rsa_select: topk >= 0");
+  const int64_t max_sel = blk_idx->size[2];
+  if (blk_idx->dtype != FL_I32 || blk_cnt->dtype != FL_I32 || blk_idx->rank != 3 || blk_cnt->rank != 2 ||
+      blk_idx->size[0] != B * G * Hq || blk_idx->size[1] != nqb || blk_idx->stride[2] != 1 ||
+      blk_idx->stride[1] != max_sel || blk_idx->stride[0] != nqb * max_sel || blk_cnt->size[0] != B * G * Hq ||
+      blk_cnt->size[1] != nqb || blk_cnt->stride[1] != 1 || blk_cnt->stride[0] != nqb)
+    return fail(FL_ERR_SHAPE_MISMATCH, "rsa_select: blk_idx i32 [B*G*Hq, n_qblk, max_sel], blk_cnt i32 [B*G*Hq, n_qblk], contiguous");
+  if (max_sel < topk + 2 || max_sel > 512) return fail(FL_ERR_INVALID_ARGUMENT, "rsa_select: topk + 2 <= max_sel <= 512");
+  for (const void* ptr : {q->data, kmin->data, kmax->data, blk_idx->data, blk_cnt->data})
+    if (!on_device(ptr)) return fail(FL_ERR_INVALID_ARGUMENT, "rsa_select: pointers must be device memory");
+  if (Sq == 0 || Hq == 0) return FL_OK;
+  CUtensorMap tq, tmn, tmx;
+  int qbg, qbb, d0, d1;
+  fl_status st;
+  if ((st = encode_map(qv, 64, &tq, &qbg, &qbb)) != FL_OK) return st;
+  for (int w = 0; w < 2; ++w) {
+    const fl_tensor* t = w ? kmax : kmin;
+    View5 sv;
+    sv.present = true;
+    sv.data = t->data;
+    sv.dtype = FL_BF16;
+    sv.size[2] = t->size[0]; sv.stride[2] = t->stride[0];
+    sv.size[3] = t->size[1]; sv.stride[3] = t->stride[1];
+    sv.size[4] = t->size[2]; sv.stride[4] = 1;
+    if ((st = encode_map(sv, 64, w ? &tmx : &tmn, &d0, &d1)) != FL_OK) return st;
+  }
+  RsaSelParams p{};
+  p.B = (int)B; p.G = (int)G; p.Hq = (int)Hq; p.Hkv = (int)Hkv; p.grp = (int)(Hq / Hkv);
+  p.Sq = (int)Sq; p.Sk = s_k; p.D = (int)D; p.nkb = (int)nkb; p.nqb = (int)nqb; p.topk = topk;
+  p.max_sel = (int)max_sel; p.q_off = causal_align ? 0 : (int)(s_k - Sq);
+  p.blk_idx = static_cast<int32_t*>(blk_idx->data); p.blk_cnt = static_cast<int32_t*>(blk_cnt->data);
+  p.q_bcast_g = qbg; p.q_bcast_b = qbb;
+  cudaError_t e = launch_rsa_select(p, tq, tmn, tmx, static_cast<cudaStream_t>(stream));
+  ++g_launches;
+  return e == cudaSuccess ? FL_OK : cuda_fail(e, "rsa_select launch");
 }
 
 const char* fl_status_string(fl_status s) {

@@ -54,4 +54,12 @@ struct TmaMaps {
   int32_t q_bcast_g, q_bcast_b, k_bcast_g, k_bcast_b, v_bcast_g, v_bcast_b;
 };
 
+// RSA block selection (rsa.cu), built by host.cu's fl_rsa_select.
+struct RsaSelParams {
+  int B, G, Hq, Hkv, grp, Sq, Sk, D, nkb, nqb, topk, max_sel, q_off, parts;
+  int32_t* blk_idx;  // [B*G*Hq][nqb][max_sel]
+  int32_t* blk_cnt;  // [B*G*Hq][nqb]
+  int q_bcast_g, q_bcast_b;
+};
+
 }  // namespace fl

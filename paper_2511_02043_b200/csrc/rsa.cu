@@ -1,0 +1,325 @@
+// rsa.cu -- the data-dependent half of Rectified Sparse Attention (reading G10;
+// the paper only names RSA, as a variant beyond FlexAttention's
+// template): per-KV-block key summaries and the per-query-block block list that
+// the attention kernels then walk (mask FL_MASK_BLOCKLIST).
+//
+//  * rsa_summaries_kernel: kmin/kmax[bh, j, d] = element-wise min / max of the keys
+//    of KV block j.  Exact (min/max of bf16 values is a bf16 value).  One pass over
+//    K: HBM-bound, 16-byte loads, one CTA per (bh, block).
+//
+//  * rsa_select_kernel: score_j = max_{q in block} sum_d max(q_d kmax_jd, q_d kmin_jd).
+//    Because kmax >= kmin the per-d maximum is exactly linear in the split
+//    q = q+ + q-:  max(q_d kmax_d, q_d kmin_d) = q+_d kmax_d + q-_d kmin_d, so every
+//    score of a (b, h) is ONE tensor-core GEMM over K = 2D:
+//        D[j, q] = [kmax | kmin]_j . [q+ | q-]_q        (tcgen05, accumulator in TMEM)
+//    issued with the summaries as the A operand (M = 128 blocks per tile) so that a
+//    TMEM lane is one block j: the max over the 128 queries of the block is then a
+//    register-local row max of that thread (no cross-thread reduction).  The top-k
+//    (ties to the lower j) is a rank count over the candidates in shared memory, and
+//    the ascending list {0} U {c} U top-k is written with a ballot prefix sum.
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <math.h>
+
+#include "params.h"
+#include "ptx.cuh"
+
+namespace fl {
+
+// ------------------------------------------------------------------ summaries
+// grid (n_kblk, BGH), 128 threads.  K row r of block j is K[bgh][j*blk + r][:].
+__global__ void __launch_bounds__(128) rsa_summaries_kernel(const __nv_bfloat16* __restrict__ k, int64_t sb,
+                                                            int64_t sg, int64_t sh, int64_t ss, int B, int G, int H,
+                                                            int Sk, int D, int blk, __nv_bfloat16* __restrict__ kmin,
+                                                            __nv_bfloat16* __restrict__ kmax) {
+  __shared__ uint4 red_min[128], red_max[128];
+  const int j = blockIdx.x;
+  const int bgh = blockIdx.y;
+  const int h = bgh % H, g = (bgh / H) % G, b = bgh / (H * G);
+  const int nkb = gridDim.x;
+  const int nch = D / 8;                       // 16-byte chunks per row
+  const int rows_par = 128 / nch;              // rows handled in parallel
+  const int t = threadIdx.x;
+  const int ch = t % nch, r0 = t / nch;
+  const __nv_bfloat16* base = k + b * sb + g * sg + (int64_t)h * sh;
+  __nv_bfloat162 mn[4], mx[4];
+  const __nv_bfloat162 pinf = __floats2bfloat162_rn(INFINITY, INFINITY), ninf = __floats2bfloat162_rn(-INFINITY, -INFINITY);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    mn[i] = pinf;
+    mx[i] = ninf;
+  }
+  const int k_end = min(Sk, (j + 1) * blk);
+  if (r0 < rows_par) {
+    for (int kk = j * blk + r0; kk < k_end; kk += rows_par) {
+      const uint4 u = __ldg(reinterpret_cast<const uint4*>(base + (int64_t)kk * ss) + ch);
+      const __nv_bfloat162* v = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        mn[i] = __hmin2(mn[i], v[i]);
+        mx[i] = __hmax2(mx[i], v[i]);
+      }
+    }
+  }
+  red_min[t] = *reinterpret_cast<uint4*>(mn);
+  red_max[t] = *reinterpret_cast<uint4*>(mx);
+  __syncthreads();
+  if (t < nch) {
+    for (int r = 1; r < rows_par; ++r) {
+      const uint4 a = red_min[r * nch + t], z = red_max[r * nch + t];
+      const __nv_bfloat162* va = reinterpret_cast<const __nv_bfloat162*>(&a);
+      const __nv_bfloat162* vz = reinterpret_cast<const __nv_bfloat162*>(&z);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        mn[i] = __hmin2(mn[i], va[i]);
+        mx[i] = __hmax2(mx[i], vz[i]);
+      }
+    }
+    const int64_t o = ((int64_t)bgh * nkb + j) * D;
+    reinterpret_cast<uint4*>(kmin + o)[t] = *reinterpret_cast<uint4*>(mn);
+    reinterpret_cast<uint4*>(kmax + o)[t] = *reinterpret_cast<uint4*>(mx);
+  }
+}
+
+cudaError_t launch_rsa_summaries(const void* k, int64_t sb, int64_t sg, int64_t sh, int64_t ss, int B, int G, int H,
+                                 int Sk, int D, int blk, void* kmin, void* kmax, cudaStream_t stream) {
+  const int nkb = (Sk + blk - 1) / blk;
+  dim3 grid(nkb, B * G * H);
+  rsa_summaries_kernel<<<grid, 128, 0, stream>>>(static_cast<const __nv_bfloat16*>(k), sb, sg, sh, ss, B, G, H, Sk,
+                                                 D, blk, static_cast<__nv_bfloat16*>(kmin),
+                                                 static_cast<__nv_bfloat16*>(kmax));
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ selection
+template <int D>
+struct SelCfg {
+  static constexpr int CH = 64;                         // bf16 per 128-byte swizzle row
+  static constexpr int NCH = D / CH;
+  static constexpr int CHUNK = 128 * 128;               // one 128-row x 128-byte swizzle slab
+  static constexpr int QTILE = NCH * CHUNK;             // one 128 x D tile
+  static constexpr uint32_t IDESC = idesc_bf16_f32(128, 128, 0);
+  // summaries (kmax, kmin) + q+ (TMA lands Q here, split in place) / q- tiles + scores + flags + barriers
+  // + alignment slack
+  static int smem(int n_mt) { return 2 * n_mt * QTILE + 2 * QTILE + n_mt * 128 * 4 + 64 + 64 + 1024; }
+};
+
+template <int D>
+__global__ void __launch_bounds__(128, 1)
+    rsa_select_kernel(const __grid_constant__ RsaSelParams p, const __grid_constant__ CUtensorMap tq,
+                      const __grid_constant__ CUtensorMap tmin, const __grid_constant__ CUtensorMap tmax) {
+  using C = SelCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int n_mt = (p.nkb + 127) / 128;
+  uint8_t* sMax = smem;                                 // [n_mt][NCH] slabs
+  uint8_t* sMin = sMax + n_mt * C::QTILE;
+  uint8_t* sQp = sMin + n_mt * C::QTILE;
+  uint8_t* sQn = sQp + C::QTILE;
+  float* sc = reinterpret_cast<float*>(sQn + C::QTILE);  // [n_mt*128] scores
+  uint32_t* flags = reinterpret_cast<uint32_t*>(sc + n_mt * 128);  // [16] selection bitmap
+  uint64_t* bars = reinterpret_cast<uint64_t*>(flags + 16);
+  uint64_t* bar_sum = bars;
+  uint64_t* bar_q = bars + 1;
+  uint64_t* bar_mma = bars + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3);
+
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int bgk = blockIdx.x / p.parts;                  // (b, g, h_kv)
+  const int part = blockIdx.x % p.parts;
+  const int hk = bgk % p.Hkv, g = (bgk / p.Hkv) % p.G, b = bgk / (p.Hkv * p.G);
+  const int gq = p.q_bcast_g ? 0 : g, bq = p.q_bcast_b ? 0 : b;
+  const int n_blocks_mine = part < p.nqb ? (p.nqb - 1 - part) / p.parts + 1 : 0;
+  const int n_items = n_blocks_mine * p.grp;             // (q-block, head in group) pairs
+
+  if (t == 0) {
+    mbar_init(bar_sum, 1);
+    mbar_init(bar_q, 1);
+    mbar_init(bar_mma, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // item n -> (q-block i, head h); q-blocks interleaved over parts, heaviest (latest) first
+  auto item_qblk = [&](int n) { return p.nqb - 1 - (part + (n / p.grp) * p.parts); };
+  auto item_head = [&](int n) { return hk * p.grp + n % p.grp; };
+  auto load_q = [&](int n) {
+    mbar_arrive_expect_tx(bar_q, C::QTILE);
+    for (int c = 0; c < C::NCH; ++c)
+      tma_load_5d(sQp + c * C::CHUNK, &tq, bar_q, c * C::CH, item_qblk(n) * 128, item_head(n), gq, bq);
+  };
+  if (t == 0 && n_items > 0) {
+    tma_prefetch_desc(&tq);
+    mbar_arrive_expect_tx(bar_sum, 2 * n_mt * C::QTILE);
+    for (int m = 0; m < n_mt; ++m)
+      for (int c = 0; c < C::NCH; ++c) {
+        tma_load_5d(sMax + (m * C::NCH + c) * C::CHUNK, &tmax, bar_sum, c * C::CH, m * 128, bgk, 0, 0);
+        tma_load_5d(sMin + (m * C::NCH + c) * C::CHUNK, &tmin, bar_sum, c * C::CH, m * 128, bgk, 0, 0);
+      }
+    load_q(0);
+  }
+  if (n_items > 0) mbar_wait(bar_sum, 0);
+
+  float run0 = -INFINITY, run1 = -INFINITY, run2 = -INFINITY, run3 = -INFINITY;  // block j = m*128 + t
+  for (int n = 0; n < n_items; ++n) {
+    const int i = item_qblk(n);
+    const int h_in_grp = n % p.grp;
+    const int q_last = min(p.Sq, (i + 1) * 128) - 1;
+    const int q_last_abs = q_last + p.q_off;
+    int c = q_last_abs < 0 ? 0 : q_last_abs / 128;     // diagonal block (reading G10)
+    c = min(c, p.nkb - 1);
+    const int n_mt_i = c >= 2 ? (c - 1 + 127) / 128 : 0; // M-tiles holding candidates 1 <= j < c
+    // ---- q+ / q- split of the landed Q tile (element-wise: the swizzle is preserved)
+    mbar_wait(bar_q, n & 1);
+    {
+      const uint4* src = reinterpret_cast<const uint4*>(sQp);
+      uint4* dp = reinterpret_cast<uint4*>(sQp);
+      uint4* dn = reinterpret_cast<uint4*>(sQn);
+      const __nv_bfloat162 z = __floats2bfloat162_rn(0.f, 0.f);
+      for (int e = t; e < C::QTILE / 16; e += 128) {
+        uint4 u = src[e], up, un;
+        const __nv_bfloat162* v = reinterpret_cast<const __nv_bfloat162*>(&u);
+        __nv_bfloat162* vp = reinterpret_cast<__nv_bfloat162*>(&up);
+        __nv_bfloat162* vn = reinterpret_cast<__nv_bfloat162*>(&un);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          vp[w] = __hmax2(v[w], z);
+          vn[w] = __hmin2(v[w], z);
+        }
+        dp[e] = up;
+        dn[e] = un;
+      }
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (t == 0) {
+      const uint32_t ap = smem_u32(sMax), an = smem_u32(sMin), bp = smem_u32(sQp), bn = smem_u32(sQn);
+      for (int m = 0; m < n_mt_i; ++m) {
+#pragma unroll
+        for (int kk = 0; kk < 2 * D / 16; ++kk) {
+          const int kd = kk % (D / 16);                  // K step within the half
+          const uint32_t off = (kd * 16 / C::CH) * C::CHUNK + (kd * 16 % C::CH) * 2;
+          const uint32_t a = (kk < D / 16 ? ap : an) + m * C::QTILE + off;
+          const uint32_t bb = (kk < D / 16 ? bp : bn) + off;
+          umma_ss(tmem + m * 128, smem_desc(a, 16, 1024, kLayoutSW128), smem_desc(bb, 16, 1024, kLayoutSW128),
+                  C::IDESC, kk > 0);
+        }
+      }
+      umma_commit(bar_mma);
+    }
+    mbar_wait(bar_mma, n & 1);
+    tc_fence_after();
+    if (t == 0 && n + 1 < n_items) load_q(n + 1);        // the MMAs have read q+ / q-: land the next Q tile
+    // ---- row max over the block's valid queries: thread t owns blocks m*128 + t
+    const int nvalid = min(128, p.Sq - i * 128);
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    float mine[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      if (m >= n_mt_i) break;
+      float mx = -INFINITY;
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + lane_base + m * 128 + c0, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if (c0 + e < nvalid) mx = fmaxf(mx, __uint_as_float(r[e]));
+      }
+      mine[m] = mx;
+    }
+    if (h_in_grp == 0) {
+      run0 = mine[0]; run1 = mine[1]; run2 = mine[2]; run3 = mine[3];
+    } else {
+      run0 = fmaxf(run0, mine[0]); run1 = fmaxf(run1, mine[1]);
+      run2 = fmaxf(run2, mine[2]); run3 = fmaxf(run3, mine[3]);
+    }
+    if (h_in_grp == p.grp - 1) {
+      // ---- top-k by rank over candidates 1 <= j < c (ties toward the lower j, G11)
+      const float runs[4] = {run0, run1, run2, run3};
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        if (m < n_mt) sc[m * 128 + t] = runs[m];
+      if (t < 16) flags[t] = 0u;
+      __syncthreads();
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int j = m * 128 + t;
+        bool sel = false;
+        if (j < p.nkb && j <= c) {
+          if (j == 0 || j == c) {
+            sel = true;
+          } else {
+            const float s = sc[j];
+            int rank = 0;
+            for (int jj = 1; jj < c; ++jj) {
+              const float o = sc[jj];
+              rank += (o > s) || (o == s && jj < j);
+            }
+            sel = rank < p.topk;
+          }
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, sel);
+        if (lane == 0) flags[m * 4 + warp] = bal;
+      }
+      __syncthreads();
+      int cnt = 0;
+      for (int w = 0; w < 16; ++w) cnt += __popc(flags[w]);
+      for (int hh = 0; hh < p.grp; ++hh) {
+        const int64_t row = (((int64_t)b * p.G + g) * p.Hq + hk * p.grp + hh) * p.nqb + i;
+        int32_t* out = p.blk_idx + row * p.max_sel;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const int j = m * 128 + t;
+          const int w = j >> 5;
+          if (m < n_mt && ((flags[w] >> (j & 31)) & 1u)) {
+            int pos = __popc(flags[w] & ((1u << (j & 31)) - 1u));
+            for (int ww = 0; ww < w; ++ww) pos += __popc(flags[ww]);
+            if (pos < p.max_sel) out[pos] = j;
+          }
+        }
+        for (int e = cnt + t; e < p.max_sel; e += 128) out[e] = -1;
+        if (t == 0) p.blk_cnt[row] = min(cnt, p.max_sel);
+      }
+    }
+    tc_fence_before();
+    __syncthreads();                                      // sc/flags reuse; TMEM reads done before next MMA
+    tc_fence_after();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+int rsa_select_max_blocks(int D) { return D == 128 ? 256 : 512; }
+
+cudaError_t launch_rsa_select(const RsaSelParams& p0, const CUtensorMap& tq, const CUtensorMap& tmin,
+                              const CUtensorMap& tmax, cudaStream_t stream) {
+  RsaSelParams p = p0;
+  const int units = p.B * p.G * p.Hkv;
+  int parts = (148 * 2 + units - 1) / units;
+  parts = parts < 1 ? 1 : (parts > p.nqb ? p.nqb : parts);
+  p.parts = parts;
+  const int n_mt = (p.nkb + 127) / 128;
+  if (p.D == 128) {
+    const int sm = SelCfg<128>::smem(n_mt);
+    cudaError_t e = cudaFuncSetAttribute(rsa_select_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e != cudaSuccess) return e;
+    rsa_select_kernel<128><<<units * parts, 128, sm, stream>>>(p, tq, tmin, tmax);
+  } else {
+    const int sm = SelCfg<64>::smem(n_mt);
+    cudaError_t e = cudaFuncSetAttribute(rsa_select_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e != cudaSuccess) return e;
+    rsa_select_kernel<64><<<units * parts, 128, sm, stream>>>(p, tq, tmin, tmax);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace fl

@@ -151,6 +151,51 @@ class HostRunner:
         return out
 
 
+def _stream_handle(device, stream=None):
+    stream = stream or torch.cuda.current_stream(device)
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+
+
+def rsa_build_summaries(k: torch.Tensor, blk_k: int = 128, kmin=None, kmax=None, stream=None):
+    """RSA per-KV-block key summaries (fl_rsa_build_summaries): returns (kmin, kmax),
+    bf16 [B*G*Hkv, ceil(S_k/blk_k), D], the exact element-wise min / max of each block."""
+    rank = k.dim()
+    bgh = 1
+    for s_ in k.shape[:rank - 2]:
+        bgh *= s_
+    Sk, D = k.shape[-2], k.shape[-1]
+    nkb = (Sk + blk_k - 1) // blk_k
+    if kmin is None:
+        kmin = torch.empty(bgh, nkb, D, device=k.device, dtype=torch.bfloat16)
+    if kmax is None:
+        kmax = torch.empty(bgh, nkb, D, device=k.device, dtype=torch.bfloat16)
+    tk, tmn, tmx = tensor(k), tensor(kmin), tensor(kmax)
+    _lib.check(_lib.lib().fl_rsa_build_summaries(C.byref(tk), C.byref(tmn), C.byref(tmx), int(blk_k),
+                                                 _stream_handle(k.device, stream)))
+    return kmin, kmax
+
+
+def rsa_select(q: torch.Tensor, kmin: torch.Tensor, kmax: torch.Tensor, s_k: int, *, topk: int = 16,
+               blk_q: int = 128, blk_k: int = 128, causal_align: int = 0, max_sel=None, blk_idx=None,
+               blk_cnt=None, stream=None):
+    """RSA data-dependent block selection (fl_rsa_select): returns (blk_idx i32
+    [B*G*Hq, n_qblk, max_sel], blk_cnt i32 [B*G*Hq, n_qblk]) ready for mask="blocklist"."""
+    bgh = 1
+    for s_ in q.shape[:-2]:
+        bgh *= s_
+    nqb = (q.shape[-2] + blk_q - 1) // blk_q
+    max_sel = topk + 2 if max_sel is None else max_sel
+    if blk_idx is None:
+        blk_idx = torch.empty(bgh, nqb, max_sel, device=q.device, dtype=torch.int32)
+    if blk_cnt is None:
+        blk_cnt = torch.empty(bgh, nqb, device=q.device, dtype=torch.int32)
+    tq, tmn, tmx, ti, tc = tensor(q), tensor(kmin), tensor(kmax), tensor(blk_idx), tensor(blk_cnt)
+    _lib.check(_lib.lib().fl_rsa_select(C.byref(tq), C.byref(tmn), C.byref(tmx), int(s_k), int(topk), int(blk_q),
+                                        int(blk_k), int(causal_align), C.byref(ti), C.byref(tc),
+                                        _stream_handle(q.device, stream)))
+    return blk_idx, blk_cnt
+
+
 def diag_umma_gemm(a: torch.Tensor, b: torch.Tensor, n: int, k: int, b_mn_major=False, a_from_tmem=False):
     c = torch.empty(128, n, device=a.device, dtype=torch.float32)
     s = torch.cuda.current_stream(a.device).cuda_stream
