@@ -184,23 +184,30 @@ __device__ __forceinline__ void load_sched(Work& w, const uint32_t* sched) {
   w.hi_cta = meta[0];
 }
 
+template <bool LIST>
 __device__ __forceinline__ bool needs(const Work& w, int i, int j) {
-  if (w.sched) return (w.sched[j] >> (30 + i)) & 1u;
+  if constexpr (LIST) return (w.sched[j] >> (30 + i)) & 1u;
   return j >= w.lo[i] && j < w.hi[i];
 }
-__device__ __forceinline__ int kv_tile(const Work& w, int j) { return w.sched ? (int)(w.sched[j] & 0x3FFFFFFFu) : j; }
+template <bool LIST>
+__device__ __forceinline__ int kv_tile(const Work& w, int j) {
+  if constexpr (LIST) return (int)(w.sched[j] & 0x3FFFFFFFu);
+  return j;
+}
+template <bool LIST>
 __device__ __forceinline__ int next_tile(const Work& w, int j) {
   for (++j; j < w.hi_cta; ++j)
-    if (needs(w, 0, j) || needs(w, 1, j)) return j;
+    if (needs<LIST>(w, 0, j) || needs<LIST>(w, 1, j)) return j;
   return -1;
 }
 
-template <int D, bool DIFF, int MOD, bool BIAS>
+template <int D, bool DIFF, int MOD, bool BIAS, bool LIST>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     attn_tc_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ TmaMaps maps) {
   using C = TcCfg<D, DIFF>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned (SW128 atoms); offset arithmetic on smem_raw keeps the shared address space visible
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sQ = smem + C::SMEM_Q;
   uint8_t* sRing = smem + C::SMEM_RING;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::SMEM_BAR);
@@ -216,9 +223,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   const int lane = threadIdx.x & 31;
   Work w = decode_work<D, DIFF>(p);
   uint32_t* sched = reinterpret_cast<uint32_t*>(smem + C::SMEM_SCHED);
-  const bool blocklist = p.mask == MASK_BLOCKLIST;
+  constexpr bool blocklist = LIST;                  // p.mask == MASK_BLOCKLIST
 
-  if (blocklist && warp == 9 && lane == 0) build_sched(p, w, sched);
+  if constexpr (blocklist) if (warp == 9 && lane == 0) build_sched(p, w, sched);
   if (warp == 8 && lane == 0) {
     mbar_init(q_full, 1);
     for (int s = 0; s < C::NSLOT; ++s) {
@@ -237,7 +244,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (blocklist) load_sched(w, sched);
+  if constexpr (blocklist) load_sched(w, sched);
 
   const int hkv = w.h / p.grp;
   const int gq = maps.q_bcast_g ? 0 : w.g, bq = maps.q_bcast_b ? 0 : w.b;
@@ -259,7 +266,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           tma_load_5d(sQ + i * C::TILE_BYTES + c * C::CHUNK_BYTES, &maps.q, q_full, c * C::CH, w.q0[i], qh, gq, bq);
       }
       int e = 0;
-      for (int j = next_tile(w, w.lo_cta - 1); j >= 0; j = next_tile(w, j)) {
+      for (int j = next_tile<LIST>(w, w.lo_cta - 1); j >= 0; j = next_tile<LIST>(w, j)) {
         for (int t = 0; t < C::ENTRIES_PER_TILE; ++t, ++e) {
           const int slot = e % C::NSLOT;
           if (e >= C::NSLOT) mbar_wait(&empty[slot], ((e / C::NSLOT) - 1) & 1);
@@ -270,7 +277,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           const int head = is_v ? hkv : hkv + t * p.Hkv;
           const int gg = is_v ? gv : gk, bb = is_v ? bv : bk;
           for (int c = 0; c < C::NCH; ++c)
-            tma_load_5d(dst + c * C::CHUNK_BYTES, m, &full[slot], c * C::CH, kv_tile(w, j) * C::BN, head, gg, bb);
+            tma_load_5d(dst + c * C::CHUNK_BYTES, m, &full[slot], c * C::CH, kv_tile<LIST>(w, j) * C::BN, head, gg, bb);
         }
       }
     }
@@ -309,36 +316,36 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         }
         ++pv_cnt[i];
       };
-      int j = next_tile(w, w.lo_cta - 1);
+      int j = next_tile<LIST>(w, w.lo_cta - 1);
       mbar_wait(q_full, 0);                          // always: no CTA exits with Q's TMA in flight
       tc_fence_after();
       if (j >= 0) {
         int ks0 = acquire();
         int ks1 = DIFF ? acquire() : ks0;
-        if (needs(w, 0, j)) issue_s(0, ks0);
-        if (needs(w, 1, j)) issue_s(1, ks1);
+        if (needs<LIST>(w, 0, j)) issue_s(0, ks0);
+        if (needs<LIST>(w, 1, j)) issue_s(1, ks1);
         umma_commit(&empty[ks0]);
         if (DIFF) umma_commit(&empty[ks1]);
         while (j >= 0) {
           const int vs = acquire();
-          const int jn = next_tile(w, j);
+          const int jn = next_tile<LIST>(w, j);
           int kn0 = -1, kn1 = -1;
           if (jn >= 0) {
             kn0 = acquire();
             kn1 = DIFF ? acquire() : kn0;
           }
-          if (needs(w, 0, j)) {
+          if (needs<LIST>(w, 0, j)) {
             issue_pv(0, vs);
             if (j == w.hi[0] - 1) umma_commit(&o_full[0]);
           }
-          if (jn >= 0 && needs(w, 0, jn)) issue_s(0, kn0);
-          if (needs(w, 1, j)) {
+          if (jn >= 0 && needs<LIST>(w, 0, jn)) issue_s(0, kn0);
+          if (needs<LIST>(w, 1, j)) {
             issue_pv(1, vs);
             if (j == w.hi[1] - 1) umma_commit(&o_full[1]);
           }
           umma_commit(&empty[vs]);
           if (jn >= 0) {
-            if (needs(w, 1, jn)) issue_s(1, kn1);
+            if (needs<LIST>(w, 1, jn)) issue_s(1, kn1);
             umma_commit(&empty[kn0]);
             if (DIFF) umma_commit(&empty[kn1]);
           }
@@ -359,11 +366,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     const Interval iv = row_interval(p, w.b, q);
     // first / one-past-last schedule steps both warpgroups need (ping-pong range)
     int c_lo = max(w.lo[0], w.lo[1]), c_hi = min(w.hi[0], w.hi[1]);
-    if (w.sched) {
+    if constexpr (LIST) {
       c_lo = 1 << 30;
       c_hi = 0;
       for (int t = w.lo_cta; t < w.hi_cta; ++t)
-        if (needs(w, 0, t) && needs(w, 1, t)) {
+        if (needs<LIST>(w, 0, t) && needs<LIST>(w, 1, t)) {
           c_lo = min(c_lo, t);
           c_hi = t + 1;
         }
@@ -385,9 +392,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 
     float m_ref = -INFINITY, l = 0.f;
     int n_done = 0;
-    for (int j = next_tile(w, w.lo_cta - 1); j >= 0; j = next_tile(w, j)) {
-      if (!needs(w, wg, j)) continue;
-      const int k0 = kv_tile(w, j) * 128;
+    for (int j = next_tile<LIST>(w, w.lo_cta - 1); j >= 0; j = next_tile<LIST>(w, j)) {
+      if (!needs<LIST>(w, wg, j)) continue;
+      const int k0 = kv_tile<LIST>(w, j) * 128;
       mbar_wait(&s_full[wg], n_done & 1);
       tc_fence_after();
       uint32_t s[128];
@@ -499,7 +506,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       // Ping-pong: the two warpgroups take turns on the MUFU (exp) pipe for the
       // tiles both need, so each exp loop runs at full rate while the tensor
       // pipe works for the other warpgroup (CTA-local named barriers 2 and 3).
-      const bool common = needs(w, 0, j) && needs(w, 1, j);
+      const bool common = needs<LIST>(w, 0, j) && needs<LIST>(w, 1, j);
       if (common) {
         if (wg == 0 && j > c_lo) named_bar_sync(2, 256);
         if (wg == 1) named_bar_sync(3, 256);
@@ -630,7 +637,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 template <int D, bool DIFF, int MOD>
 static cudaError_t launch_one(const AttnParams& p, const TmaMaps& maps, cudaStream_t stream) {
   using C = TcCfg<D, DIFF>;
-  auto kern = p.bias ? attn_tc_kernel<D, DIFF, MOD, true> : attn_tc_kernel<D, DIFF, MOD, false>;
+  // RSA block lists (FL_MASK_BLOCKLIST) get their own instantiation (no bias, no diff: host.cu) so the
+  // interval-mask kernels keep the schedule arithmetic out of their softmax loop.
+  auto kern = p.mask == MASK_BLOCKLIST ? attn_tc_kernel<D, false, MOD, false, true>
+              : p.bias                 ? attn_tc_kernel<D, DIFF, MOD, true, false>
+                                       : attn_tc_kernel<D, DIFF, MOD, false, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_TOTAL);
   if (e != cudaSuccess) return e;
   const int rows_per_unit = DIFF ? 128 : 256;

@@ -22,7 +22,8 @@ __global__ void __launch_bounds__(128, 1)
   constexpr uint32_t LN = SWN == 128 ? kLayoutSW128 : kLayoutSW64;
   constexpr int A_BYTES = 128 * K * 2, B_BYTES = N * K * 2;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned (SW128 atoms); offset arithmetic on smem_raw keeps the shared address space visible
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + A_BYTES;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + A_BYTES + B_BYTES);

@@ -275,6 +275,8 @@ fl_status prepare(const fl_attn_args* a, Prepared& P, bool device_ptrs) {
       return fail(FL_ERR_UNSUPPORTED, "bf16 blocklist path needs blk_q == blk_k == 128");
     if (P.bf16 && var.blk_idx.data && var.blk_idx.rank == 3 && var.blk_idx.size[2] > 256)
       return fail(FL_ERR_UNSUPPORTED, "bf16 blocklist path: max_sel <= 256");
+    if (P.bf16 && (var.diff || var.bias.data))
+      return fail(FL_ERR_UNSUPPORTED, "bf16 blocklist path: no diff, no additive bias (RSA lists only)");
     const int64_t nqb = (Sq + var.blk_q - 1) / var.blk_q;
     const fl_tensor &bi = var.blk_idx, &bc = var.blk_cnt;
     if (!bi.data || !bc.data || bi.dtype != FL_I32 || bc.dtype != FL_I32 || bi.rank != 3 || bc.rank != 2 ||

@@ -110,7 +110,8 @@ __global__ void __launch_bounds__(128, 1)
                       const __grid_constant__ CUtensorMap tmin, const __grid_constant__ CUtensorMap tmax) {
   using C = SelCfg<D>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned (SW128 atoms); offset arithmetic on smem_raw keeps the shared address space visible
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int n_mt = (p.nkb + 127) / 128;
   uint8_t* sMax = smem;                                 // [n_mt][NCH] slabs
   uint8_t* sMin = sMax + n_mt * C::QTILE;

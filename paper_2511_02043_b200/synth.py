@@ -115,21 +115,28 @@ def alibi_slopes(H: int) -> np.ndarray:
     return np.array([2.0 ** (-8.0 * (h + 1) / H) for h in range(H)], dtype=np.float32)
 
 
-def clustered_qk(q_shape, k_shape, *, seed=2, blk=128, n_clusters=32, dtype=torch.bfloat16):
+def clustered_qk(q_shape, k_shape, *, seed=2, blk=128, n_clusters=32, dtype=torch.bfloat16, b_range=None):
     """RSA inputs: per slab 32 centroids in {+-0.6}^D; each KV block / q block
-    draws a cluster and its rows are clip(c_z + 0.4 U[-1,1), +-1)."""
+    draws a cluster and its rows are clip(c_z + 0.4 U[-1,1), +-1).
+
+    Shapes are the GLOBAL [B,H,S,D]; b_range=(b0, b1) returns only batches
+    [b0, b1) (identical to that slice of the full tensors: streams are keyed by
+    the global batch index)."""
+    b0, b1 = (0, q_shape[0]) if b_range is None else b_range
+
     def one(shape, tensor, heads_per_centroid_slab):
-        B, H, S, D = shape
-        out = np.empty(shape, dtype=np.float32)
-        for b in range(B):
+        _, H, S, D = shape
+        out = np.empty((b1 - b0, H, S, D), dtype=np.float32)
+        nb = (S + blk - 1) // blk
+        for b in range(b0, b1):
             for h in range(H):
                 r = _rng(seed, tensor, b * H + h)
                 cr = _rng(seed + 1000, "k", b * (H // heads_per_centroid_slab) + h // heads_per_centroid_slab)
-                cents = np.where(cr.random((n_clusters, D)) < 0.5, -0.6, 0.6)
-                nb = (S + blk - 1) // blk
+                cents = np.where(cr.random((n_clusters, D)) < 0.5, -0.6, 0.6).astype(np.float32)
                 z = r.integers(0, n_clusters, size=nb)
-                x = cents[np.repeat(z, blk)[:S]] + 0.4 * (r.random((S, D)) * 2 - 1)
-                out[b, h] = np.clip(x, -1.0, 1.0)
+                x = cents[np.repeat(z, blk)[:S]]
+                x += 0.4 * (r.random((S, D), dtype=np.float32) * 2 - 1)
+                np.clip(x, -1.0, 1.0, out=out[b - b0, h])
         return _to(out, dtype)
     grp = q_shape[1] // k_shape[1]
     return one(q_shape, "q", grp), one(k_shape, "k", 1)
