@@ -246,6 +246,7 @@ def dense_job(names, rank, world, device, with_host=True):
     wl = names[0] if len(names) == 1 else "flexattention_variants(" + ",".join(names) + ")"
     job = Job(names[0] if len(names) == 1 else "flex",
               f"{wl}_bf16_B{cfg0['B']}_H{cfg0['H']}_S{cfg0['S']}_D{cfg0['D']}")
+    ws = torch.empty(1 << 20, dtype=torch.uint8, device=device)       # scheduler counter + packed key mask
     kws, pairs_by = {}, {}
     for n in names:
         cfg = VARIANTS[n]
@@ -258,7 +259,8 @@ def dense_job(names, rank, world, device, with_host=True):
         pairs = kept_pairs(cfg, offs)
         flops = pairs * flops_per_pair(cfg)
         nbytes = sum(t.numel() * t.element_size() for t in (q, k, v, out))
-        job.calls.append(Call(n, (lambda kw=kw: fl.attn_fwd(q, k, v, out=out, **kw)), flops, nbytes, "tensor",
+        job.calls.append(Call(n, (lambda kw=kw: fl.attn_fwd(q, k, v, out=out, workspace=ws, **kw)), flops, nbytes,
+                              "tensor",
                               kernel="attn_tc_kernel"))
         job.step_flops += flops
         kws[n] = (kw, offs)
@@ -400,8 +402,9 @@ def rsa_job(name, rank, world, device, with_host=True):
         att_bytes = q.numel() * 2 + out.numel() * 2 + listed * 128 * D * 2 * 2
     else:        # K/V read once per (b,h) (a block listed by several q-blocks is re-read from L2)
         att_bytes = (q.numel() + k.numel() + v.numel() + out.numel()) * 2
+    ws = torch.empty(1 << 20, dtype=torch.uint8, device=device)
     job.calls.append(Call("attn_blocklist", lambda: fl.attn_fwd(q, k, v, out=out, mask="blocklist", blk_idx=idx,
-                                                                blk_cnt=cnt), flops, att_bytes,
+                                                                blk_cnt=cnt, workspace=ws), flops, att_bytes,
                           "hbm" if decode else "tensor", kernel="attn_tc_kernel"))
     job.step_flops = flops
     job.extra.update(listed_blocks=listed, kv_blocks=nkb * B * H * nqb, rsa_decode=decode)
@@ -417,7 +420,7 @@ def rsa_job(name, rank, world, device, with_host=True):
                 v.copy_(hv, non_blocking=True)
                 fl.rsa_build_summaries(k, 128, kmin, kmax, stream=stream)
                 fl.rsa_select(q, kmin, kmax, S, topk=topk, blk_idx=idx, blk_cnt=cnt, stream=stream)
-                fl.attn_fwd(q, k, v, out=out, mask="blocklist", blk_idx=idx, blk_cnt=cnt, stream=stream)
+                fl.attn_fwd(q, k, v, out=out, mask="blocklist", blk_idx=idx, blk_cnt=cnt, workspace=ws, stream=stream)
                 hout.copy_(out, non_blocking=True)
         h2d = (hq.numel() + hk.numel() + hv.numel()) * 2
         job.e2e = (e2e_step, h2d, hout.numel() * 2)

@@ -127,8 +127,11 @@ typedef struct {
  * lse = -inf (G7); a fully masked row likewise gives O = 0, lse = -inf. */
 fl_status fl_attn_fwd(const fl_attn_args* args);
 
-/* Bytes of device workspace fl_attn_fwd needs for these args: the key mask packed to one bit per
- * key (ceil(S_k/128)*16 bytes per (b, g)) when key_mask is present, else 0. */
+/* Bytes of device workspace fl_attn_fwd needs for these args (caller-owned, >= 16-byte aligned, not
+ * shared by concurrent calls): bf16 path: 256 bytes for the persistent kernel's work-unit ticket
+ * counter (reset by the call itself with a stream-ordered memset), then -- when key_mask is present --
+ * the key mask packed to one bit per key (ceil(S_k/128)*16 bytes per (b, g), 256-byte rounded).
+ * f32 path: the packed key mask only.  0 when the call has no work. */
 fl_status fl_attn_workspace_size(const fl_attn_args* args, size_t* bytes);
 
 /* Host-buffer entry (the end-to-end path): same as fl_attn_fwd, but q/k/v (and

@@ -30,6 +30,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <algorithm>
+
 #include "masks.cuh"
 #include "params.h"
 #include "ptx.cuh"
@@ -66,9 +68,11 @@ struct TcCfg {
   static constexpr int SMEM_Q = 0;
   static constexpr int SMEM_RING = 2 * TILE_BYTES;
   static constexpr int SMEM_BAR = SMEM_RING + NSLOT * TILE_BYTES;
-  static constexpr int NBAR = 1 + 2 * NSLOT + 6;
-  static constexpr int SMEM_SCHED = SMEM_BAR + NBAR * 8 + 16;       // blocklist schedule (RSA)
-  static constexpr int SMEM_TOTAL = SMEM_SCHED + (2 * kMaxSelTc + 8) * 4 + 1024;  // + alignment slack
+  // q_full q_empty | full[NSLOT] empty[NSLOT] | s_full[2] p_full[2] o_full[2] | unit_full[2] unit_empty[2]
+  static constexpr int NBAR = 2 + 2 * NSLOT + 6 + 4;
+  static constexpr int SMEM_SCHED = SMEM_BAR + NBAR * 8 + 16;       // blocklist schedule (RSA), 2 slots
+  static constexpr int SCHED_WORDS = 2 * kMaxSelTc + 8;   // schedule + meta (n, lo0, hi0, lo1, hi1, ..., unit id)
+  static constexpr int SMEM_TOTAL = SMEM_SCHED + 2 * SCHED_WORDS * 4 + 1024;  // + alignment slack
   static constexpr uint32_t IDESC_S = idesc_bf16_f32(128, BN, 0);   // Q (K-major) x K (K-major)
   static constexpr uint32_t IDESC_O = idesc_bf16_f32(128, D, 1);    // P (TMEM) x V (MN-major)
   static constexpr int ENTRIES_PER_TILE = DIFF ? 3 : 2;              // K0 [K1] V
@@ -87,18 +91,17 @@ struct Work {
   const uint32_t* sched;  // blocklist schedule (nullptr for interval masks)
 };
 
+// Work unit u (persistent CTAs walk u = blockIdx.x, blockIdx.x + gridDim.x, ...).
+// (b,h)-major so the ~148 co-resident CTAs share a few heads' K/V in L2; inside a
+// head the heaviest (latest, for causal) query blocks go first, and the stride of
+// gridDim.x cycles every CTA through light and heavy blocks (static balance).
 template <int D, bool DIFF>
-__device__ __forceinline__ Work decode_work(const AttnParams& p) {
+__device__ __forceinline__ Work decode_work(const AttnParams& p, int u) {
   Work w;
   const int rows_per_unit = DIFF ? 128 : 256;
   const int nqb = (p.Sq + rows_per_unit - 1) / rows_per_unit;
-  const int nbgh = p.B * p.G * p.Hq;
-  const int u = blockIdx.x;
-  // (b,h)-major so the ~148 co-resident CTAs share a few heads' K/V in L2;
-  // inside a head the heaviest (latest, for causal) query blocks go first.
   const int bgh = u / nqb;
   const int qb = nqb - 1 - u % nqb;
-  (void)nbgh;
   w.h = bgh % p.Hq;
   w.g = (bgh / p.Hq) % p.G;
   w.b = bgh / (p.Hq * p.G);
@@ -187,7 +190,9 @@ __device__ __forceinline__ void load_sched(Work& w, const uint32_t* sched) {
 template <bool LIST>
 __device__ __forceinline__ bool needs(const Work& w, int i, int j) {
   if constexpr (LIST) return (w.sched[j] >> (30 + i)) & 1u;
-  return j >= w.lo[i] && j < w.hi[i];
+  // select, not w.lo[i]: a runtime index would force Work into local memory
+  const int lo = i ? w.lo[1] : w.lo[0], hi = i ? w.hi[1] : w.hi[0];
+  return j >= lo && j < hi;
 }
 template <bool LIST>
 __device__ __forceinline__ int kv_tile(const Work& w, int j) {
@@ -203,7 +208,7 @@ __device__ __forceinline__ int next_tile(const Work& w, int j) {
 
 template <int D, bool DIFF, int MOD, bool BIAS, bool LIST>
 __global__ void __launch_bounds__(kThreadsTc, 1)
-    attn_tc_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ TmaMaps maps) {
+    attn_tc_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ TmaMaps maps, int n_units) {
   using C = TcCfg<D, DIFF>;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned (SW128 atoms); offset arithmetic on smem_raw keeps the shared address space visible
@@ -212,22 +217,23 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   uint8_t* sRing = smem + C::SMEM_RING;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::SMEM_BAR);
   uint64_t* q_full = bars;
-  uint64_t* full = bars + 1;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* full = bars + 2;
   uint64_t* empty = full + C::NSLOT;
   uint64_t* s_full = empty + C::NSLOT;
   uint64_t* p_full = s_full + 2;
   uint64_t* o_full = p_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
+  uint64_t* unit_full = o_full + 2;                  // work-unit broadcast (producer -> MMA, softmax), 2 slots
+  uint64_t* unit_empty = unit_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(unit_empty + 2);
+  uint32_t* sched_base = reinterpret_cast<uint32_t*>(smem + C::SMEM_SCHED);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  Work w = decode_work<D, DIFF>(p);
-  uint32_t* sched = reinterpret_cast<uint32_t*>(smem + C::SMEM_SCHED);
-  constexpr bool blocklist = LIST;                  // p.mask == MASK_BLOCKLIST
 
-  if constexpr (blocklist) if (warp == 9 && lane == 0) build_sched(p, w, sched);
   if (warp == 8 && lane == 0) {
     mbar_init(q_full, 1);
+    mbar_init(q_empty, DIFF ? 1 + 128 : 1);          // last S MMA of a unit (+ diff: WG0 done with xbuf)
     for (int s = 0; s < C::NSLOT; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -236,6 +242,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 128);
       mbar_init(&o_full[i], 1);
+      mbar_init(&unit_full[i], 1);
+      mbar_init(&unit_empty[i], 1 + 256);            // MMA lane + both softmax warpgroups
     }
     fence_mbar_init();
   }
@@ -244,12 +252,22 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if constexpr (blocklist) load_sched(w, sched);
 
-  const int hkv = w.h / p.grp;
-  const int gq = maps.q_bcast_g ? 0 : w.g, bq = maps.q_bcast_b ? 0 : w.b;
-  const int gk = maps.k_bcast_g ? 0 : w.g, bk = maps.k_bcast_b ? 0 : w.b;
-  const int gv = maps.v_bcast_g ? 0 : w.g, bv = maps.v_bcast_b ? 0 : w.b;
+  // Dynamic persistent scheduling: the producer claims units (first blockIdx.x, then
+  // gridDim.x + atomicAdd(tile_ctr)) in the (b,h)-major, heaviest-first order of
+  // decode_work, so SMs that finish early take the next unit (greedy LPT within a head)
+  // and publishes the id (and, for block lists, the merged schedule) in slot it & 1.
+  auto get_unit = [&](int it) -> int {
+    mbar_wait(&unit_full[it & 1], (it >> 1) & 1);
+    return static_cast<int>(sched_base[(it & 1) * C::SCHED_WORDS + C::SCHED_WORDS - 1]);
+  };
+  // Work of the unit published in slot it & 1 (by value: keeps it in registers)
+  auto unit_work = [&](int u, int it) -> Work {
+    Work w = decode_work<D, DIFF>(p, u);
+    if constexpr (LIST) load_sched(w, sched_base + (it & 1) * C::SCHED_WORDS);
+    return w;
+  };
+  auto release_unit = [&](int it) { mbar_arrive(&unit_empty[it & 1]); };
 
   if (warp >= 8) {
    regs_dec<kRegsCtl>();
@@ -259,26 +277,51 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       tma_prefetch_desc(&maps.q);
       tma_prefetch_desc(&maps.k);
       tma_prefetch_desc(&maps.v);
-      mbar_arrive_expect_tx(q_full, 2 * C::TILE_BYTES);
-      for (int i = 0; i < 2; ++i) {
-        const int qh = DIFF ? w.h + i * p.Hq : w.h;
-        for (int c = 0; c < C::NCH; ++c)
-          tma_load_5d(sQ + i * C::TILE_BYTES + c * C::CHUNK_BYTES, &maps.q, q_full, c * C::CH, w.q0[i], qh, gq, bq);
-      }
-      int e = 0;
-      for (int j = next_tile<LIST>(w, w.lo_cta - 1); j >= 0; j = next_tile<LIST>(w, j)) {
-        for (int t = 0; t < C::ENTRIES_PER_TILE; ++t, ++e) {
-          const int slot = e % C::NSLOT;
-          if (e >= C::NSLOT) mbar_wait(&empty[slot], ((e / C::NSLOT) - 1) & 1);
-          mbar_arrive_expect_tx(&full[slot], C::TILE_BYTES);
-          uint8_t* dst = sRing + slot * C::TILE_BYTES;
-          const bool is_v = t == C::ENTRIES_PER_TILE - 1;
-          const CUtensorMap* m = is_v ? &maps.v : &maps.k;
-          const int head = is_v ? hkv : hkv + t * p.Hkv;
-          const int gg = is_v ? gv : gk, bb = is_v ? bv : bk;
-          for (int c = 0; c < C::NCH; ++c)
-            tma_load_5d(dst + c * C::CHUNK_BYTES, m, &full[slot], c * C::CH, kv_tile<LIST>(w, j) * C::BN, head, gg, bb);
+      int e = 0, it = 0;
+      int u = blockIdx.x;
+      for (;; ++it) {
+        uint32_t* sc = sched_base + (it & 1) * C::SCHED_WORDS;
+        if (it >= 2) mbar_wait(&unit_empty[it & 1], ((it >> 1) - 1) & 1);
+        sc[C::SCHED_WORDS - 1] = static_cast<uint32_t>(u);
+        if (u >= n_units) {
+          mbar_arrive(&unit_full[it & 1]);             // end marker
+          break;
         }
+        Work w = decode_work<D, DIFF>(p, u);
+        if constexpr (LIST) {
+          build_sched(p, w, sc);
+          load_sched(w, sc);
+        }
+        mbar_arrive(&unit_full[it & 1]);               // release: id / schedule visible to the waiters
+        const int u_next = (int)gridDim.x + atomicAdd(p.tile_ctr, 1);   // latency hidden behind this unit
+        const int hkv = w.h / p.grp;
+        const int gq = maps.q_bcast_g ? 0 : w.g, bq = maps.q_bcast_b ? 0 : w.b;
+        const int gk = maps.k_bcast_g ? 0 : w.g, bk = maps.k_bcast_b ? 0 : w.b;
+        const int gv = maps.v_bcast_g ? 0 : w.g, bv = maps.v_bcast_b ? 0 : w.b;
+        if (it > 0) mbar_wait(q_empty, (it - 1) & 1);  // the previous unit's S MMAs (and diff xbuf) are done
+        mbar_arrive_expect_tx(q_full, 2 * C::TILE_BYTES);
+        for (int i = 0; i < 2; ++i) {
+          const int qh = DIFF ? w.h + i * p.Hq : w.h;
+          for (int c = 0; c < C::NCH; ++c)
+            tma_load_5d(sQ + i * C::TILE_BYTES + c * C::CHUNK_BYTES, &maps.q, q_full, c * C::CH, w.q0[i], qh, gq,
+                        bq);
+        }
+        for (int j = next_tile<LIST>(w, w.lo_cta - 1); j >= 0; j = next_tile<LIST>(w, j)) {
+          for (int t = 0; t < C::ENTRIES_PER_TILE; ++t, ++e) {
+            const int slot = e % C::NSLOT;
+            if (e >= C::NSLOT) mbar_wait(&empty[slot], ((e / C::NSLOT) - 1) & 1);
+            mbar_arrive_expect_tx(&full[slot], C::TILE_BYTES);
+            uint8_t* dst = sRing + slot * C::TILE_BYTES;
+            const bool is_v = t == C::ENTRIES_PER_TILE - 1;
+            const CUtensorMap* m = is_v ? &maps.v : &maps.k;
+            const int head = is_v ? hkv : hkv + t * p.Hkv;
+            const int gg = is_v ? gv : gk, bb = is_v ? bv : bk;
+            for (int c = 0; c < C::NCH; ++c)
+              tma_load_5d(dst + c * C::CHUNK_BYTES, m, &full[slot], c * C::CH, kv_tile<LIST>(w, j) * C::BN, head,
+                          gg, bb);
+          }
+        }
+        u = u_next;
       }
     }
   } else if (warp == 9) {
@@ -302,7 +345,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         }
         umma_commit(&s_full[i]);
       };
-      int pv_cnt[2] = {0, 0};
+      int pv_cnt[2] = {0, 0};                          // cumulative: p_full parity
+      bool first_pv[2];                                // per unit: first PV overwrites O
       auto issue_pv = [&](int i, int vslot) {
         mbar_wait(&p_full[i], pv_cnt[i] & 1);
         tc_fence_after();
@@ -312,45 +356,58 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         for (int kk = 0; kk < C::BN / 16; ++kk) {
           umma_ts(tmem + (i ? C::COL_O1 : C::COL_O0), tmem + pcol + kk * 8,
                   smem_desc(va + kk * 16 * C::SWB, C::CHUNK_BYTES, C::SBO, C::LAYOUT), C::IDESC_O,
-                  (pv_cnt[i] > 0 || kk > 0) ? 1u : 0u);
+                  (!first_pv[i] || kk > 0) ? 1u : 0u);
         }
+        first_pv[i] = false;
         ++pv_cnt[i];
       };
-      int j = next_tile<LIST>(w, w.lo_cta - 1);
-      mbar_wait(q_full, 0);                          // always: no CTA exits with Q's TMA in flight
-      tc_fence_after();
-      if (j >= 0) {
-        int ks0 = acquire();
-        int ks1 = DIFF ? acquire() : ks0;
-        if (needs<LIST>(w, 0, j)) issue_s(0, ks0);
-        if (needs<LIST>(w, 1, j)) issue_s(1, ks1);
-        umma_commit(&empty[ks0]);
-        if (DIFF) umma_commit(&empty[ks1]);
-        while (j >= 0) {
-          const int vs = acquire();
-          const int jn = next_tile<LIST>(w, j);
-          int kn0 = -1, kn1 = -1;
-          if (jn >= 0) {
-            kn0 = acquire();
-            kn1 = DIFF ? acquire() : kn0;
+      int it = 0;
+      for (;; ++it) {
+        const int u = get_unit(it);
+        if (u >= n_units) break;
+        const Work w = unit_work(u, it);
+        first_pv[0] = first_pv[1] = true;
+        int j = next_tile<LIST>(w, w.lo_cta - 1);
+        mbar_wait(q_full, it & 1);                     // always: Q of this unit has landed
+        tc_fence_after();
+        if (j >= 0) {
+          int ks0 = acquire();
+          int ks1 = DIFF ? acquire() : ks0;
+          if (needs<LIST>(w, 0, j)) issue_s(0, ks0);
+          if (needs<LIST>(w, 1, j)) issue_s(1, ks1);
+          umma_commit(&empty[ks0]);
+          if (DIFF) umma_commit(&empty[ks1]);
+          if (next_tile<LIST>(w, j) < 0) umma_commit(q_empty);   // Q is free once the last S MMA is done
+          while (j >= 0) {
+            const int vs = acquire();
+            const int jn = next_tile<LIST>(w, j);
+            int kn0 = -1, kn1 = -1;
+            if (jn >= 0) {
+              kn0 = acquire();
+              kn1 = DIFF ? acquire() : kn0;
+            }
+            if (needs<LIST>(w, 0, j)) {
+              issue_pv(0, vs);
+              if (j == w.hi[0] - 1) umma_commit(&o_full[0]);
+            }
+            if (jn >= 0 && needs<LIST>(w, 0, jn)) issue_s(0, kn0);
+            if (needs<LIST>(w, 1, j)) {
+              issue_pv(1, vs);
+              if (j == w.hi[1] - 1) umma_commit(&o_full[1]);
+            }
+            umma_commit(&empty[vs]);
+            if (jn >= 0) {
+              if (needs<LIST>(w, 1, jn)) issue_s(1, kn1);
+              umma_commit(&empty[kn0]);
+              if (DIFF) umma_commit(&empty[kn1]);
+              if (next_tile<LIST>(w, jn) < 0) umma_commit(q_empty);
+            }
+            j = jn;
           }
-          if (needs<LIST>(w, 0, j)) {
-            issue_pv(0, vs);
-            if (j == w.hi[0] - 1) umma_commit(&o_full[0]);
-          }
-          if (jn >= 0 && needs<LIST>(w, 0, jn)) issue_s(0, kn0);
-          if (needs<LIST>(w, 1, j)) {
-            issue_pv(1, vs);
-            if (j == w.hi[1] - 1) umma_commit(&o_full[1]);
-          }
-          umma_commit(&empty[vs]);
-          if (jn >= 0) {
-            if (needs<LIST>(w, 1, jn)) issue_s(1, kn1);
-            umma_commit(&empty[kn0]);
-            if (DIFF) umma_commit(&empty[kn1]);
-          }
-          j = jn;
+        } else {
+          umma_commit(q_empty);
         }
+        release_unit(it);
       }
     }
    }
@@ -360,29 +417,25 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     const int wg = warp >> 2;
     const int r = threadIdx.x & 127;                 // row within the tile == TMEM lane
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    const int q = w.q0[wg] + r;
-    const bool row_valid = q < p.Sq;
-    const int q_abs = q + p.q_off;
-    const Interval iv = row_interval(p, w.b, q);
-    // first / one-past-last schedule steps both warpgroups need (ping-pong range)
-    int c_lo = max(w.lo[0], w.lo[1]), c_hi = min(w.hi[0], w.hi[1]);
-    if constexpr (LIST) {
-      c_lo = 1 << 30;
-      c_hi = 0;
-      for (int t = w.lo_cta; t < w.hi_cta; ++t)
-        if (needs<LIST>(w, 0, t) && needs<LIST>(w, 1, t)) {
-          c_lo = min(c_lo, t);
-          c_hi = t + 1;
-        }
-    }
     const uint32_t col_s = wg ? C::COL_S1 : C::COL_S0;
     const uint32_t col_o = wg ? C::COL_O1 : C::COL_O0;
-    float slope_l2 = 0.f;
-    if (MOD == MOD_ALIBI)
-      slope_l2 = kLog2e * (p.alibi ? p.alibi[w.h] : exp2f(-8.f * (float)(w.h + 1) / (float)p.Hq));
     const float sc_l2 = p.scale * kLog2e;
     const float cap_in = MOD == MOD_SOFTCAP ? p.scale / p.softcap : 0.f;   // s*scale/cap
     const float cap_out = MOD == MOD_SOFTCAP ? p.softcap * kLog2e : 0.f;
+    int s_cnt = 0, o_cnt = 0;                        // cumulative s_full / o_full phases of this WG
+    bool pp_started = false;                         // ping-pong: first common tile of the CTA's life seen
+    int it = 0;
+    for (;; ++it) {
+    const int u = get_unit(it);
+    if (u >= n_units) break;
+    const Work w = unit_work(u, it);
+    const int q = (wg ? w.q0[1] : w.q0[0]) + r;
+    const bool row_valid = q < p.Sq;
+    const int q_abs = q + p.q_off;
+    const Interval iv = row_interval(p, w.b, q);
+    float slope_l2 = 0.f;
+    if (MOD == MOD_ALIBI)
+      slope_l2 = kLog2e * (p.alibi ? p.alibi[w.h] : exp2f(-8.f * (float)(w.h + 1) / (float)p.Hq));
     const uint32_t* kbits = p.keybits ? p.keybits + ((int64_t)w.b * p.G + w.g) * p.keybits_words : nullptr;
     const unsigned char* bias_row = nullptr;
     if (BIAS)
@@ -395,7 +448,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     for (int j = next_tile<LIST>(w, w.lo_cta - 1); j >= 0; j = next_tile<LIST>(w, j)) {
       if (!needs<LIST>(w, wg, j)) continue;
       const int k0 = kv_tile<LIST>(w, j) * 128;
-      mbar_wait(&s_full[wg], n_done & 1);
+      mbar_wait(&s_full[wg], s_cnt & 1);
+      ++s_cnt;
       tc_fence_after();
       uint32_t s[128];
       tmem_ld32(tmem + lane_base + col_s + 0, &s[0]);
@@ -424,8 +478,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 #pragma unroll
           for (int c8 = 0; c8 < 16; ++c8) {
             if (k0 + c8 * 8 + 8 <= p.Sk) {
-              const uint4 u = __ldg(br + c8);
-              const uint32_t ww[4] = {u.x, u.y, u.z, u.w};
+              const uint4 u4 = __ldg(br + c8);
+              const uint32_t ww[4] = {u4.x, u4.y, u4.z, u4.w};
 #pragma unroll
               for (int t = 0; t < 4; ++t) {
                 x[c8 * 8 + 2 * t] = fmaf(bf16_lo(ww[t]), kLog2e, x[c8 * 8 + 2 * t]);
@@ -435,8 +489,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 #pragma unroll
               for (int t = 0; t < 8; ++t) {
                 const int k = k0 + c8 * 8 + t;
-                const unsigned short u = k < p.Sk ? reinterpret_cast<const unsigned short*>(bias_row)[k] : 0;
-                x[c8 * 8 + t] = fmaf(__uint_as_float((uint32_t)u << 16), kLog2e, x[c8 * 8 + t]);
+                const unsigned short us = k < p.Sk ? reinterpret_cast<const unsigned short*>(bias_row)[k] : 0;
+                x[c8 * 8 + t] = fmaf(__uint_as_float((uint32_t)us << 16), kLog2e, x[c8 * 8 + t]);
               }
             }
           }
@@ -506,10 +560,14 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       // Ping-pong: the two warpgroups take turns on the MUFU (exp) pipe for the
       // tiles both need, so each exp loop runs at full rate while the tensor
       // pipe works for the other warpgroup (CTA-local named barriers 2 and 3).
+      // The alternation runs across units: WG0 waits for WG1's previous common
+      // tile except at the CTA's first one (and once more after its last unit);
+      // WG1 signals after every common tile.
       const bool common = needs<LIST>(w, 0, j) && needs<LIST>(w, 1, j);
       if (common) {
-        if (wg == 0 && j > c_lo) named_bar_sync(2, 256);
+        if (wg == 0 && pp_started) named_bar_sync(2, 256);
         if (wg == 1) named_bar_sync(3, 256);
+        pp_started = true;
       }
       float ls0 = 0.f, ls1 = 0.f, ls2 = 0.f, ls3 = 0.f;
       uint32_t pk[64];
@@ -529,7 +587,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       }
       if (common) {
         if (wg == 0) named_bar_arrive(3, 256);
-        if (wg == 1 && j < c_hi - 1) named_bar_arrive(2, 256);
+        if (wg == 1) named_bar_arrive(2, 256);
       }
       l += (ls0 + ls1) + (ls2 + ls3);
       tmem_st32(tmem + lane_base + col_s + C::P_OFF, &pk[0]);
@@ -539,17 +597,21 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       mbar_arrive(&p_full[wg]);
       ++n_done;
     }
+    release_unit(it);
 
     // ============================== epilogue ==============================
+    // O_i of the next unit is first written by PV_i(next, first), which waits for this
+    // warpgroup's p_full of that tile -- i.e. after this epilogue has read O_i.
     if (n_done > 0) {
-      mbar_wait(&o_full[wg], 0);
+      mbar_wait(&o_full[wg], o_cnt & 1);
+      ++o_cnt;
       tc_fence_after();
     }
     const float inv_l = l > 0.f ? 1.f / l : 0.f;
     const float lam = DIFF ? (p.lambda_h ? p.lambda_h[w.h] : p.lambda) : 0.f;
     float* xbuf = reinterpret_cast<float*>(sQ);      // diff: map-1 rows handed to WG0 (Q is dead now)
     if (DIFF && wg == 1) {
-      if (n_done == 0) mbar_wait(q_full, 0);         // never overwrite Q while its TMA may be in flight
+      if (n_done == 0) mbar_wait(q_full, it & 1);    // never overwrite Q while its TMA may be in flight
 #pragma unroll
       for (int c = 0; c < D; c += 32) {
         uint32_t o[32];
@@ -600,8 +662,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           const uint4* gp = reinterpret_cast<const uint4*>(static_cast<const unsigned short*>(p.gate) + gbase + c);
 #pragma unroll
           for (int t8 = 0; t8 < 4; ++t8) {
-            const uint4 u = __ldg(gp + t8);
-            const uint32_t ww[4] = {u.x, u.y, u.z, u.w};
+            const uint4 u4 = __ldg(gp + t8);
+            const uint32_t ww[4] = {u4.x, u4.y, u4.z, u4.w};
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
               float g0 = bf16_lo(ww[t]), g1 = bf16_hi(ww[t]);
@@ -625,13 +687,29 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       if (p.lse && row_valid)
         p.lse[w.b * p.lses.b + w.g * p.lses.g + (int64_t)w.h * p.lses.h + (int64_t)q * p.lses.s] =
             l > 0.f ? (m_ref + __log2f(l)) * kLn2 : -INFINITY;
+      if (DIFF) mbar_arrive(q_empty);                 // WG0 is done reading xbuf (sQ)
     }
+    }  // unit loop
+    if (wg == 0 && pp_started) named_bar_sync(2, 256);   // matches WG1's arrive after its last common tile
   }
 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 9) tmem_dealloc<512>(tmem);
+}
+
+static int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
 }
 
 template <int D, bool DIFF, int MOD>
@@ -646,7 +724,10 @@ static cudaError_t launch_one(const AttnParams& p, const TmaMaps& maps, cudaStre
   if (e != cudaSuccess) return e;
   const int rows_per_unit = DIFF ? 128 : 256;
   const long long units = (long long)p.B * p.G * p.Hq * ((p.Sq + rows_per_unit - 1) / rows_per_unit);
-  kern<<<(unsigned)units, kThreadsTc, C::SMEM_TOTAL, stream>>>(p, maps);
+  if (units >= (1ll << 31)) return cudaErrorInvalidValue;
+  // persistent: one CTA per SM (TMEM and shared memory admit one), each walks units with stride grid
+  const int grid = (int)std::min<long long>(units, num_sms());
+  kern<<<grid, kThreadsTc, C::SMEM_TOTAL, stream>>>(p, maps, (int)units);
   return cudaGetLastError();
 }
 

@@ -37,6 +37,8 @@ using namespace fl;
 
 namespace {
 
+constexpr size_t kSchedBytes = 256;   // persistent-scheduler counter region at the head of the workspace
+
 thread_local std::string g_err;
 thread_local int64_t g_launches = 0;
 
@@ -198,6 +200,7 @@ struct Prepared {
   View5 q, k, v, o, lse, bias, gate, km;
   int q_rank = 4;
   size_t keybits_bytes = 0;
+  size_t ws_bytes = 0;       // bf16: [0,256) scheduler ticket counter, then the packed key mask
   bool empty_work = false;
   bool no_keys = false;
   bool bf16 = false;
@@ -383,6 +386,7 @@ fl_status prepare(const fl_attn_args* a, Prepared& P, bool device_ptrs) {
   p.max_sel = var.mask == FL_MASK_BLOCKLIST ? (int)var.blk_idx.size[2] : 0;
   p.n_qblk = var.mask == FL_MASK_BLOCKLIST ? (int)((Sq + var.blk_q - 1) / var.blk_q) : 0;
   p.in_dtype = P.bf16 ? 0 : 1;
+  P.ws_bytes = (P.bf16 ? kSchedBytes : 0) + ((P.keybits_bytes + 255) & ~size_t(255));
   P.empty_work = B * G * Hq * Sq == 0 || Dv == 0;
   P.no_keys = Sk == 0;
   return FL_OK;
@@ -406,10 +410,15 @@ fl_status launch_prepared(Prepared& P, const fl_attn_args* a) {
     if ((s = encode_map(P.k, ch, &maps.k, &maps.k_bcast_g, &maps.k_bcast_b)) != FL_OK) return s;
     if ((s = encode_map(P.v, ch, &maps.v, &maps.v_bcast_g, &maps.v_bcast_b)) != FL_OK) return s;
   }
+  if (P.ws_bytes && (!a->workspace || a->workspace_bytes < P.ws_bytes))
+    return fail(FL_ERR_WORKSPACE, "this call needs %zu bytes of workspace (fl_attn_workspace_size)", P.ws_bytes);
+  if (P.bf16) {
+    P.p.tile_ctr = static_cast<int32_t*>(a->workspace);
+    e = cudaMemsetAsync(P.p.tile_ctr, 0, sizeof(int32_t), stream);
+    if (e != cudaSuccess) return cuda_fail(e, "scheduler counter reset");
+  }
   if (P.km.present) {
-    if (!a->workspace || a->workspace_bytes < P.keybits_bytes)
-      return fail(FL_ERR_WORKSPACE, "key_mask needs %zu bytes of workspace", P.keybits_bytes);
-    uint32_t* bits = static_cast<uint32_t*>(a->workspace);
+    uint32_t* bits = reinterpret_cast<uint32_t*>(static_cast<char*>(a->workspace) + (P.bf16 ? kSchedBytes : 0));
     e = launch_pack_keymask(static_cast<const unsigned char*>(P.km.data), P.km.size[0] > 1 ? P.km.stride[0] : 0,
                             P.km.size[1] > 1 ? P.km.stride[1] : 0, P.km.stride[4], P.p.B, P.p.G, P.p.Sk,
                             P.p.keybits_words, bits, stream);
@@ -445,7 +454,7 @@ fl_status fl_attn_workspace_size(const fl_attn_args* args, size_t* bytes) {
   Prepared P;
   fl_status s = prepare(args, P, false);
   if (s != FL_OK) return s;
-  *bytes = P.keybits_bytes;
+  *bytes = P.empty_work || P.no_keys ? 0 : P.ws_bytes;
   return FL_OK;
 }
 
@@ -507,7 +516,7 @@ fl_status fl_attn_host_scratch_size(const fl_attn_args* args, size_t* bytes) {
   if (s != FL_OK) return s;
   Prepared P;
   if ((s = prepare(args, P, false)) != FL_OK) return s;
-  *bytes = hp.total + align256(P.keybits_bytes);
+  *bytes = hp.total + P.ws_bytes;
   return FL_OK;
 }
 
@@ -519,7 +528,7 @@ fl_status fl_attn_fwd_host(const fl_attn_args* host_args, void* scratch, size_t 
   if (s != FL_OK) return s;
   Prepared P0;
   if ((s = prepare(host_args, P0, false)) != FL_OK) return s;
-  const size_t need = hp.total + align256(P0.keybits_bytes);
+  const size_t need = hp.total + P0.ws_bytes;
   if (!scratch || scratch_bytes < need) return fail(FL_ERR_WORKSPACE, "fl_attn_fwd_host needs %zu scratch bytes", need);
   if (!on_device(scratch)) return fail(FL_ERR_INVALID_ARGUMENT, "scratch must be device memory");
   cudaStream_t stream = static_cast<cudaStream_t>(host_args->stream);
@@ -531,7 +540,7 @@ fl_status fl_attn_fwd_host(const fl_attn_args* host_args, void* scratch, size_t 
     // re-stride as dense row-major (same layout as the contiguous host tensor)
   }
   d.workspace = base + hp.total;
-  d.workspace_bytes = align256(P0.keybits_bytes);
+  d.workspace_bytes = P0.ws_bytes;
   Prepared P;
   if ((s = prepare(&d, P, true)) != FL_OK) return s;
   for (int i = 0; i < hp.n; ++i) {

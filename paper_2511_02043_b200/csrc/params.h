@@ -44,6 +44,7 @@ struct AttnParams {
   // ---- block list (RSA)
   const int32_t* blk_idx; const int32_t* blk_cnt; int32_t blk_q, blk_k, max_sel, n_qblk;
   int32_t in_dtype;        // 0 bf16, 1 f32
+  int32_t* tile_ctr;       // bf16 path: persistent-scheduler ticket counter (workspace, zeroed per call)
 };
 
 // TMA tensor maps for the tcgen05 kernel family (5-D: D, S, H, G, B).

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Summarise ncu captures for profiles/ (run HERE, no GPU needed).
 
-    python tools/ncu_summary.py full <name> <report.ncu-rep> [variant]   # one --set full capture
+    python tools/ncu_summary.py full <name> <report.ncu-rep|raw.csv> [variant]   # one --set full capture
     python tools/ncu_summary.py launches <name> <launches.csv>           # gpu__time_duration launch list
 
 `full` updates profiles/ncu_summary.json[variant] (bench.py reads
@@ -44,7 +44,11 @@ def _val(vals, key, default=None):
 
 
 def full(name, rep, variant):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    raw = raw[raw.index('"ID"'):] if '"ID"' in raw else raw
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     out_lines, summ = [f"ncu --set full capture {os.path.basename(rep)} (clock-control none)"], {}
