@@ -448,6 +448,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     for (int j = next_tile<LIST>(w, w.lo_cta - 1); j >= 0; j = next_tile<LIST>(w, j)) {
       if (!needs<LIST>(w, wg, j)) continue;
       const int k0 = kv_tile<LIST>(w, j) * 128;
+      uint32_t kw[4];                                  // key-mask bits of this tile, loaded before the S wait
+      if (kbits) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) kw[t] = __ldg(kbits + (k0 >> 5) + t);
+      }
       mbar_wait(&s_full[wg], s_cnt & 1);
       ++s_cnt;
       tc_fence_after();
@@ -473,26 +478,39 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         x[c] = v;
       }
       if (BIAS) {  // additive bias (Evoformer pair bias), then softcap if any (order G16)
-        if (p.bias_vec) {
+        if (p.bias_vec && k0 + 128 <= p.Sk) {
+          // full tile: issue 8 independent 16-byte loads before the first use (one L2 round trip
+          // per half row instead of one per load)
           const uint4* br = reinterpret_cast<const uint4*>(bias_row + (int64_t)k0 * 2);
 #pragma unroll
-          for (int c8 = 0; c8 < 16; ++c8) {
-            if (k0 + c8 * 8 + 8 <= p.Sk) {
-              const uint4 u4 = __ldg(br + c8);
-              const uint32_t ww[4] = {u4.x, u4.y, u4.z, u4.w};
+          for (int h8 = 0; h8 < 2; ++h8) {
+            uint4 u4[8];
+#pragma unroll
+            for (int c8 = 0; c8 < 8; ++c8) u4[c8] = __ldg(br + h8 * 8 + c8);
+#pragma unroll
+            for (int c8 = 0; c8 < 8; ++c8) {
+              const uint32_t ww[4] = {u4[c8].x, u4[c8].y, u4[c8].z, u4[c8].w};
 #pragma unroll
               for (int t = 0; t < 4; ++t) {
-                x[c8 * 8 + 2 * t] = fmaf(bf16_lo(ww[t]), kLog2e, x[c8 * 8 + 2 * t]);
-                x[c8 * 8 + 2 * t + 1] = fmaf(bf16_hi(ww[t]), kLog2e, x[c8 * 8 + 2 * t + 1]);
-              }
-            } else {  // ragged tail: element loads, predicated
-#pragma unroll
-              for (int t = 0; t < 8; ++t) {
-                const int k = k0 + c8 * 8 + t;
-                const unsigned short us = k < p.Sk ? reinterpret_cast<const unsigned short*>(bias_row)[k] : 0;
-                x[c8 * 8 + t] = fmaf(__uint_as_float((uint32_t)us << 16), kLog2e, x[c8 * 8 + t]);
+                const int c = (h8 * 8 + c8) * 8 + 2 * t;
+                x[c] = fmaf(bf16_lo(ww[t]), kLog2e, x[c]);
+                x[c + 1] = fmaf(bf16_hi(ww[t]), kLog2e, x[c + 1]);
               }
             }
+          }
+        } else if (p.bias_vec) {  // ragged last tile: element loads, predicated, batched the same way
+          const unsigned short* bs16 = reinterpret_cast<const unsigned short*>(bias_row);
+#pragma unroll
+          for (int h8 = 0; h8 < 4; ++h8) {
+            unsigned short us[32];
+#pragma unroll
+            for (int t = 0; t < 32; ++t) {
+              const int k = k0 + h8 * 32 + t;
+              us[t] = k < p.Sk ? bs16[k] : (unsigned short)0;
+            }
+#pragma unroll
+            for (int t = 0; t < 32; ++t)
+              x[h8 * 32 + t] = fmaf(__uint_as_float((uint32_t)us[t] << 16), kLog2e, x[h8 * 32 + t]);
           }
         } else {
 #pragma unroll
@@ -521,9 +539,6 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         }
       }
       if (kbits) {
-        uint32_t kw[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) kw[t] = __ldg(kbits + (k0 >> 5) + t);
 #pragma unroll
         for (int c = 0; c < 128; ++c) x[c] = ((kw[c >> 5] >> (c & 31)) & 1u) ? x[c] : -INFINITY;
       }
@@ -602,6 +617,15 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     // ============================== epilogue ==============================
     // O_i of the next unit is first written by PV_i(next, first), which waits for this
     // warpgroup's p_full of that tile -- i.e. after this epilogue has read O_i.
+    const bool gated = p.gate_mode != GATE_NONE && row_valid && !(DIFF && wg == 1);
+    const uint4* gp = reinterpret_cast<const uint4*>(static_cast<const unsigned short*>(p.gate) + w.b * p.gs.b +
+                                                     w.g * p.gs.g + (int64_t)w.h * p.gs.h + (int64_t)q * p.gs.s);
+    constexpr bool kGateEarly = D <= 32;               // small head: the whole gate row is 4 registers x 4
+    uint4 gv[kGateEarly ? D / 8 : 1];                  // in flight while the last PV runs
+    if (kGateEarly && gated) {
+#pragma unroll
+      for (int t = 0; t < (kGateEarly ? D / 8 : 1); ++t) gv[t] = __ldg(gp + t);
+    }
     if (n_done > 0) {
       mbar_wait(&o_full[wg], o_cnt & 1);
       ++o_cnt;
@@ -634,7 +658,6 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     } else {
       if (DIFF) named_bar_sync(1, 256);
       const int64_t obase = w.b * p.os.b + w.g * p.os.g + (int64_t)w.h * p.os.h + (int64_t)q * p.os.s;
-      const int64_t gbase = w.b * p.gs.b + w.g * p.gs.g + (int64_t)w.h * p.gs.h + (int64_t)q * p.gs.s;
 #pragma unroll
       for (int c = 0; c < D; c += 32) {
         uint32_t o[32];
@@ -658,18 +681,21 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             f[4 * t4 + 3] -= lam * v.w;
           }
         }
-        if (p.gate_mode != GATE_NONE && row_valid) {
-          const uint4* gp = reinterpret_cast<const uint4*>(static_cast<const unsigned short*>(p.gate) + gbase + c);
+        if (gated) {
+#pragma unroll
+          uint4 g4[4];
+#pragma unroll
+          for (int t8 = 0; t8 < 4; ++t8) g4[t8] = kGateEarly ? gv[kGateEarly ? (c >> 3) + t8 : 0] : __ldg(gp + (c >> 3) + t8);
 #pragma unroll
           for (int t8 = 0; t8 < 4; ++t8) {
-            const uint4 u4 = __ldg(gp + t8);
+            const uint4 u4 = g4[t8];
             const uint32_t ww[4] = {u4.x, u4.y, u4.z, u4.w};
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
               float g0 = bf16_lo(ww[t]), g1 = bf16_hi(ww[t]);
-              if (p.gate_mode == GATE_SIGMOID) {
-                g0 = 1.f / (1.f + ex2(-g0 * kLog2e));
-                g1 = 1.f / (1.f + ex2(-g1 * kLog2e));
+              if (p.gate_mode == GATE_SIGMOID) {           // sigma(g) = 1 / (1 + 2^(-g log2 e))
+                g0 = __fdividef(1.f, 1.f + ex2(-g0 * kLog2e));
+                g1 = __fdividef(1.f, 1.f + ex2(-g1 * kLog2e));
               }
               f[t8 * 8 + 2 * t] *= g0;
               f[t8 * 8 + 2 * t + 1] *= g1;
