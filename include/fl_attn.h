@@ -178,6 +178,12 @@ void fl_shard_range(int64_t units, int32_t world, int32_t rank, int64_t* begin, 
 fl_status fl_diag_umma_gemm(const void* a, const void* b, float* c, int32_t n, int32_t k,
                             int32_t b_mn_major, int32_t a_from_tmem, void* stream);
 
+/* Diagnostic: cycle counters of the bf16 kernel's pipeline phases, only in a library built with
+ * -DFL_TIMING (FL_ERR_UNSUPPORTED otherwise).  out48 receives [3][16] uint64 sums over CTAs:
+ * rows 0/1 = softmax warpgroups (slots 0..8: bookkeeping, S wait, S load, score+mask+max, O rescale,
+ * ping-pong wait, exp loop, P store, tail; slot 15 = tiles), row 2 reserved.  Synchronises. */
+fl_status fl_debug_timing(uint64_t* out48, int32_t reset);
+
 const char* fl_status_string(fl_status s);
 const char* fl_last_error(void);   /* thread-local detail of the last non-OK status */
 int32_t fl_abi_version(void);

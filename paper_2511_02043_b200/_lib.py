@@ -16,7 +16,7 @@ ABI_VERSION = 1
 
 EXPORTS = ["fl_attn_fwd", "fl_attn_workspace_size", "fl_attn_host_scratch_size", "fl_attn_fwd_host",
            "fl_rsa_build_summaries", "fl_rsa_select", "fl_shard_range", "fl_diag_umma_gemm",
-           "fl_status_string", "fl_last_error", "fl_abi_version", "fl_launch_count"]
+           "fl_status_string", "fl_last_error", "fl_abi_version", "fl_launch_count", "fl_debug_timing"]
 
 
 class Tensor(C.Structure):
@@ -77,6 +77,8 @@ def lib():
         L.fl_status_string.restype = C.c_char_p
         L.fl_last_error.restype = C.c_char_p
         L.fl_abi_version.restype = C.c_int32
+        L.fl_debug_timing.argtypes = [C.POINTER(C.c_uint64), C.c_int32]
+        L.fl_debug_timing.restype = C.c_int
         L.fl_launch_count.argtypes = [C.c_int32]
         L.fl_launch_count.restype = C.c_int64
         for name in ("fl_attn_fwd", "fl_attn_workspace_size", "fl_attn_host_scratch_size", "fl_attn_fwd_host",

@@ -49,6 +49,9 @@ def build(verbose: bool = False, extra=None) -> str:
     extra = list(extra or [])
     if os.environ.get("FL_DEBUG_HANG"):
         extra.append("-DFL_DEBUG_HANG")
+    if os.environ.get("FL_TIMING"):
+        extra.append("-DFL_TIMING")
+    extra += os.environ.get("FL_EXTRA", "").split()   # experiment flags, e.g. "-DFL_EMU_MASK=0"
     os.makedirs(BUILD, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:

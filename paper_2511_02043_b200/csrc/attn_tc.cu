@@ -38,6 +38,22 @@
 
 namespace fl {
 
+#ifdef FL_TIMING
+// Diagnostic build only (-DFL_TIMING): cycle counters of thread 0 of each softmax
+// warpgroup and of the MMA issuer, summed over CTAs; read with fl_debug_timing().
+__device__ unsigned long long g_fl_timing[3][16];
+#define FL_T(slot)                                    \
+  do {                                                \
+    const long long t_now_ = clock64();               \
+    t_acc[slot] += t_now_ - t_prev;                   \
+    t_prev = t_now_;                                  \
+  } while (0)
+#else
+#define FL_T(slot) \
+  do {             \
+  } while (0)
+#endif
+
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kTau = 8.0f;
@@ -77,6 +93,28 @@ struct TcCfg {
   static constexpr uint32_t IDESC_O = idesc_bf16_f32(128, D, 1);    // P (TMEM) x V (MN-major)
   static constexpr int ENTRIES_PER_TILE = DIFF ? 3 : 2;              // K0 [K1] V
 };
+
+// Which groups of 4 scores (index (c/4) % 8) take the FMA-pipe exp2 (ex2_emu2) instead of
+// the MUFU.  On paper a 3/8 fraction balances the pipes (MUFU 1/16 clk/SM per score vs FMA
+// ~(2 + 6 f)/128), but measured on B200 (profiles/r01_ab_*.txt) the softmax warpgroups are
+// latency/issue-bound, not MUFU-bound, and the extra ~5 instructions per emulated score cost
+// more than they save (causal 1071 -> 982 TF/s with 3/8), so the default is 0 (all MUFU).
+template <int MOD>
+struct EmuCfg {
+#ifdef FL_EMU_MASK
+  static constexpr uint32_t MASK = FL_EMU_MASK;
+#else
+  static constexpr uint32_t MASK = 0u;
+#endif
+};
+// Ping-pong of the two softmax warpgroups' exp loops on named barriers (FA3-style).  Measured
+// slower with the persistent kernel (causal 982 vs 1071 TF/s, diff 624 vs 681): the alternation
+// serialises the exp loops while neither the MUFU nor the issue slots are saturated.  Opt-in.
+#ifdef FL_PINGPONG
+constexpr bool kPingPong = true;
+#else
+constexpr bool kPingPong = false;
+#endif
 
 // The KV tiles a CTA walks form a "schedule" indexed by t.  For every interval
 // mask (masks.cuh) t IS the KV tile index and warpgroup i needs t in [lo[i], hi[i]).
@@ -413,6 +451,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
    }
   } else {
     regs_inc<kRegsSoftmax>();
+#ifdef FL_TIMING
+    long long t_acc[16] = {0};
+    long long t_prev = clock64();
+#endif
     // ============================== softmax warpgroups ==============================
     const int wg = warp >> 2;
     const int r = threadIdx.x & 127;                 // row within the tile == TMEM lane
@@ -453,7 +495,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 #pragma unroll
         for (int t = 0; t < 4; ++t) kw[t] = __ldg(kbits + (k0 >> 5) + t);
       }
+      FL_T(0);                                         // 0: tile bookkeeping / previous epilogue
       mbar_wait(&s_full[wg], s_cnt & 1);
+      FL_T(1);                                         // 1: waiting for S
       ++s_cnt;
       tc_fence_after();
       uint32_t s[128];
@@ -462,6 +506,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       tmem_ld32(tmem + lane_base + col_s + 64, &s[64]);
       tmem_ld32(tmem + lane_base + col_s + 96, &s[96]);
       tmem_wait_ld();
+      FL_T(2);                                         // 2: tcgen05.ld of S
       // ---- score modification (Eq.4) in the log2 domain: x = log2(e) * mod(scale * s)
       float x[128];
       constexpr bool kRaw = MOD == MOD_NONE && !BIAS;  // keep raw s; scale folds into the exp FFMA
@@ -553,6 +598,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       }
       const float xscale = kRaw ? sc_l2 : 1.f;        // x * xscale is the log2-domain score
       const float mt = fmaxf(fmaxf(mt0, mt1), fmaxf(mt2, mt3)) * xscale;
+      FL_T(3);                                         // 3: score mod + mask + row max
       const bool rescale = mt > m_ref + kTau;          // also true for the first finite tile (m_ref = -inf)
       const float factor = rescale ? ex2(m_ref - mt) : 1.f;
       if (n_done > 0 && __any_sync(0xffffffffu, rescale)) {
@@ -578,12 +624,14 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       // The alternation runs across units: WG0 waits for WG1's previous common
       // tile except at the CTA's first one (and once more after its last unit);
       // WG1 signals after every common tile.
-      const bool common = needs<LIST>(w, 0, j) && needs<LIST>(w, 1, j);
+      const bool common = kPingPong && needs<LIST>(w, 0, j) && needs<LIST>(w, 1, j);
+      FL_T(4);                                         // 4: O rescale
       if (common) {
         if (wg == 0 && pp_started) named_bar_sync(2, 256);
         if (wg == 1) named_bar_sync(3, 256);
         pp_started = true;
       }
+      FL_T(5);                                         // 5: ping-pong wait
       float ls0 = 0.f, ls1 = 0.f, ls2 = 0.f, ls3 = 0.f;
       uint32_t pk[64];
 #pragma unroll
@@ -591,15 +639,21 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         float a0, a1, a2, a3;
         ffma2(a0, a1, x[c], x[c + 1], xscale, xscale, neg_m, neg_m);
         ffma2(a2, a3, x[c + 2], x[c + 3], xscale, xscale, neg_m, neg_m);
-        a0 = ex2(a0);
-        a1 = ex2(a1);
-        a2 = ex2(a2);
-        a3 = ex2(a3);
+        if ((EmuCfg<MOD>::MASK >> ((c >> 2) & 7)) & 1u) {
+          ex2_emu2(a0, a1);
+          ex2_emu2(a2, a3);
+        } else {
+          a0 = ex2(a0);
+          a1 = ex2(a1);
+          a2 = ex2(a2);
+          a3 = ex2(a3);
+        }
         fadd2(ls0, ls1, ls0, ls1, a0, a1);
         fadd2(ls2, ls3, ls2, ls3, a2, a3);
         pk[c >> 1] = pack_bf16(a0, a1);
         pk[(c >> 1) + 1] = pack_bf16(a2, a3);
       }
+      FL_T(6);                                         // 6: exp loop
       if (common) {
         if (wg == 0) named_bar_arrive(3, 256);
         if (wg == 1) named_bar_arrive(2, 256);
@@ -611,6 +665,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       tc_fence_before();
       mbar_arrive(&p_full[wg]);
       ++n_done;
+      FL_T(7);                                         // 7: P store + arrive
     }
     release_unit(it);
 
@@ -631,7 +686,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       ++o_cnt;
       tc_fence_after();
     }
-    const float inv_l = l > 0.f ? 1.f / l : 0.f;
+    const bool empty_row = m_ref == -INFINITY || !(l > 0.f);   // G7 (emulated exps of -inf are ~2^-126, not 0)
+    const float inv_l = empty_row ? 0.f : 1.f / l;
     const float lam = DIFF ? (p.lambda_h ? p.lambda_h[w.h] : p.lambda) : 0.f;
     float* xbuf = reinterpret_cast<float*>(sQ);      // diff: map-1 rows handed to WG0 (Q is dead now)
     if (DIFF && wg == 1) {
@@ -712,11 +768,18 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       }
       if (p.lse && row_valid)
         p.lse[w.b * p.lses.b + w.g * p.lses.g + (int64_t)w.h * p.lses.h + (int64_t)q * p.lses.s] =
-            l > 0.f ? (m_ref + __log2f(l)) * kLn2 : -INFINITY;
+            empty_row ? -INFINITY : (m_ref + __log2f(l)) * kLn2;
       if (DIFF) mbar_arrive(q_empty);                 // WG0 is done reading xbuf (sQ)
     }
     }  // unit loop
     if (wg == 0 && pp_started) named_bar_sync(2, 256);   // matches WG1's arrive after its last common tile
+#ifdef FL_TIMING
+    FL_T(8);
+    if (r == 0) {
+      for (int i = 0; i < 9; ++i) atomicAdd(&g_fl_timing[wg][i], (unsigned long long)t_acc[i]);
+      atomicAdd(&g_fl_timing[wg][15], (unsigned long long)s_cnt);
+    }
+#endif
   }
 
   tc_fence_before();
@@ -777,5 +840,21 @@ cudaError_t launch_attn_tc(const AttnParams& p, const TmaMaps& maps, cudaStream_
 }
 
 int tc_chunk_elems(int D) { return D >= 64 ? 64 : 32; }
+
+// fl_debug_timing support: copies (and with reset, clears) the FL_TIMING counters.
+cudaError_t debug_timing(unsigned long long* out, int reset) {
+#ifdef FL_TIMING
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_fl_timing, sizeof(g_fl_timing));
+  if (e == cudaSuccess && reset) {
+    unsigned long long z[3][16] = {};
+    e = cudaMemcpyToSymbol(g_fl_timing, z, sizeof(z));
+  }
+  return e;
+#else
+  (void)out;
+  (void)reset;
+  return cudaErrorNotSupported;
+#endif
+}
 
 }  // namespace fl

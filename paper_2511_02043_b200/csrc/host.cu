@@ -31,6 +31,7 @@ cudaError_t launch_rsa_summaries(const void* k, int64_t sb, int64_t sg, int64_t 
 cudaError_t launch_rsa_select(const RsaSelParams& p, const CUtensorMap& tq, const CUtensorMap& tmin,
                               const CUtensorMap& tmax, cudaStream_t stream);
 int rsa_select_max_blocks(int D);
+cudaError_t debug_timing(unsigned long long* out, int reset);
 }  // namespace fl
 
 using namespace fl;
@@ -703,6 +704,16 @@ const char* fl_status_string(fl_status s) {
     case FL_ERR_ABI_VERSION: return "FL_ERR_ABI_VERSION";
   }
   return "FL_ERR_UNKNOWN";
+}
+
+fl_status fl_debug_timing(uint64_t* out48, int32_t reset) {
+  if (!out48) return fail(FL_ERR_INVALID_ARGUMENT, "out48 is NULL");
+  cudaError_t e = debug_timing(reinterpret_cast<unsigned long long*>(out48), reset);
+  if (e == cudaErrorNotSupported) {
+    cudaGetLastError();
+    return fail(FL_ERR_UNSUPPORTED, "library built without -DFL_TIMING");
+  }
+  return e == cudaSuccess ? FL_OK : cuda_fail(e, "debug timing copy");
 }
 
 const char* fl_last_error(void) { return g_err.c_str(); }

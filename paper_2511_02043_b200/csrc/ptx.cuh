@@ -40,6 +40,20 @@ FL_DEVICE bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait with a suspend-time hint: a waiting warp is parked until the phase completes (or
+// the hint elapses) instead of spinning SYNCS/BRA/YIELD through the issue slots that the
+// softmax warps sharing its SM sub-partition need.
+FL_DEVICE bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
+      : "memory");
+  return ok != 0;
+}
 FL_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
 #ifdef FL_DEBUG_HANG
   long long spins = 0;
@@ -50,7 +64,7 @@ FL_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
   }
 #else
-  while (!mbar_try_wait(bar, parity)) {
+  while (!mbar_try_wait_sleep(bar, parity)) {
   }
 #endif
 }
@@ -218,6 +232,27 @@ FL_DEVICE void fadd2(float& dx, float& dy, float ax, float ay, float bx, float b
       : "=f"(dx), "=f"(dy)
       : "f"(ax), "f"(ay), "f"(bx), "f"(by));
 }
+// 2^x for a pair on the FMA pipe (MUFU offload): x = j + f, j = rint(x), f in [-0.5, 0.5],
+// 2^f ~ ((c3 f + c2) f + c1) f + c0 (relative-error minimax fit, max rel. error 7.5e-5 << bf16's
+// 2^-9 rounding of P), 2^j added to the exponent field.  Inputs are clamped at -126 so masked
+// (-inf) scores give ~2^-126, not NaN; callers treat rows whose running max is still -inf as
+// empty, so these tiny weights never reach an output.
+FL_DEVICE void ex2_emu2(float& a, float& b) {
+  constexpr float kRound = 12582912.0f;   // 1.5 * 2^23: adding it rounds to an integer in the low mantissa bits
+  constexpr float c0 = 0.99992811f, c1 = 0.69326099f, c2 = 0.24261054f, c3 = 0.05517132f;
+  a = fmaxf(a, -126.0f);
+  b = fmaxf(b, -126.0f);
+  float ta, tb, ja, jb, fa, fb, pa, pb;
+  fadd2(ta, tb, a, b, kRound, kRound);
+  fadd2(ja, jb, ta, tb, -kRound, -kRound);
+  ffma2(fa, fb, ja, jb, -1.0f, -1.0f, a, b);            // f = x - j
+  ffma2(pa, pb, fa, fb, c3, c3, c2, c2);
+  ffma2(pa, pb, pa, pb, fa, fb, c1, c1);
+  ffma2(pa, pb, pa, pb, fa, fb, c0, c0);
+  a = __int_as_float(__float_as_int(pa) + (__float_as_int(ta) << 23));
+  b = __int_as_float(__float_as_int(pb) + (__float_as_int(tb) << 23));
+}
+
 FL_DEVICE void named_bar_arrive(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
