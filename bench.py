@@ -234,6 +234,7 @@ class Job:
         self.e2e = None           # (fn, h2d_bytes, d2h_bytes)
         self.oracle = None        # fn(budget_s) -> (tflops, threads, sample, secs)
         self.extra = {}
+        self.parity = {}          # host inputs / outputs / oracle kwargs for the full-size parity tests
 
 
 def dense_job(names, rank, world, device, with_host=True):
@@ -265,7 +266,10 @@ def dense_job(names, rank, world, device, with_host=True):
         job.step_flops += flops
         kws[n] = (kw, offs)
         pairs_by[n] = pairs
-    job.extra["dev"] = (q, k, v, out)
+    job.parity = {"host": host, "out": out,
+                  "oracle_kw": {n: dict({x: VARIANTS[n][x] for x in VARIANT_KW if x in VARIANTS[n]},
+                                        **({"doc_offsets": kws[n][1]} if kws[n][1] is not None else {}))
+                                for n in names}}
 
     if with_host:
         runner = fl.HostRunner(device)
@@ -331,6 +335,7 @@ def evo_job(name, rank, world, device, with_host=True):
     job.calls.append(Call(name, lambda: fl.attn_fwd(q, k, v, out=out, workspace=ws, **kw), flops, nbytes, "tensor",
                           kernel="attn_tc_kernel"))
     job.step_flops = flops
+    job.parity = {"host": host, "out": out}
 
     if with_host:
         pin = {n: t.pin_memory() for n, t in host.items()}
@@ -408,6 +413,8 @@ def rsa_job(name, rank, world, device, with_host=True):
                           "hbm" if decode else "tensor", kernel="attn_tc_kernel"))
     job.step_flops = flops
     job.extra.update(listed_blocks=listed, kv_blocks=nkb * B * H * nqb, rsa_decode=decode)
+    job.parity = {"host": {"q": qh, "k": kh, "v": vh}, "out": out, "idx": idx, "cnt": cnt, "kmin": kmin,
+                  "kmax": kmax, "Sq": Sq}
 
     if with_host:
         hq, hk, hv = qh.pin_memory(), kh.pin_memory(), vh.pin_memory()
@@ -490,7 +497,7 @@ def run_reference(args, world, rank):
     if rank != 0:
         return
     job = oracle_only_job(args.variant)
-    budget = max(2.0, 60.0 / (args.steps + args.warmup))
+    budget = float(os.environ.get("FL_REF_BUDGET_S", max(2.0, 60.0 / (args.steps + args.warmup))))
     vals, samples = [], ""
     for i in range(args.warmup + args.steps):
         v, cores, samples, _ = job.oracle(budget)
