@@ -563,6 +563,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="time eager launches instead of CUDA-graph replays of the step")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup()
@@ -589,9 +591,30 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    E = lambda: torch.cuda.Event(enable_timing=True)
+    # The timed step is a CUDA graph of the step's library calls (captured once after warm-up and
+    # replayed): launch overhead of the Python binding stays off the clock, which matters for the
+    # microsecond-scale decode step.  Each call is also captured alone for the per-call breakdown.
+    use_graph = not args.no_graph
+    launches_per_step = 0
+    if use_graph:
+        fl.launch_count(reset=True)
+        g_step = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_step):
+            step()
+        launches_per_step = fl.launch_count(reset=True)
+        g_calls = []
+        for c in job.calls:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                c.fn()
+            g_calls.append(g)
+        g_step.replay()
+        for g in g_calls:
+            g.replay()
+        torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    E = lambda: torch.cuda.Event(enable_timing=True)
     evs = [[(E(), E()) for _ in job.calls] for _ in range(args.steps)]
     fl.launch_count(reset=True)
     with ClockSampler(local) as clk:
@@ -599,13 +622,27 @@ def main():
         t0, t1 = E(), E()
         t0.record(stream)
         for i in range(args.steps):
-            step(evs[i])
+            if use_graph:
+                g_step.replay()
+            else:
+                step(evs[i])
         t1.record(stream)
         torch.cuda.synchronize()
-    launches = fl.launch_count()
+    launches = launches_per_step * args.steps if use_graph else fl.launch_count()
     total_ms = t0.elapsed_time(t1)
-    call_ms = [float(np.mean([evs[i][ci][0].elapsed_time(evs[i][ci][1]) for i in range(args.steps)]))
-               for ci in range(len(job.calls))]
+    if use_graph:
+        call_ms = []
+        for g in g_calls:
+            c0, c1 = E(), E()
+            c0.record(stream)
+            for _ in range(args.steps):
+                g.replay()
+            c1.record(stream)
+            torch.cuda.synchronize()
+            call_ms.append(c0.elapsed_time(c1) / args.steps)
+    else:
+        call_ms = [float(np.mean([evs[i][ci][0].elapsed_time(evs[i][ci][1]) for i in range(args.steps)]))
+                   for ci in range(len(job.calls))]
     red = max_over_ranks([total_ms] + call_ms, device, world)
     total_ms, call_ms = red[0], red[1:]
     ms_per_step = total_ms / args.steps
@@ -670,7 +707,9 @@ def main():
                        "parallelism": f"batch-x-head shards over {world} GPU(s), no collective",
                        "useful_tflop_per_step_per_gpu": job.step_flops / 1e12,
                        "l2": "inputs larger than L2 (per-GPU working set > 126 MB); no flush"},
-            "per_call": per_call, "roofline": roof, "gpu_launches": int(launches), "clocks": clk.summary()}
+            "per_call": per_call, "roofline": roof, "gpu_launches": int(launches), "clocks": clk.summary(),
+            "timing": "CUDA-graph replay of the step (per call: graph of that call alone)" if use_graph
+                      else "eager launches, CUDA events around each call"}
     for key, val in job.extra.items():
         if key != "dev":
             line["config"][key] = val

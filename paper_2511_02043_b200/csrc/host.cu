@@ -31,6 +31,11 @@ cudaError_t launch_rsa_summaries(const void* k, int64_t sb, int64_t sg, int64_t 
 cudaError_t launch_rsa_select(const RsaSelParams& p, const CUtensorMap& tq, const CUtensorMap& tmin,
                               const CUtensorMap& tmax, cudaStream_t stream);
 int rsa_select_max_blocks(int D);
+bool rsa_select_small_ok(const RsaSelParams& p);
+cudaError_t launch_rsa_select_small(const RsaSelParams& p, const void* q, int64_t qsb, int64_t qsg, int64_t qsh,
+                                    int64_t qss, const void* kmin, const void* kmax, cudaStream_t stream);
+size_t decode_workspace_bytes(const AttnParams& p, int n_sms);
+cudaError_t launch_attn_decode(const AttnParams& p, float* part, int n_sms, cudaStream_t stream);
 cudaError_t debug_timing(unsigned long long* out, int reset);
 }  // namespace fl
 
@@ -39,6 +44,21 @@ using namespace fl;
 namespace {
 
 constexpr size_t kSchedBytes = 256;   // persistent-scheduler counter region at the head of the workspace
+
+int device_sm_count() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+    cudaGetLastError();
+    return 148;
+  }
+  if (!cache[dev]) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) cudaGetLastError();
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
+}
 
 thread_local std::string g_err;
 thread_local int64_t g_launches = 0;
@@ -201,7 +221,10 @@ struct Prepared {
   View5 q, k, v, o, lse, bias, gate, km;
   int q_rank = 4;
   size_t keybits_bytes = 0;
-  size_t ws_bytes = 0;       // bf16: [0,256) scheduler ticket counter, then the packed key mask
+  size_t ws_bytes = 0;       // bf16: [0,256) scheduler ticket counter, then the packed key mask,
+                             // then (short-query path) the split-KV partials
+  bool decode = false;       // bf16 short-query split-KV path (decode.cu)
+  size_t decode_off = 0;
   bool empty_work = false;
   bool no_keys = false;
   bool bf16 = false;
@@ -387,7 +410,12 @@ fl_status prepare(const fl_attn_args* a, Prepared& P, bool device_ptrs) {
   p.max_sel = var.mask == FL_MASK_BLOCKLIST ? (int)var.blk_idx.size[2] : 0;
   p.n_qblk = var.mask == FL_MASK_BLOCKLIST ? (int)((Sq + var.blk_q - 1) / var.blk_q) : 0;
   p.in_dtype = P.bf16 ? 0 : 1;
+  // Short query blocks (decode, S_q <= 16): split-KV kernels instead of 128-row tensor-core tiles.
+  P.decode = P.bf16 && Sq <= 16 && maps == 1 && !P.bias.present && var.gate_mode == FL_GATE_NONE &&
+             Dqk == Dv && (Dqk == 64 || Dqk == 128) && (var.mask != FL_MASK_BLOCKLIST || var.blk_k == 128);
   P.ws_bytes = (P.bf16 ? kSchedBytes : 0) + ((P.keybits_bytes + 255) & ~size_t(255));
+  P.decode_off = P.ws_bytes;
+  if (P.decode) P.ws_bytes += (decode_workspace_bytes(p, device_sm_count()) + 255) & ~size_t(255);
   P.empty_work = B * G * Hq * Sq == 0 || Dv == 0;
   P.no_keys = Sk == 0;
   return FL_OK;
@@ -427,7 +455,11 @@ fl_status launch_prepared(Prepared& P, const fl_attn_args* a) {
     if (e != cudaSuccess) return cuda_fail(e, "pack_keymask launch");
     P.p.keybits = bits;
   }
-  if (P.bf16) {
+  if (P.bf16 && P.decode) {
+    e = launch_attn_decode(P.p, reinterpret_cast<float*>(static_cast<char*>(a->workspace) + P.decode_off),
+                           device_sm_count(), stream);
+    ++g_launches;                                       // split + combine
+  } else if (P.bf16) {
     e = launch_attn_tc(P.p, maps, stream);
   } else {
     e = launch_attn_simt(P.p, stream);
@@ -652,9 +684,6 @@ fl_status fl_rsa_select(const fl_tensor* q, const fl_tensor* kmin, const fl_tens
     if (t->rank != 3 || t->size[0] != B * G * Hkv || t->size[1] != nkb || t->size[2] != D || t->stride[2] != 1 ||
         t->stride[1] != D || t->stride[0] != nkb * D)
       return fail(FL_ERR_SHAPE_MISMATCH, "rsa_select: kmin/kmax must be contiguous [B*G*Hkv, ceil(s_k/blk_k), D]");
-  if (nkb > rsa_select_max_blocks((int)D))
-    return fail(FL_ERR_UNSUPPORTED, "rsa_select: n_kblk %lld exceeds %d at D=%lld", (long long)nkb,
-                rsa_select_max_blocks((int)D), (long long)D);
   if (topk < 0) return fail(FL_ERR_INVALID_ARGUMENT, "rsa_select: topk >= 0");
   const int64_t max_sel = blk_idx->size[2];
   if (blk_idx->dtype != FL_I32 || blk_cnt->dtype != FL_I32 || blk_idx->rank != 3 || blk_cnt->rank != 2 ||
@@ -666,6 +695,21 @@ fl_status fl_rsa_select(const fl_tensor* q, const fl_tensor* kmin, const fl_tens
   for (const void* ptr : {q->data, kmin->data, kmax->data, blk_idx->data, blk_cnt->data})
     if (!on_device(ptr)) return fail(FL_ERR_INVALID_ARGUMENT, "rsa_select: pointers must be device memory");
   if (Sq == 0 || Hq == 0) return FL_OK;
+  RsaSelParams p{};
+  p.B = (int)B; p.G = (int)G; p.Hq = (int)Hq; p.Hkv = (int)Hkv; p.grp = (int)(Hq / Hkv);
+  p.Sq = (int)Sq; p.Sk = s_k; p.D = (int)D; p.nkb = (int)nkb; p.nqb = (int)nqb; p.topk = topk;
+  p.max_sel = (int)max_sel; p.q_off = causal_align ? 0 : (int)(s_k - Sq);
+  p.blk_idx = static_cast<int32_t*>(blk_idx->data); p.blk_cnt = static_cast<int32_t*>(blk_cnt->data);
+  if (rsa_select_small_ok(p)) {                         // decode-sized query blocks: SIMT scores, one pass over summaries
+    cudaError_t e = launch_rsa_select_small(p, qv.data, qv.size[0] > 1 ? qv.stride[0] : 0,
+                                            qv.size[1] > 1 ? qv.stride[1] : 0, qv.size[2] > 1 ? qv.stride[2] : 0,
+                                            qv.stride[3], kmin->data, kmax->data, static_cast<cudaStream_t>(stream));
+    ++g_launches;
+    return e == cudaSuccess ? FL_OK : cuda_fail(e, "rsa_select_small launch");
+  }
+  if (nkb > rsa_select_max_blocks((int)D))
+    return fail(FL_ERR_UNSUPPORTED, "rsa_select: n_kblk %lld exceeds %d at D=%lld", (long long)nkb,
+                rsa_select_max_blocks((int)D), (long long)D);
   CUtensorMap tq, tmn, tmx;
   int qbg, qbb, d0, d1;
   fl_status st;
@@ -681,11 +725,6 @@ fl_status fl_rsa_select(const fl_tensor* q, const fl_tensor* kmin, const fl_tens
     sv.size[4] = t->size[2]; sv.stride[4] = 1;
     if ((st = encode_map(sv, 64, w ? &tmx : &tmn, &d0, &d1)) != FL_OK) return st;
   }
-  RsaSelParams p{};
-  p.B = (int)B; p.G = (int)G; p.Hq = (int)Hq; p.Hkv = (int)Hkv; p.grp = (int)(Hq / Hkv);
-  p.Sq = (int)Sq; p.Sk = s_k; p.D = (int)D; p.nkb = (int)nkb; p.nqb = (int)nqb; p.topk = topk;
-  p.max_sel = (int)max_sel; p.q_off = causal_align ? 0 : (int)(s_k - Sq);
-  p.blk_idx = static_cast<int32_t*>(blk_idx->data); p.blk_cnt = static_cast<int32_t*>(blk_cnt->data);
   p.q_bcast_g = qbg; p.q_bcast_b = qbb;
   cudaError_t e = launch_rsa_select(p, tq, tmn, tmx, static_cast<cudaStream_t>(stream));
   ++g_launches;

@@ -16,7 +16,7 @@ DT = {"bf16": torch.bfloat16, "f32": torch.float32}
 def admissible(case, Sq, Sk, b=0):
     """Admissible key interval [lo, hi) per query row (for needle inputs)."""
     mask = case.get("mask", "none")
-    off = Sk - Sq
+    off = 0 if case.get("causal_align") else Sk - Sq
     def f(q):
         qa = q + off
         if mask in ("causal", "blocklist"):

@@ -107,6 +107,22 @@ for D in (128, 64, 32):
     ]
 
 
+# short query blocks (S_q <= 16) take the split-KV decode kernels (decode.cu)
+for D in (128, 64):
+    BF16_CASES += [
+        dict(name=f"dec_causal_needle_D{D}", Hq=2, Sq=1, Sk=3000, D=D, mask="causal", dist="needle"),
+        dict(name=f"dec_causal_const_D{D}", B=2, Hq=2, Sq=7, Sk=5000, D=D, mask="causal", dist="constant"),
+        dict(name=f"dec_vanilla_D{D}", Hq=3, Sq=16, Sk=777, D=D),
+        dict(name=f"dec_sliding_needle_D{D}", Hq=1, Sq=3, Sk=4000, D=D, mask="sliding", window=300, dist="needle"),
+        dict(name=f"dec_alibi_needle_D{D}", Hq=4, Sq=2, Sk=1000, D=D, mod="alibi", dist="needle"),
+        dict(name=f"dec_softcap_needle_D{D}", Hq=2, Sq=1, Sk=1500, D=D, mod="softcap", softcap=20.0, dist="needle"),
+        dict(name=f"dec_gqa_needle_D{D}", Hq=8, Hkv=2, Sq=4, Sk=2000, D=D, mask="causal", dist="needle"),
+        dict(name=f"dec_keymask_const_D{D}", Hq=2, Sq=5, Sk=900, D=D, key_mask=True, p_zero=0.5, dist="constant"),
+        dict(name=f"dec_doc_const_D{D}", B=2, Hq=1, Sq=9, Sk=3000, D=D, mask="document", n_docs=5, dist="constant"),
+        dict(name=f"dec_topleft_needle_D{D}", Hq=1, Sq=12, Sk=600, D=D, mask="causal", causal_align=1, dist="needle"),
+    ]
+
+
 @pytest.mark.parametrize("case", BF16_CASES, ids=[c["name"] for c in BF16_CASES])
 def test_bf16_path(fl, case):
     ins, gk, ok = cases.build(dict(case, dtype="bf16"))
@@ -115,6 +131,17 @@ def test_bf16_path(fl, case):
     strong = case.get("dist") in ("needle", "constant")
     check(out.cpu().double().reshape(ref.shape), ref, TOL["bf16"], min_ref=0.1 if strong else 0.0,
           what=case["name"])
+
+
+def test_decode_lse_and_empty_rows(fl):
+    """split-KV path: LSE across splits (combine) and fully-masked rows (G7: O = 0, lse = -inf)."""
+    ins, gk, ok = cases.build(dict(Sq=4, Sk=3000, D=128, mask="causal", dist="needle"))
+    out, lse = cases.run_gpu(fl, ins, gk, return_lse=True)
+    ref, rl = cases.run_oracle(ins, ok)
+    check(lse.cpu().double().reshape(-1), rl, 1e-2, what="decode lse")
+    ins, gk, ok = cases.build(dict(Sq=3, Sk=700, D=64, key_mask=True, p_zero=1.0))
+    out, lse = cases.run_gpu(fl, ins, gk, return_lse=True)
+    assert (out == 0).all() and torch.isneginf(lse).all()
 
 
 def test_bf16_lse(fl):
