@@ -83,12 +83,20 @@ struct TcCfg {
   static constexpr uint32_t P_OFF = 64;              // P_i at S_i + 64
   static constexpr int SMEM_Q = 0;
   static constexpr int SMEM_RING = 2 * TILE_BYTES;
-  static constexpr int SMEM_BAR = SMEM_RING + NSLOT * TILE_BYTES;
+  // Small heads (D = 32, Evoformer) have shared memory to spare: the additive (pair) bias tiles come
+  // through TMA into a per-warpgroup double buffer (2 slabs of 128 rows x 64 keys, 128-B swizzle).
+  static constexpr bool BIAS_TMA_OK = D == 32;
+  static constexpr int BIAS_TILE = 128 * 128 * 2;
+  static constexpr int SMEM_BIAS = SMEM_RING + NSLOT * TILE_BYTES;
+  static constexpr int SMEM_BAR = SMEM_BIAS + (BIAS_TMA_OK ? 4 * BIAS_TILE : 0);
   // q_full q_empty | full[NSLOT] empty[NSLOT] | s_full[2] p_full[2] o_full[2] | unit_full[2] unit_empty[2]
-  static constexpr int NBAR = 2 + 2 * NSLOT + 6 + 4;
+  // | bias_full[4] bias_empty[4]
+  static constexpr int NBAR = 2 + 2 * NSLOT + 6 + 4 + 8;
   static constexpr int SMEM_SCHED = SMEM_BAR + NBAR * 8 + 16;       // blocklist schedule (RSA), 2 slots
   static constexpr int SCHED_WORDS = 2 * kMaxSelTc + 8;   // schedule + meta (n, lo0, hi0, lo1, hi1, ..., unit id)
-  static constexpr int SMEM_TOTAL = SMEM_SCHED + 2 * SCHED_WORDS * 4 + 1024;  // + alignment slack
+  static constexpr int SMEM_KBITS = SMEM_SCHED + 2 * SCHED_WORDS * 4;   // per-WG key-mask bits of the unit
+  static constexpr int KBITS_WORDS = 64;                                 // S_k <= 2048 staged in smem
+  static constexpr int SMEM_TOTAL = SMEM_KBITS + 2 * KBITS_WORDS * 4 + 1024;  // + alignment slack
   static constexpr uint32_t IDESC_S = idesc_bf16_f32(128, BN, 0);   // Q (K-major) x K (K-major)
   static constexpr uint32_t IDESC_O = idesc_bf16_f32(128, D, 1);    // P (TMEM) x V (MN-major)
   static constexpr int ENTRIES_PER_TILE = DIFF ? 3 : 2;              // K0 [K1] V
@@ -263,7 +271,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   uint64_t* o_full = p_full + 2;
   uint64_t* unit_full = o_full + 2;                  // work-unit broadcast (producer -> MMA, softmax), 2 slots
   uint64_t* unit_empty = unit_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(unit_empty + 2);
+  uint64_t* bias_full = unit_empty + 2;              // [wg * 2 + stage]
+  uint64_t* bias_empty = bias_full + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bias_empty + 4);
+  uint8_t* sBias = smem + C::SMEM_BIAS;
+  const bool bias_tma = C::BIAS_TMA_OK && BIAS && maps.bias_tma;
   uint32_t* sched_base = reinterpret_cast<uint32_t*>(smem + C::SMEM_SCHED);
 
   const int warp = threadIdx.x >> 5;
@@ -282,6 +294,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       mbar_init(&o_full[i], 1);
       mbar_init(&unit_full[i], 1);
       mbar_init(&unit_empty[i], 1 + 256);            // MMA lane + both softmax warpgroups
+      for (int st = 0; st < 2; ++st) {
+        mbar_init(&bias_full[i * 2 + st], 1);
+        mbar_init(&bias_empty[i * 2 + st], 128);     // the warpgroup's threads, after reading their rows
+      }
     }
     fence_mbar_init();
   }
@@ -317,6 +333,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       tma_prefetch_desc(&maps.v);
       int e = 0, it = 0;
       int u = blockIdx.x;
+      int bcnt[2] = {0, 0};                            // bias tiles issued per warpgroup (stage = bcnt & 1)
+      if (bias_tma) tma_prefetch_desc(&maps.bias);
       for (;; ++it) {
         uint32_t* sc = sched_base + (it & 1) * C::SCHED_WORDS;
         if (it >= 2) mbar_wait(&unit_empty[it & 1], ((it >> 1) - 1) & 1);
@@ -357,6 +375,20 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             for (int c = 0; c < C::NCH; ++c)
               tma_load_5d(dst + c * C::CHUNK_BYTES, m, &full[slot], c * C::CH, kv_tile<LIST>(w, j) * C::BN, head,
                           gg, bb);
+          }
+          if (bias_tma) {
+            const int gb = maps.bias_bcast_g ? 0 : w.g, bb2 = maps.bias_bcast_b ? 0 : w.b;
+            for (int i = 0; i < 2; ++i) {
+              if (!needs<LIST>(w, i, j)) continue;
+              const int st = bcnt[i] & 1;
+              if (bcnt[i] >= 2) mbar_wait(&bias_empty[i * 2 + st], ((bcnt[i] >> 1) - 1) & 1);
+              mbar_arrive_expect_tx(&bias_full[i * 2 + st], C::BIAS_TILE);
+              uint8_t* dst = sBias + (i * 2 + st) * C::BIAS_TILE;
+              for (int c = 0; c < 2; ++c)
+                tma_load_5d(dst + c * (C::BIAS_TILE / 2), &maps.bias, &bias_full[i * 2 + st],
+                            kv_tile<LIST>(w, j) * C::BN + c * 64, w.q0[i], w.h, gb, bb2);
+              ++bcnt[i];
+            }
           }
         }
         u = u_next;
@@ -465,6 +497,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     const float cap_in = MOD == MOD_SOFTCAP ? p.scale / p.softcap : 0.f;   // s*scale/cap
     const float cap_out = MOD == MOD_SOFTCAP ? p.softcap * kLog2e : 0.f;
     int s_cnt = 0, o_cnt = 0;                        // cumulative s_full / o_full phases of this WG
+    int b_cnt = 0;                                   // bias tiles consumed (TMA path)
     bool pp_started = false;                         // ping-pong: first common tile of the CTA's life seen
     int it = 0;
     for (;; ++it) {
@@ -479,6 +512,15 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     if (MOD == MOD_ALIBI)
       slope_l2 = kLog2e * (p.alibi ? p.alibi[w.h] : exp2f(-8.f * (float)(w.h + 1) / (float)p.Hq));
     const uint32_t* kbits = p.keybits ? p.keybits + ((int64_t)w.b * p.G + w.g) * p.keybits_words : nullptr;
+    // The unit's key-mask bits (Evoformer MSA mask: <= 16 words) are staged once per unit in shared
+    // memory, so no tile waits on a global load for them.
+    uint32_t* kb_smem = reinterpret_cast<uint32_t*>(smem + C::SMEM_KBITS) + wg * C::KBITS_WORDS;
+    const bool kb_staged = C::BIAS_TMA_OK && kbits && p.keybits_words <= C::KBITS_WORDS;   // small heads only
+    if (kb_staged) {
+      named_bar_sync(2 + wg, 128);                   // the warpgroup is done with the previous unit's bits
+      for (int i = r; i < p.keybits_words; i += 128) kb_smem[i] = __ldg(kbits + i);
+      named_bar_sync(2 + wg, 128);
+    }
     const unsigned char* bias_row = nullptr;
     if (BIAS)
       bias_row = static_cast<const unsigned char*>(p.bias) +
@@ -491,7 +533,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       if (!needs<LIST>(w, wg, j)) continue;
       const int k0 = kv_tile<LIST>(w, j) * 128;
       uint32_t kw[4];                                  // key-mask bits of this tile, loaded before the S wait
-      if (kbits) {
+      if (kb_staged) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) kw[t] = kb_smem[(k0 >> 5) + t];
+      } else if (kbits) {
 #pragma unroll
         for (int t = 0; t < 4; ++t) kw[t] = __ldg(kbits + (k0 >> 5) + t);
       }
@@ -523,7 +568,29 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         x[c] = v;
       }
       if (BIAS) {  // additive bias (Evoformer pair bias), then softcap if any (order G16)
-        if (p.bias_vec && k0 + 128 <= p.Sk) {
+        if (bias_tma) {
+          // this row of the bias tile from shared memory: slab c holds keys [64c, 64c+64), 16-byte
+          // chunk k of row r at (k ^ (r & 7)) -- the TMA 128-B swizzle, so 8 consecutive rows hit
+          // 8 different bank groups
+          const int st = b_cnt & 1;
+          mbar_wait(&bias_full[wg * 2 + st], (b_cnt >> 1) & 1);
+          const uint8_t* bt = sBias + (wg * 2 + st) * C::BIAS_TILE + r * 128;
+          uint4 u4[16];
+#pragma unroll
+          for (int c8 = 0; c8 < 16; ++c8)
+            u4[c8] = *reinterpret_cast<const uint4*>(bt + (c8 >> 3) * (C::BIAS_TILE / 2) + (((c8 & 7) ^ (r & 7)) << 4));
+#pragma unroll
+          for (int c8 = 0; c8 < 16; ++c8) {
+            const uint32_t ww[4] = {u4[c8].x, u4[c8].y, u4[c8].z, u4[c8].w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              x[c8 * 8 + 2 * t] = fmaf(bf16_lo(ww[t]), kLog2e, x[c8 * 8 + 2 * t]);
+              x[c8 * 8 + 2 * t + 1] = fmaf(bf16_hi(ww[t]), kLog2e, x[c8 * 8 + 2 * t + 1]);
+            }
+          }
+          mbar_arrive(&bias_empty[wg * 2 + st]);
+          ++b_cnt;
+        } else if (p.bias_vec && k0 + 128 <= p.Sk) {
           // full tile: issue 8 independent 16-byte loads before the first use (one L2 round trip
           // per half row instead of one per load)
           const uint4* br = reinterpret_cast<const uint4*>(bias_row + (int64_t)k0 * 2);

@@ -438,6 +438,12 @@ fl_status launch_prepared(Prepared& P, const fl_attn_args* a) {
     if ((s = encode_map(P.q, ch, &maps.q, &maps.q_bcast_g, &maps.q_bcast_b)) != FL_OK) return s;
     if ((s = encode_map(P.k, ch, &maps.k, &maps.k_bcast_g, &maps.k_bcast_b)) != FL_OK) return s;
     if ((s = encode_map(P.v, ch, &maps.v, &maps.v_bcast_g, &maps.v_bcast_b)) != FL_OK) return s;
+    // D = 32 kernels stage bf16 bias tiles through TMA when the view allows it (else: direct loads)
+    if (P.bias.present && P.p.bias_vec && P.p.Dqk == 32 && !P.decode) {
+      const std::string saved = g_err;
+      maps.bias_tma = encode_map(P.bias, 64, &maps.bias, &maps.bias_bcast_g, &maps.bias_bcast_b) == FL_OK;
+      g_err = saved;
+    }
   }
   if (P.ws_bytes && (!a->workspace || a->workspace_bytes < P.ws_bytes))
     return fail(FL_ERR_WORKSPACE, "this call needs %zu bytes of workspace (fl_attn_workspace_size)", P.ws_bytes);

@@ -53,6 +53,9 @@ struct TmaMaps {
   // dims whose tensor-map extent was collapsed to 1 because the view broadcasts
   // them (stride 0): the kernel passes coordinate 0 there.
   int32_t q_bcast_g, q_bcast_b, k_bcast_g, k_bcast_b, v_bcast_g, v_bcast_b;
+  // additive bias through TMA (D = 32 kernels, bf16 key-contiguous bias): dims (S_k, S_q, H, G, B)
+  CUtensorMap bias;
+  int32_t bias_tma, bias_bcast_g, bias_bcast_b;
 };
 
 // RSA block selection (rsa.cu), built by host.cu's fl_rsa_select.
