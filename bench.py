@@ -216,8 +216,9 @@ def evo_views(cfg, t):
 
 # ------------------------------------------------------------------ jobs: the calls of one step
 class Call:
-    def __init__(self, label, fn, flops=0.0, bytes_=0.0, bound="tensor", kernel=None):
+    def __init__(self, label, fn, flops=0.0, bytes_=0.0, bound="tensor", kernel=None, alu=0.0):
         self.label, self.fn, self.flops, self.bytes, self.bound = label, fn, flops, bytes_, bound
+        self.alu = alu            # MUFU ex2 operations per launch (bound == "alu")
         self.kernel = kernel or label
         self.ms = []
 
@@ -332,8 +333,10 @@ def evo_job(name, rank, world, device, with_host=True):
     flops = pairs * flops_per_pair(cfg)
     nbytes = sum(t.numel() * t.element_size() for t in dev.values()) + out.numel() * 2
     job = Job(name, f"evoformer_{cfg['evo']}_bf16_Nseq{cfg['Ns']}_Nres{cfg['Nr']}_H{cfg['H']}_c{cfg['D']}")
-    job.calls.append(Call(name, lambda: fl.attn_fwd(q, k, v, out=out, workspace=ws, **kw), flops, nbytes, "tensor",
-                          kernel="attn_tc_kernel"))
+    # c = 32: one ex2 per kept pair against 4c = 128 MMA flops, so the MUFU (16 ex2/clk/SM), not the
+    # tensor pipe, bounds the kernel (MUFU 187/250 us vs tensor 47/62 us vs HBM 77 us)
+    job.calls.append(Call(name, lambda: fl.attn_fwd(q, k, v, out=out, workspace=ws, **kw), flops, nbytes, "alu",
+                          kernel="attn_tc_kernel", alu=float(pairs)))
     job.step_flops = flops
     job.parity = {"host": host, "out": out}
 
@@ -686,8 +689,18 @@ def main():
         per_call[c.label] = d
     dom_i = int(np.argmax(call_ms))
     dom = job.calls[dom_i]
-    traffic = (prof.get(f"{job.name}:{dom.label}") or prof.get(dom.label) or {}).get("dram_bytes_per_launch")
-    if dom.bound == "hbm":
+    # ncu --set full summary of this kernel on this workload (profiles/ncu_summary.json, key "<variant>:<kernel>")
+    prof_key = f"{dom.label if job.name == 'flex' else job.name}:{dom.kernel}"
+    traffic = (prof.get(prof_key) or {}).get("dram_bytes_per_launch")
+    if dom.bound == "alu":
+        # MUFU ex2 roofline: 16 ex2/clk/SM (B200; the 2x SFU rate is sm_103a-only) x 148 SMs x max SM clock
+        mufu_peak = 16 * 148 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e9
+        ach = dom.alu / (call_ms[dom_i] * 1e-3) / 1e9
+        roof = {"bound": "alu", "achieved": ach, "peak": mufu_peak, "unit": "Gex2/s", "frac": ach / mufu_peak,
+                "traffic": traffic, "peak_derivation": "16 ex2/clk/SM x 148 SMs x sm_max_mhz (DESIGN.md)",
+                "hbm_gbs": dom.bytes / (call_ms[dom_i] * 1e-3) / 1e9, "hbm_frac": dom.bytes / (call_ms[dom_i] * 1e-3) / 1e9 / pk["hbm_gbs"],
+                "tensor_frac": dom.flops / (call_ms[dom_i] * 1e-3) / 1e12 / pk["bf16_tflops"]}
+    elif dom.bound == "hbm":
         ach = dom.bytes / (call_ms[dom_i] * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": ach / pk["hbm_gbs"],
                 "traffic": traffic, "algorithmic_bytes": dom.bytes}
@@ -696,8 +709,9 @@ def main():
         roof = {"bound": "tensor", "achieved": ach, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
                 "frac": ach / pk["bf16_tflops"], "traffic": traffic, "algorithmic_flops": dom.flops,
                 "frac_of_sustained": ach / pk.get("bf16_tflops_sustained", pk["bf16_tflops"])}
-    roof.update(kernel=dom.kernel, call=dom.label, peak_source=f"{pk_src} (MEASURED_PEAKS.json burst)",
-                launch_ms=call_ms[dom_i])
+    roof.update(kernel=dom.kernel, call=dom.label, launch_ms=call_ms[dom_i],
+                peak_source="derived (DESIGN.md §6)" if dom.bound == "alu"
+                else f"{pk_src} (MEASURED_PEAKS.json burst)")
     cfg0 = VARIANTS[SUITES.get(args.variant, [args.variant])[0]]
     line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",

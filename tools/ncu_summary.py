@@ -67,7 +67,8 @@ def full(name, rep, variant):
             out_lines.append(f"  {k:78s} {v:>16.4f} {u}")
         dr, dw = _val(vals, "dram__bytes_read.sum"), _val(vals, "dram__bytes_write.sum")
         if dr is not None and dw is not None:
-            summ = {"kernel": kname, "dram_bytes_per_launch": dr + dw,
+            short = kname.split("(")[0].replace("void ", "").split("<")[0].strip()
+            summ[short] = {"kernel": kname, "dram_bytes_per_launch": dr + dw,
                     "ncu_duration_s": _val(vals, "gpu__time_duration.sum"),
                     "tensor_pipe_pct": _val(vals, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
                     "xu_pipe_pct": _val(vals, "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
@@ -78,7 +79,10 @@ def full(name, rep, variant):
     open(os.path.join(PROF, f"{name}.txt"), "w").write("\n".join(out_lines) + "\n")
     jp = os.path.join(PROF, "ncu_summary.json")
     allj = json.load(open(jp)) if os.path.exists(jp) else {}
-    allj[variant] = summ
+    if len(summ) == 1:
+        allj[variant] = next(iter(summ.values()))
+    for short, rec in summ.items():
+        allj[f"{variant}:{short}"] = rec
     json.dump(allj, open(jp, "w"), indent=1, sort_keys=True)
     print("\n".join(out_lines))
 
