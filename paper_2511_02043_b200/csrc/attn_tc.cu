@@ -107,12 +107,14 @@ struct TcCfg {
 // ~(2 + 6 f)/128), but measured on B200 (profiles/r01_ab_*.txt) the softmax warpgroups are
 // latency/issue-bound, not MUFU-bound, and the extra ~5 instructions per emulated score cost
 // more than they save (causal 1071 -> 982 TF/s with 3/8), so the default is 0 (all MUFU).
-template <int MOD>
+template <int D, int MOD>
 struct EmuCfg {
 #ifdef FL_EMU_MASK
   static constexpr uint32_t MASK = FL_EMU_MASK;
 #else
-  static constexpr uint32_t MASK = 0u;
+  // measured (profiles/r01_ab_pingpong_emu.txt): softcap (tanh + ex2 on the MUFU) +2 % with 3/8,
+  // D = 64 (diff, 2x MUFU per flop) +1.6 % with 2/8, D = 128 plain exp: no gain -> all MUFU
+  static constexpr uint32_t MASK = MOD == MOD_SOFTCAP ? 0x4Au : (D <= 64 ? 0x11u : 0u);
 #endif
 };
 // Ping-pong of the two softmax warpgroups' exp loops on named barriers (FA3-style).  Measured
@@ -706,7 +708,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         float a0, a1, a2, a3;
         ffma2(a0, a1, x[c], x[c + 1], xscale, xscale, neg_m, neg_m);
         ffma2(a2, a3, x[c + 2], x[c + 3], xscale, xscale, neg_m, neg_m);
-        if ((EmuCfg<MOD>::MASK >> ((c >> 2) & 7)) & 1u) {
+        if ((EmuCfg<D, MOD>::MASK >> ((c >> 2) & 7)) & 1u) {
           ex2_emu2(a0, a1);
           ex2_emu2(a2, a3);
         } else {
