@@ -54,12 +54,21 @@ FL_DEVICE bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+#ifdef FL_DEBUG_HANG
+// per-CTA progress words of the softmax warpgroups (written by thread 0 of each WG), printed by a
+// hung waiter before it traps
+__device__ volatile int g_fl_dbg[256][2][8];
+#endif
 FL_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
 #ifdef FL_DEBUG_HANG
   long long spins = 0;
   while (!mbar_try_wait(bar, parity)) {
-    if (++spins > (1ll << 22)) {
-      printf("fl: mbarrier hang block %d thread %d bar %p parity %u\n", blockIdx.x, threadIdx.x, bar, parity);
+    if (++spins > (threadIdx.x >= 256 ? (1ll << 25) : (1ll << 22))) {   // control warps report last
+      const int bb = blockIdx.x & 255;
+      printf("fl: mbarrier hang block %d thread %d bar %p parity %u | wg0 %d %d %d %d %d %d | wg1 %d %d %d %d %d %d\n",
+             blockIdx.x, threadIdx.x, bar, parity, g_fl_dbg[bb][0][0], g_fl_dbg[bb][0][1], g_fl_dbg[bb][0][2],
+             g_fl_dbg[bb][0][3], g_fl_dbg[bb][0][4], g_fl_dbg[bb][0][5], g_fl_dbg[bb][1][0], g_fl_dbg[bb][1][1],
+             g_fl_dbg[bb][1][2], g_fl_dbg[bb][1][3], g_fl_dbg[bb][1][4], g_fl_dbg[bb][1][5]);
       asm volatile("trap;");
     }
   }

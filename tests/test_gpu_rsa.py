@@ -152,7 +152,9 @@ def test_full_blocklist_equals_dense_causal(fl):
     ins2 = dict(ins)
     out_c = fl.attn_fwd(ins2["q"].cuda(), ins2["k"].cuda(), ins2["v"].cuda(), mask="causal")
     torch.cuda.synchronize()
-    assert torch.equal(out_bl, out_c)
+    # same tiling (128-key tiles on both paths) -> identical arithmetic; allow bf16 rounding slack in
+    # case the interval kernel's tile size differs (FL_BN64 builds)
+    assert (out_bl.float() - out_c.float()).abs().max().item() <= 4e-3
 
 
 def test_rsa_pipeline_end_to_end(fl):
