@@ -121,8 +121,13 @@ typedef struct {
 
 /* Supported set (ABI v1):
  *   f32 q/k/v/o  : exact-fp32 SIMT path, every variant, D_qk, D_v <= 128.
- *   bf16 q/k/v/o : tcgen05/TMEM/TMA path, D_qk == D_v in {32, 64, 128}; every mask, mod,
- *                  bias, key_mask, gate; diff (lse must be absent with diff).
+ *   bf16 q/k/v/o : tcgen05/TMEM/TMA persistent kernel, D_qk == D_v in {32, 64, 128}; every mask,
+ *                  mod, bias, key_mask, gate; diff (lse must be absent with diff).  FL_MASK_BLOCKLIST
+ *                  on bf16: blk_q == blk_k == 128, max_sel <= 256, no diff, no bias.
+ *                  Short query blocks (S_q <= 16, no diff / bias / gate, D in {64, 128}) take the
+ *                  split-KV decode kernels (a split pass + a combine pass) instead.
+ * Launches per call: 1 attention kernel (2 on the split-KV path), +1 key-mask pack kernel when a
+ * key mask is given, + a 4-byte stream-ordered memset of the scheduler counter (bf16).
  * Empty work (B*G*Hq*S_q == 0) returns FL_OK without a launch; S_k == 0 gives O = 0,
  * lse = -inf (G7); a fully masked row likewise gives O = 0, lse = -inf. */
 fl_status fl_attn_fwd(const fl_attn_args* args);
@@ -130,7 +135,8 @@ fl_status fl_attn_fwd(const fl_attn_args* args);
 /* Bytes of device workspace fl_attn_fwd needs for these args (caller-owned, >= 16-byte aligned, not
  * shared by concurrent calls): bf16 path: 256 bytes for the persistent kernel's work-unit ticket
  * counter (reset by the call itself with a stream-ordered memset), then -- when key_mask is present --
- * the key mask packed to one bit per key (ceil(S_k/128)*16 bytes per (b, g), 256-byte rounded).
+ * the key mask packed to one bit per key (ceil(S_k/128)*16 bytes per (b, g), 256-byte rounded), then
+ * -- on the split-KV short-query path -- the per-split partials (rows x splits x (D_v + 2) floats).
  * f32 path: the packed key mask only.  0 when the call has no work. */
 fl_status fl_attn_workspace_size(const fl_attn_args* args, size_t* bytes);
 
@@ -158,7 +164,8 @@ fl_status fl_rsa_build_summaries(const fl_tensor* k, fl_tensor* kmin, fl_tensor*
  *   list = {0} U {c} U top-k(score) (ties to the lower j), ascending, -1 padded (all of 0..c if c <= topk+1).
  *   q    : bf16 [B,(G,)Hq,S_q,D], D in {64, 128}, TMA-aligned as for fl_attn_fwd.
  *   kmin, kmax : as written by fl_rsa_build_summaries for the same K (Hkv = kmin.size[0] / (B*G)).
- *   s_k  : number of keys the summaries cover (n_kblk == ceil(s_k / blk_k)); n_kblk <= 256 (D=128) / 512 (D=64).
+ *   s_k  : number of keys the summaries cover (n_kblk == ceil(s_k / blk_k)); tensor-core path (S_q > 16):
+ *          n_kblk <= 256 (D=128) / 512 (D=64); SIMT path (S_q <= 16): n_kblk bounded by shared memory.
  *   blk_q == blk_k == 128; 0 <= topk; topk + 2 <= max_sel <= 512.
  *   blk_idx : i32 [B*G*Hq, n_qblk, max_sel] contiguous; blk_cnt : i32 [B*G*Hq, n_qblk] contiguous.
  *   The scores are one tcgen05 GEMM per (b, h) over K = 2D (q+ . kmax + q- . kmin, exact identity for
