@@ -67,7 +67,12 @@ constexpr uint32_t kRegsLaunch = 168, kRegsCtl = 88, kRegsSoftmax = 208;
 constexpr int kMaxSelTc = 256;
 static_assert(2 * 128 * kRegsSoftmax + 128 * kRegsCtl <= kThreadsTc * kRegsLaunch, "setmaxnreg split exceeds CTA pool");
 
-template <int D, bool DIFF>
+// LIST (RSA block lists): both warpgroups work on the SAME 128-row query block and split its
+// listed KV blocks (WG0 entries 0, 2, 4, ..., WG1 entries 1, 3, 5, ...), each with its own
+// (m, l, O) partial; WG0 merges the two partials in the epilogue (the online-softmax closed
+// form, applied across the two halves of the list).  One Q tile, and step j of the
+// schedule carries two different KV tiles, so the ring holds 4 entries per step.
+template <int D, bool DIFF, bool LIST = false>
 struct TcCfg {
   static constexpr int BM = 128;                     // query rows per tile (= TMEM lanes)
   static constexpr int BN = 128;                     // keys per KV tile
@@ -76,13 +81,14 @@ struct TcCfg {
   static constexpr int NCH = D / CH;                 // swizzle chunks per row
   static constexpr int CHUNK_BYTES = BM * SWB;
   static constexpr int TILE_BYTES = BM * D * 2;
-  static constexpr int NSLOT = D == 128 ? 4 : (D == 64 ? 6 : 8);
+  static constexpr int NQ = LIST ? 1 : 2;            // Q tiles resident per unit
+  static constexpr int NSLOT = LIST ? (D == 128 ? 5 : 8) : (D == 128 ? 4 : (D == 64 ? 6 : 8));
   static constexpr uint32_t LAYOUT = SWB == 128 ? kLayoutSW128 : kLayoutSW64;
   static constexpr int SBO = 8 * SWB;                // 8-row (K-major) / 8-key (MN-major) group stride
   static constexpr uint32_t COL_S0 = 0, COL_S1 = 128, COL_O0 = 256, COL_O1 = 256 + D;
   static constexpr uint32_t P_OFF = 64;              // P_i at S_i + 64
   static constexpr int SMEM_Q = 0;
-  static constexpr int SMEM_RING = 2 * TILE_BYTES;
+  static constexpr int SMEM_RING = NQ * TILE_BYTES;
   // Small heads (D = 32, Evoformer) have shared memory to spare: the additive (pair) bias tiles come
   // through TMA into a per-warpgroup double buffer (2 slabs of 128 rows x 64 keys, 128-B swizzle).
   static constexpr bool BIAS_TMA_OK = D == 32;
@@ -96,7 +102,8 @@ struct TcCfg {
   static constexpr int SCHED_WORDS = 2 * kMaxSelTc + 8;   // schedule + meta (n, lo0, hi0, lo1, hi1, ..., unit id)
   static constexpr int SMEM_KBITS = SMEM_SCHED + 2 * SCHED_WORDS * 4;   // per-WG key-mask bits of the unit
   static constexpr int KBITS_WORDS = 64;                                 // S_k <= 2048 staged in smem
-  static constexpr int SMEM_TOTAL = SMEM_KBITS + 2 * KBITS_WORDS * 4 + 1024;  // + alignment slack
+  static constexpr int SMEM_ML = SMEM_KBITS + 2 * KBITS_WORDS * 4;      // LIST: WG1's (m, l) per row
+  static constexpr int SMEM_TOTAL = SMEM_ML + (LIST ? 2 * 128 * 4 : 0) + 1024;  // + alignment slack
   static constexpr uint32_t IDESC_S = idesc_bf16_f32(128, BN, 0);   // Q (K-major) x K (K-major)
   static constexpr uint32_t IDESC_O = idesc_bf16_f32(128, D, 1);    // P (TMEM) x V (MN-major)
   static constexpr int ENTRIES_PER_TILE = DIFF ? 3 : 2;              // K0 [K1] V
@@ -126,11 +133,11 @@ constexpr bool kPingPong = true;
 constexpr bool kPingPong = false;
 #endif
 
-// The KV tiles a CTA walks form a "schedule" indexed by t.  For every interval
-// mask (masks.cuh) t IS the KV tile index and warpgroup i needs t in [lo[i], hi[i]).
-// For the RSA block list (FL_MASK_BLOCKLIST) the two warpgroups' sorted lists are
-// merged in shared memory: sched[t] = kv tile | need0 << 30 | need1 << 31, and
-// lo/hi are the first / one-past-last schedule steps each warpgroup needs.
+// The KV tiles a CTA walks form a "schedule" indexed by step j; warpgroup i works on
+// steps [lo[i], hi[i]).  For every interval mask (masks.cuh) step j IS KV tile j.  For
+// the RSA block list (FL_MASK_BLOCKLIST) the unit is ONE query block whose cleaned,
+// ascending list sits in shared memory: step j gives KV tile sched[2j] to WG0 and
+// sched[2j+1] to WG1.
 struct Work {
   int b, g, h;
   int q0[2];            // first query row of each warpgroup's tile
@@ -143,10 +150,10 @@ struct Work {
 // (b,h)-major so the ~148 co-resident CTAs share a few heads' K/V in L2; inside a
 // head the heaviest (latest, for causal) query blocks go first, and the stride of
 // gridDim.x cycles every CTA through light and heavy blocks (static balance).
-template <int D, bool DIFF>
+template <int D, bool DIFF, bool LIST>
 __device__ __forceinline__ Work decode_work(const AttnParams& p, int u) {
   Work w;
-  const int rows_per_unit = DIFF ? 128 : 256;
+  const int rows_per_unit = (DIFF || LIST) ? 128 : 256;
   const int nqb = (p.Sq + rows_per_unit - 1) / rows_per_unit;
   const int bgh = u / nqb;
   const int qb = nqb - 1 - u % nqb;
@@ -157,9 +164,9 @@ __device__ __forceinline__ Work decode_work(const AttnParams& p, int u) {
   w.hi_cta = 0;
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
-    w.q0[i] = DIFF ? qb * 128 : qb * 256 + i * 128;
+    w.q0[i] = (DIFF || LIST) ? qb * 128 : qb * 256 + i * 128;
     w.lo[i] = w.hi[i] = 0;
-    if (w.q0[i] < p.Sq) {
+    if (!LIST && w.q0[i] < p.Sq) {
       const int q_last = min(p.Sq, w.q0[i] + 128) - 1;
       Interval iv = rows_union(p, w.b, w.q0[i], q_last);
       if (iv.hi > iv.lo) {
@@ -177,87 +184,57 @@ __device__ __forceinline__ Work decode_work(const AttnParams& p, int u) {
   return w;
 }
 
-// Blocklist mode: one thread merges the two warpgroups' sorted lists into `sched`
-// (kv tile | need bits) and stores [n, lo0, hi0, lo1, hi1] after it.  Entries
-// outside the valid key range or duplicated are dropped.
+// Blocklist mode: one thread copies the unit's list into `sched`, dropping entries
+// outside [0, nkb) and repeats (the list is ascending, fl_attn.h), and stores the
+// entry count n after it.  WG0 takes entries 0, 2, ... (ceil(n/2) steps), WG1 entries
+// 1, 3, ... (floor(n/2) steps).
 __device__ __forceinline__ void build_sched(const AttnParams& p, const Work& w, uint32_t* sched) {
   const int nkb = (p.Sk + 127) / 128;
-  const int32_t* li[2];
-  int cnt[2];
   const int64_t bgh = ((int64_t)w.b * p.G + w.g) * p.Hq + w.h;
-  for (int i = 0; i < 2; ++i) {
-    cnt[i] = 0;
-    li[i] = nullptr;
-    if (w.q0[i] < p.Sq) {
-      const int64_t row = bgh * p.n_qblk + w.q0[i] / 128;
-      li[i] = p.blk_idx + row * p.max_sel;
-      cnt[i] = min(p.blk_cnt[row], p.max_sel);
-    }
-  }
-  int a = 0, z = 0, n = 0, last = -1;
-  int lo[2] = {1 << 30, 1 << 30}, hi[2] = {0, 0};
-  while (a < cnt[0] || z < cnt[1]) {
-    const int ja = a < cnt[0] ? li[0][a] : (1 << 30), jz = z < cnt[1] ? li[1][z] : (1 << 30);
-    const int j = min(ja, jz);
-    uint32_t need = 0;
-    if (ja == j) { need |= 1u; ++a; }
-    if (jz == j) { need |= 2u; ++z; }
-    if (j < 0 || j >= nkb) continue;
-    if (j == last) {                                   // duplicate entry: merge its bits
-      sched[n - 1] |= need << 30;
-      for (int i = 0; i < 2; ++i) if (need >> i & 1u) hi[i] = n;
-      continue;
-    }
-    if (n >= 2 * kMaxSelTc) break;
-    sched[n] = (uint32_t)j | (need << 30);
-    for (int i = 0; i < 2; ++i)
-      if (need >> i & 1u) {
-        lo[i] = min(lo[i], n);
-        hi[i] = n + 1;
-      }
+  const int64_t row = bgh * p.n_qblk + w.q0[0] / 128;
+  const int32_t* li = p.blk_idx + row * p.max_sel;
+  const int cnt = min(p.blk_cnt[row], p.max_sel);
+  int n = 0, last = -1;
+  for (int a = 0; a < cnt && n < kMaxSelTc; ++a) {
+    const int j = li[a];
+    if (j < 0 || j >= nkb || j <= last) continue;
+    sched[n++] = (uint32_t)j;
     last = j;
-    ++n;
   }
-  int* meta = reinterpret_cast<int*>(sched + 2 * kMaxSelTc);
-  meta[0] = n;
-  for (int i = 0; i < 2; ++i) {
-    meta[1 + 2 * i] = hi[i] > 0 ? lo[i] : 0;
-    meta[2 + 2 * i] = hi[i];
-  }
+  reinterpret_cast<int*>(sched + 2 * kMaxSelTc)[0] = n;
 }
 
 __device__ __forceinline__ void load_sched(Work& w, const uint32_t* sched) {
-  const int* meta = reinterpret_cast<const int*>(sched + 2 * kMaxSelTc);
+  const int n = reinterpret_cast<const int*>(sched + 2 * kMaxSelTc)[0];
   w.sched = sched;
-  w.lo[0] = meta[1]; w.hi[0] = meta[2];
-  w.lo[1] = meta[3]; w.hi[1] = meta[4];
+  w.lo[0] = w.lo[1] = 0;
+  w.hi[0] = (n + 1) >> 1;
+  w.hi[1] = n >> 1;
   w.lo_cta = 0;
-  w.hi_cta = meta[0];
+  w.hi_cta = w.hi[0];
 }
 
-template <bool LIST>
 __device__ __forceinline__ bool needs(const Work& w, int i, int j) {
-  if constexpr (LIST) return (w.sched[j] >> (30 + i)) & 1u;
   // select, not w.lo[i]: a runtime index would force Work into local memory
   const int lo = i ? w.lo[1] : w.lo[0], hi = i ? w.hi[1] : w.hi[0];
   return j >= lo && j < hi;
 }
+// KV tile of warpgroup i at step j
 template <bool LIST>
-__device__ __forceinline__ int kv_tile(const Work& w, int j) {
-  if constexpr (LIST) return (int)(w.sched[j] & 0x3FFFFFFFu);
+__device__ __forceinline__ int kv_tile(const Work& w, int i, int j) {
+  if constexpr (LIST) return (int)w.sched[2 * j + i];
   return j;
 }
-template <bool LIST>
 __device__ __forceinline__ int next_tile(const Work& w, int j) {
   for (++j; j < w.hi_cta; ++j)
-    if (needs<LIST>(w, 0, j) || needs<LIST>(w, 1, j)) return j;
+    if (needs(w, 0, j) || needs(w, 1, j)) return j;
   return -1;
 }
 
 template <int D, bool DIFF, int MOD, bool BIAS, bool LIST>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     attn_tc_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ TmaMaps maps, int n_units) {
-  using C = TcCfg<D, DIFF>;
+  using C = TcCfg<D, DIFF, LIST>;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned (SW128 atoms); offset arithmetic on smem_raw keeps the shared address space visible
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -319,7 +296,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   };
   // Work of the unit published in slot it & 1 (by value: keeps it in registers)
   auto unit_work = [&](int u, int it) -> Work {
-    Work w = decode_work<D, DIFF>(p, u);
+    Work w = decode_work<D, DIFF, LIST>(p, u);
     if constexpr (LIST) load_sched(w, sched_base + (it & 1) * C::SCHED_WORDS);
     return w;
   };
@@ -345,7 +322,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           mbar_arrive(&unit_full[it & 1]);             // end marker
           break;
         }
-        Work w = decode_work<D, DIFF>(p, u);
+        Work w = decode_work<D, DIFF, LIST>(p, u);
         if constexpr (LIST) {
           build_sched(p, w, sc);
           load_sched(w, sc);
@@ -357,38 +334,47 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         const int gk = maps.k_bcast_g ? 0 : w.g, bk = maps.k_bcast_b ? 0 : w.b;
         const int gv = maps.v_bcast_g ? 0 : w.g, bv = maps.v_bcast_b ? 0 : w.b;
         if (it > 0) mbar_wait(q_empty, (it - 1) & 1);  // the previous unit's S MMAs (and diff xbuf) are done
-        mbar_arrive_expect_tx(q_full, 2 * C::TILE_BYTES);
-        for (int i = 0; i < 2; ++i) {
+        mbar_arrive_expect_tx(q_full, C::NQ * C::TILE_BYTES);
+        for (int i = 0; i < C::NQ; ++i) {
           const int qh = DIFF ? w.h + i * p.Hq : w.h;
           for (int c = 0; c < C::NCH; ++c)
             tma_load_5d(sQ + i * C::TILE_BYTES + c * C::CHUNK_BYTES, &maps.q, q_full, c * C::CH, w.q0[i], qh, gq,
                         bq);
         }
-        for (int j = next_tile<LIST>(w, w.lo_cta - 1); j >= 0; j = next_tile<LIST>(w, j)) {
-          for (int t = 0; t < C::ENTRIES_PER_TILE; ++t, ++e) {
-            const int slot = e % C::NSLOT;
-            if (e >= C::NSLOT) mbar_wait(&empty[slot], ((e / C::NSLOT) - 1) & 1);
-            mbar_arrive_expect_tx(&full[slot], C::TILE_BYTES);
-            uint8_t* dst = sRing + slot * C::TILE_BYTES;
-            const bool is_v = t == C::ENTRIES_PER_TILE - 1;
-            const CUtensorMap* m = is_v ? &maps.v : &maps.k;
-            const int head = is_v ? hkv : hkv + t * p.Hkv;
-            const int gg = is_v ? gv : gk, bb = is_v ? bv : bk;
-            for (int c = 0; c < C::NCH; ++c)
-              tma_load_5d(dst + c * C::CHUNK_BYTES, m, &full[slot], c * C::CH, kv_tile<LIST>(w, j) * C::BN, head,
-                          gg, bb);
+        auto load_entry = [&](const CUtensorMap* m, int tile, int head, int gg, int bb) {
+          const int slot = e % C::NSLOT;
+          if (e >= C::NSLOT) mbar_wait(&empty[slot], ((e / C::NSLOT) - 1) & 1);
+          mbar_arrive_expect_tx(&full[slot], C::TILE_BYTES);
+          uint8_t* dst = sRing + slot * C::TILE_BYTES;
+          for (int c = 0; c < C::NCH; ++c)
+            tma_load_5d(dst + c * C::CHUNK_BYTES, m, &full[slot], c * C::CH, tile * C::BN, head, gg, bb);
+          ++e;
+        };
+        for (int j = next_tile(w, w.lo_cta - 1); j >= 0; j = next_tile(w, j)) {
+          if constexpr (LIST) {
+            // step j: K(WG0) [K(WG1)] V(WG0) [V(WG1)] -- the order the MMA issuer acquires them
+            const bool n1 = needs(w, 1, j);
+            load_entry(&maps.k, kv_tile<LIST>(w, 0, j), hkv, gk, bk);
+            if (n1) load_entry(&maps.k, kv_tile<LIST>(w, 1, j), hkv, gk, bk);
+            load_entry(&maps.v, kv_tile<LIST>(w, 0, j), hkv, gv, bv);
+            if (n1) load_entry(&maps.v, kv_tile<LIST>(w, 1, j), hkv, gv, bv);
+          } else {
+            for (int t = 0; t < C::ENTRIES_PER_TILE; ++t) {
+              const bool is_v = t == C::ENTRIES_PER_TILE - 1;
+              load_entry(is_v ? &maps.v : &maps.k, j, is_v ? hkv : hkv + t * p.Hkv, is_v ? gv : gk, is_v ? bv : bk);
+            }
           }
           if (bias_tma) {
             const int gb = maps.bias_bcast_g ? 0 : w.g, bb2 = maps.bias_bcast_b ? 0 : w.b;
             for (int i = 0; i < 2; ++i) {
-              if (!needs<LIST>(w, i, j)) continue;
+              if (!needs(w, i, j)) continue;
               const int st = bcnt[i] & 1;
               if (bcnt[i] >= 2) mbar_wait(&bias_empty[i * 2 + st], ((bcnt[i] >> 1) - 1) & 1);
               mbar_arrive_expect_tx(&bias_full[i * 2 + st], C::BIAS_TILE);
               uint8_t* dst = sBias + (i * 2 + st) * C::BIAS_TILE;
               for (int c = 0; c < 2; ++c)
                 tma_load_5d(dst + c * (C::BIAS_TILE / 2), &maps.bias, &bias_full[i * 2 + st],
-                            kv_tile<LIST>(w, j) * C::BN + c * 64, w.q0[i], w.h, gb, bb2);
+                            kv_tile<LIST>(w, i, j) * C::BN + c * 64, w.q0[i], w.h, gb, bb2);
               ++bcnt[i];
             }
           }
@@ -408,7 +394,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         return slot;
       };
       auto issue_s = [&](int i, int kslot) {
-        const uint32_t qa = sq_addr + i * C::TILE_BYTES, ka = ring_addr + kslot * C::TILE_BYTES;
+        const uint32_t qa = sq_addr + (LIST ? 0 : i) * C::TILE_BYTES, ka = ring_addr + kslot * C::TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk * 16 / C::CH) * C::CHUNK_BYTES + (kk * 16 % C::CH) * 2;
@@ -439,40 +425,45 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         if (u >= n_units) break;
         const Work w = unit_work(u, it);
         first_pv[0] = first_pv[1] = true;
-        int j = next_tile<LIST>(w, w.lo_cta - 1);
+        int j = next_tile(w, w.lo_cta - 1);
         mbar_wait(q_full, it & 1);                     // always: Q of this unit has landed
         tc_fence_after();
         if (j >= 0) {
+          // K of warpgroup 1 is a separate ring entry for diff (map 1) and block lists (its own tile);
+          // V is separate for block lists only.  Entries a warpgroup does not need are not loaded.
+          constexpr bool kSepK = DIFF || LIST;
           int ks0 = acquire();
-          int ks1 = DIFF ? acquire() : ks0;
-          if (needs<LIST>(w, 0, j)) issue_s(0, ks0);
-          if (needs<LIST>(w, 1, j)) issue_s(1, ks1);
+          int ks1 = kSepK ? ((!LIST || needs(w, 1, j)) ? acquire() : -1) : ks0;
+          if (needs(w, 0, j)) issue_s(0, ks0);
+          if (needs(w, 1, j)) issue_s(1, ks1);
           umma_commit(&empty[ks0]);
-          if (DIFF) umma_commit(&empty[ks1]);
-          if (next_tile<LIST>(w, j) < 0) umma_commit(q_empty);   // Q is free once the last S MMA is done
+          if (kSepK && ks1 >= 0) umma_commit(&empty[ks1]);
+          if (next_tile(w, j) < 0) umma_commit(q_empty);   // Q is free once the last S MMA is done
           while (j >= 0) {
-            const int vs = acquire();
-            const int jn = next_tile<LIST>(w, j);
+            const int va = acquire();
+            const int vb = LIST ? (needs(w, 1, j) ? acquire() : -1) : va;
+            const int jn = next_tile(w, j);
             int kn0 = -1, kn1 = -1;
             if (jn >= 0) {
               kn0 = acquire();
-              kn1 = DIFF ? acquire() : kn0;
+              kn1 = kSepK ? ((!LIST || needs(w, 1, jn)) ? acquire() : -1) : kn0;
             }
-            if (needs<LIST>(w, 0, j)) {
-              issue_pv(0, vs);
+            if (needs(w, 0, j)) {
+              issue_pv(0, va);
               if (j == w.hi[0] - 1) umma_commit(&o_full[0]);
             }
-            if (jn >= 0 && needs<LIST>(w, 0, jn)) issue_s(0, kn0);
-            if (needs<LIST>(w, 1, j)) {
-              issue_pv(1, vs);
+            if (jn >= 0 && needs(w, 0, jn)) issue_s(0, kn0);
+            if (needs(w, 1, j)) {
+              issue_pv(1, vb);
               if (j == w.hi[1] - 1) umma_commit(&o_full[1]);
             }
-            umma_commit(&empty[vs]);
+            umma_commit(&empty[va]);
+            if (LIST && vb >= 0) umma_commit(&empty[vb]);
             if (jn >= 0) {
-              if (needs<LIST>(w, 1, jn)) issue_s(1, kn1);
+              if (needs(w, 1, jn)) issue_s(1, kn1);
               umma_commit(&empty[kn0]);
-              if (DIFF) umma_commit(&empty[kn1]);
-              if (next_tile<LIST>(w, jn) < 0) umma_commit(q_empty);
+              if (kSepK && kn1 >= 0) umma_commit(&empty[kn1]);
+              if (next_tile(w, jn) < 0) umma_commit(q_empty);
             }
             j = jn;
           }
@@ -501,6 +492,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     int s_cnt = 0, o_cnt = 0;                        // cumulative s_full / o_full phases of this WG
     int b_cnt = 0;                                   // bias tiles consumed (TMA path)
     bool pp_started = false;                         // ping-pong: first common tile of the CTA's life seen
+    bool o_lent = false;                             // LIST, WG1: O1 / (m, l) still being read by WG0
     int it = 0;
     for (;; ++it) {
     const int u = get_unit(it);
@@ -531,9 +523,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 
     float m_ref = -INFINITY, l = 0.f;
     int n_done = 0;
-    for (int j = next_tile<LIST>(w, w.lo_cta - 1); j >= 0; j = next_tile<LIST>(w, j)) {
-      if (!needs<LIST>(w, wg, j)) continue;
-      const int k0 = kv_tile<LIST>(w, j) * 128;
+    for (int j = next_tile(w, w.lo_cta - 1); j >= 0; j = next_tile(w, j)) {
+      if (!needs(w, wg, j)) continue;
+      const int k0 = kv_tile<LIST>(w, wg, j) * 128;
       uint32_t kw[4];                                  // key-mask bits of this tile, loaded before the S wait
       if (kb_staged) {
 #pragma unroll
@@ -693,7 +685,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       // The alternation runs across units: WG0 waits for WG1's previous common
       // tile except at the CTA's first one (and once more after its last unit);
       // WG1 signals after every common tile.
-      const bool common = kPingPong && needs<LIST>(w, 0, j) && needs<LIST>(w, 1, j);
+      const bool common = kPingPong && needs(w, 0, j) && needs(w, 1, j);
       FL_T(4);                                         // 4: O rescale
       if (common) {
         if (wg == 0 && pp_started) named_bar_sync(2, 256);
@@ -732,6 +724,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       tmem_st32(tmem + lane_base + col_s + C::P_OFF + 32, &pk[32]);
       tmem_wait_st();
       tc_fence_before();
+      if (LIST && o_lent) {                            // PV1 of this tile overwrites O1: WG0 must have read it
+        named_bar_sync(5, 256);
+        o_lent = false;
+      }
       mbar_arrive(&p_full[wg]);
       ++n_done;
       FL_T(7);                                         // 7: P store + arrive
@@ -755,8 +751,32 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       ++o_cnt;
       tc_fence_after();
     }
-    const bool empty_row = m_ref == -INFINITY || !(l > 0.f);   // G7 (emulated exps of -inf are ~2^-126, not 0)
-    const float inv_l = empty_row ? 0.f : 1.f / l;
+    bool empty_row = m_ref == -INFINITY || !(l > 0.f);   // G7 (emulated exps of -inf are ~2^-126, not 0)
+    float inv_l = empty_row ? 0.f : 1.f / l;
+    float* ml = reinterpret_cast<float*>(smem + C::SMEM_ML);   // LIST: WG1's (m, l) per row
+    float c1 = 0.f;                                  // LIST: weight of WG1's partial O1
+    if (LIST && wg == 1) {
+      if (o_lent) named_bar_sync(5, 256);            // WG0 is done with the previous unit's (m, l)
+      ml[r] = m_ref;
+      ml[128 + r] = l;
+      named_bar_arrive(4, 256);
+      o_lent = true;
+      continue;                                      // WG0 writes the merged rows
+    }
+    if (LIST) {
+      // merge the two halves of the list: O = (O0 2^(m0-m) + O1 2^(m1-m)) / (l0 2^(m0-m) + l1 2^(m1-m))
+      named_bar_sync(4, 256);
+      tc_fence_after();
+      const float m1 = ml[r], l1 = ml[128 + r];
+      const float mm = fmaxf(m_ref, m1);
+      const float a0 = m_ref == -INFINITY ? 0.f : ex2(m_ref - mm), a1 = m1 == -INFINITY ? 0.f : ex2(m1 - mm);
+      const float lt = l * a0 + l1 * a1;
+      empty_row = mm == -INFINITY || !(lt > 0.f);
+      inv_l = empty_row ? 0.f : a0 / lt;
+      c1 = empty_row ? 0.f : a1 / lt;
+      m_ref = mm;
+      l = lt;
+    }
     const float lam = DIFF ? (p.lambda_h ? p.lambda_h[w.h] : p.lambda) : 0.f;
     float* xbuf = reinterpret_cast<float*>(sQ);      // diff: map-1 rows handed to WG0 (Q is dead now)
     if (DIFF && wg == 1) {
@@ -796,6 +816,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         float f[32];
 #pragma unroll
         for (int t = 0; t < 32; ++t) f[t] = __uint_as_float(o[t]) * inv_l;
+        if (LIST && w.hi[1] > 0) {                     // WG1's partial, read from its TMEM columns (same lanes)
+          tmem_ld32(tmem + lane_base + C::COL_O1 + c, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int t = 0; t < 32; ++t) f[t] = fmaf(__uint_as_float(o[t]), c1, f[t]);
+        }
         if (DIFF) {
 #pragma unroll
           for (int t4 = 0; t4 < 8; ++t4) {
@@ -839,8 +865,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         p.lse[w.b * p.lses.b + w.g * p.lses.g + (int64_t)w.h * p.lses.h + (int64_t)q * p.lses.s] =
             empty_row ? -INFINITY : (m_ref + __log2f(l)) * kLn2;
       if (DIFF) mbar_arrive(q_empty);                 // WG0 is done reading xbuf (sQ)
+      if (LIST) named_bar_arrive(5, 256);             // WG0 is done reading O1 and (m, l)
     }
     }  // unit loop
+    if (LIST && o_lent) named_bar_sync(5, 256);
     if (wg == 0 && pp_started) named_bar_sync(2, 256);   // matches WG1's arrive after its last common tile
 #ifdef FL_TIMING
     FL_T(8);
@@ -872,20 +900,21 @@ static int num_sms() {
 
 template <int D, bool DIFF, int MOD>
 static cudaError_t launch_one(const AttnParams& p, const TmaMaps& maps, cudaStream_t stream) {
-  using C = TcCfg<D, DIFF>;
   // RSA block lists (FL_MASK_BLOCKLIST) get their own instantiation (no bias, no diff: host.cu) so the
   // interval-mask kernels keep the schedule arithmetic out of their softmax loop.
   auto kern = p.mask == MASK_BLOCKLIST ? attn_tc_kernel<D, false, MOD, false, true>
               : p.bias                 ? attn_tc_kernel<D, DIFF, MOD, true, false>
                                        : attn_tc_kernel<D, DIFF, MOD, false, false>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_TOTAL);
+  const bool list = p.mask == MASK_BLOCKLIST;
+  const int smem_bytes = list ? TcCfg<D, false, true>::SMEM_TOTAL : TcCfg<D, DIFF>::SMEM_TOTAL;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
   if (e != cudaSuccess) return e;
-  const int rows_per_unit = DIFF ? 128 : 256;
+  const int rows_per_unit = (DIFF || list) ? 128 : 256;
   const long long units = (long long)p.B * p.G * p.Hq * ((p.Sq + rows_per_unit - 1) / rows_per_unit);
   if (units >= (1ll << 31)) return cudaErrorInvalidValue;
   // persistent: one CTA per SM (TMEM and shared memory admit one), each walks units with stride grid
   const int grid = (int)std::min<long long>(units, num_sms());
-  kern<<<grid, kThreadsTc, C::SMEM_TOTAL, stream>>>(p, maps, (int)units);
+  kern<<<grid, kThreadsTc, smem_bytes, stream>>>(p, maps, (int)units);
   return cudaGetLastError();
 }
 
