@@ -21,6 +21,8 @@
 #include <cuda_bf16.h>
 #include <math.h>
 
+#include <algorithm>
+
 #include "params.h"
 #include "ptx.cuh"
 
@@ -92,6 +94,15 @@ cudaError_t launch_rsa_summaries(const void* k, int64_t sb, int64_t sg, int64_t 
 }
 
 // ------------------------------------------------------------------ selection
+// Pipelined, warp-specialised: 256 threads, one CTA per SM, each CTA a contiguous range of
+// (b, g, h_kv, q-block) pairs (x grp heads), so the summaries of a (b, g, h_kv) are loaded once
+// per CTA per head it touches.
+//   warps 4-7 ("split" WG): q+ / q- split of the landed Q tile into the operand buffers; its
+//     thread 0 also issues the TMA loads (next Q tile into a separate raw buffer, summaries)
+//     and the tcgen05 MMAs into a double-buffered TMEM accumulator;
+//   warps 0-3 ("select" WG, thread = TMEM lane = KV block): row max over the block's queries,
+//     running max over the heads of a GQA group, top-k by rank, ascending list.
+// So the split of item n+1, the MMAs of item n+1 and the selection of item n overlap.
 template <int D>
 struct SelCfg {
   static constexpr int CH = 64;                         // bf16 per 128-byte swizzle row
@@ -99,13 +110,12 @@ struct SelCfg {
   static constexpr int CHUNK = 128 * 128;               // one 128-row x 128-byte swizzle slab
   static constexpr int QTILE = NCH * CHUNK;             // one 128 x D tile
   static constexpr uint32_t IDESC = idesc_bf16_f32(128, 128, 0);
-  // summaries (kmax, kmin) + q+ (TMA lands Q here, split in place) / q- tiles + scores + flags + barriers
-  // + alignment slack
-  static int smem(int n_mt) { return 2 * n_mt * QTILE + 2 * QTILE + n_mt * 128 * 4 + 64 + 64 + 1024; }
+  // summaries (kmax, kmin) + raw Q + q+ / q- tiles + scores + flags + barriers + alignment slack
+  static int smem(int n_mt) { return 2 * n_mt * QTILE + 3 * QTILE + n_mt * 128 * 4 + 64 + 128 + 1024; }
 };
 
 template <int D>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(256, 1)
     rsa_select_kernel(const __grid_constant__ RsaSelParams p, const __grid_constant__ CUtensorMap tq,
                       const __grid_constant__ CUtensorMap tmin, const __grid_constant__ CUtensorMap tmax) {
   using C = SelCfg<D>;
@@ -113,30 +123,35 @@ __global__ void __launch_bounds__(128, 1)
   // 1024-B aligned (SW128 atoms); offset arithmetic on smem_raw keeps the shared address space visible
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int n_mt = (p.nkb + 127) / 128;
+  const int nbuf = n_mt <= 2 ? 2 : 1;                   // TMEM accumulators in flight (512 columns)
   uint8_t* sMax = smem;                                 // [n_mt][NCH] slabs
   uint8_t* sMin = sMax + n_mt * C::QTILE;
-  uint8_t* sQp = sMin + n_mt * C::QTILE;
+  uint8_t* sQraw = sMin + n_mt * C::QTILE;              // TMA destination of the next Q tile
+  uint8_t* sQp = sQraw + C::QTILE;
   uint8_t* sQn = sQp + C::QTILE;
   float* sc = reinterpret_cast<float*>(sQn + C::QTILE);  // [n_mt*128] scores
   uint32_t* flags = reinterpret_cast<uint32_t*>(sc + n_mt * 128);  // [16] selection bitmap
   uint64_t* bars = reinterpret_cast<uint64_t*>(flags + 16);
-  uint64_t* bar_sum = bars;
-  uint64_t* bar_q = bars + 1;
-  uint64_t* bar_mma = bars + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3);
+  uint64_t* bar_sum = bars;                             // summaries landed
+  uint64_t* bar_q = bars + 1;                           // raw Q tile landed
+  uint64_t* bar_qfree = bars + 2;                       // MMAs of the previous item done (q+/q-, summaries free)
+  uint64_t* mma_done = bars + 3;                        // [2] accumulator ready
+  uint64_t* acc_empty = bars + 5;                       // [2] accumulator read by the select WG
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7);
 
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const int bgk = blockIdx.x / p.parts;                  // (b, g, h_kv)
-  const int part = blockIdx.x % p.parts;
-  const int hk = bgk % p.Hkv, g = (bgk / p.Hkv) % p.G, b = bgk / (p.Hkv * p.G);
-  const int gq = p.q_bcast_g ? 0 : g, bq = p.q_bcast_b ? 0 : b;
-  const int n_blocks_mine = part < p.nqb ? (p.nqb - 1 - part) / p.parts + 1 : 0;
-  const int n_items = n_blocks_mine * p.grp;             // (q-block, head in group) pairs
+  const int64_t n_pairs = (int64_t)p.B * p.G * p.Hkv * p.nqb;
+  const int64_t pb = n_pairs * blockIdx.x / gridDim.x, pe = n_pairs * (blockIdx.x + 1) / gridDim.x;
+  const int n_items = (int)(pe - pb) * p.grp;           // (pair, head in group)
 
   if (t == 0) {
     mbar_init(bar_sum, 1);
     mbar_init(bar_q, 1);
-    mbar_init(bar_mma, 1);
+    mbar_init(bar_qfree, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&mma_done[i], 1);
+      mbar_init(&acc_empty[i], 128);
+    }
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc<512>(tmem_slot);
@@ -145,153 +160,187 @@ __global__ void __launch_bounds__(128, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  // item n -> (q-block i, head h); q-blocks interleaved over parts, heaviest (latest) first
-  auto item_qblk = [&](int n) { return p.nqb - 1 - (part + (n / p.grp) * p.parts); };
-  auto item_head = [&](int n) { return hk * p.grp + n % p.grp; };
-  auto load_q = [&](int n) {
-    mbar_arrive_expect_tx(bar_q, C::QTILE);
-    for (int c = 0; c < C::NCH; ++c)
-      tma_load_5d(sQp + c * C::CHUNK, &tq, bar_q, c * C::CH, item_qblk(n) * 128, item_head(n), gq, bq);
-  };
-  if (t == 0 && n_items > 0) {
-    tma_prefetch_desc(&tq);
-    mbar_arrive_expect_tx(bar_sum, 2 * n_mt * C::QTILE);
-    for (int m = 0; m < n_mt; ++m)
-      for (int c = 0; c < C::NCH; ++c) {
-        tma_load_5d(sMax + (m * C::NCH + c) * C::CHUNK, &tmax, bar_sum, c * C::CH, m * 128, bgk, 0, 0);
-        tma_load_5d(sMin + (m * C::NCH + c) * C::CHUNK, &tmin, bar_sum, c * C::CH, m * 128, bgk, 0, 0);
-      }
-    load_q(0);
-  }
-  if (n_items > 0) mbar_wait(bar_sum, 0);
-
-  float run0 = -INFINITY, run1 = -INFINITY, run2 = -INFINITY, run3 = -INFINITY;  // block j = m*128 + t
-  for (int n = 0; n < n_items; ++n) {
-    const int i = item_qblk(n);
-    const int h_in_grp = n % p.grp;
+  auto item_pair = [&](int n) { return pb + n / p.grp; };
+  auto item_bgk = [&](int n) { return (int)(item_pair(n) / p.nqb); };
+  auto item_qblk = [&](int n) { return (int)(item_pair(n) % p.nqb); };
+  auto item_head = [&](int n) { return (item_bgk(n) % p.Hkv) * p.grp + n % p.grp; };
+  // candidates 1 <= j < c, c = the diagonal block of the q-block's last row (reading G10)
+  auto diag = [&](int i) {
     const int q_last = min(p.Sq, (i + 1) * 128) - 1;
     const int q_last_abs = q_last + p.q_off;
-    int c = q_last_abs < 0 ? 0 : q_last_abs / 128;     // diagonal block (reading G10)
-    c = min(c, p.nkb - 1);
-    const int n_mt_i = c >= 2 ? (c - 1 + 127) / 128 : 0; // M-tiles holding candidates 1 <= j < c
-    // ---- q+ / q- split of the landed Q tile (element-wise: the swizzle is preserved)
-    mbar_wait(bar_q, n & 1);
-    {
-      const uint4* src = reinterpret_cast<const uint4*>(sQp);
-      uint4* dp = reinterpret_cast<uint4*>(sQp);
-      uint4* dn = reinterpret_cast<uint4*>(sQn);
-      const __nv_bfloat162 z = __floats2bfloat162_rn(0.f, 0.f);
-      for (int e = t; e < C::QTILE / 16; e += 128) {
-        uint4 u = src[e], up, un;
-        const __nv_bfloat162* v = reinterpret_cast<const __nv_bfloat162*>(&u);
-        __nv_bfloat162* vp = reinterpret_cast<__nv_bfloat162*>(&up);
-        __nv_bfloat162* vn = reinterpret_cast<__nv_bfloat162*>(&un);
+    const int c = q_last_abs < 0 ? 0 : q_last_abs / 128;
+    return min(c, p.nkb - 1);
+  };
+  auto n_mt_of = [&](int c) { return c >= 2 ? (c - 1 + 127) / 128 : 0; };
+
+  if (warp >= 4) {
+    // ============================== split + TMA + MMA ==============================
+    const int st = t - 128;
+    int cur_bgk = -1, sum_phase = 0;
+    auto load_q = [&](int n) {
+      const int bgk = item_bgk(n);
+      const int g = (bgk / p.Hkv) % p.G, b = bgk / (p.Hkv * p.G);
+      const int gq = p.q_bcast_g ? 0 : g, bq = p.q_bcast_b ? 0 : b;
+      mbar_arrive_expect_tx(bar_q, C::QTILE);
+      for (int c = 0; c < C::NCH; ++c)
+        tma_load_5d(sQraw + c * C::CHUNK, &tq, bar_q, c * C::CH, item_qblk(n) * 128, item_head(n), gq, bq);
+    };
+    if (st == 0 && n_items > 0) {
+      tma_prefetch_desc(&tq);
+      tma_prefetch_desc(&tmin);
+      tma_prefetch_desc(&tmax);
+      load_q(0);
+    }
+    for (int n = 0; n < n_items; ++n) {
+      mbar_wait(bar_q, n & 1);                            // raw Q(n) landed
+      if (n > 0) mbar_wait(bar_qfree, (n - 1) & 1);       // MMAs of n-1 have read q+ / q-
+      {
+        const uint4* src = reinterpret_cast<const uint4*>(sQraw);
+        uint4* dp = reinterpret_cast<uint4*>(sQp);
+        uint4* dn = reinterpret_cast<uint4*>(sQn);
+        const __nv_bfloat162 z = __floats2bfloat162_rn(0.f, 0.f);
+#pragma unroll 4
+        for (int e = st; e < C::QTILE / 16; e += 128) {
+          uint4 u = src[e], up, un;
+          const __nv_bfloat162* v = reinterpret_cast<const __nv_bfloat162*>(&u);
+          __nv_bfloat162* vp = reinterpret_cast<__nv_bfloat162*>(&up);
+          __nv_bfloat162* vn = reinterpret_cast<__nv_bfloat162*>(&un);
 #pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          vp[w] = __hmax2(v[w], z);
-          vn[w] = __hmin2(v[w], z);
+          for (int w = 0; w < 4; ++w) {
+            vp[w] = __hmax2(v[w], z);
+            vn[w] = __hmin2(v[w], z);
+          }
+          dp[e] = up;
+          dn[e] = un;
         }
-        dp[e] = up;
-        dn[e] = un;
       }
-    }
-    fence_proxy_async_smem();
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    if (t == 0) {
-      const uint32_t ap = smem_u32(sMax), an = smem_u32(sMin), bp = smem_u32(sQp), bn = smem_u32(sQn);
-      for (int m = 0; m < n_mt_i; ++m) {
-#pragma unroll
-        for (int kk = 0; kk < 2 * D / 16; ++kk) {
-          const int kd = kk % (D / 16);                  // K step within the half
-          const uint32_t off = (kd * 16 / C::CH) * C::CHUNK + (kd * 16 % C::CH) * 2;
-          const uint32_t a = (kk < D / 16 ? ap : an) + m * C::QTILE + off;
-          const uint32_t bb = (kk < D / 16 ? bp : bn) + off;
-          umma_ss(tmem + m * 128, smem_desc(a, 16, 1024, kLayoutSW128), smem_desc(bb, 16, 1024, kLayoutSW128),
-                  C::IDESC, kk > 0);
-        }
-      }
-      umma_commit(bar_mma);
-    }
-    mbar_wait(bar_mma, n & 1);
-    tc_fence_after();
-    if (t == 0 && n + 1 < n_items) load_q(n + 1);        // the MMAs have read q+ / q-: land the next Q tile
-    // ---- row max over the block's valid queries: thread t owns blocks m*128 + t
-    const int nvalid = min(128, p.Sq - i * 128);
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-    float mine[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      if (m >= n_mt_i) break;
-      float mx = -INFINITY;
-      for (int c0 = 0; c0 < 128; c0 += 32) {
-        uint32_t r[32];
-        tmem_ld32(tmem + lane_base + m * 128 + c0, r);
-        tmem_wait_ld();
-#pragma unroll
-        for (int e = 0; e < 32; ++e)
-          if (c0 + e < nvalid) mx = fmaxf(mx, __uint_as_float(r[e]));
-      }
-      mine[m] = mx;
-    }
-    if (h_in_grp == 0) {
-      run0 = mine[0]; run1 = mine[1]; run2 = mine[2]; run3 = mine[3];
-    } else {
-      run0 = fmaxf(run0, mine[0]); run1 = fmaxf(run1, mine[1]);
-      run2 = fmaxf(run2, mine[2]); run3 = fmaxf(run3, mine[3]);
-    }
-    if (h_in_grp == p.grp - 1) {
-      // ---- top-k by rank over candidates 1 <= j < c (ties toward the lower j, G11)
-      const float runs[4] = {run0, run1, run2, run3};
-#pragma unroll
-      for (int m = 0; m < 4; ++m)
-        if (m < n_mt) sc[m * 128 + t] = runs[m];
-      if (t < 16) flags[t] = 0u;
-      __syncthreads();
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int j = m * 128 + t;
-        bool sel = false;
-        if (j < p.nkb && j <= c) {
-          if (j == 0 || j == c) {
-            sel = true;
-          } else {
-            const float s = sc[j];
-            int rank = 0;
-            for (int jj = 1; jj < c; ++jj) {
-              const float o = sc[jj];
-              rank += (o > s) || (o == s && jj < j);
+      fence_proxy_async_smem();                           // generic writes -> tensor-core reads
+      named_bar_sync(1, 128);
+      if (st == 0) {
+        if (n + 1 < n_items) load_q(n + 1);               // the raw buffer has been read
+        const int bgk = item_bgk(n);
+        if (bgk != cur_bgk) {                             // MMAs of n-1 are done (bar_qfree above)
+          mbar_arrive_expect_tx(bar_sum, 2 * n_mt * C::QTILE);
+          for (int m = 0; m < n_mt; ++m)
+            for (int c = 0; c < C::NCH; ++c) {
+              tma_load_5d(sMax + (m * C::NCH + c) * C::CHUNK, &tmax, bar_sum, c * C::CH, m * 128, bgk, 0, 0);
+              tma_load_5d(sMin + (m * C::NCH + c) * C::CHUNK, &tmin, bar_sum, c * C::CH, m * 128, bgk, 0, 0);
             }
-            sel = rank < p.topk;
+          mbar_wait(bar_sum, sum_phase & 1);
+          ++sum_phase;
+          cur_bgk = bgk;
+        }
+        const int buf = n % nbuf;
+        if (n >= nbuf) mbar_wait(&acc_empty[buf], ((n / nbuf) - 1) & 1);
+        tc_fence_after();
+        const int n_mt_i = n_mt_of(diag(item_qblk(n)));
+        const uint32_t acc = tmem + buf * n_mt * 128;
+        const uint32_t ap = smem_u32(sMax), an = smem_u32(sMin), bp = smem_u32(sQp), bn = smem_u32(sQn);
+        for (int m = 0; m < n_mt_i; ++m) {
+#pragma unroll
+          for (int kk = 0; kk < 2 * D / 16; ++kk) {
+            const int kd = kk % (D / 16);                  // K step within the half
+            const uint32_t off = (kd * 16 / C::CH) * C::CHUNK + (kd * 16 % C::CH) * 2;
+            const uint32_t a = (kk < D / 16 ? ap : an) + m * C::QTILE + off;
+            const uint32_t bb = (kk < D / 16 ? bp : bn) + off;
+            umma_ss(acc + m * 128, smem_desc(a, 16, 1024, kLayoutSW128), smem_desc(bb, 16, 1024, kLayoutSW128),
+                    C::IDESC, kk > 0);
           }
         }
-        const uint32_t bal = __ballot_sync(0xffffffffu, sel);
-        if (lane == 0) flags[m * 4 + warp] = bal;
+        umma_commit(&mma_done[buf]);
+        umma_commit(bar_qfree);
       }
-      __syncthreads();
-      int cnt = 0;
-      for (int w = 0; w < 16; ++w) cnt += __popc(flags[w]);
-      for (int hh = 0; hh < p.grp; ++hh) {
-        const int64_t row = (((int64_t)b * p.G + g) * p.Hq + hk * p.grp + hh) * p.nqb + i;
-        int32_t* out = p.blk_idx + row * p.max_sel;
+    }
+  } else {
+    // ============================== selection (thread = KV block) ==============================
+    float run0 = -INFINITY, run1 = -INFINITY, run2 = -INFINITY, run3 = -INFINITY;  // block j = m*128 + t
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    for (int n = 0; n < n_items; ++n) {
+      const int i = item_qblk(n);
+      const int bgk = item_bgk(n);
+      const int hk = bgk % p.Hkv, g = (bgk / p.Hkv) % p.G, b = bgk / (p.Hkv * p.G);
+      const int h_in_grp = n % p.grp;
+      const int c = diag(i);
+      const int n_mt_i = n_mt_of(c);
+      const int buf = n % nbuf;
+      mbar_wait(&mma_done[buf], (n / nbuf) & 1);
+      tc_fence_after();
+      // ---- row max over the block's valid queries: thread t owns blocks m*128 + t
+      const int nvalid = min(128, p.Sq - i * 128);
+      const uint32_t acc = tmem + buf * n_mt * 128;
+      float mine[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        if (m >= n_mt_i) break;
+        float mx = -INFINITY;
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(acc + lane_base + m * 128 + c0, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (c0 + e < nvalid) mx = fmaxf(mx, __uint_as_float(r[e]));
+        }
+        mine[m] = mx;
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[buf]);                       // the accumulator may take item n + nbuf
+      if (h_in_grp == 0) {
+        run0 = mine[0]; run1 = mine[1]; run2 = mine[2]; run3 = mine[3];
+      } else {
+        run0 = fmaxf(run0, mine[0]); run1 = fmaxf(run1, mine[1]);
+        run2 = fmaxf(run2, mine[2]); run3 = fmaxf(run3, mine[3]);
+      }
+      if (h_in_grp == p.grp - 1) {
+        // ---- top-k by rank over candidates 1 <= j < c (ties toward the lower j, G11)
+        const float runs[4] = {run0, run1, run2, run3};
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+          if (m < n_mt) sc[m * 128 + t] = runs[m];
+        if (t < 16) flags[t] = 0u;
+        named_bar_sync(2, 128);
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
           const int j = m * 128 + t;
-          const int w = j >> 5;
-          if (m < n_mt && ((flags[w] >> (j & 31)) & 1u)) {
-            int pos = __popc(flags[w] & ((1u << (j & 31)) - 1u));
-            for (int ww = 0; ww < w; ++ww) pos += __popc(flags[ww]);
-            if (pos < p.max_sel) out[pos] = j;
+          bool sel = false;
+          if (j < p.nkb && j <= c) {
+            if (j == 0 || j == c) {
+              sel = true;
+            } else {
+              const float s = sc[j];
+              int rank = 0;
+              for (int jj = 1; jj < c; ++jj) {
+                const float o = sc[jj];
+                rank += (o > s) || (o == s && jj < j);
+              }
+              sel = rank < p.topk;
+            }
           }
+          const uint32_t bal = __ballot_sync(0xffffffffu, sel);
+          if (lane == 0) flags[m * 4 + warp] = bal;
         }
-        for (int e = cnt + t; e < p.max_sel; e += 128) out[e] = -1;
-        if (t == 0) p.blk_cnt[row] = min(cnt, p.max_sel);
+        named_bar_sync(2, 128);
+        int cnt = 0;
+        for (int w = 0; w < 16; ++w) cnt += __popc(flags[w]);
+        for (int hh = 0; hh < p.grp; ++hh) {
+          const int64_t row = (((int64_t)b * p.G + g) * p.Hq + hk * p.grp + hh) * p.nqb + i;
+          int32_t* out = p.blk_idx + row * p.max_sel;
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            const int j = m * 128 + t;
+            const int w = j >> 5;
+            if (m < n_mt && ((flags[w] >> (j & 31)) & 1u)) {
+              int pos = __popc(flags[w] & ((1u << (j & 31)) - 1u));
+              for (int ww = 0; ww < w; ++ww) pos += __popc(flags[ww]);
+              if (pos < p.max_sel) out[pos] = j;
+            }
+          }
+          for (int e = cnt + t; e < p.max_sel; e += 128) out[e] = -1;
+          if (t == 0) p.blk_cnt[row] = min(cnt, p.max_sel);
+        }
+        named_bar_sync(2, 128);                           // sc / flags reuse
       }
     }
-    tc_fence_before();
-    __syncthreads();                                      // sc/flags reuse; TMEM reads done before next MMA
-    tc_fence_after();
   }
   tc_fence_before();
   __syncthreads();
@@ -304,21 +353,24 @@ int rsa_select_max_blocks(int D) { return D == 128 ? 256 : 512; }
 cudaError_t launch_rsa_select(const RsaSelParams& p0, const CUtensorMap& tq, const CUtensorMap& tmin,
                               const CUtensorMap& tmax, cudaStream_t stream) {
   RsaSelParams p = p0;
-  const int units = p.B * p.G * p.Hkv;
-  int parts = (148 * 2 + units - 1) / units;
-  parts = parts < 1 ? 1 : (parts > p.nqb ? p.nqb : parts);
-  p.parts = parts;
+  p.parts = 1;
+  const long long pairs = (long long)p.B * p.G * p.Hkv * p.nqb;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::min<long long>(pairs, sms > 0 ? sms : 148);   // persistent: one CTA per SM
+  if (grid <= 0) return cudaSuccess;
   const int n_mt = (p.nkb + 127) / 128;
   if (p.D == 128) {
     const int sm = SelCfg<128>::smem(n_mt);
     cudaError_t e = cudaFuncSetAttribute(rsa_select_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     if (e != cudaSuccess) return e;
-    rsa_select_kernel<128><<<units * parts, 128, sm, stream>>>(p, tq, tmin, tmax);
+    rsa_select_kernel<128><<<grid, 256, sm, stream>>>(p, tq, tmin, tmax);
   } else {
     const int sm = SelCfg<64>::smem(n_mt);
     cudaError_t e = cudaFuncSetAttribute(rsa_select_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     if (e != cudaSuccess) return e;
-    rsa_select_kernel<64><<<units * parts, 128, sm, stream>>>(p, tq, tmin, tmax);
+    rsa_select_kernel<64><<<grid, 256, sm, stream>>>(p, tq, tmin, tmax);
   }
   return cudaGetLastError();
 }
