@@ -100,9 +100,8 @@ struct TcCfg {
   static constexpr int NBAR = 2 + 2 * NSLOT + 6 + 4 + 8;
   static constexpr int SMEM_SCHED = SMEM_BAR + NBAR * 8 + 16;       // blocklist schedule (RSA), 2 slots
   static constexpr int SCHED_WORDS = 2 * kMaxSelTc + 8;   // schedule + meta (n, lo0, hi0, lo1, hi1, ..., unit id)
-  static constexpr int SMEM_KBITS = SMEM_SCHED + 2 * SCHED_WORDS * 4;   // per-WG key-mask bits of the unit
-  static constexpr int KBITS_WORDS = 64;                                 // S_k <= 2048 staged in smem
-  static constexpr int SMEM_ML = SMEM_KBITS + 2 * KBITS_WORDS * 4;      // LIST: WG1's (m, l) per row
+  static constexpr int KBITS_WORDS = 64;             // small heads: key-mask bits (S_k <= 2048) in the unit slot
+  static constexpr int SMEM_ML = SMEM_SCHED + 2 * SCHED_WORDS * 4;      // LIST: WG1's (m, l) per row
   static constexpr int SMEM_TOTAL = SMEM_ML + (LIST ? 2 * 128 * 4 : 0) + 1024;  // + alignment slack
   static constexpr uint32_t IDESC_S = idesc_bf16_f32(128, BN, 0);   // Q (K-major) x K (K-major)
   static constexpr uint32_t IDESC_O = idesc_bf16_f32(128, D, 1);    // P (TMEM) x V (MN-major)
@@ -326,6 +325,19 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         if constexpr (LIST) {
           build_sched(p, w, sc);
           load_sched(w, sc);
+        } else if (C::BIAS_TMA_OK && p.keybits && p.keybits_words <= C::KBITS_WORDS) {
+          // small heads: the unit's key-mask bits (Evoformer MSA mask, <= 64 words) ride in the unit
+          // slot, so the softmax warpgroups never wait on a global load for them
+          const uint32_t* kb = p.keybits + ((int64_t)w.b * p.G + w.g) * p.keybits_words;
+          for (int i0 = 0; i0 < p.keybits_words; i0 += 16) {   // 16 loads in flight per batch
+            uint32_t tmp[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (i0 + i < p.keybits_words) tmp[i] = __ldg(kb + i0 + i);
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (i0 + i < p.keybits_words) sc[i0 + i] = tmp[i];
+          }
         }
         mbar_arrive(&unit_full[it & 1]);               // release: id / schedule visible to the waiters
         const int u_next = (int)gridDim.x + atomicAdd(p.tile_ctr, 1);   // latency hidden behind this unit
@@ -497,6 +509,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     for (;; ++it) {
     const int u = get_unit(it);
     if (u >= n_units) break;
+    FL_T(11);                                        // 11: waiting for the next unit id
     const Work w = unit_work(u, it);
     const int q = (wg ? w.q0[1] : w.q0[0]) + r;
     const bool row_valid = q < p.Sq;
@@ -508,13 +521,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     const uint32_t* kbits = p.keybits ? p.keybits + ((int64_t)w.b * p.G + w.g) * p.keybits_words : nullptr;
     // The unit's key-mask bits (Evoformer MSA mask: <= 16 words) are staged once per unit in shared
     // memory, so no tile waits on a global load for them.
-    uint32_t* kb_smem = reinterpret_cast<uint32_t*>(smem + C::SMEM_KBITS) + wg * C::KBITS_WORDS;
-    const bool kb_staged = C::BIAS_TMA_OK && kbits && p.keybits_words <= C::KBITS_WORDS;   // small heads only
-    if (kb_staged) {
-      named_bar_sync(2 + wg, 128);                   // the warpgroup is done with the previous unit's bits
-      for (int i = r; i < p.keybits_words; i += 128) kb_smem[i] = __ldg(kbits + i);
-      named_bar_sync(2 + wg, 128);
-    }
+    // small heads: staged in the unit slot by the producer (read before release_unit)
+    const uint32_t* kb_smem = sched_base + (it & 1) * C::SCHED_WORDS;
+    const bool kb_staged = !LIST && C::BIAS_TMA_OK && kbits && p.keybits_words <= C::KBITS_WORDS;
+    FL_T(12);                                        // 12: unit setup (work decode, key-mask staging)
     const unsigned char* bias_row = nullptr;
     if (BIAS)
       bias_row = static_cast<const unsigned char*>(p.bias) +
@@ -548,7 +558,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       FL_T(2);                                         // 2: tcgen05.ld of S
       // ---- score modification (Eq.4) in the log2 domain: x = log2(e) * mod(scale * s)
       float x[128];
-      constexpr bool kRaw = MOD == MOD_NONE && !BIAS;  // keep raw s; scale folds into the exp FFMA
+      // kRaw: keep raw s (an additive bias enters as bias / scale); scale * log2(e) folds into the exp FFMA
+      constexpr bool kRaw = MOD == MOD_NONE;
+      const float bias_k = kRaw ? 1.f / p.scale : kLog2e;
       const float alibi_base = slope_l2 * (float)(k0 - q_abs);
 #pragma unroll
       for (int c = 0; c < 128; ++c) {
@@ -567,19 +579,29 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           // chunk k of row r at (k ^ (r & 7)) -- the TMA 128-B swizzle, so 8 consecutive rows hit
           // 8 different bank groups
           const int st = b_cnt & 1;
+          FL_T(3);
           mbar_wait(&bias_full[wg * 2 + st], (b_cnt >> 1) & 1);
+          FL_T(9);                                     // 9: waiting for the pair-bias tile
           const uint8_t* bt = sBias + (wg * 2 + st) * C::BIAS_TILE + r * 128;
-          uint4 u4[16];
 #pragma unroll
-          for (int c8 = 0; c8 < 16; ++c8)
-            u4[c8] = *reinterpret_cast<const uint4*>(bt + (c8 >> 3) * (C::BIAS_TILE / 2) + (((c8 & 7) ^ (r & 7)) << 4));
+#ifdef FL_ABL_BIAS
+          if (false)
+#endif
+          for (int b4 = 0; b4 < 4; ++b4) {             // 4 batches of 4 x 16 B: no spills in the score loop
+            uint4 u4[4];
 #pragma unroll
-          for (int c8 = 0; c8 < 16; ++c8) {
-            const uint32_t ww[4] = {u4[c8].x, u4[c8].y, u4[c8].z, u4[c8].w};
+            for (int e = 0; e < 4; ++e) {
+              const int c8 = b4 * 4 + e;
+              u4[e] = *reinterpret_cast<const uint4*>(bt + (c8 >> 3) * (C::BIAS_TILE / 2) + (((c8 & 7) ^ (r & 7)) << 4));
+            }
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              x[c8 * 8 + 2 * t] = fmaf(bf16_lo(ww[t]), kLog2e, x[c8 * 8 + 2 * t]);
-              x[c8 * 8 + 2 * t + 1] = fmaf(bf16_hi(ww[t]), kLog2e, x[c8 * 8 + 2 * t + 1]);
+            for (int e = 0; e < 4; ++e) {
+              const int c8 = b4 * 4 + e;
+              const uint32_t ww[4] = {u4[e].x, u4[e].y, u4[e].z, u4[e].w};
+#pragma unroll
+              for (int t = 0; t < 4; ++t)
+                ffma2(x[c8 * 8 + 2 * t], x[c8 * 8 + 2 * t + 1], bf16_lo(ww[t]), bf16_hi(ww[t]), bias_k, bias_k,
+                      x[c8 * 8 + 2 * t], x[c8 * 8 + 2 * t + 1]);
             }
           }
           mbar_arrive(&bias_empty[wg * 2 + st]);
@@ -599,8 +621,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 #pragma unroll
               for (int t = 0; t < 4; ++t) {
                 const int c = (h8 * 8 + c8) * 8 + 2 * t;
-                x[c] = fmaf(bf16_lo(ww[t]), kLog2e, x[c]);
-                x[c + 1] = fmaf(bf16_hi(ww[t]), kLog2e, x[c + 1]);
+                x[c] = fmaf(bf16_lo(ww[t]), bias_k, x[c]);
+                x[c + 1] = fmaf(bf16_hi(ww[t]), bias_k, x[c + 1]);
               }
             }
           }
@@ -616,7 +638,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             }
 #pragma unroll
             for (int t = 0; t < 32; ++t)
-              x[h8 * 32 + t] = fmaf(__uint_as_float((uint32_t)us[t] << 16), kLog2e, x[h8 * 32 + t]);
+              x[h8 * 32 + t] = fmaf(__uint_as_float((uint32_t)us[t] << 16), bias_k, x[h8 * 32 + t]);
           }
         } else {
 #pragma unroll
@@ -627,7 +649,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                     ? reinterpret_cast<const float*>(bias_row)[(int64_t)k * p.bs.d]
                     : __uint_as_float((uint32_t)reinterpret_cast<const unsigned short*>(bias_row)[(int64_t)k * p.bs.d]
                                       << 16);
-            x[c] = fmaf(bv, kLog2e, x[c]);
+            x[c] = fmaf(bv, bias_k, x[c]);
           }
         }
         if (MOD == MOD_SOFTCAP) {
@@ -644,7 +666,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           x[c] = (k >= iv.lo && k < iv.hi) ? x[c] : -INFINITY;
         }
       }
-      if (kbits) {
+      // key mask: the words are the same for every row (warp-uniform), so fully kept tiles skip it
+      if (kbits && (kw[0] & kw[1] & kw[2] & kw[3]) != 0xFFFFFFFFu) {
 #pragma unroll
         for (int c = 0; c < 128; ++c) x[c] = ((kw[c >> 5] >> (c & 31)) & 1u) ? x[c] : -INFINITY;
       }
@@ -737,7 +760,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     // ============================== epilogue ==============================
     // O_i of the next unit is first written by PV_i(next, first), which waits for this
     // warpgroup's p_full of that tile -- i.e. after this epilogue has read O_i.
+#ifndef FL_ABL_GATE
     const bool gated = p.gate_mode != GATE_NONE && row_valid && !(DIFF && wg == 1);
+#else
+    const bool gated = false;
+#endif
     const uint4* gp = reinterpret_cast<const uint4*>(static_cast<const unsigned short*>(p.gate) + w.b * p.gs.b +
                                                      w.g * p.gs.g + (int64_t)w.h * p.gs.h + (int64_t)q * p.gs.s);
     constexpr bool kGateEarly = D <= 32;               // small head: the whole gate row is 4 registers x 4
@@ -844,9 +871,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
               float g0 = bf16_lo(ww[t]), g1 = bf16_hi(ww[t]);
-              if (p.gate_mode == GATE_SIGMOID) {           // sigma(g) = 1 / (1 + 2^(-g log2 e))
-                g0 = __fdividef(1.f, 1.f + ex2(-g0 * kLog2e));
-                g1 = __fdividef(1.f, 1.f + ex2(-g1 * kLog2e));
+              if (p.gate_mode == GATE_SIGMOID) {           // sigma(g) = (1 + tanh(g/2)) / 2: one MUFU op
+                g0 = fmaf(0.5f, tanh_approx(0.5f * g0), 0.5f);
+                g1 = fmaf(0.5f, tanh_approx(0.5f * g1), 0.5f);
               }
               f[t8 * 8 + 2 * t] *= g0;
               f[t8 * 8 + 2 * t + 1] *= g1;
@@ -867,13 +894,14 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       if (DIFF) mbar_arrive(q_empty);                 // WG0 is done reading xbuf (sQ)
       if (LIST) named_bar_arrive(5, 256);             // WG0 is done reading O1 and (m, l)
     }
+    FL_T(10);                                        // 10: epilogue
     }  // unit loop
     if (LIST && o_lent) named_bar_sync(5, 256);
     if (wg == 0 && pp_started) named_bar_sync(2, 256);   // matches WG1's arrive after its last common tile
 #ifdef FL_TIMING
     FL_T(8);
     if (r == 0) {
-      for (int i = 0; i < 9; ++i) atomicAdd(&g_fl_timing[wg][i], (unsigned long long)t_acc[i]);
+      for (int i = 0; i < 13; ++i) atomicAdd(&g_fl_timing[wg][i], (unsigned long long)t_acc[i]);
       atomicAdd(&g_fl_timing[wg][15], (unsigned long long)s_cnt);
     }
 #endif

@@ -1,0 +1,7 @@
+# Evoformer iteration: parity (evoformer + key-mask cases), bench evo_row/evo_col, optional timing probe
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+timeout 600 python -m pytest tests -q -m gpu -x -k "evo or Evo or key_mask or gate or bias or small" > gpurun_out/pytest_evo.txt 2>&1; echo "evo tests rc=$?"; tail -3 gpurun_out/pytest_evo.txt
+for v in ${BENCH_VARIANTS:-evo_row evo_col}; do
+  timeout 300 python bench.py --variant $v --steps 20 --no-cpu-baseline --no-e2e > gpurun_out/bench_$v.json 2> gpurun_out/bench_$v.err; echo "$v rc=$?"; tail -3 gpurun_out/bench_$v.err | grep -i error; python -c "import json,sys;d=json.loads(open('gpurun_out/bench_$v.json').read().strip().splitlines()[-1]);print('$v', round(d['value'],1), 'ms', round(d['ms_per_step'],4), d['roofline']['frac'])" 2>/dev/null
+done
+if [ -n "$PROBE" ]; then PROBE_VARIANTS="${BENCH_VARIANTS:-evo_row evo_col}" bash tools/gpu_timing.sh > /dev/null 2>&1; cat gpurun_out/timing_probe.txt; fi

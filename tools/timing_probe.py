@@ -16,7 +16,7 @@ import bench  # noqa: E402
 from paper_2511_02043_b200 import _lib, fl  # noqa: E402
 
 NAMES = ["bookkeeping", "S wait", "S tmem.ld", "score+mask+max", "O rescale", "ping-pong wait", "exp loop",
-         "P store+arrive", "tail"]
+         "P store+arrive", "tail", "bias wait", "epilogue", "unit id wait", "unit setup"]
 
 
 def main():
@@ -39,7 +39,7 @@ def main():
         print(f"== {v}: {ms:.3f} ms (timing build), {call.flops / ms / 1e9:.1f} TFLOP/s")
         for wg in range(2):
             tiles = buf[wg * 16 + 15]
-            tot = sum(buf[wg * 16 + i] for i in range(9))
+            tot = sum(buf[wg * 16 + i] for i in range(13))
             print(f"  WG{wg}: {tiles} tiles (thread 0 of each CTA, summed), {tot / max(tiles, 1):.0f} cycles/tile")
             for i, n in enumerate(NAMES):
                 c = buf[wg * 16 + i]
