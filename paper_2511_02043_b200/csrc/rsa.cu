@@ -110,8 +110,10 @@ struct SelCfg {
   static constexpr int CHUNK = 128 * 128;               // one 128-row x 128-byte swizzle slab
   static constexpr int QTILE = NCH * CHUNK;             // one 128 x D tile
   static constexpr uint32_t IDESC = idesc_bf16_f32(128, 128, 0);
-  // summaries (kmax, kmin) + raw Q + q+ / q- tiles + scores + flags + barriers + alignment slack
-  static int smem(int n_mt) { return 2 * n_mt * QTILE + 3 * QTILE + n_mt * 128 * 4 + 64 + 128 + 1024; }
+  // summaries (kmax, kmin) + raw Q + q+ / q- tiles + radix-select scratch (256-bin histogram + state)
+  // + flags + barriers + alignment slack
+  static constexpr int SCRATCH = 256 * 4 + 64;
+  static int smem(int n_mt) { return 2 * n_mt * QTILE + 3 * QTILE + SCRATCH + 64 + 128 + 1024; }
 };
 
 template <int D>
@@ -129,8 +131,9 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t* sQraw = sMin + n_mt * C::QTILE;              // TMA destination of the next Q tile
   uint8_t* sQp = sQraw + C::QTILE;
   uint8_t* sQn = sQp + C::QTILE;
-  float* sc = reinterpret_cast<float*>(sQn + C::QTILE);  // [n_mt*128] scores
-  uint32_t* flags = reinterpret_cast<uint32_t*>(sc + n_mt * 128);  // [16] selection bitmap
+  uint32_t* hist = reinterpret_cast<uint32_t*>(sQn + C::QTILE);  // [256] radix-select histogram
+  uint32_t* rstate = hist + 256;                        // [16] digit / counts of the current pass
+  uint32_t* flags = hist + C::SCRATCH / 4;              // [16] selection bitmap
   uint64_t* bars = reinterpret_cast<uint64_t*>(flags + 16);
   uint64_t* bar_sum = bars;                             // summaries landed
   uint64_t* bar_q = bars + 1;                           // raw Q tile landed
@@ -292,28 +295,106 @@ __global__ void __launch_bounds__(256, 1)
         run2 = fmaxf(run2, mine[2]); run3 = fmaxf(run3, mine[3]);
       }
       if (h_in_grp == p.grp - 1) {
-        // ---- top-k by rank over candidates 1 <= j < c (ties toward the lower j, G11)
+        // ---- top-k over candidates 1 <= j < c (ties toward the lower j, G11) by an exact radix select:
+        // order-preserving 32-bit keys of the scores, MSB-first 8-bit digits with a 256-bin histogram
+        // per pass, stopping once the threshold bin is taken whole; exact ties at the threshold go to
+        // the lowest j.  Thread t holds the scores of blocks m*128 + t in registers.
         const float runs[4] = {run0, run1, run2, run3};
+        uint32_t key[4];
+        bool cand[4];
 #pragma unroll
-        for (int m = 0; m < 4; ++m)
-          if (m < n_mt) sc[m * 128 + t] = runs[m];
+        for (int m = 0; m < 4; ++m) {
+          const int j = m * 128 + t;
+          cand[m] = m < n_mt && j >= 1 && j < c;
+          const uint32_t bits = __float_as_uint(runs[m] + 0.f);     // -0 -> +0 (equal scores tie)
+          key[m] = bits ^ ((bits >> 31) ? 0xFFFFFFFFu : 0x80000000u);
+        }
+        const int ncand = c >= 2 ? c - 1 : 0;
+        const bool take_all = ncand <= p.topk, take_none = p.topk <= 0;
+        uint32_t P = 0u, M = 0u;
+        int krem = p.topk;
+        if (!take_all && !take_none) {
+          for (int pass = 0; pass < 4; ++pass) {
+            const int shift = 24 - 8 * pass;
+            hist[t] = 0u;
+            hist[t + 128] = 0u;
+            named_bar_sync(2, 128);
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+              if (cand[m] && (key[m] & M) == P) atomicAdd(&hist[(key[m] >> shift) & 255u], 1u);
+            named_bar_sync(2, 128);
+            if (warp == 0) {                              // lane l owns bins [8l, 8l + 8); count from the top
+              uint32_t cnts[8], lsum = 0u;
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                cnts[e] = hist[8 * lane + e];
+                lsum += cnts[e];
+              }
+              uint32_t suf = lsum;                        // keys in bins of lanes >= lane
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_down_sync(0xffffffffu, suf, o);
+                if (lane + o < 32) suf += v;
+              }
+              const uint32_t above = suf - lsum;
+              if (above < (uint32_t)krem && (uint32_t)krem <= suf) {
+                uint32_t acc = above, d = 0u, in_bin = 0u;
+                bool found = false;
+#pragma unroll
+                for (int e = 7; e >= 0; --e) {
+                  if (!found && acc + cnts[e] >= (uint32_t)krem) {
+                    d = 8u * lane + e;
+                    in_bin = cnts[e];
+                    found = true;
+                  } else if (!found) {
+                    acc += cnts[e];
+                  }
+                }
+                rstate[0] = d;
+                rstate[1] = acc;                          // keys above the threshold digit
+                rstate[2] = in_bin;
+              }
+            }
+            named_bar_sync(2, 128);
+            const uint32_t d = rstate[0];
+            krem -= (int)rstate[1];
+            const bool whole = rstate[2] == (uint32_t)krem;
+            P |= d << shift;
+            M |= 0xFFu << shift;
+            if (whole) break;                             // the threshold bin is selected entirely
+          }
+        }
+        // keys equal to the threshold prefix: the lowest-j krem of them (all of them unless exact ties)
+        bool eq[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          eq[m] = !take_all && !take_none && cand[m] && (key[m] & M) == P;
+          const uint32_t bal = __ballot_sync(0xffffffffu, eq[m]);
+          if (lane == 0) hist[m * 4 + warp] = bal;        // the histogram is dead after the last pass
+        }
         if (t < 16) flags[t] = 0u;
         named_bar_sync(2, 128);
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
           const int j = m * 128 + t;
           bool sel = false;
-          if (j < p.nkb && j <= c) {
+          if (m < n_mt && j < p.nkb && j <= c) {
             if (j == 0 || j == c) {
               sel = true;
-            } else {
-              const float s = sc[j];
-              int rank = 0;
-              for (int jj = 1; jj < c; ++jj) {
-                const float o = sc[jj];
-                rank += (o > s) || (o == s && jj < j);
+            } else if (cand[m]) {
+              if (take_all) {
+                sel = true;
+              } else if (!take_none) {
+                const uint32_t pref = key[m] & M;
+                if (pref > P) {
+                  sel = true;
+                } else if (eq[m]) {
+                  const int w = j >> 5;
+                  int tr = __popc(hist[w] & ((1u << (j & 31)) - 1u));
+                  for (int ww = 0; ww < w; ++ww) tr += __popc(hist[ww]);
+                  sel = tr < krem;
+                }
               }
-              sel = rank < p.topk;
             }
           }
           const uint32_t bal = __ballot_sync(0xffffffffu, sel);
