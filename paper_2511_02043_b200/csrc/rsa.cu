@@ -275,16 +275,24 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
         if (m >= n_mt_i) break;
-        float mx = -INFINITY;
+        float mx0 = -INFINITY, mx1 = -INFINITY;
         for (int c0 = 0; c0 < 128; c0 += 32) {
           uint32_t r[32];
           tmem_ld32(acc + lane_base + m * 128 + c0, r);
           tmem_wait_ld();
+          if (c0 + 32 <= nvalid) {                        // warp-uniform: every query of the chunk is valid
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (c0 + e < nvalid) mx = fmaxf(mx, __uint_as_float(r[e]));
+            for (int e = 0; e < 32; e += 4) {
+              mx0 = fmax3(mx0, __uint_as_float(r[e]), __uint_as_float(r[e + 1]));
+              mx1 = fmax3(mx1, __uint_as_float(r[e + 2]), __uint_as_float(r[e + 3]));
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (c0 + e < nvalid) mx0 = fmaxf(mx0, __uint_as_float(r[e]));
+          }
         }
-        mine[m] = mx;
+        mine[m] = fmaxf(mx0, mx1);
       }
       tc_fence_before();
       mbar_arrive(&acc_empty[buf]);                       // the accumulator may take item n + nbuf
