@@ -139,6 +139,7 @@ constexpr bool kPingPong = false;
 // sched[2j+1] to WG1.
 struct Work {
   int b, g, h;
+  int g1;               // G index of warpgroup 1 (PAIR: g + 1, else g)
   int q0[2];            // first query row of each warpgroup's tile
   int lo[2], hi[2];     // schedule range [lo, hi) each warpgroup needs
   int lo_cta, hi_cta;
@@ -149,23 +150,34 @@ struct Work {
 // (b,h)-major so the ~148 co-resident CTAs share a few heads' K/V in L2; inside a
 // head the heaviest (latest, for causal) query blocks go first, and the stride of
 // gridDim.x cycles every CTA through light and heavy blocks (static balance).
-template <int D, bool DIFF, bool LIST>
+// PAIR (small heads whose S_q leaves half of a 256-row unit empty, e.g. Evoformer rows at
+// N_res = 384): the two warpgroups take the same 128-row query block of two neighbouring G
+// entries (MSA rows s, s+1), each with its own Q, K, V and output, so no warpgroup idles.
+template <int D, bool DIFF, bool LIST, bool PAIR>
 __device__ __forceinline__ Work decode_work(const AttnParams& p, int u) {
   Work w;
-  const int rows_per_unit = (DIFF || LIST) ? 128 : 256;
+  const int rows_per_unit = (DIFF || LIST || PAIR) ? 128 : 256;
   const int nqb = (p.Sq + rows_per_unit - 1) / rows_per_unit;
   const int bgh = u / nqb;
   const int qb = nqb - 1 - u % nqb;
   w.h = bgh % p.Hq;
-  w.g = (bgh / p.Hq) % p.G;
-  w.b = bgh / (p.Hq * p.G);
+  if (PAIR) {
+    const int ngp = (p.G + 1) >> 1;
+    w.g = ((bgh / p.Hq) % ngp) * 2;
+    w.g1 = w.g + 1;
+    w.b = bgh / (p.Hq * ngp);
+  } else {
+    w.g = (bgh / p.Hq) % p.G;
+    w.g1 = w.g;
+    w.b = bgh / (p.Hq * p.G);
+  }
   w.lo_cta = 1 << 30;
   w.hi_cta = 0;
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
-    w.q0[i] = (DIFF || LIST) ? qb * 128 : qb * 256 + i * 128;
+    w.q0[i] = (DIFF || LIST || PAIR) ? qb * 128 : qb * 256 + i * 128;
     w.lo[i] = w.hi[i] = 0;
-    if (!LIST && w.q0[i] < p.Sq) {
+    if (!LIST && w.q0[i] < p.Sq && !(PAIR && i == 1 && w.g1 >= p.G)) {
       const int q_last = min(p.Sq, w.q0[i] + 128) - 1;
       Interval iv = rows_union(p, w.b, w.q0[i], q_last);
       if (iv.hi > iv.lo) {
@@ -230,7 +242,7 @@ __device__ __forceinline__ int next_tile(const Work& w, int j) {
   return -1;
 }
 
-template <int D, bool DIFF, int MOD, bool BIAS, bool LIST>
+template <int D, bool DIFF, int MOD, bool BIAS, bool LIST, bool PAIR = false>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     attn_tc_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ TmaMaps maps, int n_units) {
   using C = TcCfg<D, DIFF, LIST>;
@@ -295,7 +307,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   };
   // Work of the unit published in slot it & 1 (by value: keeps it in registers)
   auto unit_work = [&](int u, int it) -> Work {
-    Work w = decode_work<D, DIFF, LIST>(p, u);
+    Work w = decode_work<D, DIFF, LIST, PAIR>(p, u);
     if constexpr (LIST) load_sched(w, sched_base + (it & 1) * C::SCHED_WORDS);
     return w;
   };
@@ -321,37 +333,43 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           mbar_arrive(&unit_full[it & 1]);             // end marker
           break;
         }
-        Work w = decode_work<D, DIFF, LIST>(p, u);
+        Work w = decode_work<D, DIFF, LIST, PAIR>(p, u);
         if constexpr (LIST) {
           build_sched(p, w, sc);
           load_sched(w, sc);
-        } else if (C::BIAS_TMA_OK && p.keybits && p.keybits_words <= C::KBITS_WORDS) {
+        } else if (C::BIAS_TMA_OK && p.keybits && p.keybits_words <= (PAIR ? C::KBITS_WORDS / 2 : C::KBITS_WORDS)) {
           // small heads: the unit's key-mask bits (Evoformer MSA mask, <= 64 words) ride in the unit
-          // slot, so the softmax warpgroups never wait on a global load for them
-          const uint32_t* kb = p.keybits + ((int64_t)w.b * p.G + w.g) * p.keybits_words;
-          for (int i0 = 0; i0 < p.keybits_words; i0 += 16) {   // 16 loads in flight per batch
-            uint32_t tmp[16];
+          // slot, so the softmax warpgroups never wait on a global load for them (PAIR: both G entries)
+          for (int pi = 0; pi < (PAIR ? 2 : 1); ++pi) {
+            const int gg = pi ? min(w.g1, p.G - 1) : w.g;
+            const uint32_t* kb = p.keybits + ((int64_t)w.b * p.G + gg) * p.keybits_words;
+            uint32_t* dst = sc + pi * (C::KBITS_WORDS / 2);
+            for (int i0 = 0; i0 < p.keybits_words; i0 += 16) {   // 16 loads in flight per batch
+              uint32_t tmp[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (i0 + i < p.keybits_words) tmp[i] = __ldg(kb + i0 + i);
+              for (int i = 0; i < 16; ++i)
+                if (i0 + i < p.keybits_words) tmp[i] = __ldg(kb + i0 + i);
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (i0 + i < p.keybits_words) sc[i0 + i] = tmp[i];
+              for (int i = 0; i < 16; ++i)
+                if (i0 + i < p.keybits_words) dst[i0 + i] = tmp[i];
+            }
           }
         }
         mbar_arrive(&unit_full[it & 1]);               // release: id / schedule visible to the waiters
         const int u_next = (int)gridDim.x + atomicAdd(p.tile_ctr, 1);   // latency hidden behind this unit
         const int hkv = w.h / p.grp;
+        const int g1c = min(w.g1, p.G - 1);               // PAIR with odd G: WG1 of the last pair idles
         const int gq = maps.q_bcast_g ? 0 : w.g, bq = maps.q_bcast_b ? 0 : w.b;
         const int gk = maps.k_bcast_g ? 0 : w.g, bk = maps.k_bcast_b ? 0 : w.b;
         const int gv = maps.v_bcast_g ? 0 : w.g, bv = maps.v_bcast_b ? 0 : w.b;
+        const int gq1 = maps.q_bcast_g ? 0 : g1c, gk1 = maps.k_bcast_g ? 0 : g1c, gv1 = maps.v_bcast_g ? 0 : g1c;
         if (it > 0) mbar_wait(q_empty, (it - 1) & 1);  // the previous unit's S MMAs (and diff xbuf) are done
         mbar_arrive_expect_tx(q_full, C::NQ * C::TILE_BYTES);
         for (int i = 0; i < C::NQ; ++i) {
           const int qh = DIFF ? w.h + i * p.Hq : w.h;
           for (int c = 0; c < C::NCH; ++c)
-            tma_load_5d(sQ + i * C::TILE_BYTES + c * C::CHUNK_BYTES, &maps.q, q_full, c * C::CH, w.q0[i], qh, gq,
-                        bq);
+            tma_load_5d(sQ + i * C::TILE_BYTES + c * C::CHUNK_BYTES, &maps.q, q_full, c * C::CH, w.q0[i], qh,
+                        i ? gq1 : gq, bq);
         }
         auto load_entry = [&](const CUtensorMap* m, int tile, int head, int gg, int bb) {
           const int slot = e % C::NSLOT;
@@ -370,6 +388,13 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             if (n1) load_entry(&maps.k, kv_tile<LIST>(w, 1, j), hkv, gk, bk);
             load_entry(&maps.v, kv_tile<LIST>(w, 0, j), hkv, gv, bv);
             if (n1) load_entry(&maps.v, kv_tile<LIST>(w, 1, j), hkv, gv, bv);
+          } else if constexpr (PAIR) {
+            // step j: K(g) [K(g+1)] V(g) [V(g+1)] -- the same KV tile of two G entries
+            const bool n1 = needs(w, 1, j);
+            load_entry(&maps.k, j, hkv, gk, bk);
+            if (n1) load_entry(&maps.k, j, hkv, gk1, bk);
+            load_entry(&maps.v, j, hkv, gv, bv);
+            if (n1) load_entry(&maps.v, j, hkv, gv1, bv);
           } else {
             for (int t = 0; t < C::ENTRIES_PER_TILE; ++t) {
               const bool is_v = t == C::ENTRIES_PER_TILE - 1;
@@ -377,9 +402,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             }
           }
           if (bias_tma) {
-            const int gb = maps.bias_bcast_g ? 0 : w.g, bb2 = maps.bias_bcast_b ? 0 : w.b;
+            const int bb2 = maps.bias_bcast_b ? 0 : w.b;
             for (int i = 0; i < 2; ++i) {
               if (!needs(w, i, j)) continue;
+              const int gb = maps.bias_bcast_g ? 0 : (i ? g1c : w.g);
               const int st = bcnt[i] & 1;
               if (bcnt[i] >= 2) mbar_wait(&bias_empty[i * 2 + st], ((bcnt[i] >> 1) - 1) & 1);
               mbar_arrive_expect_tx(&bias_full[i * 2 + st], C::BIAS_TILE);
@@ -443,9 +469,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         if (j >= 0) {
           // K of warpgroup 1 is a separate ring entry for diff (map 1) and block lists (its own tile);
           // V is separate for block lists only.  Entries a warpgroup does not need are not loaded.
-          constexpr bool kSepK = DIFF || LIST;
+          constexpr bool kSepK = DIFF || LIST || PAIR;
+          constexpr bool kSepV = LIST || PAIR;
           int ks0 = acquire();
-          int ks1 = kSepK ? ((!LIST || needs(w, 1, j)) ? acquire() : -1) : ks0;
+          int ks1 = kSepK ? ((!kSepV || needs(w, 1, j)) ? acquire() : -1) : ks0;
           if (needs(w, 0, j)) issue_s(0, ks0);
           if (needs(w, 1, j)) issue_s(1, ks1);
           umma_commit(&empty[ks0]);
@@ -453,12 +480,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           if (next_tile(w, j) < 0) umma_commit(q_empty);   // Q is free once the last S MMA is done
           while (j >= 0) {
             const int va = acquire();
-            const int vb = LIST ? (needs(w, 1, j) ? acquire() : -1) : va;
+            const int vb = kSepV ? (needs(w, 1, j) ? acquire() : -1) : va;
             const int jn = next_tile(w, j);
             int kn0 = -1, kn1 = -1;
             if (jn >= 0) {
               kn0 = acquire();
-              kn1 = kSepK ? ((!LIST || needs(w, 1, jn)) ? acquire() : -1) : kn0;
+              kn1 = kSepK ? ((!kSepV || needs(w, 1, jn)) ? acquire() : -1) : kn0;
             }
             if (needs(w, 0, j)) {
               issue_pv(0, va);
@@ -470,7 +497,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
               if (j == w.hi[1] - 1) umma_commit(&o_full[1]);
             }
             umma_commit(&empty[va]);
-            if (LIST && vb >= 0) umma_commit(&empty[vb]);
+            if (kSepV && vb >= 0) umma_commit(&empty[vb]);
             if (jn >= 0) {
               if (needs(w, 1, jn)) issue_s(1, kn1);
               umma_commit(&empty[kn0]);
@@ -511,24 +538,27 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     if (u >= n_units) break;
     FL_T(11);                                        // 11: waiting for the next unit id
     const Work w = unit_work(u, it);
+    const int gw = wg ? w.g1 : w.g;                  // this warpgroup's G entry
     const int q = (wg ? w.q0[1] : w.q0[0]) + r;
-    const bool row_valid = q < p.Sq;
+    const bool row_valid = q < p.Sq && (!PAIR || gw < p.G);
     const int q_abs = q + p.q_off;
     const Interval iv = row_interval(p, w.b, q);
     float slope_l2 = 0.f;
     if (MOD == MOD_ALIBI)
       slope_l2 = kLog2e * (p.alibi ? p.alibi[w.h] : exp2f(-8.f * (float)(w.h + 1) / (float)p.Hq));
-    const uint32_t* kbits = p.keybits ? p.keybits + ((int64_t)w.b * p.G + w.g) * p.keybits_words : nullptr;
+    const uint32_t* kbits =
+        p.keybits ? p.keybits + ((int64_t)w.b * p.G + min(gw, p.G - 1)) * p.keybits_words : nullptr;
     // The unit's key-mask bits (Evoformer MSA mask: <= 16 words) are staged once per unit in shared
     // memory, so no tile waits on a global load for them.
     // small heads: staged in the unit slot by the producer (read before release_unit)
-    const uint32_t* kb_smem = sched_base + (it & 1) * C::SCHED_WORDS;
-    const bool kb_staged = !LIST && C::BIAS_TMA_OK && kbits && p.keybits_words <= C::KBITS_WORDS;
+    const uint32_t* kb_smem = sched_base + (it & 1) * C::SCHED_WORDS + (PAIR && wg ? C::KBITS_WORDS / 2 : 0);
+    const bool kb_staged =
+        !LIST && C::BIAS_TMA_OK && kbits && p.keybits_words <= (PAIR ? C::KBITS_WORDS / 2 : C::KBITS_WORDS);
     FL_T(12);                                        // 12: unit setup (work decode, key-mask staging)
     const unsigned char* bias_row = nullptr;
     if (BIAS)
       bias_row = static_cast<const unsigned char*>(p.bias) +
-                 (w.b * p.bs.b + w.g * p.bs.g + (int64_t)w.h * p.bs.h + (int64_t)(row_valid ? q : 0) * p.bs.s) *
+                 (w.b * p.bs.b + min(gw, p.G - 1) * p.bs.g + (int64_t)w.h * p.bs.h + (int64_t)(row_valid ? q : 0) * p.bs.s) *
                      (p.bias_dtype == 1 ? 4 : 2);
 
     float m_ref = -INFINITY, l = 0.f;
@@ -766,7 +796,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     const bool gated = false;
 #endif
     const uint4* gp = reinterpret_cast<const uint4*>(static_cast<const unsigned short*>(p.gate) + w.b * p.gs.b +
-                                                     w.g * p.gs.g + (int64_t)w.h * p.gs.h + (int64_t)q * p.gs.s);
+                                                     gw * p.gs.g + (int64_t)w.h * p.gs.h + (int64_t)q * p.gs.s);
     constexpr bool kGateEarly = D <= 32;               // small head: the whole gate row is 4 registers x 4
     uint4 gv[kGateEarly ? D / 8 : 1];                  // in flight while the last PV runs
     if (kGateEarly && gated) {
@@ -829,7 +859,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       named_bar_sync(1, 256);
     } else {
       if (DIFF) named_bar_sync(1, 256);
-      const int64_t obase = w.b * p.os.b + w.g * p.os.g + (int64_t)w.h * p.os.h + (int64_t)q * p.os.s;
+      const int64_t obase = w.b * p.os.b + gw * p.os.g + (int64_t)w.h * p.os.h + (int64_t)q * p.os.s;
 #pragma unroll
       for (int c = 0; c < D; c += 32) {
         uint32_t o[32];
@@ -889,7 +919,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         }
       }
       if (p.lse && row_valid)
-        p.lse[w.b * p.lses.b + w.g * p.lses.g + (int64_t)w.h * p.lses.h + (int64_t)q * p.lses.s] =
+        p.lse[w.b * p.lses.b + gw * p.lses.g + (int64_t)w.h * p.lses.h + (int64_t)q * p.lses.s] =
             empty_row ? -INFINITY : (m_ref + __log2f(l)) * kLn2;
       if (DIFF) mbar_arrive(q_empty);                 // WG0 is done reading xbuf (sQ)
       if (LIST) named_bar_arrive(5, 256);             // WG0 is done reading O1 and (m, l)
@@ -934,11 +964,19 @@ static cudaError_t launch_one(const AttnParams& p, const TmaMaps& maps, cudaStre
               : p.bias                 ? attn_tc_kernel<D, DIFF, MOD, true, false>
                                        : attn_tc_kernel<D, DIFF, MOD, false, false>;
   const bool list = p.mask == MASK_BLOCKLIST;
+  // small heads whose S_q leaves half of the last 256-row unit empty (Evoformer rows): pair G entries
+  bool pair = false;
+  if constexpr (D == 32 && !DIFF) {
+    if (!list && p.G >= 2 && p.Sq % 256 != 0 && p.Sq % 256 <= 128) {
+      pair = true;
+      kern = p.bias ? attn_tc_kernel<D, false, MOD, true, false, true> : attn_tc_kernel<D, false, MOD, false, false, true>;
+    }
+  }
   const int smem_bytes = list ? TcCfg<D, false, true>::SMEM_TOTAL : TcCfg<D, DIFF>::SMEM_TOTAL;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
   if (e != cudaSuccess) return e;
-  const int rows_per_unit = (DIFF || list) ? 128 : 256;
-  const long long units = (long long)p.B * p.G * p.Hq * ((p.Sq + rows_per_unit - 1) / rows_per_unit);
+  const int rows_per_unit = (DIFF || list || pair) ? 128 : 256;
+  const long long units = (long long)p.B * (pair ? (p.G + 1) / 2 : p.G) * p.Hq * ((p.Sq + rows_per_unit - 1) / rows_per_unit);
   if (units >= (1ll << 31)) return cudaErrorInvalidValue;
   // persistent: one CTA per SM (TMEM and shared memory admit one), each walks units with stride grid
   const int grid = (int)std::min<long long>(units, num_sms());

@@ -161,6 +161,17 @@ def test_evoformer(fl, kind, dtype):
     check(out.cpu().double().reshape(ref.shape), ref, TOL[dtype], what=f"evoformer {kind} {dtype}")
 
 
+@pytest.mark.parametrize("Ns,Nr", [(25, 300), (7, 130), (3, 384), (2, 200)])
+def test_evoformer_row_pairs(fl, Ns, Nr):
+    """Row attention at S_q % 256 <= 128 runs the paired-G kernel (two MSA rows per unit): odd G (last
+    pair half empty), several query tiles, ragged tails; S_q % 256 > 128 keeps the 256-row units."""
+    case = dict(kind="row", B=1, Ns=Ns, Nr=Nr, H=2, c=32, p_zero=0.1, dtype="bf16", seed=Ns)
+    ins, gk, ok = cases.evoformer(case)
+    out = cases.run_gpu(fl, ins, gk)
+    ref, _ = cases.run_oracle(ins, ok)
+    check(out.cpu().double().reshape(ref.shape), ref, TOL["bf16"], what=f"evoformer row pairs Ns{Ns} Nr{Nr}")
+
+
 def test_determinism(fl):
     ins, gk, _ = cases.build(dict(S=700, D=128, mask="causal", Hq=2))
     a = cases.run_gpu(fl, ins, gk)
