@@ -3,11 +3,13 @@
 // K/V block is read once per (b, h)), so the tensor-core tile of 128 query rows would idle 127/128
 // of its MMA work and one CTA per (b, h) would leave SMs idle; instead
 //
-//  * attn_decode_split_kernel: grid (n_split, rows).  Each CTA walks `bps` KV blocks of one query
-//    row (the row's RSA list, or the 128-key tiles of its mask interval): thread t scores key t of
-//    the block (16-byte K loads, q in shared memory), block max/sum by warp shuffles (Alg.2's
-//    online update, at block granularity), then 8 key-groups x D/8 column groups
-//    accumulate P V with 16-byte V loads.  It writes the unnormalised partial (O_s, m_s, l_s).
+//  * attn_decode_split_kernel: persistent (one CTA per SM) over items = (row, split of `bps` 128-key
+//    blocks).  A producer warp resolves the blocks (the row's RSA list, or the tiles of its mask
+//    interval) 32 at a time and streams each block's K and V tiles by TMA into a 3-stage shared-memory
+//    ring; 256 compute threads score the keys (two threads per key, 128-B swizzled rows read
+//    conflict-free), take the block max/sum by warp shuffles (Alg.2's online update, at
+//    block granularity), accumulate P V (16 key groups x D/8 column groups) and write the item's
+//    unnormalised partial (O_s, m_s, l_s).
 //  * attn_decode_combine_kernel: O = sum_s O_s 2^(m_s - M) / sum_s l_s 2^(m_s - M), M = max_s m_s
 //    (the same closed form of the online softmax, applied across splits).
 //  * rsa_select_small_kernel: the selection score of every KV block for a query block of <= 16 rows
@@ -16,6 +18,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math.h>
+
+#include <algorithm>
 
 #include "masks.cuh"
 #include "params.h"
@@ -58,152 +62,275 @@ __device__ __forceinline__ DecRow dec_row(const AttnParams& p, int64_t bgh, int 
   return r;
 }
 
+// Persistent, TMA-fed split-KV kernel.  grid = min(items, SMs); item = (row, split) with `bps`
+// consecutive 128-key blocks of that row.  Warp 4 (one lane) walks the CTA's items and streams every
+// block's K and V tiles (128-B swizzled, the tcgen05 kernels' tensor maps) into an NST-stage
+// shared-memory ring through full/empty mbarriers, so the next blocks are in flight while the 128
+// compute threads work on the current one: thread t scores key t (chunk c of row r sits at
+// (c ^ (r & 7)) * 16 -- conflict-free), block max/sum by warp shuffles (Alg.2 at block granularity),
+// then 8 key groups x D/8 column groups accumulate P V.  The item's unnormalised partial
+// (O_s, m_s, l_s) goes to the workspace for the combine kernel.
 template <int D>
-__global__ void __launch_bounds__(kDecThreads) attn_decode_split_kernel(const __grid_constant__ AttnParams p,
-                                                                         float* __restrict__ part, int bps) {
+struct DecCfg {
+  static constexpr int NST = D == 128 ? 3 : 6;            // ring stages (K + V of one block each)
+  static constexpr int TILE = 128 * D * 2;
+  static constexpr int SLAB = 128 * 128;                  // 128 rows x 64 columns (128-B swizzle)
+  static constexpr int SMEM = NST * 2 * TILE + 1024;      // + alignment slack (1024-B swizzle atoms)
+};
+
+constexpr int kDecCompute = 256;            // compute threads: 2 per key for Q K^T
+template <int D>
+__global__ void __launch_bounds__(kDecCompute + 32, 1)
+    attn_decode_split_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ TmaMaps maps,
+                             float* __restrict__ part, int bps, int n_split, long long n_items) {
+  using C = DecCfg<D>;
   constexpr int DG = D / 8;                 // 16-byte column groups
-  constexpr int KG = kDecThreads / DG;      // key groups for P V
+  constexpr int KG = kDecCompute / DG;      // key groups for P V
   constexpr int KPG = 128 / KG;             // keys per key group
+  constexpr int NW = kDecCompute / 32;
+  extern __shared__ uint8_t dec_smem_raw[];
+  uint8_t* ring = dec_smem_raw + ((1024u - (smem_u32(dec_smem_raw) & 1023u)) & 1023u);
   __shared__ __align__(16) float qs[D];
   __shared__ float ps[128];
-  __shared__ float red[2][4];
+  __shared__ float red[2][NW];
   __shared__ __align__(16) float accs[KG][D];
+  __shared__ uint64_t full[C::NST], empty[C::NST];
+  __shared__ int kbinfo[C::NST];
 
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const int split = blockIdx.x, n_split = gridDim.x;
-  const int64_t row = blockIdx.y;                       // ((b*G + g)*Hq + h)*Sq + q
-  const int q = (int)(row % p.Sq);
-  const int64_t bgh = row / p.Sq;
-  const int h = (int)(bgh % p.Hq), g = (int)((bgh / p.Hq) % p.G), b = (int)(bgh / ((int64_t)p.Hq * p.G));
-  const int hkv = h / p.grp;
-  const int q_abs = q + p.q_off;
-  const Interval iv = row_interval(p, b, q);
-  const DecRow dr = dec_row(p, bgh, q, iv);
-  const unsigned short* kbase = static_cast<const unsigned short*>(p.k) + b * p.ks.b + g * p.ks.g + (int64_t)hkv * p.ks.h;
-  const unsigned short* vbase = static_cast<const unsigned short*>(p.v) + b * p.vs.b + g * p.vs.g + (int64_t)hkv * p.vs.h;
-  const uint32_t* kbits = p.keybits ? p.keybits + ((int64_t)b * p.G + g) * p.keybits_words : nullptr;
-  float slope_l2 = 0.f;
-  if (p.mod == MOD_ALIBI) slope_l2 = kDecLog2e * (p.alibi ? p.alibi[h] : exp2f(-8.f * (float)(h + 1) / (float)p.Hq));
-  const float sc_l2 = p.scale * kDecLog2e;
-
-  if (t < D) {
-    const unsigned short* qp = static_cast<const unsigned short*>(p.q) + b * p.qs.b + g * p.qs.g +
-                               (int64_t)h * p.qs.h + (int64_t)q * p.qs.s;
-    qs[t] = __uint_as_float((uint32_t)qp[t] << 16);
+  if (t == 0) {
+    for (int s = 0; s < C::NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kDecCompute);
+    }
+    fence_mbar_init();
   }
   __syncthreads();
 
-  const int dg = t % DG, kg = t / DG;
-  float acc[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-  float m = -INFINITY, l = 0.f;
-  const int i0 = split * bps, i1 = min(dr.n, i0 + bps);
-  for (int i = i0; i < i1; ++i) {
-    const int kb = dr.list ? dr.list[i] : dr.lo_tile + i;
-    const int k = kb * 128 + t;
-    // V rows of this thread's key group: issued first so they stream in while Q K^T and the block
-    // reductions run (keys past S_k get p = 0; their row index is clamped to stay in bounds)
-    uint4 vv[KPG];
-#pragma unroll
-    for (int t2 = 0; t2 < KPG; ++t2) {
-      const int kr = min(max(kb, 0) * 128 + kg * KPG + t2, p.Sk - 1);
-      vv[t2] = __ldg(reinterpret_cast<const uint4*>(vbase + (int64_t)kr * p.vs.s) + dg);
+  auto split_of = [&](long long it) { return (int)(it % n_split); };
+  auto row_coords = [&](int64_t row, int& q, int64_t& bgh, int& h, int& g, int& b) {
+    q = (int)(row % p.Sq);
+    bgh = row / p.Sq;
+    h = (int)(bgh % p.Hq);
+    g = (int)((bgh / p.Hq) % p.G);
+    b = (int)(bgh / ((int64_t)p.Hq * p.G));
+  };
+
+  if (warp == NW) {
+    // ============================== producer ==============================
+    // The warp resolves 32 ring slots at a time in parallel (lane = slot: the row's list entry or
+    // interval tile, one dependent global round trip per 32 slots instead of per item); lane 0 then
+    // issues them in order.
+    if (lane == 0) {
+      tma_prefetch_desc(&maps.k);
+      tma_prefetch_desc(&maps.v);
     }
-    bool keep = kb >= 0 && k < p.Sk && k >= iv.lo && k < iv.hi;
-    if (keep && kbits) keep = (kbits[k >> 5] >> (k & 31)) & 1u;
-    float s = -INFINITY;
-    if (keep) {
-      const uint4* kr = reinterpret_cast<const uint4*>(kbase + (int64_t)k * p.ks.s);
-      uint4 kv[DG];
-#pragma unroll
-      for (int c = 0; c < DG; ++c) kv[c] = __ldg(kr + c);
-      float d0 = 0.f, d1 = 0.f;
-#pragma unroll
-      for (int c = 0; c < DG; ++c) {
-        const float4 qa = *reinterpret_cast<const float4*>(qs + c * 8);
-        const float4 qb = *reinterpret_cast<const float4*>(qs + c * 8 + 4);
-        const uint32_t w[4] = {kv[c].x, kv[c].y, kv[c].z, kv[c].w};
-        d0 = fmaf(qa.x, bf16_lo(w[0]), d0);
-        d1 = fmaf(qa.y, bf16_hi(w[0]), d1);
-        d0 = fmaf(qa.z, bf16_lo(w[1]), d0);
-        d1 = fmaf(qa.w, bf16_hi(w[1]), d1);
-        d0 = fmaf(qb.x, bf16_lo(w[2]), d0);
-        d1 = fmaf(qb.y, bf16_hi(w[2]), d1);
-        d0 = fmaf(qb.z, bf16_lo(w[3]), d0);
-        d1 = fmaf(qb.w, bf16_hi(w[3]), d1);
+    const long long my_items = blockIdx.x < n_items ? (n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const long long n_slots = my_items * bps;
+    for (long long e0 = 0; e0 < n_slots; e0 += 32) {
+      const long long es = e0 + lane;
+      int kb = -1, hkv = 0, gk = 0, bk = 0, gv = 0, bv = 0;
+      if (es < n_slots) {
+        const long long it = blockIdx.x + (es / bps) * gridDim.x;
+        const int i = split_of(it) * bps + (int)(es % bps);
+        const int64_t row = it / n_split;
+        int q, h, g, b;
+        int64_t bgh;
+        row_coords(row, q, bgh, h, g, b);
+        hkv = h / p.grp;
+        gk = maps.k_bcast_g ? 0 : g; bk = maps.k_bcast_b ? 0 : b;
+        gv = maps.v_bcast_g ? 0 : g; bv = maps.v_bcast_b ? 0 : b;
+        const DecRow dr = dec_row(p, bgh, q, row_interval(p, b, q));
+        if (i < dr.n) kb = dr.list ? dr.list[i] : dr.lo_tile + i;
+        if (kb * 128 >= p.Sk) kb = -1;
       }
-      s = (d0 + d1) * sc_l2;                            // log2-domain score (G1, Eq.4)
-      if (p.mod == MOD_ALIBI) s += slope_l2 * (float)(k - q_abs);
-      if (p.mod == MOD_SOFTCAP) s = p.softcap * kDecLog2e * tanh_approx((d0 + d1) * p.scale / p.softcap);
+      const int cnt = (int)min(32ll, n_slots - e0);
+      for (int j = 0; j < cnt; ++j) {
+        const int kbj = __shfl_sync(0xffffffffu, kb, j), hj = __shfl_sync(0xffffffffu, hkv, j);
+        const int gkj = __shfl_sync(0xffffffffu, gk, j), bkj = __shfl_sync(0xffffffffu, bk, j);
+        const int gvj = __shfl_sync(0xffffffffu, gv, j), bvj = __shfl_sync(0xffffffffu, bv, j);
+        if (lane == 0) {
+          const int e = (int)(e0 + j);
+          const int s = e % C::NST;
+          if (e >= C::NST) mbar_wait(&empty[s], ((e / C::NST) - 1) & 1);
+          kbinfo[s] = kbj;
+          if (kbj >= 0) {
+            uint8_t* ks = ring + s * 2 * C::TILE;
+            mbar_arrive_expect_tx(&full[s], 2 * C::TILE);
+            for (int c = 0; c < D / 64; ++c) {
+              tma_load_5d(ks + c * C::SLAB, &maps.k, &full[s], c * 64, kbj * 128, hj, gkj, bkj);
+              tma_load_5d(ks + C::TILE + c * C::SLAB, &maps.v, &full[s], c * 64, kbj * 128, hj, gvj, bvj);
+            }
+          } else {
+            mbar_arrive(&full[s]);
+          }
+        }
+        __syncwarp();
+      }
     }
-    float bm = dec_warp_max(s);
-    if (lane == 0) red[0][warp] = bm;
-    __syncthreads();
-    bm = fmaxf(fmaxf(red[0][0], red[0][1]), fmaxf(red[0][2], red[0][3]));
-    const float m_new = fmaxf(m, bm);
-    if (m_new == -INFINITY) {                           // nothing kept so far (block-uniform)
-      __syncthreads();
-      continue;
-    }
-    const float corr = ex2(m - m_new);                  // 0 when m = -inf
-    const float pe = s == -INFINITY ? 0.f : ex2(s - m_new);
-    ps[t] = pe;
-    const float ws = dec_warp_sum(pe);
-    if (lane == 0) red[1][warp] = ws;
-    __syncthreads();
-    l = l * corr + ((red[1][0] + red[1][1]) + (red[1][2] + red[1][3]));
-    m = m_new;
+    return;
+  }
+
+  // ============================== compute (256 threads) ==============================
+  const int dg = t % DG, kg = t / DG;
+  const int key = t >> 1, half = t & 1;               // Q K^T: thread pair (2k, 2k+1) splits key k's D
+  auto load_q = [&](long long it) -> unsigned short {  // element t of the item's query row
+    int q, h, g, b;
+    int64_t bgh;
+    row_coords(it / n_split, q, bgh, h, g, b);
+    return static_cast<const unsigned short*>(p.q)[b * p.qs.b + g * p.qs.g + (int64_t)h * p.qs.h + (int64_t)q * p.qs.s + t];
+  };
+  unsigned short q_next = 0;
+  if (t < D && blockIdx.x < n_items) q_next = load_q(blockIdx.x);
+  int e = 0;
+  for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
+    const int64_t row = it / n_split;
+    const int split = (int)(it % n_split);
+    int q, h, g, b;
+    int64_t bgh;
+    row_coords(row, q, bgh, h, g, b);
+    const int q_abs = q + p.q_off;
+    const Interval iv = row_interval(p, b, q);
+    const uint32_t* kbits = p.keybits ? p.keybits + ((int64_t)b * p.G + g) * p.keybits_words : nullptr;
+    float slope_l2 = 0.f;
+    if (p.mod == MOD_ALIBI) slope_l2 = kDecLog2e * (p.alibi ? p.alibi[h] : exp2f(-8.f * (float)(h + 1) / (float)p.Hq));
+    const float sc_l2 = p.scale * kDecLog2e;
+    named_bar_sync(1, kDecCompute);                     // previous item done with qs / accs
+    if (t < D) qs[t] = __uint_as_float((uint32_t)q_next << 16);
+    named_bar_sync(1, kDecCompute);
+    if (t < D && it + gridDim.x < n_items) q_next = load_q(it + gridDim.x);   // in flight during this item
+
+    float acc[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] *= corr;
-    {
+    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+    float m = -INFINITY, l = 0.f;
+    for (int i = 0; i < bps; ++i, ++e) {
+      const int s = e % C::NST;
+      mbar_wait(&full[s], (e / C::NST) & 1);
+      const int kb = kbinfo[s];
+      if (kb < 0) {                                     // no block in this slot (block-uniform)
+        mbar_arrive(&empty[s]);
+        continue;
+      }
+      const uint8_t* ks = ring + s * 2 * C::TILE;
+      const uint8_t* vs = ks + C::TILE;
+      const int k = kb * 128 + key;
+      bool keep = k < p.Sk && k >= iv.lo && k < iv.hi;
+      if (keep && kbits) keep = (kbits[k >> 5] >> (k & 31)) & 1u;
+      float sv = -INFINITY, dot = 0.f;
+      if (keep) {
+        float d0 = 0.f, d1 = 0.f;
+#pragma unroll
+        for (int cc = 0; cc < DG / 2; ++cc) {
+          // this half's chunks (128-B swizzled tile: chunk c of row r at (c ^ (r & 7)) * 16), rotated by 4
+          // for half 1 so the pair hits different bank groups
+          const int c = half * (DG / 2) + ((cc + 4 * half) % (DG / 2));
+          const uint4 kv = *reinterpret_cast<const uint4*>(ks + (c >> 3) * C::SLAB + key * 128 + (((c & 7) ^ (key & 7)) << 4));
+          const float4 qa = *reinterpret_cast<const float4*>(qs + c * 8);
+          const float4 qb = *reinterpret_cast<const float4*>(qs + c * 8 + 4);
+          d0 = fmaf(qa.x, bf16_lo(kv.x), d0);
+          d1 = fmaf(qa.y, bf16_hi(kv.x), d1);
+          d0 = fmaf(qa.z, bf16_lo(kv.y), d0);
+          d1 = fmaf(qa.w, bf16_hi(kv.y), d1);
+          d0 = fmaf(qb.x, bf16_lo(kv.z), d0);
+          d1 = fmaf(qb.y, bf16_hi(kv.z), d1);
+          d0 = fmaf(qb.z, bf16_lo(kv.w), d0);
+          d1 = fmaf(qb.w, bf16_hi(kv.w), d1);
+        }
+        dot = d0 + d1;
+      }
+      dot += __shfl_xor_sync(0xffffffffu, dot, 1);      // the pair's two halves of the dot product
+      if (keep) {
+        sv = dot * sc_l2;                               // log2-domain score (G1, Eq.4)
+        if (p.mod == MOD_ALIBI) sv += slope_l2 * (float)(k - q_abs);
+        if (p.mod == MOD_SOFTCAP) sv = p.softcap * kDecLog2e * tanh_approx(dot * p.scale / p.softcap);
+      }
+      float bm = dec_warp_max(sv);
+      if (lane == 0) red[0][warp] = bm;
+      named_bar_sync(1, kDecCompute);
+      bm = red[0][0];
+#pragma unroll
+      for (int w2 = 1; w2 < NW; ++w2) bm = fmaxf(bm, red[0][w2]);
+      const float m_new = fmaxf(m, bm);
+      if (m_new == -INFINITY) {                         // nothing kept so far (block-uniform)
+        mbar_arrive(&empty[s]);
+        named_bar_sync(1, kDecCompute);
+        continue;
+      }
+      const float corr = ex2(m - m_new);                // 0 when m = -inf
+      const float pe = sv == -INFINITY ? 0.f : ex2(sv - m_new);
+      if (half == 0) ps[key] = pe;
+      const float ws = dec_warp_sum(half == 0 ? pe : 0.f);
+      if (lane == 0) red[1][warp] = ws;
+      named_bar_sync(1, kDecCompute);
+      float bs = 0.f;
+#pragma unroll
+      for (int w2 = 0; w2 < NW; ++w2) bs += red[1][w2];
+      l = l * corr + bs;
+      m = m_new;
+#pragma unroll
+      for (int i2 = 0; i2 < 8; ++i2) acc[i2] *= corr;
 #pragma unroll
       for (int t2 = 0; t2 < KPG; ++t2) {
-        const float pv = ps[kg * KPG + t2];
-        const uint32_t w[4] = {vv[t2].x, vv[t2].y, vv[t2].z, vv[t2].w};
+        const int kr = kg * KPG + t2;
+        const float pv = ps[kr];
+        const uint4 vv = *reinterpret_cast<const uint4*>(vs + (dg >> 3) * C::SLAB + kr * 128 + (((dg & 7) ^ (kr & 7)) << 4));
+        const uint32_t w4[4] = {vv.x, vv.y, vv.z, vv.w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          acc[2 * e] = fmaf(pv, bf16_lo(w[e]), acc[2 * e]);
-          acc[2 * e + 1] = fmaf(pv, bf16_hi(w[e]), acc[2 * e + 1]);
+        for (int e2 = 0; e2 < 4; ++e2) {
+          acc[2 * e2] = fmaf(pv, bf16_lo(w4[e2]), acc[2 * e2]);
+          acc[2 * e2 + 1] = fmaf(pv, bf16_hi(w4[e2]), acc[2 * e2 + 1]);
         }
       }
+      mbar_arrive(&empty[s]);                           // this thread is done with the stage
+      named_bar_sync(1, kDecCompute);                   // ps / red reuse
     }
-    __syncthreads();                                    // ps / red reuse
-  }
 #pragma unroll
-  for (int e = 0; e < 8; ++e) accs[kg][dg * 8 + e] = acc[e];
-  __syncthreads();
-  float* out = part + (row * n_split + split) * (D + 2);
-  if (t < D) {
-    float o = 0.f;
+    for (int i2 = 0; i2 < 8; ++i2) accs[kg][dg * 8 + i2] = acc[i2];
+    named_bar_sync(1, kDecCompute);
+    float* out = part + (row * n_split + split) * (D + 2);
+    if (t < D) {
+      float o = 0.f;
 #pragma unroll
-    for (int g2 = 0; g2 < KG; ++g2) o += accs[g2][t];
-    out[t] = o;
-  }
-  if (t == 0) {
-    out[D] = m;
-    out[D + 1] = l;
+      for (int g2 = 0; g2 < KG; ++g2) o += accs[g2][t];
+      out[t] = o;
+    }
+    if (t == 0) {
+      out[D] = m;
+      out[D + 1] = l;
+    }
   }
 }
 
 template <int D>
 __global__ void __launch_bounds__(D) attn_decode_combine_kernel(const __grid_constant__ AttnParams p,
                                                                 const float* __restrict__ part, int n_split) {
+  // The splits' (m_s, l_s) are staged in shared memory in one round of loads; every thread then
+  // needs only its own column of the partial outputs (independent loads, unrolled).
+  constexpr int kMaxStage = 512;
+  __shared__ float sm_m[kMaxStage], sm_l[kMaxStage];
   const int t = threadIdx.x;
   const int64_t row = blockIdx.x;
   const int q = (int)(row % p.Sq);
   const int64_t bgh = row / p.Sq;
   const int h = (int)(bgh % p.Hq), g = (int)((bgh / p.Hq) % p.G), b = (int)(bgh / ((int64_t)p.Hq * p.G));
   const float* pr = part + row * n_split * (D + 2);
+  const int ns = min(n_split, kMaxStage);
+  for (int s = t; s < ns; s += D) {
+    sm_m[s] = pr[s * (D + 2) + D];
+    sm_l[s] = pr[s * (D + 2) + D + 1];
+  }
+  __syncthreads();
   float M = -INFINITY;
-  for (int s = 0; s < n_split; ++s) M = fmaxf(M, pr[s * (D + 2) + D]);
+  for (int s = 0; s < n_split; ++s) M = fmaxf(M, s < ns ? sm_m[s] : pr[s * (D + 2) + D]);
   float L = 0.f, o = 0.f;
   if (M != -INFINITY) {
+#pragma unroll 8
     for (int s = 0; s < n_split; ++s) {
-      const float ms = pr[s * (D + 2) + D];
-      if (ms == -INFINITY) continue;
-      const float f = ex2(ms - M);
-      L = fmaf(pr[s * (D + 2) + D + 1], f, L);
+      const float ms = s < ns ? sm_m[s] : pr[s * (D + 2) + D];
+      const float ls = s < ns ? sm_l[s] : pr[s * (D + 2) + D + 1];
+      const float f = ms == -INFINITY ? 0.f : ex2(ms - M);
+      L = fmaf(ls, f, L);
       o = fmaf(pr[s * (D + 2) + t], f, o);
     }
   }
@@ -236,17 +363,25 @@ size_t decode_workspace_bytes(const AttnParams& p, int n_sms) {
   return (size_t)p.B * p.G * p.Hq * p.Sq * ns * (p.Dv + 2) * sizeof(float);
 }
 
-cudaError_t launch_attn_decode(const AttnParams& p, float* part, int n_sms, cudaStream_t stream) {
+cudaError_t launch_attn_decode(const AttnParams& p, const TmaMaps& maps, float* part, int n_sms, cudaStream_t stream) {
   int bps, ns;
   decode_plan(p, n_sms, &bps, &ns);
   const long long rows = (long long)p.B * p.G * p.Hq * p.Sq;
+  const long long items = rows * ns;
   if (rows > 65535LL * 32768LL) return cudaErrorInvalidValue;
-  dim3 grid(ns, (unsigned)rows);
+  const int grid = (int)std::min<long long>(items, n_sms > 0 ? n_sms : 148);   // persistent
+  cudaError_t e;
   if (p.Dqk == 128) {
-    attn_decode_split_kernel<128><<<grid, kDecThreads, 0, stream>>>(p, part, bps);
+    e = cudaFuncSetAttribute(attn_decode_split_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             DecCfg<128>::SMEM);
+    if (e != cudaSuccess) return e;
+    attn_decode_split_kernel<128><<<grid, kDecCompute + 32, DecCfg<128>::SMEM, stream>>>(p, maps, part, bps, ns, items);
     attn_decode_combine_kernel<128><<<(unsigned)rows, 128, 0, stream>>>(p, part, ns);
   } else {
-    attn_decode_split_kernel<64><<<grid, kDecThreads, 0, stream>>>(p, part, bps);
+    e = cudaFuncSetAttribute(attn_decode_split_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             DecCfg<64>::SMEM);
+    if (e != cudaSuccess) return e;
+    attn_decode_split_kernel<64><<<grid, kDecCompute + 32, DecCfg<64>::SMEM, stream>>>(p, maps, part, bps, ns, items);
     attn_decode_combine_kernel<64><<<(unsigned)rows, 64, 0, stream>>>(p, part, ns);
   }
   return cudaGetLastError();

@@ -35,7 +35,7 @@ bool rsa_select_small_ok(const RsaSelParams& p);
 cudaError_t launch_rsa_select_small(const RsaSelParams& p, const void* q, int64_t qsb, int64_t qsg, int64_t qsh,
                                     int64_t qss, const void* kmin, const void* kmax, cudaStream_t stream);
 size_t decode_workspace_bytes(const AttnParams& p, int n_sms);
-cudaError_t launch_attn_decode(const AttnParams& p, float* part, int n_sms, cudaStream_t stream);
+cudaError_t launch_attn_decode(const AttnParams& p, const TmaMaps& maps, float* part, int n_sms, cudaStream_t stream);
 cudaError_t debug_timing(unsigned long long* out, int reset);
 }  // namespace fl
 
@@ -462,7 +462,7 @@ fl_status launch_prepared(Prepared& P, const fl_attn_args* a) {
     P.p.keybits = bits;
   }
   if (P.bf16 && P.decode) {
-    e = launch_attn_decode(P.p, reinterpret_cast<float*>(static_cast<char*>(a->workspace) + P.decode_off),
+    e = launch_attn_decode(P.p, maps, reinterpret_cast<float*>(static_cast<char*>(a->workspace) + P.decode_off),
                            device_sm_count(), stream);
     ++g_launches;                                       // split + combine
   } else if (P.bf16) {
