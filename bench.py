@@ -405,7 +405,8 @@ def rsa_job(name, rank, world, device, with_host=True):
                                             for i in range(nqb)) * B * H   # executed GEMM tiles
     sel_bytes = q.numel() * 2 + 2 * kmin.numel() * 2 + idx.numel() * 4 + cnt.numel() * 4
     job.calls.append(Call("rsa_select", lambda: fl.rsa_select(q, kmin, kmax, S, topk=topk, blk_idx=idx, blk_cnt=cnt),
-                          sel_flops, sel_bytes, "hbm" if decode else "tensor", kernel="rsa_select_kernel"))
+                          sel_flops, sel_bytes, "hbm" if decode else "tensor",
+                          kernel="rsa_select_small_kernel" if decode else "rsa_select_kernel"))
     if decode:   # each listed KV block is read once per (b,h): K + V rows
         att_bytes = q.numel() * 2 + out.numel() * 2 + listed * 128 * D * 2 * 2
     else:        # K/V read once per (b,h) (a block listed by several q-blocks is re-read from L2)
@@ -413,7 +414,8 @@ def rsa_job(name, rank, world, device, with_host=True):
     ws = torch.empty(1 << 20, dtype=torch.uint8, device=device)
     job.calls.append(Call("attn_blocklist", lambda: fl.attn_fwd(q, k, v, out=out, mask="blocklist", blk_idx=idx,
                                                                 blk_cnt=cnt, workspace=ws), flops, att_bytes,
-                          "hbm" if decode else "tensor", kernel="attn_tc_kernel"))
+                          "hbm" if decode else "tensor",
+                          kernel="attn_decode_split_kernel" if decode else "attn_tc_kernel"))
     job.step_flops = flops
     job.extra.update(listed_blocks=listed, kv_blocks=nkb * B * H * nqb, rsa_decode=decode)
     job.parity = {"host": {"q": qh, "k": kh, "v": vh}, "out": out, "idx": idx, "cnt": cnt, "kmin": kmin,

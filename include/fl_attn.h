@@ -158,6 +158,17 @@ fl_status fl_attn_fwd_host(const fl_attn_args* host_args, void* device_scratch, 
 fl_status fl_rsa_build_summaries(const fl_tensor* k, fl_tensor* kmin, fl_tensor* kmax,
                                  int32_t blk_k, void* stream);
 
+/* Incremental summary maintenance after a KV append (RSA's decode loop, P:L47,
+ * P:L443 name only): k is the whole cache after the append (S_k keys), kmin/kmax as for
+ * fl_rsa_build_summaries with n_kblk = ceil(S_k / blk_k), already valid for keys [0, k_begin).
+ * Recomputes exactly the blocks floor(k_begin / blk_k) .. n_kblk - 1 (the one the append started
+ * in, which may have been partial, and every new one); the rest is untouched.  The result equals
+ * fl_rsa_build_summaries on the whole cache bit for bit.  k_begin >= 0 (no launch when
+ * floor(k_begin / blk_k) >= n_kblk).
+ * Same argument checks, errors and ownership as fl_rsa_build_summaries; one launch (none if no block). */
+fl_status fl_rsa_update_summaries(const fl_tensor* k, fl_tensor* kmin, fl_tensor* kmax,
+                                  int32_t blk_k, int64_t k_begin, void* stream);
+
 /* RSA selection (reading G10/G11): for each (b, g, h, q-block i of blk_q rows) with diagonal block
  *   c = min(floor(q_abs(last row of block i) / blk_k), n_kblk - 1)   (q_abs per causal_align, G12),
  *   score_j = max_{q in block i, h' in h's KV group} sum_d max(q_d kmax_jd, q_d kmin_jd),  0 < j < c;

@@ -15,7 +15,7 @@ FL_BF16, FL_F32, FL_U8, FL_I32 = 0, 1, 2, 3
 ABI_VERSION = 1
 
 EXPORTS = ["fl_attn_fwd", "fl_attn_workspace_size", "fl_attn_host_scratch_size", "fl_attn_fwd_host",
-           "fl_rsa_build_summaries", "fl_rsa_select", "fl_shard_range", "fl_diag_umma_gemm",
+           "fl_rsa_build_summaries", "fl_rsa_update_summaries", "fl_rsa_select", "fl_shard_range", "fl_diag_umma_gemm",
            "fl_status_string", "fl_last_error", "fl_abi_version", "fl_launch_count", "fl_debug_timing"]
 
 
@@ -66,6 +66,8 @@ def lib():
         L.fl_attn_fwd_host.argtypes = [C.POINTER(AttnArgs), C.c_void_p, C.c_size_t]
         L.fl_rsa_build_summaries.argtypes = [C.POINTER(Tensor), C.POINTER(Tensor), C.POINTER(Tensor), C.c_int32,
                                              C.c_void_p]
+        L.fl_rsa_update_summaries.argtypes = [C.POINTER(Tensor), C.POINTER(Tensor), C.POINTER(Tensor), C.c_int32,
+                                              C.c_int64, C.c_void_p]
         L.fl_rsa_select.argtypes = [C.POINTER(Tensor), C.POINTER(Tensor), C.POINTER(Tensor), C.c_int32, C.c_int32,
                                     C.c_int32, C.c_int32, C.c_int32, C.POINTER(Tensor), C.POINTER(Tensor),
                                     C.c_void_p]
@@ -82,7 +84,7 @@ def lib():
         L.fl_launch_count.argtypes = [C.c_int32]
         L.fl_launch_count.restype = C.c_int64
         for name in ("fl_attn_fwd", "fl_attn_workspace_size", "fl_attn_host_scratch_size", "fl_attn_fwd_host",
-                     "fl_rsa_build_summaries", "fl_rsa_select", "fl_diag_umma_gemm"):
+                     "fl_rsa_build_summaries", "fl_rsa_update_summaries", "fl_rsa_select", "fl_diag_umma_gemm"):
             getattr(L, name).restype = C.c_int
         if L.fl_abi_version() != ABI_VERSION:
             raise RuntimeError("libfl_attn.so ABI version mismatch")

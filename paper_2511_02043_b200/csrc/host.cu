@@ -27,7 +27,7 @@ cudaError_t launch_diag_gemm(int n, int k, const CUtensorMap& ta, const CUtensor
                              bool bmn, bool atmem, cudaStream_t s);
 int tc_chunk_elems(int D);
 cudaError_t launch_rsa_summaries(const void* k, int64_t sb, int64_t sg, int64_t sh, int64_t ss, int B, int G, int H,
-                                 int Sk, int D, int blk, void* kmin, void* kmax, cudaStream_t stream);
+                                 int Sk, int D, int blk, int j0, void* kmin, void* kmax, cudaStream_t stream);
 cudaError_t launch_rsa_select(const RsaSelParams& p, const CUtensorMap& tq, const CUtensorMap& tmin,
                               const CUtensorMap& tmax, cudaStream_t stream);
 int rsa_select_max_blocks(int D);
@@ -636,10 +636,12 @@ fl_status fl_diag_umma_gemm(const void* a, const void* b, float* c, int32_t n, i
   return e == cudaSuccess ? FL_OK : cuda_fail(e, "diag gemm launch");
 }
 
-fl_status fl_rsa_build_summaries(const fl_tensor* k, fl_tensor* kmin, fl_tensor* kmax, int32_t blk_k, void* stream) {
+static fl_status rsa_summaries(const fl_tensor* k, fl_tensor* kmin, fl_tensor* kmax, int32_t blk_k, int64_t k_begin,
+                               void* stream) {
   if (!k || !kmin || !kmax || !k->data || !kmin->data || !kmax->data)
     return fail(FL_ERR_INVALID_ARGUMENT, "rsa_build_summaries: k, kmin, kmax are required");
   if (blk_k <= 0) return fail(FL_ERR_INVALID_ARGUMENT, "rsa_build_summaries: blk_k must be > 0");
+  if (k_begin < 0) return fail(FL_ERR_INVALID_ARGUMENT, "rsa_update_summaries: k_begin must be >= 0");
   if (k->dtype != FL_BF16 || kmin->dtype != FL_BF16 || kmax->dtype != FL_BF16)
     return fail(FL_ERR_UNSUPPORTED, "rsa_build_summaries: bf16 only");
   if (k->rank != 4 && k->rank != 5) return fail(FL_ERR_INVALID_ARGUMENT, "rsa_build_summaries: k rank 4 or 5");
@@ -660,9 +662,19 @@ fl_status fl_rsa_build_summaries(const fl_tensor* k, fl_tensor* kmin, fl_tensor*
   if (B * G * H > 65535) return fail(FL_ERR_UNSUPPORTED, "rsa_build_summaries: B*G*H > 65535");
   cudaError_t e = launch_rsa_summaries(kv.data, kv.size[0] > 1 ? kv.stride[0] : 0, kv.size[1] > 1 ? kv.stride[1] : 0,
                                        kv.size[2] > 1 ? kv.stride[2] : 0, kv.stride[3], (int)B, (int)G, (int)H, (int)Sk,
-                                       (int)D, blk_k, kmin->data, kmax->data, static_cast<cudaStream_t>(stream));
+                                       (int)D, blk_k, (int)std::min<int64_t>(k_begin / blk_k, nkb), kmin->data,
+                                       kmax->data, static_cast<cudaStream_t>(stream));
   ++g_launches;
   return e == cudaSuccess ? FL_OK : cuda_fail(e, "rsa_summaries launch");
+}
+
+fl_status fl_rsa_build_summaries(const fl_tensor* k, fl_tensor* kmin, fl_tensor* kmax, int32_t blk_k, void* stream) {
+  return rsa_summaries(k, kmin, kmax, blk_k, 0, stream);
+}
+
+fl_status fl_rsa_update_summaries(const fl_tensor* k, fl_tensor* kmin, fl_tensor* kmax, int32_t blk_k, int64_t k_begin,
+                                  void* stream) {
+  return rsa_summaries(k, kmin, kmax, blk_k, k_begin, stream);
 }
 
 fl_status fl_rsa_select(const fl_tensor* q, const fl_tensor* kmin, const fl_tensor* kmax, int32_t s_k, int32_t topk,

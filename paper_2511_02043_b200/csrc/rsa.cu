@@ -32,13 +32,13 @@ namespace fl {
 // grid (n_kblk, BGH), 128 threads.  K row r of block j is K[bgh][j*blk + r][:].
 __global__ void __launch_bounds__(128) rsa_summaries_kernel(const __nv_bfloat16* __restrict__ k, int64_t sb,
                                                             int64_t sg, int64_t sh, int64_t ss, int B, int G, int H,
-                                                            int Sk, int D, int blk, __nv_bfloat16* __restrict__ kmin,
+                                                            int Sk, int D, int blk, int j0, __nv_bfloat16* __restrict__ kmin,
                                                             __nv_bfloat16* __restrict__ kmax) {
   __shared__ uint4 red_min[128], red_max[128];
-  const int j = blockIdx.x;
+  const int j = j0 + blockIdx.x;                       // blocks [j0, nkb): all of them, or the tail after a KV append
   const int bgh = blockIdx.y;
   const int h = bgh % H, g = (bgh / H) % G, b = bgh / (H * G);
-  const int nkb = gridDim.x;
+  const int nkb = (Sk + blk - 1) / blk;
   const int nch = D / 8;                       // 16-byte chunks per row
   const int rows_par = 128 / nch;              // rows handled in parallel
   const int t = threadIdx.x;
@@ -84,11 +84,12 @@ __global__ void __launch_bounds__(128) rsa_summaries_kernel(const __nv_bfloat16*
 }
 
 cudaError_t launch_rsa_summaries(const void* k, int64_t sb, int64_t sg, int64_t sh, int64_t ss, int B, int G, int H,
-                                 int Sk, int D, int blk, void* kmin, void* kmax, cudaStream_t stream) {
+                                 int Sk, int D, int blk, int j0, void* kmin, void* kmax, cudaStream_t stream) {
   const int nkb = (Sk + blk - 1) / blk;
-  dim3 grid(nkb, B * G * H);
+  if (j0 >= nkb) return cudaSuccess;
+  dim3 grid(nkb - j0, B * G * H);
   rsa_summaries_kernel<<<grid, 128, 0, stream>>>(static_cast<const __nv_bfloat16*>(k), sb, sg, sh, ss, B, G, H, Sk,
-                                                 D, blk, static_cast<__nv_bfloat16*>(kmin),
+                                                 D, blk, j0, static_cast<__nv_bfloat16*>(kmin),
                                                  static_cast<__nv_bfloat16*>(kmax));
   return cudaGetLastError();
 }

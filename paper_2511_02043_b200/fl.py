@@ -175,6 +175,16 @@ def rsa_build_summaries(k: torch.Tensor, blk_k: int = 128, kmin=None, kmax=None,
     return kmin, kmax
 
 
+def rsa_update_summaries(k: torch.Tensor, kmin: torch.Tensor, kmax: torch.Tensor, k_begin: int, blk_k: int = 128,
+                         stream=None):
+    """Refresh the summaries of the blocks from floor(k_begin / blk_k) on after a KV append
+    (fl_rsa_update_summaries); k is the whole cache, kmin / kmax sized for it.  Returns (kmin, kmax)."""
+    tk, tmn, tmx = tensor(k), tensor(kmin), tensor(kmax)
+    _lib.check(_lib.lib().fl_rsa_update_summaries(C.byref(tk), C.byref(tmn), C.byref(tmx), int(blk_k), int(k_begin),
+                                                  _stream_handle(k.device, stream)))
+    return kmin, kmax
+
+
 def rsa_select(q: torch.Tensor, kmin: torch.Tensor, kmax: torch.Tensor, s_k: int, *, topk: int = 16,
                blk_q: int = 128, blk_k: int = 128, causal_align: int = 0, max_sel=None, blk_idx=None,
                blk_cnt=None, stream=None):

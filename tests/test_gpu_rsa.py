@@ -46,6 +46,35 @@ def test_summaries_rank5_strided(fl):
     assert np.array_equal(kmax.cpu().double().numpy(), rmax)
 
 
+@pytest.mark.parametrize("s1,s2,blk", [(640, 1000, 128), (600, 1000, 128), (1000, 1001, 128), (0, 300, 64),
+                                       (777, 777, 128)])
+def test_summaries_update_after_append(fl, s1, s2, blk):
+    """KV append: summaries valid for keys [0, s1), cache grows to s2, update from
+    k_begin = s1 -> bit-equal to the oracle's summaries of the whole cache; blocks before
+    floor(s1 / blk) are not rewritten (sentinel preserved)."""
+    k = synth.uniform((1, 2, s2, 64), seed=5, tensor="k")
+    kd = k.cuda()
+    nkb = (s2 + blk - 1) // blk
+    kmin = torch.full((2, nkb, 64), 7.0, device="cuda", dtype=torch.bfloat16)
+    kmax = torch.full((2, nkb, 64), 7.0, device="cuda", dtype=torch.bfloat16)
+    j0 = s1 // blk
+    if s1 > 0:                                   # the pre-append state: summaries of [0, s1)
+        pmin, pmax = fl.rsa_build_summaries(kd[:, :, :s1], blk)
+        kmin[:, :j0] = pmin[:, :j0]
+        kmax[:, :j0] = pmax[:, :j0]
+    fl.rsa_update_summaries(kd, kmin, kmax, s1, blk)
+    torch.cuda.synchronize()
+    rmin, rmax = oracle.rsa_summaries(k, blk)
+    assert np.array_equal(kmin.cpu().double().numpy(), rmin)
+    assert np.array_equal(kmax.cpu().double().numpy(), rmax)
+    sentinel = torch.full((2, nkb, 64), 7.0, dtype=torch.bfloat16)
+    kmin2 = sentinel.clone().cuda()
+    fl.rsa_update_summaries(kd, kmin2, sentinel.clone().cuda(), s2, blk)     # k_begin = S_k: only the tail block
+    torch.cuda.synchronize()
+    keep = (s2 // blk)
+    assert torch.equal(kmin2[:, :keep].cpu(), sentinel[:, :keep])
+
+
 # ------------------------------------------------------------------ selection (G11)
 def selection_eps(q, kmin, kmax, Hq, Hkv):
     """G11 bound on the fp32 accumulation error of one score, maxed over blocks/queries:
