@@ -797,12 +797,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 #endif
     const uint4* gp = reinterpret_cast<const uint4*>(static_cast<const unsigned short*>(p.gate) + w.b * p.gs.b +
                                                      gw * p.gs.g + (int64_t)w.h * p.gs.h + (int64_t)q * p.gs.s);
-    constexpr bool kGateEarly = D <= 32;               // small head: the whole gate row is 4 registers x 4
-    uint4 gv[kGateEarly ? D / 8 : 1];                  // in flight while the last PV runs
-    if (kGateEarly && gated) {
-#pragma unroll
-      for (int t = 0; t < (kGateEarly ? D / 8 : 1); ++t) gv[t] = __ldg(gp + t);
-    }
+    // the gate row (64 B at c = 32) is pulled into L1 while the last PV runs; holding it in registers
+    // made the compiler spill it right after the load (the spill store then waited for the load)
+    if (D <= 32 && gated) asm volatile("prefetch.global.L1 [%0];" ::"l"(gp) : "memory");
     if (n_done > 0) {
       mbar_wait(&o_full[wg], o_cnt & 1);
       ++o_cnt;
@@ -893,7 +890,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 #pragma unroll
           uint4 g4[4];
 #pragma unroll
-          for (int t8 = 0; t8 < 4; ++t8) g4[t8] = kGateEarly ? gv[kGateEarly ? (c >> 3) + t8 : 0] : __ldg(gp + (c >> 3) + t8);
+          for (int t8 = 0; t8 < 4; ++t8) g4[t8] = __ldg(gp + (c >> 3) + t8);
 #pragma unroll
           for (int t8 = 0; t8 < 4; ++t8) {
             const uint4 u4 = g4[t8];
