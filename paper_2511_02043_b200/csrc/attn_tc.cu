@@ -27,6 +27,7 @@
 //  * Masks are per-row key intervals (masks.cuh): KV tiles outside the union
 //    are never loaded, tiles inside every row's interval run mask-free, only
 //    boundary tiles pay two compares per element.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -105,6 +106,11 @@ struct TcCfg {
   static constexpr int SMEM_TOTAL = SMEM_ML + (LIST ? 2 * 128 * 4 : 0) + 1024;  // + alignment slack
   static constexpr uint32_t IDESC_S = idesc_bf16_f32(128, BN, 0);   // Q (K-major) x K (K-major)
   static constexpr uint32_t IDESC_O = idesc_bf16_f32(128, D, 1);    // P (TMEM) x V (MN-major)
+  // Small heads with a TMA'd pair bias: the tensor core adds it, S += (c I) . Bias with c = 1/scale
+  // split into two bf16 terms (c_hi + c_lo, relative error ~2e-7); the scaled identities live in TMEM
+  // (A operand, 64 columns each, after O1) and the bias tile is the MN-major B operand (like V).
+  static constexpr uint32_t COL_ID = 256 + 2 * D;
+  static constexpr uint32_t IDESC_B = idesc_bf16_f32(128, 128, 1);
   static constexpr int ENTRIES_PER_TILE = DIFF ? 3 : 2;              // K0 [K1] V
 };
 
@@ -266,6 +272,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bias_empty + 4);
   uint8_t* sBias = smem + C::SMEM_BIAS;
   const bool bias_tma = C::BIAS_TMA_OK && BIAS && maps.bias_tma;
+  const bool bias_mma = bias_tma && MOD == MOD_NONE;  // raw-score domain: S += bias / scale on the tensor core
   uint32_t* sched_base = reinterpret_cast<uint32_t*>(smem + C::SMEM_SCHED);
 
   const int warp = threadIdx.x >> 5;
@@ -286,7 +293,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       mbar_init(&unit_empty[i], 1 + 256);            // MMA lane + both softmax warpgroups
       for (int st = 0; st < 2; ++st) {
         mbar_init(&bias_full[i * 2 + st], 1);
-        mbar_init(&bias_empty[i * 2 + st], 128);     // the warpgroup's threads, after reading their rows
+        // the warpgroup's threads after reading their rows, or the MMA commit when the tensor core adds it
+        mbar_init(&bias_empty[i * 2 + st], bias_mma ? 1 : 128);
       }
     }
     fence_mbar_init();
@@ -296,6 +304,34 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (bias_mma) {
+    // scaled identities c_hi I, c_lo I (bf16 pairs per 32-bit column: row r's entry at column r / 2)
+    if (warp < 4) {
+      const int r = threadIdx.x;
+      const float cf = 1.f / p.scale;
+      const float c_hi = __bfloat162float(__float2bfloat16_rn(cf));
+      const float c_lo = cf - c_hi;
+      const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+#pragma unroll
+      for (int t2 = 0; t2 < 2; ++t2) {
+        const float cv = t2 ? c_lo : c_hi;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          uint32_t v[32];
+#pragma unroll
+          for (int w2 = 0; w2 < 32; ++w2) {
+            const int word = half * 32 + w2;
+            v[w2] = word == (r >> 1) ? pack_bf16((r & 1) ? 0.f : cv, (r & 1) ? cv : 0.f) : 0u;
+          }
+          tmem_st32(tmem + lane_base + C::COL_ID + t2 * 64 + half * 32, v);
+        }
+      }
+      tmem_wait_st();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
 
   // Dynamic persistent scheduling: the producer claims units (first blockIdx.x, then
   // gridDim.x + atomicAdd(tile_ctr)) in the (b,h)-major, heaviest-first order of
@@ -431,6 +467,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         ++e;
         return slot;
       };
+      int bcnt_m[2] = {0, 0};                          // bias tiles consumed per warpgroup (bias_mma)
+      const uint32_t sbias_addr = smem_u32(sBias);
       auto issue_s = [&](int i, int kslot) {
         const uint32_t qa = sq_addr + (LIST ? 0 : i) * C::TILE_BYTES, ka = ring_addr + kslot * C::TILE_BYTES;
 #pragma unroll
@@ -438,6 +476,20 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           const uint32_t off = (kk * 16 / C::CH) * C::CHUNK_BYTES + (kk * 16 % C::CH) * 2;
           umma_ss(tmem + (i ? C::COL_S1 : C::COL_S0), smem_desc(qa + off, 16, C::SBO, C::LAYOUT),
                   smem_desc(ka + off, 16, C::SBO, C::LAYOUT), C::IDESC_S, kk > 0);
+        }
+        if (bias_mma) {                                // S_i += (c_hi I + c_lo I) . Bias tile
+          const int st = bcnt_m[i] & 1;
+          mbar_wait(&bias_full[i * 2 + st], (bcnt_m[i] >> 1) & 1);
+          tc_fence_after();
+          const uint32_t ba = sbias_addr + (i * 2 + st) * C::BIAS_TILE;
+#pragma unroll
+          for (int t2 = 0; t2 < 2; ++t2)
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+              umma_ts(tmem + (i ? C::COL_S1 : C::COL_S0), tmem + C::COL_ID + t2 * 64 + kk * 8,
+                      smem_desc(ba + kk * 16 * 128, C::BIAS_TILE / 2, 1024, kLayoutSW128), C::IDESC_B, 1u);
+          umma_commit(&bias_empty[i * 2 + st]);
+          ++bcnt_m[i];
         }
         umma_commit(&s_full[i]);
       };
@@ -603,7 +655,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         }
         x[c] = v;
       }
-      if (BIAS) {  // additive bias (Evoformer pair bias), then softcap if any (order G16)
+      if (BIAS && !bias_mma) {  // additive bias (Evoformer pair bias), then softcap if any (order G16)
         if (bias_tma) {
           // this row of the bias tile from shared memory: slab c holds keys [64c, 64c+64), 16-byte
           // chunk k of row r at (k ^ (r & 7)) -- the TMA 128-B swizzle, so 8 consecutive rows hit
