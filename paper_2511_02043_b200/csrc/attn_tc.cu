@@ -640,18 +640,25 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       FL_T(2);                                         // 2: tcgen05.ld of S
       // ---- score modification (Eq.4) in the log2 domain: x = log2(e) * mod(scale * s)
       float x[128];
-      // kRaw: keep raw s (an additive bias enters as bias / scale); scale * log2(e) folds into the exp FFMA
-      constexpr bool kRaw = MOD == MOD_NONE;
+      // The log2-domain score is x * xscale + delta, with the per-element work kept minimal:
+      //  * kRaw (none / ALiBi): x = s + bias / scale + (slope / scale) * c, xscale = scale * log2(e),
+      //    delta = slope * log2(e) * (k0 - q_abs) (per row and tile) -- one FFMA per element for ALiBi;
+      //  * softcap without bias: x = tanh(s * scale / cap), xscale = cap * log2(e), delta = 0;
+      //  * softcap with bias: x in log2 units (G16 order: bias before the cap), xscale = 1.
+      // xscale and delta fold into the row max (a scalar op) and into the exp FFMA.
+      constexpr bool kRaw = MOD == MOD_NONE || MOD == MOD_ALIBI;
       const float bias_k = kRaw ? 1.f / p.scale : kLog2e;
-      const float alibi_base = slope_l2 * (float)(k0 - q_abs);
+      const float delta = MOD == MOD_ALIBI ? slope_l2 * (float)(k0 - q_abs) : 0.f;
+      const float slope_r = MOD == MOD_ALIBI ? slope_l2 / sc_l2 : 0.f;
 #pragma unroll
       for (int c = 0; c < 128; ++c) {
         float v = __uint_as_float(s[c]);
         if (MOD == MOD_SOFTCAP && !BIAS) {
-          v = cap_out * tanh_approx(v * cap_in);
+          v = tanh_approx(v * cap_in);
+        } else if (MOD == MOD_ALIBI) {
+          v = fmaf(slope_r, (float)c, v);
         } else if (!kRaw) {
           v *= sc_l2;
-          if (MOD == MOD_ALIBI) v += fmaf(slope_l2, (float)c, alibi_base);
         }
         x[c] = v;
       }
@@ -762,8 +769,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         mt2 = fmax3(mt2, x[c + 4], x[c + 5]);
         mt3 = fmax3(mt3, x[c + 6], x[c + 7]);
       }
-      const float xscale = kRaw ? sc_l2 : 1.f;        // x * xscale is the log2-domain score
-      const float mt = fmaxf(fmaxf(mt0, mt1), fmaxf(mt2, mt3)) * xscale;
+      const float xscale = kRaw ? sc_l2 : (MOD == MOD_SOFTCAP && !BIAS ? cap_out : 1.f);
+      const float mt = fmaf(fmaxf(fmaxf(mt0, mt1), fmaxf(mt2, mt3)), xscale, delta);   // -inf stays -inf
       FL_T(3);                                         // 3: score mod + mask + row max
       const bool rescale = mt > m_ref + kTau;          // also true for the first finite tile (m_ref = -inf)
       const float factor = rescale ? ex2(m_ref - mt) : 1.f;
@@ -783,7 +790,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         l *= factor;
         m_ref = mt;
       }
-      const float neg_m = m_ref == -INFINITY ? 0.f : -m_ref;
+      const float neg_m = (m_ref == -INFINITY ? 0.f : -m_ref) + delta;   // exp2(x * xscale + delta - m_ref)
       // Ping-pong: the two warpgroups take turns on the MUFU (exp) pipe for the
       // tiles both need, so each exp loop runs at full rate while the tensor
       // pipe works for the other warpgroup (CTA-local named barriers 2 and 3).
