@@ -104,6 +104,13 @@ for D in (128, 64, 32):
         dict(name=f"bias_needle_D{D}", Hq=2, S=260, D=D, bias="bf16", dist="needle"),
         dict(name=f"keymask_const_D{D}", S=300, D=D, key_mask=True, p_zero=0.2, dist="constant"),
         dict(name=f"sq_ne_sk_D{D}", Sq=200, Sk=333, D=D, mask="causal", dist="needle"),
+        # score-mod combinations (raw-score domain for ALiBi + bias, log2 domain for softcap + bias, G16)
+        dict(name=f"alibi_bias_causal_D{D}", Hq=2, S=300, D=D, mod="alibi", bias="bf16", mask="causal",
+             dist="needle"),
+        dict(name=f"softcap_bias_D{D}", Hq=2, S=260, D=D, mod="softcap", softcap=5.0, bias="bf16", dist="needle"),
+        dict(name=f"alibi_custom_keymask_D{D}", Hq=4, S=300, D=D, mod="alibi", alibi_custom=True, key_mask=True,
+             p_zero=0.2, dist="constant"),
+        dict(name=f"bias_f32_gate_mul_D{D}", Hq=2, S=200, D=D, bias="f32", gate_mode="mul", dist="constant"),
     ]
 
 
