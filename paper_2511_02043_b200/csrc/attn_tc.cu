@@ -63,10 +63,20 @@ constexpr int kThreadsTc = 384;
 // bounds 384 x 1); the control warpgroup gives registers back and the two softmax
 // warpgroups take them.  inc blocks until the CTA's pool can pay, so the split
 // must fit in what the CTA owns or the second softmax WG deadlocks.
-constexpr uint32_t kRegsLaunch = 168, kRegsCtl = 88, kRegsSoftmax = 208;
+// Measured per head dim (profiles/r01b_ab_regs.txt): D >= 64 gains from 216 softmax registers (ALiBi
+// +2 %, diff +4 %, causal =), the small-head kernels keep 208 (evo_row -6 % at 216).
+#ifndef FL_REGS_CTL
+#define FL_REGS_CTL(D) ((D) >= 64 ? 72 : 88)
+#define FL_REGS_SOFTMAX(D) ((D) >= 64 ? 216 : 208)
+#endif
+constexpr uint32_t kRegsLaunch = 168;
+template <int D>
+struct RegCfg {
+  static constexpr uint32_t CTL = FL_REGS_CTL(D), SOFTMAX = FL_REGS_SOFTMAX(D);
+  static_assert(2 * 128 * SOFTMAX + 128 * CTL <= kThreadsTc * kRegsLaunch, "setmaxnreg split exceeds CTA pool");
+};
 // FL_MASK_BLOCKLIST: at most this many listed KV blocks per query block on the bf16 path.
 constexpr int kMaxSelTc = 256;
-static_assert(2 * 128 * kRegsSoftmax + 128 * kRegsCtl <= kThreadsTc * kRegsLaunch, "setmaxnreg split exceeds CTA pool");
 
 // LIST (RSA block lists): both warpgroups work on the SAME 128-row query block and split its
 // listed KV blocks (WG0 entries 0, 2, 4, ..., WG1 entries 1, 3, 5, ...), each with its own
@@ -350,7 +360,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   auto release_unit = [&](int it) { mbar_arrive(&unit_empty[it & 1]); };
 
   if (warp >= 8) {
-   regs_dec<kRegsCtl>();
+   regs_dec<RegCfg<D>::CTL>();
    if (warp == 8) {
     // ============================== TMA producer ==============================
     if (lane == 0) {
@@ -566,7 +576,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     }
    }
   } else {
-    regs_inc<kRegsSoftmax>();
+    regs_inc<RegCfg<D>::SOFTMAX>();
 #ifdef FL_TIMING
     long long t_acc[16] = {0};
     long long t_prev = clock64();
