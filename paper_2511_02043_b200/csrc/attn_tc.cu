@@ -63,16 +63,17 @@ constexpr int kThreadsTc = 384;
 // bounds 384 x 1); the control warpgroup gives registers back and the two softmax
 // warpgroups take them.  inc blocks until the CTA's pool can pay, so the split
 // must fit in what the CTA owns or the second softmax WG deadlocks.
-// Measured per head dim (profiles/r01b_ab_regs.txt): D >= 64 gains from 216 softmax registers (ALiBi
-// +2 %, diff +4 %, causal =), the small-head kernels keep 208 (evo_row -6 % at 216).
+// Measured (profiles/r01b_ab_regs.txt): differential attention and ALiBi gain from 216 softmax registers
+// (diff 699 -> 727, ALiBi 1022 -> 1040 TF/s), softcap / sliding / document lose 2-4 % and the small
+// heads 6 %, plain causal is neutral -> 216 only for DIFF and ALiBi.
 #ifndef FL_REGS_CTL
-#define FL_REGS_CTL(D) ((D) >= 64 ? 72 : 88)
-#define FL_REGS_SOFTMAX(D) ((D) >= 64 ? 216 : 208)
+#define FL_REGS_CTL(W) ((W) ? 72 : 88)
+#define FL_REGS_SOFTMAX(W) ((W) ? 216 : 208)
 #endif
 constexpr uint32_t kRegsLaunch = 168;
-template <int D>
+template <bool WIDE>
 struct RegCfg {
-  static constexpr uint32_t CTL = FL_REGS_CTL(D), SOFTMAX = FL_REGS_SOFTMAX(D);
+  static constexpr uint32_t CTL = FL_REGS_CTL(WIDE), SOFTMAX = FL_REGS_SOFTMAX(WIDE);
   static_assert(2 * 128 * SOFTMAX + 128 * CTL <= kThreadsTc * kRegsLaunch, "setmaxnreg split exceeds CTA pool");
 };
 // FL_MASK_BLOCKLIST: at most this many listed KV blocks per query block on the bf16 path.
@@ -360,7 +361,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   auto release_unit = [&](int it) { mbar_arrive(&unit_empty[it & 1]); };
 
   if (warp >= 8) {
-   regs_dec<RegCfg<D>::CTL>();
+   regs_dec<RegCfg<(DIFF || MOD == MOD_ALIBI)>::CTL>();
    if (warp == 8) {
     // ============================== TMA producer ==============================
     if (lane == 0) {
@@ -576,7 +577,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     }
    }
   } else {
-    regs_inc<RegCfg<D>::SOFTMAX>();
+    regs_inc<RegCfg<(DIFF || MOD == MOD_ALIBI)>::SOFTMAX>();
 #ifdef FL_TIMING
     long long t_acc[16] = {0};
     long long t_prev = clock64();
