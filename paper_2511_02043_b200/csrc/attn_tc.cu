@@ -63,7 +63,7 @@ constexpr int kThreadsTc = 384;
 // bounds 384 x 1); the control warpgroup gives registers back and the two softmax
 // warpgroups take them.  inc blocks until the CTA's pool can pay, so the split
 // must fit in what the CTA owns or the second softmax WG deadlocks.
-// Measured (profiles/r01b_ab_regs.txt): differential attention and ALiBi gain from 216 softmax registers
+// Measured (profiles/r01b_ab_knobs.txt): differential attention and ALiBi gain from 216 softmax registers
 // (diff 699 -> 727, ALiBi 1022 -> 1040 TF/s), softcap / sliding / document lose 2-4 % and the small
 // heads 6 %, plain causal is neutral -> 216 only for DIFF and ALiBi.
 #ifndef FL_REGS_CTL
@@ -94,7 +94,10 @@ struct TcCfg {
   static constexpr int CHUNK_BYTES = BM * SWB;
   static constexpr int TILE_BYTES = BM * D * 2;
   static constexpr int NQ = LIST ? 1 : 2;            // Q tiles resident per unit
-  static constexpr int NSLOT = LIST ? (D == 128 ? 5 : 8) : (D == 128 ? 4 : (D == 64 ? 6 : 8));
+#ifndef FL_NSLOT64
+#define FL_NSLOT64 6
+#endif
+  static constexpr int NSLOT = LIST ? (D == 128 ? 5 : 8) : (D == 128 ? 4 : (D == 64 ? FL_NSLOT64 : 8));
   static constexpr uint32_t LAYOUT = SWB == 128 ? kLayoutSW128 : kLayoutSW64;
   static constexpr int SBO = 8 * SWB;                // 8-row (K-major) / 8-key (MN-major) group stride
   static constexpr uint32_t COL_S0 = 0, COL_S1 = 128, COL_O0 = 256, COL_O1 = 256 + D;
