@@ -57,7 +57,10 @@ __device__ unsigned long long g_fl_timing[3][16];
 
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
-constexpr float kTau = 8.0f;
+#ifndef FL_TAU
+#define FL_TAU 8.0f
+#endif
+constexpr float kTau = FL_TAU;
 constexpr int kThreadsTc = 384;
 // Register split via setmaxnreg: the CTA launches with 168 regs/thread (launch
 // bounds 384 x 1); the control warpgroup gives registers back and the two softmax
