@@ -95,14 +95,15 @@ cudaError_t launch_rsa_summaries(const void* k, int64_t sb, int64_t sg, int64_t 
 }
 
 // ------------------------------------------------------------------ selection
-// Pipelined, warp-specialised: 256 threads, one CTA per SM, each CTA a contiguous range of
+// Pipelined, warp-specialised: 384 threads, one CTA per SM, each CTA a contiguous range of
 // (b, g, h_kv, q-block) pairs (x grp heads), so the summaries of a (b, g, h_kv) are loaded once
 // per CTA per head it touches.
 //   warps 4-7 ("split" WG): q+ / q- split of the landed Q tile into the operand buffers; its
 //     thread 0 also issues the TMA loads (next Q tile into a separate raw buffer, summaries)
 //     and the tcgen05 MMAs into a double-buffered TMEM accumulator;
-//   warps 0-3 ("select" WG, thread = TMEM lane = KV block): row max over the block's queries,
-//     running max over the heads of a GQA group, top-k by rank, ascending list.
+//   warps 0-3 and 8-11 ("select" WGs, thread = TMEM lane = KV block, alternate items when GQA groups
+//     do not span items): row max over the block's queries, running max over the heads of a GQA
+//     group, exact radix top-k, ascending list.
 // So the split of item n+1, the MMAs of item n+1 and the selection of item n overlap.
 template <int D>
 struct SelCfg {
@@ -111,14 +112,15 @@ struct SelCfg {
   static constexpr int CHUNK = 128 * 128;               // one 128-row x 128-byte swizzle slab
   static constexpr int QTILE = NCH * CHUNK;             // one 128 x D tile
   static constexpr uint32_t IDESC = idesc_bf16_f32(128, 128, 0);
-  // summaries (kmax, kmin) + raw Q + q+ / q- tiles + radix-select scratch (256-bin histogram + state)
-  // + flags + barriers + alignment slack
-  static constexpr int SCRATCH = 256 * 4 + 64;
-  static int smem(int n_mt) { return 2 * n_mt * QTILE + 3 * QTILE + SCRATCH + 64 + 128 + 1024; }
+  // summaries (kmax, kmin) + raw Q + q+ / q- tiles + per-select-warpgroup scratch (256-bin histogram as
+  // 16-bit counts, pass state, selection bitmap) + barriers + alignment slack
+  static constexpr int SCR_WORDS = 128 + 16 + 16;
+  static constexpr int SCRATCH = 2 * SCR_WORDS * 4;
+  static int smem(int n_mt) { return 2 * n_mt * QTILE + 3 * QTILE + SCRATCH + 128 + 1024; }
 };
 
 template <int D>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     rsa_select_kernel(const __grid_constant__ RsaSelParams p, const __grid_constant__ CUtensorMap tq,
                       const __grid_constant__ CUtensorMap tmin, const __grid_constant__ CUtensorMap tmax) {
   using C = SelCfg<D>;
@@ -132,10 +134,8 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t* sQraw = sMin + n_mt * C::QTILE;              // TMA destination of the next Q tile
   uint8_t* sQp = sQraw + C::QTILE;
   uint8_t* sQn = sQp + C::QTILE;
-  uint32_t* hist = reinterpret_cast<uint32_t*>(sQn + C::QTILE);  // [256] radix-select histogram
-  uint32_t* rstate = hist + 256;                        // [16] digit / counts of the current pass
-  uint32_t* flags = hist + C::SCRATCH / 4;              // [16] selection bitmap
-  uint64_t* bars = reinterpret_cast<uint64_t*>(flags + 16);
+  uint32_t* scratch = reinterpret_cast<uint32_t*>(sQn + C::QTILE);   // [2][SCR_WORDS], one per select WG
+  uint64_t* bars = reinterpret_cast<uint64_t*>(scratch + 2 * C::SCR_WORDS);
   uint64_t* bar_sum = bars;                             // summaries landed
   uint64_t* bar_q = bars + 1;                           // raw Q tile landed
   uint64_t* bar_qfree = bars + 2;                       // MMAs of the previous item done (q+/q-, summaries free)
@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(256, 1)
   };
   auto n_mt_of = [&](int c) { return c >= 2 ? (c - 1 + 127) / 128 : 0; };
 
-  if (warp >= 4) {
+  if (warp >= 4 && warp < 8) {
     // ============================== split + TMA + MMA ==============================
     const int st = t - 128;
     int cur_bgk = -1, sum_phase = 0;
@@ -257,9 +257,18 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else {
     // ============================== selection (thread = KV block) ==============================
-    float run0 = -INFINITY, run1 = -INFINITY, run2 = -INFINITY, run3 = -INFINITY;  // block j = m*128 + t
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-    for (int n = 0; n < n_items; ++n) {
+    // Two select warpgroups (warps 0-3 and 8-11) take alternate items when each item has its own TMEM
+    // accumulator buffer and no GQA group spans items; otherwise warps 0-3 take every item.
+    const int sel = warp >= 8 ? 1 : 0;
+    const int nsel = (nbuf == 2 && p.grp == 1) ? 2 : 1;
+    const int tt = t & 127, wq = warp & 3;              // thread / warp within the select warpgroup
+    uint32_t* hist = scratch + sel * C::SCR_WORDS;      // [128] packed 16-bit bin counts
+    uint32_t* rstate = hist + 128;                      // [16] digit / counts of the current pass
+    uint32_t* flags = hist + 144;                       // [16] selection bitmap
+    const uint32_t bar_id = 2 + sel;
+    float run0 = -INFINITY, run1 = -INFINITY, run2 = -INFINITY, run3 = -INFINITY;  // block j = m*128 + tt
+    const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+    for (int n = sel; n < n_items && sel < nsel; n += nsel) {
       const int i = item_qblk(n);
       const int bgk = item_bgk(n);
       const int hk = bgk % p.Hkv, g = (bgk / p.Hkv) % p.G, b = bgk / (p.Hkv * p.G);
@@ -313,7 +322,7 @@ __global__ void __launch_bounds__(256, 1)
         bool cand[4];
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
-          const int j = m * 128 + t;
+          const int j = m * 128 + tt;
           cand[m] = m < n_mt && j >= 1 && j < c;
           const uint32_t bits = __float_as_uint(runs[m] + 0.f);     // -0 -> +0 (equal scores tie)
           key[m] = bits ^ ((bits >> 31) ? 0xFFFFFFFFu : 0x80000000u);
@@ -325,18 +334,20 @@ __global__ void __launch_bounds__(256, 1)
         if (!take_all && !take_none) {
           for (int pass = 0; pass < 4; ++pass) {
             const int shift = 24 - 8 * pass;
-            hist[t] = 0u;
-            hist[t + 128] = 0u;
-            named_bar_sync(2, 128);
+            hist[tt] = 0u;
+            named_bar_sync(bar_id, 128);
 #pragma unroll
             for (int m = 0; m < 4; ++m)
-              if (cand[m] && (key[m] & M) == P) atomicAdd(&hist[(key[m] >> shift) & 255u], 1u);
-            named_bar_sync(2, 128);
-            if (warp == 0) {                              // lane l owns bins [8l, 8l + 8); count from the top
+              if (cand[m] && (key[m] & M) == P) {
+                const uint32_t d = (key[m] >> shift) & 255u;
+                atomicAdd(&hist[d >> 1], 1u << ((d & 1u) * 16));   // two 16-bit bins per word (<= 512 keys)
+              }
+            named_bar_sync(bar_id, 128);
+            if (wq == 0) {                                // lane l owns bins [8l, 8l + 8); count from the top
               uint32_t cnts[8], lsum = 0u;
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
-                cnts[e] = hist[8 * lane + e];
+                cnts[e] = (hist[4 * lane + (e >> 1)] >> ((e & 1) * 16)) & 0xFFFFu;
                 lsum += cnts[e];
               }
               uint32_t suf = lsum;                        // keys in bins of lanes >= lane
@@ -364,7 +375,7 @@ __global__ void __launch_bounds__(256, 1)
                 rstate[2] = in_bin;
               }
             }
-            named_bar_sync(2, 128);
+            named_bar_sync(bar_id, 128);
             const uint32_t d = rstate[0];
             krem -= (int)rstate[1];
             const bool whole = rstate[2] == (uint32_t)krem;
@@ -379,13 +390,13 @@ __global__ void __launch_bounds__(256, 1)
         for (int m = 0; m < 4; ++m) {
           eq[m] = !take_all && !take_none && cand[m] && (key[m] & M) == P;
           const uint32_t bal = __ballot_sync(0xffffffffu, eq[m]);
-          if (lane == 0) hist[m * 4 + warp] = bal;        // the histogram is dead after the last pass
+          if (lane == 0) hist[m * 4 + wq] = bal;          // the histogram is dead after the last pass
         }
-        if (t < 16) flags[t] = 0u;
-        named_bar_sync(2, 128);
+        if (tt < 16) flags[tt] = 0u;
+        named_bar_sync(bar_id, 128);
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
-          const int j = m * 128 + t;
+          const int j = m * 128 + tt;
           bool sel = false;
           if (m < n_mt && j < p.nkb && j <= c) {
             if (j == 0 || j == c) {
@@ -407,9 +418,9 @@ __global__ void __launch_bounds__(256, 1)
             }
           }
           const uint32_t bal = __ballot_sync(0xffffffffu, sel);
-          if (lane == 0) flags[m * 4 + warp] = bal;
+          if (lane == 0) flags[m * 4 + wq] = bal;
         }
-        named_bar_sync(2, 128);
+        named_bar_sync(bar_id, 128);
         int cnt = 0;
         for (int w = 0; w < 16; ++w) cnt += __popc(flags[w]);
         for (int hh = 0; hh < p.grp; ++hh) {
@@ -417,7 +428,7 @@ __global__ void __launch_bounds__(256, 1)
           int32_t* out = p.blk_idx + row * p.max_sel;
 #pragma unroll
           for (int m = 0; m < 4; ++m) {
-            const int j = m * 128 + t;
+            const int j = m * 128 + tt;
             const int w = j >> 5;
             if (m < n_mt && ((flags[w] >> (j & 31)) & 1u)) {
               int pos = __popc(flags[w] & ((1u << (j & 31)) - 1u));
@@ -425,10 +436,10 @@ __global__ void __launch_bounds__(256, 1)
               if (pos < p.max_sel) out[pos] = j;
             }
           }
-          for (int e = cnt + t; e < p.max_sel; e += 128) out[e] = -1;
-          if (t == 0) p.blk_cnt[row] = min(cnt, p.max_sel);
+          for (int e = cnt + tt; e < p.max_sel; e += 128) out[e] = -1;
+          if (tt == 0) p.blk_cnt[row] = min(cnt, p.max_sel);
         }
-        named_bar_sync(2, 128);                           // sc / flags reuse
+        named_bar_sync(bar_id, 128);                           // sc / flags reuse
       }
     }
   }
@@ -455,12 +466,12 @@ cudaError_t launch_rsa_select(const RsaSelParams& p0, const CUtensorMap& tq, con
     const int sm = SelCfg<128>::smem(n_mt);
     cudaError_t e = cudaFuncSetAttribute(rsa_select_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     if (e != cudaSuccess) return e;
-    rsa_select_kernel<128><<<grid, 256, sm, stream>>>(p, tq, tmin, tmax);
+    rsa_select_kernel<128><<<grid, 384, sm, stream>>>(p, tq, tmin, tmax);
   } else {
     const int sm = SelCfg<64>::smem(n_mt);
     cudaError_t e = cudaFuncSetAttribute(rsa_select_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     if (e != cudaSuccess) return e;
-    rsa_select_kernel<64><<<grid, 256, sm, stream>>>(p, tq, tmin, tmax);
+    rsa_select_kernel<64><<<grid, 384, sm, stream>>>(p, tq, tmin, tmax);
   }
   return cudaGetLastError();
 }
