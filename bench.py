@@ -509,8 +509,11 @@ def run_reference(args, world, rank):
         if i >= args.warmup:
             vals.append(v)
     value = float(np.mean(vals))
+    # one full-workload step at the sampled rate (the oracle runs a bounded sample of it per step)
+    step_flops = getattr(job, "step_flops", None)
+    ms_per_step = step_flops / (value * 1e12) * 1e3 if step_flops and value > 0 else None
     line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": job.workload, "variant": args.variant},
             "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": samples},
