@@ -175,7 +175,8 @@ __global__ void __launch_bounds__(384, 1)
     const int c = q_last_abs < 0 ? 0 : q_last_abs / 128;
     return min(c, p.nkb - 1);
   };
-  auto n_mt_of = [&](int c) { return c >= 2 ? (c - 1 + 127) / 128 : 0; };
+  // candidates j = 1 .. c-1 live in accumulator tiles 0 .. (c-1)/128, i.e. ceil(c / 128) tiles
+  auto n_mt_of = [&](int c) { return c >= 2 ? (c + 127) / 128 : 0; };
 
   if (warp >= 4 && warp < 8) {
     // ============================== split + TMA + MMA ==============================

@@ -69,33 +69,80 @@ def constant_v(shape, *, seed=0, dtype=torch.bfloat16, lead=2, slab_range=None) 
     return t.reshape(tuple(shape)) if slab_range is None else t
 
 
-def needle(q_shape, k_shape, *, seed=0, dtype=torch.bfloat16, interval=None, sq_sk=None):
-    """Peaked inputs: K in {+-1}^D; Q[b,h,q] = K[b,h_kv,pi(q)] with pi(q) drawn
-    uniformly from the admissible keys [lo(q), hi(q)) of row q.
-
-    ``interval(q) -> (lo, hi)`` gives the admissible key range (None = all keys).
-    Shapes are [B,H,S,D]; GQA groups copy from their shared KV head."""
-    B, Hq, Sq, D = q_shape
-    _, Hkv, Sk, _ = k_shape
+def _pm1_keys(k_shape, seed):
+    B, Hkv, Sk, D = k_shape
     k = np.empty(k_shape, dtype=np.float32)
     for i in range(B * Hkv):
         r = _rng(seed, "k", i)
         k.reshape(B * Hkv, Sk, D)[i] = np.where(r.random((Sk, D)) < 0.5, -1.0, 1.0)
+    return k
+
+
+def _interval_of(interval, b, Sq):
+    if interval is None:
+        return None
+    import inspect
+    if len(inspect.signature(interval).parameters) >= 2:
+        return interval(np.arange(Sq), b)
+    return interval(np.arange(Sq))
+
+
+def needle(q_shape, k_shape, *, seed=0, dtype=torch.bfloat16, interval=None, sq_sk=None):
+    """Peaked inputs: K in {+-1}^D; Q[b,h,q] = K[b,h_kv,pi(q)] with pi(q) drawn
+    uniformly from the admissible keys [lo(q), hi(q)) of row q.
+
+    ``interval(q[, b]) -> (lo, hi)`` gives the admissible key range of the rows of
+    batch b (None = all keys).  Shapes are [B,H,S,D]; GQA groups copy from their
+    shared KV head."""
+    B, Hq, Sq, D = q_shape
+    _, Hkv, Sk, _ = k_shape
+    k = _pm1_keys(k_shape, seed)
+    q = np.empty(q_shape, dtype=np.float32)
+    grp = Hq // Hkv
+    for b in range(B):
+        iv = _interval_of(interval, b, Sq)
+        if iv is None:
+            lo = np.zeros(Sq, dtype=np.int64)
+            hi = np.full(Sq, Sk, dtype=np.int64)
+        else:
+            lo, hi = (np.asarray(a, dtype=np.int64) for a in iv)
+        hi = np.maximum(hi, lo + 1)
+        for h in range(Hq):
+            r = _rng(seed, "q", b * Hq + h)
+            u = r.random(Sq)
+            pick = np.clip(lo + np.floor(u * (hi - lo)).astype(np.int64), 0, Sk - 1)
+            q[b, h] = k[b, h // grp][pick]
+    return _to(q, dtype), _to(k, dtype)
+
+
+def needle_at(q_shape, k_shape, pick, *, seed=0, dtype=torch.bfloat16):
+    """Needle inputs with an explicit key per row: K in {+-1}^D, Q[b,h,q] = K[b,h_kv,pick[q]]
+    (pick clipped to [0, S_k)).  With pick just outside a row's admissible keys ("leak"
+    inputs) a mask that admits one key too many is dominated by that key."""
+    B, Hq, Sq, D = q_shape
+    _, Hkv, Sk, _ = k_shape
+    k = _pm1_keys(k_shape, seed)
+    pick = np.clip(np.asarray(pick, dtype=np.int64), 0, Sk - 1)
     q = np.empty(q_shape, dtype=np.float32)
     grp = Hq // Hkv
     for b in range(B):
         for h in range(Hq):
-            r = _rng(seed, "q", b * Hq + h)
-            u = r.random(Sq)
-            if interval is None:
-                lo = np.zeros(Sq, dtype=np.int64)
-                hi = np.full(Sq, Sk, dtype=np.int64)
-            else:
-                lo, hi = (np.asarray(a, dtype=np.int64) for a in interval(np.arange(Sq)))
-            hi = np.maximum(hi, lo + 1)
-            pick = np.minimum(lo + np.floor(u * (hi - lo)).astype(np.int64), Sk - 1)
             q[b, h] = k[b, h // grp][pick]
     return _to(q, dtype), _to(k, dtype)
+
+
+def block_constant_v(shape, *, blk=128, seed=0, dtype=torch.bfloat16, lead=2):
+    """V[..., k, :] = c_(slab, k // blk), one c ~ U[-1,1)^Dv per key block: O is the mixture of
+    the block vectors weighted by each block's softmax mass, so a wrong block list or a wrong
+    K/V tile moves it by O(1) while the normalisation is pinned as for constant V."""
+    n, inner = _slabs(shape, lead)
+    S, Dv = inner[-2], inner[-1]
+    nb = (S + blk - 1) // blk
+    out = np.empty((n,) + tuple(inner), dtype=np.float32)
+    for i in range(n):
+        c = _rng(seed, "v", i).random((nb, Dv), dtype=np.float32) * 2 - 1
+        out[i] = np.repeat(c, blk, axis=0)[:S]
+    return _to(out, dtype).reshape(tuple(shape))
 
 
 def doc_offsets(B, S, n_docs=12, *, seed=1) -> np.ndarray:

@@ -17,7 +17,7 @@ def admissible(case, Sq, Sk, b=0):
     """Admissible key interval [lo, hi) per query row (for needle inputs)."""
     mask = case.get("mask", "none")
     off = 0 if case.get("causal_align") else Sk - Sq
-    def f(q):
+    def f(q, b=b):
         qa = q + off
         if mask in ("causal", "blocklist"):
             return np.zeros_like(q), np.minimum(qa + 1, Sk)
@@ -48,13 +48,21 @@ def build(case: dict):
         c["doc_offsets"] = synth.doc_offsets(B, Sk, c.get("n_docs", 12), seed=seed + 1)
     qs, ks, vs = (B, Hq * maps, Sq, D), (B, Hkv * maps, Sk, D), (B, Hkv, Sk, Dv)
     if dist == "needle":
-        assert B == 1 or c.get("mask") != "document"
         q, k = synth.needle(qs, ks, seed=seed, dtype=dt, interval=admissible(c, Sq, Sk))
+    elif dist == "leak":
+        # needle one key past each row's admissible interval (window start - 1 for sliding windows,
+        # the first key after the interval otherwise): a mask that admits one key too many is
+        # dominated by that key (T4 mutants in tests/test_mutants.py)
+        lo, hi = admissible(c, Sq, Sk)(np.arange(Sq), 0)
+        pick = lo - 1 if c.get("mask") == "sliding" else hi
+        q, k = synth.needle_at(qs, ks, pick, seed=seed, dtype=dt)
     else:
         q = synth.uniform(qs, seed=seed, tensor="q", dtype=dt)
         k = synth.uniform(ks, seed=seed, tensor="k", dtype=dt)
     if dist == "constant":
         v = synth.constant_v(vs, seed=seed, dtype=dt)
+    elif c.get("v") == "blockconst":
+        v = synth.block_constant_v(vs, seed=seed, dtype=dt)
     else:
         v = synth.uniform(vs, seed=seed, tensor="v", dtype=dt)
     gk, ok = {}, {}

@@ -91,6 +91,8 @@ for D in (128, 64, 32):
         dict(name=f"causal_const_D{D}", S=700, D=D, mask="causal", dist="constant"),
         dict(name=f"alibi_needle_D{D}", S=400, D=D, mod="alibi", Hq=4, dist="needle"),
         dict(name=f"softcap_needle_D{D}", S=400, D=D, mod="softcap", softcap=20.0, dist="needle"),
+        # cap 2: the cap bends the needle score as well as the rest (cap 20 leaves needle rows unchanged)
+        dict(name=f"softcap2_needle_D{D}", S=400, D=D, mod="softcap", softcap=2.0, dist="needle"),
         dict(name=f"sliding_needle_D{D}", S=900, D=D, mask="sliding", window=200, dist="needle"),
         dict(name=f"sliding_const_D{D}", S=900, D=D, mask="sliding", window=200, dist="constant"),
         dict(name=f"prefix_needle_D{D}", S=640, D=D, mask="prefix", prefix=200, dist="needle"),
@@ -111,6 +113,18 @@ for D in (128, 64, 32):
         dict(name=f"alibi_custom_keymask_D{D}", Hq=4, S=300, D=D, mod="alibi", alibi_custom=True, key_mask=True,
              p_zero=0.2, dist="constant"),
         dict(name=f"bias_f32_gate_mul_D{D}", Hq=2, S=200, D=D, bias="f32", gate_mode="mul", dist="constant"),
+        # differential attention with per-map needles (map 1's needle moves O by lambda x O(1), so a kernel
+        # that drops, swaps or mis-indexes map 1 fails: tests/test_mutants.py)
+        dict(name=f"diff_needle_D{D}", Hq=2, S=400, D=D, diff=True, lam=0.7, dist="needle"),
+        dict(name=f"diff_needle_lambda_h_causal_D{D}", Hq=3, S=333, D=D, diff=True, lambda_h=True, mask="causal",
+             dist="needle"),
+        # "leak" inputs: each row's needle sits one key past its admissible interval
+        dict(name=f"causal_leak_D{D}", S=700, D=D, mask="causal", dist="leak"),
+        dict(name=f"sliding_leak_D{D}", S=900, D=D, mask="sliding", window=200, dist="leak"),
+        dict(name=f"prefix_leak_D{D}", S=640, D=D, mask="prefix", prefix=200, dist="leak"),
+        dict(name=f"document_leak_D{D}", S=1000, D=D, mask="document", n_docs=6, dist="leak"),
+        dict(name=f"keymask_needle_D{D}", S=300, D=D, key_mask=True, p_zero=0.2, dist="needle"),
+        dict(name=f"document_needle_B2_D{D}", B=2, S=1000, D=D, mask="document", n_docs=6, dist="needle"),
     ]
 
 

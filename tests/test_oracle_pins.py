@@ -112,6 +112,18 @@ def test_vanilla_and_causal_vs_sdpa(sq, sk, dtype):
     if sq == sk:
         ref2 = F.scaled_dot_product_attention(qd, kd, vd, is_causal=True)
         torch.testing.assert_close(O(out, ref.shape), ref2, rtol=1e-12, atol=1e-13)
+    # top-left alignment (causal_align = 1, the G12 flag): keep k <= q, which is torch's is_causal
+    # convention (tril with diagonal 0) for any S_q, S_k; and a top-left sliding window / prefix
+    out, _ = oracle.attn(q, k, v, mask="causal", causal_align=1)
+    ref3 = F.scaled_dot_product_attention(qd, kd, vd, is_causal=True)
+    torch.testing.assert_close(O(out, ref.shape), ref3, rtol=1e-12, atol=1e-13)
+    qi, ki = torch.arange(sq).view(-1, 1), torch.arange(sk).view(1, -1)
+    out, _ = oracle.attn(q, k, v, mask="sliding", window=3, causal_align=1)
+    ref4 = F.scaled_dot_product_attention(qd, kd, vd, attn_mask=(ki <= qi) & (qi - ki <= 3))
+    torch.testing.assert_close(O(out, ref.shape), ref4, rtol=1e-12, atol=1e-13)
+    out, _ = oracle.attn(q, k, v, mask="prefix", prefix=5, causal_align=1)
+    ref5 = F.scaled_dot_product_attention(qd, kd, vd, attn_mask=(ki < 5) | (ki <= qi))
+    torch.testing.assert_close(O(out, ref.shape), ref5, rtol=1e-12, atol=1e-13)
 
 
 def test_gqa_vs_sdpa_enable_gqa():
@@ -272,8 +284,6 @@ def test_constant_v_gives_constant(mask, kw, mod):
         assert nqb == idx.shape[1]
     out, _ = oracle.attn(q, k, v, mask=mask, mod=mod, softcap=5.0, **kw)
     for r in range(out.shape[0]):
-        if mask == "blocklist" and (r % S) // 16 == 0 and False:
-            continue
         np.testing.assert_allclose(out[r], c.numpy(), rtol=0, atol=1e-14)
 
 
@@ -391,9 +401,13 @@ def test_invariances():
         a, b = offs[0, j], offs[0, j + 1]
         seg, _ = oracle.attn(q[:, :, a:b], k[:, :, a:b], v[:, :, a:b])
         np.testing.assert_allclose(O(out, (2, S, 8))[:, a:b].reshape(-1, 8).numpy(), seg, rtol=1e-14, atol=1e-15)
-    # GQA with Hkv == Hq is MHA, bit for bit
-    out, _ = oracle.attn(q, k, v, mask="causal")
-    np.testing.assert_array_equal(out, causal)
+    # GQA (G15, consecutive groups) == MHA on K/V heads repeated group by group, bit for bit
+    q4 = rnd(1, 4, S, 8, seed=59)
+    out, _ = oracle.attn(q4, k, v, mask="causal")
+    rep, _ = oracle.attn(q4, k.repeat_interleave(2, dim=1), v.repeat_interleave(2, dim=1), mask="causal")
+    np.testing.assert_array_equal(out, rep)
+    wrong, _ = oracle.attn(q4, k.repeat(1, 2, 1, 1), v.repeat(1, 2, 1, 1), mask="causal")
+    assert not np.allclose(out, wrong)                  # the interleaved map is a different operator
 
 
 def test_row_subset_equals_full_run():
@@ -470,17 +484,25 @@ def test_rsa_summaries_and_bound_identity():
     np.testing.assert_allclose(lhs, rhs, rtol=1e-12, atol=1e-12)
 
 
-def test_rsa_selection_matches_sort_reference():
-    Sq = Sk = 256
+@pytest.mark.parametrize("Sq,Sk,align", [(256, 256, 0), (64, 256, 0), (100, 256, 0), (1, 256, 0), (100, 256, 1),
+                                        (256, 256, 1)])
+def test_rsa_selection_matches_sort_reference(Sq, Sk, align):
+    """G10 selection incl. S_q < S_k (the C5 decode / chunked-prefill shapes) with bottom-right
+    (G12) and top-left alignment: diagonal block c of q-block i from the last query's absolute
+    position, scores by the q+/q- identity (P14), top-k by a sort with ties to the lower j."""
     blk, topk = 16, 4
-    q, k = synth.clustered_qk((1, 4, Sq, 16), (1, 2, Sk, 16), blk=blk, dtype=torch.bfloat16)
-    idx, cnt, sc = oracle.rsa_select(q, k, blk_q=blk, blk_k=blk, topk=topk, want_scores=True)
+    qf, k = synth.clustered_qk((1, 4, Sk, 16), (1, 2, Sk, 16), blk=blk, dtype=torch.bfloat16)
+    q = qf[:, :, Sk - Sq:].contiguous()
+    idx, cnt, sc = oracle.rsa_select(q, k, blk_q=blk, blk_k=blk, topk=topk, causal_align=align, want_scores=True)
     kmin, kmax = oracle.rsa_summaries(k, blk)
     qd = q.to(D64).numpy()
+    nqb = (Sq + blk - 1) // blk
+    assert idx.shape[1] == nqb
     for h in range(4):
         hk = h // 2
-        for i in range(Sq // blk):
-            c = i
+        for i in range(nqb):
+            q_last = min(Sq, (i + 1) * blk) - 1
+            c = (q_last + (0 if align else Sk - Sq)) // blk
             if c <= topk + 1:
                 assert list(idx[h, i, : cnt[h, i]]) == list(range(c + 1))
                 continue
