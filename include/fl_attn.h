@@ -196,6 +196,24 @@ void fl_shard_range(int64_t units, int32_t world, int32_t rank, int64_t* begin, 
 fl_status fl_diag_umma_gemm(const void* a, const void* b, float* c, int32_t n, int32_t k,
                             int32_t b_mn_major, int32_t a_from_tmem, void* stream);
 
+/* Diagnostic: the bf16 tcgen05 kernel's work decomposition and tile classification
+ * for `args` (interval masks only), computed on the device by the kernel's own decode_work / needs /
+ * tile_inside functions.  One record per (unit, softmax warpgroup): 8 int32 [unit, wg, b, g, h, q0,
+ * lo, hi] followed by max_tiles int32 codes per KV tile j: -1 = not run by that warpgroup, else a 4-bit
+ * mask of its warps (32 rows each) that apply the element-wise mask on tile j (0 = mask-free tile).
+ * With out == NULL only *n_records / *max_tiles are set.  out: device buffer of >= n_records *
+ * (8 + max_tiles) words, on args->stream.  FL_ERR_UNSUPPORTED for block lists, decode shapes, fp32. */
+fl_status fl_debug_schedule(const fl_attn_args* args, int32_t* out, int64_t out_words, int64_t* n_records,
+                            int32_t* max_tiles);
+
+/* Diagnostic: measured pipe throughput for the MUFU-bound rooflines.  Enqueues one kernel
+ * (one CTA of 512 threads per SM, 8 independent chains per thread, `iters` steps each) of op
+ * 0 = ex2.approx.ftz.f32, 1 = ex2.approx.ftz.bf16x2, 2 = tanh.approx.f32, 3 = fma.rn.f32x2; *ops receives
+ * the number of elementary operations it performs (bf16x2 / f32x2: 2 per instruction).  The caller
+ * times the launch on `stream` (rate = ops / time).  sink: device buffer of >= n_SM*512 floats (never
+ * written in practice; keeps the chains live).  Asynchronous. */
+fl_status fl_diag_pipe_rate(int32_t op, int32_t iters, float* sink, int64_t* ops, void* stream);
+
 /* Diagnostic: cycle counters of the bf16 kernel's pipeline phases, only in a library built with
  * -DFL_TIMING (FL_ERR_UNSUPPORTED otherwise).  out48 receives [3][16] uint64 sums over CTAs:
  * rows 0/1 = softmax warpgroups (slots 0..8: bookkeeping, S wait, S load, score+mask+max, O rescale,

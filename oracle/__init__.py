@@ -77,6 +77,9 @@ def lib():
                                         C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32),
                                         C.POINTER(C.c_int32), C.POINTER(C.c_double)]
         _lib.flo_num_threads.restype = C.c_int
+        _lib.flo_keep_row.argtypes = [C.POINTER(_Problem), C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                      C.POINTER(C.c_uint8)]
+        _lib.flo_keep_row.restype = C.c_int
     return _lib
 
 
@@ -139,6 +142,54 @@ def attn(q, k, v, *, scale=0.0, mod="none", softcap=0.0, alibi_slopes=None,
     rows are flat ((b*G+g)*Hq+h)*Sq+q ids (None = all rows in that order).
     """
     keep: list = []
+    p = _problem(q, k, v, keep, scale=scale, mod=mod, softcap=softcap, alibi_slopes=alibi_slopes, mask=mask,
+                 window=window, prefix=prefix, doc_offsets=doc_offsets, doc_causal=doc_causal,
+                 causal_align=causal_align, bias=bias, key_mask=key_mask, gate_mode=gate_mode, gate=gate, diff=diff,
+                 lam=lam, lambda_h=lambda_h, blk_idx=blk_idx, blk_cnt=blk_cnt, blk_q=blk_q, blk_k=blk_k)
+    maps = 2 if diff else 1
+    qs = p.q.size
+    total = qs[0] * qs[1] * (qs[2] // maps) * qs[3]
+    if rows is None:
+        rows_arr, n = None, total
+    else:
+        ra = np.ascontiguousarray(np.asarray(rows, dtype=np.int64))
+        keep.append(ra)
+        rows_arr, n = ra.ctypes.data_as(C.POINTER(C.c_int64)), ra.size
+    dv = p.v.size[4]
+    out = np.zeros((n, dv), dtype=np.float64)
+    lse = np.zeros((n,), dtype=np.float64)
+    rc = lib().flo_attn(C.byref(p), rows_arr, n, out.ctypes.data_as(C.POINTER(C.c_double)),
+                        lse.ctypes.data_as(C.POINTER(C.c_double)))
+    if rc != 0:
+        raise ValueError(f"flo_attn rejected the problem (code {rc})")
+    return out, lse
+
+
+def keep_rows(q, k, v, rows, **variant):
+    """Kept-key predicate (definition step 2: mask AND key mask) of each flat output row id
+    ((b*G+g)*Hq+h)*Sq+q: returns uint8 [len(rows), S_k]."""
+    keep: list = []
+    p = _problem(q, k, v, keep, **variant)
+    maps = 2 if variant.get("diff") else 1
+    _, G, H2, Sq = (p.q.size[i] for i in range(4))
+    Hq = H2 // maps
+    Sk = p.k.size[3]
+    out = np.zeros((len(rows), Sk), dtype=np.uint8)
+    for i, r in enumerate(rows):
+        qq, t = r % Sq, r // Sq
+        h, t = t % Hq, t // Hq
+        g, b = t % G, t // G
+        rc = lib().flo_keep_row(C.byref(p), b, g, h, qq, out[i].ctypes.data_as(C.POINTER(C.c_uint8)))
+        if rc != 0:
+            raise ValueError(f"flo_keep_row rejected the problem (code {rc})")
+    return out
+
+
+def _problem(q, k, v, keep, *, scale=0.0, mod="none", softcap=0.0, alibi_slopes=None,
+             mask="none", window=0, prefix=0, doc_offsets=None, doc_causal=False,
+             causal_align=0, bias=None, key_mask=None, gate_mode="none", gate=None,
+             diff=False, lam=0.0, lambda_h=None, blk_idx=None, blk_cnt=None,
+             blk_q=128, blk_k=128):
     p = _Problem()
     p.q, p.k, p.v = _tensor(q, keep), _tensor(k, keep), _tensor(v, keep)
     p.scale = float(scale)
@@ -182,24 +233,7 @@ def attn(q, k, v, *, scale=0.0, mod="none", softcap=0.0, alibi_slopes=None,
         p.blk_cnt = bc.ctypes.data_as(C.POINTER(C.c_int32))
         p.max_sel = bi.shape[-1]
     p.blk_q, p.blk_k = int(blk_q), int(blk_k)
-
-    maps = 2 if diff else 1
-    qs = p.q.size
-    total = qs[0] * qs[1] * (qs[2] // maps) * qs[3]
-    if rows is None:
-        rows_arr, n = None, total
-    else:
-        ra = np.ascontiguousarray(np.asarray(rows, dtype=np.int64))
-        keep.append(ra)
-        rows_arr, n = ra.ctypes.data_as(C.POINTER(C.c_int64)), ra.size
-    dv = p.v.size[4]
-    out = np.zeros((n, dv), dtype=np.float64)
-    lse = np.zeros((n,), dtype=np.float64)
-    rc = lib().flo_attn(C.byref(p), rows_arr, n, out.ctypes.data_as(C.POINTER(C.c_double)),
-                        lse.ctypes.data_as(C.POINTER(C.c_double)))
-    if rc != 0:
-        raise ValueError(f"flo_attn rejected the problem (code {rc})")
-    return out, lse
+    return p
 
 
 def stable_softmax(x):

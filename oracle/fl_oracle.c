@@ -111,6 +111,17 @@ static int check_problem(const flo_problem* p, int64_t* maps_out) {
   return 0;
 }
 
+/* Step 2 of the definition: is key k kept for output row (b, g, h, q)?  The mask
+ * predicate (Listing 1, Listing 2, readings G4-G6, G10, G12) AND the key mask. */
+static int kept(const flo_problem* p, int64_t bgh, int64_t b, int64_t g, int64_t q, int64_t q_abs, int64_t k) {
+  int keep = keep_key(p, bgh, b, q, q_abs, k);
+  if (keep && p->key_mask.data) {
+    int64_t mo = b * p->key_mask.stride[0] + g * p->key_mask.stride[1] + k * p->key_mask.stride[2];
+    keep = elem(&p->key_mask, mo) != 0.0;
+  }
+  return keep;
+}
+
 /* One output row (b, g, h, q): the plain definition, map by map. */
 static void one_row(const flo_problem* p, int64_t maps, int64_t b, int64_t g, int64_t h, int64_t q,
                     double* s, double* acc, double* out, double* lse_out) {
@@ -129,12 +140,7 @@ static void one_row(const flo_problem* p, int64_t maps, int64_t b, int64_t g, in
     const int64_t qh = h + map * Hq, kh = h_kv + map * Hkv;
     int any = 0;
     for (int64_t k = 0; k < Sk; ++k) {
-      int keep = keep_key(p, bgh, b, q, q_abs, k);
-      if (keep && p->key_mask.data) {
-        int64_t mo = b * p->key_mask.stride[0] + g * p->key_mask.stride[1] + k * p->key_mask.stride[2];
-        keep = elem(&p->key_mask, mo) != 0.0;
-      }
-      if (!keep) { s[k] = -INFINITY; continue; }
+      if (!kept(p, bgh, b, g, q, q_abs, k)) { s[k] = -INFINITY; continue; }
       any = 1;
       double dot = 0.0;                         /* QK^T, Eq.3 */
       for (int64_t d = 0; d < Dqk; ++d)
@@ -205,6 +211,17 @@ int flo_attn(const flo_problem* p, const int64_t* rows, int64_t nrows, double* o
     free(acc);
   }
   return bad ? -10 : 0;
+}
+
+int flo_keep_row(const flo_problem* p, int64_t b, int64_t g, int64_t h, int64_t q, uint8_t* keep_out) {
+  int64_t maps;
+  int rc = check_problem(p, &maps);
+  if (rc) return rc;
+  const int64_t G = p->q.size[1], Hq = p->q.size[2] / maps, Sq = p->q.size[3], Sk = p->k.size[3];
+  const int64_t q_abs = p->causal_align ? q : q + (Sk - Sq);                /* G12 */
+  const int64_t bgh = (b * G + g) * Hq + h;
+  for (int64_t k = 0; k < Sk; ++k) keep_out[k] = (uint8_t)kept(p, bgh, b, g, q, q_abs, k);
+  return 0;
 }
 
 /* ---- RSA (reading G10/G11; the paper only names RSA) ---- */

@@ -71,6 +71,10 @@ typedef struct {
 int flo_attn(const flo_problem* p, const int64_t* rows, int64_t nrows,
              double* out, double* lse);
 
+/* The kept-key predicate of output row (b, g, h, q) (definition step 2: mask AND key mask) as
+ * S_k bytes 0/1 -- the scheduler / tile-classifier test compares the kernel's tiles against it. */
+int flo_keep_row(const flo_problem* p, int64_t b, int64_t g, int64_t h, int64_t q, uint8_t* keep_out);
+
 /* Alg.1: two serial loops, m_N = max x, d_N = sum e^{x_j - m_N}.
  * Writes sigma(x) (Eq.2) into y and returns d_N; *m gets m_N. */
 double flo_stable_softmax(const double* x, int64_t n, double* y, double* m);

@@ -16,7 +16,7 @@ ABI_VERSION = 1
 
 EXPORTS = ["fl_attn_fwd", "fl_attn_workspace_size", "fl_attn_host_scratch_size", "fl_attn_fwd_host",
            "fl_rsa_build_summaries", "fl_rsa_update_summaries", "fl_rsa_select", "fl_shard_range", "fl_diag_umma_gemm",
-           "fl_status_string", "fl_last_error", "fl_abi_version", "fl_launch_count", "fl_debug_timing"]
+           "fl_diag_pipe_rate", "fl_debug_schedule", "fl_status_string", "fl_last_error", "fl_abi_version", "fl_launch_count", "fl_debug_timing"]
 
 
 class Tensor(C.Structure):
@@ -75,6 +75,11 @@ def lib():
         L.fl_shard_range.restype = None
         L.fl_diag_umma_gemm.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                         C.c_int32, C.c_void_p]
+        L.fl_diag_pipe_rate.argtypes = [C.c_int32, C.c_int32, C.c_void_p, C.POINTER(C.c_int64), C.c_void_p]
+        L.fl_diag_pipe_rate.restype = C.c_int
+        L.fl_debug_schedule.argtypes = [C.POINTER(AttnArgs), C.c_void_p, C.c_int64, C.POINTER(C.c_int64),
+                                        C.POINTER(C.c_int32)]
+        L.fl_debug_schedule.restype = C.c_int
         L.fl_status_string.argtypes = [C.c_int]
         L.fl_status_string.restype = C.c_char_p
         L.fl_last_error.restype = C.c_char_p

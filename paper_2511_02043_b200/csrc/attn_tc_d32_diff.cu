@@ -6,4 +6,5 @@ namespace fl {
 cudaError_t launch_attn_tc_32_1(const AttnParams& p, const TmaMaps& maps, cudaStream_t stream) {
   return launch_mod<32, true>(p, maps, stream);
 }
+cudaError_t debug_timing_32_1(unsigned long long* out, int reset) { return debug_timing_tu<0>(out, reset); }
 }  // namespace fl

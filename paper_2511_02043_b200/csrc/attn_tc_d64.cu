@@ -6,4 +6,5 @@ namespace fl {
 cudaError_t launch_attn_tc_64_0(const AttnParams& p, const TmaMaps& maps, cudaStream_t stream) {
   return launch_mod<64, false>(p, maps, stream);
 }
+cudaError_t debug_timing_64_0(unsigned long long* out, int reset) { return debug_timing_tu<0>(out, reset); }
 }  // namespace fl

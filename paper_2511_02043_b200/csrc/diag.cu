@@ -140,3 +140,50 @@ cudaError_t launch_diag_gemm(int n, int k, const CUtensorMap& ta, const CUtensor
 }
 
 }  // namespace fl
+
+// ------------------------------------------------------------------ pipe-rate microbenchmark
+// fl_diag_pipe_rate: the measured MUFU / FMA throughput that bench.py uses as the roofline denominator of
+// the MUFU-bound kernels (ex2.approx.f32, ex2.approx.ftz.bf16x2, tanh.approx.f32, FFMA2).
+// One CTA per SM, 512 threads (4 warps per SM sub-partition), 8 independent dependency chains per
+// thread so the pipe, not its latency, is the limit.  x <- ex2(-x) / tanh(x) stay bounded.
+namespace fl {
+template <int OP>
+__global__ void __launch_bounds__(512, 1) pipe_rate_kernel(float* sink, int iters) {
+  float x[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) x[j] = 0.01f * (float)(threadIdx.x + j);
+  uint32_t h[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) h[j] = pack_bf16(x[j], -x[j]);
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (OP == 0) {
+        asm volatile("{.reg .f32 t;\n\tneg.f32 t, %1;\n\tex2.approx.ftz.f32 %0, t;}" : "=f"(x[j]) : "f"(x[j]));
+      } else if (OP == 1) {
+        asm volatile("{.reg .b32 t;\n\txor.b32 t, %1, 0x80008000;\n\tex2.approx.ftz.bf16x2 %0, t;}"
+                     : "=r"(h[j]) : "r"(h[j]));
+      } else if (OP == 2) {
+        asm volatile("tanh.approx.f32 %0, %0;" : "+f"(x[j]));
+      } else if ((j & 1) == 0) {                  // 4 independent packed pairs (x[j], x[j+1])
+        ffma2(x[j], x[j + 1], x[j], x[j + 1], 0.999f, 0.998f, 1e-3f, 2e-3f);
+      }
+    }
+  }
+  float acc = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc += x[j] + bf16_lo(h[j]);
+  if (acc == 123.456f) sink[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
+cudaError_t launch_pipe_rate(int op, int iters, int n_sms, float* sink, cudaStream_t s) {
+  switch (op) {
+    case 0: pipe_rate_kernel<0><<<n_sms, 512, 0, s>>>(sink, iters); break;
+    case 1: pipe_rate_kernel<1><<<n_sms, 512, 0, s>>>(sink, iters); break;
+    case 2: pipe_rate_kernel<2><<<n_sms, 512, 0, s>>>(sink, iters); break;
+    case 3: pipe_rate_kernel<3><<<n_sms, 512, 0, s>>>(sink, iters); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+}  // namespace fl

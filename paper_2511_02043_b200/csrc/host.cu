@@ -37,6 +37,9 @@ cudaError_t launch_rsa_select_small(const RsaSelParams& p, const void* q, int64_
 size_t decode_workspace_bytes(const AttnParams& p, int n_sms);
 cudaError_t launch_attn_decode(const AttnParams& p, const TmaMaps& maps, float* part, int n_sms, cudaStream_t stream);
 cudaError_t debug_timing(unsigned long long* out, int reset);
+cudaError_t launch_pipe_rate(int op, int iters, int n_sms, float* sink, cudaStream_t s);
+cudaError_t launch_sched_dump(const AttnParams& p, int32_t* out, int64_t out_words, int64_t* n_records,
+                              int32_t* max_tiles, cudaStream_t stream);
 }  // namespace fl
 
 using namespace fl;
@@ -634,6 +637,32 @@ fl_status fl_diag_umma_gemm(const void* a, const void* b, float* c, int32_t n, i
   cudaError_t e = launch_diag_gemm(n, k, ta, tb, a, c, b_mn_major != 0, a_from_tmem != 0, static_cast<cudaStream_t>(stream));
   ++g_launches;
   return e == cudaSuccess ? FL_OK : cuda_fail(e, "diag gemm launch");
+}
+
+fl_status fl_debug_schedule(const fl_attn_args* args, int32_t* out, int64_t out_words, int64_t* n_records,
+                            int32_t* max_tiles) {
+  if (!args || !n_records || !max_tiles) return fail(FL_ERR_INVALID_ARGUMENT, "NULL argument");
+  Prepared P;
+  fl_status s = prepare(args, P, true);
+  if (s != FL_OK) return s;
+  if (!P.bf16 || P.decode || P.p.mask == MASK_BLOCKLIST || P.empty_work || P.no_keys)
+    return fail(FL_ERR_UNSUPPORTED, "schedule dump covers the bf16 tcgen05 path with interval masks");
+  cudaError_t e = launch_sched_dump(P.p, out, out_words, n_records, max_tiles, static_cast<cudaStream_t>(args->stream));
+  if (out) ++g_launches;
+  if (e == cudaErrorInvalidValue) return fail(FL_ERR_WORKSPACE, "out needs n_records * (8 + max_tiles) words");
+  return e == cudaSuccess ? FL_OK : cuda_fail(e, "schedule dump launch");
+}
+
+fl_status fl_diag_pipe_rate(int32_t op, int32_t iters, float* sink, int64_t* ops, void* stream) {
+  if (op < 0 || op > 3 || iters <= 0) return fail(FL_ERR_INVALID_ARGUMENT, "op in 0..3, iters > 0");
+  if (!sink) return fail(FL_ERR_INVALID_ARGUMENT, "NULL sink");
+  const int n = device_sm_count();
+  // elementary ops per chain step: ex2.f32 / tanh 1, ex2.bf16x2 2 (packed), FFMA2 1 (4 packed pairs / 8 chains)
+  const int64_t per = op == 1 ? 2 : 1;
+  if (ops) *ops = (int64_t)n * 512 * 8 * (int64_t)iters * per;
+  cudaError_t e = launch_pipe_rate(op, iters, n, sink, static_cast<cudaStream_t>(stream));
+  ++g_launches;
+  return e == cudaSuccess ? FL_OK : cuda_fail(e, "pipe rate launch");
 }
 
 static fl_status rsa_summaries(const fl_tensor* k, fl_tensor* kmin, fl_tensor* kmax, int32_t blk_k, int64_t k_begin,

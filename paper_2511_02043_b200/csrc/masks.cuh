@@ -53,6 +53,13 @@ __host__ __device__ inline Interval row_interval(const AttnParams& p, int32_t b,
   return {lo, hi};
 }
 
+// A 128-key tile starting at k0 needs no per-element mask for a row with interval iv iff it lies
+// inside the interval and inside [0, S_k).  The kernel (attn_tc.cuh) and the schedule dump
+// (fl_debug_schedule) classify tiles with this one predicate.
+__host__ __device__ inline bool tile_inside(const Interval& iv, int32_t k0, int32_t Sk) {
+  return k0 >= iv.lo && k0 + 128 <= iv.hi && k0 + 128 <= Sk;
+}
+
 // Union of the row intervals of rows [q_first, q_last] (all intervals are monotone in q).
 __host__ __device__ inline Interval rows_union(const AttnParams& p, int32_t b, int32_t q_first, int32_t q_last) {
   Interval a = row_interval(p, b, q_first), z = row_interval(p, b, q_last);

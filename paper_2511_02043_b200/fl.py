@@ -214,6 +214,43 @@ def diag_umma_gemm(a: torch.Tensor, b: torch.Tensor, n: int, k: int, b_mn_major=
     return c
 
 
+def debug_schedule(q, k, v, **variant):
+    """The bf16 kernel's (unit, warpgroup) work and tile classes for this problem (fl_debug_schedule):
+    int32 numpy array [n_records, 8 + max_tiles] (see include/fl_attn.h)."""
+    import numpy as np
+    out = torch.empty(out_shape(q, v, variant.get("diff", False)), device=q.device, dtype=q.dtype)
+    keep: list = []
+    a = make_args(q, k, v, out, None, keep=keep, **variant)
+    n, mt = C.c_int64(0), C.c_int32(0)
+    _lib.check(_lib.lib().fl_debug_schedule(C.byref(a), None, 0, C.byref(n), C.byref(mt)))
+    buf = torch.empty(n.value * (8 + mt.value), dtype=torch.int32, device=q.device)
+    _lib.check(_lib.lib().fl_debug_schedule(C.byref(a), buf.data_ptr(), buf.numel(), C.byref(n), C.byref(mt)))
+    torch.cuda.synchronize(q.device)
+    return buf.cpu().numpy().reshape(n.value, 8 + mt.value)
+
+
+PIPE_OPS = {"ex2_f32": 0, "ex2_bf16x2": 1, "tanh_f32": 2, "ffma2": 3}
+
+
+def pipe_rate(op: str, device=None, iters: int = 4096, reps: int = 5) -> float:
+    """Measured throughput (elementary ops / s) of one MUFU / FMA operation (fl_diag_pipe_rate), the
+    best of `reps` launches timed with CUDA events on the current stream."""
+    device = torch.device(device or "cuda")
+    sink = torch.empty(1 << 20, dtype=torch.float32, device=device)
+    s = torch.cuda.current_stream(device)
+    ops = C.c_int64(0)
+    best = 0.0
+    for r in range(reps + 1):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        _lib.check(_lib.lib().fl_diag_pipe_rate(PIPE_OPS[op], iters, sink.data_ptr(), C.byref(ops), s.cuda_stream))
+        e1.record(s)
+        torch.cuda.synchronize(device)
+        if r:
+            best = max(best, ops.value / (e0.elapsed_time(e1) * 1e-3))
+    return best
+
+
 def shard_range(units: int, world: int, rank: int):
     b, e = C.c_int64(), C.c_int64()
     _lib.lib().fl_shard_range(units, world, rank, C.byref(b), C.byref(e))

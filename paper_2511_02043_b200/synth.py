@@ -42,31 +42,38 @@ def _slabs(shape, lead):
     return n, inner
 
 
+def _slab_ids(n, slab_range, slabs):
+    if slabs is not None:
+        return list(slabs)
+    b, e = (0, n) if slab_range is None else slab_range
+    return list(range(b, e))
+
+
 def uniform(shape, *, seed=0, tensor="q", dtype=torch.bfloat16, lo=-1.0, hi=1.0, lead=2,
-            slab_range=None) -> torch.Tensor:
+            slab_range=None, slabs=None) -> torch.Tensor:
     """U[lo,hi) drawn slab by slab over the first ``lead`` dims.
 
-    slab_range=(begin, end) returns only those slabs (flattened over the lead
-    dims), identical to the same slabs of the full tensor."""
+    slab_range=(begin, end) -- or an explicit list ``slabs`` of flattened slab ids -- returns only
+    those slabs (flattened over the lead dims), identical to the same slabs of the full tensor."""
     n, inner = _slabs(shape, lead)
-    b, e = (0, n) if slab_range is None else slab_range
-    out = np.empty((e - b,) + tuple(inner), dtype=np.float32)
-    for i in range(b, e):
-        out[i - b] = _rng(seed, tensor, i).random(tuple(inner), dtype=np.float32) * (hi - lo) + lo
+    ids = _slab_ids(n, slab_range, slabs)
+    out = np.empty((len(ids),) + tuple(inner), dtype=np.float32)
+    for j, i in enumerate(ids):
+        out[j] = _rng(seed, tensor, i).random(tuple(inner), dtype=np.float32) * (hi - lo) + lo
     t = _to(out, dtype)
-    return t.reshape(tuple(shape)) if slab_range is None else t
+    return t.reshape(tuple(shape)) if slab_range is None and slabs is None else t
 
 
-def constant_v(shape, *, seed=0, dtype=torch.bfloat16, lead=2, slab_range=None) -> torch.Tensor:
+def constant_v(shape, *, seed=0, dtype=torch.bfloat16, lead=2, slab_range=None, slabs=None) -> torch.Tensor:
     """V[..., k, :] = c (one c ~ U[-1,1)^Dv per slab) -- the closed-form check O = c (P13)."""
     n, inner = _slabs(shape, lead)
-    b, e = (0, n) if slab_range is None else slab_range
-    out = np.empty((e - b,) + tuple(inner), dtype=np.float32)
-    for i in range(b, e):
+    ids = _slab_ids(n, slab_range, slabs)
+    out = np.empty((len(ids),) + tuple(inner), dtype=np.float32)
+    for j, i in enumerate(ids):
         c = _rng(seed, "v", i).random((inner[-1],), dtype=np.float32) * 2 - 1
-        out[i - b] = np.broadcast_to(c, tuple(inner))
+        out[j] = np.broadcast_to(c, tuple(inner))
     t = _to(out, dtype)
-    return t.reshape(tuple(shape)) if slab_range is None else t
+    return t.reshape(tuple(shape)) if slab_range is None and slabs is None else t
 
 
 def _pm1_keys(k_shape, seed):
@@ -162,30 +169,34 @@ def alibi_slopes(H: int) -> np.ndarray:
     return np.array([2.0 ** (-8.0 * (h + 1) / H) for h in range(H)], dtype=np.float32)
 
 
-def clustered_qk(q_shape, k_shape, *, seed=2, blk=128, n_clusters=32, dtype=torch.bfloat16, b_range=None):
+def clustered_qk(q_shape, k_shape, *, seed=2, blk=128, n_clusters=32, dtype=torch.bfloat16, b_range=None,
+                 kv_head_range=None):
     """RSA inputs: per slab 32 centroids in {+-0.6}^D; each KV block / q block
     draws a cluster and its rows are clip(c_z + 0.4 U[-1,1), +-1).
 
     Shapes are the GLOBAL [B,H,S,D]; b_range=(b0, b1) returns only batches
-    [b0, b1) (identical to that slice of the full tensors: streams are keyed by
-    the global batch index)."""
+    [b0, b1) and kv_head_range=(g0, g1) only KV heads [g0, g1) with their query
+    heads (identical to that slice of the full tensors: streams are keyed by
+    the global batch and head indices)."""
     b0, b1 = (0, q_shape[0]) if b_range is None else b_range
+    grp = q_shape[1] // k_shape[1]
+    g0, g1 = (0, k_shape[1]) if kv_head_range is None else kv_head_range
 
     def one(shape, tensor, heads_per_centroid_slab):
         _, H, S, D = shape
-        out = np.empty((b1 - b0, H, S, D), dtype=np.float32)
+        h0, h1 = g0 * heads_per_centroid_slab, g1 * heads_per_centroid_slab
+        out = np.empty((b1 - b0, h1 - h0, S, D), dtype=np.float32)
         nb = (S + blk - 1) // blk
         for b in range(b0, b1):
-            for h in range(H):
+            for h in range(h0, h1):
                 r = _rng(seed, tensor, b * H + h)
                 cr = _rng(seed + 1000, "k", b * (H // heads_per_centroid_slab) + h // heads_per_centroid_slab)
                 cents = np.where(cr.random((n_clusters, D)) < 0.5, -0.6, 0.6).astype(np.float32)
                 z = r.integers(0, n_clusters, size=nb)
                 x = cents[np.repeat(z, blk)[:S]]
                 x += 0.4 * (r.random((S, D), dtype=np.float32) * 2 - 1)
-                np.clip(x, -1.0, 1.0, out=out[b - b0, h])
+                np.clip(x, -1.0, 1.0, out=out[b - b0, h - h0])
         return _to(out, dtype)
-    grp = q_shape[1] // k_shape[1]
     return one(q_shape, "q", grp), one(k_shape, "k", 1)
 
 

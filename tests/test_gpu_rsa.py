@@ -132,6 +132,11 @@ SEL_CASES = [
     dict(name="nkb256_tail", B=1, Hq=1, Hkv=1, Sq=1024, Sk=32768, D=128, topk=16),
     dict(name="nkb512_D64", B=1, Hq=1, Hkv=1, Sq=256, Sk=65536, D=64, topk=16),
     dict(name="topk0", B=1, Hq=1, Hkv=1, Sq=1024, Sk=1024, D=128, topk=0),
+    # diagonal c = 129 (and 257 at D = 64): candidate c-1 opens a new 128-block accumulator tile; the
+    # planted key block (= the query block's own rows) has the top score, so dropping it fails
+    dict(name="c129_plant", B=1, Hq=1, Hkv=1, Sq=16640, Sk=16640, D=128, topk=16, plant=[(129, 128), (200, 199)]),
+    dict(name="c257_plant_D64", B=1, Hq=1, Hkv=1, Sq=33024, Sk=33024, D=64, topk=16,
+         plant=[(129, 128), (257, 256)]),
 ]
 
 
@@ -140,8 +145,12 @@ def test_selection_vs_oracle(fl, case):
     B, Hq, Hkv, Sq, Sk, D, topk = (case[x] for x in ("B", "Hq", "Hkv", "Sq", "Sk", "D", "topk"))
     ca = case.get("causal_align", 0)
     q, k = synth.clustered_qk((B, Hq, Sk, D), (B, Hkv, Sk, D), seed=2)
+    for i, j in case.get("plant", ()):                  # key block j := query block i (bottom-right, Sq = Sk)
+        k[:, :, j * 128:(j + 1) * 128] = q[:, :Hkv, i * 128:(i + 1) * 128]
     q = q[:, :, Sk - Sq:].contiguous()                 # the last Sq queries (bottom-right)
     ref_idx, ref_cnt, sc = oracle.rsa_select(q, k, topk=topk, causal_align=ca, want_scores=True)
+    for i, j in case.get("plant", ()):
+        assert j in ref_idx[0, i, :ref_cnt[0, i]]       # the planted block is the oracle's pick
     kmin, kmax = fl.rsa_build_summaries(k.cuda(), 128)
     idx, cnt = fl.rsa_select(q.cuda(), kmin, kmax, Sk, topk=topk, causal_align=ca)
     torch.cuda.synchronize()

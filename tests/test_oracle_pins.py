@@ -514,3 +514,35 @@ def test_rsa_selection_matches_sort_reference(Sq, Sk, align):
             want = sorted({0, c, *order})
             assert list(idx[h, i, : cnt[h, i]]) == want
             assert cnt[h, i] == topk + 2
+
+
+def test_keep_rows_is_the_mask_predicate():
+    """oracle.keep_rows (definition step 2, used by the T2 schedule test) against the predicates written
+    out: Listing 2's window (G4), causal / prefix (G5, G12 both alignments), documents (G6),
+    key mask, block list (G10)."""
+    Sq, Sk = 37, 50
+    q, k, v = rnd(2, 2, Sq, 4, seed=70), rnd(2, 2, Sk, 4, seed=71), rnd(2, 2, Sk, 4, seed=72)
+    rows = np.arange(2 * 2 * Sq)
+    b, h, qq = rows // (2 * Sq), (rows // Sq) % 2, rows % Sq
+    kk = np.arange(Sk)[None, :]
+    qa = (qq + Sk - Sq)[:, None]
+    offs = np.array([[0, 7, 30, 50], [0, 20, 21, 50]], dtype=np.int32)
+    doc = lambda b_, x: np.searchsorted(offs[b_], x, side="right") - 1
+    km = (torch.arange(Sk) % 3 != 1).to(torch.uint8).view(1, Sk).expand(2, Sk)
+    expect = {
+        "causal": (dict(mask="causal"), kk <= qa),
+        "topleft": (dict(mask="causal", causal_align=1), kk <= qq[:, None]),
+        "sliding": (dict(mask="sliding", window=5), (kk <= qa) & (qa - kk <= 5)),
+        "prefix": (dict(mask="prefix", prefix=9), (kk < 9) | (kk <= qa)),
+        "document": (dict(mask="document", doc_offsets=offs),
+                     np.stack([doc(bb, np.arange(Sk)) == doc(bb, a) for bb, a in zip(b, qa[:, 0])])),
+        "keymask": (dict(key_mask=km), np.broadcast_to(km[0].numpy().astype(bool), (len(rows), Sk))),
+    }
+    for name, (kw, want) in expect.items():
+        got = oracle.keep_rows(q, k, v, rows, **kw).astype(bool)
+        assert np.array_equal(got, want), name
+    idx = np.array([[[0, 2, -1]] * 3] * 4, dtype=np.int32)
+    cnt = np.array([[2] * 3] * 4, dtype=np.int32)
+    got = oracle.keep_rows(q, k, v, rows, mask="blocklist", blk_idx=idx, blk_cnt=cnt, blk_q=16, blk_k=16).astype(bool)
+    listed = ((kk // 16) == 0) | ((kk // 16) == 2)
+    assert np.array_equal(got, listed & (kk <= qa))
