@@ -351,7 +351,7 @@ def dense_job(names, rank, world, device, with_host=True):
     cfg0 = VARIANTS[names[0]]
     wl = names[0] if len(names) == 1 else "flexattention_variants(" + ",".join(names) + ")"
     job = Job(names[0] if len(names) == 1 else "flex",
-              f"{wl}_bf16_B{cfg0['B']}_H{cfg0['H']}_S{cfg0['S']}_D{cfg0['D']}")
+              f"{wl}_{cfg0.get('dtype', 'bf16')}_B{cfg0['B']}_H{cfg0['H']}_S{cfg0['S']}_D{cfg0['D']}")
     maps = 2 if cfg0.get("diff") else 1
     ws = torch.empty(1 << 20, dtype=torch.uint8, device=device)       # scheduler counter + packed key mask
     blocks = []                                                       # (blk, host, q, k, v, out)
@@ -368,7 +368,8 @@ def dense_job(names, rank, world, device, with_host=True):
         for blk, host, q, k, v, out in blocks:
             kw, offs = block_variant_kw(cfg, blk)
             flops += kept_pairs(block_cfg(cfg, blk), offs) * flops_per_pair(cfg)
-            eflops += executed_pairs(block_cfg(cfg, blk), offs) * flops_per_pair(cfg)
+            if cfg.get("dtype") != "f32":                # 128 x 128 tiles of the tcgen05 kernel
+                eflops += executed_pairs(block_cfg(cfg, blk), offs) * flops_per_pair(cfg)
             nbytes += sum(t.numel() * t.element_size() for t in (q, k, v, out))
             dkw = _dev_kw(kw, device)
             fns.append(lambda q=q, k=k, v=v, out=out, dkw=dkw: fl.attn_fwd(q, k, v, out=out, workspace=ws, **dkw))

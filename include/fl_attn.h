@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define FL_ABI_VERSION 1
+#define FL_ABI_VERSION 2
 
 typedef enum {
   FL_OK = 0,
@@ -105,6 +105,13 @@ typedef struct {
   fl_tensor blk_cnt;         /* FL_MASK_BLOCKLIST: i32 [B*(G)*Hq, n_qblk] */
   int32_t blk_q;             /* FL_MASK_BLOCKLIST query block (must be 128) */
   int32_t blk_k;             /* FL_MASK_BLOCKLIST key block (must be 128) */
+  /* Paged KV (serving-side RSA): when kv_page_table.data != NULL, k and v are page
+   * POOLS of rank 4 [n_pages, Hkv(x2 if diff), 128, D] (one 128-key page per KV tile, any page order),
+   * and logical KV tile t of batch b (keys [128 t, 128 t + 128)) is page kv_page_table[b, t].  i32
+   * [B, n_pages_per_seq], contiguous rows; the logical key count S_k is kv_len (<= 128 n_pages_per_seq).
+   * bf16 only, rank-4 q only (G = 1); every mask incl. block lists, and the split-KV decode path. */
+  fl_tensor kv_page_table;
+  int32_t kv_len;
 } fl_variant;
 
 typedef struct {
@@ -119,7 +126,7 @@ typedef struct {
   size_t workspace_bytes;
 } fl_attn_args;
 
-/* Supported set (ABI v1):
+/* Supported set (ABI v2 = v1 + paged KV):
  *   f32 q/k/v/o  : exact-fp32 SIMT path, every variant, D_qk, D_v <= 128.
  *   bf16 q/k/v/o : tcgen05/TMEM/TMA persistent kernel, D_qk == D_v in {32, 64, 128}; every mask,
  *                  mod, bias, key_mask, gate; diff (lse must be absent with diff).  FL_MASK_BLOCKLIST

@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(HERE, "libfl_attn.so")
 
 FL_BF16, FL_F32, FL_U8, FL_I32 = 0, 1, 2, 3
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 EXPORTS = ["fl_attn_fwd", "fl_attn_workspace_size", "fl_attn_host_scratch_size", "fl_attn_fwd_host",
            "fl_rsa_build_summaries", "fl_rsa_update_summaries", "fl_rsa_select", "fl_shard_range", "fl_diag_umma_gemm",
@@ -32,6 +32,7 @@ class Variant(C.Structure):
         ("bias", Tensor), ("key_mask", Tensor), ("gate_mode", C.c_int32), ("gate", Tensor),
         ("diff", C.c_int32), ("lambda_", C.c_float), ("lambda_h", Tensor),
         ("blk_idx", Tensor), ("blk_cnt", Tensor), ("blk_q", C.c_int32), ("blk_k", C.c_int32),
+        ("kv_page_table", Tensor), ("kv_len", C.c_int32),
     ]
 
 

@@ -114,16 +114,15 @@ struct TcCfg {
   static constexpr int BIAS_TILE = 128 * 128 * 2;
   static constexpr int SMEM_BIAS = SMEM_RING + NSLOT * TILE_BYTES;
   static constexpr int SMEM_BAR = SMEM_BIAS + (BIAS_TMA_OK ? 4 * BIAS_TILE : 0);
-  // q_full q_empty | full[NSLOT] empty[NSLOT] | s_full[2] p_full[4] o_full[2] s_free[2] | unit_full[2]
-  // unit_empty[2] | bias_full[4] bias_empty[4]
-  static constexpr int NBAR = 2 + 2 * NSLOT + 10 + 4 + 8;
+  // q_full q_empty | full[NSLOT] empty[NSLOT] | s_full[2] p_full[2] o_full[2] | unit_full[2] unit_empty[2]
+  // | bias_full[4] bias_empty[4]
+  static constexpr int NBAR = 2 + 2 * NSLOT + 6 + 4 + 8;
   static constexpr int SMEM_SCHED = SMEM_BAR + NBAR * 8 + 16;       // blocklist schedule (RSA), 2 slots
   static constexpr int SCHED_WORDS = 2 * kMaxSelTc + 8;   // schedule + meta (n, lo0, hi0, lo1, hi1, ..., unit id)
   static constexpr int KBITS_WORDS = 64;             // small heads: key-mask bits (S_k <= 2048) in the unit slot
   static constexpr int SMEM_ML = SMEM_SCHED + 2 * SCHED_WORDS * 4;      // LIST: WG1's (m, l) per row
   static constexpr int SMEM_TOTAL = SMEM_ML + (LIST ? 2 * 128 * 4 : 0) + 1024;  // + alignment slack
   static constexpr uint32_t IDESC_S = idesc_bf16_f32(128, BN, 0);   // Q (K-major) x K (K-major)
-  static constexpr uint32_t IDESC_S64 = idesc_bf16_f32(128, 64, 0); // half an S tile (64 keys)
   static constexpr uint32_t IDESC_O = idesc_bf16_f32(128, D, 1);    // P (TMEM) x V (MN-major)
   // Small heads with a TMA'd pair bias: the tensor core adds it, S += (c I) . Bias with c = 1/scale
   // split into two bf16 terms (c_hi + c_lo, relative error ~2e-7); the scaled identities live in TMEM
@@ -148,17 +147,6 @@ struct EmuCfg {
   static constexpr uint32_t MASK = MOD == MOD_SOFTCAP ? 0x4Au : (D <= 64 ? 0x11u : 0u);
 #endif
 };
-// Split tiles (kSplit): the softmax warpgroup publishes P in two 64-key halves (p_full[wg*2+h]) and frees
-// its S columns as soon as they sit in registers (s_free), so the MMA issuer writes the first half of the
-// next S tile (keys 0-63 -> S columns [0,64), disjoint from P in [64,128)) while the softmax still runs,
-// starts PV on P's first half while the second half is computed, and only the second S half waits for
-// PV to release P.  The warpgroup's exposed tensor-pipe latency per tile drops from PV + S (1024 cycles
-// at D = 128) to half a PV + half an S.
-#ifndef FL_NO_SPLIT
-constexpr bool kSplit = true;
-#else
-constexpr bool kSplit = false;
-#endif
 // Ping-pong of the two softmax warpgroups' exp loops on named barriers (FA3-style).  Measured
 // slower with the persistent kernel (causal 982 vs 1071 TF/s, diff 624 vs 681): the alternation
 // serialises the exp loops while neither the MUFU nor the issue slots are saturated.  Opt-in.
@@ -293,10 +281,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   uint64_t* full = bars + 2;
   uint64_t* empty = full + C::NSLOT;
   uint64_t* s_full = empty + C::NSLOT;
-  uint64_t* p_full = s_full + 2;                     // [wg * 2 + half]
-  uint64_t* o_full = p_full + 4;
-  uint64_t* s_free = o_full + 2;                     // kSplit: S_i's columns loaded into registers
-  uint64_t* unit_full = s_free + 2;                  // work-unit broadcast (producer -> MMA, softmax), 2 slots
+  uint64_t* p_full = s_full + 2;
+  uint64_t* o_full = p_full + 2;
+  uint64_t* unit_full = o_full + 2;                  // work-unit broadcast (producer -> MMA, softmax), 2 slots
   uint64_t* unit_empty = unit_full + 2;
   uint64_t* bias_full = unit_empty + 2;              // [wg * 2 + stage]
   uint64_t* bias_empty = bias_full + 4;
@@ -306,7 +293,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 #ifdef FL_NO_BIAS_MMA
   const bool bias_mma = false;
 #else
+#ifdef FL_NO_BIAS_MMA
+  const bool bias_mma = false;
+#else
   const bool bias_mma = bias_tma && MOD == MOD_NONE;  // raw-score domain: S += bias / scale on the tensor core
+#endif
 #endif
   uint32_t* sched_base = reinterpret_cast<uint32_t*>(smem + C::SMEM_SCHED);
 
@@ -322,10 +313,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i * 2], 128);
-      mbar_init(&p_full[i * 2 + 1], 128);
+      mbar_init(&p_full[i], 128);
       mbar_init(&o_full[i], 1);
-      mbar_init(&s_free[i], 4);                      // one elected lane per warp of the warpgroup
       mbar_init(&unit_full[i], 1);
       mbar_init(&unit_empty[i], 1 + 256);            // MMA lane + both softmax warpgroups
       for (int st = 0; st < 2; ++st) {
@@ -446,11 +435,13 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         }
         auto load_entry = [&](const CUtensorMap* m, int tile, int head, int gg, int bb) {
           const int slot = e % C::NSLOT;
+          int row, bc;
+          kv_tile_coords(p, w.b, tile, bb, row, bc);    // paged KV: the tile's page of the pool
           if (e >= C::NSLOT) mbar_wait(&empty[slot], ((e / C::NSLOT) - 1) & 1);
           mbar_arrive_expect_tx(&full[slot], C::TILE_BYTES);
           uint8_t* dst = sRing + slot * C::TILE_BYTES;
           for (int c = 0; c < C::NCH; ++c)
-            tma_load_5d(dst + c * C::CHUNK_BYTES, m, &full[slot], c * C::CH, tile * C::BN, head, gg, bb);
+            tma_load_5d(dst + c * C::CHUNK_BYTES, m, &full[slot], c * C::CH, row, head, gg, bc);
           ++e;
         };
         for (int j = next_tile(w, w.lo_cta - 1); j >= 0; j = next_tile(w, j)) {
@@ -506,18 +497,15 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       };
       int bcnt_m[2] = {0, 0};                          // bias tiles consumed per warpgroup (bias_mma)
       const uint32_t sbias_addr = smem_u32(sBias);
-      // S_i (or, with kSplit, half hf of it: keys [64 hf, 64 hf + 64) -> S columns [64 hf, 64 hf + 64))
-      auto issue_s_part = [&](int i, int kslot, int hf, bool whole) {
-        const uint32_t qa = sq_addr + (LIST ? 0 : i) * C::TILE_BYTES;
-        const uint32_t ka = ring_addr + kslot * C::TILE_BYTES + (whole ? 0 : hf * 64 * C::SWB);
-        const uint32_t dcol = tmem + (i ? C::COL_S1 : C::COL_S0) + (whole ? 0 : hf * 64);
+      auto issue_s = [&](int i, int kslot) {
+        const uint32_t qa = sq_addr + (LIST ? 0 : i) * C::TILE_BYTES, ka = ring_addr + kslot * C::TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk * 16 / C::CH) * C::CHUNK_BYTES + (kk * 16 % C::CH) * 2;
-          umma_ss(dcol, smem_desc(qa + off, 16, C::SBO, C::LAYOUT), smem_desc(ka + off, 16, C::SBO, C::LAYOUT),
-                  whole ? C::IDESC_S : C::IDESC_S64, kk > 0);
+          umma_ss(tmem + (i ? C::COL_S1 : C::COL_S0), smem_desc(qa + off, 16, C::SBO, C::LAYOUT),
+                  smem_desc(ka + off, 16, C::SBO, C::LAYOUT), C::IDESC_S, kk > 0);
         }
-        if (bias_mma && (whole || hf == 1)) {          // S_i += (c_hi I + c_lo I) . Bias tile (whole tile)
+        if (bias_mma) {                                // S_i += (c_hi I + c_lo I) . Bias tile
           const int st = bcnt_m[i] & 1;
           mbar_wait(&bias_full[i * 2 + st], (bcnt_m[i] >> 1) & 1);
           tc_fence_after();
@@ -531,41 +519,24 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           umma_commit(&bias_empty[i * 2 + st]);
           ++bcnt_m[i];
         }
-      };
-      auto issue_s = [&](int i, int kslot) {
-        issue_s_part(i, kslot, 0, true);
         umma_commit(&s_full[i]);
       };
       int pv_cnt[2] = {0, 0};                          // cumulative: p_full parity
       bool first_pv[2];                                // per unit: first PV overwrites O
-      // PV_i over keys [64 hf, 64 hf + 64) of the tile (P half hf); hf = -1: the whole tile
-      auto issue_pv_part = [&](int i, int vslot, int hf) {
-        mbar_wait(&p_full[i * 2 + (hf > 0 ? 1 : 0)], pv_cnt[i] & 1);
+      auto issue_pv = [&](int i, int vslot) {
+        mbar_wait(&p_full[i], pv_cnt[i] & 1);
         tc_fence_after();
         const uint32_t va = ring_addr + vslot * C::TILE_BYTES;
         const uint32_t pcol = (i ? C::COL_S1 : C::COL_S0) + C::P_OFF;
-        const int k_lo = hf < 0 ? 0 : hf * (C::BN / 32), k_hi = hf < 0 ? C::BN / 16 : (hf + 1) * (C::BN / 32);
 #pragma unroll
-        for (int kk = k_lo; kk < k_hi; ++kk) {
+        for (int kk = 0; kk < C::BN / 16; ++kk) {
           umma_ts(tmem + (i ? C::COL_O1 : C::COL_O0), tmem + pcol + kk * 8,
                   smem_desc(va + kk * 16 * C::SWB, C::CHUNK_BYTES, C::SBO, C::LAYOUT), C::IDESC_O,
                   (!first_pv[i] || kk > 0) ? 1u : 0u);
         }
-        if (hf != 0) {
-          first_pv[i] = false;
-          ++pv_cnt[i];
-        }
+        first_pv[i] = false;
+        ++pv_cnt[i];
       };
-      auto issue_pv = [&](int i, int vslot) { issue_pv_part(i, vslot, -1); };
-      int s_iss[2] = {0, 0};                           // kSplit: S_i issues over the CTA's life (s_free parity)
-      auto wait_s_free = [&](int i) {
-        if (s_iss[i] > 0) mbar_wait(&s_free[i], (s_iss[i] - 1) & 1);
-        ++s_iss[i];
-      };
-      // K of warpgroup 1 is a separate ring entry for diff (map 1) and block lists (its own tile);
-      // V is separate for block lists only.  Entries a warpgroup does not need are not loaded.
-      constexpr bool kSepK = DIFF || LIST || PAIR;
-      constexpr bool kSepV = LIST || PAIR;
       int it = 0;
       for (;; ++it) {
         const int u = get_unit(it);
@@ -576,14 +547,14 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         mbar_wait(q_full, it & 1);                     // always: Q of this unit has landed
         tc_fence_after();
         if (j >= 0) {
+          // K of warpgroup 1 is a separate ring entry for diff (map 1) and block lists (its own tile);
+          // V is separate for block lists only.  Entries a warpgroup does not need are not loaded.
+          constexpr bool kSepK = DIFF || LIST || PAIR;
+          constexpr bool kSepV = LIST || PAIR;
           int ks0 = acquire();
           int ks1 = kSepK ? ((!kSepV || needs(w, 1, j)) ? acquire() : -1) : ks0;
-#pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            if (!needs(w, i, j)) continue;
-            if (kSplit) wait_s_free(i);
-            issue_s(i, i ? ks1 : ks0);
-          }
+          if (needs(w, 0, j)) issue_s(0, ks0);
+          if (needs(w, 1, j)) issue_s(1, ks1);
           umma_commit(&empty[ks0]);
           if (kSepK && ks1 >= 0) umma_commit(&empty[ks1]);
           if (next_tile(w, j) < 0) umma_commit(q_empty);   // Q is free once the last S MMA is done
@@ -596,52 +567,22 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
               kn0 = acquire();
               kn1 = kSepK ? ((!kSepV || needs(w, 1, jn)) ? acquire() : -1) : kn0;
             }
-            if constexpr (kSplit) {
-              // per warpgroup: S_i(j+1) keys 0-63 (overlaps the softmax of tile j), PV_i(j) by halves as P
-              // arrives, then S_i(j+1) keys 64-127 into the columns P_i(j) occupied
-#pragma unroll
-              for (int i = 0; i < 2; ++i) {
-                const bool sn = jn >= 0 && needs(w, i, jn);
-                const int kn = i ? kn1 : kn0;
-                if (sn) {
-                  wait_s_free(i);
-                  issue_s_part(i, kn, 0, false);
-                }
-                if (needs(w, i, j)) {
-                  issue_pv_part(i, i ? vb : va, 0);
-                  issue_pv_part(i, i ? vb : va, 1);
-                  if (j == (i ? w.hi[1] : w.hi[0]) - 1) umma_commit(&o_full[i]);
-                }
-                if (sn) {
-                  issue_s_part(i, kn, 1, false);
-                  umma_commit(&s_full[i]);
-                }
-              }
-              umma_commit(&empty[va]);
-              if (kSepV && vb >= 0) umma_commit(&empty[vb]);
-              if (jn >= 0) {
-                umma_commit(&empty[kn0]);
-                if (kSepK && kn1 >= 0) umma_commit(&empty[kn1]);
-                if (next_tile(w, jn) < 0) umma_commit(q_empty);
-              }
-            } else {
-              if (needs(w, 0, j)) {
-                issue_pv(0, va);
-                if (j == w.hi[0] - 1) umma_commit(&o_full[0]);
-              }
-              if (jn >= 0 && needs(w, 0, jn)) issue_s(0, kn0);
-              if (needs(w, 1, j)) {
-                issue_pv(1, vb);
-                if (j == w.hi[1] - 1) umma_commit(&o_full[1]);
-              }
-              umma_commit(&empty[va]);
-              if (kSepV && vb >= 0) umma_commit(&empty[vb]);
-              if (jn >= 0) {
-                if (needs(w, 1, jn)) issue_s(1, kn1);
-                umma_commit(&empty[kn0]);
-                if (kSepK && kn1 >= 0) umma_commit(&empty[kn1]);
-                if (next_tile(w, jn) < 0) umma_commit(q_empty);
-              }
+            if (needs(w, 0, j)) {
+              issue_pv(0, va);
+              if (j == w.hi[0] - 1) umma_commit(&o_full[0]);
+            }
+            if (jn >= 0 && needs(w, 0, jn)) issue_s(0, kn0);
+            if (needs(w, 1, j)) {
+              issue_pv(1, vb);
+              if (j == w.hi[1] - 1) umma_commit(&o_full[1]);
+            }
+            umma_commit(&empty[va]);
+            if (kSepV && vb >= 0) umma_commit(&empty[vb]);
+            if (jn >= 0) {
+              if (needs(w, 1, jn)) issue_s(1, kn1);
+              umma_commit(&empty[kn0]);
+              if (kSepK && kn1 >= 0) umma_commit(&empty[kn1]);
+              if (next_tile(w, jn) < 0) umma_commit(q_empty);
             }
             j = jn;
           }
@@ -724,11 +665,6 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       tmem_ld32(tmem + lane_base + col_s + 64, &s[64]);
       tmem_ld32(tmem + lane_base + col_s + 96, &s[96]);
       tmem_wait_ld();
-      if (kSplit) {                                    // S_i's columns may take the next tile's first half
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s_free[wg]);
-      }
       FL_T(2);                                         // 2: tcgen05.ld of S
       // ---- score modification (Eq.4) in the log2 domain: x = log2(e) * mod(scale * s)
       float x[128];
@@ -900,9 +836,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       float ls0 = 0.f, ls1 = 0.f, ls2 = 0.f, ls3 = 0.f;
       uint32_t pk[64];
 #pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {
-#pragma unroll
-      for (int c = hf * 64; c < hf * 64 + 64; c += 4) {
+      for (int c = 0; c < 128; c += 4) {
         float a0, a1, a2, a3;
         ffma2(a0, a1, x[c], x[c + 1], xscale, xscale, neg_m, neg_m);
         ffma2(a2, a3, x[c + 2], x[c + 3], xscale, xscale, neg_m, neg_m);
@@ -920,34 +854,21 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         pk[c >> 1] = pack_bf16(a0, a1);
         pk[(c >> 1) + 1] = pack_bf16(a2, a3);
       }
-      if (kSplit) {                                    // P keys [64 hf, 64 hf + 64): PV may start on them
-        tmem_st32(tmem + lane_base + col_s + C::P_OFF + hf * 32, &pk[hf * 32]);
-        tmem_wait_st();
-        tc_fence_before();
-        if (hf == 0 && LIST && o_lent) {               // PV1 of this tile overwrites O1: WG0 must have read it
-          named_bar_sync(5, 256);
-          o_lent = false;
-        }
-        mbar_arrive(&p_full[wg * 2 + hf]);
-      }
-      }
       FL_T(6);                                         // 6: exp loop
       if (common) {
         if (wg == 0) named_bar_arrive(3, 256);
         if (wg == 1) named_bar_arrive(2, 256);
       }
       l += (ls0 + ls1) + (ls2 + ls3);
-      if (!kSplit) {
-        tmem_st32(tmem + lane_base + col_s + C::P_OFF, &pk[0]);
-        tmem_st32(tmem + lane_base + col_s + C::P_OFF + 32, &pk[32]);
-        tmem_wait_st();
-        tc_fence_before();
-        if (LIST && o_lent) {                          // PV1 of this tile overwrites O1: WG0 must have read it
-          named_bar_sync(5, 256);
-          o_lent = false;
-        }
-        mbar_arrive(&p_full[wg * 2]);
+      tmem_st32(tmem + lane_base + col_s + C::P_OFF, &pk[0]);
+      tmem_st32(tmem + lane_base + col_s + C::P_OFF + 32, &pk[32]);
+      tmem_wait_st();
+      tc_fence_before();
+      if (LIST && o_lent) {                            // PV1 of this tile overwrites O1: WG0 must have read it
+        named_bar_sync(5, 256);
+        o_lent = false;
       }
+      mbar_arrive(&p_full[wg]);
       ++n_done;
       FL_T(7);                                         // 7: P store + arrive
     }
@@ -1053,7 +974,6 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           }
         }
         if (gated) {
-#pragma unroll
           uint4 g4[4];
 #pragma unroll
           for (int t8 = 0; t8 < 4; ++t8) g4[t8] = __ldg(gp + (c >> 3) + t8);

@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kDecCompute + 32, 1)
     const long long n_slots = my_items * bps;
     for (long long e0 = 0; e0 < n_slots; e0 += 32) {
       const long long es = e0 + lane;
-      int kb = -1, hkv = 0, gk = 0, bk = 0, gv = 0, bv = 0;
+      int kb = -1, hkv = 0, gk = 0, bk = 0, gv = 0, bv = 0, kr = 0;
       if (es < n_slots) {
         const long long it = blockIdx.x + (es / bps) * gridDim.x;
         const int i = split_of(it) * bps + (int)(es % bps);
@@ -143,12 +143,17 @@ __global__ void __launch_bounds__(kDecCompute + 32, 1)
         const DecRow dr = dec_row(p, bgh, q, row_interval(p, b, q));
         if (i < dr.n) kb = dr.list ? dr.list[i] : dr.lo_tile + i;
         if (kb * 128 >= p.Sk) kb = -1;
+        if (kb >= 0) {                                 // paged KV: the tile's page of the pools
+          kv_tile_coords(p, b, kb, bk, kr, bk);
+          bv = p.page_table ? bk : bv;
+        }
       }
       const int cnt = (int)min(32ll, n_slots - e0);
       for (int j = 0; j < cnt; ++j) {
         const int kbj = __shfl_sync(0xffffffffu, kb, j), hj = __shfl_sync(0xffffffffu, hkv, j);
         const int gkj = __shfl_sync(0xffffffffu, gk, j), bkj = __shfl_sync(0xffffffffu, bk, j);
         const int gvj = __shfl_sync(0xffffffffu, gv, j), bvj = __shfl_sync(0xffffffffu, bv, j);
+        const int krj = __shfl_sync(0xffffffffu, kr, j);
         if (lane == 0) {
           const int e = (int)(e0 + j);
           const int s = e % C::NST;
@@ -158,8 +163,8 @@ __global__ void __launch_bounds__(kDecCompute + 32, 1)
             uint8_t* ks = ring + s * 2 * C::TILE;
             mbar_arrive_expect_tx(&full[s], 2 * C::TILE);
             for (int c = 0; c < D / 64; ++c) {
-              tma_load_5d(ks + c * C::SLAB, &maps.k, &full[s], c * 64, kbj * 128, hj, gkj, bkj);
-              tma_load_5d(ks + C::TILE + c * C::SLAB, &maps.v, &full[s], c * 64, kbj * 128, hj, gvj, bvj);
+              tma_load_5d(ks + c * C::SLAB, &maps.k, &full[s], c * 64, krj, hj, gkj, bkj);
+              tma_load_5d(ks + C::TILE + c * C::SLAB, &maps.v, &full[s], c * 64, krj, hj, gvj, bvj);
             }
           } else {
             mbar_arrive(&full[s]);

@@ -263,14 +263,27 @@ fl_status prepare(const fl_attn_args* a, Prepared& P, bool device_ptrs) {
       return fail(FL_ERR_UNSUPPORTED, "the last dim of q/k/v/o must be contiguous");
   const int maps = var.diff ? 2 : 1;
   const int64_t B = P.q.size[0], G = P.q.size[1];
+  // paged KV: k / v are page pools [n_pages, H, 128, D]; their batch dim indexes pages
+  const bool paged = var.kv_page_table.data != nullptr;
+  if (paged) {
+    const fl_tensor& t = var.kv_page_table;
+    if (!P.bf16 || R != 4) return fail(FL_ERR_UNSUPPORTED, "paged KV: bf16, rank-4 q/k/v/o only");
+    if (t.dtype != FL_I32 || t.rank != 2 || t.size[0] != B || t.size[1] < 1 || t.stride[1] != 1)
+      return fail(FL_ERR_INVALID_ARGUMENT, "kv_page_table: i32 [B, n_pages] with contiguous rows");
+    if (P.k.size[3] != 128 || P.v.size[3] != 128)
+      return fail(FL_ERR_SHAPE_MISMATCH, "paged KV: k/v pools are [n_pages, H, 128, D] (128-key pages)");
+    if (var.kv_len < 0 || var.kv_len > t.size[1] * 128)
+      return fail(FL_ERR_INVALID_ARGUMENT, "paged KV: 0 <= kv_len <= 128 * n_pages_per_seq");
+  }
   for (const View5* t : {&P.k, &P.v, &P.o})
-    if (t->size[0] != B || t->size[1] != G) return fail(FL_ERR_SHAPE_MISMATCH, "batch dims of q/k/v/o differ");
+    if ((!paged || t == &P.o) && (t->size[0] != B || t->size[1] != G))
+      return fail(FL_ERR_SHAPE_MISMATCH, "batch dims of q/k/v/o differ");
   if (P.q.size[2] % maps || P.k.size[2] % maps) return fail(FL_ERR_SHAPE_MISMATCH, "diff: q, k carry 2*H heads");
   const int64_t Hq = P.q.size[2] / maps, Hkv = P.k.size[2] / maps;
   if (P.v.size[2] != Hkv || P.o.size[2] != Hq || Hkv == 0 || Hq % Hkv)
     return fail(FL_ERR_SHAPE_MISMATCH, "heads: need v.H == k.H/maps, o.H == q.H/maps, Hq %% Hkv == 0");
-  const int64_t Sq = P.q.size[3], Sk = P.k.size[3], Dqk = P.q.size[4], Dv = P.v.size[4];
-  if (P.o.size[3] != Sq || P.v.size[3] != Sk || P.k.size[4] != Dqk || P.o.size[4] != Dv)
+  const int64_t Sq = P.q.size[3], Sk = paged ? (int64_t)var.kv_len : P.k.size[3], Dqk = P.q.size[4], Dv = P.v.size[4];
+  if (P.o.size[3] != Sq || P.v.size[3] != P.k.size[3] || P.k.size[4] != Dqk || P.o.size[4] != Dv)
     return fail(FL_ERR_SHAPE_MISMATCH, "q/k/v/o sequence or head-dim sizes disagree");
   if (Sq >= (1ll << 30) || Sk >= (1ll << 30) || B * G * Hq >= (1ll << 30))
     return fail(FL_ERR_UNSUPPORTED, "sizes beyond 2^30");
@@ -378,7 +391,7 @@ fl_status prepare(const fl_attn_args* a, Prepared& P, bool device_ptrs) {
   if (device_ptrs) {
     const void* ptrs[] = {a->q.data, a->k.data, a->v.data, a->o.data, a->lse.data, var.bias.data, var.key_mask.data,
                           var.gate.data, var.alibi_slopes.data, var.lambda_h.data, var.doc_offsets.data,
-                          var.blk_idx.data, var.blk_cnt.data};
+                          var.blk_idx.data, var.blk_cnt.data, var.kv_page_table.data};
     for (const void* p : ptrs)
       if (!on_device(p)) return fail(FL_ERR_INVALID_ARGUMENT, "a tensor pointer is not device memory on this device");
   }
@@ -412,6 +425,8 @@ fl_status prepare(const fl_attn_args* a, Prepared& P, bool device_ptrs) {
   p.blk_q = var.blk_q; p.blk_k = var.blk_k;
   p.max_sel = var.mask == FL_MASK_BLOCKLIST ? (int)var.blk_idx.size[2] : 0;
   p.n_qblk = var.mask == FL_MASK_BLOCKLIST ? (int)((Sq + var.blk_q - 1) / var.blk_q) : 0;
+  p.page_table = static_cast<const int32_t*>(var.kv_page_table.data);
+  p.page_stride = paged ? var.kv_page_table.stride[0] : 0;
   p.in_dtype = P.bf16 ? 0 : 1;
   // Short query blocks (decode, S_q <= 16): split-KV kernels instead of 128-row tensor-core tiles.
   P.decode = P.bf16 && Sq <= 16 && maps == 1 && !P.bias.present && var.gate_mode == FL_GATE_NONE &&
@@ -532,7 +547,7 @@ bool is_contiguous(const fl_tensor& t) {
 
 fl_status plan_host(fl_attn_args& d, HostPlan& hp) {
   fl_tensor* ins[] = {&d.q, &d.k, &d.v, &d.var.bias, &d.var.key_mask, &d.var.gate, &d.var.alibi_slopes,
-                      &d.var.lambda_h, &d.var.doc_offsets, &d.var.blk_idx, &d.var.blk_cnt};
+                      &d.var.lambda_h, &d.var.doc_offsets, &d.var.blk_idx, &d.var.blk_cnt, &d.var.kv_page_table};
   for (fl_tensor* t : ins) {
     if (!t->data) continue;
     if (!is_contiguous(*t)) return fail(FL_ERR_UNSUPPORTED, "fl_attn_fwd_host: host tensors must be contiguous");

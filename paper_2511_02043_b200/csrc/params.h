@@ -43,9 +43,25 @@ struct AttnParams {
   float lambda; const float* lambda_h;
   // ---- block list (RSA)
   const int32_t* blk_idx; const int32_t* blk_cnt; int32_t blk_q, blk_k, max_sel, n_qblk;
+  // ---- paged KV: logical KV tile t of batch b is page page_table[b * page_stride + t] of the k/v pools
+  const int32_t* page_table; int64_t page_stride;
   int32_t in_dtype;        // 0 bf16, 1 f32
   int32_t* tile_ctr;       // bf16 path: persistent-scheduler ticket counter (workspace, zeroed per call)
 };
+
+// TMA (row, batch) coordinates of logical KV tile `tile` of batch b: contiguous K/V -> (128 tile, b);
+// paged K/V -> (0, page) with page = page_table[b, tile] (the pool's batch dim indexes pages).
+#ifdef __CUDACC__
+__device__ __forceinline__ void kv_tile_coords(const AttnParams& p, int b, int tile, int bb, int& row, int& bcoord) {
+  if (p.page_table) {
+    row = 0;
+    bcoord = __ldg(p.page_table + (int64_t)b * p.page_stride + tile);
+  } else {
+    row = tile * 128;
+    bcoord = bb;
+  }
+}
+#endif
 
 // TMA tensor maps for the tcgen05 kernel family (5-D: D, S, H, G, B).
 struct TmaMaps {

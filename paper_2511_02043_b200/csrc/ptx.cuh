@@ -235,6 +235,12 @@ FL_DEVICE void ffma2(float& dx, float& dy, float ax, float ay, float bx, float b
       : "=f"(dx), "=f"(dy)
       : "f"(ax), "f"(ay), "f"(bx), "f"(by), "f"(cx), "f"(cy));
 }
+FL_DEVICE void fmul2(float& dx, float& dy, float ax, float ay, float bx, float by) {
+  asm("{.reg .b64 a, b, d;\n\tmov.b64 a, {%2,%3};\n\tmov.b64 b, {%4,%5};\n\tmul.rn.f32x2 d, a, b;\n\t"
+      "mov.b64 {%0,%1}, d;}"
+      : "=f"(dx), "=f"(dy)
+      : "f"(ax), "f"(ay), "f"(bx), "f"(by));
+}
 FL_DEVICE void fadd2(float& dx, float& dy, float ax, float ay, float bx, float by) {
   asm("{.reg .b64 a, b, d;\n\tmov.b64 a, {%2,%3};\n\tmov.b64 b, {%4,%5};\n\tadd.rn.f32x2 d, a, b;\n\t"
       "mov.b64 {%0,%1}, d;}"

@@ -95,16 +95,24 @@ cudaError_t launch_rsa_summaries(const void* k, int64_t sb, int64_t sg, int64_t 
 }
 
 // ------------------------------------------------------------------ selection
-// Pipelined, warp-specialised: 384 threads, one CTA per SM, each CTA a contiguous range of
+// Pipelined, warp-specialised: 128 x (1 + kSelWG) threads, one CTA per SM, each CTA a contiguous range of
 // (b, g, h_kv, q-block) pairs (x grp heads), so the summaries of a (b, g, h_kv) are loaded once
 // per CTA per head it touches.
 //   warps 4-7 ("split" WG): q+ / q- split of the landed Q tile into the operand buffers; its
 //     thread 0 also issues the TMA loads (next Q tile into a separate raw buffer, summaries)
 //     and the tcgen05 MMAs into a double-buffered TMEM accumulator;
-//   warps 0-3 and 8-11 ("select" WGs, thread = TMEM lane = KV block, alternate items when GQA groups
+//   warps 0-3, 8-11, 12-15, 16-19 ("select" WGs, thread = TMEM lane = KV block, round-robin items when GQA groups
 //     do not span items): row max over the block's queries, running max over the heads of a GQA
 //     group, exact radix top-k, ascending list.
 // So the split of item n+1, the MMAs of item n+1 and the selection of item n overlap.
+// Select warpgroups per CTA.  The accumulator is released right after the row max, so the top-k of
+// up to kSelWG items runs concurrently; the radix passes are barrier / latency bound, not ALU bound.
+#ifndef FL_SEL_WG
+#define FL_SEL_WG 4
+#endif
+constexpr int kSelWG = FL_SEL_WG;
+constexpr int kSelThreads = 128 * (kSelWG + 1);
+
 template <int D>
 struct SelCfg {
   static constexpr int CH = 64;                         // bf16 per 128-byte swizzle row
@@ -115,12 +123,12 @@ struct SelCfg {
   // summaries (kmax, kmin) + raw Q + q+ / q- tiles + per-select-warpgroup scratch (256-bin histogram as
   // 16-bit counts, pass state, selection bitmap) + barriers + alignment slack
   static constexpr int SCR_WORDS = 128 + 16 + 16;
-  static constexpr int SCRATCH = 2 * SCR_WORDS * 4;
+  static constexpr int SCRATCH = kSelWG * SCR_WORDS * 4;
   static int smem(int n_mt) { return 2 * n_mt * QTILE + 3 * QTILE + SCRATCH + 128 + 1024; }
 };
 
 template <int D>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(kSelThreads, 1)
     rsa_select_kernel(const __grid_constant__ RsaSelParams p, const __grid_constant__ CUtensorMap tq,
                       const __grid_constant__ CUtensorMap tmin, const __grid_constant__ CUtensorMap tmax) {
   using C = SelCfg<D>;
@@ -134,8 +142,8 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sQraw = sMin + n_mt * C::QTILE;              // TMA destination of the next Q tile
   uint8_t* sQp = sQraw + C::QTILE;
   uint8_t* sQn = sQp + C::QTILE;
-  uint32_t* scratch = reinterpret_cast<uint32_t*>(sQn + C::QTILE);   // [2][SCR_WORDS], one per select WG
-  uint64_t* bars = reinterpret_cast<uint64_t*>(scratch + 2 * C::SCR_WORDS);
+  uint32_t* scratch = reinterpret_cast<uint32_t*>(sQn + C::QTILE);   // [kSelWG][SCR_WORDS], one per select WG
+  uint64_t* bars = reinterpret_cast<uint64_t*>(scratch + kSelWG * C::SCR_WORDS);
   uint64_t* bar_sum = bars;                             // summaries landed
   uint64_t* bar_q = bars + 1;                           // raw Q tile landed
   uint64_t* bar_qfree = bars + 2;                       // MMAs of the previous item done (q+/q-, summaries free)
@@ -258,10 +266,10 @@ __global__ void __launch_bounds__(384, 1)
     }
   } else {
     // ============================== selection (thread = KV block) ==============================
-    // Two select warpgroups (warps 0-3 and 8-11) take alternate items when each item has its own TMEM
+    // kSelWG select warpgroups (warps 0-3, 8-11, ...) take items round-robin when each item has its own TMEM
     // accumulator buffer and no GQA group spans items; otherwise warps 0-3 take every item.
-    const int sel = warp >= 8 ? 1 : 0;
-    const int nsel = (nbuf == 2 && p.grp == 1) ? 2 : 1;
+    const int sel = warp < 4 ? 0 : (warp - 4) / 4;      // warps 0-3, 8-11, 12-15, ...
+    const int nsel = (nbuf == 2 && p.grp == 1) ? kSelWG : 1;
     const int tt = t & 127, wq = warp & 3;              // thread / warp within the select warpgroup
     uint32_t* hist = scratch + sel * C::SCR_WORDS;      // [128] packed 16-bit bin counts
     uint32_t* rstate = hist + 128;                      // [16] digit / counts of the current pass
@@ -467,12 +475,12 @@ cudaError_t launch_rsa_select(const RsaSelParams& p0, const CUtensorMap& tq, con
     const int sm = SelCfg<128>::smem(n_mt);
     cudaError_t e = cudaFuncSetAttribute(rsa_select_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     if (e != cudaSuccess) return e;
-    rsa_select_kernel<128><<<grid, 384, sm, stream>>>(p, tq, tmin, tmax);
+    rsa_select_kernel<128><<<grid, kSelThreads, sm, stream>>>(p, tq, tmin, tmax);
   } else {
     const int sm = SelCfg<64>::smem(n_mt);
     cudaError_t e = cudaFuncSetAttribute(rsa_select_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     if (e != cudaSuccess) return e;
-    rsa_select_kernel<64><<<grid, 384, sm, stream>>>(p, tq, tmin, tmax);
+    rsa_select_kernel<64><<<grid, kSelThreads, sm, stream>>>(p, tq, tmin, tmax);
   }
   return cudaGetLastError();
 }

@@ -49,7 +49,7 @@ def _f32vec(x, device):
 def make_args(q, k, v, o, lse=None, *, scale=0.0, mod="none", softcap=0.0, alibi_slopes=None, mask="none",
               window=0, prefix=0, doc_offsets=None, doc_causal=False, causal_align=0, bias=None, key_mask=None,
               gate_mode="none", gate=None, diff=False, lam=0.0, lambda_h=None, blk_idx=None, blk_cnt=None,
-              blk_q=128, blk_k=128, stream=None, keep=None):
+              blk_q=128, blk_k=128, kv_page_table=None, kv_len=0, stream=None, keep=None):
     """Fill an fl_attn_args.  ``keep`` collects temporaries that must outlive the call."""
     keep = [] if keep is None else keep
     dev = q.device
@@ -91,10 +91,35 @@ def make_args(q, k, v, o, lse=None, *, scale=0.0, mod="none", softcap=0.0, alibi
             keep.append(t)
             setattr(var, name, tensor(t))
     var.blk_q, var.blk_k = int(blk_q), int(blk_k)
+    if kv_page_table is not None:          # paged KV: k / v are page pools [n_pages, H, 128, D]
+        t = (kv_page_table if torch.is_tensor(kv_page_table) else torch.as_tensor(kv_page_table))
+        t = t.to(device=dev, dtype=torch.int32).contiguous()
+        keep.append(t)
+        var.kv_page_table = tensor(t)
+        var.kv_len = int(kv_len)
     if stream is None and q.is_cuda:
         stream = torch.cuda.current_stream(q.device)
     a.stream = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
     return a
+
+
+def paged_kv(k: torch.Tensor, v: torch.Tensor, n_pages_total=None, seed=0):
+    """Scatter contiguous K/V [B, H, S_k, D] into page pools [n_pages, H, 128, D] in a shuffled page
+    order; returns (k_pool, v_pool, page_table i32 [B, ceil(S_k / 128)]).  A test / serving helper
+    (data movement only)."""
+    B, H, S, D = k.shape
+    npb = (S + 127) // 128
+    n_pages = n_pages_total or B * npb
+    g = torch.Generator().manual_seed(seed)
+    perm = torch.randperm(n_pages, generator=g)[:B * npb].view(B, npb)
+    kp = torch.zeros(n_pages, H, 128, D, dtype=k.dtype, device=k.device)
+    vp = torch.zeros(n_pages, H, 128, v.shape[-1], dtype=v.dtype, device=v.device)
+    for b in range(B):
+        for t in range(npb):
+            n = min(128, S - 128 * t)
+            kp[perm[b, t], :, :n] = k[b, :, 128 * t:128 * t + n]
+            vp[perm[b, t], :, :n] = v[b, :, 128 * t:128 * t + n]
+    return kp, vp, perm.to(torch.int32)
 
 
 def out_shape(q, v, diff):
@@ -127,7 +152,18 @@ def attn_fwd(q, k, v, *, out=None, return_lse=False, lse=None, workspace=None, *
         a.workspace = workspace.data_ptr()
         a.workspace_bytes = need.value
     _lib.check(_lib.lib().fl_attn_fwd(C.byref(a)))
+    _keep_alive_on(variant.get("stream"), keep)
     return (out, lse) if return_lse else out
+
+
+def _keep_alive_on(stream, tensors):
+    """The kernel may still read temporaries (workspace, slopes, offsets, lists) on a caller-given stream
+    after this call returns: tell the caching allocator they are in use there."""
+    if stream is None or not hasattr(stream, "cuda_stream"):
+        return
+    for t in tensors:
+        if torch.is_tensor(t) and t.is_cuda:
+            t.record_stream(stream)
 
 
 class HostRunner:
@@ -148,6 +184,7 @@ class HostRunner:
         if self.scratch is None or self.scratch.numel() < need.value:
             self.scratch = torch.empty(max(need.value, 1), dtype=torch.uint8, device=self.device)
         _lib.check(_lib.lib().fl_attn_fwd_host(C.byref(a), self.scratch.data_ptr(), self.scratch.numel()))
+        _keep_alive_on(stream, keep)
         return out
 
 

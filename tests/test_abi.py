@@ -35,7 +35,8 @@ def test_exports_every_declared_symbol(L):
 
 
 def test_abi_version_and_status_strings(L):
-    assert L.fl_abi_version() == 1
+    from paper_2511_02043_b200 import _lib
+    assert L.fl_abi_version() == _lib.ABI_VERSION == 2
     assert L.fl_status_string(0) == b"FL_OK"
     assert L.fl_status_string(2) == b"FL_ERR_UNSUPPORTED"
 
@@ -46,7 +47,7 @@ def test_validation_before_any_cuda_call(L):
     a = _lib.AttnArgs()
     a.var.abi_version = 99
     assert L.fl_attn_fwd(C.byref(a)) == 7          # FL_ERR_ABI_VERSION
-    a.var.abi_version = 1
+    a.var.abi_version = _lib.ABI_VERSION
     assert L.fl_attn_fwd(C.byref(a)) == 1          # q/k/v/o missing
     assert b"required" in L.fl_last_error()
 

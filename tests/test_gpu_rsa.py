@@ -134,7 +134,7 @@ SEL_CASES = [
     dict(name="topk0", B=1, Hq=1, Hkv=1, Sq=1024, Sk=1024, D=128, topk=0),
     # diagonal c = 129 (and 257 at D = 64): candidate c-1 opens a new 128-block accumulator tile; the
     # planted key block (= the query block's own rows) has the top score, so dropping it fails
-    dict(name="c129_plant", B=1, Hq=1, Hkv=1, Sq=16640, Sk=16640, D=128, topk=16, plant=[(129, 128), (200, 199)]),
+    dict(name="c129_plant", B=1, Hq=1, Hkv=1, Sq=16640, Sk=16640, D=128, topk=16, plant=[(129, 128), (101, 100)]),
     dict(name="c257_plant_D64", B=1, Hq=1, Hkv=1, Sq=33024, Sk=33024, D=64, topk=16,
          plant=[(129, 128), (257, 256)]),
 ]

@@ -39,7 +39,7 @@ SCHED_CASES = [
 ]
 
 
-def _check(rec, keep_of, B, G, H, Sq, Sk, pair=False):
+def _check(rec, keep_of, B, G, H, Sq, Sk, maps=1):
     mt = rec.shape[1] - 8
     seen = np.zeros((B, G, H, Sq), dtype=np.int32)
     waste = 0
@@ -66,7 +66,8 @@ def _check(rec, keep_of, B, G, H, Sq, Sk, pair=False):
                 if not (codes[j] >> w) & 1:            # mask-free for warp w: every key of its rows kept
                     sub = kt[w * 32:(w + 1) * 32]
                     assert sub.shape[1] == 128 and sub.all(), f"unit {u} wg {wg} tile {j} warp {w} skips a needed mask"
-    assert (seen == 1).all(), "unit decomposition does not cover every row exactly once"
+    # differential attention: warpgroup i computes map i of the same rows (G8) -> every row twice
+    assert (seen == maps).all(), "unit decomposition does not cover every row exactly once per map"
     return waste
 
 
@@ -82,7 +83,7 @@ def test_schedule_dump_matches_keep_predicate(fl, case):
     def keep_of(b, g, h, rows):
         ids = ((b * 1 + g) * Hq + h) * Sq + rows
         return oracle.keep_rows(ins["q"], ins["k"], ins["v"], ids, **ok).astype(bool)
-    waste = _check(rec, keep_of, B, 1, Hq, Sq, Sk)
+    waste = _check(rec, keep_of, B, 1, Hq, Sq, Sk, maps=2 if case.get("diff") else 1)
     assert waste == 0, f"{waste} run tiles hold no kept key"
 
 
