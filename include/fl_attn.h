@@ -112,6 +112,17 @@ typedef struct {
    * bf16 only, rank-4 q only (G = 1); every mask incl. block lists, and the split-KV decode path. */
   fl_tensor kv_page_table;
   int32_t kv_len;
+  /* DIFF-Transformer epilogue (reading G8b, external: Ye et al. 2024), diff only:
+   *   lambda_qk (optional f32 [4, D_qk] = lambda_q1, lambda_k1, lambda_q2, lambda_k2): the re-parameterised
+   *     lambda = exp(lambda_q1 . lambda_k1) - exp(lambda_q2 . lambda_k2) + lambda_init, overriding
+   *     lambda / lambda_h;
+   *   diff_norm = 1: O <- (1 - lambda_init) * RMSNorm(A_0 - lambda A_1) per output row and head, over D_v,
+   *     RMSNorm(x) = x / sqrt(mean_d x_d^2 + diff_norm_eps) * w, w = diff_norm_w f32 [D_v] (absent: ones). */
+  fl_tensor lambda_qk;
+  float lambda_init;
+  int32_t diff_norm;
+  float diff_norm_eps;
+  fl_tensor diff_norm_w;
 } fl_variant;
 
 typedef struct {
@@ -230,6 +241,8 @@ fl_status fl_debug_timing(uint64_t* out48, int32_t reset);
 const char* fl_status_string(fl_status s);
 const char* fl_last_error(void);   /* thread-local detail of the last non-OK status */
 int32_t fl_abi_version(void);
+/* sizeof(fl_attn_args) of this build: bindings compare it with their own mirror at load time. */
+size_t fl_attn_args_size(void);
 /* Number of kernel launches enqueued by the calling thread since the last reset. */
 int64_t fl_launch_count(int32_t reset);
 

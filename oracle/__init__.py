@@ -55,6 +55,8 @@ class _Problem(C.Structure):
         ("diff", C.c_int32), ("lambda_", C.c_double), ("lambda_h", C.POINTER(C.c_double)),
         ("blk_idx", C.POINTER(C.c_int32)), ("blk_cnt", C.POINTER(C.c_int32)),
         ("blk_q", C.c_int32), ("blk_k", C.c_int32), ("max_sel", C.c_int32),
+        ("lambda_qk", C.POINTER(C.c_double)), ("lambda_init", C.c_double), ("diff_norm", C.c_int32),
+        ("diff_norm_eps", C.c_double), ("diff_norm_w", C.POINTER(C.c_double)),
     ]
 
 
@@ -132,7 +134,8 @@ def attn(q, k, v, *, scale=0.0, mod="none", softcap=0.0, alibi_slopes=None,
          mask="none", window=0, prefix=0, doc_offsets=None, doc_causal=False,
          causal_align=0, bias=None, key_mask=None, gate_mode="none", gate=None,
          diff=False, lam=0.0, lambda_h=None, blk_idx=None, blk_cnt=None,
-         blk_q=128, blk_k=128, rows=None):
+         blk_q=128, blk_k=128, lambda_qk=None, lambda_init=0.0, diff_norm=False, diff_norm_eps=1e-5,
+         diff_norm_w=None, rows=None):
     """Evaluate the plain definition on CPU in fp64.
 
     q/k/v/bias/gate: torch CPU tensors [B,H,S,D] or [B,G,H,S,D] (any strides,
@@ -145,7 +148,9 @@ def attn(q, k, v, *, scale=0.0, mod="none", softcap=0.0, alibi_slopes=None,
     p = _problem(q, k, v, keep, scale=scale, mod=mod, softcap=softcap, alibi_slopes=alibi_slopes, mask=mask,
                  window=window, prefix=prefix, doc_offsets=doc_offsets, doc_causal=doc_causal,
                  causal_align=causal_align, bias=bias, key_mask=key_mask, gate_mode=gate_mode, gate=gate, diff=diff,
-                 lam=lam, lambda_h=lambda_h, blk_idx=blk_idx, blk_cnt=blk_cnt, blk_q=blk_q, blk_k=blk_k)
+                 lam=lam, lambda_h=lambda_h, blk_idx=blk_idx, blk_cnt=blk_cnt, blk_q=blk_q, blk_k=blk_k,
+                 lambda_qk=lambda_qk, lambda_init=lambda_init, diff_norm=diff_norm, diff_norm_eps=diff_norm_eps,
+                 diff_norm_w=diff_norm_w)
     maps = 2 if diff else 1
     qs = p.q.size
     total = qs[0] * qs[1] * (qs[2] // maps) * qs[3]
@@ -189,7 +194,8 @@ def _problem(q, k, v, keep, *, scale=0.0, mod="none", softcap=0.0, alibi_slopes=
              mask="none", window=0, prefix=0, doc_offsets=None, doc_causal=False,
              causal_align=0, bias=None, key_mask=None, gate_mode="none", gate=None,
              diff=False, lam=0.0, lambda_h=None, blk_idx=None, blk_cnt=None,
-             blk_q=128, blk_k=128):
+             blk_q=128, blk_k=128, lambda_qk=None, lambda_init=0.0, diff_norm=False, diff_norm_eps=1e-5,
+             diff_norm_w=None):
     p = _Problem()
     p.q, p.k, p.v = _tensor(q, keep), _tensor(k, keep), _tensor(v, keep)
     p.scale = float(scale)
@@ -233,6 +239,11 @@ def _problem(q, k, v, keep, *, scale=0.0, mod="none", softcap=0.0, alibi_slopes=
         p.blk_cnt = bc.ctypes.data_as(C.POINTER(C.c_int32))
         p.max_sel = bi.shape[-1]
     p.blk_q, p.blk_k = int(blk_q), int(blk_k)
+    p.lambda_qk = _dptr(None if lambda_qk is None else np.asarray(lambda_qk, dtype=np.float64).reshape(-1), keep)
+    p.lambda_init = float(lambda_init)
+    p.diff_norm = int(bool(diff_norm))
+    p.diff_norm_eps = float(diff_norm_eps)
+    p.diff_norm_w = _dptr(diff_norm_w, keep)
     return p
 
 

@@ -14,6 +14,7 @@
  *     m    = max_k s_k ;  d = sum_k e^{s_k - m}    Alg.1 P:L146-160 (two serial loops)
  *     O_q  = sum_k (e^{s_k - m} / d) V_k           Eq.2  P:L134-141, Listing 1
  *     diff:  O = A_0 - lambda * A_1                Listing 4
+ *            [ (1 - lambda_init) RMSNorm(O), lambda re-parameterised ]   reading G8b (NEXT-2)
  *     gate:  O = O * sigmoid(G) | O * G            Evoformer P:L865 (reading G9)
  * with every intermediate in fp64, one row at a time, no blocking, no online
  * rescaling, no reordering beyond the definition.  OpenMP splits rows only.
@@ -133,6 +134,14 @@ static void one_row(const flo_problem* p, int64_t maps, int64_t b, int64_t g, in
   const int64_t q_abs = p->causal_align ? q : q + (Sk - Sq);                /* G12 */
   const int64_t bgh = (b * G + g) * Hq + h;
   double lam = p->lambda_h ? p->lambda_h[h] : p->lambda;
+  if (maps == 2 && p->lambda_qk) {               /* lambda re-parameterisation (G8b) */
+    double d1 = 0.0, d2 = 0.0;
+    for (int64_t d = 0; d < Dqk; ++d) {
+      d1 += p->lambda_qk[d] * p->lambda_qk[Dqk + d];
+      d2 += p->lambda_qk[2 * Dqk + d] * p->lambda_qk[3 * Dqk + d];
+    }
+    lam = exp(d1) - exp(d2) + p->lambda_init;
+  }
 
   for (int64_t d = 0; d < Dv; ++d) out[d] = 0.0;
   double lse = NAN;
@@ -175,6 +184,13 @@ static void one_row(const flo_problem* p, int64_t maps, int64_t b, int64_t g, in
     double coef = map == 0 ? 1.0 : -lam;
     for (int64_t d = 0; d < Dv; ++d) out[d] += coef * acc[d];
     if (maps == 1) lse = m + log(dsum);
+  }
+  if (maps == 2 && p->diff_norm) {               /* per-head RMSNorm of the diff output (G8b) */
+    double ms = 0.0;
+    for (int64_t d = 0; d < Dv; ++d) ms += out[d] * out[d];
+    ms /= (double)Dv;
+    const double k = (1.0 - p->lambda_init) / sqrt(ms + p->diff_norm_eps);
+    for (int64_t d = 0; d < Dv; ++d) out[d] *= k * (p->diff_norm_w ? p->diff_norm_w[d] : 1.0);
   }
   if (p->gate_mode != FLO_GATE_NONE) {
     for (int64_t d = 0; d < Dv; ++d) {

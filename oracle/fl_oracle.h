@@ -61,6 +61,12 @@ typedef struct {
   const int32_t* blk_idx;       /* [B*G*Hq][n_qblk][max_sel]   (G10) */
   const int32_t* blk_cnt;       /* [B*G*Hq][n_qblk] */
   int32_t blk_q, blk_k, max_sel;
+  /* DIFF-Transformer epilogue (reading G8b, external Ye et al. 2024) */
+  const double* lambda_qk;      /* [4][Dqk]: lambda = exp(q1.k1) - exp(q2.k2) + lambda_init, or NULL */
+  double lambda_init;
+  int32_t diff_norm;            /* 1: O <- (1 - lambda_init) * w * O / sqrt(mean_d O_d^2 + eps) */
+  double diff_norm_eps;
+  const double* diff_norm_w;    /* [Dv] or NULL (ones) */
 } flo_problem;
 
 /* Output rows.  rows[i] = ((b*G + g)*Hq + h)*Sq + q; rows == NULL means all

@@ -16,7 +16,7 @@ ABI_VERSION = 2
 
 EXPORTS = ["fl_attn_fwd", "fl_attn_workspace_size", "fl_attn_host_scratch_size", "fl_attn_fwd_host",
            "fl_rsa_build_summaries", "fl_rsa_update_summaries", "fl_rsa_select", "fl_shard_range", "fl_diag_umma_gemm",
-           "fl_diag_pipe_rate", "fl_debug_schedule", "fl_status_string", "fl_last_error", "fl_abi_version", "fl_launch_count", "fl_debug_timing"]
+           "fl_diag_pipe_rate", "fl_debug_schedule", "fl_attn_args_size", "fl_status_string", "fl_last_error", "fl_abi_version", "fl_launch_count", "fl_debug_timing"]
 
 
 class Tensor(C.Structure):
@@ -33,6 +33,8 @@ class Variant(C.Structure):
         ("diff", C.c_int32), ("lambda_", C.c_float), ("lambda_h", Tensor),
         ("blk_idx", Tensor), ("blk_cnt", Tensor), ("blk_q", C.c_int32), ("blk_k", C.c_int32),
         ("kv_page_table", Tensor), ("kv_len", C.c_int32),
+        ("lambda_qk", Tensor), ("lambda_init", C.c_float), ("diff_norm", C.c_int32), ("diff_norm_eps", C.c_float),
+        ("diff_norm_w", Tensor),
     ]
 
 
@@ -94,6 +96,10 @@ def lib():
             getattr(L, name).restype = C.c_int
         if L.fl_abi_version() != ABI_VERSION:
             raise RuntimeError("libfl_attn.so ABI version mismatch")
+        L.fl_attn_args_size.restype = C.c_size_t
+        if L.fl_attn_args_size() != C.sizeof(AttnArgs):
+            raise RuntimeError(f"libfl_attn.so was built for a different fl_attn_args layout "
+                               f"({L.fl_attn_args_size()} vs {C.sizeof(AttnArgs)} bytes): rebuild it")
         _lib = L
     return _lib
 

@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(SIMT_THREADS) attn_simt_kernel(const __grid_co
 
   float slope = 0.f;
   if (p.mod == MOD_ALIBI) slope = p.alibi ? p.alibi[h] : exp2f(-8.f * (float)(h + 1) / (float)p.Hq);
-  const float lam = p.lambda_h ? p.lambda_h[h] : p.lambda;
+  const float lam = p.maps == 2 ? diff_lambda(p, h) : 0.f;
 
   float res[4][4];                             // final output accumulators (rows x d-chunks)
 #pragma unroll
@@ -174,6 +174,19 @@ __global__ void __launch_bounds__(SIMT_THREADS) attn_simt_kernel(const __grid_co
     }
   }
 
+  // DIFF-Transformer epilogue (NEXT-2): per-head RMSNorm of A_0 - lambda A_1 over D_v, times (1 - lambda_init)
+  float norm_k[4] = {1.f, 1.f, 1.f, 1.f};
+  if (p.maps == 2 && p.diff_norm) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      float ss = 0.f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (lane + 32 * c < Dv) ss = fmaf(res[r][c], res[r][c], ss);
+      ss = warp_sum(ss);
+      norm_k[r] = (1.f - p.lambda_init) / sqrtf(ss / (float)Dv + p.diff_norm_eps);
+    }
+  }
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const int q = q_first + warp * 4 + r;
@@ -183,6 +196,7 @@ __global__ void __launch_bounds__(SIMT_THREADS) attn_simt_kernel(const __grid_co
       const int d = lane + 32 * c;
       if (d >= Dv) continue;
       float o = res[r][c];
+      if (p.maps == 2 && p.diff_norm) o *= norm_k[r] * (p.diff_norm_w ? p.diff_norm_w[d] : 1.f);
       if (p.gate_mode != GATE_NONE) {
         float gv = ld_in(p.gate, b * p.gs.b + g * p.gs.g + h * p.gs.h + (int64_t)q * p.gs.s + d, p.gate_dtype);
         o *= p.gate_mode == GATE_SIGMOID ? 1.f / (1.f + expf(-gv)) : gv;

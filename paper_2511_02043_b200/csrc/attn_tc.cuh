@@ -132,6 +132,21 @@ struct TcCfg {
   static constexpr int ENTRIES_PER_TILE = DIFF ? 3 : 2;              // K0 [K1] V
 };
 
+// Softcap (no bias): tanh is monotone, so the row max of cap*tanh(a s) is cap*tanh(a max s) -- the max is
+// taken on the raw scores (one tanh per row), and the per-score tanh moves off the critical max -> exp
+// chain into the exp loop.  There it runs on the FMA pipe (kSoftcapPoly): tanh(a s) = a s P((a s)^2), P the
+// odd minimax fit of degree 9 on |a s| <= 1.5 (|error| < 8.2e-5 in fp32, below tanh.approx.f32's 2^-11
+// relative error), prescaled by a = scale / cap per call, whenever every |a s| of a warp's tile is <= 1.5
+// (one warp vote on the raw max / min; with |Q|, |K| <= 1 and cap = 20 that is every tile at D <= 512),
+// else on the MUFU.  The MUFU then carries one op per score (ex2) instead of two.
+#ifndef FL_SOFTCAP_MUFU
+constexpr bool kSoftcapPoly = true;
+#else
+constexpr bool kSoftcapPoly = false;
+#endif
+constexpr float kTanhX0 = 1.5f;
+constexpr float kTanhC0 = 0.9993646741f, kTanhC1 = -0.3268460035f, kTanhC2 = 0.1141102985f,
+                kTanhC3 = -0.02846436948f, kTanhC4 = 0.003358259564f;
 // Which groups of 4 scores (index (c/4) % 8) take the FMA-pipe exp2 (ex2_emu2) instead of
 // the MUFU.  On paper a 3/8 fraction balances the pipes (MUFU 1/16 clk/SM per score vs FMA
 // ~(2 + 6 f)/128), but measured on B200 (profiles/r01_ab_*.txt) the softmax warpgroups are
@@ -144,9 +159,10 @@ struct EmuCfg {
 #else
   // measured (profiles/r01_ab_pingpong_emu.txt): softcap (tanh + ex2 on the MUFU) +2 % with 3/8,
   // D = 64 (diff, 2x MUFU per flop) +1.6 % with 2/8, D = 128 plain exp: no gain -> all MUFU
-  static constexpr uint32_t MASK = MOD == MOD_SOFTCAP ? 0x4Au : (D <= 64 ? 0x11u : 0u);
+  static constexpr uint32_t MASK = MOD == MOD_SOFTCAP ? (kSoftcapPoly ? 0u : 0x4Au) : (D <= 64 ? 0x11u : 0u);
 #endif
 };
+
 // Ping-pong of the two softmax warpgroups' exp loops on named barriers (FA3-style).  Measured
 // slower with the persistent kernel (causal 982 vs 1071 TF/s, diff 624 vs 681): the alternation
 // serialises the exp loops while neither the MUFU nor the issue slots are saturated.  Opt-in.
@@ -608,6 +624,18 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     const float sc_l2 = p.scale * kLog2e;
     const float cap_in = MOD == MOD_SOFTCAP ? p.scale / p.softcap : 0.f;   // s*scale/cap
     const float cap_out = MOD == MOD_SOFTCAP ? p.softcap * kLog2e : 0.f;
+    // softcap tanh polynomial prescaled by a = cap_in: tanh(a s) = s * sum_i (kTanhC_i a^(2i+1)) (s^2)^i
+    constexpr bool kCapFirst = MOD == MOD_SOFTCAP && !BIAS;   // max on raw scores, tanh in the exp loop
+    float tc0 = 0.f, tc1 = 0.f, tc2 = 0.f, tc3 = 0.f, tc4 = 0.f;
+    if (kCapFirst && kSoftcapPoly) {
+      const float a2 = cap_in * cap_in;
+      tc0 = kTanhC0 * cap_in;
+      tc1 = kTanhC1 * cap_in * a2;
+      tc2 = kTanhC2 * cap_in * a2 * a2;
+      tc3 = kTanhC3 * cap_in * a2 * a2 * a2;
+      tc4 = kTanhC4 * cap_in * a2 * a2 * a2 * a2;
+    }
+    const float s_poly_max = MOD == MOD_SOFTCAP ? kTanhX0 / cap_in : 0.f;   // |s| bound of the polynomial
     int s_cnt = 0, o_cnt = 0;                        // cumulative s_full / o_full phases of this WG
     int b_cnt = 0;                                   // bias tiles consumed (TMA path)
     bool pp_started = false;                         // ping-pong: first common tile of the CTA's life seen
@@ -678,11 +706,21 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       const float bias_k = kRaw ? 1.f / p.scale : kLog2e;
       const float delta = MOD == MOD_ALIBI ? slope_l2 * (float)(k0 - q_abs) : 0.f;
       const float slope_r = MOD == MOD_ALIBI ? slope_l2 / sc_l2 : 0.f;
+      bool poly = false;                               // kCapFirst: this warp's tile takes the FMA-pipe tanh
+      if (kCapFirst && kSoftcapPoly) {
+        float am0 = 0.f, am1 = 0.f;
+#pragma unroll
+        for (int c = 0; c < 128; c += 4) {
+          am0 = fmax3(am0, fabsf(__uint_as_float(s[c])), fabsf(__uint_as_float(s[c + 1])));
+          am1 = fmax3(am1, fabsf(__uint_as_float(s[c + 2])), fabsf(__uint_as_float(s[c + 3])));
+        }
+        poly = __all_sync(0xffffffffu, fmaxf(am0, am1) <= s_poly_max);
+      }
 #pragma unroll
       for (int c = 0; c < 128; ++c) {
         float v = __uint_as_float(s[c]);
-        if (MOD == MOD_SOFTCAP && !BIAS) {
-          v = tanh_approx(v * cap_in);
+        if (kCapFirst) {
+          // raw score: tanh after the row max (exp loop)
         } else if (MOD == MOD_ALIBI) {
           v = fmaf(slope_r, (float)c, v);
         } else if (!kRaw) {
@@ -798,7 +836,13 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         mt3 = fmax3(mt3, x[c + 6], x[c + 7]);
       }
       const float xscale = kRaw ? sc_l2 : (MOD == MOD_SOFTCAP && !BIAS ? cap_out : 1.f);
-      const float mt = fmaf(fmaxf(fmaxf(mt0, mt1), fmaxf(mt2, mt3)), xscale, delta);   // -inf stays -inf
+      float mt;
+      if (kCapFirst) {                                 // max of cap tanh(a s) = cap tanh(a max s): one tanh per row
+        const float smax = fmaxf(fmaxf(mt0, mt1), fmaxf(mt2, mt3));
+        mt = smax == -INFINITY ? -INFINITY : cap_out * tanh_approx(smax * cap_in);
+      } else {
+        mt = fmaf(fmaxf(fmaxf(mt0, mt1), fmaxf(mt2, mt3)), xscale, delta);   // -inf stays -inf
+      }
       FL_T(3);                                         // 3: score mod + mask + row max
       const bool rescale = mt > m_ref + kTau;          // also true for the first finite tile (m_ref = -inf)
       const float factor = rescale ? ex2(m_ref - mt) : 1.f;
@@ -833,6 +877,23 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         pp_started = true;
       }
       FL_T(5);                                         // 5: ping-pong wait
+      if (kCapFirst) {                                 // x = tanh(a s); masked (-inf) scores stay -inf
+        if (poly) {
+#pragma unroll
+          for (int c = 0; c < 128; c += 2) {           // -inf: u = +inf, P = +inf (tc4 > 0), x = -inf
+            float u0, u1, p0, p1;
+            fmul2(u0, u1, x[c], x[c + 1], x[c], x[c + 1]);
+            ffma2(p0, p1, u0, u1, tc4, tc4, tc3, tc3);
+            ffma2(p0, p1, p0, p1, u0, u1, tc2, tc2);
+            ffma2(p0, p1, p0, p1, u0, u1, tc1, tc1);
+            ffma2(p0, p1, p0, p1, u0, u1, tc0, tc0);
+            fmul2(x[c], x[c + 1], p0, p1, x[c], x[c + 1]);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 128; ++c) x[c] = x[c] == -INFINITY ? -INFINITY : tanh_approx(x[c] * cap_in);
+        }
+      }
       float ls0 = 0.f, ls1 = 0.f, ls2 = 0.f, ls3 = 0.f;
       uint32_t pk[64];
 #pragma unroll
@@ -918,7 +979,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       m_ref = mm;
       l = lt;
     }
-    const float lam = DIFF ? (p.lambda_h ? p.lambda_h[w.h] : p.lambda) : 0.f;
+    const float lam = DIFF ? diff_lambda(p, w.h) : 0.f;
     float* xbuf = reinterpret_cast<float*>(sQ);      // diff: map-1 rows handed to WG0 (Q is dead now)
     if (DIFF && wg == 1) {
       if (n_done == 0) mbar_wait(q_full, it & 1);    // never overwrite Q while its TMA may be in flight
@@ -944,8 +1005,44 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     } else {
       if (DIFF) named_bar_sync(1, 256);
       const int64_t obase = w.b * p.os.b + gw * p.os.g + (int64_t)w.h * p.os.h + (int64_t)q * p.os.s;
+      // DIFF-Transformer epilogue (NEXT-2): the row's A_0 - lambda A_1 in registers, then per-head RMSNorm
+      // over D_v and the (1 - lambda_init) scale before the store
+      float norm_k = 1.f;
+      float drow[DIFF ? D : 1];
+      if (DIFF && p.diff_norm) {
+        float ss0 = 0.f, ss1 = 0.f;
+#pragma unroll
+        for (int c = 0; c < D; c += 32) {
+          uint32_t o[32];
+          if (n_done > 0) {
+            tmem_ld32(tmem + lane_base + col_o + c, o);
+            tmem_wait_ld();
+          } else {
+#pragma unroll
+            for (int t = 0; t < 32; ++t) o[t] = 0u;
+          }
+#pragma unroll
+          for (int t4 = 0; t4 < 8; ++t4) {
+            const float4 v = reinterpret_cast<const float4*>(xbuf + r * D)[((c >> 2) + t4) ^ (r & 7)];
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float f = fmaf(-lam, vv[e], __uint_as_float(o[4 * t4 + e]) * inv_l);
+              drow[c + 4 * t4 + e] = f;
+              if (e & 1) ss1 = fmaf(f, f, ss1); else ss0 = fmaf(f, f, ss0);
+            }
+          }
+        }
+        norm_k = rsqrtf((ss0 + ss1) / (float)D + p.diff_norm_eps) * (1.f - p.lambda_init);
+      }
 #pragma unroll
       for (int c = 0; c < D; c += 32) {
+        float f[32];
+        if (DIFF && p.diff_norm) {
+#pragma unroll
+          for (int t = 0; t < 32; ++t)
+            f[t] = drow[c + t] * norm_k * (p.diff_norm_w ? __ldg(p.diff_norm_w + c + t) : 1.f);
+        } else {
         uint32_t o[32];
         if (n_done > 0) {
           tmem_ld32(tmem + lane_base + col_o + c, o);
@@ -954,7 +1051,6 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 #pragma unroll
           for (int t = 0; t < 32; ++t) o[t] = 0u;
         }
-        float f[32];
 #pragma unroll
         for (int t = 0; t < 32; ++t) f[t] = __uint_as_float(o[t]) * inv_l;
         if (LIST && w.hi[1] > 0) {                     // WG1's partial, read from its TMEM columns (same lanes)
@@ -972,6 +1068,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             f[4 * t4 + 2] -= lam * v.z;
             f[4 * t4 + 3] -= lam * v.w;
           }
+        }
         }
         if (gated) {
           uint4 g4[4];

@@ -77,6 +77,7 @@ fl_status fail(fl_status s, const char* fmt, ...) {
 }
 
 fl_status cuda_fail(cudaError_t e, const char* what) {
+  cudaGetLastError();                     // a failed launch / attribute call must not leak into the next call
   return fail(FL_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
 }
 
@@ -301,6 +302,14 @@ fl_status prepare(const fl_attn_args* a, Prepared& P, bool device_ptrs) {
   if (var.mod == FL_MOD_SOFTCAP && !(var.softcap > 0.f)) return fail(FL_ERR_INVALID_ARGUMENT, "softcap must be > 0");
   if (var.mod == FL_MOD_ALIBI && check_vec(var.alibi_slopes, FL_F32, Hq, "alibi_slopes")) return FL_ERR_INVALID_ARGUMENT;
   if (var.diff && check_vec(var.lambda_h, FL_F32, Hq, "lambda_h")) return FL_ERR_INVALID_ARGUMENT;
+  if ((var.lambda_qk.data || var.diff_norm) && !var.diff)
+    return fail(FL_ERR_INVALID_ARGUMENT, "lambda_qk / diff_norm need diff (differential attention)");
+  if (var.lambda_qk.data && check_vec(var.lambda_qk, FL_F32, 4 * P.q.size[4], "lambda_qk [4, D_qk]"))
+    return FL_ERR_INVALID_ARGUMENT;
+  if (var.diff_norm && (var.diff_norm != 1 || !(var.diff_norm_eps > 0.f)))
+    return fail(FL_ERR_INVALID_ARGUMENT, "diff_norm is 0 or 1, with diff_norm_eps > 0");
+  if (var.diff_norm && var.diff_norm_w.data && check_vec(var.diff_norm_w, FL_F32, P.v.size[4], "diff_norm_w [D_v]"))
+    return FL_ERR_INVALID_ARGUMENT;
   if (var.causal_align != 0 && var.causal_align != 1) return fail(FL_ERR_INVALID_ARGUMENT, "causal_align is 0 or 1");
   if (var.mask == FL_MASK_SLIDING && var.window < 0) return fail(FL_ERR_INVALID_ARGUMENT, "window must be >= 0");
   if (var.mask == FL_MASK_PREFIX && var.prefix_len < 0) return fail(FL_ERR_INVALID_ARGUMENT, "prefix_len >= 0");
@@ -391,7 +400,8 @@ fl_status prepare(const fl_attn_args* a, Prepared& P, bool device_ptrs) {
   if (device_ptrs) {
     const void* ptrs[] = {a->q.data, a->k.data, a->v.data, a->o.data, a->lse.data, var.bias.data, var.key_mask.data,
                           var.gate.data, var.alibi_slopes.data, var.lambda_h.data, var.doc_offsets.data,
-                          var.blk_idx.data, var.blk_cnt.data, var.kv_page_table.data};
+                          var.blk_idx.data, var.blk_cnt.data, var.kv_page_table.data, var.lambda_qk.data,
+                          var.diff_norm_w.data};
     for (const void* p : ptrs)
       if (!on_device(p)) return fail(FL_ERR_INVALID_ARGUMENT, "a tensor pointer is not device memory on this device");
   }
@@ -421,6 +431,9 @@ fl_status prepare(const fl_attn_args* a, Prepared& P, bool device_ptrs) {
   p.gate_mode = var.gate_mode; p.gate = P.gate.data; p.gs = strides_of(P.gate);
   p.gate_dtype = P.gate.present ? (P.gate.dtype == FL_F32 ? 1 : 0) : 0;
   p.lambda = var.lambda; p.lambda_h = static_cast<const float*>(var.lambda_h.data);
+  p.lambda_qk = static_cast<const float*>(var.lambda_qk.data); p.lambda_init = var.lambda_init;
+  p.diff_norm = var.diff_norm; p.diff_norm_eps = var.diff_norm_eps;
+  p.diff_norm_w = static_cast<const float*>(var.diff_norm_w.data);
   p.blk_idx = static_cast<const int32_t*>(var.blk_idx.data); p.blk_cnt = static_cast<const int32_t*>(var.blk_cnt.data);
   p.blk_q = var.blk_q; p.blk_k = var.blk_k;
   p.max_sel = var.mask == FL_MASK_BLOCKLIST ? (int)var.blk_idx.size[2] : 0;
@@ -524,7 +537,7 @@ struct HostPlan {
     size_t off;
     bool out;
   };
-  Item items[16];
+  Item items[20];
   int n = 0;
   size_t total = 0;
   size_t ws_off = 0, ws_bytes = 0;
@@ -547,7 +560,8 @@ bool is_contiguous(const fl_tensor& t) {
 
 fl_status plan_host(fl_attn_args& d, HostPlan& hp) {
   fl_tensor* ins[] = {&d.q, &d.k, &d.v, &d.var.bias, &d.var.key_mask, &d.var.gate, &d.var.alibi_slopes,
-                      &d.var.lambda_h, &d.var.doc_offsets, &d.var.blk_idx, &d.var.blk_cnt, &d.var.kv_page_table};
+                      &d.var.lambda_h, &d.var.doc_offsets, &d.var.blk_idx, &d.var.blk_cnt, &d.var.kv_page_table,
+                      &d.var.lambda_qk, &d.var.diff_norm_w};
   for (fl_tensor* t : ins) {
     if (!t->data) continue;
     if (!is_contiguous(*t)) return fail(FL_ERR_UNSUPPORTED, "fl_attn_fwd_host: host tensors must be contiguous");
@@ -806,6 +820,8 @@ const char* fl_status_string(fl_status s) {
   }
   return "FL_ERR_UNKNOWN";
 }
+
+size_t fl_attn_args_size(void) { return sizeof(fl_attn_args); }
 
 fl_status fl_debug_timing(uint64_t* out48, int32_t reset) {
   if (!out48) return fail(FL_ERR_INVALID_ARGUMENT, "out48 is NULL");

@@ -41,6 +41,8 @@ struct AttnParams {
   // ---- gate / diff
   int32_t gate_mode; const void* gate; Strided5 gs; int32_t gate_dtype;
   float lambda; const float* lambda_h;
+  // DIFF-Transformer epilogue (NEXT-2): lambda re-parameterisation [4][Dqk] and per-head RMSNorm
+  const float* lambda_qk; float lambda_init; int32_t diff_norm; float diff_norm_eps; const float* diff_norm_w;
   // ---- block list (RSA)
   const int32_t* blk_idx; const int32_t* blk_cnt; int32_t blk_q, blk_k, max_sel, n_qblk;
   // ---- paged KV: logical KV tile t of batch b is page page_table[b * page_stride + t] of the k/v pools
@@ -48,6 +50,22 @@ struct AttnParams {
   int32_t in_dtype;        // 0 bf16, 1 f32
   int32_t* tile_ctr;       // bf16 path: persistent-scheduler ticket counter (workspace, zeroed per call)
 };
+
+// lambda of head h (Listing 4's lambda_full, G8): re-parameterised from lambda_qk when given (NEXT-2:
+// exp(q1 . k1) - exp(q2 . k2) + lambda_init), else the per-head or scalar value.
+#ifdef __CUDACC__
+__device__ inline float diff_lambda(const AttnParams& p, int h) {
+  if (p.lambda_qk) {
+    float d1 = 0.f, d2 = 0.f;
+    for (int d = 0; d < p.Dqk; ++d) {
+      d1 = fmaf(p.lambda_qk[d], p.lambda_qk[p.Dqk + d], d1);
+      d2 = fmaf(p.lambda_qk[2 * p.Dqk + d], p.lambda_qk[3 * p.Dqk + d], d2);
+    }
+    return expf(d1) - expf(d2) + p.lambda_init;
+  }
+  return p.lambda_h ? p.lambda_h[h] : p.lambda;
+}
+#endif
 
 // TMA (row, batch) coordinates of logical KV tile `tile` of batch b: contiguous K/V -> (128 tile, b);
 // paged K/V -> (0, page) with page = page_table[b, tile] (the pool's batch dim indexes pages).

@@ -268,12 +268,15 @@ FL_DEVICE void ex2_emu2(float& a, float& b) {
   b = __int_as_float(__float_as_int(pb) + (__float_as_int(tb) << 23));
 }
 
+// Named barriers are reached from DIFFERENT code paths by the warpgroups that share them (e.g. the
+// two softmax warpgroups' epilogues), so they use the non-.aligned barrier forms: bar.sync / bar.arrive
+// are barrier.*.aligned, which requires every participating thread to execute the same instruction.
 FL_DEVICE void named_bar_arrive(uint32_t id, uint32_t nthreads) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+  asm volatile("barrier.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 FL_DEVICE void named_bar_sync(uint32_t id, uint32_t nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 }  // namespace fl

@@ -105,8 +105,9 @@ cudaError_t launch_rsa_summaries(const void* k, int64_t sb, int64_t sg, int64_t 
 //     do not span items): row max over the block's queries, running max over the heads of a GQA
 //     group, exact radix top-k, ascending list.
 // So the split of item n+1, the MMAs of item n+1 and the selection of item n overlap.
-// Select warpgroups per CTA.  The accumulator is released right after the row max, so the top-k of
-// up to kSelWG items runs concurrently; the radix passes are barrier / latency bound, not ALU bound.
+// Select warpgroups per CTA (up to kSelWG, as many as the shared memory admits): the accumulator is
+// released right after the row max, so the top-k of several items runs concurrently; the radix passes
+// are barrier / latency bound, not ALU bound.
 #ifndef FL_SEL_WG
 #define FL_SEL_WG 4
 #endif
@@ -123,14 +124,14 @@ struct SelCfg {
   // summaries (kmax, kmin) + raw Q + q+ / q- tiles + per-select-warpgroup scratch (256-bin histogram as
   // 16-bit counts, pass state, selection bitmap) + barriers + alignment slack
   static constexpr int SCR_WORDS = 128 + 16 + 16;
-  static constexpr int SCRATCH = kSelWG * SCR_WORDS * 4;
-  static int smem(int n_mt) { return 2 * n_mt * QTILE + 3 * QTILE + SCRATCH + 128 + 1024; }
+  static int scratch(int nsel) { return nsel * SCR_WORDS * 4; }
+  static int smem(int n_mt, int nsel) { return 2 * n_mt * QTILE + 3 * QTILE + scratch(nsel) + 128 + 1024; }
 };
 
 template <int D>
 __global__ void __launch_bounds__(kSelThreads, 1)
     rsa_select_kernel(const __grid_constant__ RsaSelParams p, const __grid_constant__ CUtensorMap tq,
-                      const __grid_constant__ CUtensorMap tmin, const __grid_constant__ CUtensorMap tmax) {
+                      const __grid_constant__ CUtensorMap tmin, const __grid_constant__ CUtensorMap tmax, int n_sel_wg) {
   using C = SelCfg<D>;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned (SW128 atoms); offset arithmetic on smem_raw keeps the shared address space visible
@@ -142,8 +143,8 @@ __global__ void __launch_bounds__(kSelThreads, 1)
   uint8_t* sQraw = sMin + n_mt * C::QTILE;              // TMA destination of the next Q tile
   uint8_t* sQp = sQraw + C::QTILE;
   uint8_t* sQn = sQp + C::QTILE;
-  uint32_t* scratch = reinterpret_cast<uint32_t*>(sQn + C::QTILE);   // [kSelWG][SCR_WORDS], one per select WG
-  uint64_t* bars = reinterpret_cast<uint64_t*>(scratch + kSelWG * C::SCR_WORDS);
+  uint32_t* scratch = reinterpret_cast<uint32_t*>(sQn + C::QTILE);   // [n_sel_wg][SCR_WORDS], one per select WG
+  uint64_t* bars = reinterpret_cast<uint64_t*>(scratch + n_sel_wg * C::SCR_WORDS);
   uint64_t* bar_sum = bars;                             // summaries landed
   uint64_t* bar_q = bars + 1;                           // raw Q tile landed
   uint64_t* bar_qfree = bars + 2;                       // MMAs of the previous item done (q+/q-, summaries free)
@@ -269,7 +270,7 @@ __global__ void __launch_bounds__(kSelThreads, 1)
     // kSelWG select warpgroups (warps 0-3, 8-11, ...) take items round-robin when each item has its own TMEM
     // accumulator buffer and no GQA group spans items; otherwise warps 0-3 take every item.
     const int sel = warp < 4 ? 0 : (warp - 4) / 4;      // warps 0-3, 8-11, 12-15, ...
-    const int nsel = (nbuf == 2 && p.grp == 1) ? kSelWG : 1;
+    const int nsel = (nbuf == 2 && p.grp == 1) ? n_sel_wg : 1;
     const int tt = t & 127, wq = warp & 3;              // thread / warp within the select warpgroup
     uint32_t* hist = scratch + sel * C::SCR_WORDS;      // [128] packed 16-bit bin counts
     uint32_t* rstate = hist + 128;                      // [16] digit / counts of the current pass
@@ -471,16 +472,22 @@ cudaError_t launch_rsa_select(const RsaSelParams& p0, const CUtensorMap& tq, con
   const int grid = (int)std::min<long long>(pairs, sms > 0 ? sms : 148);   // persistent: one CTA per SM
   if (grid <= 0) return cudaSuccess;
   const int n_mt = (p.nkb + 127) / 128;
+  int smem_max = 0;
+  cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  int nsel = kSelWG;
+  auto fits = [&](int ns) { return (p.D == 128 ? SelCfg<128>::smem(n_mt, ns) : SelCfg<64>::smem(n_mt, ns)) <= smem_max; };
+  while (nsel > 1 && !fits(nsel)) --nsel;
+  const int threads = 128 * (nsel + 1);
   if (p.D == 128) {
-    const int sm = SelCfg<128>::smem(n_mt);
+    const int sm = SelCfg<128>::smem(n_mt, nsel);
     cudaError_t e = cudaFuncSetAttribute(rsa_select_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     if (e != cudaSuccess) return e;
-    rsa_select_kernel<128><<<grid, kSelThreads, sm, stream>>>(p, tq, tmin, tmax);
+    rsa_select_kernel<128><<<grid, threads, sm, stream>>>(p, tq, tmin, tmax, nsel);
   } else {
-    const int sm = SelCfg<64>::smem(n_mt);
+    const int sm = SelCfg<64>::smem(n_mt, nsel);
     cudaError_t e = cudaFuncSetAttribute(rsa_select_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     if (e != cudaSuccess) return e;
-    rsa_select_kernel<64><<<grid, kSelThreads, sm, stream>>>(p, tq, tmin, tmax);
+    rsa_select_kernel<64><<<grid, threads, sm, stream>>>(p, tq, tmin, tmax, nsel);
   }
   return cudaGetLastError();
 }

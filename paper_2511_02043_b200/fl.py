@@ -49,7 +49,8 @@ def _f32vec(x, device):
 def make_args(q, k, v, o, lse=None, *, scale=0.0, mod="none", softcap=0.0, alibi_slopes=None, mask="none",
               window=0, prefix=0, doc_offsets=None, doc_causal=False, causal_align=0, bias=None, key_mask=None,
               gate_mode="none", gate=None, diff=False, lam=0.0, lambda_h=None, blk_idx=None, blk_cnt=None,
-              blk_q=128, blk_k=128, kv_page_table=None, kv_len=0, stream=None, keep=None):
+              blk_q=128, blk_k=128, kv_page_table=None, kv_len=0, lambda_qk=None, lambda_init=0.0,
+              diff_norm=False, diff_norm_eps=1e-5, diff_norm_w=None, stream=None, keep=None):
     """Fill an fl_attn_args.  ``keep`` collects temporaries that must outlive the call."""
     keep = [] if keep is None else keep
     dev = q.device
@@ -91,6 +92,16 @@ def make_args(q, k, v, o, lse=None, *, scale=0.0, mod="none", softcap=0.0, alibi
             keep.append(t)
             setattr(var, name, tensor(t))
     var.blk_q, var.blk_k = int(blk_q), int(blk_k)
+    lq = _f32vec(lambda_qk, dev)            # DIFF-Transformer epilogue (NEXT-2): [4, D_qk] flattened
+    lq = lq.reshape(-1) if lq is not None else None
+    keep.append(lq)
+    var.lambda_qk = tensor(lq)
+    var.lambda_init = float(lambda_init)
+    var.diff_norm = int(bool(diff_norm))
+    var.diff_norm_eps = float(diff_norm_eps)
+    nw = _f32vec(diff_norm_w, dev)
+    keep.append(nw)
+    var.diff_norm_w = tensor(nw)
     if kv_page_table is not None:          # paged KV: k / v are page pools [n_pages, H, 128, D]
         t = (kv_page_table if torch.is_tensor(kv_page_table) else torch.as_tensor(kv_page_table))
         t = t.to(device=dev, dtype=torch.int32).contiguous()

@@ -84,6 +84,19 @@ def build(case: dict):
             lh = np.linspace(0.1, 0.9, Hq).astype(np.float32)
             gk["lambda_h"] = torch.from_numpy(lh)
             ok["lambda_h"] = lh.astype(np.float64)
+    if c.get("diff") and c.get("lambda_qk"):          # DIFF-Transformer lambda re-parameterisation (G8b)
+        lq = (np.random.default_rng(seed + 7).random((4, D)) * 0.2 - 0.1).astype(np.float32)
+        gk["lambda_qk"] = torch.from_numpy(lq)
+        ok["lambda_qk"] = lq.astype(np.float64)
+    if c.get("diff") and ("lambda_init" in c):
+        gk["lambda_init"] = ok["lambda_init"] = c["lambda_init"]
+    if c.get("diff") and c.get("diff_norm"):           # per-head RMSNorm epilogue (G8b)
+        gk["diff_norm"] = ok["diff_norm"] = True
+        gk["diff_norm_eps"] = ok["diff_norm_eps"] = c.get("diff_norm_eps", 1e-5)
+        if c.get("diff_norm_w"):
+            w = (np.random.default_rng(seed + 8).random(Dv) * 1.5 + 0.25).astype(np.float32)
+            gk["diff_norm_w"] = torch.from_numpy(w)
+            ok["diff_norm_w"] = w.astype(np.float64)
     if c.get("gate_mode"):
         g = synth.gate_logits((B, Hq, Sq, Dv), seed=seed, dtype=torch.bfloat16 if dt == torch.bfloat16 else dt)
         gk["gate_mode"] = ok["gate_mode"] = c["gate_mode"]

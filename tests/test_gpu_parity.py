@@ -52,6 +52,9 @@ F32_CASES = [
     dict(name="gqa", Hq=8, Hkv=2, S=70, D=32, mask="causal"),
     dict(name="diff", Hq=2, S=90, D=32, diff=True, lam=0.3),
     dict(name="diff_lambda_h", Hq=3, S=90, D=32, diff=True, lambda_h=True, mask="causal"),
+    dict(name="diff_norm_reparam", Hq=2, S=90, D=64, diff=True, lambda_qk=True, lambda_init=0.8, diff_norm=True,
+         diff_norm_w=True, mask="causal"),
+    dict(name="diff_norm_lambda_h", Hq=3, S=77, D=48, diff=True, lambda_h=True, lambda_init=0.2, diff_norm=True),
     dict(name="gate_sigmoid", S=64, D=32, gate_mode="sigmoid"),
     dict(name="gate_mul", S=64, D=32, gate_mode="mul"),
     dict(name="bias", Hq=2, S=64, D=32, bias="f32"),
@@ -124,6 +127,11 @@ for D in (128, 64, 32):
         dict(name=f"prefix_leak_D{D}", S=640, D=D, mask="prefix", prefix=200, dist="leak"),
         dict(name=f"document_leak_D{D}", S=1000, D=D, mask="document", n_docs=6, dist="leak"),
         dict(name=f"keymask_needle_D{D}", S=300, D=D, key_mask=True, p_zero=0.2, dist="needle"),
+        # DIFF-Transformer epilogue (NEXT-2, G8b): lambda re-parameterised, per-head RMSNorm x (1 - lambda_init)
+        dict(name=f"diff_norm_needle_D{D}", Hq=2, S=400, D=D, diff=True, lambda_qk=True, lambda_init=0.5,
+             diff_norm=True, diff_norm_w=True, dist="needle"),
+        dict(name=f"diff_norm_causal_D{D}", Hq=2, S=333, D=D, diff=True, lam=0.6, lambda_init=0.3,
+             diff_norm=True, mask="causal"),
         dict(name=f"document_needle_B2_D{D}", B=2, S=1000, D=D, mask="document", n_docs=6, dist="needle"),
     ]
 

@@ -243,3 +243,27 @@ def test_evoformer_mutants_fail(kind, drop):
         okm.pop(drop)
     got, _ = cases.run_oracle(ins, okm)
     must_fail(got, ref, f"evoformer {kind} without {drop}", strong=False)
+
+
+@pytest.mark.parametrize("name", ["diff_norm_needle_D128", "diff_norm_needle_D64", "diff_norm_causal_D32"])
+@pytest.mark.parametrize("mut", ["no_norm", "no_lambda_init_scale", "no_weight", "reparam_sign"])
+def test_diff_transformer_epilogue_mutants_fail(name, mut):
+    case, ins, ok, ref = setup(name)
+    okm = dict(ok)
+    if mut == "no_norm":
+        okm.pop("diff_norm")
+    elif mut == "no_lambda_init_scale":                    # (1 - lambda_init) factor dropped
+        if "lambda_qk" in okm:
+            pytest.skip("lambda_init also enters lambda here")
+        okm["lambda_init"] = 0.0
+    elif mut == "no_weight":
+        if "diff_norm_w" not in okm:
+            pytest.skip("unit weight")
+        okm.pop("diff_norm_w")
+    elif mut == "reparam_sign":                            # exp(q2.k2) - exp(q1.k1) + lambda_init
+        if "lambda_qk" not in okm:
+            pytest.skip("no re-parameterisation")
+        lq = okm["lambda_qk"]
+        okm["lambda_qk"] = np.concatenate([lq[2:], lq[:2]])
+    got, _ = cases.run_oracle(ins, okm)
+    must_fail(got, ref, f"{name} {mut}", strong=False)

@@ -546,3 +546,36 @@ def test_keep_rows_is_the_mask_predicate():
     got = oracle.keep_rows(q, k, v, rows, mask="blocklist", blk_idx=idx, blk_cnt=cnt, blk_q=16, blk_k=16).astype(bool)
     listed = ((kk // 16) == 0) | ((kk // 16) == 2)
     assert np.array_equal(got, listed & (kk <= qa))
+
+
+def test_diff_transformer_epilogue_brute_force_and_closed_forms():
+    """Reading G8b (NEXT-2, DIFF Transformer): lambda = exp(q1.k1) - exp(q2.k2) + lambda_init and
+    O = (1 - lambda_init) w * x / sqrt(mean(x^2) + eps), x = A_0 - lambda A_1 -- checked against an
+    independent math.fsum loop, and closed forms (mean square of a unit-weight row = ms/(ms+eps))."""
+    H, S, D = 2, 6, 4
+    q, k, v = rnd(1, 2 * H, S, D, seed=80), rnd(1, 2 * H, S, D, seed=81), rnd(1, H, S, D, seed=82)
+    lq = rnd(4, D, seed=83, lo=-0.5, hi=0.5).numpy()
+    w = rnd(D, seed=84, lo=0.5, hi=1.5).numpy()
+    out, _ = oracle.attn(q, k, v, diff=True, lambda_qk=lq, lambda_init=0.7, diff_norm=True, diff_norm_eps=1e-3,
+                         diff_norm_w=w)
+    lam = math.exp(math.fsum(lq[0] * lq[1])) - math.exp(math.fsum(lq[2] * lq[3])) + 0.7
+    a0 = brute(q[:, :H].numpy(), k[:, :H].numpy(), v.numpy(), lambda b, h, i, j: True)
+    a1 = brute(q[:, H:].numpy(), k[:, H:].numpy(), v.numpy(), lambda b, h, i, j: True)
+    x = a0 - lam * a1
+    want = np.zeros_like(x)
+    for h in range(H):
+        for i in range(S):
+            ms = math.fsum(float(t) ** 2 for t in x[0, h, i]) / D
+            want[0, h, i] = (1 - 0.7) * w * x[0, h, i] / math.sqrt(ms + 1e-3)
+    np.testing.assert_allclose(out.reshape(want.shape), want, rtol=1e-12, atol=1e-14)
+    # unit weight, lambda_init 0: every row's mean square is ms / (ms + eps)
+    plain, _ = oracle.attn(q, k, v, diff=True, lam=0.4)
+    normed, _ = oracle.attn(q, k, v, diff=True, lam=0.4, diff_norm=True, diff_norm_eps=1e-3)
+    ms = (plain ** 2).mean(1)
+    np.testing.assert_allclose((normed ** 2).mean(1), ms / (ms + 1e-3), rtol=1e-12)
+    # q2 = k2 = 0: lambda = exp(q1.k1) - 1 + lambda_init
+    lq2 = lq.copy()
+    lq2[2:] = 0
+    a, _ = oracle.attn(q, k, v, diff=True, lambda_qk=lq2, lambda_init=0.3)
+    b, _ = oracle.attn(q, k, v, diff=True, lam=math.exp(float(lq[0] @ lq[1])) - 1 + 0.3)
+    np.testing.assert_allclose(a, b, rtol=1e-14, atol=1e-15)

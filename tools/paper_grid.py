@@ -1,0 +1,193 @@
+#!/usr/bin/env python
+"""the paper's own benchmark grid (§4) on this
+B200, this kernel next to the on-box comparators (CONTEXT, not the bench line):
+  * FlexAttention-expressible variants (vanilla, ALiBi, softcap, causal, sliding window 256, PrefixLM 256,
+    12 documents), MHA (16/16 heads) and GQA (16:2), D = 64, S = 512 ... 16k with B * S = 16k tokens;
+    FlexAttention (torch.compile'd flex_attention) kernel time and block-mask creation time separately,
+    as the paper's Fig. 2 splits them;
+  * DiffAttn (Listing 4) at the MHA shapes, D = 64 and D = 128 (G17), vs torch.compile of Listing 4;
+  * Evoformer row attention with pair bias and gate, N_seq = 1 ... 32, N_res = 256, 4 heads, D = 64 / 128,
+    vs torch.compile of the eager Evoformer attention.
+Timing follows the paper: mean of 20 runs after 10 warm-ups, CUDA events.  Clocks are not capped
+(the paper capped at 1290 MHz).  Writes a markdown table to stdout.
+
+    python tools/paper_grid.py [--quick]
+"""
+import argparse
+import math
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2511_02043_b200 import fl, synth  # noqa: E402
+
+TOKENS, H, D, W, P, NDOC, CAP = 16384, 16, 64, 256, 256, 12, 20.0
+
+
+def timeit(fn, n=20, warm=10):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(n):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / n
+
+
+def pairs_of(variant, B, Hq, S, offs):
+    q = torch.arange(S, dtype=torch.float64)
+    if variant == "causal":
+        per = (q + 1).sum().item()
+    elif variant == "sliding":
+        per = (torch.clamp(q, max=W) + 1).sum().item()
+    elif variant == "prefix":
+        per = torch.clamp(torch.maximum(torch.full_like(q, P), q + 1), max=S).sum().item()
+    elif variant == "document":
+        return Hq * sum(int(((o[1:] - o[:-1]).astype("int64") ** 2).sum()) for o in offs)
+    else:
+        per = S * S
+    return per * B * Hq
+
+
+def flex_grid(quick):
+    from torch.nn.attention.flex_attention import create_block_mask, flex_attention
+    fa = torch.compile(flex_attention)
+    dev = torch.device("cuda")
+    rows = []
+    seqs = [512, 2048, 8192] if quick else [512, 1024, 2048, 4096, 8192, 16384]
+    for S in seqs:
+        B = TOKENS // S
+        for Hkv in (16, 2):
+            g = torch.Generator(device=dev).manual_seed(S + Hkv)
+            rnd = lambda h: (torch.rand(B, h, S, D, device=dev, generator=g) * 2 - 1).bfloat16()
+            q, k, v = rnd(H), rnd(Hkv), rnd(Hkv)
+            offs = synth.doc_offsets(B, S, NDOC, seed=1)
+            doc_id = torch.zeros(B, S, dtype=torch.long)
+            for b in range(B):
+                for j in range(NDOC):
+                    doc_id[b, offs[b, j]:offs[b, j + 1]] = j
+            doc_id = doc_id.to(dev)
+            slopes = torch.tensor(synth.alibi_slopes(H), device=dev)
+            mods = {
+                "alibi": lambda s, b, h, qi, ki: s + slopes[h] * (ki - qi),
+                "softcap": lambda s, b, h, qi, ki: CAP * torch.tanh(s / CAP),
+            }
+            masks = {
+                "causal": lambda b, h, qi, ki: qi >= ki,
+                "sliding": lambda b, h, qi, ki: (qi >= ki) & (qi - ki <= W),
+                "prefix": lambda b, h, qi, ki: (ki < P) | (qi >= ki),
+                "document": lambda b, h, qi, ki: doc_id[b, qi] == doc_id[b, ki],
+            }
+            ours_kw = {"vanilla": {}, "alibi": dict(mod="alibi"), "softcap": dict(mod="softcap", softcap=CAP),
+                       "causal": dict(mask="causal"), "sliding": dict(mask="sliding", window=W),
+                       "prefix": dict(mask="prefix", prefix=P),
+                       "document": dict(mask="document", doc_offsets=torch.from_numpy(offs).to(dev))}
+            out = torch.empty(B, H, S, D, device=dev, dtype=torch.bfloat16)
+            ws = torch.empty(1 << 20, device=dev, dtype=torch.uint8)
+            for name, kw in ours_kw.items():
+                t_ours = timeit(lambda: fl.attn_fwd(q, k, v, out=out, workspace=ws, **kw))
+                t_mask, t_flex = 0.0, float("nan")
+                try:
+                    fkw = {"enable_gqa": Hkv != H}
+                    if name in mods:
+                        fkw["score_mod"] = mods[name]
+                    elif name in masks:
+                        mb = B if name == "document" else None
+                        t_mask = timeit(lambda: create_block_mask(masks[name], mb, None, S, S), n=5, warm=2)
+                        fkw["block_mask"] = create_block_mask(masks[name], mb, None, S, S)
+                    t_flex = timeit(lambda: fa(q, k, v, **fkw))
+                except Exception as e:  # pragma: no cover
+                    print(f"<!-- flex {name} S{S} failed: {str(e).splitlines()[0][:120]} -->")
+                pairs = pairs_of(name, B, H, S, offs)
+                rows.append((name, "MHA" if Hkv == H else "GQA", S, B, t_ours, t_flex, t_mask,
+                             pairs * 4 * D / t_ours / 1e9))
+                sys.stdout.flush()
+    return rows
+
+
+def diff_grid(quick):
+    dev = torch.device("cuda")
+
+    def listing4(q, k, v, lam):                        # Listing 4 with Listing 1's attention
+        q0, q1 = q.chunk(2, dim=1)
+        k0, k1 = k.chunk(2, dim=1)
+
+        def attention(q, k, v):
+            s = torch.matmul(q, k.transpose(-2, -1)) * (1 / math.sqrt(q.size(-1)))
+            return torch.matmul(torch.softmax(s.float(), dim=-1).to(q.dtype), v)
+        return attention(q0, k0, v) - lam * attention(q1, k1, v)
+    tc = torch.compile(listing4)
+    rows = []
+    for Dh in (64, 128):
+        for S in ([512, 4096] if quick else [512, 1024, 2048, 4096, 8192]):
+            B = TOKENS // S
+            g = torch.Generator(device=dev).manual_seed(S)
+            q = (torch.rand(B, 2 * H, S, Dh, device=dev, generator=g) * 2 - 1).bfloat16()
+            k = (torch.rand(B, 2 * H, S, Dh, device=dev, generator=g) * 2 - 1).bfloat16()
+            v = (torch.rand(B, H, S, Dh, device=dev, generator=g) * 2 - 1).bfloat16()
+            t_ours = timeit(lambda: fl.attn_fwd(q, k, v, diff=True, lam=0.2))
+            try:
+                t_tc = timeit(lambda: tc(q, k, v, 0.2))
+            except Exception:  # pragma: no cover (memory at long S)
+                t_tc = float("nan")
+            flops = 2 * B * H * S * S * 4 * Dh
+            rows.append(("diff", f"D{Dh}", S, B, t_ours, t_tc, 0.0, flops / t_ours / 1e9))
+    return rows
+
+
+def evo_grid(quick):
+    dev = torch.device("cuda")
+
+    def evo_eager(q, k, v, g, pb, km):                 # AF2 Alg.7 lines 5-6 on [B, s, h, i, c] views
+        s = torch.matmul(q, k.transpose(-2, -1)) * (1 / math.sqrt(q.size(-1))) + pb.unsqueeze(1)
+        s = s.float().masked_fill(~km[:, :, None, None, :].bool(), float("-inf"))
+        return torch.sigmoid(g) * torch.matmul(torch.softmax(s, -1).to(q.dtype), v)
+    tc = torch.compile(evo_eager)
+    rows = []
+    Nr, Hh = 256, 4
+    for Dh in (64, 128):
+        for Ns in ([1, 8, 32] if quick else [1, 2, 4, 8, 16, 32]):
+            g = torch.Generator(device=dev).manual_seed(Ns)
+            mk = lambda *shape: (torch.rand(*shape, device=dev, generator=g) * 2 - 1).bfloat16()
+            Q, K, V, G = (mk(1, Ns, Nr, Hh, Dh) for _ in range(4))
+            pb = (mk(1, Hh, Nr, Nr) * 4)
+            km = torch.ones(1, Ns, Nr, device=dev, dtype=torch.uint8)
+            view = lambda x: x.permute(0, 1, 3, 2, 4)
+            kw = dict(gate_mode="sigmoid", gate=view(G), bias=pb.unsqueeze(1).expand(1, Ns, Hh, Nr, Nr), key_mask=km)
+            t_ours = timeit(lambda: fl.attn_fwd(view(Q), view(K), view(V), **kw))
+            qe, ke, ve, ge = (view(x).contiguous() for x in (Q, K, V, G))
+            try:
+                t_tc = timeit(lambda: tc(qe, ke, ve, ge, pb, km))
+            except Exception:  # pragma: no cover
+                t_tc = float("nan")
+            flops = Ns * Hh * Nr * Nr * 4 * Dh
+            rows.append(("evoformer_row", f"D{Dh}", Ns, 1, t_ours, t_tc, 0.0, flops / t_ours / 1e9))
+    return rows
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--quick", action="store_true")
+    a = ap.parse_args()
+    print(f"# Paper benchmark grid on {torch.cuda.get_device_name()} (torch {torch.__version__}); context only\n")
+    print("| variant | heads | S (or N_seq) | B | ours ms | comparator ms | flex block-mask ms | ours TFLOP/s | "
+          "speed-up vs comparator kernel | incl. mask |")
+    print("|---|---|---|---|---|---|---|---|---|---|")
+    for rows in (flex_grid(a.quick), diff_grid(a.quick), evo_grid(a.quick)):
+        for name, heads, S, B, to, tf, tm, tfl in rows:
+            sp = tf / to if tf == tf else float("nan")
+            spm = (tf + tm) / to if tf == tf else float("nan")
+            print(f"| {name} | {heads} | {S} | {B} | {to:.4f} | {tf:.4f} | {tm:.4f} | {tfl:.1f} | {sp:.2f} | {spm:.2f} |")
+            sys.stdout.flush()
+    print("\ncomparator: FlexAttention (torch.compile'd flex_attention) for the first block; torch.compile of "
+          "Listing 4 for diff; torch.compile of the eager Evoformer row attention for evoformer_row.")
+
+
+if __name__ == "__main__":
+    main()
