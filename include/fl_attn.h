@@ -150,6 +150,27 @@ typedef struct {
  * lse = -inf (G7); a fully masked row likewise gives O = 0, lse = -inf. */
 fl_status fl_attn_fwd(const fl_attn_args* args);
 
+/* ---- backward (the training half, §2.4) ------------------------------
+ * dQ, dK, dV of L = sum(O * dout) for the forward fl_attn_fwd computes with the same q, k, v, variant,
+ * given its output o and natural-log LSE (G19).  Two tcgen05 kernels (a KV-tile-major dK/dV pass and a
+ * query-tile-major dQ pass, no atomics) after a rowsum(dO * O) pass.  Supported (v1): bf16, rank-4 q/k/v,
+ * D_qk == D_v in {64, 128}, GQA, masks none / causal / sliding / prefix / document (either alignment),
+ * mods none / ALiBi / softcap.  Not yet: diff, gate, bias, key_mask, block lists, paged KV, fp32
+ * (FL_ERR_UNSUPPORTED).  Workspace: 4 * B * Hq * S_q bytes (fl_attn_bwd_workspace_size). */
+typedef struct {
+  fl_tensor q, k, v, o;      /* the forward's inputs and output (bf16) */
+  fl_tensor lse;             /* the forward's LSE, f32 [B, Hq, S_q] (required) */
+  fl_tensor dout;            /* dL/dO, bf16, o's shape */
+  fl_tensor dq, dk, dv;      /* outputs, bf16, the shapes of q, k, v; written in full */
+  fl_variant var;
+  void* stream;
+  void* workspace;
+  size_t workspace_bytes;
+} fl_attn_bwd_args;
+
+fl_status fl_attn_bwd(const fl_attn_bwd_args* args);
+fl_status fl_attn_bwd_workspace_size(const fl_attn_bwd_args* args, size_t* bytes);
+
 /* Bytes of device workspace fl_attn_fwd needs for these args (caller-owned, >= 16-byte aligned, not
  * shared by concurrent calls): bf16 path: 256 bytes for the persistent kernel's work-unit ticket
  * counter (reset by the call itself with a stream-ordered memset), then -- when key_mask is present --

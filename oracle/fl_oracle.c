@@ -240,6 +240,124 @@ int flo_keep_row(const flo_problem* p, int64_t b, int64_t g, int64_t h, int64_t 
   return 0;
 }
 
+/* ---- backward (the training half of the same program, §2.4 AOTAutograd) ----
+ * The plain chain rule through the definition evaluated by one_row, per output row (b, g, h, q):
+ *   P_k = e^{s_k - m} / d over the kept keys,   O = sum_k P_k V_k  (map by map; diff: O = A_0 - lambda A_1)
+ *   dA_map = dO * gate' (gate' = sigma(G) or G) * (map 0: 1, map 1: -lambda)
+ *   dV_k += P_k dA ;  dP_k = <dA, V_k> ;  dS_k = P_k (dP_k - <dA, A_map>)      (softmax Jacobian)
+ *   dx_k = dS_k * (softcap: 1 - (s_k / cap)^2, else 1)                          (s = cap tanh(x / cap))
+ *   dQ += scale dx_k K_k ;  dK_k += scale dx_k Q                                (x = scale <Q, K_k> + ...)
+ * dK, dV of a KV head accumulate over its GQA group (G15).  Outputs are fp64 arrays with the logical shapes
+ * of q, k, v ([B,G,H,S,D], row-major).  diff_norm is not differentiated here (returns -11). */
+int flo_attn_bwd(const flo_problem* p, const flo_tensor* dout, double* dq, double* dk, double* dv) {
+  int64_t maps;
+  int rc = check_problem(p, &maps);
+  if (rc) return rc;
+  if (p->diff_norm) return -11;
+  const int64_t B = p->q.size[0], G = p->q.size[1], Hq = p->q.size[2] / maps, Hkv = p->k.size[2] / maps;
+  const int64_t Sq = p->q.size[3], Sk = p->k.size[3], Dqk = p->q.size[4], Dv = p->v.size[4];
+  const int64_t grp = Hq / Hkv;
+  const double scale = p->scale != 0.0 ? p->scale : 1.0 / sqrt((double)Dqk);     /* G1 */
+  const int64_t nq = B * G * Hq * maps * Sq * Dqk, nk = B * G * Hkv * maps * Sk * Dqk, nv = B * G * Hkv * Sk * Dv;
+  for (int64_t i = 0; i < nq; ++i) dq[i] = 0.0;
+  for (int64_t i = 0; i < nk; ++i) dk[i] = 0.0;
+  for (int64_t i = 0; i < nv; ++i) dv[i] = 0.0;
+  /* one task per (b, g, kv head): every write of the task stays inside it */
+#pragma omp parallel
+  {
+    double* sc = (double*)malloc(sizeof(double) * (size_t)(Sk > 0 ? Sk : 1));
+    double* pr = (double*)malloc(sizeof(double) * (size_t)(Sk > 0 ? Sk : 1));
+    double* a = (double*)malloc(sizeof(double) * (size_t)(Dv > 0 ? Dv : 1));
+    double* da = (double*)malloc(sizeof(double) * (size_t)(Dv > 0 ? Dv : 1));
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t task = 0; task < B * G * Hkv; ++task) {
+      const int64_t hk = task % Hkv, g = (task / Hkv) % G, b = task / (Hkv * G);
+      for (int64_t h = hk * grp; h < (hk + 1) * grp; ++h) {
+        const int64_t bgh = (b * G + g) * Hq + h;
+        double lam = p->lambda_h ? p->lambda_h[h] : p->lambda;
+        if (maps == 2 && p->lambda_qk) {
+          double d1 = 0.0, d2 = 0.0;
+          for (int64_t d = 0; d < Dqk; ++d) {
+            d1 += p->lambda_qk[d] * p->lambda_qk[Dqk + d];
+            d2 += p->lambda_qk[2 * Dqk + d] * p->lambda_qk[3 * Dqk + d];
+          }
+          lam = exp(d1) - exp(d2) + p->lambda_init;
+        }
+        for (int64_t q = 0; q < Sq; ++q) {
+          const int64_t q_abs = p->causal_align ? q : q + (Sk - Sq);            /* G12 */
+          for (int64_t map = 0; map < maps; ++map) {
+            const int64_t qh = h + map * Hq, kh = hk + map * Hkv;
+            /* forward of this map: kept scores, P (Alg.1 two-pass), A = P V */
+            int any = 0;
+            for (int64_t k = 0; k < Sk; ++k) {
+              if (!kept(p, bgh, b, g, q, q_abs, k)) { sc[k] = -INFINITY; continue; }
+              any = 1;
+              double dot = 0.0;
+              for (int64_t d = 0; d < Dqk; ++d)
+                dot += elem(&p->q, off5(&p->q, b, g, qh, q, d)) * elem(&p->k, off5(&p->k, b, g, kh, k, d));
+              double x = scale * dot;
+              if (p->mod == FLO_MOD_ALIBI) {
+                double slope = p->alibi_slopes ? p->alibi_slopes[h] : pow(2.0, -8.0 * (double)(h + 1) / (double)Hq);
+                x += slope * (double)(k - q_abs);
+              }
+              if (p->bias.data) x += elem(&p->bias, off5(&p->bias, b, g, h, q, k));
+              if (p->mod == FLO_MOD_SOFTCAP) x = p->softcap * tanh(x / p->softcap);
+              sc[k] = x;
+            }
+            if (!any) continue;                                                   /* G7: O = 0, no gradient */
+            double m = -INFINITY, den = 0.0;
+            for (int64_t k = 0; k < Sk; ++k) m = sc[k] > m ? sc[k] : m;
+            for (int64_t k = 0; k < Sk; ++k) den += exp(sc[k] - m);
+            for (int64_t d = 0; d < Dv; ++d) a[d] = 0.0;
+            for (int64_t k = 0; k < Sk; ++k) {
+              pr[k] = sc[k] == -INFINITY ? 0.0 : exp(sc[k] - m) / den;
+              if (pr[k] != 0.0)
+                for (int64_t d = 0; d < Dv; ++d) a[d] += pr[k] * elem(&p->v, off5(&p->v, b, g, hk, k, d));
+            }
+            /* dA = dO * gate' * (1 or -lambda) */
+            double coef = map == 0 ? 1.0 : -lam;
+            double dot_da_a = 0.0;
+            for (int64_t d = 0; d < Dv; ++d) {
+              double gv = 1.0;
+              if (p->gate_mode != FLO_GATE_NONE) {
+                double gl = elem(&p->gate, off5(&p->gate, b, g, h, q, d));
+                gv = p->gate_mode == FLO_GATE_SIGMOID ? 1.0 / (1.0 + exp(-gl)) : gl;
+              }
+              da[d] = coef * gv * elem(dout, off5(dout, b, g, h, q, d));
+              dot_da_a += da[d] * a[d];
+            }
+            for (int64_t k = 0; k < Sk; ++k) {
+              if (pr[k] == 0.0 && sc[k] == -INFINITY) continue;
+              double dp = 0.0;
+              for (int64_t d = 0; d < Dv; ++d) {
+                const double vv = elem(&p->v, off5(&p->v, b, g, hk, k, d));
+                dp += da[d] * vv;
+                dv[(((b * G + g) * Hkv + hk) * Sk + k) * Dv + d] += pr[k] * da[d];
+              }
+              double dx = pr[k] * (dp - dot_da_a);
+              if (p->mod == FLO_MOD_SOFTCAP) {
+                const double t = sc[k] / p->softcap;
+                dx *= 1.0 - t * t;
+              }
+              for (int64_t d = 0; d < Dqk; ++d) {
+                dq[((((b * G + g) * Hq * maps) + qh) * Sq + q) * Dqk + d] +=
+                    scale * dx * elem(&p->k, off5(&p->k, b, g, kh, k, d));
+                dk[((((b * G + g) * Hkv * maps) + kh) * Sk + k) * Dqk + d] +=
+                    scale * dx * elem(&p->q, off5(&p->q, b, g, qh, q, d));
+              }
+            }
+          }
+        }
+      }
+    }
+    free(sc);
+    free(pr);
+    free(a);
+    free(da);
+  }
+  return 0;
+}
+
 /* ---- RSA (reading G10/G11; the paper only names RSA) ---- */
 int flo_rsa_summaries(const flo_tensor* k, int32_t blk_k, double* kmin, double* kmax) {
   const int64_t B = k->size[0], G = k->size[1], H = k->size[2], Sk = k->size[3], D = k->size[4];

@@ -101,6 +101,11 @@ int flo_rsa_select(const flo_tensor* q, const flo_tensor* k, int32_t blk_q, int3
                    int32_t topk, int32_t causal_align, int32_t max_sel,
                    int32_t* blk_idx, int32_t* blk_cnt, double* scores);
 
+/* Backward: dQ, dK, dV (fp64, logical shapes of q, k, v, row-major) of
+ * L = sum O * dO for the problem's forward, by the plain chain rule through the definition (see the
+ * comment at the definition).  dout: logical [B,G,Hq,Sq,Dv].  -11 when diff_norm is set (not derived). */
+int flo_attn_bwd(const flo_problem* p, const flo_tensor* dout, double* dq, double* dk, double* dv);
+
 int flo_num_threads(void);
 
 #ifdef __cplusplus

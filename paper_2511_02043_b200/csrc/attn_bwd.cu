@@ -1,0 +1,605 @@
+// attn_bwd.cu -- bf16 backward of the fused attention forward on the 5th-generation tensor cores
+// (the training half of the same attention program, which Flashlight hands to
+// AOTAutograd as a forward and a backward graph, §2.4).  Given Q, K, V, O, dO and the forward's
+// natural-log LSE (G19), with s = score_mod(scale QK^T) and P = exp(s - LSE) (no online softmax: the LSE
+// is known):
+//     Dvec_q = <dO_q, O_q>                                  (bwd_dvec_kernel)
+//     dV_k   = sum_q P_qk dO_q
+//     dS_qk  = P_qk (<dO_q, V_k> - Dvec_q) * (softcap: 1 - (s_qk / cap)^2)
+//     dK_k   = scale sum_q dS_qk Q_q,   dQ_q = scale sum_k dS_qk K_k
+// Two tcgen05 kernels, each a 128-row tile of TMEM lanes with TMA-fed operands (the forward's tensor
+// maps, 128-B swizzle) and one softmax-like warpgroup (thread = TMEM lane):
+//  * bwd_dkdv_kernel: CTA = one 128-key tile of one (b, kv head); walks the query tiles (of every query
+//    head of its GQA group) whose mask interval meets the tile:  S^T = K Q^T and dP^T = V dO^T (SS),
+//    P^T and dS^T (bf16) written back to TMEM, dV += P^T dO and dK += dS^T Q (TS, P / dS from TMEM).
+//  * bwd_dq_kernel: CTA = one 128-query tile of one (b, head); walks its KV tiles: S = Q K^T,
+//    dP = dO V^T, dS to TMEM, dQ += dS K.
+// TMEM columns (dkdv): S^T [0,128) with P^T (bf16) at [64,128) and dS^T at [0,64); dP^T [128,256);
+// dV [256, 256+D); dK [256+D, 256+2D).  (dq): S [0,128) with dS at [64,128); dP [128,256); dQ [256,256+D).
+// No atomics: every output element has one writer.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include <algorithm>
+
+#include "masks.cuh"
+#include "params.h"
+#include "ptx.cuh"
+
+namespace fl {
+
+constexpr float kBwdLog2e = 1.4426950408889634f;
+
+// ---------------------------------------------------------------- Dvec = rowsum(dO * O)
+// one warp per output row, 16-byte loads; dvec [B, G, Hq, Sq] f32 contiguous
+__global__ void __launch_bounds__(256) bwd_dvec_kernel(const AttnParams p, const __nv_bfloat16* __restrict__ dout,
+                                                      Strided5 dos, float* __restrict__ dvec) {
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int64_t n_rows = (int64_t)p.B * p.G * p.Hq * p.Sq;
+  if (row >= n_rows) return;
+  const int q = (int)(row % p.Sq);
+  const int64_t bgh = row / p.Sq;
+  const int h = (int)(bgh % p.Hq), g = (int)((bgh / p.Hq) % p.G), b = (int)(bgh / ((int64_t)p.Hq * p.G));
+  const __nv_bfloat16* o = static_cast<const __nv_bfloat16*>(p.o) + b * p.os.b + g * p.os.g + h * p.os.h + q * p.os.s;
+  const __nv_bfloat16* d = dout + b * dos.b + g * dos.g + h * dos.h + q * dos.s;
+  float acc = 0.f;
+  for (int c = lane * 8; c < p.Dv; c += 256) {
+    const uint4 uo = *reinterpret_cast<const uint4*>(o + c), ud = *reinterpret_cast<const uint4*>(d + c);
+    const uint32_t wo[4] = {uo.x, uo.y, uo.z, uo.w}, wd[4] = {ud.x, ud.y, ud.z, ud.w};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      acc = fmaf(bf16_lo(wo[t]), bf16_lo(wd[t]), acc);
+      acc = fmaf(bf16_hi(wo[t]), bf16_hi(wd[t]), acc);
+    }
+  }
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+  if (lane == 0) dvec[row] = acc;
+}
+
+// ---------------------------------------------------------------- shared configuration
+template <int D>
+struct BwdCfg {
+  static constexpr int CH = 64;                      // bf16 per 128-byte swizzle row
+  static constexpr int SWB = 128;
+  static constexpr int NCH = D / CH;
+  static constexpr int CHUNK_BYTES = 128 * SWB;      // 128 rows x 128 B
+  static constexpr int TILE_BYTES = 128 * D * 2;
+  static constexpr uint32_t LAYOUT = kLayoutSW128;
+  static constexpr int SBO = 8 * SWB;
+  static constexpr uint32_t IDESC_NN = idesc_bf16_f32(128, 128, 0);   // [128 x D] . [128 x D]^T (both K-major)
+  static constexpr uint32_t IDESC_ND = idesc_bf16_f32(128, D, 1);     // TMEM A [128 x 128] . smem B [128 x D] MN-major
+  static constexpr int NST = 2;                      // ring stages (pairs of tiles)
+  // smem: two resident tiles | NST x two streamed tiles | per-stage LSE / Dvec rows (dkdv) | barriers
+  static constexpr int SMEM_FIXED = 0;
+  static constexpr int SMEM_RING = 2 * TILE_BYTES;
+  static constexpr int SMEM_ROWS = SMEM_RING + NST * 2 * TILE_BYTES;
+  static constexpr int SMEM_BAR = SMEM_ROWS + NST * 2 * 128 * 4;
+  static constexpr int SMEM_TOTAL = SMEM_BAR + 128 + 1024;
+};
+
+// K-major 128 x D tile as UMMA operand, K step kk (16 elements)
+template <int D>
+__device__ __forceinline__ uint64_t kmajor_desc(uint32_t base, int kk) {
+  using C = BwdCfg<D>;
+  const uint32_t off = (kk * 16 / C::CH) * C::CHUNK_BYTES + (kk * 16 % C::CH) * 2;
+  return smem_desc(base + off, 16, C::SBO, C::LAYOUT);
+}
+// the same tile read as an MN-major B operand [K = its 128 rows, N = D], K step kk
+template <int D>
+__device__ __forceinline__ uint64_t mnmajor_desc(uint32_t base, int kk) {
+  using C = BwdCfg<D>;
+  return smem_desc(base + kk * 16 * C::SWB, C::CHUNK_BYTES, C::SBO, C::LAYOUT);
+}
+
+// Per-element score of the forward (natural units) for query row q (absolute q_abs), key k, head h:
+// scale s (+ ALiBi) (-> softcap), plus the softcap derivative factor.
+template <int MOD>
+__device__ __forceinline__ float bwd_score(const AttnParams& p, float s_raw, float slope, int k, int q_abs, float& ft) {
+  float x = s_raw * p.scale;
+  if (MOD == MOD_ALIBI) x = fmaf(slope, (float)(k - q_abs), x);
+  ft = 1.f;
+  if (MOD == MOD_SOFTCAP) {
+    const float t = tanh_approx(x / p.softcap);
+    ft = 1.f - t * t;
+    x = p.softcap * t;
+  }
+  return x;
+}
+
+__device__ __forceinline__ float head_slope(const AttnParams& p, int h) {
+  return p.alibi ? p.alibi[h] : exp2f(-8.f * (float)(h + 1) / (float)p.Hq);
+}
+
+// ================================================================ dK / dV
+// grid = B * Hkv * n_kvtile (kv tile ascending within a head: causal's heaviest tiles first), 192 threads:
+// warps 0-3 compute (thread = key row), warp 4 TMA producer, warp 5 MMA issuer + TMEM allocator.
+template <int D, int MOD>
+__global__ void __launch_bounds__(192, 1)
+    bwd_dkdv_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ TmaMaps maps,
+                    const __grid_constant__ CUtensorMap tdo, const float* __restrict__ lse_g, Strided5 ls,
+                    const float* __restrict__ dvec, __nv_bfloat16* __restrict__ dk, Strided5 dks,
+                    __nv_bfloat16* __restrict__ dv, Strided5 dvs) {
+  using C = BwdCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sK = smem;
+  uint8_t* sV = smem + C::TILE_BYTES;
+  uint8_t* sRing = smem + C::SMEM_RING;              // stage st: Q tile, dO tile
+  float* sRows = reinterpret_cast<float*>(smem + C::SMEM_ROWS);   // stage st: lse_l2[128], dvec[128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::SMEM_BAR);
+  uint64_t* kv_full = bars;
+  uint64_t* full = bars + 1;                         // [NST]
+  uint64_t* empty = full + C::NST;                   // [NST]
+  uint64_t* s_full = empty + C::NST;
+  uint64_t* p_full = s_full + 1;
+  uint64_t* o_full = p_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
+
+  const int n_kt = (p.Sk + 127) / 128;
+  const int kt = blockIdx.x % n_kt;
+  const int hk = (blockIdx.x / n_kt) % p.Hkv;
+  const int b = blockIdx.x / (n_kt * p.Hkv);
+  const int k0 = kt * 128;
+  const int n_qt = (p.Sq + 127) / 128;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // the (query head, query tile) items of this CTA: every tile whose rows' key intervals meet [k0, k0+128)
+  auto item_needed = [&](int qt) {
+    const int q_first = qt * 128, q_last = min(p.Sq, q_first + 128) - 1;
+    const Interval u = rows_union(p, b, q_first, q_last);
+    return u.hi > k0 && u.lo < k0 + 128;
+  };
+
+  if (threadIdx.x == 0) {
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < C::NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 128);
+    mbar_init(o_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 5) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DV = 256, COL_DK = 256 + D;
+
+  if (warp == 4) {
+    // ============================== TMA producer ==============================
+    if (lane == 0) {
+      const int gk = maps.k_bcast_g ? 0 : 0, bk = maps.k_bcast_b ? 0 : b;
+      const int bv = maps.v_bcast_b ? 0 : b;
+      mbar_arrive_expect_tx(kv_full, 2 * C::TILE_BYTES);
+      int krow, kb;
+      kv_tile_coords(p, b, kt, bk, krow, kb);
+      int vrow, vb;
+      kv_tile_coords(p, b, kt, bv, vrow, vb);
+      for (int c = 0; c < C::NCH; ++c) {
+        tma_load_5d(sK + c * C::CHUNK_BYTES, &maps.k, kv_full, c * C::CH, krow, hk, gk, kb);
+        tma_load_5d(sV + c * C::CHUNK_BYTES, &maps.v, kv_full, c * C::CH, vrow, hk, gk, vb);
+      }
+      const int bq = maps.q_bcast_b ? 0 : b;
+      int e = 0;
+      for (int hh = hk * p.grp; hh < (hk + 1) * p.grp; ++hh)
+        for (int qt = 0; qt < n_qt; ++qt) {
+          if (!item_needed(qt)) continue;
+          const int st = e % C::NST;
+          if (e >= C::NST) mbar_wait(&empty[st], ((e / C::NST) - 1) & 1);
+          mbar_arrive_expect_tx(&full[st], 2 * C::TILE_BYTES);
+          uint8_t* dq_ = sRing + st * 2 * C::TILE_BYTES;
+          for (int c = 0; c < C::NCH; ++c) {
+            tma_load_5d(dq_ + c * C::CHUNK_BYTES, &maps.q, &full[st], c * C::CH, qt * 128, hh, 0, bq);
+            tma_load_5d(dq_ + C::TILE_BYTES + c * C::CHUNK_BYTES, &tdo, &full[st], c * C::CH, qt * 128, hh, 0, b);
+          }
+          ++e;
+        }
+    }
+  } else if (warp == 5) {
+    // ============================== MMA issuer ==============================
+    if (lane == 0) {
+      const uint32_t ka = smem_u32(sK), va = smem_u32(sV), ring = smem_u32(sRing);
+      mbar_wait(kv_full, 0);
+      int e = 0;
+      for (int hh = hk * p.grp; hh < (hk + 1) * p.grp; ++hh)
+        for (int qt = 0; qt < n_qt; ++qt) {
+          if (!item_needed(qt)) continue;
+          const int st = e % C::NST;
+          mbar_wait(&full[st], (e / C::NST) & 1);
+          tc_fence_after();
+          const uint32_t qa = ring + st * 2 * C::TILE_BYTES, doa = qa + C::TILE_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)   // S^T = K Q^T
+            umma_ss(tmem + COL_S, kmajor_desc<D>(ka, kk), kmajor_desc<D>(qa, kk), C::IDESC_NN, kk > 0);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)   // dP^T = V dO^T
+            umma_ss(tmem + COL_DP, kmajor_desc<D>(va, kk), kmajor_desc<D>(doa, kk), C::IDESC_NN, kk > 0);
+          umma_commit(s_full);
+          mbar_wait(p_full, e & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)        // dV += P^T dO   (P^T bf16 in TMEM [64, 128))
+            umma_ts(tmem + COL_DV, tmem + COL_S + 64 + kk * 8, mnmajor_desc<D>(doa, kk), C::IDESC_ND,
+                    (e > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)        // dK += dS^T Q   (dS^T bf16 in TMEM [0, 64))
+            umma_ts(tmem + COL_DK, tmem + COL_S + kk * 8, mnmajor_desc<D>(qa, kk), C::IDESC_ND,
+                    (e > 0 || kk > 0) ? 1u : 0u);
+          umma_commit(&empty[st]);
+          ++e;
+        }
+      umma_commit(o_full);
+    }
+  } else {
+    // ============================== compute (thread = key row) ==============================
+    const int r = threadIdx.x;                      // 0..127
+    const int k = k0 + r;
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    int e = 0;
+    for (int hh = hk * p.grp; hh < (hk + 1) * p.grp; ++hh) {
+      const float slope_l2 = MOD == MOD_ALIBI ? head_slope(p, hh) : 0.f;
+      for (int qt = 0; qt < n_qt; ++qt) {
+        if (!item_needed(qt)) continue;
+        const int st = e % C::NST;
+        const int q0 = qt * 128;
+        // this tile's LSE (log2 units) and Dvec rows, one per thread, into the stage's row buffer
+        float* rl = sRows + st * 256;
+        {
+          const int q = q0 + r;
+          const bool ok = q < p.Sq;
+          const int64_t li = (int64_t)b * ls.b + (int64_t)hh * ls.h + (int64_t)(ok ? q : 0) * ls.s;
+          rl[r] = ok ? lse_g[li] * kBwdLog2e : INFINITY;     // rows past S_q: P = 0
+          rl[128 + r] = ok ? dvec[(((int64_t)b * p.G) * p.Hq + hh) * p.Sq + q] : 0.f;
+        }
+        named_bar_sync(1, 128);
+        // tile class: mask-free when every row's interval covers [k0, k0 + 128) (intervals are monotone)
+        const int q_last = min(p.Sq, q0 + 128) - 1;
+        const Interval a0 = row_interval(p, b, q0), a1 = row_interval(p, b, q_last);
+        const bool full_tile = q_last - q0 == 127 && a1.lo <= k0 && a0.hi >= k0 + 128 && k0 + 128 <= p.Sk;
+        mbar_wait(s_full, e & 1);
+        tc_fence_after();
+        uint32_t sv[128];
+        tmem_ld32(tmem + lane_base + COL_S + 0, &sv[0]);
+        tmem_ld32(tmem + lane_base + COL_S + 32, &sv[32]);
+        tmem_ld32(tmem + lane_base + COL_S + 64, &sv[64]);
+        tmem_ld32(tmem + lane_base + COL_S + 96, &sv[96]);
+        tmem_wait_ld();
+        // P^T (bf16 pairs) and the softcap factor, query j = column
+        uint32_t pk[64], fk[64];
+#pragma unroll
+        for (int j = 0; j < 128; j += 2) {
+          float pr[2], f[2];
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            const int q = q0 + j + t;
+            float ft;
+            const float s = bwd_score<MOD>(p, __uint_as_float(sv[j + t]), slope_l2, k, q + p.q_off, ft);
+            bool keep = k < p.Sk;
+            if (!full_tile) {
+              const Interval iv = row_interval(p, b, q);
+              keep = keep && k >= iv.lo && k < iv.hi;
+            }
+            pr[t] = keep ? exp2f(fmaf(s, kBwdLog2e, -rl[j + t])) : 0.f;
+            f[t] = ft;
+          }
+          pk[j >> 1] = pack_bf16(pr[0], pr[1]);
+          fk[j >> 1] = pack_bf16(f[0], f[1]);
+        }
+        tmem_st32(tmem + lane_base + COL_S + 64, &pk[0]);
+        tmem_st32(tmem + lane_base + COL_S + 96, &pk[32]);
+        // dS^T = P^T (dP^T - Dvec) * f, 32 queries at a time, into [0, 64) (S^T is consumed)
+#pragma unroll
+        for (int c = 0; c < 128; c += 32) {
+          uint32_t dp[32];
+          tmem_ld32(tmem + lane_base + COL_DP + c, dp);
+          tmem_wait_ld();
+          uint32_t ds[16];
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            const uint32_t pw = pk[(c + j) >> 1], fw = fk[(c + j) >> 1];
+            float d0 = bf16_lo(pw) * (__uint_as_float(dp[j]) - rl[128 + c + j]);
+            float d1 = bf16_hi(pw) * (__uint_as_float(dp[j + 1]) - rl[128 + c + j + 1]);
+            if (MOD == MOD_SOFTCAP) {
+              d0 *= bf16_lo(fw);
+              d1 *= bf16_hi(fw);
+            }
+            ds[j >> 1] = pack_bf16(d0, d1);
+          }
+          tmem_st16(tmem + lane_base + COL_S + (c >> 1), ds);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        named_bar_sync(1, 128);                     // every thread has read this stage's row buffer
+        mbar_arrive(p_full);
+        ++e;
+      }
+    }
+    // ---- epilogue: dK (x scale) and dV rows of this key tile
+    if (e > 0) {
+      mbar_wait(o_full, 0);
+      tc_fence_after();
+    }
+    if (k < p.Sk) {
+      __nv_bfloat16* dkp = dk + b * dks.b + (int64_t)hk * dks.h + (int64_t)k * dks.s;
+      __nv_bfloat16* dvp = dv + b * dvs.b + (int64_t)hk * dvs.h + (int64_t)k * dvs.s;
+#pragma unroll
+      for (int which = 0; which < 2; ++which) {
+#pragma unroll
+        for (int c = 0; c < D; c += 32) {
+          uint32_t o[32];
+          if (e > 0) {
+            tmem_ld32(tmem + lane_base + (which ? COL_DK : COL_DV) + c, o);
+            tmem_wait_ld();
+          } else {
+#pragma unroll
+            for (int t = 0; t < 32; ++t) o[t] = 0u;
+          }
+          const float sc = which ? p.scale : 1.f;
+          uint4* op = reinterpret_cast<uint4*>((which ? dkp : dvp) + c);
+#pragma unroll
+          for (int t8 = 0; t8 < 4; ++t8)
+            op[t8] = make_uint4(pack_bf16(__uint_as_float(o[t8 * 8 + 0]) * sc, __uint_as_float(o[t8 * 8 + 1]) * sc),
+                                pack_bf16(__uint_as_float(o[t8 * 8 + 2]) * sc, __uint_as_float(o[t8 * 8 + 3]) * sc),
+                                pack_bf16(__uint_as_float(o[t8 * 8 + 4]) * sc, __uint_as_float(o[t8 * 8 + 5]) * sc),
+                                pack_bf16(__uint_as_float(o[t8 * 8 + 6]) * sc, __uint_as_float(o[t8 * 8 + 7]) * sc));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 5) tmem_dealloc<512>(tmem);
+}
+
+// ================================================================ dQ
+// grid = B * Hq * n_qtile (query tile descending: causal's heaviest tiles first), 192 threads.
+template <int D, int MOD>
+__global__ void __launch_bounds__(192, 1)
+    bwd_dq_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ TmaMaps maps,
+                  const __grid_constant__ CUtensorMap tdo, const float* __restrict__ lse_g, Strided5 ls,
+                  const float* __restrict__ dvec, __nv_bfloat16* __restrict__ dq, Strided5 dqs) {
+  using C = BwdCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sQ = smem;
+  uint8_t* sDO = smem + C::TILE_BYTES;
+  uint8_t* sRing = smem + C::SMEM_RING;              // stage st: K tile, V tile
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::SMEM_BAR);
+  uint64_t* q_full = bars;
+  uint64_t* full = bars + 1;
+  uint64_t* empty = full + C::NST;
+  uint64_t* s_full = empty + C::NST;
+  uint64_t* p_full = s_full + 1;
+  uint64_t* o_full = p_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
+
+  const int n_qt = (p.Sq + 127) / 128;
+  const int qt = n_qt - 1 - (int)(blockIdx.x % n_qt);
+  const int h = (blockIdx.x / n_qt) % p.Hq;
+  const int b = blockIdx.x / (n_qt * p.Hq);
+  const int hk = h / p.grp;
+  const int q0 = qt * 128;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const Interval u = rows_union(p, b, q0, min(p.Sq, q0 + 128) - 1);
+  const int kt_lo = u.hi > u.lo ? u.lo / 128 : 0, kt_hi = u.hi > u.lo ? (u.hi + 127) / 128 : 0;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < C::NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 128);
+    mbar_init(o_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 5) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DQ = 256;
+
+  if (warp == 4) {
+    if (lane == 0) {
+      const int bq = maps.q_bcast_b ? 0 : b;
+      mbar_arrive_expect_tx(q_full, 2 * C::TILE_BYTES);
+      for (int c = 0; c < C::NCH; ++c) {
+        tma_load_5d(sQ + c * C::CHUNK_BYTES, &maps.q, q_full, c * C::CH, q0, h, 0, bq);
+        tma_load_5d(sDO + c * C::CHUNK_BYTES, &tdo, q_full, c * C::CH, q0, h, 0, b);
+      }
+      const int bk = maps.k_bcast_b ? 0 : b, bv = maps.v_bcast_b ? 0 : b;
+      for (int kt = kt_lo; kt < kt_hi; ++kt) {
+        const int e = kt - kt_lo, st = e % C::NST;
+        if (e >= C::NST) mbar_wait(&empty[st], ((e / C::NST) - 1) & 1);
+        mbar_arrive_expect_tx(&full[st], 2 * C::TILE_BYTES);
+        uint8_t* dst = sRing + st * 2 * C::TILE_BYTES;
+        int krow, kb, vrow, vb;
+        kv_tile_coords(p, b, kt, bk, krow, kb);
+        kv_tile_coords(p, b, kt, bv, vrow, vb);
+        for (int c = 0; c < C::NCH; ++c) {
+          tma_load_5d(dst + c * C::CHUNK_BYTES, &maps.k, &full[st], c * C::CH, krow, hk, 0, kb);
+          tma_load_5d(dst + C::TILE_BYTES + c * C::CHUNK_BYTES, &maps.v, &full[st], c * C::CH, vrow, hk, 0, vb);
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {
+      const uint32_t qa = smem_u32(sQ), doa = smem_u32(sDO), ring = smem_u32(sRing);
+      mbar_wait(q_full, 0);
+      for (int kt = kt_lo; kt < kt_hi; ++kt) {
+        const int e = kt - kt_lo, st = e % C::NST;
+        mbar_wait(&full[st], (e / C::NST) & 1);
+        tc_fence_after();
+        const uint32_t ka = ring + st * 2 * C::TILE_BYTES, va = ka + C::TILE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)     // S = Q K^T
+          umma_ss(tmem + COL_S, kmajor_desc<D>(qa, kk), kmajor_desc<D>(ka, kk), C::IDESC_NN, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)     // dP = dO V^T
+          umma_ss(tmem + COL_DP, kmajor_desc<D>(doa, kk), kmajor_desc<D>(va, kk), C::IDESC_NN, kk > 0);
+        umma_commit(s_full);
+        mbar_wait(p_full, e & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)          // dQ += dS K   (dS bf16 in TMEM [64, 128))
+          umma_ts(tmem + COL_DQ, tmem + COL_S + 64 + kk * 8, mnmajor_desc<D>(ka, kk), C::IDESC_ND,
+                  (e > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&empty[st]);
+      }
+      umma_commit(o_full);
+    }
+  } else {
+    const int r = threadIdx.x;
+    const int q = q0 + r;
+    const bool row_ok = q < p.Sq;
+    const int q_abs = q + p.q_off;
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const float slope_l2 = MOD == MOD_ALIBI ? head_slope(p, h) : 0.f;
+    const float lse_l2 = row_ok ? lse_g[(int64_t)b * ls.b + (int64_t)h * ls.h + (int64_t)q * ls.s] * kBwdLog2e : INFINITY;
+    const float dvr = row_ok ? dvec[(((int64_t)b * p.G) * p.Hq + h) * p.Sq + q] : 0.f;
+    const Interval iv = row_interval(p, b, q);
+    for (int kt = kt_lo; kt < kt_hi; ++kt) {
+      const int e = kt - kt_lo;
+      const int k0 = kt * 128;
+      const bool full_tile = tile_inside(iv, k0, p.Sk);
+      mbar_wait(s_full, e & 1);
+      tc_fence_after();
+      uint32_t sv[128];
+      tmem_ld32(tmem + lane_base + COL_S + 0, &sv[0]);
+      tmem_ld32(tmem + lane_base + COL_S + 32, &sv[32]);
+      tmem_ld32(tmem + lane_base + COL_S + 64, &sv[64]);
+      tmem_ld32(tmem + lane_base + COL_S + 96, &sv[96]);
+      tmem_wait_ld();
+      uint32_t pk[64], fk[64];
+#pragma unroll
+      for (int j = 0; j < 128; j += 2) {
+        float pr[2], f[2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int k = k0 + j + t;
+          float ft;
+          const float s = bwd_score<MOD>(p, __uint_as_float(sv[j + t]), slope_l2, k, q_abs, ft);
+          const bool keep = full_tile || (k >= iv.lo && k < iv.hi && k < p.Sk);
+          pr[t] = keep ? exp2f(fmaf(s, kBwdLog2e, -lse_l2)) : 0.f;
+          f[t] = ft;
+        }
+        pk[j >> 1] = pack_bf16(pr[0], pr[1]);
+        fk[j >> 1] = pack_bf16(f[0], f[1]);
+      }
+#pragma unroll
+      for (int c = 0; c < 128; c += 32) {           // dS = P (dP - Dvec) f -> TMEM [64 + c/2, ...)
+        uint32_t dp[32];
+        tmem_ld32(tmem + lane_base + COL_DP + c, dp);
+        tmem_wait_ld();
+        uint32_t ds[16];
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const uint32_t pw = pk[(c + j) >> 1], fw = fk[(c + j) >> 1];
+          float d0 = bf16_lo(pw) * (__uint_as_float(dp[j]) - dvr);
+          float d1 = bf16_hi(pw) * (__uint_as_float(dp[j + 1]) - dvr);
+          if (MOD == MOD_SOFTCAP) {
+            d0 *= bf16_lo(fw);
+            d1 *= bf16_hi(fw);
+          }
+          ds[j >> 1] = pack_bf16(d0, d1);
+        }
+        tmem_st16(tmem + lane_base + COL_S + 64 + (c >> 1), ds);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(p_full);
+    }
+    if (kt_hi > kt_lo) {
+      mbar_wait(o_full, 0);
+      tc_fence_after();
+    }
+    if (row_ok) {
+      __nv_bfloat16* qp = dq + b * dqs.b + (int64_t)h * dqs.h + (int64_t)q * dqs.s;
+#pragma unroll
+      for (int c = 0; c < D; c += 32) {
+        uint32_t o[32];
+        if (kt_hi > kt_lo) {
+          tmem_ld32(tmem + lane_base + COL_DQ + c, o);
+          tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int t = 0; t < 32; ++t) o[t] = 0u;
+        }
+        const float sc = p.scale;
+        uint4* op = reinterpret_cast<uint4*>(qp + c);
+#pragma unroll
+        for (int t8 = 0; t8 < 4; ++t8)
+          op[t8] = make_uint4(pack_bf16(__uint_as_float(o[t8 * 8 + 0]) * sc, __uint_as_float(o[t8 * 8 + 1]) * sc),
+                              pack_bf16(__uint_as_float(o[t8 * 8 + 2]) * sc, __uint_as_float(o[t8 * 8 + 3]) * sc),
+                              pack_bf16(__uint_as_float(o[t8 * 8 + 4]) * sc, __uint_as_float(o[t8 * 8 + 5]) * sc),
+                              pack_bf16(__uint_as_float(o[t8 * 8 + 6]) * sc, __uint_as_float(o[t8 * 8 + 7]) * sc));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 5) tmem_dealloc<512>(tmem);
+}
+
+// ---------------------------------------------------------------- launch
+struct BwdLaunch {
+  const float* lse; Strided5 ls;
+  const __nv_bfloat16* dout; Strided5 dos;
+  float* dvec;
+  __nv_bfloat16 *dq, *dk, *dv;
+  Strided5 dqs, dks, dvs;
+};
+
+template <int D, int MOD>
+static cudaError_t launch_bwd_dm(const AttnParams& p, const TmaMaps& maps, const CUtensorMap& tdo, const BwdLaunch& L,
+                                 cudaStream_t s) {
+  using C = BwdCfg<D>;
+  const int n_kt = (p.Sk + 127) / 128, n_qt = (p.Sq + 127) / 128;
+  cudaError_t e = cudaFuncSetAttribute(bwd_dkdv_kernel<D, MOD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_TOTAL);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(bwd_dq_kernel<D, MOD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_TOTAL);
+  if (e != cudaSuccess) return e;
+  bwd_dkdv_kernel<D, MOD><<<p.B * p.Hkv * n_kt, 192, C::SMEM_TOTAL, s>>>(p, maps, tdo, L.lse, L.ls, L.dvec, L.dk, L.dks,
+                                                                        L.dv, L.dvs);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  bwd_dq_kernel<D, MOD><<<p.B * p.Hq * n_qt, 192, C::SMEM_TOTAL, s>>>(p, maps, tdo, L.lse, L.ls, L.dvec, L.dq, L.dqs);
+  return cudaGetLastError();
+}
+
+template <int D>
+static cudaError_t launch_bwd_d(const AttnParams& p, const TmaMaps& maps, const CUtensorMap& tdo, const BwdLaunch& L,
+                                cudaStream_t s) {
+  switch (p.mod) {
+    case MOD_ALIBI: return launch_bwd_dm<D, MOD_ALIBI>(p, maps, tdo, L, s);
+    case MOD_SOFTCAP: return launch_bwd_dm<D, MOD_SOFTCAP>(p, maps, tdo, L, s);
+    default: return launch_bwd_dm<D, MOD_NONE>(p, maps, tdo, L, s);
+  }
+}
+
+cudaError_t launch_attn_bwd(const AttnParams& p, const TmaMaps& maps, const CUtensorMap& tdo, const float* lse,
+                            Strided5 ls, const void* dout, Strided5 dos, float* dvec, void* dq, Strided5 dqs, void* dk,
+                            Strided5 dks, void* dv, Strided5 dvs, cudaStream_t s) {
+  const int64_t rows = (int64_t)p.B * p.G * p.Hq * p.Sq;
+  bwd_dvec_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(p, static_cast<const __nv_bfloat16*>(dout), dos, dvec);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  BwdLaunch L{lse, ls, static_cast<const __nv_bfloat16*>(dout), dos, dvec, static_cast<__nv_bfloat16*>(dq),
+              static_cast<__nv_bfloat16*>(dk), static_cast<__nv_bfloat16*>(dv), dqs, dks, dvs};
+  switch (p.Dqk) {
+    case 128: return launch_bwd_d<128>(p, maps, tdo, L, s);
+    case 64: return launch_bwd_d<64>(p, maps, tdo, L, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace fl

@@ -40,6 +40,9 @@ cudaError_t debug_timing(unsigned long long* out, int reset);
 cudaError_t launch_pipe_rate(int op, int iters, int n_sms, float* sink, cudaStream_t s);
 cudaError_t launch_sched_dump(const AttnParams& p, int32_t* out, int64_t out_words, int64_t* n_records,
                               int32_t* max_tiles, cudaStream_t stream);
+cudaError_t launch_attn_bwd(const AttnParams& p, const TmaMaps& maps, const CUtensorMap& tdo, const float* lse,
+                            Strided5 ls, const void* dout, Strided5 dos, float* dvec, void* dq, Strided5 dqs, void* dk,
+                            Strided5 dks, void* dv, Strided5 dvs, cudaStream_t s);
 }  // namespace fl
 
 using namespace fl;
@@ -680,6 +683,82 @@ fl_status fl_debug_schedule(const fl_attn_args* args, int32_t* out, int64_t out_
   if (out) ++g_launches;
   if (e == cudaErrorInvalidValue) return fail(FL_ERR_WORKSPACE, "out needs n_records * (8 + max_tiles) words");
   return e == cudaSuccess ? FL_OK : cuda_fail(e, "schedule dump launch");
+}
+
+namespace {
+struct BwdPrepared {
+  Prepared P;
+  View5 dout, dq, dk, dv;
+  size_t ws = 0;
+};
+
+fl_status prepare_bwd(const fl_attn_bwd_args* a, BwdPrepared& B, bool device_ptrs) {
+  if (!a) return fail(FL_ERR_INVALID_ARGUMENT, "args is NULL");
+  fl_attn_args f;
+  memset(&f, 0, sizeof f);
+  f.q = a->q; f.k = a->k; f.v = a->v; f.o = a->o; f.lse = a->lse; f.var = a->var;
+  f.stream = a->stream;
+  fl_status s = prepare(&f, B.P, device_ptrs);
+  if (s != FL_OK) return s;
+  const fl_variant& var = a->var;
+  const AttnParams& p = B.P.p;
+  if (!B.P.bf16 || B.P.q_rank != 4) return fail(FL_ERR_UNSUPPORTED, "backward: bf16, rank-4 q/k/v/o");
+  if (p.Dqk != 64 && p.Dqk != 128) return fail(FL_ERR_UNSUPPORTED, "backward: D in {64, 128}");
+  if (var.diff || var.gate_mode != FL_GATE_NONE || var.bias.data || var.key_mask.data || var.kv_page_table.data ||
+      var.mask == FL_MASK_BLOCKLIST)
+    return fail(FL_ERR_UNSUPPORTED, "backward v1: no diff / gate / bias / key_mask / block list / paged KV");
+  if (!a->lse.data) return fail(FL_ERR_INVALID_ARGUMENT, "backward needs the forward's lse");
+  const fl_tensor* ts[4] = {&a->dout, &a->dq, &a->dk, &a->dv};
+  View5* vs[4] = {&B.dout, &B.dq, &B.dk, &B.dv};
+  const View5* like[4] = {&B.P.o, &B.P.q, &B.P.k, &B.P.v};
+  for (int i = 0; i < 4; ++i) {
+    if (!ts[i]->data || ts[i]->dtype != FL_BF16) return fail(FL_ERR_INVALID_ARGUMENT, "dout / dq / dk / dv: bf16, required");
+    if (!to_view(*ts[i], 4, 0, *vs[i])) return fail(FL_ERR_SHAPE_MISMATCH, "dout / dq / dk / dv must be rank 4");
+    for (int d = 0; d < 5; ++d)
+      if (vs[i]->size[d] != like[i]->size[d]) return fail(FL_ERR_SHAPE_MISMATCH, "dout / dq / dk / dv shapes must match o / q / k / v");
+    if (vs[i]->stride[4] != 1 || !aligned16(*vs[i])) return fail(FL_ERR_MISALIGNED, "dout / dq / dk / dv: contiguous last dim, 16-byte aligned");
+  }
+  for (int i = 1; i < 4; ++i)
+    for (const View5* in : {&B.P.q, &B.P.k, &B.P.v, &B.P.o, &B.dout})
+      if (overlaps(*vs[i], *in)) return fail(FL_ERR_INVALID_ARGUMENT, "gradients must not overlap inputs");
+  if (device_ptrs)
+    for (int i = 0; i < 4; ++i)
+      if (!on_device(ts[i]->data)) return fail(FL_ERR_INVALID_ARGUMENT, "dout / dq / dk / dv must be device memory");
+  B.ws = ((size_t)p.B * p.G * p.Hq * p.Sq * sizeof(float) + 255) & ~size_t(255);
+  return FL_OK;
+}
+}  // namespace
+
+fl_status fl_attn_bwd_workspace_size(const fl_attn_bwd_args* args, size_t* bytes) {
+  if (!bytes) return fail(FL_ERR_INVALID_ARGUMENT, "bytes is NULL");
+  BwdPrepared B;
+  fl_status s = prepare_bwd(args, B, false);
+  if (s != FL_OK) return s;
+  *bytes = B.ws;
+  return FL_OK;
+}
+
+fl_status fl_attn_bwd(const fl_attn_bwd_args* args) {
+  BwdPrepared B;
+  fl_status s = prepare_bwd(args, B, true);
+  if (s != FL_OK) return s;
+  if (B.P.empty_work) return FL_OK;
+  if (!args->workspace || args->workspace_bytes < B.ws)
+    return fail(FL_ERR_WORKSPACE, "the backward needs %zu bytes of workspace", B.ws);
+  TmaMaps maps;
+  memset(&maps, 0, sizeof maps);
+  CUtensorMap tdo;
+  int bg, bb;
+  if ((s = encode_map(B.P.q, 64, &maps.q, &maps.q_bcast_g, &maps.q_bcast_b)) != FL_OK) return s;
+  if ((s = encode_map(B.P.k, 64, &maps.k, &maps.k_bcast_g, &maps.k_bcast_b)) != FL_OK) return s;
+  if ((s = encode_map(B.P.v, 64, &maps.v, &maps.v_bcast_g, &maps.v_bcast_b)) != FL_OK) return s;
+  if ((s = encode_map(B.dout, 64, &tdo, &bg, &bb)) != FL_OK) return s;
+  const cudaError_t e = launch_attn_bwd(B.P.p, maps, tdo, static_cast<const float*>(B.P.lse.data), strides_of(B.P.lse),
+                                        B.dout.data, strides_of(B.dout), static_cast<float*>(args->workspace),
+                                        B.dq.data, strides_of(B.dq), B.dk.data, strides_of(B.dk), B.dv.data,
+                                        strides_of(B.dv), static_cast<cudaStream_t>(args->stream));
+  g_launches += 3;
+  return e == cudaSuccess ? FL_OK : cuda_fail(e, "backward launch");
 }
 
 fl_status fl_diag_pipe_rate(int32_t op, int32_t iters, float* sink, int64_t* ops, void* stream) {

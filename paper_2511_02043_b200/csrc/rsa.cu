@@ -148,23 +148,28 @@ __global__ void __launch_bounds__(kSelThreads, 1)
   uint64_t* bar_sum = bars;                             // summaries landed
   uint64_t* bar_q = bars + 1;                           // raw Q tile landed
   uint64_t* bar_qfree = bars + 2;                       // MMAs of the previous item done (q+/q-, summaries free)
-  uint64_t* mma_done = bars + 3;                        // [2] accumulator ready
-  uint64_t* acc_empty = bars + 5;                       // [2] accumulator read by the select WG
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7);
+  // accumulator ready, one barrier per select warpgroup: with more select warpgroups than accumulator
+  // buffers a per-buffer barrier would be waited phases ahead (parity aliasing); per warpgroup its k-th
+  // item is its barrier's phase k
+  uint64_t* mma_done = bars + 3;                        // [kSelWG]
+  uint64_t* acc_empty = bars + 3 + kSelWG;              // [2] accumulator read by the select WG
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5 + kSelWG);
 
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int64_t n_pairs = (int64_t)p.B * p.G * p.Hkv * p.nqb;
   const int64_t pb = n_pairs * blockIdx.x / gridDim.x, pe = n_pairs * (blockIdx.x + 1) / gridDim.x;
   const int n_items = (int)(pe - pb) * p.grp;           // (pair, head in group)
+  const int n_mt0 = (p.nkb + 127) / 128;
+  // select warpgroups taking items round-robin (each with its own TMEM buffer use and no GQA group
+  // spanning items), else one warpgroup takes every item
+  const int nsel_items = (n_mt0 <= 2 && p.grp == 1) ? n_sel_wg : 1;
 
   if (t == 0) {
     mbar_init(bar_sum, 1);
     mbar_init(bar_q, 1);
     mbar_init(bar_qfree, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&mma_done[i], 1);
-      mbar_init(&acc_empty[i], 128);
-    }
+    for (int i = 0; i < 2; ++i) mbar_init(&acc_empty[i], 128);
+    for (int i = 0; i < kSelWG; ++i) mbar_init(&mma_done[i], 1);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc<512>(tmem_slot);
@@ -261,7 +266,7 @@ __global__ void __launch_bounds__(kSelThreads, 1)
                     C::IDESC, kk > 0);
           }
         }
-        umma_commit(&mma_done[buf]);
+        umma_commit(&mma_done[n % nsel_items]);
         umma_commit(bar_qfree);
       }
     }
@@ -270,7 +275,7 @@ __global__ void __launch_bounds__(kSelThreads, 1)
     // kSelWG select warpgroups (warps 0-3, 8-11, ...) take items round-robin when each item has its own TMEM
     // accumulator buffer and no GQA group spans items; otherwise warps 0-3 take every item.
     const int sel = warp < 4 ? 0 : (warp - 4) / 4;      // warps 0-3, 8-11, 12-15, ...
-    const int nsel = (nbuf == 2 && p.grp == 1) ? n_sel_wg : 1;
+    const int nsel = nsel_items;
     const int tt = t & 127, wq = warp & 3;              // thread / warp within the select warpgroup
     uint32_t* hist = scratch + sel * C::SCR_WORDS;      // [128] packed 16-bit bin counts
     uint32_t* rstate = hist + 128;                      // [16] digit / counts of the current pass
@@ -286,7 +291,7 @@ __global__ void __launch_bounds__(kSelThreads, 1)
       const int c = diag(i);
       const int n_mt_i = n_mt_of(c);
       const int buf = n % nbuf;
-      mbar_wait(&mma_done[buf], (n / nbuf) & 1);
+      mbar_wait(&mma_done[sel], (n / nsel) & 1);
       tc_fence_after();
       // ---- row max over the block's valid queries: thread t owns blocks m*128 + t
       const int nvalid = min(128, p.Sq - i * 128);

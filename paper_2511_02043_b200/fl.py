@@ -177,6 +177,31 @@ def _keep_alive_on(stream, tensors):
             t.record_stream(stream)
 
 
+def attn_bwd(q, k, v, out, lse, dout, *, dq=None, dk=None, dv=None, workspace=None, **variant):
+    """Backward of attn_fwd (fl_attn_bwd, NEXT-3): returns (dq, dk, dv) of L = sum(out * dout), given the
+    forward's output and natural-log LSE (attn_fwd(..., return_lse=True))."""
+    dq = torch.empty_like(q) if dq is None else dq
+    dk = torch.empty_like(k) if dk is None else dk
+    dv = torch.empty_like(v) if dv is None else dv
+    keep: list = []
+    fa = make_args(q, k, v, out, lse, keep=keep, **variant)
+    a = _lib.BwdArgs()
+    a.q, a.k, a.v, a.o, a.lse = fa.q, fa.k, fa.v, fa.o, fa.lse
+    a.dout, a.dq, a.dk, a.dv = tensor(dout), tensor(dq), tensor(dk), tensor(dv)
+    a.var = fa.var
+    a.stream = fa.stream
+    need = C.c_size_t(0)
+    _lib.check(_lib.lib().fl_attn_bwd_workspace_size(C.byref(a), C.byref(need)))
+    if workspace is None or workspace.numel() * workspace.element_size() < need.value:
+        workspace = torch.empty(max(need.value, 1), dtype=torch.uint8, device=q.device)
+    keep.append(workspace)
+    a.workspace = workspace.data_ptr()
+    a.workspace_bytes = need.value
+    _lib.check(_lib.lib().fl_attn_bwd(C.byref(a)))
+    _keep_alive_on(variant.get("stream"), keep)
+    return dq, dk, dv
+
+
 class HostRunner:
     """End-to-end entry over HOST buffers (fl_attn_fwd_host): H2D copies of the
     inputs, the kernel and the D2H copy of the output, all enqueued by the C ABI

@@ -1,0 +1,63 @@
+"""Backward parity (-m gpu): fl_attn_bwd's dQ, dK, dV against the fp64 oracle's plain
+chain rule (oracle.attn_bwd, itself pinned to central differences and torch.autograd of Listing 1).
+The forward's O and LSE come from fl_attn_fwd on the same inputs (as in training).  Tolerance: max-abs
+2e-2 per gradient with |Q|, |K|, |V|, |dO| <= 1 (the north_star's bf16 bar, applied to each gradient),
+and max|ref| >= 0.05 so the comparison is not vacuous."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2511_02043_b200 import synth
+from tests import cases
+from tests.parity import check
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fl():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2511_02043_b200 import fl as _fl
+    return _fl
+
+
+BWD = []
+for D in (128, 64):
+    BWD += [
+        dict(name=f"vanilla_D{D}", Hq=2, S=300, D=D),
+        dict(name=f"causal_needle_D{D}", Hq=2, S=520, D=D, mask="causal", dist="needle"),
+        dict(name=f"sliding_D{D}", S=700, D=D, mask="sliding", window=150, dist="needle"),
+        dict(name=f"prefix_D{D}", S=400, D=D, mask="prefix", prefix=100),
+        dict(name=f"document_D{D}", B=2, S=600, D=D, mask="document", n_docs=5),
+        dict(name=f"alibi_D{D}", Hq=4, S=260, D=D, mod="alibi", dist="needle"),
+        dict(name=f"softcap_D{D}", S=300, D=D, mod="softcap", softcap=2.0, dist="needle"),
+        dict(name=f"gqa_causal_D{D}", Hq=4, Hkv=2, S=333, D=D, mask="causal", dist="needle"),
+        dict(name=f"sq_lt_sk_D{D}", Sq=100, Sk=450, D=D, mask="causal"),
+    ]
+
+
+@pytest.mark.parametrize("case", BWD, ids=[c["name"] for c in BWD])
+def test_backward_vs_oracle(fl, case):
+    ins, gk, ok = cases.build(dict(case, dtype="bf16"))
+    q, k, v = (ins[n].cuda() for n in ("q", "k", "v"))
+    kw = {x: cases.to_dev(y, "cuda") for x, y in gk.items()}
+    out, lse = fl.attn_fwd(q, k, v, return_lse=True, **kw)
+    dout = synth.uniform(tuple(out.shape), seed=17, tensor="gate")
+    dq, dk, dv = fl.attn_bwd(q, k, v, out, lse, dout.cuda(), **kw)
+    torch.cuda.synchronize()
+    rq, rk, rv = oracle.attn_bwd(ins["q"], ins["k"], ins["v"], dout, **ok)
+    for name, got, ref in (("dq", dq, rq), ("dk", dk, rk), ("dv", dv, rv)):
+        check(got.cpu().double().numpy(), ref, 2e-2, min_ref=0.05, what=f"{case['name']} {name}")
+
+
+def test_backward_unsupported_is_loud(fl):
+    q = torch.zeros(1, 2, 128, 64, device="cuda", dtype=torch.bfloat16)
+    o, lse = fl.attn_fwd(q, q, q[:, :1].expand(1, 2, 128, 64).contiguous(), return_lse=True)
+    with pytest.raises(fl.FlError, match="UNSUPPORTED"):
+        fl.attn_bwd(q, q, q, o, lse, o, gate_mode="mul", gate=o)
+    q32 = torch.zeros(1, 1, 128, 32, device="cuda", dtype=torch.bfloat16)
+    o32, l32 = fl.attn_fwd(q32, q32, q32, return_lse=True)
+    with pytest.raises(fl.FlError, match="UNSUPPORTED"):
+        fl.attn_bwd(q32, q32, q32, o32, l32, o32)

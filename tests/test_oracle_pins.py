@@ -579,3 +579,50 @@ def test_diff_transformer_epilogue_brute_force_and_closed_forms():
     a, _ = oracle.attn(q, k, v, diff=True, lambda_qk=lq2, lambda_init=0.3)
     b, _ = oracle.attn(q, k, v, diff=True, lam=math.exp(float(lq[0] @ lq[1])) - 1 + 0.3)
     np.testing.assert_allclose(a, b, rtol=1e-14, atol=1e-15)
+
+
+# ----------------------------------------------------------------- backward (NEXT-3)
+@pytest.mark.parametrize("kw", [dict(), dict(mask="causal"), dict(mask="sliding", window=2), dict(mod="alibi"),
+                                dict(mod="softcap", softcap=0.7), dict(mask="prefix", prefix=2),
+                                dict(gate_mode="sigmoid"), dict(diff=True, lam=0.4), dict(gqa=True)])
+def test_backward_matches_central_differences(kw):
+    """The oracle's dQ, dK, dV (plain chain rule) against central differences of the oracle's own
+    FORWARD (an independent route: no derivative formula involved), L = sum(O * dO), h = 1e-6."""
+    kw = dict(kw)
+    gqa = kw.pop("gqa", False)
+    maps = 2 if kw.get("diff") else 1
+    H, Hkv, S, D = 2, (1 if gqa else 2), 5, 3
+    q = rnd(1, H * maps, S, D, seed=90)
+    k = rnd(1, Hkv * maps, S, D, seed=91)
+    v = rnd(1, Hkv, S, D, seed=92)
+    do = rnd(1, H, S, D, seed=93)
+    if kw.get("gate_mode"):
+        kw["gate"] = rnd(1, H, S, D, seed=94, lo=-2, hi=2)
+    dq, dk, dv = oracle.attn_bwd(q, k, v, do, **kw)
+    L = lambda q_, k_, v_: float((oracle.attn(q_, k_, v_, **kw)[0].reshape(do.shape) * do.numpy()).sum())
+    h = 1e-6
+    for t, grad in ((q, dq), (k, dk), (v, dv)):
+        num = np.zeros(grad.shape)
+        flat = t.view(-1)
+        for i in range(flat.numel()):
+            old = flat[i].item()
+            flat[i] = old + h
+            lp = L(q, k, v)
+            flat[i] = old - h
+            lm = L(q, k, v)
+            flat[i] = old
+            num.reshape(-1)[i] = (lp - lm) / (2 * h)
+        np.testing.assert_allclose(grad, num, rtol=1e-6, atol=1e-8)
+
+
+def test_backward_matches_torch_autograd_listing1():
+    """Listing 1 executed eagerly in fp64 under torch.autograd, causal and GQA via repeats."""
+    q, k, v, do = rnd(2, 4, 33, 8, seed=95), rnd(2, 2, 33, 8, seed=96), rnd(2, 2, 33, 8, seed=97), rnd(2, 4, 33, 8, seed=98)
+    qt, kt, vt = (t.clone().requires_grad_(True) for t in (q, k, v))
+    mask = ~torch.ones(33, 33, dtype=torch.bool).tril()
+    out = listing1(qt, kt.repeat_interleave(2, dim=1), vt.repeat_interleave(2, dim=1), attn_mask=mask)
+    (out * do).sum().backward()
+    dq, dk, dv = oracle.attn_bwd(q, k, v, do, mask="causal")
+    np.testing.assert_allclose(dq, qt.grad.numpy(), rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(dk, kt.grad.numpy(), rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(dv, vt.grad.numpy(), rtol=1e-10, atol=1e-12)
