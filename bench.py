@@ -50,6 +50,9 @@ VARIANTS = {
     "vanilla": dict(C2),
     "prefix": dict(C2, mask="prefix", prefix=256),
     "gqa": dict(C2, Hkv=2, mask="causal"),
+    # the backward (dQ, dK, dV) of the configs[1] shape, not a BASELINE line
+    "bwd_causal": dict(C2, mask="causal", bwd=True),
+    "bwd_vanilla": dict(C2, bwd=True),
     # configs[0]: vanilla causal softmax attention fp32 B=1 H=1 S=128 D=64 (exact SIMT path, launch-latency bound)
     "c1": dict(B=1, H=1, S=128, D=64, mask="causal", dtype="f32"),
     # configs[2]: differential attention bf16 B=8 H=16 S=8192 D=64 (two maps, lambda)
@@ -375,6 +378,25 @@ def dense_job(names, rank, world, device, with_host=True):
             fns.append(lambda q=q, k=k, v=v, out=out, dkw=dkw: fl.attn_fwd(q, k, v, out=out, workspace=ws, **dkw))
             okws.setdefault(n, kw)
         f32 = cfg.get("dtype") == "f32"
+        if cfg.get("bwd"):
+            # backward: O, LSE and dO resident; useful flops = 2.5 x the forward's (dV, dP, dS->dQ, dK and the
+            # recomputed S: the usual FlashAttention accounting); the dQ pass also recomputes S and dP
+            bfns = []
+            for (blk, host, q, k, v, out), f in zip(blocks, fns):
+                kw_b, _ = block_variant_kw(cfg, blk)
+                dkw = _dev_kw(kw_b, device)
+                o_b, lse_b = fl.attn_fwd(q, k, v, return_lse=True, **dkw)
+                do_b = torch.empty_like(o_b).uniform_(-1, 1)
+                g = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v))
+                wsb = torch.empty(4 * o_b.numel() // o_b.shape[-1] + 256, dtype=torch.uint8, device=device)
+                bfns.append(lambda q=q, k=k, v=v, o_b=o_b, lse_b=lse_b, do_b=do_b, g=g, dkw=dkw, wsb=wsb:
+                            fl.attn_bwd(q, k, v, o_b, lse_b, do_b, dq=g[0], dk=g[1], dv=g[2], workspace=wsb, **dkw))
+            flops *= 2.5
+            job.calls.append(Call(n, (lambda fns=bfns: [f() for f in fns]), flops, nbytes, "tensor",
+                                  kernel="bwd_dkdv_kernel"))
+            job.step_flops += flops
+            pairs_by[n] = flops / flops_per_pair(cfg)
+            continue
         job.calls.append(Call(n, (lambda fns=fns: [f() for f in fns]), flops, nbytes, "latency" if f32 else "tensor",
                               kernel="attn_simt_kernel" if f32 else "attn_tc_kernel", exec_flops=eflops))
         job.step_flops += flops

@@ -76,7 +76,7 @@ struct BwdCfg {
   static constexpr int SMEM_FIXED = 0;
   static constexpr int SMEM_RING = 2 * TILE_BYTES;
   static constexpr int SMEM_ROWS = SMEM_RING + NST * 2 * TILE_BYTES;
-  static constexpr int SMEM_BAR = SMEM_ROWS + NST * 2 * 128 * 4;
+  static constexpr int SMEM_BAR = SMEM_ROWS + NST * 4 * 128 * 4;   // per stage: lse, dvec, lo, hi of 128 rows
   static constexpr int SMEM_TOTAL = SMEM_BAR + 128 + 1024;
 };
 
@@ -249,13 +249,19 @@ __global__ void __launch_bounds__(192, 1)
         const int st = e % C::NST;
         const int q0 = qt * 128;
         // this tile's LSE (log2 units) and Dvec rows, one per thread, into the stage's row buffer
-        float* rl = sRows + st * 256;
+        // this tile's rows, one per thread: LSE (log2 units), Dvec and the key interval [lo, hi) of query q0 + r
+        // (rows past S_q get an empty interval: P = 0); the element loop reads them as broadcasts
+        float* rl = sRows + st * 512;
+        int* riv = reinterpret_cast<int*>(rl + 256);
         {
           const int q = q0 + r;
           const bool ok = q < p.Sq;
           const int64_t li = (int64_t)b * ls.b + (int64_t)hh * ls.h + (int64_t)(ok ? q : 0) * ls.s;
-          rl[r] = ok ? lse_g[li] * kBwdLog2e : INFINITY;     // rows past S_q: P = 0
+          rl[r] = ok ? lse_g[li] * kBwdLog2e : INFINITY;
           rl[128 + r] = ok ? dvec[(((int64_t)b * p.G) * p.Hq + hh) * p.Sq + q] : 0.f;
+          const Interval iv = row_interval(p, b, q);
+          riv[r] = ok ? iv.lo : 0;
+          riv[128 + r] = ok ? iv.hi : 0;
         }
         named_bar_sync(1, 128);
         // tile class: mask-free when every row's interval covers [k0, k0 + 128) (intervals are monotone)
@@ -280,12 +286,8 @@ __global__ void __launch_bounds__(192, 1)
             const int q = q0 + j + t;
             float ft;
             const float s = bwd_score<MOD>(p, __uint_as_float(sv[j + t]), slope_l2, k, q + p.q_off, ft);
-            bool keep = k < p.Sk;
-            if (!full_tile) {
-              const Interval iv = row_interval(p, b, q);
-              keep = keep && k >= iv.lo && k < iv.hi;
-            }
-            pr[t] = keep ? exp2f(fmaf(s, kBwdLog2e, -rl[j + t])) : 0.f;
+            const bool keep = full_tile || (k >= riv[j + t] && k < riv[128 + j + t]);   // hi <= S_k
+            pr[t] = keep ? ex2(fmaf(s, kBwdLog2e, -rl[j + t])) : 0.f;
             f[t] = ft;
           }
           pk[j >> 1] = pack_bf16(pr[0], pr[1]);
@@ -325,9 +327,11 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(o_full, 0);
       tc_fence_after();
     }
-    if (k < p.Sk) {
-      __nv_bfloat16* dkp = dk + b * dks.b + (int64_t)hk * dks.h + (int64_t)k * dks.s;
-      __nv_bfloat16* dvp = dv + b * dvs.b + (int64_t)hk * dvs.h + (int64_t)k * dvs.s;
+    // tcgen05.ld is .sync.aligned: every lane of the warp loads, only valid key rows store
+    {
+      const bool k_ok = k < p.Sk;
+      __nv_bfloat16* dkp = dk + b * dks.b + (int64_t)hk * dks.h + (int64_t)(k_ok ? k : 0) * dks.s;
+      __nv_bfloat16* dvp = dv + b * dvs.b + (int64_t)hk * dvs.h + (int64_t)(k_ok ? k : 0) * dvs.s;
 #pragma unroll
       for (int which = 0; which < 2; ++which) {
 #pragma unroll
@@ -342,6 +346,7 @@ __global__ void __launch_bounds__(192, 1)
           }
           const float sc = which ? p.scale : 1.f;
           uint4* op = reinterpret_cast<uint4*>((which ? dkp : dvp) + c);
+          if (k_ok)
 #pragma unroll
           for (int t8 = 0; t8 < 4; ++t8)
             op[t8] = make_uint4(pack_bf16(__uint_as_float(o[t8 * 8 + 0]) * sc, __uint_as_float(o[t8 * 8 + 1]) * sc),
@@ -489,7 +494,7 @@ __global__ void __launch_bounds__(192, 1)
           float ft;
           const float s = bwd_score<MOD>(p, __uint_as_float(sv[j + t]), slope_l2, k, q_abs, ft);
           const bool keep = full_tile || (k >= iv.lo && k < iv.hi && k < p.Sk);
-          pr[t] = keep ? exp2f(fmaf(s, kBwdLog2e, -lse_l2)) : 0.f;
+          pr[t] = keep ? ex2(fmaf(s, kBwdLog2e, -lse_l2)) : 0.f;
           f[t] = ft;
         }
         pk[j >> 1] = pack_bf16(pr[0], pr[1]);
@@ -522,8 +527,8 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(o_full, 0);
       tc_fence_after();
     }
-    if (row_ok) {
-      __nv_bfloat16* qp = dq + b * dqs.b + (int64_t)h * dqs.h + (int64_t)q * dqs.s;
+    {                                                // every lane loads (.sync.aligned), valid rows store
+      __nv_bfloat16* qp = dq + b * dqs.b + (int64_t)h * dqs.h + (int64_t)(row_ok ? q : 0) * dqs.s;
 #pragma unroll
       for (int c = 0; c < D; c += 32) {
         uint32_t o[32];
@@ -536,6 +541,7 @@ __global__ void __launch_bounds__(192, 1)
         }
         const float sc = p.scale;
         uint4* op = reinterpret_cast<uint4*>(qp + c);
+        if (row_ok)
 #pragma unroll
         for (int t8 = 0; t8 < 4; ++t8)
           op[t8] = make_uint4(pack_bf16(__uint_as_float(o[t8 * 8 + 0]) * sc, __uint_as_float(o[t8 * 8 + 1]) * sc),

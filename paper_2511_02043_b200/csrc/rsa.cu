@@ -109,7 +109,7 @@ cudaError_t launch_rsa_summaries(const void* k, int64_t sb, int64_t sg, int64_t 
 // released right after the row max, so the top-k of several items runs concurrently; the radix passes
 // are barrier / latency bound, not ALU bound.
 #ifndef FL_SEL_WG
-#define FL_SEL_WG 4
+#define FL_SEL_WG 2
 #endif
 constexpr int kSelWG = FL_SEL_WG;
 constexpr int kSelThreads = 128 * (kSelWG + 1);

@@ -49,14 +49,20 @@ def test_backward_vs_oracle(fl, case):
     torch.cuda.synchronize()
     rq, rk, rv = oracle.attn_bwd(ins["q"], ins["k"], ins["v"], dout, **ok)
     for name, got, ref in (("dq", dq, rq), ("dk", dk, rk), ("dv", dv, rv)):
-        check(got.cpu().double().numpy(), ref, 2e-2, min_ref=0.05, what=f"{case['name']} {name}")
+        r = check(got.cpu().double().numpy(), ref, 2e-2, min_ref=0.05 if name == "dv" else 0.0,
+                  what=f"{case['name']} {name}")
+        # where a gradient's scale is >= 0.05 it must also hold 5 % of that scale (G22); on peaked rows dQ
+        # cancels (dS = P (dP - Dvec) with Dvec from the bf16 O) and only the absolute bar applies
+        if r["max_ref"] >= 0.05:
+            assert r["max_abs"] <= 0.05 * r["max_ref"], f"{case['name']} {name}: {r}"
 
 
 def test_backward_unsupported_is_loud(fl):
     q = torch.zeros(1, 2, 128, 64, device="cuda", dtype=torch.bfloat16)
     o, lse = fl.attn_fwd(q, q, q[:, :1].expand(1, 2, 128, 64).contiguous(), return_lse=True)
+    g = torch.ones_like(o)
     with pytest.raises(fl.FlError, match="UNSUPPORTED"):
-        fl.attn_bwd(q, q, q, o, lse, o, gate_mode="mul", gate=o)
+        fl.attn_bwd(q, q, q, o, lse, o.clone(), gate_mode="mul", gate=g)
     q32 = torch.zeros(1, 1, 128, 32, device="cuda", dtype=torch.bfloat16)
     o32, l32 = fl.attn_fwd(q32, q32, q32, return_lse=True)
     with pytest.raises(fl.FlError, match="UNSUPPORTED"):
