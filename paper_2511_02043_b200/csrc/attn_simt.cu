@@ -18,7 +18,9 @@
 
 namespace fl {
 
-constexpr int SIMT_ROWS = 16;
+// RPW rows per warp, 4 warps: 16-row CTAs for big problems (K/V tiles shared by 16 rows); 4-row CTAs
+// when the problem has too few 16-row tiles to fill the SMs (C1: 128 rows -> 32 CTAs instead of 8)
+constexpr int SIMT_MAX_ROWS = 16;
 constexpr int SIMT_KT = 32;
 constexpr int SIMT_THREADS = 128;
 
@@ -39,7 +41,9 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
+template <int RPW>
 __global__ void __launch_bounds__(SIMT_THREADS) attn_simt_kernel(const __grid_constant__ AttnParams p) {
+  constexpr int SIMT_ROWS = 4 * RPW;
   extern __shared__ float sm[];
   const int Dq = p.Dqk, Dv = p.Dv;
   float* Ks = sm;                              // [KT][Dq+1]
@@ -79,12 +83,14 @@ __global__ void __launch_bounds__(SIMT_THREADS) attn_simt_kernel(const __grid_co
   if (p.mod == MOD_ALIBI) slope = p.alibi ? p.alibi[h] : exp2f(-8.f * (float)(h + 1) / (float)p.Hq);
   const float lam = p.maps == 2 ? diff_lambda(p, h) : 0.f;
 
-  float res[4][4];                             // final output accumulators (rows x d-chunks)
+  float res[RPW][4];                           // final output accumulators (rows x d-chunks)
 #pragma unroll
-  for (int r = 0; r < 4; ++r)
+  for (int r = 0; r < RPW; ++r)
 #pragma unroll
     for (int c = 0; c < 4; ++c) res[r][c] = 0.f;
-  float lse_out[4] = {0.f, 0.f, 0.f, 0.f};
+  float lse_out[RPW];
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) lse_out[r] = 0.f;
 
   for (int map = 0; map < p.maps; ++map) {
     const int qh = h + map * p.Hq, kh = hkv + map * p.Hkv;
@@ -94,15 +100,15 @@ __global__ void __launch_bounds__(SIMT_THREADS) attn_simt_kernel(const __grid_co
       int r = i / Dq, d = i % Dq, q = q_first + r;
       Qs[i] = q < p.Sq ? ld_in(p.q, b * p.qs.b + g * p.qs.g + qh * p.qs.h + q * p.qs.s + d, p.in_dtype) : 0.f;
     }
-    float m[4], l[4], acc[4][4];
-    int klo[4], khi[4];
+    float m[RPW], l[RPW], acc[RPW][4];
+    int klo[RPW], khi[RPW];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
+    for (int r = 0; r < RPW; ++r) {
       m[r] = -INFINITY;
       l[r] = 0.f;
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[r][c] = 0.f;
-      Interval iv = row_interval(p, b, q_first + warp * 4 + r);
+      Interval iv = row_interval(p, b, q_first + warp * RPW + r);
       klo[r] = iv.lo;
       khi[r] = iv.hi;
     }
@@ -130,13 +136,21 @@ __global__ void __launch_bounds__(SIMT_THREADS) attn_simt_kernel(const __grid_co
         key_ok = (kb[k >> 5] >> (k & 31)) & 1u;
       }
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int qrow = warp * 4 + r, q = q_first + qrow;
+      for (int r = 0; r < RPW; ++r) {
+        const int qrow = warp * RPW + r, q = q_first + qrow;
         if (q >= p.Sq) continue;                       // warp-uniform
         const float* qv = Qs + qrow * Dq;
         const float* kv = Ks + lane * (Dq + 1);
-        float dot = 0.f;
-        for (int d = 0; d < Dq; ++d) dot = fmaf(qv[d], kv[d], dot);
+        float d0 = 0.f, d1 = 0.f, d2 = 0.f, d3 = 0.f;   // four chains: latency, not the FMA pipe, bounds a row
+        int d = 0;
+        for (; d + 4 <= Dq; d += 4) {
+          d0 = fmaf(qv[d], kv[d], d0);
+          d1 = fmaf(qv[d + 1], kv[d + 1], d1);
+          d2 = fmaf(qv[d + 2], kv[d + 2], d2);
+          d3 = fmaf(qv[d + 3], kv[d + 3], d3);
+        }
+        for (; d < Dq; ++d) d0 = fmaf(qv[d], kv[d], d0);
+        const float dot = (d0 + d1) + (d2 + d3);
         float s = dot * p.scale;                       // Listing 1: scores *= 1/sqrt(d)
         if (p.mod == MOD_ALIBI) s += slope * (float)(k - (q + p.q_off));
         if (p.bias)
@@ -166,7 +180,7 @@ __global__ void __launch_bounds__(SIMT_THREADS) attn_simt_kernel(const __grid_co
     }
     const float coef = map == 0 ? 1.f : -lam;          // Listing 4: attn0 - lambda * attn1
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
+    for (int r = 0; r < RPW; ++r) {
       const float inv = l[r] > 0.f ? 1.f / l[r] : 0.f;
 #pragma unroll
       for (int c = 0; c < 4; ++c) res[r][c] += coef * acc[r][c] * inv;
@@ -175,10 +189,12 @@ __global__ void __launch_bounds__(SIMT_THREADS) attn_simt_kernel(const __grid_co
   }
 
   // DIFF-Transformer epilogue (NEXT-2): per-head RMSNorm of A_0 - lambda A_1 over D_v, times (1 - lambda_init)
-  float norm_k[4] = {1.f, 1.f, 1.f, 1.f};
+  float norm_k[RPW];
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) norm_k[r] = 1.f;
   if (p.maps == 2 && p.diff_norm) {
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
+    for (int r = 0; r < RPW; ++r) {
       float ss = 0.f;
 #pragma unroll
       for (int c = 0; c < 4; ++c)
@@ -188,8 +204,8 @@ __global__ void __launch_bounds__(SIMT_THREADS) attn_simt_kernel(const __grid_co
     }
   }
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int q = q_first + warp * 4 + r;
+  for (int r = 0; r < RPW; ++r) {
+    const int q = q_first + warp * RPW + r;
     if (q >= p.Sq) continue;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -210,19 +226,22 @@ __global__ void __launch_bounds__(SIMT_THREADS) attn_simt_kernel(const __grid_co
 
 size_t simt_smem_bytes(const AttnParams& p) {
   const int nkb = p.mask == MASK_BLOCKLIST ? (p.Sk + p.blk_k - 1) / p.blk_k : 0;
-  return sizeof(float) * (SIMT_KT * (p.Dqk + 1) + SIMT_KT * (p.Dv + 1) + SIMT_ROWS * p.Dqk) +
+  return sizeof(float) * (SIMT_KT * (p.Dqk + 1) + SIMT_KT * (p.Dv + 1) + SIMT_MAX_ROWS * p.Dqk) +
          sizeof(uint32_t) * ((nkb + 31) / 32 + 1);
 }
 
 cudaError_t launch_attn_simt(const AttnParams& p, cudaStream_t stream) {
-  const int nrb = (p.Sq + SIMT_ROWS - 1) / SIMT_ROWS;
-  const long long grid = (long long)p.B * p.G * p.Hq * nrb;
+  const long long bgh = (long long)p.B * p.G * p.Hq;
+  const bool small = bgh * ((p.Sq + SIMT_MAX_ROWS - 1) / SIMT_MAX_ROWS) < 2 * 148;
+  const int rows = small ? 4 : SIMT_MAX_ROWS;
+  const long long grid = bgh * ((p.Sq + rows - 1) / rows);
   const size_t smem = simt_smem_bytes(p);
+  auto kern = small ? attn_simt_kernel<1> : attn_simt_kernel<4>;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(attn_simt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  attn_simt_kernel<<<(unsigned)grid, SIMT_THREADS, smem, stream>>>(p);
+  kern<<<(unsigned)grid, SIMT_THREADS, smem, stream>>>(p);
   return cudaGetLastError();
 }
 
