@@ -29,7 +29,9 @@ int tc_chunk_elems(int D) { return D >= 64 ? 64 : 32; }
 cudaError_t launch_sched_dump(const AttnParams& p, int32_t* out, int64_t out_words, int64_t* n_records,
                               int32_t* max_tiles, cudaStream_t stream) {
   const bool diff = p.maps == 2;
-  const bool pair = p.Dqk == 32 && !diff && p.G >= 2 && p.Sq % 256 != 0 && p.Sq % 256 <= 128;
+  const bool pair = small_head_pair(p);
+  AttnParams pp = p;
+  pp.unit_order = pair && bias_resident(p) ? 1 : 0;   // the order launch_one gives the kernel
   const int rows_per_unit = (diff || pair) ? 128 : 256;
   const long long units =
       (long long)p.B * (pair ? (p.G + 1) / 2 : p.G) * p.Hq * ((p.Sq + rows_per_unit - 1) / rows_per_unit);
@@ -39,9 +41,9 @@ cudaError_t launch_sched_dump(const AttnParams& p, int32_t* out, int64_t out_wor
   if (!out) return cudaSuccess;                        // size query
   if (out_words < units * 2 * (8 + mt)) return cudaErrorInvalidValue;
   const int blocks = (int)((units * 2 + 127) / 128);
-  if (diff) sched_dump_kernel<true, false><<<blocks, 128, 0, stream>>>(p, (int)units, mt, out);
-  else if (pair) sched_dump_kernel<false, true><<<blocks, 128, 0, stream>>>(p, (int)units, mt, out);
-  else sched_dump_kernel<false, false><<<blocks, 128, 0, stream>>>(p, (int)units, mt, out);
+  if (diff) sched_dump_kernel<true, false><<<blocks, 128, 0, stream>>>(pp, (int)units, mt, out);
+  else if (pair) sched_dump_kernel<false, true><<<blocks, 128, 0, stream>>>(pp, (int)units, mt, out);
+  else sched_dump_kernel<false, false><<<blocks, 128, 0, stream>>>(pp, (int)units, mt, out);
   return cudaGetLastError();
 }
 

@@ -88,7 +88,10 @@ constexpr int kMaxSelTc = 256;
 // (m, l, O) partial; WG0 merges the two partials in the epilogue (the online-softmax closed
 // form, applied across the two halves of the list).  One Q tile, and step j of the
 // schedule carries two different KV tiles, so the ring holds 4 entries per step.
-template <int D, bool DIFF, bool LIST = false>
+// BIG: small heads (D = 32) without staged bias tiles (no bias, or the pair bias resident in TMEM) spend
+// the shared memory the bias tiles would take on a second Q buffer (the next unit's Q loads while this
+// unit's S MMAs still read the current one) and a 16-entry K/V ring (more than one unit of look-ahead).
+template <int D, bool DIFF, bool LIST = false, bool BIG = false>
 struct TcCfg {
   static constexpr int BM = 128;                     // query rows per tile (= TMEM lanes)
   static constexpr int BN = 128;                     // keys per KV tile
@@ -101,33 +104,43 @@ struct TcCfg {
 #ifndef FL_NSLOT64
 #define FL_NSLOT64 6
 #endif
-  static constexpr int NSLOT = LIST ? (D == 128 ? 5 : 8) : (D == 128 ? 4 : (D == 64 ? FL_NSLOT64 : 8));
+  static constexpr int NSLOT = LIST ? (D == 128 ? 5 : 8) : (D == 128 ? 4 : (D == 64 ? FL_NSLOT64 : (BIG ? 16 : 8)));
+  static constexpr int NQBUF = BIG ? 2 : 1;          // Q buffers (units it, it + 1)
   static constexpr uint32_t LAYOUT = SWB == 128 ? kLayoutSW128 : kLayoutSW64;
   static constexpr int SBO = 8 * SWB;                // 8-row (K-major) / 8-key (MN-major) group stride
   static constexpr uint32_t COL_S0 = 0, COL_S1 = 128, COL_O0 = 256, COL_O1 = 256 + D;
   static constexpr uint32_t P_OFF = 64;              // P_i at S_i + 64
   static constexpr int SMEM_Q = 0;
-  static constexpr int SMEM_RING = NQ * TILE_BYTES;
+  static constexpr int SMEM_RING = NQBUF * NQ * TILE_BYTES;
   // Small heads (D = 32, Evoformer) have shared memory to spare: the additive (pair) bias tiles come
   // through TMA into a per-warpgroup double buffer (2 slabs of 128 rows x 64 keys, 128-B swizzle).
   static constexpr bool BIAS_TMA_OK = D == 32;
   static constexpr int BIAS_TILE = 128 * 128 * 2;
   static constexpr int SMEM_BIAS = SMEM_RING + NSLOT * TILE_BYTES;
-  static constexpr int SMEM_BAR = SMEM_BIAS + (BIAS_TMA_OK ? 4 * BIAS_TILE : 0);
-  // q_full q_empty | full[NSLOT] empty[NSLOT] | s_full[2] p_full[2] o_full[2] | unit_full[2] unit_empty[2]
+  static constexpr int SMEM_BAR = SMEM_BIAS + (BIAS_TMA_OK && !BIG ? 4 * BIAS_TILE : 0);
+  // q_full[NQBUF] q_empty[NQBUF] | full[NSLOT] empty[NSLOT] | s_full[2] p_full[2] o_full[2] | unit_full[2] unit_empty[2]
   // | bias_full[4] bias_empty[4]
-  static constexpr int NBAR = 2 + 2 * NSLOT + 6 + 4 + 8;
+  static constexpr int NBAR = 2 * NQBUF + 2 * NSLOT + 6 + 4 + 8;
   static constexpr int SMEM_SCHED = SMEM_BAR + NBAR * 8 + 16;       // blocklist schedule (RSA), 2 slots
   static constexpr int SCHED_WORDS = 2 * kMaxSelTc + 8;   // schedule + meta (n, lo0, hi0, lo1, hi1, ..., unit id)
   static constexpr int KBITS_WORDS = 64;             // small heads: key-mask bits (S_k <= 2048) in the unit slot
   static constexpr int SMEM_ML = SMEM_SCHED + 2 * SCHED_WORDS * 4;      // LIST: WG1's (m, l) per row
+  // ALiBi on the tensor core (kAlibiMma): the constant A tile of ones and two per-unit B tiles of slope*c
+  // (K = 16, 32-B rows, SW32 atoms), 1024-B aligned
+  static constexpr int SMEM_AUG = (SMEM_ML + (LIST ? 2 * 128 * 4 : 0) + 1023) / 1024 * 1024;
+  static constexpr int AUG_TILE = 128 * 32;
   static constexpr int SMEM_TOTAL = SMEM_ML + (LIST ? 2 * 128 * 4 : 0) + 1024;  // + alignment slack
+  static constexpr int SMEM_TOTAL_AUG = SMEM_AUG + 3 * AUG_TILE + 1024;
   static constexpr uint32_t IDESC_S = idesc_bf16_f32(128, BN, 0);   // Q (K-major) x K (K-major)
   static constexpr uint32_t IDESC_O = idesc_bf16_f32(128, D, 1);    // P (TMEM) x V (MN-major)
   // Small heads with a TMA'd pair bias: the tensor core adds it, S += (c I) . Bias with c = 1/scale
   // split into two bf16 terms (c_hi + c_lo, relative error ~2e-7); the scaled identities live in TMEM
   // (A operand, 64 columns each, after O1) and the bias tile is the MN-major B operand (like V).
   static constexpr uint32_t COL_ID = 256 + 2 * D;
+  // Resident pair bias (unit_order 1, S_k <= 384): row r's bias for keys [0, S_k) as bf16 pairs in the
+  // 192 columns after O1 (D = 32: [320, 512)), key k at column COL_BR + k / 2 -- replaces the identity MMAs
+  static constexpr uint32_t COL_BR = 256 + 2 * D;
+  static constexpr int BR_KEYS = 2 * (512 - (256 + 2 * D));
   static constexpr uint32_t IDESC_B = idesc_bf16_f32(128, 128, 1);
   static constexpr int ENTRIES_PER_TILE = DIFF ? 3 : 2;              // K0 [K1] V
 };
@@ -162,6 +175,17 @@ struct EmuCfg {
   static constexpr uint32_t MASK = MOD == MOD_SOFTCAP ? (kSoftcapPoly ? 0u : 0x4Au) : (D <= 64 ? 0x11u : 0u);
 #endif
 };
+
+// ALiBi on the tensor core: s + (slope / scale) * c for the key index c within the tile is a rank-1 term,
+// so S_i gets it from one extra K = 16 MMA: A = ones (columns 0-2), B row c = slope*c/scale split into
+// three bf16 terms (hi + mid + lo, residual ~ |slope c / scale| 2^-24).  The per-tile remainder
+// slope * (k0 - q_abs) stays in the exp FFMA's offset (delta), so the softmax loop runs ALiBi at the
+// cost of plain attention (one FFMA per score less); 1/8 more tensor work on the S MMA.
+#ifndef FL_ALIBI_FFMA
+constexpr bool kAlibiMma = true;
+#else
+constexpr bool kAlibiMma = false;
+#endif
 
 // Ping-pong of the two softmax warpgroups' exp loops on named barriers (FA3-style).  Measured
 // slower with the persistent kernel (causal 982 vs 1071 TF/s, diff 624 vs 681): the alternation
@@ -201,7 +225,20 @@ __device__ __forceinline__ Work decode_work(const AttnParams& p, int u) {
   const int bgh = u / nqb;
   const int qb = nqb - 1 - u % nqb;
   w.h = bgh % p.Hq;
-  if (PAIR) {
+  if (PAIR && p.unit_order == 1) {
+    // resident pair bias: segment (b, h, q-block) major, G pairs minor -- a CTA's consecutive units share
+    // the bias rows it holds in TMEM; q-blocks of one head run in lockstep on sibling CTAs (K/V via L2)
+    const int ngp = (p.G + 1) >> 1;
+    const int nqb128 = (p.Sq + 127) / 128;
+    int seg = u / ngp;
+    w.g = (u % ngp) * 2;
+    w.g1 = w.g + 1;
+    const int qb128 = seg % nqb128;
+    seg /= nqb128;
+    w.h = seg % p.Hq;
+    w.b = seg / p.Hq;
+    w.q0[0] = w.q0[1] = qb128 * 128;
+  } else if (PAIR) {
     const int ngp = (p.G + 1) >> 1;
     w.g = ((bgh / p.Hq) % ngp) * 2;
     w.g1 = w.g + 1;
@@ -215,7 +252,7 @@ __device__ __forceinline__ Work decode_work(const AttnParams& p, int u) {
   w.hi_cta = 0;
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
-    w.q0[i] = (DIFF || LIST || PAIR) ? qb * 128 : qb * 256 + i * 128;
+    if (!(PAIR && p.unit_order == 1)) w.q0[i] = (DIFF || LIST || PAIR) ? qb * 128 : qb * 256 + i * 128;
     w.lo[i] = w.hi[i] = 0;
     if (!LIST && w.q0[i] < p.Sq && !(PAIR && i == 1 && w.g1 >= p.G)) {
       const int q_last = min(p.Sq, w.q0[i] + 128) - 1;
@@ -282,19 +319,24 @@ __device__ __forceinline__ int next_tile(const Work& w, int j) {
   return -1;
 }
 
-template <int D, bool DIFF, int MOD, bool BIAS, bool LIST, bool PAIR = false>
+// PAIR: 0 none, 1 paired G entries, 2 paired with the pair bias resident in TMEM (unit_order 1)
+template <int D, bool DIFF, int MOD, bool BIAS, bool LIST, int PAIR = 0>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     attn_tc_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ TmaMaps maps, int n_units) {
+#ifdef FL_BIG   // measured slower (evo_row 0.405 -> 0.423 ms, evo_col unchanged: profiles/r02_ab.md): opt-in
+  using C = TcCfg<D, DIFF, LIST, (D == 32 && !DIFF && !LIST && (!BIAS || PAIR == 2))>;
+#else
   using C = TcCfg<D, DIFF, LIST>;
+#endif
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned (SW128 atoms); offset arithmetic on smem_raw keeps the shared address space visible
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sQ = smem + C::SMEM_Q;
   uint8_t* sRing = smem + C::SMEM_RING;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::SMEM_BAR);
-  uint64_t* q_full = bars;
-  uint64_t* q_empty = bars + 1;
-  uint64_t* full = bars + 2;
+  uint64_t* q_full = bars;                           // [NQBUF]
+  uint64_t* q_empty = bars + C::NQBUF;               // [NQBUF]
+  uint64_t* full = bars + 2 * C::NQBUF;
   uint64_t* empty = full + C::NSLOT;
   uint64_t* s_full = empty + C::NSLOT;
   uint64_t* p_full = s_full + 2;
@@ -305,15 +347,13 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   uint64_t* bias_empty = bias_full + 4;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bias_empty + 4);
   uint8_t* sBias = smem + C::SMEM_BIAS;
-  const bool bias_tma = C::BIAS_TMA_OK && BIAS && maps.bias_tma;
-#ifdef FL_NO_BIAS_MMA
-  const bool bias_mma = false;
-#else
+  // resident pair bias (Evoformer rows, unit_order 1): the softmax warpgroups add it from TMEM
+  constexpr bool bias_res = C::BIAS_TMA_OK && BIAS && PAIR == 2;
+  const bool bias_tma = C::BIAS_TMA_OK && BIAS && maps.bias_tma && !bias_res;
 #ifdef FL_NO_BIAS_MMA
   const bool bias_mma = false;
 #else
   const bool bias_mma = bias_tma && MOD == MOD_NONE;  // raw-score domain: S += bias / scale on the tensor core
-#endif
 #endif
   uint32_t* sched_base = reinterpret_cast<uint32_t*>(smem + C::SMEM_SCHED);
 
@@ -321,8 +361,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   const int lane = threadIdx.x & 31;
 
   if (warp == 8 && lane == 0) {
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, DIFF ? 1 + 128 : 1);          // last S MMA of a unit (+ diff: WG0 done with xbuf)
+    for (int b = 0; b < C::NQBUF; ++b) {
+      mbar_init(&q_full[b], 1);
+      mbar_init(&q_empty[b], DIFF ? 1 + 128 : 1);    // last S MMA of a unit (+ diff: WG0 done with xbuf)
+    }
     for (int s = 0; s < C::NSLOT; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -340,6 +382,19 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       }
     }
     fence_mbar_init();
+  }
+  constexpr bool kAug = kAlibiMma && MOD == MOD_ALIBI;
+  uint8_t* sAug = smem + C::SMEM_AUG;               // [ones A | B unit parity 0 | B unit parity 1]
+  if constexpr (kAug) {
+    // A: every row [1 1 1 0 0 0 0 0 | 1 1 1 0 0 0 0 0] -- ones in BOTH 16-B chunks of the 32-B row, so A
+    // reads the same whatever the 32-B swizzle does; B (written per unit by the producer) holds its three
+    // terms in one chunk and zeros in the other, so each term is counted exactly once either way
+    for (int i = threadIdx.x; i < 3 * C::AUG_TILE / 16; i += kThreadsTc) {
+      uint4 v = make_uint4(0u, 0u, 0u, 0u);
+      if (i < C::AUG_TILE / 16) v = make_uint4(0x3F803F80u, 0x3F80u, 0u, 0u);
+      reinterpret_cast<uint4*>(sAug)[i] = v;
+    }
+    fence_proxy_async_smem();
   }
   if (warp == 9) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
@@ -385,7 +440,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   };
   // Work of the unit published in slot it & 1 (by value: keeps it in registers)
   auto unit_work = [&](int u, int it) -> Work {
-    Work w = decode_work<D, DIFF, LIST, PAIR>(p, u);
+    Work w = decode_work<D, DIFF, LIST, (PAIR != 0)>(p, u);
     if constexpr (LIST) load_sched(w, sched_base + (it & 1) * C::SCHED_WORDS);
     return w;
   };
@@ -400,7 +455,20 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       tma_prefetch_desc(&maps.k);
       tma_prefetch_desc(&maps.v);
       int e = 0, it = 0;
-      int u = blockIdx.x;
+      int u = blockIdx.x, u_end = n_units;
+      if (PAIR != 0 && p.unit_order == 1) {
+        // static contiguous chunks: with grid = n_seg * cps every segment gets cps CTAs at the same offsets
+        const int ngp = (p.G + 1) >> 1, n_seg = n_units / ngp, grid = (int)gridDim.x, c = (int)blockIdx.x;
+        if (grid >= n_seg && grid % n_seg == 0) {
+          const int cps = grid / n_seg, seg = c / cps, part = c % cps;
+          u = seg * ngp + (int)((long long)part * ngp / cps);
+          u_end = seg * ngp + (int)((long long)(part + 1) * ngp / cps);
+        } else {
+          u = (int)((long long)c * n_units / grid);
+          u_end = (int)((long long)(c + 1) * n_units / grid);
+        }
+        if (u >= u_end) u = n_units;
+      }
       int bcnt[2] = {0, 0};                            // bias tiles issued per warpgroup (stage = bcnt & 1)
       if (bias_tma) tma_prefetch_desc(&maps.bias);
       for (;; ++it) {
@@ -411,7 +479,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           mbar_arrive(&unit_full[it & 1]);             // end marker
           break;
         }
-        Work w = decode_work<D, DIFF, LIST, PAIR>(p, u);
+        Work w = decode_work<D, DIFF, LIST, (PAIR != 0)>(p, u);
         if constexpr (LIST) {
           build_sched(p, w, sc);
           load_sched(w, sc);
@@ -434,19 +502,38 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           }
         }
         mbar_arrive(&unit_full[it & 1]);               // release: id / schedule visible to the waiters
-        const int u_next = (int)gridDim.x + atomicAdd(p.tile_ctr, 1);   // latency hidden behind this unit
+        const int u_next = (PAIR != 0 && p.unit_order == 1) ? (u + 1 < u_end ? u + 1 : n_units)
+                                                       : (int)gridDim.x + atomicAdd(p.tile_ctr, 1);   // latency hidden behind this unit
         const int hkv = w.h / p.grp;
         const int g1c = min(w.g1, p.G - 1);               // PAIR with odd G: WG1 of the last pair idles
         const int gq = maps.q_bcast_g ? 0 : w.g, bq = maps.q_bcast_b ? 0 : w.b;
         const int gk = maps.k_bcast_g ? 0 : w.g, bk = maps.k_bcast_b ? 0 : w.b;
         const int gv = maps.v_bcast_g ? 0 : w.g, bv = maps.v_bcast_b ? 0 : w.b;
         const int gq1 = maps.q_bcast_g ? 0 : g1c, gk1 = maps.k_bcast_g ? 0 : g1c, gv1 = maps.v_bcast_g ? 0 : g1c;
-        if (it > 0) mbar_wait(q_empty, (it - 1) & 1);  // the previous unit's S MMAs (and diff xbuf) are done
-        mbar_arrive_expect_tx(q_full, C::NQ * C::TILE_BYTES);
+        const int qbuf = it % C::NQBUF, quse = it / C::NQBUF;
+        // the S MMAs (and diff xbuf reads) of the unit that last used this Q buffer are done
+        if (it >= C::NQBUF) mbar_wait(&q_empty[qbuf], (quse - 1) & 1);
+        if constexpr (kAug) {
+          // this unit's B tile (buffer it & 1; the S MMAs of unit it - 2 that read it are done): key c ->
+          // slope*c/scale as hi + mid + lo bf16 terms in the 16-B chunk the SW32 swizzle maps chunk 0 to
+          const float sl = (p.alibi ? p.alibi[w.h] : exp2f(-8.f * (float)(w.h + 1) / (float)p.Hq)) / p.scale;
+          uint8_t* bt = sAug + (1 + (it & 1)) * C::AUG_TILE;
+          for (int c = 0; c < 128; ++c) {
+            const float a = sl * (float)c;
+            const float hi = __bfloat162float(__float2bfloat16_rn(a));
+            const float mid = __bfloat162float(__float2bfloat16_rn(a - hi));
+            const float lo = a - hi - mid;
+            const int ch = (c >> 2) & 1;
+            *reinterpret_cast<uint2*>(bt + c * 32 + ch * 16) = make_uint2(pack_bf16(hi, mid), pack_bf16(lo, 0.f));
+            *reinterpret_cast<uint2*>(bt + c * 32 + (ch ^ 1) * 16) = make_uint2(0u, 0u);
+          }
+          fence_proxy_async_smem();                    // generic-proxy stores -> the tensor core (via q_full)
+        }
+        mbar_arrive_expect_tx(&q_full[qbuf], C::NQ * C::TILE_BYTES);
         for (int i = 0; i < C::NQ; ++i) {
           const int qh = DIFF ? w.h + i * p.Hq : w.h;
           for (int c = 0; c < C::NCH; ++c)
-            tma_load_5d(sQ + i * C::TILE_BYTES + c * C::CHUNK_BYTES, &maps.q, q_full, c * C::CH, w.q0[i], qh,
+            tma_load_5d(sQ + (qbuf * C::NQ + i) * C::TILE_BYTES + c * C::CHUNK_BYTES, &maps.q, &q_full[qbuf], c * C::CH, w.q0[i], qh,
                         i ? gq1 : gq, bq);
         }
         auto load_entry = [&](const CUtensorMap* m, int tile, int head, int gg, int bb) {
@@ -468,7 +555,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             if (n1) load_entry(&maps.k, kv_tile<LIST>(w, 1, j), hkv, gk, bk);
             load_entry(&maps.v, kv_tile<LIST>(w, 0, j), hkv, gv, bv);
             if (n1) load_entry(&maps.v, kv_tile<LIST>(w, 1, j), hkv, gv, bv);
-          } else if constexpr (PAIR) {
+          } else if constexpr (PAIR != 0) {
             // step j: K(g) [K(g+1)] V(g) [V(g+1)] -- the same KV tile of two G entries
             const bool n1 = needs(w, 1, j);
             load_entry(&maps.k, j, hkv, gk, bk);
@@ -503,7 +590,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   } else if (warp == 9) {
     // ============================== MMA issuer ==============================
     if (lane == 0) {
-      const uint32_t sq_addr = smem_u32(sQ), ring_addr = smem_u32(sRing);
+      const uint32_t ring_addr = smem_u32(sRing);
+      uint32_t sq_addr = smem_u32(sQ);                 // this unit's Q buffer
       int e = 0;
       auto acquire = [&]() -> int {
         const int slot = e % C::NSLOT;
@@ -512,6 +600,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         return slot;
       };
       int bcnt_m[2] = {0, 0};                          // bias tiles consumed per warpgroup (bias_mma)
+      const uint32_t saug_addr = smem_u32(sAug);
+      int it_mma = 0;                                  // unit counter (ALiBi B tile parity)
       const uint32_t sbias_addr = smem_u32(sBias);
       auto issue_s = [&](int i, int kslot) {
         const uint32_t qa = sq_addr + (LIST ? 0 : i) * C::TILE_BYTES, ka = ring_addr + kslot * C::TILE_BYTES;
@@ -521,6 +611,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           umma_ss(tmem + (i ? C::COL_S1 : C::COL_S0), smem_desc(qa + off, 16, C::SBO, C::LAYOUT),
                   smem_desc(ka + off, 16, C::SBO, C::LAYOUT), C::IDESC_S, kk > 0);
         }
+        if constexpr (kAug)                            // S_i += ones . (slope c / scale)^T (ALiBi, rank 1)
+          umma_ss(tmem + (i ? C::COL_S1 : C::COL_S0), smem_desc(saug_addr, 16, 256, kLayoutSW32),
+                  smem_desc(saug_addr + (1 + (it_mma & 1)) * C::AUG_TILE, 16, 256, kLayoutSW32), C::IDESC_S, 1u);
         if (bias_mma) {                                // S_i += (c_hi I + c_lo I) . Bias tile
           const int st = bcnt_m[i] & 1;
           mbar_wait(&bias_full[i * 2 + st], (bcnt_m[i] >> 1) & 1);
@@ -558,22 +651,26 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         const int u = get_unit(it);
         if (u >= n_units) break;
         const Work w = unit_work(u, it);
+        it_mma = it;
         first_pv[0] = first_pv[1] = true;
         int j = next_tile(w, w.lo_cta - 1);
-        mbar_wait(q_full, it & 1);                     // always: Q of this unit has landed
+        const int qbuf = it % C::NQBUF;
+        uint64_t* q_empty_u = &q_empty[qbuf];
+        sq_addr = smem_u32(sQ) + qbuf * C::NQ * C::TILE_BYTES;
+        mbar_wait(&q_full[qbuf], (it / C::NQBUF) & 1);  // always: Q of this unit has landed
         tc_fence_after();
         if (j >= 0) {
           // K of warpgroup 1 is a separate ring entry for diff (map 1) and block lists (its own tile);
           // V is separate for block lists only.  Entries a warpgroup does not need are not loaded.
-          constexpr bool kSepK = DIFF || LIST || PAIR;
-          constexpr bool kSepV = LIST || PAIR;
+          constexpr bool kSepK = DIFF || LIST || PAIR != 0;
+          constexpr bool kSepV = LIST || PAIR != 0;
           int ks0 = acquire();
           int ks1 = kSepK ? ((!kSepV || needs(w, 1, j)) ? acquire() : -1) : ks0;
           if (needs(w, 0, j)) issue_s(0, ks0);
           if (needs(w, 1, j)) issue_s(1, ks1);
           umma_commit(&empty[ks0]);
           if (kSepK && ks1 >= 0) umma_commit(&empty[ks1]);
-          if (next_tile(w, j) < 0) umma_commit(q_empty);   // Q is free once the last S MMA is done
+          if (next_tile(w, j) < 0) umma_commit(q_empty_u);   // Q is free once the last S MMA is done
           while (j >= 0) {
             const int va = acquire();
             const int vb = kSepV ? (needs(w, 1, j) ? acquire() : -1) : va;
@@ -598,12 +695,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
               if (needs(w, 1, jn)) issue_s(1, kn1);
               umma_commit(&empty[kn0]);
               if (kSepK && kn1 >= 0) umma_commit(&empty[kn1]);
-              if (next_tile(w, jn) < 0) umma_commit(q_empty);
+              if (next_tile(w, jn) < 0) umma_commit(q_empty_u);
             }
             j = jn;
           }
         } else {
-          umma_commit(q_empty);
+          umma_commit(q_empty_u);
         }
         release_unit(it);
       }
@@ -640,6 +737,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     int b_cnt = 0;                                   // bias tiles consumed (TMA path)
     bool pp_started = false;                         // ping-pong: first common tile of the CTA's life seen
     bool o_lent = false;                             // LIST, WG1: O1 / (m, l) still being read by WG0
+    int res_seg = -1;                                // bias_res: segment whose bias rows TMEM holds
     int it = 0;
     for (;; ++it) {
     const int u = get_unit(it);
@@ -663,6 +761,53 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     const bool kb_staged =
         !LIST && C::BIAS_TMA_OK && kbits && p.keybits_words <= (PAIR ? C::KBITS_WORDS / 2 : C::KBITS_WORDS);
     FL_T(12);                                        // 12: unit setup (work decode, key-mask staging)
+    // the gate row (64 B at c = 32) is pulled into L1 now, three or more tiles before the epilogue reads it
+    if (D <= 32 && p.gate_mode != GATE_NONE && row_valid)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(static_cast<const unsigned short*>(p.gate) + w.b * p.gs.b +
+                                                   gw * p.gs.g + (int64_t)w.h * p.gs.h + (int64_t)q * p.gs.s)
+                   : "memory");
+    if constexpr (bias_res) {
+      // resident pair bias: on a new (b, h, q-block) segment both warpgroups refill the row's bias in TMEM
+      // (WG0 keys [0, BR_KEYS/2), WG1 the rest), between two barriers so no tile reads a half-written row
+      const int seg = u / ((p.G + 1) >> 1);
+      if (seg != res_seg) {
+        if (res_seg >= 0) named_bar_sync(6, 256);   // both warpgroups are done with the old rows
+        const unsigned short* brow = static_cast<const unsigned short*>(p.bias) + w.b * p.bs.b +
+                                     (int64_t)w.h * p.bs.h + (int64_t)(q < p.Sq ? q : 0) * p.bs.s;
+#pragma unroll 1
+        for (int ch = 0; ch < C::BR_KEYS / 2 / 64; ++ch) {
+          const int kb0 = wg * (C::BR_KEYS / 2) + ch * 64;
+          uint32_t bv[32];
+#pragma unroll
+          for (int t8 = 0; t8 < 8; ++t8) {
+            const int k8 = kb0 + t8 * 8;
+            uint4 v4 = make_uint4(0u, 0u, 0u, 0u);
+            if (q < p.Sq) {
+              if (k8 + 8 <= p.Sk) {
+                v4 = __ldg(reinterpret_cast<const uint4*>(brow + k8));
+              } else {
+                uint32_t e2[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                  e2[t] = (k8 + 2 * t < p.Sk ? (uint32_t)brow[k8 + 2 * t] : 0u) |
+                          ((k8 + 2 * t + 1 < p.Sk ? (uint32_t)brow[k8 + 2 * t + 1] : 0u) << 16);
+                v4 = make_uint4(e2[0], e2[1], e2[2], e2[3]);
+              }
+            }
+            bv[4 * t8] = v4.x;
+            bv[4 * t8 + 1] = v4.y;
+            bv[4 * t8 + 2] = v4.z;
+            bv[4 * t8 + 3] = v4.w;
+          }
+          tmem_st32(tmem + lane_base + C::COL_BR + (kb0 >> 1), bv);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        named_bar_sync(6, 256);
+        tc_fence_after();
+        res_seg = seg;
+      }
+    }
     const unsigned char* bias_row = nullptr;
     if (BIAS)
       bias_row = static_cast<const unsigned char*>(p.bias) +
@@ -721,7 +866,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         float v = __uint_as_float(s[c]);
         if (kCapFirst) {
           // raw score: tanh after the row max (exp loop)
-        } else if (MOD == MOD_ALIBI) {
+        } else if (MOD == MOD_ALIBI && !kAug) {
           v = fmaf(slope_r, (float)c, v);
         } else if (!kRaw) {
           v *= sc_l2;
@@ -729,6 +874,19 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         x[c] = v;
       }
       if (BIAS && !bias_mma) {  // additive bias (Evoformer pair bias), then softcap if any (order G16)
+        if constexpr (bias_res) {
+          // this row's bias for the tile's keys: 64 TMEM columns of bf16 pairs
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            uint32_t bw[32];
+            tmem_ld32(tmem + lane_base + C::COL_BR + (k0 >> 1) + h2 * 32, bw);
+            tmem_wait_ld();
+#pragma unroll
+            for (int t = 0; t < 32; ++t)
+              ffma2(x[h2 * 64 + 2 * t], x[h2 * 64 + 2 * t + 1], bf16_lo(bw[t]), bf16_hi(bw[t]), bias_k, bias_k,
+                    x[h2 * 64 + 2 * t], x[h2 * 64 + 2 * t + 1]);
+          }
+        } else {
         if (bias_tma) {
           // this row of the bias tile from shared memory: slab c holds keys [64c, 64c+64), 16-byte
           // chunk k of row r at (k ^ (r & 7)) -- the TMA 128-B swizzle, so 8 consecutive rows hit
@@ -807,6 +965,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             x[c] = fmaf(bv, bias_k, x[c]);
           }
         }
+        }
         if (MOD == MOD_SOFTCAP) {
 #pragma unroll
           for (int c = 0; c < 128; ++c) x[c] = cap_out * tanh_approx(x[c] * (kLn2 / p.softcap));
@@ -877,30 +1036,14 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         pp_started = true;
       }
       FL_T(5);                                         // 5: ping-pong wait
-      if (kCapFirst) {                                 // x = tanh(a s); masked (-inf) scores stay -inf
-        if (poly) {
-#pragma unroll
-          for (int c = 0; c < 128; c += 2) {           // -inf: u = +inf, P = +inf (tc4 > 0), x = -inf
-            float u0, u1, p0, p1;
-            fmul2(u0, u1, x[c], x[c + 1], x[c], x[c + 1]);
-            ffma2(p0, p1, u0, u1, tc4, tc4, tc3, tc3);
-            ffma2(p0, p1, p0, p1, u0, u1, tc2, tc2);
-            ffma2(p0, p1, p0, p1, u0, u1, tc1, tc1);
-            ffma2(p0, p1, p0, p1, u0, u1, tc0, tc0);
-            fmul2(x[c], x[c + 1], p0, p1, x[c], x[c + 1]);
-          }
-        } else {
-#pragma unroll
-          for (int c = 0; c < 128; ++c) x[c] = x[c] == -INFINITY ? -INFINITY : tanh_approx(x[c] * cap_in);
-        }
-      }
       float ls0 = 0.f, ls1 = 0.f, ls2 = 0.f, ls3 = 0.f;
       uint32_t pk[64];
-#pragma unroll
-      for (int c = 0; c < 128; c += 4) {
+      // P for scores c..c+3 given their (modified) log2-domain values: exp FFMA, ex2 (MUFU or FMA-pipe
+      // emulation), row-sum, bf16 pack
+      auto exp4 = [&](const int c, float v0, float v1, float v2, float v3) {
         float a0, a1, a2, a3;
-        ffma2(a0, a1, x[c], x[c + 1], xscale, xscale, neg_m, neg_m);
-        ffma2(a2, a3, x[c + 2], x[c + 3], xscale, xscale, neg_m, neg_m);
+        ffma2(a0, a1, v0, v1, xscale, xscale, neg_m, neg_m);
+        ffma2(a2, a3, v2, v3, xscale, xscale, neg_m, neg_m);
         if ((EmuCfg<D, MOD>::MASK >> ((c >> 2) & 7)) & 1u) {
           ex2_emu2(a0, a1);
           ex2_emu2(a2, a3);
@@ -914,6 +1057,47 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         fadd2(ls2, ls3, ls2, ls3, a2, a3);
         pk[c >> 1] = pack_bf16(a0, a1);
         pk[(c >> 1) + 1] = pack_bf16(a2, a3);
+      };
+      // tanh(a s) of a pair on the FMA pipe; -inf: u = +inf, P = +inf (tc4 > 0), result -inf
+      auto tanh_poly2 = [&](float& v0, float& v1) {
+        float u0, u1, p0, p1;
+        fmul2(u0, u1, v0, v1, v0, v1);
+        ffma2(p0, p1, u0, u1, tc4, tc4, tc3, tc3);
+        ffma2(p0, p1, p0, p1, u0, u1, tc2, tc2);
+        ffma2(p0, p1, p0, p1, u0, u1, tc1, tc1);
+        ffma2(p0, p1, p0, p1, u0, u1, tc0, tc0);
+        fmul2(v0, v1, p0, p1, v0, v1);
+      };
+      if (kCapFirst && kSoftcapPoly && poly) {
+        // software-pipelined: the FMA-pipe tanh of scores c+4..c+7 is issued before the MUFU ex2 of
+        // c..c+3, so the polynomial runs under the exp loop instead of as a pass before it
+        float t0 = x[0], t1 = x[1], t2 = x[2], t3 = x[3];
+        tanh_poly2(t0, t1);
+        tanh_poly2(t2, t3);
+#pragma unroll
+        for (int c = 0; c < 128; c += 4) {
+          float n0 = 0.f, n1 = 0.f, n2 = 0.f, n3 = 0.f;
+          if (c + 4 < 128) {
+            n0 = x[c + 4];
+            n1 = x[c + 5];
+            n2 = x[c + 6];
+            n3 = x[c + 7];
+            tanh_poly2(n0, n1);
+            tanh_poly2(n2, n3);
+          }
+          exp4(c, t0, t1, t2, t3);
+          t0 = n0;
+          t1 = n1;
+          t2 = n2;
+          t3 = n3;
+        }
+      } else {
+        if (kCapFirst) {                               // x = tanh(a s) on the MUFU; -inf stays -inf
+#pragma unroll
+          for (int c = 0; c < 128; ++c) x[c] = x[c] == -INFINITY ? -INFINITY : tanh_approx(x[c] * cap_in);
+        }
+#pragma unroll
+        for (int c = 0; c < 128; c += 4) exp4(c, x[c], x[c + 1], x[c + 2], x[c + 3]);
       }
       FL_T(6);                                         // 6: exp loop
       if (common) {
@@ -945,9 +1129,6 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 #endif
     const uint4* gp = reinterpret_cast<const uint4*>(static_cast<const unsigned short*>(p.gate) + w.b * p.gs.b +
                                                      gw * p.gs.g + (int64_t)w.h * p.gs.h + (int64_t)q * p.gs.s);
-    // the gate row (64 B at c = 32) is pulled into L1 while the last PV runs; holding it in registers
-    // made the compiler spill it right after the load (the spill store then waited for the load)
-    if (D <= 32 && gated) asm volatile("prefetch.global.L1 [%0];" ::"l"(gp) : "memory");
     if (n_done > 0) {
       mbar_wait(&o_full[wg], o_cnt & 1);
       ++o_cnt;
@@ -1154,6 +1335,15 @@ __global__ void sched_dump_kernel(const __grid_constant__ AttnParams p, int n_un
   }
 }
 
+// Small-head pairing (Evoformer rows: S_q leaves half of a 256-row unit empty) and the resident pair bias
+// (bf16, key-contiguous, broadcast over G, S_k within the free TMEM columns, raw-score domain).
+static inline bool small_head_pair(const AttnParams& p) {
+  return p.Dqk == 32 && p.maps == 1 && p.mask != MASK_BLOCKLIST && p.G >= 2 && p.Sq % 256 != 0 && p.Sq % 256 <= 128;
+}
+static inline bool bias_resident(const AttnParams& p) {
+  return p.bias && p.bias_vec && p.bs.g == 0 && p.Sk <= TcCfg<32, false>::BR_KEYS && p.mod == MOD_NONE;
+}
+
 static inline int num_sms() {
   int dev = 0;
   cudaGetDevice(&dev);
@@ -1172,21 +1362,38 @@ static cudaError_t launch_one(const AttnParams& p, const TmaMaps& maps, cudaStre
   const bool list = p.mask == MASK_BLOCKLIST;
   // small heads whose S_q leaves half of the last 256-row unit empty (Evoformer rows): pair G entries
   bool pair = false;
+  AttnParams pp = p;
   if constexpr (D == 32 && !DIFF) {
-    if (!list && p.G >= 2 && p.Sq % 256 != 0 && p.Sq % 256 <= 128) {
+    if (small_head_pair(p)) {
       pair = true;
-      kern = p.bias ? attn_tc_kernel<D, false, MOD, true, false, true> : attn_tc_kernel<D, false, MOD, false, false, true>;
+      kern = p.bias ? attn_tc_kernel<D, false, MOD, true, false, 1> : attn_tc_kernel<D, false, MOD, false, false, 1>;
+      if constexpr (MOD == MOD_NONE) {
+        if (bias_resident(p)) {
+          pp.unit_order = 1;
+          kern = attn_tc_kernel<D, false, MOD, true, false, 2>;
+        }
+      }
     }
   }
-  const int smem_bytes = list ? TcCfg<D, false, true>::SMEM_TOTAL : TcCfg<D, DIFF>::SMEM_TOTAL;
+  const int smem_bytes = (kAlibiMma && MOD == MOD_ALIBI) ? (list ? TcCfg<D, false, true>::SMEM_TOTAL_AUG
+                                                                  : TcCfg<D, DIFF>::SMEM_TOTAL_AUG)
+                       : list ? TcCfg<D, false, true>::SMEM_TOTAL
+#ifdef FL_BIG
+                       : D == 32 ? std::max(TcCfg<D, DIFF>::SMEM_TOTAL, TcCfg<D, DIFF, false, true>::SMEM_TOTAL)
+#endif
+                                 : TcCfg<D, DIFF>::SMEM_TOTAL;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
   if (e != cudaSuccess) return e;
   const int rows_per_unit = (DIFF || list || pair) ? 128 : 256;
   const long long units = (long long)p.B * (pair ? (p.G + 1) / 2 : p.G) * p.Hq * ((p.Sq + rows_per_unit - 1) / rows_per_unit);
   if (units >= (1ll << 31)) return cudaErrorInvalidValue;
   // persistent: one CTA per SM (TMEM and shared memory admit one), each walks units with stride grid
-  const int grid = (int)std::min<long long>(units, num_sms());
-  kern<<<grid, kThreadsTc, smem_bytes, stream>>>(p, maps, (int)units);
+  int grid = (int)std::min<long long>(units, num_sms());
+  if (pp.unit_order == 1) {                          // static chunks: cps CTAs per (b, h, q-block) segment
+    const int n_seg = (int)(units / ((p.G + 1) / 2));
+    grid = n_seg <= num_sms() ? n_seg * (num_sms() / n_seg) : num_sms();
+  }
+  kern<<<grid, kThreadsTc, smem_bytes, stream>>>(pp, maps, (int)units);
   return cudaGetLastError();
 }
 

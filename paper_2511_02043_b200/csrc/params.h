@@ -49,6 +49,9 @@ struct AttnParams {
   const int32_t* page_table; int64_t page_stride;
   int32_t in_dtype;        // 0 bf16, 1 f32
   int32_t* tile_ctr;       // bf16 path: persistent-scheduler ticket counter (workspace, zeroed per call)
+  // bf16 small heads (attn_tc.cuh): 0 = (b, g, h)-major units claimed by tickets; 1 = pair bias resident in
+  // TMEM (Evoformer rows): (b, h, q-block) segments with the G pairs minor, static contiguous chunks per CTA
+  int32_t unit_order;
 };
 
 // lambda of head h (Listing 4's lambda_full, G8): re-parameterised from lambda_qk when given (NEXT-2:

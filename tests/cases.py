@@ -149,7 +149,13 @@ def evoformer(case: dict):
 
 
 def to_dev(x, dev):
+    """Copy to the device keeping broadcast (stride-0) dims broadcast: .to() would materialise an
+    expanded tensor, and the kernels take different paths for a broadcast bias (resident pair bias)."""
     if torch.is_tensor(x):
+        bdims = [i for i, (n, st) in enumerate(zip(x.shape, x.stride())) if st == 0 and n > 1]
+        if bdims:
+            sl = tuple(slice(0, 1) if i in bdims else slice(None) for i in range(x.dim()))
+            return x[sl].to(dev).expand(x.shape)
         return x.to(dev)
     return x
 

@@ -190,11 +190,14 @@ def test_evoformer(fl, kind, dtype):
     check(out.cpu().double().reshape(ref.shape), ref, TOL[dtype], what=f"evoformer {kind} {dtype}")
 
 
-@pytest.mark.parametrize("Ns,Nr", [(25, 300), (7, 130), (3, 384), (2, 200)])
-def test_evoformer_row_pairs(fl, Ns, Nr):
+@pytest.mark.parametrize("B,Ns,Nr", [(1, 25, 300), (1, 7, 130), (1, 3, 384), (1, 2, 200), (1, 9, 640), (2, 6, 257),
+                                     (2, 3, 100)])
+def test_evoformer_row_pairs(fl, B, Ns, Nr):
     """Row attention at S_q % 256 <= 128 runs the paired-G kernel (two MSA rows per unit): odd G (last
-    pair half empty), several query tiles, ragged tails; S_q % 256 > 128 keeps the 256-row units."""
-    case = dict(kind="row", B=1, Ns=Ns, Nr=Nr, H=2, c=32, p_zero=0.1, dtype="bf16", seed=Ns)
+    pair half empty), several query tiles, ragged tails; S_q % 256 > 128 keeps the 256-row units.  Up to
+    N_res = 384 the pair bias is resident in TMEM (static segment schedule, bias refilled per (b, h,
+    q-block)); N_res = 640 keeps the TMA'd bias tiles."""
+    case = dict(kind="row", B=B, Ns=Ns, Nr=Nr, H=2, c=32, p_zero=0.1, dtype="bf16", seed=Ns)
     ins, gk, ok = cases.evoformer(case)
     out = cases.run_gpu(fl, ins, gk)
     ref, _ = cases.run_oracle(ins, ok)

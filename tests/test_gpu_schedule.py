@@ -87,7 +87,7 @@ def test_schedule_dump_matches_keep_predicate(fl, case):
     assert waste == 0, f"{waste} run tiles hold no kept key"
 
 
-@pytest.mark.parametrize("Ns,Nr,kind", [(5, 130, "row"), (4, 384, "row"), (3, 200, "col")])
+@pytest.mark.parametrize("Ns,Nr,kind", [(5, 130, "row"), (4, 384, "row"), (7, 300, "row"), (3, 200, "col")])
 def test_schedule_dump_evoformer_views(fl, Ns, Nr, kind):
     """Rank-5 strided views and the paired-G units (PAIR: two MSA rows per unit when S_q % 256 <= 128)."""
     ins, gk, ok = cases.evoformer(dict(kind=kind, B=1, Ns=Ns, Nr=Nr, H=2, c=32, p_zero=0.0))
