@@ -104,7 +104,10 @@ struct TcCfg {
 #ifndef FL_NSLOT64
 #define FL_NSLOT64 6
 #endif
-  static constexpr int NSLOT = LIST ? (D == 128 ? 5 : 8) : (D == 128 ? 4 : (D == 64 ? FL_NSLOT64 : (BIG ? 16 : 8)));
+#ifndef FL_BIG_NSLOT
+#define FL_BIG_NSLOT 8
+#endif
+  static constexpr int NSLOT = LIST ? (D == 128 ? 5 : 8) : (D == 128 ? 4 : (D == 64 ? FL_NSLOT64 : (BIG ? FL_BIG_NSLOT : 8)));
   static constexpr int NQBUF = BIG ? 2 : 1;          // Q buffers (units it, it + 1)
   static constexpr uint32_t LAYOUT = SWB == 128 ? kLayoutSW128 : kLayoutSW64;
   static constexpr int SBO = 8 * SWB;                // 8-row (K-major) / 8-key (MN-major) group stride
@@ -117,7 +120,8 @@ struct TcCfg {
   static constexpr bool BIAS_TMA_OK = D == 32;
   static constexpr int BIAS_TILE = 128 * 128 * 2;
   static constexpr int SMEM_BIAS = SMEM_RING + NSLOT * TILE_BYTES;
-  static constexpr int SMEM_BAR = SMEM_BIAS + (BIAS_TMA_OK && !BIG ? 4 * BIAS_TILE : 0);
+  static constexpr bool BIAS_AREA = BIAS_TMA_OK && !BIG;   // bias tiles, else (unused) the small-head gate rows
+  static constexpr int SMEM_BAR = SMEM_BIAS + (BIAS_AREA ? 4 * BIAS_TILE : 0);
   // q_full[NQBUF] q_empty[NQBUF] | full[NSLOT] empty[NSLOT] | s_full[2] p_full[2] o_full[2] | unit_full[2] unit_empty[2]
   // | bias_full[4] bias_empty[4]
   static constexpr int NBAR = 2 * NQBUF + 2 * NSLOT + 6 + 4 + 8;
@@ -717,6 +721,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     const int r = threadIdx.x & 127;                 // row within the tile == TMEM lane
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     const uint32_t col_s = wg ? C::COL_S1 : C::COL_S0;
+    // small heads without TMA'd bias tiles: the bias-tile area holds each thread's 64-B gate row
+    const bool gate_async = D <= 32 && C::BIAS_AREA && !bias_tma && p.gate_mode != GATE_NONE && !(DIFF && wg == 1);
+    uint8_t* sGateRow = sBias + (wg * 128 + r) * 64;
     const uint32_t col_o = wg ? C::COL_O1 : C::COL_O0;
     const float sc_l2 = p.scale * kLog2e;
     const float cap_in = MOD == MOD_SOFTCAP ? p.scale / p.softcap : 0.f;   // s*scale/cap
@@ -761,11 +768,16 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     const bool kb_staged =
         !LIST && C::BIAS_TMA_OK && kbits && p.keybits_words <= (PAIR ? C::KBITS_WORDS / 2 : C::KBITS_WORDS);
     FL_T(12);                                        // 12: unit setup (work decode, key-mask staging)
-    // the gate row (64 B at c = 32) is pulled into L1 now, three or more tiles before the epilogue reads it
-    if (D <= 32 && p.gate_mode != GATE_NONE && row_valid)
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(static_cast<const unsigned short*>(p.gate) + w.b * p.gs.b +
-                                                   gw * p.gs.g + (int64_t)w.h * p.gs.h + (int64_t)q * p.gs.s)
-                   : "memory");
+    // small heads: the gate row (64 B at c = 32) is copied by cp.async into this thread's slot of the
+    // (otherwise unused) bias-tile area now, tiles before the epilogue reads it (an L1 prefetch here, or
+    // loads issued in the epilogue, left the first use of the gate stalled: 5 % of the ncu samples)
+    if (gate_async && row_valid) {
+      const uint4* gsrc = reinterpret_cast<const uint4*>(static_cast<const unsigned short*>(p.gate) + w.b * p.gs.b +
+                                                         gw * p.gs.g + (int64_t)w.h * p.gs.h + (int64_t)q * p.gs.s);
+#pragma unroll
+      for (int t8 = 0; t8 < 4; ++t8) cp_async_16(sGateRow + ((t8 ^ (r & 3)) << 4), gsrc + t8);
+      cp_async_commit();
+    }
     if constexpr (bias_res) {
       // resident pair bias: on a new (b, h, q-block) segment both warpgroups refill the row's bias in TMEM
       // (WG0 keys [0, BR_KEYS/2), WG1 the rest), between two barriers so no tile reads a half-written row
@@ -1253,8 +1265,14 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         }
         if (gated) {
           uint4 g4[4];
+          if (gate_async) {                            // staged by cp.async at the unit's start
+            cp_async_wait_all();
 #pragma unroll
-          for (int t8 = 0; t8 < 4; ++t8) g4[t8] = __ldg(gp + (c >> 3) + t8);
+            for (int t8 = 0; t8 < 4; ++t8) g4[t8] = reinterpret_cast<const uint4*>(sGateRow)[t8 ^ (r & 3)];
+          } else {
+#pragma unroll
+            for (int t8 = 0; t8 < 4; ++t8) g4[t8] = __ldg(gp + (c >> 3) + t8);
+          }
 #pragma unroll
           for (int t8 = 0; t8 < 4; ++t8) {
             const uint4 u4 = g4[t8];

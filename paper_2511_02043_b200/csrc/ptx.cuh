@@ -101,6 +101,12 @@ FL_DEVICE void tma_store_5d(const void* tmap, const void* smem_src, int c0, int 
 FL_DEVICE void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 FL_DEVICE void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 FL_DEVICE void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// 16-byte global -> shared asynchronous copy (LDGSTS, bypassing L1), completion by commit / wait groups
+FL_DEVICE void cp_async_16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+FL_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+FL_DEVICE void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 FL_DEVICE void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // ------------------------------------------------------------------ tcgen05
