@@ -85,6 +85,9 @@ def lib():
         _lib.flo_attn_bwd.argtypes = [C.POINTER(_Problem), C.POINTER(_Tensor), C.POINTER(C.c_double),
                                       C.POINTER(C.c_double), C.POINTER(C.c_double)]
         _lib.flo_attn_bwd.restype = C.c_int
+        dp = C.POINTER(C.c_double)
+        _lib.flo_linear_ln.argtypes = [C.c_int64, C.c_int64, C.c_int64, dp, dp, dp, dp, dp, C.c_double, dp, dp]
+        _lib.flo_linear_ln.restype = C.c_int
     return _lib
 
 
@@ -307,3 +310,28 @@ def rsa_select(q, k, *, blk_q=128, blk_k=128, topk=16, causal_align=0, max_sel=N
     if rc != 0:
         raise ValueError(f"flo_rsa_select failed ({rc})")
     return idx, cnt, sc
+
+
+def linear_ln(x, w, bias=None, ln_gamma=None, ln_beta=None, eps=1e-5, with_abs=False):
+    """NEXT-2 oracle (fl_oracle.c flo_linear_ln): y = [LayerNorm(x)] w^T + bias in fp64.  x [..., K],
+    w [N, K]; returns y [..., N] (and yabs = sum_k |xhat| |w| when with_abs)."""
+    xt = torch.as_tensor(x).double().reshape(-1, np.shape(x)[-1]).contiguous()
+    wt = torch.as_tensor(w).double().contiguous()
+    M, K = xt.shape
+    N = wt.shape[0]
+    keep = []
+
+    def ptr(a):
+        if a is None:
+            return None
+        arr = np.ascontiguousarray(torch.as_tensor(a).double().numpy(), dtype=np.float64)
+        keep.append(arr)
+        return arr.ctypes.data_as(C.POINTER(C.c_double))
+    y = np.empty((M, N), dtype=np.float64)
+    ya = np.empty((M, N), dtype=np.float64) if with_abs else None
+    rc = lib().flo_linear_ln(M, N, K, ptr(xt), ptr(wt), ptr(bias), ptr(ln_gamma), ptr(ln_beta), float(eps),
+                             y.ctypes.data_as(C.POINTER(C.c_double)),
+                             ya.ctypes.data_as(C.POINTER(C.c_double)) if with_abs else None)
+    assert rc == 0, rc
+    shp = tuple(np.shape(x)[:-1]) + (N,)
+    return (y.reshape(shp), ya.reshape(shp)) if with_abs else y.reshape(shp)

@@ -468,3 +468,45 @@ int flo_num_threads(void) {
   return 1;
 #endif
 }
+
+/* SURVEY §8(f) NEXT-2, the memory passes on either side of the attention kernel (Flashlight fuses
+ * "complex element-wise prologues", §3.1; the Evoformer row attention of the paper's second
+ * workload, is AF2 Alg.7: line 1 m <- LayerNorm(m), lines 2-4 q, k, v, g = Linear(m), line 7
+ * the output Linear).  Written out as defined, fp64, in this order per row m:
+ *   mean = (1/K) sum_k x[m,k];  var = (1/K) sum_k (x[m,k] - mean)^2          (LayerNorm, biased variance)
+ *   xhat[k] = (x[m,k] - mean) / sqrt(var + eps) * gamma[k] + beta[k]        (gamma == NULL: xhat = x[m,:];
+ *                                                                           beta == NULL: beta = 0)
+ *   y[m,n] = sum_k xhat[k] w[n,k] + bias[n]                                 (bias == NULL: 0)
+ *   yabs[m,n] = sum_k |xhat[k]| |w[n,k]|   (if yabs != NULL: the scale the tests derive a rounding bound from)
+ * x [M][K], w [N][K], y / yabs [M][N], all contiguous fp64. */
+int flo_linear_ln(int64_t M, int64_t N, int64_t K, const double* x, const double* w, const double* bias,
+                  const double* gamma, const double* beta, double eps, double* y, double* yabs) {
+  if (M < 0 || N < 1 || K < 1) return -1;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t m = 0; m < M; ++m) {
+    double* xhat = (double*)malloc(sizeof(double) * K);
+    const double* xr = x + m * K;
+    if (gamma) {
+      double mean = 0.0, var = 0.0;
+      for (int64_t k = 0; k < K; ++k) mean += xr[k];
+      mean /= (double)K;
+      for (int64_t k = 0; k < K; ++k) var += (xr[k] - mean) * (xr[k] - mean);
+      var /= (double)K;
+      const double inv = 1.0 / sqrt(var + eps);
+      for (int64_t k = 0; k < K; ++k) xhat[k] = (xr[k] - mean) * inv * gamma[k] + (beta ? beta[k] : 0.0);
+    } else {
+      for (int64_t k = 0; k < K; ++k) xhat[k] = xr[k];
+    }
+    for (int64_t n = 0; n < N; ++n) {
+      double acc = 0.0, aabs = 0.0;
+      for (int64_t k = 0; k < K; ++k) {
+        acc += xhat[k] * w[n * K + k];
+        aabs += fabs(xhat[k]) * fabs(w[n * K + k]);
+      }
+      y[m * N + n] = acc + (bias ? bias[n] : 0.0);
+      if (yabs) yabs[m * N + n] = aabs;
+    }
+    free(xhat);
+  }
+  return 0;
+}

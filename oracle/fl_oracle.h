@@ -111,4 +111,7 @@ int flo_num_threads(void);
 #ifdef __cplusplus
 }
 #endif
+/* NEXT-2: y = [LayerNorm(x)] w^T + bias (see fl_oracle.c). */
+int flo_linear_ln(int64_t M, int64_t N, int64_t K, const double* x, const double* w, const double* bias,
+                  const double* gamma, const double* beta, double eps, double* y, double* yabs);
 #endif

@@ -626,3 +626,61 @@ def test_backward_matches_torch_autograd_listing1():
     np.testing.assert_allclose(dq, qt.grad.numpy(), rtol=1e-10, atol=1e-12)
     np.testing.assert_allclose(dk, kt.grad.numpy(), rtol=1e-10, atol=1e-12)
     np.testing.assert_allclose(dv, vt.grad.numpy(), rtol=1e-10, atol=1e-12)
+
+
+# ---------------------------------------------------------------- NEXT-2: LayerNorm-prologue linear
+def _ln_case(M=37, K=128, N=48, seed=3):
+    g = torch.Generator().manual_seed(seed)
+    x = torch.rand(M, K, generator=g, dtype=torch.float64) * 4 - 2
+    w = (torch.rand(N, K, generator=g, dtype=torch.float64) * 2 - 1) / np.sqrt(K)
+    gam = torch.rand(K, generator=g, dtype=torch.float64) + 0.5
+    bet = torch.rand(K, generator=g, dtype=torch.float64) - 0.5
+    bias = torch.rand(N, generator=g, dtype=torch.float64) - 0.5
+    return x, w, gam, bet, bias
+
+
+def test_linear_ln_plain_is_matmul():
+    """No LayerNorm: y = x w^T + bias, the library matmul (special case that is a library routine)."""
+    x, w, _, _, bias = _ln_case()
+    y = oracle.linear_ln(x, w, bias=bias)
+    assert np.abs(y - (x.numpy() @ w.numpy().T + bias.numpy())).max() < 1e-12
+
+
+def test_linear_ln_matches_torch_layer_norm():
+    """LayerNorm prologue (AF2 Alg.7 line 1): torch.nn.functional.layer_norm (biased variance, eps inside
+    the square root) followed by the product."""
+    x, w, gam, bet, bias = _ln_case()
+    y = oracle.linear_ln(x, w, bias=bias, ln_gamma=gam, ln_beta=bet, eps=1e-5)
+    ref = torch.nn.functional.layer_norm(x, (x.shape[1],), gam, bet, 1e-5) @ w.T + bias
+    assert np.abs(y - ref.numpy()).max() < 1e-11
+
+
+def test_linear_ln_invariants():
+    """With gamma = 1, beta = 0 and w = I: every output row has mean 0 and variance var / (var + eps)
+    (closed form); LayerNorm is invariant under x -> a x + c for a > 0 up to eps; a constant row
+    normalises to beta (so y = w beta + bias)."""
+    x, _, _, bet, _ = _ln_case(K=64, N=64)
+    K = x.shape[1]
+    eye = torch.eye(K, dtype=torch.float64)
+    ones = torch.ones(K, dtype=torch.float64)
+    y = oracle.linear_ln(x, eye, ln_gamma=ones, eps=1e-5)
+    var = x.var(dim=1, unbiased=False).numpy()
+    assert np.abs(y.mean(axis=1)).max() < 1e-12
+    assert np.abs(y.var(axis=1) - var / (var + 1e-5)).max() < 1e-12
+    y0 = oracle.linear_ln(x, eye, ln_gamma=ones, eps=0.0)
+    y1 = oracle.linear_ln(3.5 * x - 1.25, eye, ln_gamma=ones, eps=0.0)
+    assert np.abs(y0 - y1).max() < 1e-12
+    xc = torch.full((2, K), 0.7, dtype=torch.float64)
+    _, w, _, _, bias = _ln_case(K=K, N=5)
+    yc = oracle.linear_ln(xc, w, bias=bias, ln_gamma=ones, ln_beta=bet, eps=1e-5)
+    assert np.abs(yc - (w.numpy() @ bet.numpy() + bias.numpy())).max() < 1e-12
+
+
+def test_linear_ln_abs_scale():
+    """yabs = sum_k |xhat| |w| bounds |y - bias| (triangle inequality) and equals it for non-negative data."""
+    x, w, gam, bet, bias = _ln_case()
+    y, ya = oracle.linear_ln(x, w, bias=bias, ln_gamma=gam, ln_beta=bet, with_abs=True)
+    assert (np.abs(y - bias.numpy()) <= ya + 1e-12).all()
+    xp, wp = x.abs(), w.abs()
+    y2, ya2 = oracle.linear_ln(xp, wp, with_abs=True)
+    assert np.abs(y2 - ya2).max() < 1e-12
