@@ -224,6 +224,31 @@ fl_status fl_rsa_select(const fl_tensor* q, const fl_tensor* kmin, const fl_tens
                         int32_t topk, int32_t blk_q, int32_t blk_k, int32_t causal_align,
                         fl_tensor* blk_idx, fl_tensor* blk_cnt, void* stream);
 
+/* ---- fused LayerNorm-prologue linear layer (the memory passes on either side of
+ * the attention kernel -- Flashlight fuses "complex element-wise prologues", §3.1; AF2 Alg.7
+ * lines 1-4 and 7 of the Evoformer row attention, the paper's second workload P:L865) ----------------
+ *   y[m, n] = sum_k xhat[m, k] w[n, k] + bias[n],
+ *   xhat[m, :] = LN(x[m, :]) = (x - mean) / sqrt(var + ln_eps) * ln_gamma + ln_beta   (ln_gamma present),
+ *              = x[m, :]                                                            (ln_gamma absent)
+ *   with mean / var (biased) over the K entries of row m, in fp32; xhat is rounded to bf16 before the
+ *   tensor-core product (fp32 accumulation).
+ *   x        : bf16 [M, K] (rank 2), contiguous last dim, 16-byte aligned base and row stride; K in
+ *              {64, 128, 192, 256} (the whole row is one tile).
+ *   w        : bf16 [N, K] (rank 2; the PyTorch Linear weight layout), contiguous last dim, aligned rows.
+ *   bias     : optional f32 [N], contiguous.   ln_gamma / ln_beta : optional f32 [K] (beta needs gamma).
+ *   y        : bf16 [M, N] (rank 2), ANY element strides (e.g. a head-major [H, i, j] pair bias written
+ *              from [i*j, H] rows); must not overlap x / w.
+ *   M >= 0, 1 <= N.  One tcgen05 kernel (TMA, in-place LayerNorm of the landed tile, K/16 MMAs, fused
+ *   bias epilogue), 128 x min(N, 256) outputs per CTA.  Asynchronous on `stream`; no workspace.
+ *   Errors: FL_ERR_INVALID_ARGUMENT (missing / non-device tensors, dtype), FL_ERR_SHAPE_MISMATCH,
+ *   FL_ERR_UNSUPPORTED (K not in the set), FL_ERR_MISALIGNED. */
+typedef struct {
+  fl_tensor x, w, bias, ln_gamma, ln_beta, y;
+  float ln_eps;
+  void* stream;
+} fl_linear_args;
+fl_status fl_linear(const fl_linear_args* args);
+
 /* Contiguous range [begin, end) of `units` independent work units owned by
  * `rank` of `world` (multi-GPU batch x head sharding; no collective). */
 void fl_shard_range(int64_t units, int32_t world, int32_t rank, int64_t* begin, int64_t* end);

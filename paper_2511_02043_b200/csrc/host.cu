@@ -20,6 +20,7 @@
 namespace fl {
 cudaError_t launch_attn_simt(const AttnParams& p, cudaStream_t stream);
 cudaError_t launch_attn_tc(const AttnParams& p, const TmaMaps& maps, cudaStream_t stream);
+cudaError_t launch_linear(const LinParams& p, const CUtensorMap& tx, const CUtensorMap& tw, cudaStream_t stream);
 cudaError_t launch_pack_keymask(const unsigned char* km, int64_t sb, int64_t sg, int64_t sk, int B, int G, int Sk,
                                 int words, uint32_t* out, cudaStream_t stream);
 cudaError_t launch_fill_empty(const AttnParams& p, cudaStream_t stream);
@@ -759,6 +760,56 @@ fl_status fl_attn_bwd(const fl_attn_bwd_args* args) {
                                         strides_of(B.dv), static_cast<cudaStream_t>(args->stream));
   g_launches += 3;
   return e == cudaSuccess ? FL_OK : cuda_fail(e, "backward launch");
+}
+
+fl_status fl_linear(const fl_linear_args* a) {
+  if (!a) return fail(FL_ERR_INVALID_ARGUMENT, "args is NULL");
+  const fl_tensor &x = a->x, &w = a->w, &y = a->y;
+  if (!x.data || !w.data || !y.data) return fail(FL_ERR_INVALID_ARGUMENT, "linear: x, w, y are required");
+  if (x.dtype != FL_BF16 || w.dtype != FL_BF16 || y.dtype != FL_BF16)
+    return fail(FL_ERR_INVALID_ARGUMENT, "linear: x, w, y must be bf16");
+  if (x.rank != 2 || w.rank != 2 || y.rank != 2) return fail(FL_ERR_SHAPE_MISMATCH, "linear: x, w, y must be rank 2");
+  const int64_t M = x.size[0], K = x.size[1], N = w.size[0];
+  if (w.size[1] != K || y.size[0] != M || y.size[1] != N)
+    return fail(FL_ERR_SHAPE_MISMATCH, "linear: x [M,K], w [N,K], y [M,N]");
+  if (K != 64 && K != 128 && K != 192 && K != 256) return fail(FL_ERR_UNSUPPORTED, "linear: K in {64, 128, 192, 256}");
+  if (N < 1 || M < 0 || M >= (1ll << 31) || N >= (1ll << 31)) return fail(FL_ERR_SHAPE_MISMATCH, "linear: bad M / N");
+  if (x.stride[1] != 1 || w.stride[1] != 1) return fail(FL_ERR_UNSUPPORTED, "linear: x and w need a contiguous last dim");
+  const fl_tensor* f32s[3] = {&a->bias, &a->ln_gamma, &a->ln_beta};
+  const int64_t want[3] = {N, K, K};
+  for (int i = 0; i < 3; ++i)
+    if (f32s[i]->data && (f32s[i]->dtype != FL_F32 || f32s[i]->rank != 1 || f32s[i]->size[0] != want[i] ||
+                          f32s[i]->stride[0] != 1))
+      return fail(FL_ERR_SHAPE_MISMATCH, "linear: bias f32 [N], ln_gamma / ln_beta f32 [K], contiguous");
+  if (a->ln_beta.data && !a->ln_gamma.data) return fail(FL_ERR_INVALID_ARGUMENT, "linear: ln_beta needs ln_gamma");
+  const void* ptrs[] = {x.data, w.data, y.data, a->bias.data, a->ln_gamma.data, a->ln_beta.data};
+  for (const void* p : ptrs)
+    if (!on_device(p)) return fail(FL_ERR_INVALID_ARGUMENT, "linear: pointers must be device memory");
+  View5 vx, vw, vy;
+  vx.present = vw.present = vy.present = true;
+  vx.data = x.data; vx.dtype = FL_BF16; vx.size[3] = M; vx.size[4] = K; vx.stride[3] = x.stride[0]; vx.stride[4] = 1;
+  vw.data = w.data; vw.dtype = FL_BF16; vw.size[3] = N; vw.size[4] = K; vw.stride[3] = w.stride[0]; vw.stride[4] = 1;
+  vy.data = y.data; vy.dtype = FL_BF16; vy.size[3] = M; vy.size[4] = N; vy.stride[3] = y.stride[0];
+  vy.stride[4] = y.stride[1];
+  if (overlaps(vy, vx) || overlaps(vy, vw)) return fail(FL_ERR_INVALID_ARGUMENT, "linear: y overlaps x or w");
+  if (M == 0) return FL_OK;
+  CUtensorMap tx, tw;
+  int bg, bb;
+  fl_status s;
+  if ((s = encode_map(vx, 64, &tx, &bg, &bb)) != FL_OK) return s;
+  if ((s = encode_map(vw, 64, &tw, &bg, &bb)) != FL_OK) return s;
+  LinParams p;
+  p.M = (int)M; p.N = (int)N; p.K = (int)K;
+  p.NT = N >= 256 ? 256 : (int)((N + 15) / 16 * 16);
+  p.bias = static_cast<const float*>(a->bias.data);
+  p.ln_g = static_cast<const float*>(a->ln_gamma.data);
+  p.ln_b = static_cast<const float*>(a->ln_beta.data);
+  p.eps = a->ln_eps;
+  p.y = y.data;
+  p.ys_m = y.stride[0]; p.ys_n = y.stride[1];
+  const cudaError_t e = launch_linear(p, tx, tw, static_cast<cudaStream_t>(a->stream));
+  ++g_launches;
+  return e == cudaSuccess ? FL_OK : cuda_fail(e, "linear launch");
 }
 
 fl_status fl_diag_pipe_rate(int32_t op, int32_t iters, float* sink, int64_t* ops, void* stream) {

@@ -95,6 +95,17 @@ struct TmaMaps {
   int32_t bias_tma, bias_bcast_g, bias_bcast_b;
 };
 
+// Fused LayerNorm-prologue linear layer (linear.cu, NEXT-2), built by host.cu's fl_linear.
+struct LinParams {
+  int32_t M, N, K, NT;       // NT: output columns per CTA (multiple of 16, <= 256)
+  const float* bias;         // [N] or nullptr
+  const float* ln_g;         // [K] or nullptr (no LayerNorm)
+  const float* ln_b;         // [K] or nullptr
+  float eps;
+  void* y;                   // bf16
+  int64_t ys_m, ys_n;        // element strides of y
+};
+
 // RSA block selection (rsa.cu), built by host.cu's fl_rsa_select.
 struct RsaSelParams {
   int B, G, Hq, Hkv, grp, Sq, Sk, D, nkb, nqb, topk, max_sel, q_off, parts;

@@ -279,6 +279,24 @@ def rsa_select(q: torch.Tensor, kmin: torch.Tensor, kmax: torch.Tensor, s_k: int
     return blk_idx, blk_cnt
 
 
+def linear(x: torch.Tensor, w: torch.Tensor, bias=None, ln_gamma=None, ln_beta=None, eps: float = 1e-5, out=None,
+           stream=None):
+    """Fused LayerNorm-prologue linear layer (fl_linear, NEXT-2): out = [LN(x)] w^T + bias.  x bf16
+    [..., K] (rows flattened), w bf16 [N, K], bias / ln_gamma / ln_beta f32; out bf16 [..., N] or any
+    rank-2 [M, N] view (e.g. a transposed one)."""
+    x2 = x.reshape(-1, x.shape[-1])
+    if out is None:
+        out = torch.empty(*x.shape[:-1], w.shape[0], device=x.device, dtype=torch.bfloat16)
+    y2 = out if out.dim() == 2 else out.view(-1, w.shape[0])
+    a = _lib.LinearArgs()
+    a.x, a.w, a.y = tensor(x2), tensor(w), tensor(y2)
+    a.bias, a.ln_gamma, a.ln_beta = tensor(bias), tensor(ln_gamma), tensor(ln_beta)
+    a.ln_eps = float(eps)
+    a.stream = _stream_handle(x.device, stream)
+    _lib.check(_lib.lib().fl_linear(C.byref(a)))
+    return out
+
+
 def diag_umma_gemm(a: torch.Tensor, b: torch.Tensor, n: int, k: int, b_mn_major=False, a_from_tmem=False):
     c = torch.empty(128, n, device=a.device, dtype=torch.float32)
     s = torch.cuda.current_stream(a.device).cuda_stream
