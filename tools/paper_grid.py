@@ -184,25 +184,63 @@ def evo_grid(quick):
     return rows
 
 
+def evo_block_grid(quick):
+    """NEXT-4: the whole synthetic-weights Evoformer row-attention block (AF2 Alg.7: LN + q|k|v|g projection,
+    LN(z) pair-bias projection, gated attention with pair bias, output projection) chained from this package's
+    kernels (paper_2511_02043_b200/evoformer.py, one CUDA graph) vs the same block in PyTorch (cuBLAS GEMMs,
+    fused layer_norm, SDPA with the pair bias as an additive mask) under torch.compile.  c_m = 256, c_z = 128,
+    H = 8, c = 32 (AF2 sizes), N_res = 384 (BASELINE configs[3])."""
+    import torch.nn.functional as F
+    from paper_2511_02043_b200 import evoformer
+    H, c, cm, cz, Nr = 8, 32, 256, 128, 384
+    w = evoformer.synthetic_weights(c_m=cm, c_z=cz, H=H, c=c, seed=1)
+
+    def torch_block(m, z):
+        Ns = m.shape[0]
+        mh = F.layer_norm(m, (cm,), w.ln_m_g.to(m.dtype), w.ln_m_b.to(m.dtype), 1e-5)
+        proj = F.linear(mh, w.w_qkvg, w.b_qkvg.to(m.dtype))
+        q, k, v, g = (proj[..., i * H * c:(i + 1) * H * c].reshape(Ns, Nr, H, c).transpose(1, 2) for i in range(4))
+        zb = F.linear(F.layer_norm(z, (cz,), w.ln_z_g.to(z.dtype), w.ln_z_b.to(z.dtype), 1e-5), w.w_b)
+        o = F.scaled_dot_product_attention(q, k, v, attn_mask=zb.permute(2, 0, 1).unsqueeze(0))
+        o = (torch.sigmoid(g) * o).transpose(1, 2).reshape(Ns, Nr, H * c)
+        return F.linear(o, w.w_o, w.b_o.to(m.dtype))
+    tc = torch.compile(torch_block)
+    rows = []
+    for Ns in ((128,) if quick else (32, 128, 512)):
+        m = (torch.rand(Ns, Nr, cm, device="cuda") * 4 - 2).to(torch.bfloat16)
+        z = (torch.rand(Nr, Nr, cz, device="cuda") * 4 - 2).to(torch.bfloat16)
+        blk = evoformer.RowAttnBlock(w, Ns, Nr)
+        t_ours = timeit(lambda: blk(m, z), graph=True)
+        t_tc = timeit(lambda: tc(m, z))
+        t_eager = timeit(lambda: torch_block(m, z))
+        flops = 2 * Ns * Nr * cm * 4 * H * c + 2 * Nr * Nr * cz * H + 4 * Ns * H * Nr * Nr * c + 2 * Ns * Nr * H * c * cm
+        rows.append(("evoformer_block", "compile", Ns, 1, t_ours, t_tc, 0.0, flops / t_ours / 1e9))
+        rows.append(("evoformer_block", "eager", Ns, 1, t_ours, t_eager, 0.0, flops / t_ours / 1e9))
+    return rows
+
+
 def main():
     import torch._dynamo
     torch._dynamo.config.recompile_limit = 100000        # every (shape, mod) recompiles flex_attention once
     torch._dynamo.config.cache_size_limit = 100000
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--block-only", action="store_true", help="only the Evoformer block rows")
     a = ap.parse_args()
     print(f"# Paper benchmark grid on {torch.cuda.get_device_name()} (torch {torch.__version__}); context only\n")
     print("| variant | heads | S (or N_seq) | B | ours ms | comparator ms | flex block-mask ms | ours TFLOP/s | "
           "speed-up vs comparator kernel | incl. mask |")
     print("|---|---|---|---|---|---|---|---|---|---|")
-    for rows in (flex_grid(a.quick), diff_grid(a.quick), evo_grid(a.quick)):
+    ap_rows = (evo_block_grid(a.quick),) if a.block_only else (flex_grid(a.quick), diff_grid(a.quick), evo_grid(a.quick), evo_block_grid(a.quick))
+    for rows in ap_rows:
         for name, heads, S, B, to, tf, tm, tfl in rows:
             sp = tf / to if tf == tf else float("nan")
             spm = (tf + tm) / to if tf == tf else float("nan")
             print(f"| {name} | {heads} | {S} | {B} | {to:.4f} | {tf:.4f} | {tm:.4f} | {tfl:.1f} | {sp:.2f} | {spm:.2f} |")
             sys.stdout.flush()
     print("\ncomparator: FlexAttention (torch.compile'd flex_attention) for the first block; torch.compile of "
-          "Listing 4 for diff; torch.compile of the eager Evoformer row attention for evoformer_row.")
+          "Listing 4 for diff; torch.compile of the eager Evoformer row attention for evoformer_row; "
+          "for evoformer_block the whole AF2 Alg.7 block in PyTorch (cuBLAS + SDPA) under torch.compile / eager.")
 
 
 if __name__ == "__main__":
