@@ -238,8 +238,9 @@ fl_status fl_rsa_select(const fl_tensor* q, const fl_tensor* kmin, const fl_tens
  *   bias     : optional f32 [N], contiguous.   ln_gamma / ln_beta : optional f32 [K] (beta needs gamma).
  *   y        : bf16 [M, N] (rank 2), ANY element strides (e.g. a head-major [H, i, j] pair bias written
  *              from [i*j, H] rows); must not overlap x / w.
- *   M >= 0, 1 <= N.  One tcgen05 kernel (TMA, in-place LayerNorm of the landed tile, K/16 MMAs, fused
- *   bias epilogue), 128 x min(N, 256) outputs per CTA.  Asynchronous on `stream`; no workspace.
+ *   M >= 0, 1 <= N.  One tcgen05 kernel: one CTA per 128 rows of x (read and normalised once, in place
+ *   in shared memory), looping over 128-column tiles of w (double-buffered) into two TMEM accumulators,
+ *   fused bias epilogue.  Asynchronous on `stream`; no workspace.
  *   Errors: FL_ERR_INVALID_ARGUMENT (missing / non-device tensors, dtype), FL_ERR_SHAPE_MISMATCH,
  *   FL_ERR_UNSUPPORTED (K not in the set), FL_ERR_MISALIGNED. */
 typedef struct {

@@ -20,7 +20,8 @@
 namespace fl {
 cudaError_t launch_attn_simt(const AttnParams& p, cudaStream_t stream);
 cudaError_t launch_attn_tc(const AttnParams& p, const TmaMaps& maps, cudaStream_t stream);
-cudaError_t launch_linear(const LinParams& p, const CUtensorMap& tx, const CUtensorMap& tw, cudaStream_t stream);
+cudaError_t launch_linear(const LinParams& p, const CUtensorMap& tx, const CUtensorMap& tw, const CUtensorMap& ty,
+                          int y_tma, cudaStream_t stream);
 cudaError_t launch_pack_keymask(const unsigned char* km, int64_t sb, int64_t sg, int64_t sk, int B, int G, int Sk,
                                 int words, uint32_t* out, cudaStream_t stream);
 cudaError_t launch_fill_empty(const AttnParams& p, cudaStream_t stream);
@@ -800,14 +801,28 @@ fl_status fl_linear(const fl_linear_args* a) {
   if ((s = encode_map(vw, 64, &tw, &bg, &bb)) != FL_OK) return s;
   LinParams p;
   p.M = (int)M; p.N = (int)N; p.K = (int)K;
-  p.NT = N >= 256 ? 256 : (int)((N + 15) / 16 * 16);
+  p.NT = N >= 128 ? 128 : (int)((N + 15) / 16 * 16);
   p.bias = static_cast<const float*>(a->bias.data);
   p.ln_g = static_cast<const float*>(a->ln_gamma.data);
   p.ln_b = static_cast<const float*>(a->ln_beta.data);
   p.eps = a->ln_eps;
   p.y = y.data;
   p.ys_m = y.stride[0]; p.ys_n = y.stride[1];
-  const cudaError_t e = launch_linear(p, tx, tw, static_cast<cudaStream_t>(a->stream));
+  // row-contiguous y with 16-byte aligned rows: the epilogue stages each tile and TMA-stores whole rows
+  CUtensorMap ty;
+  memset(&ty, 0, sizeof ty);
+  int y_tma = 0;
+#ifdef FL_LIN_TMA_STORE   // measured slower (Evoformer block 0.87 -> 1.11 ms at N_seq 512): the per-tile
+                          // wait for the bulk store to release the staging buffer serialises the epilogue
+  if (y.stride[1] == 1 && aligned16(vy)) {
+#else
+  if (false) {
+#endif
+    const std::string saved = g_err;
+    y_tma = encode_map(vy, 64, &ty, &bg, &bb) == FL_OK;
+    g_err = saved;
+  }
+  const cudaError_t e = launch_linear(p, tx, tw, ty, y_tma, static_cast<cudaStream_t>(a->stream));
   ++g_launches;
   return e == cudaSuccess ? FL_OK : cuda_fail(e, "linear launch");
 }

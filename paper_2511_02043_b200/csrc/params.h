@@ -97,7 +97,7 @@ struct TmaMaps {
 
 // Fused LayerNorm-prologue linear layer (linear.cu, NEXT-2), built by host.cu's fl_linear.
 struct LinParams {
-  int32_t M, N, K, NT;       // NT: output columns per CTA (multiple of 16, <= 256)
+  int32_t M, N, K, NT;       // NT: output columns per tile (multiple of 16, <= 128)
   const float* bias;         // [N] or nullptr
   const float* ln_g;         // [K] or nullptr (no LayerNorm)
   const float* ln_b;         // [K] or nullptr
