@@ -126,7 +126,8 @@ struct TcCfg {
   // | bias_full[4] bias_empty[4]
   static constexpr int NBAR = 2 * NQBUF + 2 * NSLOT + 6 + 4 + 8;
   static constexpr int SMEM_SCHED = SMEM_BAR + NBAR * 8 + 16;       // blocklist schedule (RSA), 2 slots
-  static constexpr int SCHED_WORDS = 2 * kMaxSelTc + 8;   // schedule + meta (n, lo0, hi0, lo1, hi1, ..., unit id)
+  static constexpr int SCHED_WORDS = 2 * kMaxSelTc + 24;  // schedule, count, the decoded Work (WORK_OFF), unit id
+  static constexpr int WORK_OFF = 2 * kMaxSelTc + 4;
   static constexpr int KBITS_WORDS = 64;             // small heads: key-mask bits (S_k <= 2048) in the unit slot
   static constexpr int SMEM_ML = SMEM_SCHED + 2 * SCHED_WORDS * 4;      // LIST: WG1's (m, l) per row
   // ALiBi on the tensor core (kAlibiMma): the constant A tile of ones and two per-unit B tiles of slope*c
@@ -443,11 +444,27 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     return static_cast<int>(sched_base[(it & 1) * C::SCHED_WORDS + C::SCHED_WORDS - 1]);
   };
   // Work of the unit published in slot it & 1 (by value: keeps it in registers)
+  // the producer publishes the decoded unit in the slot, so the MMA issuer and the softmax warpgroups do
+  // not redo decode_work's integer divisions on their critical path at every unit start
+  // (small heads only: their units are a few tiles long; at D >= 64 the registers the loaded fields occupy
+  // cost more in spills than the recomputation, which the compiler can rematerialise from the parameters)
   auto unit_work = [&](int u, int it) -> Work {
-    Work w = decode_work<D, DIFF, LIST, (PAIR != 0)>(p, u);
-    if constexpr (LIST) load_sched(w, sched_base + (it & 1) * C::SCHED_WORDS);
+    if constexpr (D > 32) {
+      Work w = decode_work<D, DIFF, LIST, (PAIR != 0)>(p, u);
+      if constexpr (LIST) load_sched(w, sched_base + (it & 1) * C::SCHED_WORDS);
+      return w;
+    }
+    const uint32_t* sc = sched_base + (it & 1) * C::SCHED_WORDS;
+    const int* f = reinterpret_cast<const int*>(sc + C::WORK_OFF);
+    Work w;
+    w.b = f[0]; w.g = f[1]; w.g1 = f[2]; w.h = f[3];
+    w.q0[0] = f[4]; w.q0[1] = f[5];
+    w.lo[0] = f[6]; w.hi[0] = f[7]; w.lo[1] = f[8]; w.hi[1] = f[9];
+    w.lo_cta = f[10]; w.hi_cta = f[11];
+    w.sched = LIST ? sc : nullptr;
     return w;
   };
+  auto unit_seg = [&](int it) { return reinterpret_cast<const int*>(sched_base + (it & 1) * C::SCHED_WORDS + C::WORK_OFF)[12]; };
   auto release_unit = [&](int it) { mbar_arrive(&unit_empty[it & 1]); };
 
   if (warp >= 8) {
@@ -505,7 +522,15 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             }
           }
         }
-        mbar_arrive(&unit_full[it & 1]);               // release: id / schedule visible to the waiters
+        {
+          int* f = reinterpret_cast<int*>(sc + C::WORK_OFF);
+          f[0] = w.b; f[1] = w.g; f[2] = w.g1; f[3] = w.h;
+          f[4] = w.q0[0]; f[5] = w.q0[1];
+          f[6] = w.lo[0]; f[7] = w.hi[0]; f[8] = w.lo[1]; f[9] = w.hi[1];
+          f[10] = w.lo_cta; f[11] = w.hi_cta;
+          f[12] = (PAIR != 0 && p.unit_order == 1) ? u / ((p.G + 1) >> 1) : 0;   // resident-bias segment
+        }
+        mbar_arrive(&unit_full[it & 1]);               // release: id / schedule / Work visible to the waiters
         const int u_next = (PAIR != 0 && p.unit_order == 1) ? (u + 1 < u_end ? u + 1 : n_units)
                                                        : (int)gridDim.x + atomicAdd(p.tile_ctr, 1);   // latency hidden behind this unit
         const int hkv = w.h / p.grp;
@@ -781,7 +806,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     if constexpr (bias_res) {
       // resident pair bias: on a new (b, h, q-block) segment both warpgroups refill the row's bias in TMEM
       // (WG0 keys [0, BR_KEYS/2), WG1 the rest), between two barriers so no tile reads a half-written row
-      const int seg = u / ((p.G + 1) >> 1);
+      const int seg = unit_seg(it);
       if (seg != res_seg) {
         if (res_seg >= 0) named_bar_sync(6, 256);   // both warpgroups are done with the old rows
         const unsigned short* brow = static_cast<const unsigned short*>(p.bias) + w.b * p.bs.b +
