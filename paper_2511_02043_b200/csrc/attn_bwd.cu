@@ -30,6 +30,8 @@
 namespace fl {
 
 constexpr float kBwdLog2e = 1.4426950408889634f;
+// two compute warpgroups (warps 0-7; each takes 64 of a tile's 128 columns), TMA warp 8, MMA warp 9
+constexpr int kBwdThreads = 320;
 
 // ---------------------------------------------------------------- Dvec = rowsum(dO * O)
 // one warp per output row, 16-byte loads; dvec [B, G, Hq, Sq] f32 contiguous
@@ -114,10 +116,11 @@ __device__ __forceinline__ float head_slope(const AttnParams& p, int h) {
 }
 
 // ================================================================ dK / dV
-// grid = B * Hkv * n_kvtile (kv tile ascending within a head: causal's heaviest tiles first), 192 threads:
-// warps 0-3 compute (thread = key row), warp 4 TMA producer, warp 5 MMA issuer + TMEM allocator.
+// grid = B * Hkv * n_kvtile (kv tile ascending within a head: causal's heaviest tiles first), 320 threads:
+// warps 0-7 compute (thread = key row; warpgroup w takes query columns [64 w, 64 w + 64)), warp 8 TMA
+// producer, warp 9 MMA issuer + TMEM allocator.
 template <int D, int MOD>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kBwdThreads, 1)
     bwd_dkdv_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ TmaMaps maps,
                     const __grid_constant__ CUtensorMap tdo, const float* __restrict__ lse_g, Strided5 ls,
                     const float* __restrict__ dvec, __nv_bfloat16* __restrict__ dk, Strided5 dks,
@@ -160,18 +163,18 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(s_full, 1);
-    mbar_init(p_full, 128);
+    mbar_init(p_full, 256);
     mbar_init(o_full, 1);
     fence_mbar_init();
   }
-  if (warp == 5) tmem_alloc<512>(tmem_slot);
+  if (warp == 9) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DV = 256, COL_DK = 256 + D;
 
-  if (warp == 4) {
+  if (warp == 8) {
     // ============================== TMA producer ==============================
     if (lane == 0) {
       const int gk = maps.k_bcast_g ? 0 : 0, bk = maps.k_bcast_b ? 0 : b;
@@ -201,7 +204,7 @@ __global__ void __launch_bounds__(192, 1)
           ++e;
         }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     // ============================== MMA issuer ==============================
     if (lane == 0) {
       const uint32_t ka = smem_u32(sK), va = smem_u32(sV), ring = smem_u32(sRing);
@@ -238,9 +241,12 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {
     // ============================== compute (thread = key row) ==============================
-    const int r = threadIdx.x;                      // 0..127
+    // Warpgroup wg takes query columns [64 wg, 64 wg + 64) of the item (same TMEM lanes, disjoint columns).
+    const int wg = warp >> 2;
+    const int r = threadIdx.x & 127;                // key row == TMEM lane
     const int k = k0 + r;
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    const int j0 = wg * 64;
     int e = 0;
     for (int hh = hk * p.grp; hh < (hk + 1) * p.grp; ++hh) {
       const float slope_l2 = MOD == MOD_ALIBI ? head_slope(p, hh) : 0.f;
@@ -248,12 +254,11 @@ __global__ void __launch_bounds__(192, 1)
         if (!item_needed(qt)) continue;
         const int st = e % C::NST;
         const int q0 = qt * 128;
-        // this tile's LSE (log2 units) and Dvec rows, one per thread, into the stage's row buffer
-        // this tile's rows, one per thread: LSE (log2 units), Dvec and the key interval [lo, hi) of query q0 + r
-        // (rows past S_q get an empty interval: P = 0); the element loop reads them as broadcasts
+        // this tile's rows, one per thread of warpgroup 0: LSE (log2 units), Dvec and the key interval
+        // [lo, hi) of query q0 + r (rows past S_q get an empty interval: P = 0); read as broadcasts
         float* rl = sRows + st * 512;
         int* riv = reinterpret_cast<int*>(rl + 256);
-        {
+        if (wg == 0) {
           const int q = q0 + r;
           const bool ok = q < p.Sq;
           const int64_t li = (int64_t)b * ls.b + (int64_t)hh * ls.h + (int64_t)(ok ? q : 0) * ls.s;
@@ -263,61 +268,71 @@ __global__ void __launch_bounds__(192, 1)
           riv[r] = ok ? iv.lo : 0;
           riv[128 + r] = ok ? iv.hi : 0;
         }
-        named_bar_sync(1, 128);
+        named_bar_sync(1, 256);
         // tile class: mask-free when every row's interval covers [k0, k0 + 128) (intervals are monotone)
         const int q_last = min(p.Sq, q0 + 128) - 1;
         const Interval a0 = row_interval(p, b, q0), a1 = row_interval(p, b, q_last);
         const bool full_tile = q_last - q0 == 127 && a1.lo <= k0 && a0.hi >= k0 + 128 && k0 + 128 <= p.Sk;
         mbar_wait(s_full, e & 1);
         tc_fence_after();
-        uint32_t sv[128];
-        tmem_ld32(tmem + lane_base + COL_S + 0, &sv[0]);
-        tmem_ld32(tmem + lane_base + COL_S + 32, &sv[32]);
-        tmem_ld32(tmem + lane_base + COL_S + 64, &sv[64]);
-        tmem_ld32(tmem + lane_base + COL_S + 96, &sv[96]);
+        uint32_t sv[64];
+        tmem_ld32(tmem + lane_base + COL_S + j0, &sv[0]);
+        tmem_ld32(tmem + lane_base + COL_S + j0 + 32, &sv[32]);
         tmem_wait_ld();
-        // P^T (bf16 pairs) and the softcap factor, query j = column
-        uint32_t pk[64], fk[64];
+        // P^T (bf16 pairs) and the softcap factor, query j0 + j = column
+        uint32_t pk[32], fk[32];
 #pragma unroll
-        for (int j = 0; j < 128; j += 2) {
-          float pr[2], f[2];
+        for (int j = 0; j < 64; j += 4) {
+          const float4 lse4 = *reinterpret_cast<const float4*>(rl + j0 + j);
+          const float lsev[4] = {lse4.x, lse4.y, lse4.z, lse4.w};
+          float pr[4], f[4];
 #pragma unroll
-          for (int t = 0; t < 2; ++t) {
-            const int q = q0 + j + t;
+          for (int t = 0; t < 4; ++t) {
+            const int q = q0 + j0 + j + t;
             float ft;
             const float s = bwd_score<MOD>(p, __uint_as_float(sv[j + t]), slope_l2, k, q + p.q_off, ft);
-            const bool keep = full_tile || (k >= riv[j + t] && k < riv[128 + j + t]);   // hi <= S_k
-            pr[t] = keep ? ex2(fmaf(s, kBwdLog2e, -rl[j + t])) : 0.f;
+            const bool keep = full_tile || (k >= riv[j0 + j + t] && k < riv[128 + j0 + j + t]);   // hi <= S_k
+            pr[t] = keep ? ex2(fmaf(s, kBwdLog2e, -lsev[t])) : 0.f;
             f[t] = ft;
           }
           pk[j >> 1] = pack_bf16(pr[0], pr[1]);
+          pk[(j >> 1) + 1] = pack_bf16(pr[2], pr[3]);
           fk[j >> 1] = pack_bf16(f[0], f[1]);
+          fk[(j >> 1) + 1] = pack_bf16(f[2], f[3]);
         }
-        tmem_st32(tmem + lane_base + COL_S + 64, &pk[0]);
-        tmem_st32(tmem + lane_base + COL_S + 96, &pk[32]);
+        // both warpgroups have read their S^T columns before either overwrites S^T's columns with P^T / dS^T
+        named_bar_sync(1, 256);
+        tmem_st32(tmem + lane_base + COL_S + 64 + (j0 >> 1), &pk[0]);
         // dS^T = P^T (dP^T - Dvec) * f, 32 queries at a time, into [0, 64) (S^T is consumed)
 #pragma unroll
-        for (int c = 0; c < 128; c += 32) {
+        for (int c = 0; c < 64; c += 32) {
           uint32_t dp[32];
-          tmem_ld32(tmem + lane_base + COL_DP + c, dp);
+          tmem_ld32(tmem + lane_base + COL_DP + j0 + c, dp);
           tmem_wait_ld();
           uint32_t ds[16];
 #pragma unroll
-          for (int j = 0; j < 32; j += 2) {
-            const uint32_t pw = pk[(c + j) >> 1], fw = fk[(c + j) >> 1];
-            float d0 = bf16_lo(pw) * (__uint_as_float(dp[j]) - rl[128 + c + j]);
-            float d1 = bf16_hi(pw) * (__uint_as_float(dp[j + 1]) - rl[128 + c + j + 1]);
+          for (int j = 0; j < 32; j += 4) {
+            const float4 dv4 = *reinterpret_cast<const float4*>(rl + 128 + j0 + c + j);
+            const uint32_t pw0 = pk[(c + j) >> 1], pw1 = pk[((c + j) >> 1) + 1];
+            const uint32_t fw0 = fk[(c + j) >> 1], fw1 = fk[((c + j) >> 1) + 1];
+            float d0 = bf16_lo(pw0) * (__uint_as_float(dp[j]) - dv4.x);
+            float d1 = bf16_hi(pw0) * (__uint_as_float(dp[j + 1]) - dv4.y);
+            float d2 = bf16_lo(pw1) * (__uint_as_float(dp[j + 2]) - dv4.z);
+            float d3 = bf16_hi(pw1) * (__uint_as_float(dp[j + 3]) - dv4.w);
             if (MOD == MOD_SOFTCAP) {
-              d0 *= bf16_lo(fw);
-              d1 *= bf16_hi(fw);
+              d0 *= bf16_lo(fw0);
+              d1 *= bf16_hi(fw0);
+              d2 *= bf16_lo(fw1);
+              d3 *= bf16_hi(fw1);
             }
             ds[j >> 1] = pack_bf16(d0, d1);
+            ds[(j >> 1) + 1] = pack_bf16(d2, d3);
           }
-          tmem_st16(tmem + lane_base + COL_S + (c >> 1), ds);
+          tmem_st16(tmem + lane_base + COL_S + ((j0 + c) >> 1), ds);
         }
         tmem_wait_st();
         tc_fence_before();
-        named_bar_sync(1, 128);                     // every thread has read this stage's row buffer
+        named_bar_sync(1, 256);                     // every thread has read this stage's row buffer
         mbar_arrive(p_full);
         ++e;
       }
@@ -332,8 +347,8 @@ __global__ void __launch_bounds__(192, 1)
       const bool k_ok = k < p.Sk;
       __nv_bfloat16* dkp = dk + b * dks.b + (int64_t)hk * dks.h + (int64_t)(k_ok ? k : 0) * dks.s;
       __nv_bfloat16* dvp = dv + b * dvs.b + (int64_t)hk * dvs.h + (int64_t)(k_ok ? k : 0) * dvs.s;
-#pragma unroll
-      for (int which = 0; which < 2; ++which) {
+      {
+        const int which = wg;                         // warpgroup 0 stores dV, warpgroup 1 dK
 #pragma unroll
         for (int c = 0; c < D; c += 32) {
           uint32_t o[32];
@@ -360,13 +375,14 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 5) tmem_dealloc<512>(tmem);
+  if (warp == 9) tmem_dealloc<512>(tmem);
 }
 
 // ================================================================ dQ
-// grid = B * Hq * n_qtile (query tile descending: causal's heaviest tiles first), 192 threads.
+// grid = B * Hq * n_qtile (query tile descending: causal's heaviest tiles first), 320 threads:
+// warps 0-7 compute (two warpgroups split the tile's 128 key columns), warp 8 TMA, warp 9 MMA + TMEM.
 template <int D, int MOD>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kBwdThreads, 1)
     bwd_dq_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ TmaMaps maps,
                   const __grid_constant__ CUtensorMap tdo, const float* __restrict__ lse_g, Strided5 ls,
                   const float* __restrict__ dvec, __nv_bfloat16* __restrict__ dq, Strided5 dqs) {
@@ -402,18 +418,18 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(s_full, 1);
-    mbar_init(p_full, 128);
+    mbar_init(p_full, 256);
     mbar_init(o_full, 1);
     fence_mbar_init();
   }
-  if (warp == 5) tmem_alloc<512>(tmem_slot);
+  if (warp == 9) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DQ = 256;
 
-  if (warp == 4) {
+  if (warp == 8) {
     if (lane == 0) {
       const int bq = maps.q_bcast_b ? 0 : b;
       mbar_arrive_expect_tx(q_full, 2 * C::TILE_BYTES);
@@ -436,7 +452,7 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     if (lane == 0) {
       const uint32_t qa = smem_u32(sQ), doa = smem_u32(sDO), ring = smem_u32(sRing);
       mbar_wait(q_full, 0);
@@ -463,11 +479,14 @@ __global__ void __launch_bounds__(192, 1)
       umma_commit(o_full);
     }
   } else {
-    const int r = threadIdx.x;
+    // warpgroup wg takes key columns [64 wg, 64 wg + 64) of each KV tile (same TMEM lanes = query rows)
+    const int wg = warp >> 2;
+    const int r = threadIdx.x & 127;
     const int q = q0 + r;
     const bool row_ok = q < p.Sq;
     const int q_abs = q + p.q_off;
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    const int j0 = wg * 64;
     const float slope_l2 = MOD == MOD_ALIBI ? head_slope(p, h) : 0.f;
     const float lse_l2 = row_ok ? lse_g[(int64_t)b * ls.b + (int64_t)h * ls.h + (int64_t)q * ls.s] * kBwdLog2e : INFINITY;
     const float dvr = row_ok ? dvec[(((int64_t)b * p.G) * p.Hq + h) * p.Sq + q] : 0.f;
@@ -478,19 +497,17 @@ __global__ void __launch_bounds__(192, 1)
       const bool full_tile = tile_inside(iv, k0, p.Sk);
       mbar_wait(s_full, e & 1);
       tc_fence_after();
-      uint32_t sv[128];
-      tmem_ld32(tmem + lane_base + COL_S + 0, &sv[0]);
-      tmem_ld32(tmem + lane_base + COL_S + 32, &sv[32]);
-      tmem_ld32(tmem + lane_base + COL_S + 64, &sv[64]);
-      tmem_ld32(tmem + lane_base + COL_S + 96, &sv[96]);
+      uint32_t sv[64];
+      tmem_ld32(tmem + lane_base + COL_S + j0, &sv[0]);
+      tmem_ld32(tmem + lane_base + COL_S + j0 + 32, &sv[32]);
       tmem_wait_ld();
-      uint32_t pk[64], fk[64];
+      uint32_t pk[32], fk[32];
 #pragma unroll
-      for (int j = 0; j < 128; j += 2) {
+      for (int j = 0; j < 64; j += 2) {
         float pr[2], f[2];
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
-          const int k = k0 + j + t;
+          const int k = k0 + j0 + j + t;
           float ft;
           const float s = bwd_score<MOD>(p, __uint_as_float(sv[j + t]), slope_l2, k, q_abs, ft);
           const bool keep = full_tile || (k >= iv.lo && k < iv.hi && k < p.Sk);
@@ -500,10 +517,12 @@ __global__ void __launch_bounds__(192, 1)
         pk[j >> 1] = pack_bf16(pr[0], pr[1]);
         fk[j >> 1] = pack_bf16(f[0], f[1]);
       }
+      // both warpgroups have read their S columns before dS overwrites S's columns [64, 128)
+      named_bar_sync(1, 256);
 #pragma unroll
-      for (int c = 0; c < 128; c += 32) {           // dS = P (dP - Dvec) f -> TMEM [64 + c/2, ...)
+      for (int c = 0; c < 64; c += 32) {            // dS = P (dP - Dvec) f -> TMEM [64 + (j0 + c)/2, ...)
         uint32_t dp[32];
-        tmem_ld32(tmem + lane_base + COL_DP + c, dp);
+        tmem_ld32(tmem + lane_base + COL_DP + j0 + c, dp);
         tmem_wait_ld();
         uint32_t ds[16];
 #pragma unroll
@@ -517,7 +536,7 @@ __global__ void __launch_bounds__(192, 1)
           }
           ds[j >> 1] = pack_bf16(d0, d1);
         }
-        tmem_st16(tmem + lane_base + COL_S + 64 + (c >> 1), ds);
+        tmem_st16(tmem + lane_base + COL_S + 64 + ((j0 + c) >> 1), ds);
       }
       tmem_wait_st();
       tc_fence_before();
@@ -530,7 +549,7 @@ __global__ void __launch_bounds__(192, 1)
     {                                                // every lane loads (.sync.aligned), valid rows store
       __nv_bfloat16* qp = dq + b * dqs.b + (int64_t)h * dqs.h + (int64_t)(row_ok ? q : 0) * dqs.s;
 #pragma unroll
-      for (int c = 0; c < D; c += 32) {
+      for (int c = wg * (D / 2); c < (wg + 1) * (D / 2); c += 32) {   // warpgroup wg: dQ columns half wg
         uint32_t o[32];
         if (kt_hi > kt_lo) {
           tmem_ld32(tmem + lane_base + COL_DQ + c, o);
@@ -554,7 +573,7 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 5) tmem_dealloc<512>(tmem);
+  if (warp == 9) tmem_dealloc<512>(tmem);
 }
 
 // ---------------------------------------------------------------- launch
@@ -575,10 +594,10 @@ static cudaError_t launch_bwd_dm(const AttnParams& p, const TmaMaps& maps, const
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(bwd_dq_kernel<D, MOD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_TOTAL);
   if (e != cudaSuccess) return e;
-  bwd_dkdv_kernel<D, MOD><<<p.B * p.Hkv * n_kt, 192, C::SMEM_TOTAL, s>>>(p, maps, tdo, L.lse, L.ls, L.dvec, L.dk, L.dks,
+  bwd_dkdv_kernel<D, MOD><<<p.B * p.Hkv * n_kt, kBwdThreads, C::SMEM_TOTAL, s>>>(p, maps, tdo, L.lse, L.ls, L.dvec, L.dk, L.dks,
                                                                         L.dv, L.dvs);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  bwd_dq_kernel<D, MOD><<<p.B * p.Hq * n_qt, 192, C::SMEM_TOTAL, s>>>(p, maps, tdo, L.lse, L.ls, L.dvec, L.dq, L.dqs);
+  bwd_dq_kernel<D, MOD><<<p.B * p.Hq * n_qt, kBwdThreads, C::SMEM_TOTAL, s>>>(p, maps, tdo, L.lse, L.ls, L.dvec, L.dq, L.dqs);
   return cudaGetLastError();
 }
 
