@@ -83,7 +83,7 @@ def lib():
                                       C.POINTER(C.c_uint8)]
         _lib.flo_keep_row.restype = C.c_int
         _lib.flo_attn_bwd.argtypes = [C.POINTER(_Problem), C.POINTER(_Tensor), C.POINTER(C.c_double),
-                                      C.POINTER(C.c_double), C.POINTER(C.c_double)]
+                                      C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]
         _lib.flo_attn_bwd.restype = C.c_int
         dp = C.POINTER(C.c_double)
         _lib.flo_linear_ln.argtypes = [C.c_int64, C.c_int64, C.c_int64, dp, dp, dp, dp, dp, C.c_double, dp, dp]
@@ -176,19 +176,22 @@ def attn(q, k, v, *, scale=0.0, mod="none", softcap=0.0, alibi_slopes=None,
     return out, lse
 
 
-def attn_bwd(q, k, v, dout, **variant):
-    """Gradients (dq, dk, dv) of L = sum(O * dout), fp64 numpy arrays shaped like q, k, v (NEXT-3)."""
+def attn_bwd(q, k, v, dout, with_dgate=False, **variant):
+    """Gradients (dq, dk, dv) of L = sum(O * dout), fp64 numpy arrays shaped like q, k, v (NEXT-3); with
+    with_dgate also dL/dgate (shaped like dout) for a gated variant."""
     keep: list = []
     p = _problem(q, k, v, keep, **variant)
     dt = _tensor(dout, keep)
     dq = np.zeros(tuple(q.shape), dtype=np.float64)
     dk = np.zeros(tuple(k.shape), dtype=np.float64)
     dv = np.zeros(tuple(v.shape), dtype=np.float64)
+    dg = np.zeros(tuple(dout.shape), dtype=np.float64) if with_dgate else None
     rc = lib().flo_attn_bwd(C.byref(p), C.byref(dt), dq.ctypes.data_as(C.POINTER(C.c_double)),
-                            dk.ctypes.data_as(C.POINTER(C.c_double)), dv.ctypes.data_as(C.POINTER(C.c_double)))
+                            dk.ctypes.data_as(C.POINTER(C.c_double)), dv.ctypes.data_as(C.POINTER(C.c_double)),
+                            dg.ctypes.data_as(C.POINTER(C.c_double)) if with_dgate else None)
     if rc != 0:
         raise ValueError(f"flo_attn_bwd rejected the problem (code {rc})")
-    return dq, dk, dv
+    return (dq, dk, dv, dg) if with_dgate else (dq, dk, dv)
 
 
 def keep_rows(q, k, v, rows, **variant):

@@ -249,7 +249,10 @@ int flo_keep_row(const flo_problem* p, int64_t b, int64_t g, int64_t h, int64_t 
  *   dQ += scale dx_k K_k ;  dK_k += scale dx_k Q                                (x = scale <Q, K_k> + ...)
  * dK, dV of a KV head accumulate over its GQA group (G15).  Outputs are fp64 arrays with the logical shapes
  * of q, k, v ([B,G,H,S,D], row-major).  diff_norm is not differentiated here (returns -11). */
-int flo_attn_bwd(const flo_problem* p, const flo_tensor* dout, double* dq, double* dk, double* dv) {
+/* dgate (optional, may be NULL): dL/dgate for the Evoformer gate of reading G9 (O = gate'(g) * A, AF2
+ * Alg.7 line 6): dgate = dO * A * sigma(g) (1 - sigma(g)) (sigmoid) or dO * A (mul), A the map-combined
+ * attention output before the gate (sum over maps of coef * P V). */
+int flo_attn_bwd(const flo_problem* p, const flo_tensor* dout, double* dq, double* dk, double* dv, double* dgate) {
   int64_t maps;
   int rc = check_problem(p, &maps);
   if (rc) return rc;
@@ -262,6 +265,8 @@ int flo_attn_bwd(const flo_problem* p, const flo_tensor* dout, double* dq, doubl
   for (int64_t i = 0; i < nq; ++i) dq[i] = 0.0;
   for (int64_t i = 0; i < nk; ++i) dk[i] = 0.0;
   for (int64_t i = 0; i < nv; ++i) dv[i] = 0.0;
+  if (dgate)
+    for (int64_t i = 0; i < B * G * Hq * Sq * Dv; ++i) dgate[i] = 0.0;
   /* one task per (b, g, kv head): every write of the task stays inside it */
 #pragma omp parallel
   {
@@ -325,6 +330,12 @@ int flo_attn_bwd(const flo_problem* p, const flo_tensor* dout, double* dq, doubl
               }
               da[d] = coef * gv * elem(dout, off5(dout, b, g, h, q, d));
               dot_da_a += da[d] * a[d];
+              if (dgate && p->gate_mode != FLO_GATE_NONE) {
+                const double gl = elem(&p->gate, off5(&p->gate, b, g, h, q, d));
+                const double dgl = p->gate_mode == FLO_GATE_SIGMOID ? gv * (1.0 - gv) : 1.0;   /* gate'(g) */
+                (void)gl;
+                dgate[(((b * G + g) * Hq + h) * Sq + q) * Dv + d] += coef * a[d] * dgl * elem(dout, off5(dout, b, g, h, q, d));
+              }
             }
             for (int64_t k = 0; k < Sk; ++k) {
               if (pr[k] == 0.0 && sc[k] == -INFINITY) continue;

@@ -584,7 +584,8 @@ def test_diff_transformer_epilogue_brute_force_and_closed_forms():
 # ----------------------------------------------------------------- backward (NEXT-3)
 @pytest.mark.parametrize("kw", [dict(), dict(mask="causal"), dict(mask="sliding", window=2), dict(mod="alibi"),
                                 dict(mod="softcap", softcap=0.7), dict(mask="prefix", prefix=2),
-                                dict(gate_mode="sigmoid"), dict(diff=True, lam=0.4), dict(gqa=True)])
+                                dict(gate_mode="sigmoid"), dict(gate_mode="mul"), dict(diff=True, lam=0.4),
+                                dict(diff=True, lam=0.4, gate_mode="sigmoid"), dict(gqa=True)])
 def test_backward_matches_central_differences(kw):
     """The oracle's dQ, dK, dV (plain chain rule) against central differences of the oracle's own
     FORWARD (an independent route: no derivative formula involved), L = sum(O * dO), h = 1e-6."""
@@ -598,10 +599,15 @@ def test_backward_matches_central_differences(kw):
     do = rnd(1, H, S, D, seed=93)
     if kw.get("gate_mode"):
         kw["gate"] = rnd(1, H, S, D, seed=94, lo=-2, hi=2)
-    dq, dk, dv = oracle.attn_bwd(q, k, v, do, **kw)
+    gated = bool(kw.get("gate_mode"))
+    if gated:
+        dq, dk, dv, dg = oracle.attn_bwd(q, k, v, do, with_dgate=True, **kw)
+    else:
+        dq, dk, dv = oracle.attn_bwd(q, k, v, do, **kw)
     L = lambda q_, k_, v_: float((oracle.attn(q_, k_, v_, **kw)[0].reshape(do.shape) * do.numpy()).sum())
     h = 1e-6
-    for t, grad in ((q, dq), (k, dk), (v, dv)):
+    pairs = [(q, dq), (k, dk), (v, dv)] + ([(kw["gate"], dg)] if gated else [])   # the gate is read through kw
+    for t, grad in pairs:
         num = np.zeros(grad.shape)
         flat = t.view(-1)
         for i in range(flat.numel()):
