@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define FL_ABI_VERSION 2
+#define FL_ABI_VERSION 3
 
 typedef enum {
   FL_OK = 0,
@@ -137,7 +137,7 @@ typedef struct {
   size_t workspace_bytes;
 } fl_attn_args;
 
-/* Supported set (ABI v2 = v1 + paged KV):
+/* Supported set (ABI v2 = v1 + paged KV; v3 = v2 + the backward's dgate and fl_linear):
  *   f32 q/k/v/o  : exact-fp32 SIMT path, every variant, D_qk, D_v <= 128.
  *   bf16 q/k/v/o : tcgen05/TMEM/TMA persistent kernel, D_qk == D_v in {32, 64, 128}; every mask,
  *                  mod, bias, key_mask, gate; diff (lse must be absent with diff).  FL_MASK_BLOCKLIST
@@ -152,11 +152,14 @@ fl_status fl_attn_fwd(const fl_attn_args* args);
 
 /* ---- backward (the training half, §2.4) ------------------------------
  * dQ, dK, dV of L = sum(O * dout) for the forward fl_attn_fwd computes with the same q, k, v, variant,
- * given its output o and natural-log LSE (G19).  Two tcgen05 kernels (a KV-tile-major dK/dV pass and a
- * query-tile-major dQ pass, no atomics) after a rowsum(dO * O) pass.  Supported (v1): bf16, rank-4 q/k/v,
- * D_qk == D_v in {64, 128}, GQA, masks none / causal / sliding / prefix / document (either alignment),
- * mods none / ALiBi / softcap.  Not yet: diff, gate, bias, key_mask, block lists, paged KV, fp32
- * (FL_ERR_UNSUPPORTED).  Workspace: 4 * B * Hq * S_q bytes (fl_attn_bwd_workspace_size). */
+ * given its output o and natural-log LSE (G19).  A rowsum pass (or, with a sigmoid gate, the gate pre-pass:
+ * dA = dO s(g) into the workspace, dgate = dO o (1 - s(g)), Dvec = rowsum(dO o)), then two tcgen05 kernels
+ * (a KV-tile-major dK/dV pass and a query-tile-major dQ pass, two compute warpgroups each, no atomics).
+ * Supported (v3): bf16, rank-4 or rank-5 q/k/v (G), D_qk == D_v in {32, 64, 128}, GQA, masks none /
+ * causal / sliding / prefix / document (either alignment), mods none / ALiBi / softcap, key_mask (MSA
+ * mask), sigmoid gate (+ dgate).  Not yet: diff, additive bias, mul gate, block lists, paged KV, fp32
+ * (FL_ERR_UNSUPPORTED).  Workspace (fl_attn_bwd_workspace_size): 4 B G Hq S_q bytes (Dvec) + the packed
+ * key mask + 2 B G Hq S_q D_v bytes with a sigmoid gate, each 256-byte rounded. */
 typedef struct {
   fl_tensor q, k, v, o;      /* the forward's inputs and output (bf16) */
   fl_tensor lse;             /* the forward's LSE, f32 [B, Hq, S_q] (required) */
@@ -166,6 +169,7 @@ typedef struct {
   void* stream;
   void* workspace;
   size_t workspace_bytes;
+  fl_tensor dgate;           /* optional (gate_mode sigmoid): dL/dgate-logits, bf16, the gate's shape (ABI v3) */
 } fl_attn_bwd_args;
 
 fl_status fl_attn_bwd(const fl_attn_bwd_args* args);

@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(HERE, "libfl_attn.so")
 
 FL_BF16, FL_F32, FL_U8, FL_I32 = 0, 1, 2, 3
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 EXPORTS = ["fl_attn_fwd", "fl_attn_workspace_size", "fl_attn_host_scratch_size", "fl_attn_fwd_host",
            "fl_rsa_build_summaries", "fl_rsa_update_summaries", "fl_rsa_select", "fl_shard_range", "fl_diag_umma_gemm",
@@ -49,7 +49,7 @@ class AttnArgs(C.Structure):
 class BwdArgs(C.Structure):
     _fields_ = [("q", Tensor), ("k", Tensor), ("v", Tensor), ("o", Tensor), ("lse", Tensor), ("dout", Tensor),
                 ("dq", Tensor), ("dk", Tensor), ("dv", Tensor), ("var", Variant), ("stream", C.c_void_p),
-                ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t)]
+                ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t), ("dgate", Tensor)]
 
 
 class LinearArgs(C.Structure):

@@ -61,15 +61,57 @@ __global__ void __launch_bounds__(256) bwd_dvec_kernel(const AttnParams p, const
   if (lane == 0) dvec[row] = acc;
 }
 
+// ---------------------------------------------------------------- sigmoid gate (reading G9, AF2 Alg.7 line 6)
+// out = s(g) * A:  dA = dO * s(g) (written as the dO the tcgen05 kernels read, contiguous [B,G,Hq,Sq,Dv]),
+// dg = dO * out * (1 - s(g))  (= dO * A * s (1 - s), no division by s), Dvec = rowsum(dA * A) = rowsum(dO * out).
+// One warp per output row, 8 elements per lane and step.
+__global__ void __launch_bounds__(256) bwd_gate_kernel(const AttnParams p, const __nv_bfloat16* __restrict__ dout,
+                                                      Strided5 dos, __nv_bfloat16* __restrict__ da,
+                                                      __nv_bfloat16* __restrict__ dgate, Strided5 dgs,
+                                                      float* __restrict__ dvec) {
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int64_t n_rows = (int64_t)p.B * p.G * p.Hq * p.Sq;
+  if (row >= n_rows) return;
+  const int q = (int)(row % p.Sq);
+  const int64_t bgh = row / p.Sq;
+  const int h = (int)(bgh % p.Hq), g = (int)((bgh / p.Hq) % p.G), b = (int)(bgh / ((int64_t)p.Hq * p.G));
+  const __nv_bfloat16* o = static_cast<const __nv_bfloat16*>(p.o) + b * p.os.b + g * p.os.g + h * p.os.h + q * p.os.s;
+  const __nv_bfloat16* d = dout + b * dos.b + g * dos.g + h * dos.h + q * dos.s;
+  const __nv_bfloat16* gl = static_cast<const __nv_bfloat16*>(p.gate) + b * p.gs.b + g * p.gs.g + h * p.gs.h + q * p.gs.s;
+  __nv_bfloat16* dar = da + row * p.Dv;
+  __nv_bfloat16* dgr = dgate ? dgate + b * dgs.b + g * dgs.g + h * dgs.h + q * dgs.s : nullptr;
+  float acc = 0.f;
+  for (int c = lane * 8; c < p.Dv; c += 256) {
+    const uint4 uo = *reinterpret_cast<const uint4*>(o + c), ud = *reinterpret_cast<const uint4*>(d + c),
+                ug = *reinterpret_cast<const uint4*>(gl + c);
+    const uint32_t wo[4] = {uo.x, uo.y, uo.z, uo.w}, wd[4] = {ud.x, ud.y, ud.z, ud.w}, wg[4] = {ug.x, ug.y, ug.z, ug.w};
+    uint32_t pa[4], pg[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const float o0 = bf16_lo(wo[t]), o1 = bf16_hi(wo[t]), d0 = bf16_lo(wd[t]), d1 = bf16_hi(wd[t]);
+      const float s0 = 1.f / (1.f + __expf(-bf16_lo(wg[t]))), s1 = 1.f / (1.f + __expf(-bf16_hi(wg[t])));
+      acc = fmaf(o0, d0, fmaf(o1, d1, acc));
+      pa[t] = pack_bf16(d0 * s0, d1 * s1);
+      pg[t] = pack_bf16(d0 * o0 * (1.f - s0), d1 * o1 * (1.f - s1));
+    }
+    *reinterpret_cast<uint4*>(dar + c) = make_uint4(pa[0], pa[1], pa[2], pa[3]);
+    if (dgr) *reinterpret_cast<uint4*>(dgr + c) = make_uint4(pg[0], pg[1], pg[2], pg[3]);
+  }
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+  if (lane == 0) dvec[row] = acc;
+}
+
 // ---------------------------------------------------------------- shared configuration
 template <int D>
 struct BwdCfg {
-  static constexpr int CH = 64;                      // bf16 per 128-byte swizzle row
-  static constexpr int SWB = 128;
+  static constexpr int CH = D >= 64 ? 64 : 32;       // bf16 per swizzle row (128 B, or 64 B at D = 32)
+  static constexpr int SWB = CH * 2;
   static constexpr int NCH = D / CH;
-  static constexpr int CHUNK_BYTES = 128 * SWB;      // 128 rows x 128 B
+  static constexpr int CHUNK_BYTES = 128 * SWB;      // 128 rows x SWB bytes
   static constexpr int TILE_BYTES = 128 * D * 2;
-  static constexpr uint32_t LAYOUT = kLayoutSW128;
+  static constexpr uint32_t LAYOUT = SWB == 128 ? kLayoutSW128 : kLayoutSW64;
   static constexpr int SBO = 8 * SWB;
   static constexpr uint32_t IDESC_NN = idesc_bf16_f32(128, 128, 0);   // [128 x D] . [128 x D]^T (both K-major)
   static constexpr uint32_t IDESC_ND = idesc_bf16_f32(128, D, 1);     // TMEM A [128 x 128] . smem B [128 x D] MN-major
@@ -144,7 +186,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int n_kt = (p.Sk + 127) / 128;
   const int kt = blockIdx.x % n_kt;
   const int hk = (blockIdx.x / n_kt) % p.Hkv;
-  const int b = blockIdx.x / (n_kt * p.Hkv);
+  const int g = (blockIdx.x / (n_kt * p.Hkv)) % p.G;
+  const int b = blockIdx.x / (n_kt * p.Hkv * p.G);
   const int k0 = kt * 128;
   const int n_qt = (p.Sq + 127) / 128;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -177,8 +220,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   if (warp == 8) {
     // ============================== TMA producer ==============================
     if (lane == 0) {
-      const int gk = maps.k_bcast_g ? 0 : 0, bk = maps.k_bcast_b ? 0 : b;
-      const int bv = maps.v_bcast_b ? 0 : b;
+      const int gk = maps.k_bcast_g ? 0 : g, bk = maps.k_bcast_b ? 0 : b;
+      const int gv = maps.v_bcast_g ? 0 : g, bv = maps.v_bcast_b ? 0 : b;
       mbar_arrive_expect_tx(kv_full, 2 * C::TILE_BYTES);
       int krow, kb;
       kv_tile_coords(p, b, kt, bk, krow, kb);
@@ -186,9 +229,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       kv_tile_coords(p, b, kt, bv, vrow, vb);
       for (int c = 0; c < C::NCH; ++c) {
         tma_load_5d(sK + c * C::CHUNK_BYTES, &maps.k, kv_full, c * C::CH, krow, hk, gk, kb);
-        tma_load_5d(sV + c * C::CHUNK_BYTES, &maps.v, kv_full, c * C::CH, vrow, hk, gk, vb);
+        tma_load_5d(sV + c * C::CHUNK_BYTES, &maps.v, kv_full, c * C::CH, vrow, hk, gv, vb);
       }
-      const int bq = maps.q_bcast_b ? 0 : b;
+      const int bq = maps.q_bcast_b ? 0 : b, gq = maps.q_bcast_g ? 0 : g;
       int e = 0;
       for (int hh = hk * p.grp; hh < (hk + 1) * p.grp; ++hh)
         for (int qt = 0; qt < n_qt; ++qt) {
@@ -198,8 +241,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           mbar_arrive_expect_tx(&full[st], 2 * C::TILE_BYTES);
           uint8_t* dq_ = sRing + st * 2 * C::TILE_BYTES;
           for (int c = 0; c < C::NCH; ++c) {
-            tma_load_5d(dq_ + c * C::CHUNK_BYTES, &maps.q, &full[st], c * C::CH, qt * 128, hh, 0, bq);
-            tma_load_5d(dq_ + C::TILE_BYTES + c * C::CHUNK_BYTES, &tdo, &full[st], c * C::CH, qt * 128, hh, 0, b);
+            tma_load_5d(dq_ + c * C::CHUNK_BYTES, &maps.q, &full[st], c * C::CH, qt * 128, hh, gq, bq);
+            tma_load_5d(dq_ + C::TILE_BYTES + c * C::CHUNK_BYTES, &tdo, &full[st], c * C::CH, qt * 128, hh, g, b);
           }
           ++e;
         }
@@ -247,6 +290,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int k = k0 + r;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     const int j0 = wg * 64;
+    // MSA / key mask (G9): a masked key has P = 0 for every query -- its dK, dV rows stay 0
+    const bool key_on = !p.keybits || k >= p.Sk ||
+                        ((p.keybits[((int64_t)b * p.G + g) * p.keybits_words + (k >> 5)] >> (k & 31)) & 1u);
     int e = 0;
     for (int hh = hk * p.grp; hh < (hk + 1) * p.grp; ++hh) {
       const float slope_l2 = MOD == MOD_ALIBI ? head_slope(p, hh) : 0.f;
@@ -261,9 +307,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (wg == 0) {
           const int q = q0 + r;
           const bool ok = q < p.Sq;
-          const int64_t li = (int64_t)b * ls.b + (int64_t)hh * ls.h + (int64_t)(ok ? q : 0) * ls.s;
+          const int64_t li = (int64_t)b * ls.b + (int64_t)g * ls.g + (int64_t)hh * ls.h + (int64_t)(ok ? q : 0) * ls.s;
           rl[r] = ok ? lse_g[li] * kBwdLog2e : INFINITY;
-          rl[128 + r] = ok ? dvec[(((int64_t)b * p.G) * p.Hq + hh) * p.Sq + q] : 0.f;
+          rl[128 + r] = ok ? dvec[(((int64_t)b * p.G + g) * p.Hq + hh) * p.Sq + q] : 0.f;
           const Interval iv = row_interval(p, b, q);
           riv[r] = ok ? iv.lo : 0;
           riv[128 + r] = ok ? iv.hi : 0;
@@ -291,7 +337,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             const int q = q0 + j0 + j + t;
             float ft;
             const float s = bwd_score<MOD>(p, __uint_as_float(sv[j + t]), slope_l2, k, q + p.q_off, ft);
-            const bool keep = full_tile || (k >= riv[j0 + j + t] && k < riv[128 + j0 + j + t]);   // hi <= S_k
+            const bool keep = key_on && (full_tile || (k >= riv[j0 + j + t] && k < riv[128 + j0 + j + t]));   // hi <= S_k
             pr[t] = keep ? ex2(fmaf(s, kBwdLog2e, -lsev[t])) : 0.f;
             f[t] = ft;
           }
@@ -345,8 +391,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // tcgen05.ld is .sync.aligned: every lane of the warp loads, only valid key rows store
     {
       const bool k_ok = k < p.Sk;
-      __nv_bfloat16* dkp = dk + b * dks.b + (int64_t)hk * dks.h + (int64_t)(k_ok ? k : 0) * dks.s;
-      __nv_bfloat16* dvp = dv + b * dvs.b + (int64_t)hk * dvs.h + (int64_t)(k_ok ? k : 0) * dvs.s;
+      __nv_bfloat16* dkp = dk + b * dks.b + (int64_t)g * dks.g + (int64_t)hk * dks.h + (int64_t)(k_ok ? k : 0) * dks.s;
+      __nv_bfloat16* dvp = dv + b * dvs.b + (int64_t)g * dvs.g + (int64_t)hk * dvs.h + (int64_t)(k_ok ? k : 0) * dvs.s;
       {
         const int which = wg;                         // warpgroup 0 stores dV, warpgroup 1 dK
 #pragma unroll
@@ -404,7 +450,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int n_qt = (p.Sq + 127) / 128;
   const int qt = n_qt - 1 - (int)(blockIdx.x % n_qt);
   const int h = (blockIdx.x / n_qt) % p.Hq;
-  const int b = blockIdx.x / (n_qt * p.Hq);
+  const int g = (blockIdx.x / (n_qt * p.Hq)) % p.G;
+  const int b = blockIdx.x / (n_qt * p.Hq * p.G);
   const int hk = h / p.grp;
   const int q0 = qt * 128;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -431,13 +478,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   if (warp == 8) {
     if (lane == 0) {
-      const int bq = maps.q_bcast_b ? 0 : b;
+      const int bq = maps.q_bcast_b ? 0 : b, gq = maps.q_bcast_g ? 0 : g;
       mbar_arrive_expect_tx(q_full, 2 * C::TILE_BYTES);
       for (int c = 0; c < C::NCH; ++c) {
-        tma_load_5d(sQ + c * C::CHUNK_BYTES, &maps.q, q_full, c * C::CH, q0, h, 0, bq);
-        tma_load_5d(sDO + c * C::CHUNK_BYTES, &tdo, q_full, c * C::CH, q0, h, 0, b);
+        tma_load_5d(sQ + c * C::CHUNK_BYTES, &maps.q, q_full, c * C::CH, q0, h, gq, bq);
+        tma_load_5d(sDO + c * C::CHUNK_BYTES, &tdo, q_full, c * C::CH, q0, h, g, b);
       }
       const int bk = maps.k_bcast_b ? 0 : b, bv = maps.v_bcast_b ? 0 : b;
+      const int gk = maps.k_bcast_g ? 0 : g, gv = maps.v_bcast_g ? 0 : g;
       for (int kt = kt_lo; kt < kt_hi; ++kt) {
         const int e = kt - kt_lo, st = e % C::NST;
         if (e >= C::NST) mbar_wait(&empty[st], ((e / C::NST) - 1) & 1);
@@ -447,8 +495,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         kv_tile_coords(p, b, kt, bk, krow, kb);
         kv_tile_coords(p, b, kt, bv, vrow, vb);
         for (int c = 0; c < C::NCH; ++c) {
-          tma_load_5d(dst + c * C::CHUNK_BYTES, &maps.k, &full[st], c * C::CH, krow, hk, 0, kb);
-          tma_load_5d(dst + C::TILE_BYTES + c * C::CHUNK_BYTES, &maps.v, &full[st], c * C::CH, vrow, hk, 0, vb);
+          tma_load_5d(dst + c * C::CHUNK_BYTES, &maps.k, &full[st], c * C::CH, krow, hk, gk, kb);
+          tma_load_5d(dst + C::TILE_BYTES + c * C::CHUNK_BYTES, &maps.v, &full[st], c * C::CH, vrow, hk, gv, vb);
         }
       }
     }
@@ -488,13 +536,20 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     const int j0 = wg * 64;
     const float slope_l2 = MOD == MOD_ALIBI ? head_slope(p, h) : 0.f;
-    const float lse_l2 = row_ok ? lse_g[(int64_t)b * ls.b + (int64_t)h * ls.h + (int64_t)q * ls.s] * kBwdLog2e : INFINITY;
-    const float dvr = row_ok ? dvec[(((int64_t)b * p.G) * p.Hq + h) * p.Sq + q] : 0.f;
+    const float lse_l2 =
+        row_ok ? lse_g[(int64_t)b * ls.b + (int64_t)g * ls.g + (int64_t)h * ls.h + (int64_t)q * ls.s] * kBwdLog2e : INFINITY;
+    const float dvr = row_ok ? dvec[(((int64_t)b * p.G + g) * p.Hq + h) * p.Sq + q] : 0.f;
+    const uint32_t* kbits = p.keybits ? p.keybits + ((int64_t)b * p.G + g) * p.keybits_words : nullptr;
     const Interval iv = row_interval(p, b, q);
     for (int kt = kt_lo; kt < kt_hi; ++kt) {
       const int e = kt - kt_lo;
       const int k0 = kt * 128;
       const bool full_tile = tile_inside(iv, k0, p.Sk);
+      uint32_t kw0 = 0xFFFFFFFFu, kw1 = 0xFFFFFFFFu;     // key-mask words of this warpgroup's 64 keys
+      if (kbits) {
+        kw0 = __ldg(kbits + ((k0 + j0) >> 5));
+        kw1 = __ldg(kbits + ((k0 + j0) >> 5) + 1);
+      }
       mbar_wait(s_full, e & 1);
       tc_fence_after();
       uint32_t sv[64];
@@ -510,7 +565,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           const int k = k0 + j0 + j + t;
           float ft;
           const float s = bwd_score<MOD>(p, __uint_as_float(sv[j + t]), slope_l2, k, q_abs, ft);
-          const bool keep = full_tile || (k >= iv.lo && k < iv.hi && k < p.Sk);
+          const bool kon = (((j + t) < 32 ? kw0 : kw1) >> ((j + t) & 31)) & 1u;
+          const bool keep = kon && (full_tile || (k >= iv.lo && k < iv.hi && k < p.Sk));
           pr[t] = keep ? ex2(fmaf(s, kBwdLog2e, -lse_l2)) : 0.f;
           f[t] = ft;
         }
@@ -547,9 +603,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_after();
     }
     {                                                // every lane loads (.sync.aligned), valid rows store
-      __nv_bfloat16* qp = dq + b * dqs.b + (int64_t)h * dqs.h + (int64_t)(row_ok ? q : 0) * dqs.s;
+      __nv_bfloat16* qp = dq + b * dqs.b + (int64_t)g * dqs.g + (int64_t)h * dqs.h + (int64_t)(row_ok ? q : 0) * dqs.s;
+      // warpgroup wg: dQ columns half wg (D = 32: warpgroup 0 stores the whole row)
+      constexpr int kHalf = D >= 64 ? D / 2 : D;
 #pragma unroll
-      for (int c = wg * (D / 2); c < (wg + 1) * (D / 2); c += 32) {   // warpgroup wg: dQ columns half wg
+      for (int c = wg * kHalf; c < (wg + 1) * kHalf && c < D; c += 32) {
         uint32_t o[32];
         if (kt_hi > kt_lo) {
           tmem_ld32(tmem + lane_base + COL_DQ + c, o);
@@ -594,10 +652,10 @@ static cudaError_t launch_bwd_dm(const AttnParams& p, const TmaMaps& maps, const
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(bwd_dq_kernel<D, MOD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_TOTAL);
   if (e != cudaSuccess) return e;
-  bwd_dkdv_kernel<D, MOD><<<p.B * p.Hkv * n_kt, kBwdThreads, C::SMEM_TOTAL, s>>>(p, maps, tdo, L.lse, L.ls, L.dvec, L.dk, L.dks,
+  bwd_dkdv_kernel<D, MOD><<<p.B * p.G * p.Hkv * n_kt, kBwdThreads, C::SMEM_TOTAL, s>>>(p, maps, tdo, L.lse, L.ls, L.dvec, L.dk, L.dks,
                                                                         L.dv, L.dvs);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  bwd_dq_kernel<D, MOD><<<p.B * p.Hq * n_qt, kBwdThreads, C::SMEM_TOTAL, s>>>(p, maps, tdo, L.lse, L.ls, L.dvec, L.dq, L.dqs);
+  bwd_dq_kernel<D, MOD><<<p.B * p.G * p.Hq * n_qt, kBwdThreads, C::SMEM_TOTAL, s>>>(p, maps, tdo, L.lse, L.ls, L.dvec, L.dq, L.dqs);
   return cudaGetLastError();
 }
 
@@ -611,18 +669,29 @@ static cudaError_t launch_bwd_d(const AttnParams& p, const TmaMaps& maps, const 
   }
 }
 
+// The gate pre-pass (when p.gate_mode is sigmoid; `da` receives dO * s(g) and the caller's tdo map points
+// at it) or the plain Dvec pass.
+cudaError_t launch_bwd_prepass(const AttnParams& p, const void* dout, Strided5 dos, float* dvec, void* da, void* dgate,
+                               Strided5 dgs, cudaStream_t s) {
+  const int64_t rows = (int64_t)p.B * p.G * p.Hq * p.Sq;
+  if (p.gate_mode == GATE_SIGMOID)
+    bwd_gate_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(p, static_cast<const __nv_bfloat16*>(dout), dos,
+                                                                static_cast<__nv_bfloat16*>(da),
+                                                                static_cast<__nv_bfloat16*>(dgate), dgs, dvec);
+  else
+    bwd_dvec_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(p, static_cast<const __nv_bfloat16*>(dout), dos, dvec);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_attn_bwd(const AttnParams& p, const TmaMaps& maps, const CUtensorMap& tdo, const float* lse,
                             Strided5 ls, const void* dout, Strided5 dos, float* dvec, void* dq, Strided5 dqs, void* dk,
                             Strided5 dks, void* dv, Strided5 dvs, cudaStream_t s) {
-  const int64_t rows = (int64_t)p.B * p.G * p.Hq * p.Sq;
-  bwd_dvec_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(p, static_cast<const __nv_bfloat16*>(dout), dos, dvec);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
   BwdLaunch L{lse, ls, static_cast<const __nv_bfloat16*>(dout), dos, dvec, static_cast<__nv_bfloat16*>(dq),
               static_cast<__nv_bfloat16*>(dk), static_cast<__nv_bfloat16*>(dv), dqs, dks, dvs};
   switch (p.Dqk) {
     case 128: return launch_bwd_d<128>(p, maps, tdo, L, s);
     case 64: return launch_bwd_d<64>(p, maps, tdo, L, s);
+    case 32: return launch_bwd_d<32>(p, maps, tdo, L, s);
     default: return cudaErrorInvalidValue;
   }
 }

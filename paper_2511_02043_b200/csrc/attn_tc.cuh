@@ -162,6 +162,12 @@ constexpr bool kSoftcapPoly = true;
 #else
 constexpr bool kSoftcapPoly = false;
 #endif
+// groups of 4 scores (index (c/4) % 8) whose softcap tanh stays on the MUFU in the poly path (balances the
+// FMA and MUFU pipes); A/B'd in profiles/r02_ab.md
+#ifndef FL_TANH_MUFU_MASK
+#define FL_TANH_MUFU_MASK 0u
+#endif
+constexpr uint32_t kTanhMufuMask = FL_TANH_MUFU_MASK;
 constexpr float kTanhX0 = 1.5f;
 constexpr float kTanhC0 = 0.9993646741f, kTanhC1 = -0.3268460035f, kTanhC2 = 0.1141102985f,
                 kTanhC3 = -0.02846436948f, kTanhC4 = 0.003358259564f;
@@ -1119,8 +1125,15 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             n1 = x[c + 5];
             n2 = x[c + 6];
             n3 = x[c + 7];
-            tanh_poly2(n0, n1);
-            tanh_poly2(n2, n3);
+            if ((kTanhMufuMask >> (((c + 4) >> 2) & 7)) & 1u) {   // this group's tanh on the MUFU
+              n0 = n0 == -INFINITY ? -INFINITY : tanh_approx(n0 * cap_in);
+              n1 = n1 == -INFINITY ? -INFINITY : tanh_approx(n1 * cap_in);
+              n2 = n2 == -INFINITY ? -INFINITY : tanh_approx(n2 * cap_in);
+              n3 = n3 == -INFINITY ? -INFINITY : tanh_approx(n3 * cap_in);
+            } else {
+              tanh_poly2(n0, n1);
+              tanh_poly2(n2, n3);
+            }
           }
           exp4(c, t0, t1, t2, t3);
           t0 = n0;

@@ -42,6 +42,8 @@ cudaError_t debug_timing(unsigned long long* out, int reset);
 cudaError_t launch_pipe_rate(int op, int iters, int n_sms, float* sink, cudaStream_t s);
 cudaError_t launch_sched_dump(const AttnParams& p, int32_t* out, int64_t out_words, int64_t* n_records,
                               int32_t* max_tiles, cudaStream_t stream);
+cudaError_t launch_bwd_prepass(const AttnParams& p, const void* dout, Strided5 dos, float* dvec, void* da, void* dgate,
+                               Strided5 dgs, cudaStream_t s);
 cudaError_t launch_attn_bwd(const AttnParams& p, const TmaMaps& maps, const CUtensorMap& tdo, const float* lse,
                             Strided5 ls, const void* dout, Strided5 dos, float* dvec, void* dq, Strided5 dqs, void* dk,
                             Strided5 dks, void* dv, Strided5 dvs, cudaStream_t s);
@@ -690,8 +692,8 @@ fl_status fl_debug_schedule(const fl_attn_args* args, int32_t* out, int64_t out_
 namespace {
 struct BwdPrepared {
   Prepared P;
-  View5 dout, dq, dk, dv;
-  size_t ws = 0;
+  View5 dout, dq, dk, dv, dgate;
+  size_t ws = 0, off_bits = 0, off_da = 0;
 };
 
 fl_status prepare_bwd(const fl_attn_bwd_args* a, BwdPrepared& B, bool device_ptrs) {
@@ -704,29 +706,49 @@ fl_status prepare_bwd(const fl_attn_bwd_args* a, BwdPrepared& B, bool device_ptr
   if (s != FL_OK) return s;
   const fl_variant& var = a->var;
   const AttnParams& p = B.P.p;
-  if (!B.P.bf16 || B.P.q_rank != 4) return fail(FL_ERR_UNSUPPORTED, "backward: bf16, rank-4 q/k/v/o");
-  if (p.Dqk != 64 && p.Dqk != 128) return fail(FL_ERR_UNSUPPORTED, "backward: D in {64, 128}");
-  if (var.diff || var.gate_mode != FL_GATE_NONE || var.bias.data || var.key_mask.data || var.kv_page_table.data ||
-      var.mask == FL_MASK_BLOCKLIST)
-    return fail(FL_ERR_UNSUPPORTED, "backward v1: no diff / gate / bias / key_mask / block list / paged KV");
+  if (!B.P.bf16) return fail(FL_ERR_UNSUPPORTED, "backward: bf16 q/k/v/o");
+  if (p.Dqk != 32 && p.Dqk != 64 && p.Dqk != 128) return fail(FL_ERR_UNSUPPORTED, "backward: D in {32, 64, 128}");
+  if (var.diff || var.bias.data || var.kv_page_table.data || var.mask == FL_MASK_BLOCKLIST ||
+      var.gate_mode == FL_GATE_MUL)
+    return fail(FL_ERR_UNSUPPORTED, "backward: no diff / bias / block list / paged KV / mul gate");
   if (!a->lse.data) return fail(FL_ERR_INVALID_ARGUMENT, "backward needs the forward's lse");
+  const int R = B.P.q_rank;
   const fl_tensor* ts[4] = {&a->dout, &a->dq, &a->dk, &a->dv};
   View5* vs[4] = {&B.dout, &B.dq, &B.dk, &B.dv};
   const View5* like[4] = {&B.P.o, &B.P.q, &B.P.k, &B.P.v};
   for (int i = 0; i < 4; ++i) {
     if (!ts[i]->data || ts[i]->dtype != FL_BF16) return fail(FL_ERR_INVALID_ARGUMENT, "dout / dq / dk / dv: bf16, required");
-    if (!to_view(*ts[i], 4, 0, *vs[i])) return fail(FL_ERR_SHAPE_MISMATCH, "dout / dq / dk / dv must be rank 4");
+    if (!to_view(*ts[i], R, 0, *vs[i])) return fail(FL_ERR_SHAPE_MISMATCH, "dout / dq / dk / dv must have q's rank");
     for (int d = 0; d < 5; ++d)
       if (vs[i]->size[d] != like[i]->size[d]) return fail(FL_ERR_SHAPE_MISMATCH, "dout / dq / dk / dv shapes must match o / q / k / v");
     if (vs[i]->stride[4] != 1 || !aligned16(*vs[i])) return fail(FL_ERR_MISALIGNED, "dout / dq / dk / dv: contiguous last dim, 16-byte aligned");
   }
+  // dgate (optional; sigmoid gate only): bf16, the gate's shape
+  if (a->dgate.data) {
+    if (var.gate_mode != FL_GATE_SIGMOID) return fail(FL_ERR_INVALID_ARGUMENT, "dgate needs gate_mode sigmoid");
+    if (a->dgate.dtype != FL_BF16 || !to_view(a->dgate, R, 0, B.dgate))
+      return fail(FL_ERR_SHAPE_MISMATCH, "dgate: bf16 with q's rank");
+    for (int d = 0; d < 5; ++d)
+      if (B.dgate.size[d] != B.P.o.size[d]) return fail(FL_ERR_SHAPE_MISMATCH, "dgate must have o's shape");
+    if (B.dgate.stride[4] != 1 || !aligned16(B.dgate)) return fail(FL_ERR_MISALIGNED, "dgate: contiguous last dim, 16-byte aligned");
+  }
   for (int i = 1; i < 4; ++i)
-    for (const View5* in : {&B.P.q, &B.P.k, &B.P.v, &B.P.o, &B.dout})
+    for (const View5* in : {&B.P.q, &B.P.k, &B.P.v, &B.P.o, &B.dout, &B.P.gate})
       if (overlaps(*vs[i], *in)) return fail(FL_ERR_INVALID_ARGUMENT, "gradients must not overlap inputs");
-  if (device_ptrs)
+  if (B.dgate.present)
+    for (const View5* in : {&B.P.q, &B.P.k, &B.P.v, &B.P.o, &B.dout, &B.P.gate, &B.dq, &B.dk, &B.dv})
+      if (overlaps(B.dgate, *in)) return fail(FL_ERR_INVALID_ARGUMENT, "dgate must not overlap inputs / gradients");
+  if (device_ptrs) {
     for (int i = 0; i < 4; ++i)
       if (!on_device(ts[i]->data)) return fail(FL_ERR_INVALID_ARGUMENT, "dout / dq / dk / dv must be device memory");
+    if (!on_device(a->dgate.data)) return fail(FL_ERR_INVALID_ARGUMENT, "dgate must be device memory");
+  }
+  // workspace: Dvec f32 [B,G,Hq,Sq] | packed key mask | dO * s(g) bf16 [B,G,Hq,Sq,Dv] (sigmoid gate)
   B.ws = ((size_t)p.B * p.G * p.Hq * p.Sq * sizeof(float) + 255) & ~size_t(255);
+  B.off_bits = B.ws;
+  B.ws += (B.P.keybits_bytes + 255) & ~size_t(255);
+  B.off_da = B.ws;
+  if (var.gate_mode == FL_GATE_SIGMOID) B.ws += ((size_t)p.B * p.G * p.Hq * p.Sq * p.Dv * 2 + 255) & ~size_t(255);
   return FL_OK;
 }
 }  // namespace
@@ -747,19 +769,48 @@ fl_status fl_attn_bwd(const fl_attn_bwd_args* args) {
   if (B.P.empty_work) return FL_OK;
   if (!args->workspace || args->workspace_bytes < B.ws)
     return fail(FL_ERR_WORKSPACE, "the backward needs %zu bytes of workspace", B.ws);
+  cudaStream_t stream = static_cast<cudaStream_t>(args->stream);
+  char* ws = static_cast<char*>(args->workspace);
+  AttnParams& p = B.P.p;
   TmaMaps maps;
   memset(&maps, 0, sizeof maps);
+  const int ch = tc_chunk_elems(p.Dqk);
+  if ((s = encode_map(B.P.q, ch, &maps.q, &maps.q_bcast_g, &maps.q_bcast_b)) != FL_OK) return s;
+  if ((s = encode_map(B.P.k, ch, &maps.k, &maps.k_bcast_g, &maps.k_bcast_b)) != FL_OK) return s;
+  if ((s = encode_map(B.P.v, ch, &maps.v, &maps.v_bcast_g, &maps.v_bcast_b)) != FL_OK) return s;
+  cudaError_t e;
+  if (B.P.km.present) {                              // MSA / key mask -> one bit per key (as the forward)
+    uint32_t* bits = reinterpret_cast<uint32_t*>(ws + B.off_bits);
+    e = launch_pack_keymask(static_cast<const unsigned char*>(B.P.km.data), B.P.km.size[0] > 1 ? B.P.km.stride[0] : 0,
+                            B.P.km.size[1] > 1 ? B.P.km.stride[1] : 0, B.P.km.stride[4], p.B, p.G, p.Sk,
+                            p.keybits_words, bits, stream);
+    ++g_launches;
+    if (e != cudaSuccess) return cuda_fail(e, "pack_keymask launch");
+    p.keybits = bits;
+  }
+  // dO as the tcgen05 kernels read it: the caller's, or dO * s(g) from the gate pre-pass (contiguous)
+  View5 vda = B.dout;
+  void* da = nullptr;
+  if (p.gate_mode == GATE_SIGMOID) {
+    da = ws + B.off_da;
+    vda.data = da;
+    vda.stride[4] = 1;
+    vda.stride[3] = p.Dv;
+    vda.stride[2] = (int64_t)p.Sq * p.Dv;
+    vda.stride[1] = (int64_t)p.Hq * p.Sq * p.Dv;
+    vda.stride[0] = (int64_t)p.G * p.Hq * p.Sq * p.Dv;
+  }
   CUtensorMap tdo;
   int bg, bb;
-  if ((s = encode_map(B.P.q, 64, &maps.q, &maps.q_bcast_g, &maps.q_bcast_b)) != FL_OK) return s;
-  if ((s = encode_map(B.P.k, 64, &maps.k, &maps.k_bcast_g, &maps.k_bcast_b)) != FL_OK) return s;
-  if ((s = encode_map(B.P.v, 64, &maps.v, &maps.v_bcast_g, &maps.v_bcast_b)) != FL_OK) return s;
-  if ((s = encode_map(B.dout, 64, &tdo, &bg, &bb)) != FL_OK) return s;
-  const cudaError_t e = launch_attn_bwd(B.P.p, maps, tdo, static_cast<const float*>(B.P.lse.data), strides_of(B.P.lse),
-                                        B.dout.data, strides_of(B.dout), static_cast<float*>(args->workspace),
-                                        B.dq.data, strides_of(B.dq), B.dk.data, strides_of(B.dk), B.dv.data,
-                                        strides_of(B.dv), static_cast<cudaStream_t>(args->stream));
-  g_launches += 3;
+  if ((s = encode_map(vda, ch, &tdo, &bg, &bb)) != FL_OK) return s;
+  float* dvec = reinterpret_cast<float*>(ws);
+  e = launch_bwd_prepass(p, B.dout.data, strides_of(B.dout), dvec, da, B.dgate.data, strides_of(B.dgate), stream);
+  ++g_launches;
+  if (e != cudaSuccess) return cuda_fail(e, "backward pre-pass launch");
+  e = launch_attn_bwd(p, maps, tdo, static_cast<const float*>(B.P.lse.data), strides_of(B.P.lse), B.dout.data,
+                      strides_of(B.dout), dvec, B.dq.data, strides_of(B.dq), B.dk.data, strides_of(B.dk), B.dv.data,
+                      strides_of(B.dv), stream);
+  g_launches += 2;
   return e == cudaSuccess ? FL_OK : cuda_fail(e, "backward launch");
 }
 

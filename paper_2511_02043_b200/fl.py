@@ -177,17 +177,22 @@ def _keep_alive_on(stream, tensors):
             t.record_stream(stream)
 
 
-def attn_bwd(q, k, v, out, lse, dout, *, dq=None, dk=None, dv=None, workspace=None, **variant):
+def attn_bwd(q, k, v, out, lse, dout, *, dq=None, dk=None, dv=None, dgate=None, workspace=None, **variant):
     """Backward of attn_fwd (fl_attn_bwd, NEXT-3): returns (dq, dk, dv) of L = sum(out * dout), given the
-    forward's output and natural-log LSE (attn_fwd(..., return_lse=True))."""
+    forward's output and natural-log LSE (attn_fwd(..., return_lse=True)); with a sigmoid gate also dgate
+    (dL/dgate-logits): (dq, dk, dv, dgate)."""
     dq = torch.empty_like(q) if dq is None else dq
     dk = torch.empty_like(k) if dk is None else dk
     dv = torch.empty_like(v) if dv is None else dv
+    gated = variant.get("gate_mode") == "sigmoid"
+    if gated and dgate is None:
+        dgate = torch.empty(out.shape, dtype=torch.bfloat16, device=q.device)
     keep: list = []
     fa = make_args(q, k, v, out, lse, keep=keep, **variant)
     a = _lib.BwdArgs()
     a.q, a.k, a.v, a.o, a.lse = fa.q, fa.k, fa.v, fa.o, fa.lse
     a.dout, a.dq, a.dk, a.dv = tensor(dout), tensor(dq), tensor(dk), tensor(dv)
+    a.dgate = tensor(dgate)
     a.var = fa.var
     a.stream = fa.stream
     need = C.c_size_t(0)
@@ -199,7 +204,7 @@ def attn_bwd(q, k, v, out, lse, dout, *, dq=None, dk=None, dv=None, workspace=No
     a.workspace_bytes = need.value
     _lib.check(_lib.lib().fl_attn_bwd(C.byref(a)))
     _keep_alive_on(variant.get("stream"), keep)
-    return dq, dk, dv
+    return (dq, dk, dv, dgate) if gated else (dq, dk, dv)
 
 
 class HostRunner:

@@ -35,7 +35,14 @@ for D in (128, 64):
         dict(name=f"softcap_D{D}", S=300, D=D, mod="softcap", softcap=2.0, dist="needle"),
         dict(name=f"gqa_causal_D{D}", Hq=4, Hkv=2, S=333, D=D, mask="causal", dist="needle"),
         dict(name=f"sq_lt_sk_D{D}", Sq=100, Sk=450, D=D, mask="causal"),
+        dict(name=f"keymask_D{D}", Hq=2, S=300, D=D, key_mask=True, dist="needle"),
+        dict(name=f"gate_sigmoid_D{D}", Hq=2, S=260, D=D, mask="causal", gate_mode="sigmoid", dist="needle"),
     ]
+BWD += [
+    dict(name="vanilla_D32", Hq=2, S=300, D=32),
+    dict(name="causal_needle_D32", Hq=2, S=520, D=32, mask="causal", dist="needle"),
+    dict(name="gate_keymask_D32", Hq=2, S=200, D=32, key_mask=True, gate_mode="sigmoid", dist="needle"),
+]
 
 
 @pytest.mark.parametrize("case", BWD, ids=[c["name"] for c in BWD])
@@ -45,10 +52,17 @@ def test_backward_vs_oracle(fl, case):
     kw = {x: cases.to_dev(y, "cuda") for x, y in gk.items()}
     out, lse = fl.attn_fwd(q, k, v, return_lse=True, **kw)
     dout = synth.uniform(tuple(out.shape), seed=17, tensor="gate")
-    dq, dk, dv = fl.attn_bwd(q, k, v, out, lse, dout.cuda(), **kw)
+    _compare(fl, case["name"], (ins["q"], ins["k"], ins["v"]), (q, k, v), out, lse, dout, kw, ok)
+
+
+def _compare(fl, name0, host_qkv, dev_qkv, out, lse, dout, kw, ok):
+    gated = kw.get("gate_mode") == "sigmoid"
+    grads = fl.attn_bwd(*dev_qkv, out, lse, dout.cuda(), **kw)
     torch.cuda.synchronize()
-    rq, rk, rv = oracle.attn_bwd(ins["q"], ins["k"], ins["v"], dout, **ok)
-    for name, got, ref in (("dq", dq, rq), ("dk", dk, rk), ("dv", dv, rv)):
+    refs = oracle.attn_bwd(*host_qkv, dout, with_dgate=gated, **ok)
+    names = ("dq", "dk", "dv", "dgate") if gated else ("dq", "dk", "dv")
+    for name, got, ref in zip(names, grads, refs):
+        case = {"name": name0}
         r = check(got.cpu().double().numpy(), ref, 2e-2, min_ref=0.05 if name == "dv" else 0.0,
                   what=f"{case['name']} {name}")
         # where a gradient's scale is >= 0.05 it must also hold 5 % of that scale (G22); on peaked rows dQ
@@ -57,13 +71,28 @@ def test_backward_vs_oracle(fl, case):
             assert r["max_abs"] <= 0.05 * r["max_ref"], f"{case['name']} {name}: {r}"
 
 
+@pytest.mark.parametrize("Nr", [130, 300])
+def test_backward_evoformer_column(fl, Nr):
+    """Rank-5 strided views, D = 32, sigmoid gate (+ dgate) and MSA key mask: the Evoformer column
+    attention (AF2 Alg.8, reading G9), all of whose steps the backward now covers."""
+    ins, gk, ok = cases.evoformer(dict(kind="col", B=1, Ns=Nr, Nr=5, H=2, c=32, p_zero=0.1))
+    q, k, v = (ins[n].cuda().contiguous() for n in ("q", "k", "v"))
+    kw = {x: cases.to_dev(y, "cuda") for x, y in gk.items()}
+    kw["gate"] = kw["gate"].contiguous()
+    ok = dict(ok, gate=ok["gate"].contiguous())
+    out, lse = fl.attn_fwd(q, k, v, return_lse=True, **kw)
+    dout = synth.uniform(tuple(out.shape), seed=18, tensor="gate", lead=3)
+    _compare(fl, f"evo_col_Nr{Nr}", tuple(ins[n].contiguous() for n in ("q", "k", "v")), (q, k, v), out, lse, dout,
+             kw, ok)
+
+
 def test_backward_unsupported_is_loud(fl):
     q = torch.zeros(1, 2, 128, 64, device="cuda", dtype=torch.bfloat16)
     o, lse = fl.attn_fwd(q, q, q[:, :1].expand(1, 2, 128, 64).contiguous(), return_lse=True)
     g = torch.ones_like(o)
     with pytest.raises(fl.FlError, match="UNSUPPORTED"):
         fl.attn_bwd(q, q, q, o, lse, o.clone(), gate_mode="mul", gate=g)
-    q32 = torch.zeros(1, 1, 128, 32, device="cuda", dtype=torch.bfloat16)
-    o32, l32 = fl.attn_fwd(q32, q32, q32, return_lse=True)
+    bias = torch.zeros(1, 2, 128, 128, device="cuda", dtype=torch.bfloat16)
+    ob, lb = fl.attn_fwd(q, q, q, return_lse=True, bias=bias)
     with pytest.raises(fl.FlError, match="UNSUPPORTED"):
-        fl.attn_bwd(q32, q32, q32, o32, l32, o32)
+        fl.attn_bwd(q, q, q, ob, lb, ob.clone(), bias=bias)
