@@ -83,7 +83,8 @@ def lib():
                                       C.POINTER(C.c_uint8)]
         _lib.flo_keep_row.restype = C.c_int
         _lib.flo_attn_bwd.argtypes = [C.POINTER(_Problem), C.POINTER(_Tensor), C.POINTER(C.c_double),
-                                      C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]
+                                      C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                      C.POINTER(C.c_double)]
         _lib.flo_attn_bwd.restype = C.c_int
         dp = C.POINTER(C.c_double)
         _lib.flo_linear_ln.argtypes = [C.c_int64, C.c_int64, C.c_int64, dp, dp, dp, dp, dp, C.c_double, dp, dp]
@@ -176,9 +177,10 @@ def attn(q, k, v, *, scale=0.0, mod="none", softcap=0.0, alibi_slopes=None,
     return out, lse
 
 
-def attn_bwd(q, k, v, dout, with_dgate=False, **variant):
+def attn_bwd(q, k, v, dout, with_dgate=False, with_dbias=False, **variant):
     """Gradients (dq, dk, dv) of L = sum(O * dout), fp64 numpy arrays shaped like q, k, v (NEXT-3); with
-    with_dgate also dL/dgate (shaped like dout) for a gated variant."""
+    with_dgate also dL/dgate (shaped like dout) for a gated variant, with with_dbias also dL/dbias as the
+    full logical [B, G, Hq, Sq, Sk] array (sum it over the dims the bias broadcasts)."""
     keep: list = []
     p = _problem(q, k, v, keep, **variant)
     dt = _tensor(dout, keep)
@@ -186,12 +188,17 @@ def attn_bwd(q, k, v, dout, with_dgate=False, **variant):
     dk = np.zeros(tuple(k.shape), dtype=np.float64)
     dv = np.zeros(tuple(v.shape), dtype=np.float64)
     dg = np.zeros(tuple(dout.shape), dtype=np.float64) if with_dgate else None
-    rc = lib().flo_attn_bwd(C.byref(p), C.byref(dt), dq.ctypes.data_as(C.POINTER(C.c_double)),
-                            dk.ctypes.data_as(C.POINTER(C.c_double)), dv.ctypes.data_as(C.POINTER(C.c_double)),
-                            dg.ctypes.data_as(C.POINTER(C.c_double)) if with_dgate else None)
+    qs = tuple(q.shape) if q.dim() == 5 else (q.shape[0], 1) + tuple(q.shape[1:])
+    maps = 2 if variant.get("diff") else 1
+    B, G, Hq, Sq = qs[0], qs[1], qs[2] // maps, qs[3]
+    Sk = tuple(k.shape)[-2]
+    db = np.zeros((B, G, Hq, Sq, Sk), dtype=np.float64) if with_dbias else None
+    dpp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double)) if a is not None else None
+    rc = lib().flo_attn_bwd(C.byref(p), C.byref(dt), dpp(dq), dpp(dk), dpp(dv), dpp(dg), dpp(db))
     if rc != 0:
         raise ValueError(f"flo_attn_bwd rejected the problem (code {rc})")
-    return (dq, dk, dv, dg) if with_dgate else (dq, dk, dv)
+    out = (dq, dk, dv) + ((dg,) if with_dgate else ()) + ((db,) if with_dbias else ())
+    return out
 
 
 def keep_rows(q, k, v, rows, **variant):

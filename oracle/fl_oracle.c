@@ -252,7 +252,11 @@ int flo_keep_row(const flo_problem* p, int64_t b, int64_t g, int64_t h, int64_t 
 /* dgate (optional, may be NULL): dL/dgate for the Evoformer gate of reading G9 (O = gate'(g) * A, AF2
  * Alg.7 line 6): dgate = dO * A * sigma(g) (1 - sigma(g)) (sigmoid) or dO * A (mul), A the map-combined
  * attention output before the gate (sum over maps of coef * P V). */
-int flo_attn_bwd(const flo_problem* p, const flo_tensor* dout, double* dq, double* dk, double* dv, double* dgate) {
+/* dbias (optional, may be NULL): dL/dbias for the additive score bias of Eq.4 / G16 (s = scale q.k + bias
+ * before the softcap), logical [B, G, Hq, Sq, Sk] contiguous: the score gradient dx of each kept (q, k) --
+ * the caller sums it over the dims its bias broadcasts (e.g. the MSA rows s of the Evoformer pair bias). */
+int flo_attn_bwd(const flo_problem* p, const flo_tensor* dout, double* dq, double* dk, double* dv, double* dgate,
+                 double* dbias) {
   int64_t maps;
   int rc = check_problem(p, &maps);
   if (rc) return rc;
@@ -267,6 +271,8 @@ int flo_attn_bwd(const flo_problem* p, const flo_tensor* dout, double* dq, doubl
   for (int64_t i = 0; i < nv; ++i) dv[i] = 0.0;
   if (dgate)
     for (int64_t i = 0; i < B * G * Hq * Sq * Dv; ++i) dgate[i] = 0.0;
+  if (dbias)
+    for (int64_t i = 0; i < B * G * Hq * Sq * Sk; ++i) dbias[i] = 0.0;
   /* one task per (b, g, kv head): every write of the task stays inside it */
 #pragma omp parallel
   {
@@ -350,6 +356,7 @@ int flo_attn_bwd(const flo_problem* p, const flo_tensor* dout, double* dq, doubl
                 const double t = sc[k] / p->softcap;
                 dx *= 1.0 - t * t;
               }
+              if (dbias) dbias[(((b * G + g) * Hq + h) * Sq + q) * Sk + k] += dx;   /* maps share the bias */
               for (int64_t d = 0; d < Dqk; ++d) {
                 dq[((((b * G + g) * Hq * maps) + qh) * Sq + q) * Dqk + d] +=
                     scale * dx * elem(&p->k, off5(&p->k, b, g, kh, k, d));

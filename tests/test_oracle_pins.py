@@ -585,7 +585,8 @@ def test_diff_transformer_epilogue_brute_force_and_closed_forms():
 @pytest.mark.parametrize("kw", [dict(), dict(mask="causal"), dict(mask="sliding", window=2), dict(mod="alibi"),
                                 dict(mod="softcap", softcap=0.7), dict(mask="prefix", prefix=2),
                                 dict(gate_mode="sigmoid"), dict(gate_mode="mul"), dict(diff=True, lam=0.4),
-                                dict(diff=True, lam=0.4, gate_mode="sigmoid"), dict(gqa=True)])
+                                dict(diff=True, lam=0.4, gate_mode="sigmoid"), dict(gqa=True),
+                                dict(bias=True, mod="softcap", softcap=0.9), dict(bias="bcast", mask="causal")])
 def test_backward_matches_central_differences(kw):
     """The oracle's dQ, dK, dV (plain chain rule) against central differences of the oracle's own
     FORWARD (an independent route: no derivative formula involved), L = sum(O * dO), h = 1e-6."""
@@ -600,13 +601,23 @@ def test_backward_matches_central_differences(kw):
     if kw.get("gate_mode"):
         kw["gate"] = rnd(1, H, S, D, seed=94, lo=-2, hi=2)
     gated = bool(kw.get("gate_mode"))
-    if gated:
-        dq, dk, dv, dg = oracle.attn_bwd(q, k, v, do, with_dgate=True, **kw)
-    else:
-        dq, dk, dv = oracle.attn_bwd(q, k, v, do, **kw)
+    bias_kind = kw.pop("bias", None)
+    if bias_kind:                  # additive bias (G16); "bcast": one [H, S, S] bias broadcast over B = 2
+        if bias_kind == "bcast":
+            q, k, v, do = (torch.cat([t, t * 0.5 + 0.1]) for t in (q, k, v, do))
+            base = rnd(1, H, S, S, seed=95, lo=-1, hi=1)
+            kw["bias"] = base.expand(2, H, S, S)
+        else:
+            base = rnd(1, H, S, S, seed=95, lo=-1, hi=1)
+            kw["bias"] = base
+    outs = oracle.attn_bwd(q, k, v, do, with_dgate=gated, with_dbias=bool(bias_kind), **kw)
+    dq, dk, dv = outs[:3]
     L = lambda q_, k_, v_: float((oracle.attn(q_, k_, v_, **kw)[0].reshape(do.shape) * do.numpy()).sum())
     h = 1e-6
-    pairs = [(q, dq), (k, dk), (v, dv)] + ([(kw["gate"], dg)] if gated else [])   # the gate is read through kw
+    pairs = [(q, dq), (k, dk), (v, dv)] + ([(kw["gate"], outs[3])] if gated else [])   # the gate is read through kw
+    if bias_kind:              # dbias summed over the dims the bias broadcasts (B for "bcast"), shaped like base
+        db = outs[-1].sum(axis=0, keepdims=True) if bias_kind == "bcast" else outs[-1]
+        pairs.append((base, db.reshape(base.shape)))
     for t, grad in pairs:
         num = np.zeros(grad.shape)
         flat = t.view(-1)
