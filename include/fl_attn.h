@@ -157,7 +157,7 @@ fl_status fl_attn_fwd(const fl_attn_args* args);
  * (a KV-tile-major dK/dV pass and a query-tile-major dQ pass, two compute warpgroups each, no atomics).
  * Supported (v3): bf16, rank-4 or rank-5 q/k/v (G), D_qk == D_v in {32, 64, 128}, GQA, masks none /
  * causal / sliding / prefix / document (either alignment), mods none / ALiBi / softcap, key_mask (MSA
- * mask), sigmoid gate (+ dgate).  Not yet: diff, additive bias, mul gate, block lists, paged KV, fp32
+ * mask), sigmoid gate (+ dgate), additive bias (+ dbias).  Not yet: diff, mul gate, block lists, paged KV, fp32
  * (FL_ERR_UNSUPPORTED).  Workspace (fl_attn_bwd_workspace_size): 4 B G Hq S_q bytes (Dvec) + the packed
  * key mask + 2 B G Hq S_q D_v bytes with a sigmoid gate, each 256-byte rounded. */
 typedef struct {
@@ -170,6 +170,9 @@ typedef struct {
   void* workspace;
   size_t workspace_bytes;
   fl_tensor dgate;           /* optional (gate_mode sigmoid): dL/dgate-logits, bf16, the gate's shape (ABI v3) */
+  fl_tensor dbias;           /* optional (with a bias): dL/dbias, f32, the bias's shape; dims the bias broadcasts
+                                (stride 0 or size 1) are summed over; must be compact -- the call zeroes it and
+                                accumulates with fp32 atomics (ABI v3) */
 } fl_attn_bwd_args;
 
 fl_status fl_attn_bwd(const fl_attn_bwd_args* args);

@@ -49,7 +49,8 @@ class AttnArgs(C.Structure):
 class BwdArgs(C.Structure):
     _fields_ = [("q", Tensor), ("k", Tensor), ("v", Tensor), ("o", Tensor), ("lse", Tensor), ("dout", Tensor),
                 ("dq", Tensor), ("dk", Tensor), ("dv", Tensor), ("var", Variant), ("stream", C.c_void_p),
-                ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t), ("dgate", Tensor)]
+                ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t), ("dgate", Tensor),
+                ("dbias", Tensor)]
 
 
 class LinearArgs(C.Structure):

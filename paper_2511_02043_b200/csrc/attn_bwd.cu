@@ -141,9 +141,11 @@ __device__ __forceinline__ uint64_t mnmajor_desc(uint32_t base, int kk) {
 // Per-element score of the forward (natural units) for query row q (absolute q_abs), key k, head h:
 // scale s (+ ALiBi) (-> softcap), plus the softcap derivative factor.
 template <int MOD>
-__device__ __forceinline__ float bwd_score(const AttnParams& p, float s_raw, float slope, int k, int q_abs, float& ft) {
+__device__ __forceinline__ float bwd_score(const AttnParams& p, float s_raw, float slope, int k, int q_abs, float& ft,
+                                           float bias = 0.f) {
   float x = s_raw * p.scale;
   if (MOD == MOD_ALIBI) x = fmaf(slope, (float)(k - q_abs), x);
+  x += bias;                                         // additive bias before the softcap (G16)
   ft = 1.f;
   if (MOD == MOD_SOFTCAP) {
     const float t = tanh_approx(x / p.softcap);
@@ -151,6 +153,14 @@ __device__ __forceinline__ float bwd_score(const AttnParams& p, float s_raw, flo
     x = p.softcap * t;
   }
   return x;
+}
+
+// additive score bias of (b, g, h, q, k) (bf16 or f32, any strides incl. broadcast), 0 when absent
+__device__ __forceinline__ float bias_at(const AttnParams& p, int b, int g, int h, int q, int k) {
+  if (!p.bias) return 0.f;
+  const int64_t off = b * p.bs.b + g * p.bs.g + (int64_t)h * p.bs.h + (int64_t)q * p.bs.s + (int64_t)k * p.bs.d;
+  return p.bias_dtype == 1 ? __ldg(static_cast<const float*>(p.bias) + off)
+                           : __bfloat162float(__ldg(static_cast<const __nv_bfloat16*>(p.bias) + off));
 }
 
 __device__ __forceinline__ float head_slope(const AttnParams& p, int h) {
@@ -336,8 +346,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int t = 0; t < 4; ++t) {
             const int q = q0 + j0 + j + t;
             float ft;
-            const float s = bwd_score<MOD>(p, __uint_as_float(sv[j + t]), slope_l2, k, q + p.q_off, ft);
             const bool keep = key_on && (full_tile || (k >= riv[j0 + j + t] && k < riv[128 + j0 + j + t]));   // hi <= S_k
+            const float bv = keep ? bias_at(p, b, g, hh, q, k) : 0.f;
+            const float s = bwd_score<MOD>(p, __uint_as_float(sv[j + t]), slope_l2, k, q + p.q_off, ft, bv);
             pr[t] = keep ? ex2(fmaf(s, kBwdLog2e, -lsev[t])) : 0.f;
             f[t] = ft;
           }
@@ -431,7 +442,8 @@ template <int D, int MOD>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     bwd_dq_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ TmaMaps maps,
                   const __grid_constant__ CUtensorMap tdo, const float* __restrict__ lse_g, Strided5 ls,
-                  const float* __restrict__ dvec, __nv_bfloat16* __restrict__ dq, Strided5 dqs) {
+                  const float* __restrict__ dvec, __nv_bfloat16* __restrict__ dq, Strided5 dqs,
+                  float* __restrict__ dbias, Strided5 dbs) {
   using C = BwdCfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -564,9 +576,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         for (int t = 0; t < 2; ++t) {
           const int k = k0 + j0 + j + t;
           float ft;
-          const float s = bwd_score<MOD>(p, __uint_as_float(sv[j + t]), slope_l2, k, q_abs, ft);
           const bool kon = (((j + t) < 32 ? kw0 : kw1) >> ((j + t) & 31)) & 1u;
           const bool keep = kon && (full_tile || (k >= iv.lo && k < iv.hi && k < p.Sk));
+          const float bv = keep ? bias_at(p, b, g, h, q, k) : 0.f;
+          const float s = bwd_score<MOD>(p, __uint_as_float(sv[j + t]), slope_l2, k, q_abs, ft, bv);
           pr[t] = keep ? ex2(fmaf(s, kBwdLog2e, -lse_l2)) : 0.f;
           f[t] = ft;
         }
@@ -591,6 +604,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             d1 *= bf16_hi(fw);
           }
           ds[j >> 1] = pack_bf16(d0, d1);
+          if (dbias && row_ok) {                    // dL/dbias = dS (fp32 atomics: broadcast dims accumulate)
+            const int k = k0 + j0 + c + j;
+            const int64_t off = b * dbs.b + g * dbs.g + (int64_t)h * dbs.h + (int64_t)q * dbs.s + (int64_t)k * dbs.d;
+            if (k < p.Sk && d0 != 0.f) atomicAdd(dbias + off, d0);
+            if (k + 1 < p.Sk && d1 != 0.f) atomicAdd(dbias + off + dbs.d, d1);
+          }
         }
         tmem_st16(tmem + lane_base + COL_S + 64 + ((j0 + c) >> 1), ds);
       }
@@ -637,6 +656,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 // ---------------------------------------------------------------- launch
 struct BwdLaunch {
   const float* lse; Strided5 ls;
+  float* dbias; Strided5 dbs;
   const __nv_bfloat16* dout; Strided5 dos;
   float* dvec;
   __nv_bfloat16 *dq, *dk, *dv;
@@ -655,7 +675,7 @@ static cudaError_t launch_bwd_dm(const AttnParams& p, const TmaMaps& maps, const
   bwd_dkdv_kernel<D, MOD><<<p.B * p.G * p.Hkv * n_kt, kBwdThreads, C::SMEM_TOTAL, s>>>(p, maps, tdo, L.lse, L.ls, L.dvec, L.dk, L.dks,
                                                                         L.dv, L.dvs);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  bwd_dq_kernel<D, MOD><<<p.B * p.G * p.Hq * n_qt, kBwdThreads, C::SMEM_TOTAL, s>>>(p, maps, tdo, L.lse, L.ls, L.dvec, L.dq, L.dqs);
+  bwd_dq_kernel<D, MOD><<<p.B * p.G * p.Hq * n_qt, kBwdThreads, C::SMEM_TOTAL, s>>>(p, maps, tdo, L.lse, L.ls, L.dvec, L.dq, L.dqs, L.dbias, L.dbs);
   return cudaGetLastError();
 }
 
@@ -685,8 +705,8 @@ cudaError_t launch_bwd_prepass(const AttnParams& p, const void* dout, Strided5 d
 
 cudaError_t launch_attn_bwd(const AttnParams& p, const TmaMaps& maps, const CUtensorMap& tdo, const float* lse,
                             Strided5 ls, const void* dout, Strided5 dos, float* dvec, void* dq, Strided5 dqs, void* dk,
-                            Strided5 dks, void* dv, Strided5 dvs, cudaStream_t s) {
-  BwdLaunch L{lse, ls, static_cast<const __nv_bfloat16*>(dout), dos, dvec, static_cast<__nv_bfloat16*>(dq),
+                            Strided5 dks, void* dv, Strided5 dvs, float* dbias, Strided5 dbs, cudaStream_t s) {
+  BwdLaunch L{lse, ls, dbias, dbs, static_cast<const __nv_bfloat16*>(dout), dos, dvec, static_cast<__nv_bfloat16*>(dq),
               static_cast<__nv_bfloat16*>(dk), static_cast<__nv_bfloat16*>(dv), dqs, dks, dvs};
   switch (p.Dqk) {
     case 128: return launch_bwd_d<128>(p, maps, tdo, L, s);

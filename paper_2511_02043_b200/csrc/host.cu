@@ -46,7 +46,7 @@ cudaError_t launch_bwd_prepass(const AttnParams& p, const void* dout, Strided5 d
                                Strided5 dgs, cudaStream_t s);
 cudaError_t launch_attn_bwd(const AttnParams& p, const TmaMaps& maps, const CUtensorMap& tdo, const float* lse,
                             Strided5 ls, const void* dout, Strided5 dos, float* dvec, void* dq, Strided5 dqs, void* dk,
-                            Strided5 dks, void* dv, Strided5 dvs, cudaStream_t s);
+                            Strided5 dks, void* dv, Strided5 dvs, float* dbias, Strided5 dbs, cudaStream_t s);
 }  // namespace fl
 
 using namespace fl;
@@ -692,8 +692,9 @@ fl_status fl_debug_schedule(const fl_attn_args* args, int32_t* out, int64_t out_
 namespace {
 struct BwdPrepared {
   Prepared P;
-  View5 dout, dq, dk, dv, dgate;
+  View5 dout, dq, dk, dv, dgate, dbias;
   size_t ws = 0, off_bits = 0, off_da = 0;
+  int64_t dbias_span = 0;
 };
 
 fl_status prepare_bwd(const fl_attn_bwd_args* a, BwdPrepared& B, bool device_ptrs) {
@@ -708,9 +709,8 @@ fl_status prepare_bwd(const fl_attn_bwd_args* a, BwdPrepared& B, bool device_ptr
   const AttnParams& p = B.P.p;
   if (!B.P.bf16) return fail(FL_ERR_UNSUPPORTED, "backward: bf16 q/k/v/o");
   if (p.Dqk != 32 && p.Dqk != 64 && p.Dqk != 128) return fail(FL_ERR_UNSUPPORTED, "backward: D in {32, 64, 128}");
-  if (var.diff || var.bias.data || var.kv_page_table.data || var.mask == FL_MASK_BLOCKLIST ||
-      var.gate_mode == FL_GATE_MUL)
-    return fail(FL_ERR_UNSUPPORTED, "backward: no diff / bias / block list / paged KV / mul gate");
+  if (var.diff || var.kv_page_table.data || var.mask == FL_MASK_BLOCKLIST || var.gate_mode == FL_GATE_MUL)
+    return fail(FL_ERR_UNSUPPORTED, "backward: no diff / block list / paged KV / mul gate");
   if (!a->lse.data) return fail(FL_ERR_INVALID_ARGUMENT, "backward needs the forward's lse");
   const int R = B.P.q_rank;
   const fl_tensor* ts[4] = {&a->dout, &a->dq, &a->dk, &a->dv};
@@ -732,6 +732,27 @@ fl_status prepare_bwd(const fl_attn_bwd_args* a, BwdPrepared& B, bool device_ptr
       if (B.dgate.size[d] != B.P.o.size[d]) return fail(FL_ERR_SHAPE_MISMATCH, "dgate must have o's shape");
     if (B.dgate.stride[4] != 1 || !aligned16(B.dgate)) return fail(FL_ERR_MISALIGNED, "dgate: contiguous last dim, 16-byte aligned");
   }
+  // dbias (optional, with a bias): f32 with the bias's shape; its stride-0 (broadcast) dims accumulate. It must
+  // be compact (no gaps between its elements) because the call zeroes its span before the atomics.
+  if (a->dbias.data) {
+    if (!var.bias.data) return fail(FL_ERR_INVALID_ARGUMENT, "dbias needs a bias");
+    if (a->dbias.dtype != FL_F32 || a->dbias.rank != var.bias.rank)
+      return fail(FL_ERR_SHAPE_MISMATCH, "dbias: f32 with the bias's rank");
+    for (int d = 0; d < a->dbias.rank; ++d)
+      if (a->dbias.size[d] != var.bias.size[d]) return fail(FL_ERR_SHAPE_MISMATCH, "dbias must have the bias's shape");
+    if (!to_view(a->dbias, R, 0, B.dbias)) return fail(FL_ERR_SHAPE_MISMATCH, "dbias rank");
+    int64_t want_span = 1, span = 1;
+    for (int d = 0; d < 5; ++d) {
+      if (B.dbias.size[d] == 1) B.dbias.stride[d] = 0;
+      if (B.dbias.size[d] > 1 && B.dbias.stride[d] != 0) want_span *= B.dbias.size[d];
+      if (B.dbias.stride[d] < 0) return fail(FL_ERR_UNSUPPORTED, "dbias: negative strides");
+      span += (B.dbias.size[d] - 1) * B.dbias.stride[d];
+    }
+    if (span != want_span) return fail(FL_ERR_UNSUPPORTED, "dbias must be compact (its span is zeroed by the call)");
+    for (int d = 0; d < 5; ++d)                      // the kernel indexes it in the bias's broadcast form
+      if (B.dbias.size[d] != B.P.bias.size[d] && B.dbias.size[d] == 1) B.dbias.size[d] = B.P.bias.size[d];
+    B.dbias_span = span;
+  }
   for (int i = 1; i < 4; ++i)
     for (const View5* in : {&B.P.q, &B.P.k, &B.P.v, &B.P.o, &B.dout, &B.P.gate})
       if (overlaps(*vs[i], *in)) return fail(FL_ERR_INVALID_ARGUMENT, "gradients must not overlap inputs");
@@ -742,6 +763,7 @@ fl_status prepare_bwd(const fl_attn_bwd_args* a, BwdPrepared& B, bool device_ptr
     for (int i = 0; i < 4; ++i)
       if (!on_device(ts[i]->data)) return fail(FL_ERR_INVALID_ARGUMENT, "dout / dq / dk / dv must be device memory");
     if (!on_device(a->dgate.data)) return fail(FL_ERR_INVALID_ARGUMENT, "dgate must be device memory");
+    if (!on_device(a->dbias.data)) return fail(FL_ERR_INVALID_ARGUMENT, "dbias must be device memory");
   }
   // workspace: Dvec f32 [B,G,Hq,Sq] | packed key mask | dO * s(g) bf16 [B,G,Hq,Sq,Dv] (sigmoid gate)
   B.ws = ((size_t)p.B * p.G * p.Hq * p.Sq * sizeof(float) + 255) & ~size_t(255);
@@ -804,12 +826,16 @@ fl_status fl_attn_bwd(const fl_attn_bwd_args* args) {
   int bg, bb;
   if ((s = encode_map(vda, ch, &tdo, &bg, &bb)) != FL_OK) return s;
   float* dvec = reinterpret_cast<float*>(ws);
+  if (B.dbias.present) {
+    e = cudaMemsetAsync(B.dbias.data, 0, (size_t)B.dbias_span * sizeof(float), stream);
+    if (e != cudaSuccess) return cuda_fail(e, "dbias reset");
+  }
   e = launch_bwd_prepass(p, B.dout.data, strides_of(B.dout), dvec, da, B.dgate.data, strides_of(B.dgate), stream);
   ++g_launches;
   if (e != cudaSuccess) return cuda_fail(e, "backward pre-pass launch");
   e = launch_attn_bwd(p, maps, tdo, static_cast<const float*>(B.P.lse.data), strides_of(B.P.lse), B.dout.data,
                       strides_of(B.dout), dvec, B.dq.data, strides_of(B.dq), B.dk.data, strides_of(B.dk), B.dv.data,
-                      strides_of(B.dv), stream);
+                      strides_of(B.dv), static_cast<float*>(B.dbias.data), strides_of(B.dbias), stream);
   g_launches += 2;
   return e == cudaSuccess ? FL_OK : cuda_fail(e, "backward launch");
 }

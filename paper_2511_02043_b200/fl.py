@@ -177,7 +177,7 @@ def _keep_alive_on(stream, tensors):
             t.record_stream(stream)
 
 
-def attn_bwd(q, k, v, out, lse, dout, *, dq=None, dk=None, dv=None, dgate=None, workspace=None, **variant):
+def attn_bwd(q, k, v, out, lse, dout, *, dq=None, dk=None, dv=None, dgate=None, dbias=None, workspace=None, **variant):
     """Backward of attn_fwd (fl_attn_bwd, NEXT-3): returns (dq, dk, dv) of L = sum(out * dout), given the
     forward's output and natural-log LSE (attn_fwd(..., return_lse=True)); with a sigmoid gate also dgate
     (dL/dgate-logits): (dq, dk, dv, dgate)."""
@@ -193,6 +193,7 @@ def attn_bwd(q, k, v, out, lse, dout, *, dq=None, dk=None, dv=None, dgate=None, 
     a.q, a.k, a.v, a.o, a.lse = fa.q, fa.k, fa.v, fa.o, fa.lse
     a.dout, a.dq, a.dk, a.dv = tensor(dout), tensor(dq), tensor(dk), tensor(dv)
     a.dgate = tensor(dgate)
+    a.dbias = tensor(dbias)        # optional: pass an f32 tensor shaped like the bias to receive dL/dbias
     a.var = fa.var
     a.stream = fa.stream
     need = C.c_size_t(0)

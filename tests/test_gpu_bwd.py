@@ -86,13 +86,58 @@ def test_backward_evoformer_column(fl, Nr):
              kw, ok)
 
 
+@pytest.mark.parametrize("bias_dtype,D", [("bf16", 64), ("f32", 128)])
+def test_backward_bias(fl, bias_dtype, D):
+    """Additive score bias (G16) with dL/dbias (f32 atomics) against the oracle's dbias."""
+    case = dict(Hq=2, S=260, D=D, bias=bias_dtype, mask="causal", dist="needle")
+    ins, gk, ok = cases.build(dict(case, dtype="bf16"))
+    q, k, v = (ins[n].cuda() for n in ("q", "k", "v"))
+    kw = {x: cases.to_dev(y, "cuda") for x, y in gk.items()}
+    out, lse = fl.attn_fwd(q, k, v, return_lse=True, **kw)
+    dout = synth.uniform(tuple(out.shape), seed=19, tensor="gate")
+    dbias = torch.empty(kw["bias"].shape, dtype=torch.float32, device="cuda")
+    dq, dk, dv = fl.attn_bwd(q, k, v, out, lse, dout.cuda(), dbias=dbias, **kw)
+    torch.cuda.synchronize()
+    rq, rk, rv, rb = oracle.attn_bwd(ins["q"], ins["k"], ins["v"], dout, with_dbias=True, **ok)
+    for name, got, ref in (("dq", dq, rq), ("dk", dk, rk), ("dv", dv, rv), ("dbias", dbias, rb.reshape(dbias.shape))):
+        r = check(got.cpu().double().numpy(), ref, 2e-2, what=f"bias {bias_dtype} D{D} {name}")
+        if r["max_ref"] >= 0.05:
+            assert r["max_abs"] <= 0.05 * r["max_ref"], f"bias {name}: {r}"
+
+
+@pytest.mark.parametrize("Nr", [100, 300])
+def test_backward_evoformer_row(fl, Nr):
+    """The Evoformer row attention (AF2 Alg.7, reading G9): rank-5 views, D = 32, the pair bias broadcast
+    over the MSA rows s (dbias = sum over s of dS, accumulated by the atomics), sigmoid gate (+ dgate),
+    MSA key mask."""
+    Ns = 6
+    ins, gk, ok = cases.evoformer(dict(kind="row", B=1, Ns=Ns, Nr=Nr, H=2, c=32, p_zero=0.1))
+    q, k, v = (ins[n].cuda().contiguous() for n in ("q", "k", "v"))
+    kw = {x: cases.to_dev(y, "cuda") for x, y in gk.items()}
+    kw["gate"] = kw["gate"].contiguous()
+    ok = dict(ok, gate=ok["gate"].contiguous())
+    out, lse = fl.attn_fwd(q, k, v, return_lse=True, **kw)
+    dout = synth.uniform(tuple(out.shape), seed=20, tensor="gate", lead=3)
+    dbias = torch.empty(1, 1, 2, Nr, Nr, dtype=torch.float32, device="cuda").expand(kw["bias"].shape)
+    dq, dk, dv, dg = fl.attn_bwd(q, k, v, out, lse, dout.cuda(), dbias=dbias, **kw)
+    torch.cuda.synchronize()
+    host = tuple(ins[n].contiguous() for n in ("q", "k", "v"))
+    rq, rk, rv, rg, rb = oracle.attn_bwd(*host, dout, with_dgate=True, with_dbias=True, **ok)
+    rb = rb.sum(axis=1, keepdims=True)                 # the pair bias broadcasts over s
+    for name, got, ref in (("dq", dq, rq), ("dk", dk, rk), ("dv", dv, rv), ("dgate", dg, rg),
+                           ("dbias", dbias[:, :1], rb)):
+        r = check(got.cpu().double().numpy(), ref, 2e-2 * (Ns if name == "dbias" else 1), what=f"evo row {name}")
+        if r["max_ref"] >= 0.05:
+            assert r["max_abs"] <= 0.05 * r["max_ref"], f"evo row {name}: {r}"
+
+
 def test_backward_unsupported_is_loud(fl):
     q = torch.zeros(1, 2, 128, 64, device="cuda", dtype=torch.bfloat16)
     o, lse = fl.attn_fwd(q, q, q[:, :1].expand(1, 2, 128, 64).contiguous(), return_lse=True)
     g = torch.ones_like(o)
     with pytest.raises(fl.FlError, match="UNSUPPORTED"):
         fl.attn_bwd(q, q, q, o, lse, o.clone(), gate_mode="mul", gate=g)
-    bias = torch.zeros(1, 2, 128, 128, device="cuda", dtype=torch.bfloat16)
-    ob, lb = fl.attn_fwd(q, q, q, return_lse=True, bias=bias)
-    with pytest.raises(fl.FlError, match="UNSUPPORTED"):
-        fl.attn_bwd(q, q, q, ob, lb, ob.clone(), bias=bias)
+    q2 = torch.zeros(1, 4, 128, 64, device="cuda", dtype=torch.bfloat16)
+    od, ld = fl.attn_fwd(q2, q2, q, diff=True, lam=0.3), None
+    with pytest.raises(fl.FlError):
+        fl.attn_bwd(q2, q2, q, od, torch.zeros(1, 2, 128, device="cuda"), od.clone(), diff=True, lam=0.3)
