@@ -454,6 +454,17 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   // not redo decode_work's integer divisions on their critical path at every unit start
   // (small heads only: their units are a few tiles long; at D >= 64 the registers the loaded fields occupy
   // cost more in spills than the recomputation, which the compiler can rematerialise from the parameters)
+  auto unit_work_pub = [&](int it) -> Work {
+    const uint32_t* sc = sched_base + (it & 1) * C::SCHED_WORDS;
+    const int* f = reinterpret_cast<const int*>(sc + C::WORK_OFF);
+    Work w;
+    w.b = f[0]; w.g = f[1]; w.g1 = f[2]; w.h = f[3];
+    w.q0[0] = f[4]; w.q0[1] = f[5];
+    w.lo[0] = f[6]; w.hi[0] = f[7]; w.lo[1] = f[8]; w.hi[1] = f[9];
+    w.lo_cta = f[10]; w.hi_cta = f[11];
+    w.sched = LIST ? sc : nullptr;
+    return w;
+  };
   auto unit_work = [&](int u, int it) -> Work {
     if constexpr (D > 32) {
       Work w = decode_work<D, DIFF, LIST, (PAIR != 0)>(p, u);
@@ -685,7 +696,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       for (;; ++it) {
         const int u = get_unit(it);
         if (u >= n_units) break;
-        const Work w = unit_work(u, it);
+        const Work w = unit_work_pub(it);           // published by the producer: no decode on the MMA's path
         it_mma = it;
         first_pv[0] = first_pv[1] = true;
         int j = next_tile(w, w.lo_cta - 1);
