@@ -116,6 +116,15 @@ struct BwdCfg {
   static constexpr uint32_t IDESC_NN = idesc_bf16_f32(128, 128, 0);   // [128 x D] . [128 x D]^T (both K-major)
   static constexpr uint32_t IDESC_ND = idesc_bf16_f32(128, D, 1);     // TMEM A [128 x 128] . smem B [128 x D] MN-major
   static constexpr int NST = 2;                      // ring stages (pairs of tiles)
+  // dK/dV kernel: 64-query items (Q and dO half tiles), two in flight (one per compute warpgroup)
+  static constexpr int HCHUNK = 64 * SWB;            // 64 rows x SWB bytes
+  static constexpr int HALF_BYTES = 64 * D * 2;
+  static constexpr int NSTH = 4;                     // ring stages of (Q half, dO half)
+  static constexpr uint32_t IDESC_N64 = idesc_bf16_f32(128, 64, 0);  // K [128 x D] . Q_half [64 x D]^T
+  static constexpr int KV_RING = 2 * TILE_BYTES;
+  static constexpr int KV_ROWS = KV_RING + NSTH * 2 * HALF_BYTES;
+  static constexpr int KV_BAR = KV_ROWS + NSTH * 256 * 4;          // per stage: lse, dvec, lo, hi of 64 rows
+  static constexpr int KV_SMEM = KV_BAR + 256 + 1024;
   // smem: two resident tiles | NST x two streamed tiles | per-stage LSE / Dvec rows (dkdv) | barriers
   static constexpr int SMEM_FIXED = 0;
   static constexpr int SMEM_RING = 2 * TILE_BYTES;
@@ -130,6 +139,17 @@ __device__ __forceinline__ uint64_t kmajor_desc(uint32_t base, int kk) {
   using C = BwdCfg<D>;
   const uint32_t off = (kk * 16 / C::CH) * C::CHUNK_BYTES + (kk * 16 % C::CH) * 2;
   return smem_desc(base + off, 16, C::SBO, C::LAYOUT);
+}
+// K-major / MN-major descriptors for a tile whose 64-column chunks are `chunk` bytes apart (64-row half tiles)
+template <int D>
+__device__ __forceinline__ uint64_t kmajor_desc_c(uint32_t base, int kk, uint32_t chunk) {
+  using C = BwdCfg<D>;
+  return smem_desc(base + (kk * 16 / C::CH) * chunk + (kk * 16 % C::CH) * 2, 16, C::SBO, C::LAYOUT);
+}
+template <int D>
+__device__ __forceinline__ uint64_t mnmajor_desc_c(uint32_t base, int kk, uint32_t chunk) {
+  using C = BwdCfg<D>;
+  return smem_desc(base + kk * 16 * C::SWB, chunk, C::SBO, C::LAYOUT);
 }
 // the same tile read as an MN-major B operand [K = its 128 rows, N = D], K step kk
 template <int D>
@@ -168,29 +188,32 @@ __device__ __forceinline__ float head_slope(const AttnParams& p, int h) {
 }
 
 // ================================================================ dK / dV
-// grid = B * Hkv * n_kvtile (kv tile ascending within a head: causal's heaviest tiles first), 320 threads:
-// warps 0-7 compute (thread = key row; warpgroup w takes query columns [64 w, 64 w + 64)), warp 8 TMA
-// producer, warp 9 MMA issuer + TMEM allocator.
-template <int D, int MOD>
+// grid = B * G * Hkv * n_kvtile, 320 threads: warps 0-7 compute (thread = key row), warp 8 TMA producer,
+// warp 9 MMA issuer + TMEM allocator.  Items are 64-query halves of the needed query tiles; warpgroup w
+// takes items e = w (mod 2) in TMEM slot w (S^T [0, 64) and dP^T [64, 128) of slot w's 128 columns, P^T
+// and dS^T written back over S^T), so the MMAs of item e + 1 (the other slot) run while warpgroup w works
+// on item e -- the forward's ping-pong: S^T(e+2), dP^T(e+2) are issued right after dV(e), dK(e) consumed
+// slot w.
+template <int D, int MOD, bool BIAS>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     bwd_dkdv_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ TmaMaps maps,
-                    const __grid_constant__ CUtensorMap tdo, const float* __restrict__ lse_g, Strided5 ls,
-                    const float* __restrict__ dvec, __nv_bfloat16* __restrict__ dk, Strided5 dks,
-                    __nv_bfloat16* __restrict__ dv, Strided5 dvs) {
+                    const __grid_constant__ CUtensorMap tq64, const __grid_constant__ CUtensorMap tdo64,
+                    const float* __restrict__ lse_g, Strided5 ls, const float* __restrict__ dvec,
+                    __nv_bfloat16* __restrict__ dk, Strided5 dks, __nv_bfloat16* __restrict__ dv, Strided5 dvs) {
   using C = BwdCfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sK = smem;
   uint8_t* sV = smem + C::TILE_BYTES;
-  uint8_t* sRing = smem + C::SMEM_RING;              // stage st: Q tile, dO tile
-  float* sRows = reinterpret_cast<float*>(smem + C::SMEM_ROWS);   // stage st: lse_l2[128], dvec[128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::SMEM_BAR);
+  uint8_t* sRing = smem + C::KV_RING;                // stage st: Q half, dO half
+  float* sRows = reinterpret_cast<float*>(smem + C::KV_ROWS);   // stage st: lse_l2[64], dvec[64], lo[64], hi[64]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::KV_BAR);
   uint64_t* kv_full = bars;
-  uint64_t* full = bars + 1;                         // [NST]
-  uint64_t* empty = full + C::NST;                   // [NST]
-  uint64_t* s_full = empty + C::NST;
-  uint64_t* p_full = s_full + 1;
-  uint64_t* o_full = p_full + 1;
+  uint64_t* full = bars + 1;                         // [NSTH]
+  uint64_t* empty = full + C::NSTH;                  // [NSTH]
+  uint64_t* s_full = empty + C::NSTH;                // [2] per slot / warpgroup
+  uint64_t* p_full = s_full + 2;                     // [2]
+  uint64_t* o_full = p_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
 
   const int n_kt = (p.Sk + 127) / 128;
@@ -199,24 +222,26 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int g = (blockIdx.x / (n_kt * p.Hkv)) % p.G;
   const int b = blockIdx.x / (n_kt * p.Hkv * p.G);
   const int k0 = kt * 128;
-  const int n_qt = (p.Sq + 127) / 128;
+  const int n_qh = (p.Sq + 63) / 64;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  // the (query head, query tile) items of this CTA: every tile whose rows' key intervals meet [k0, k0+128)
-  auto item_needed = [&](int qt) {
-    const int q_first = qt * 128, q_last = min(p.Sq, q_first + 128) - 1;
+  // the 64-row query halves whose rows' key intervals meet [k0, k0 + 128)
+  auto half_needed = [&](int qh) {
+    const int q_first = qh * 64, q_last = min(p.Sq, q_first + 64) - 1;
     const Interval u = rows_union(p, b, q_first, q_last);
     return u.hi > k0 && u.lo < k0 + 128;
   };
 
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1);
-    for (int s = 0; s < C::NST; ++s) {
+    for (int s = 0; s < C::NSTH; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(s_full, 1);
-    mbar_init(p_full, 256);
+    for (int w = 0; w < 2; ++w) {
+      mbar_init(&s_full[w], 1);
+      mbar_init(&p_full[w], 128);
+    }
     mbar_init(o_full, 1);
     fence_mbar_init();
   }
@@ -225,7 +250,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DV = 256, COL_DK = 256 + D;
+  constexpr uint32_t COL_DV = 256, COL_DK = 256 + D;
 
   if (warp == 8) {
     // ============================== TMA producer ==============================
@@ -244,15 +269,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int bq = maps.q_bcast_b ? 0 : b, gq = maps.q_bcast_g ? 0 : g;
       int e = 0;
       for (int hh = hk * p.grp; hh < (hk + 1) * p.grp; ++hh)
-        for (int qt = 0; qt < n_qt; ++qt) {
-          if (!item_needed(qt)) continue;
-          const int st = e % C::NST;
-          if (e >= C::NST) mbar_wait(&empty[st], ((e / C::NST) - 1) & 1);
-          mbar_arrive_expect_tx(&full[st], 2 * C::TILE_BYTES);
-          uint8_t* dq_ = sRing + st * 2 * C::TILE_BYTES;
+        for (int qh = 0; qh < n_qh; ++qh) {
+          if (!half_needed(qh)) continue;
+          const int st = e % C::NSTH;
+          if (e >= C::NSTH) mbar_wait(&empty[st], ((e / C::NSTH) - 1) & 1);
+          mbar_arrive_expect_tx(&full[st], 2 * C::HALF_BYTES);
+          uint8_t* dq_ = sRing + st * 2 * C::HALF_BYTES;
           for (int c = 0; c < C::NCH; ++c) {
-            tma_load_5d(dq_ + c * C::CHUNK_BYTES, &maps.q, &full[st], c * C::CH, qt * 128, hh, gq, bq);
-            tma_load_5d(dq_ + C::TILE_BYTES + c * C::CHUNK_BYTES, &tdo, &full[st], c * C::CH, qt * 128, hh, g, b);
+            tma_load_5d(dq_ + c * C::HCHUNK, &tq64, &full[st], c * C::CH, qh * 64, hh, gq, bq);
+            tma_load_5d(dq_ + C::HALF_BYTES + c * C::HCHUNK, &tdo64, &full[st], c * C::CH, qh * 64, hh, g, b);
           }
           ++e;
         }
@@ -261,93 +286,103 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // ============================== MMA issuer ==============================
     if (lane == 0) {
       const uint32_t ka = smem_u32(sK), va = smem_u32(sV), ring = smem_u32(sRing);
-      mbar_wait(kv_full, 0);
-      int e = 0;
+      int n_items = 0;
       for (int hh = hk * p.grp; hh < (hk + 1) * p.grp; ++hh)
-        for (int qt = 0; qt < n_qt; ++qt) {
-          if (!item_needed(qt)) continue;
-          const int st = e % C::NST;
-          mbar_wait(&full[st], (e / C::NST) & 1);
-          tc_fence_after();
-          const uint32_t qa = ring + st * 2 * C::TILE_BYTES, doa = qa + C::TILE_BYTES;
+        for (int qh = 0; qh < n_qh; ++qh) n_items += half_needed(qh) ? 1 : 0;
+      mbar_wait(kv_full, 0);
+      auto issue_s = [&](int e) {                    // S^T(e) = K Q_e^T, dP^T(e) = V dO_e^T into slot e & 1
+        const int st = e % C::NSTH, sl = e & 1;
+        mbar_wait(&full[st], (e / C::NSTH) & 1);
+        tc_fence_after();
+        const uint32_t qa = ring + st * 2 * C::HALF_BYTES, doa = qa + C::HALF_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk)   // S^T = K Q^T
-            umma_ss(tmem + COL_S, kmajor_desc<D>(ka, kk), kmajor_desc<D>(qa, kk), C::IDESC_NN, kk > 0);
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_ss(tmem + sl * 128, kmajor_desc<D>(ka, kk), kmajor_desc_c<D>(qa, kk, C::HCHUNK), C::IDESC_N64, kk > 0);
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk)   // dP^T = V dO^T
-            umma_ss(tmem + COL_DP, kmajor_desc<D>(va, kk), kmajor_desc<D>(doa, kk), C::IDESC_NN, kk > 0);
-          umma_commit(s_full);
-          mbar_wait(p_full, e & 1);
-          tc_fence_after();
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_ss(tmem + sl * 128 + 64, kmajor_desc<D>(va, kk), kmajor_desc_c<D>(doa, kk, C::HCHUNK), C::IDESC_N64,
+                  kk > 0);
+        umma_commit(&s_full[sl]);
+      };
+      if (n_items > 0) issue_s(0);
+      if (n_items > 1) issue_s(1);
+      for (int e = 0; e < n_items; ++e) {
+        const int st = e % C::NSTH, sl = e & 1;
+        mbar_wait(&p_full[sl], (e >> 1) & 1);
+        tc_fence_after();
+        const uint32_t qa = ring + st * 2 * C::HALF_BYTES, doa = qa + C::HALF_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)        // dV += P^T dO   (P^T bf16 in TMEM [64, 128))
-            umma_ts(tmem + COL_DV, tmem + COL_S + 64 + kk * 8, mnmajor_desc<D>(doa, kk), C::IDESC_ND,
-                    (e > 0 || kk > 0) ? 1u : 0u);
+        for (int kk = 0; kk < 4; ++kk)        // dV += P^T dO   (P^T bf16 at slot + [32, 64))
+          umma_ts(tmem + COL_DV, tmem + sl * 128 + 32 + kk * 8, mnmajor_desc_c<D>(doa, kk, C::HCHUNK), C::IDESC_ND,
+                  (e > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)        // dK += dS^T Q   (dS^T bf16 in TMEM [0, 64))
-            umma_ts(tmem + COL_DK, tmem + COL_S + kk * 8, mnmajor_desc<D>(qa, kk), C::IDESC_ND,
-                    (e > 0 || kk > 0) ? 1u : 0u);
-          umma_commit(&empty[st]);
-          ++e;
-        }
+        for (int kk = 0; kk < 4; ++kk)        // dK += dS^T Q   (dS^T bf16 at slot + [0, 32))
+          umma_ts(tmem + COL_DK, tmem + sl * 128 + kk * 8, mnmajor_desc_c<D>(qa, kk, C::HCHUNK), C::IDESC_ND,
+                  (e > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&empty[st]);
+        if (e + 2 < n_items) issue_s(e + 2);  // slot sl again: after dV(e), dK(e) read it (in order)
+      }
       umma_commit(o_full);
     }
   } else {
     // ============================== compute (thread = key row) ==============================
-    // Warpgroup wg takes query columns [64 wg, 64 wg + 64) of the item (same TMEM lanes, disjoint columns).
-    const int wg = warp >> 2;
+    const int wg = warp >> 2;                       // warpgroup wg: items e = wg (mod 2), TMEM slot wg
     const int r = threadIdx.x & 127;                // key row == TMEM lane
     const int k = k0 + r;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    const int j0 = wg * 64;
+    const uint32_t col_s = wg * 128, col_dp = wg * 128 + 64;
     // MSA / key mask (G9): a masked key has P = 0 for every query -- its dK, dV rows stay 0
     const bool key_on = !p.keybits || k >= p.Sk ||
                         ((p.keybits[((int64_t)b * p.G + g) * p.keybits_words + (k >> 5)] >> (k & 31)) & 1u);
-    int e = 0;
+    int e = 0, ew = 0;
     for (int hh = hk * p.grp; hh < (hk + 1) * p.grp; ++hh) {
       const float slope_l2 = MOD == MOD_ALIBI ? head_slope(p, hh) : 0.f;
-      for (int qt = 0; qt < n_qt; ++qt) {
-        if (!item_needed(qt)) continue;
-        const int st = e % C::NST;
-        const int q0 = qt * 128;
-        // this tile's rows, one per thread of warpgroup 0: LSE (log2 units), Dvec and the key interval
-        // [lo, hi) of query q0 + r (rows past S_q get an empty interval: P = 0); read as broadcasts
-        float* rl = sRows + st * 512;
-        int* riv = reinterpret_cast<int*>(rl + 256);
-        if (wg == 0) {
+      for (int qh = 0; qh < n_qh; ++qh) {
+        if (!half_needed(qh)) continue;
+        if ((e & 1) != wg) {
+          ++e;
+          continue;
+        }
+        const int st = e % C::NSTH;
+        const int q0 = qh * 64;
+        // this half's rows, one per thread r < 64: LSE (log2 units), Dvec and the key interval [lo, hi) of
+        // query q0 + r (rows past S_q get an empty interval: P = 0); the element loop reads them as broadcasts
+        float* rl = sRows + st * 256;
+        int* riv = reinterpret_cast<int*>(rl + 128);
+        if (r < 64) {
           const int q = q0 + r;
           const bool ok = q < p.Sq;
           const int64_t li = (int64_t)b * ls.b + (int64_t)g * ls.g + (int64_t)hh * ls.h + (int64_t)(ok ? q : 0) * ls.s;
           rl[r] = ok ? lse_g[li] * kBwdLog2e : INFINITY;
-          rl[128 + r] = ok ? dvec[(((int64_t)b * p.G + g) * p.Hq + hh) * p.Sq + q] : 0.f;
+          rl[64 + r] = ok ? dvec[(((int64_t)b * p.G + g) * p.Hq + hh) * p.Sq + q] : 0.f;
           const Interval iv = row_interval(p, b, q);
           riv[r] = ok ? iv.lo : 0;
-          riv[128 + r] = ok ? iv.hi : 0;
+          riv[64 + r] = ok ? iv.hi : 0;
         }
-        named_bar_sync(1, 256);
+        named_bar_sync(1 + wg, 128);
         // tile class: mask-free when every row's interval covers [k0, k0 + 128) (intervals are monotone)
-        const int q_last = min(p.Sq, q0 + 128) - 1;
+        const int q_last = min(p.Sq, q0 + 64) - 1;
         const Interval a0 = row_interval(p, b, q0), a1 = row_interval(p, b, q_last);
-        const bool full_tile = q_last - q0 == 127 && a1.lo <= k0 && a0.hi >= k0 + 128 && k0 + 128 <= p.Sk;
-        mbar_wait(s_full, e & 1);
+        const bool full_tile = q_last - q0 == 63 && a1.lo <= k0 && a0.hi >= k0 + 128 && k0 + 128 <= p.Sk;
+        mbar_wait(&s_full[wg], ew & 1);
         tc_fence_after();
         uint32_t sv[64];
-        tmem_ld32(tmem + lane_base + COL_S + j0, &sv[0]);
-        tmem_ld32(tmem + lane_base + COL_S + j0 + 32, &sv[32]);
+        tmem_ld32(tmem + lane_base + col_s, &sv[0]);
+        tmem_ld32(tmem + lane_base + col_s + 32, &sv[32]);
         tmem_wait_ld();
-        // P^T (bf16 pairs) and the softcap factor, query j0 + j = column
+        // P^T (bf16 pairs) and the softcap factor, query q0 + j = column j
         uint32_t pk[32], fk[32];
 #pragma unroll
         for (int j = 0; j < 64; j += 4) {
-          const float4 lse4 = *reinterpret_cast<const float4*>(rl + j0 + j);
+          const float4 lse4 = *reinterpret_cast<const float4*>(rl + j);
           const float lsev[4] = {lse4.x, lse4.y, lse4.z, lse4.w};
           float pr[4], f[4];
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
-            const int q = q0 + j0 + j + t;
+            const int q = q0 + j + t;
             float ft;
-            const bool keep = key_on && (full_tile || (k >= riv[j0 + j + t] && k < riv[128 + j0 + j + t]));   // hi <= S_k
-            const float bv = keep ? bias_at(p, b, g, hh, q, k) : 0.f;
+            const bool keep = key_on && (full_tile || (k >= riv[j + t] && k < riv[64 + j + t]));   // hi <= S_k
+            const float bv = (BIAS && keep) ? bias_at(p, b, g, hh, q, k) : 0.f;
             const float s = bwd_score<MOD>(p, __uint_as_float(sv[j + t]), slope_l2, k, q + p.q_off, ft, bv);
             pr[t] = keep ? ex2(fmaf(s, kBwdLog2e, -lsev[t])) : 0.f;
             f[t] = ft;
@@ -357,19 +392,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           fk[j >> 1] = pack_bf16(f[0], f[1]);
           fk[(j >> 1) + 1] = pack_bf16(f[2], f[3]);
         }
-        // both warpgroups have read their S^T columns before either overwrites S^T's columns with P^T / dS^T
-        named_bar_sync(1, 256);
-        tmem_st32(tmem + lane_base + COL_S + 64 + (j0 >> 1), &pk[0]);
-        // dS^T = P^T (dP^T - Dvec) * f, 32 queries at a time, into [0, 64) (S^T is consumed)
+        tmem_st32(tmem + lane_base + col_s + 32, &pk[0]);
+        // dS^T = P^T (dP^T - Dvec) * f, 32 queries at a time, into slot + [0, 32) (S^T is consumed)
 #pragma unroll
         for (int c = 0; c < 64; c += 32) {
           uint32_t dp[32];
-          tmem_ld32(tmem + lane_base + COL_DP + j0 + c, dp);
+          tmem_ld32(tmem + lane_base + col_dp + c, dp);
           tmem_wait_ld();
           uint32_t ds[16];
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
-            const float4 dv4 = *reinterpret_cast<const float4*>(rl + 128 + j0 + c + j);
+            const float4 dv4 = *reinterpret_cast<const float4*>(rl + 64 + c + j);
             const uint32_t pw0 = pk[(c + j) >> 1], pw1 = pk[((c + j) >> 1) + 1];
             const uint32_t fw0 = fk[(c + j) >> 1], fw1 = fk[((c + j) >> 1) + 1];
             float d0 = bf16_lo(pw0) * (__uint_as_float(dp[j]) - dv4.x);
@@ -385,13 +418,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             ds[j >> 1] = pack_bf16(d0, d1);
             ds[(j >> 1) + 1] = pack_bf16(d2, d3);
           }
-          tmem_st16(tmem + lane_base + COL_S + ((j0 + c) >> 1), ds);
+          tmem_st16(tmem + lane_base + col_s + (c >> 1), ds);
         }
         tmem_wait_st();
         tc_fence_before();
-        named_bar_sync(1, 256);                     // every thread has read this stage's row buffer
-        mbar_arrive(p_full);
+        mbar_arrive(&p_full[wg]);
         ++e;
+        ++ew;
       }
     }
     // ---- epilogue: dK (x scale) and dV rows of this key tile
@@ -438,7 +471,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 // ================================================================ dQ
 // grid = B * Hq * n_qtile (query tile descending: causal's heaviest tiles first), 320 threads:
 // warps 0-7 compute (two warpgroups split the tile's 128 key columns), warp 8 TMA, warp 9 MMA + TMEM.
-template <int D, int MOD>
+template <int D, int MOD, bool BIAS>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     bwd_dq_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ TmaMaps maps,
                   const __grid_constant__ CUtensorMap tdo, const float* __restrict__ lse_g, Strided5 ls,
@@ -578,7 +611,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           float ft;
           const bool kon = (((j + t) < 32 ? kw0 : kw1) >> ((j + t) & 31)) & 1u;
           const bool keep = kon && (full_tile || (k >= iv.lo && k < iv.hi && k < p.Sk));
-          const float bv = keep ? bias_at(p, b, g, h, q, k) : 0.f;
+          const float bv = (BIAS && keep) ? bias_at(p, b, g, h, q, k) : 0.f;
           const float s = bwd_score<MOD>(p, __uint_as_float(sv[j + t]), slope_l2, k, q_abs, ft, bv);
           pr[t] = keep ? ex2(fmaf(s, kBwdLog2e, -lse_l2)) : 0.f;
           f[t] = ft;
@@ -604,7 +637,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             d1 *= bf16_hi(fw);
           }
           ds[j >> 1] = pack_bf16(d0, d1);
-          if (dbias && row_ok) {                    // dL/dbias = dS (fp32 atomics: broadcast dims accumulate)
+          if (BIAS && dbias && row_ok) {            // dL/dbias = dS (fp32 atomics: broadcast dims accumulate)
             const int k = k0 + j0 + c + j;
             const int64_t off = b * dbs.b + g * dbs.g + (int64_t)h * dbs.h + (int64_t)q * dbs.s + (int64_t)k * dbs.d;
             if (k < p.Sk && d0 != 0.f) atomicAdd(dbias + off, d0);
@@ -655,6 +688,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
 // ---------------------------------------------------------------- launch
 struct BwdLaunch {
+  const CUtensorMap* tq64; const CUtensorMap* tdo64;   // 64-row boxes of q and dO (dK/dV kernel)
   const float* lse; Strided5 ls;
   float* dbias; Strided5 dbs;
   const __nv_bfloat16* dout; Strided5 dos;
@@ -663,20 +697,26 @@ struct BwdLaunch {
   Strided5 dqs, dks, dvs;
 };
 
-template <int D, int MOD>
-static cudaError_t launch_bwd_dm(const AttnParams& p, const TmaMaps& maps, const CUtensorMap& tdo, const BwdLaunch& L,
+template <int D, int MOD, bool BIAS>
+static cudaError_t launch_bwd_dmb(const AttnParams& p, const TmaMaps& maps, const CUtensorMap& tdo, const BwdLaunch& L,
                                  cudaStream_t s) {
   using C = BwdCfg<D>;
   const int n_kt = (p.Sk + 127) / 128, n_qt = (p.Sq + 127) / 128;
-  cudaError_t e = cudaFuncSetAttribute(bwd_dkdv_kernel<D, MOD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_TOTAL);
+  cudaError_t e = cudaFuncSetAttribute(bwd_dkdv_kernel<D, MOD, BIAS>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::KV_SMEM);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(bwd_dq_kernel<D, MOD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_TOTAL);
+  e = cudaFuncSetAttribute(bwd_dq_kernel<D, MOD, BIAS>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_TOTAL);
   if (e != cudaSuccess) return e;
-  bwd_dkdv_kernel<D, MOD><<<p.B * p.G * p.Hkv * n_kt, kBwdThreads, C::SMEM_TOTAL, s>>>(p, maps, tdo, L.lse, L.ls, L.dvec, L.dk, L.dks,
+  bwd_dkdv_kernel<D, MOD, BIAS><<<p.B * p.G * p.Hkv * n_kt, kBwdThreads, C::KV_SMEM, s>>>(p, maps, *L.tq64, *L.tdo64, L.lse, L.ls, L.dvec, L.dk, L.dks,
                                                                         L.dv, L.dvs);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  bwd_dq_kernel<D, MOD><<<p.B * p.G * p.Hq * n_qt, kBwdThreads, C::SMEM_TOTAL, s>>>(p, maps, tdo, L.lse, L.ls, L.dvec, L.dq, L.dqs, L.dbias, L.dbs);
+  bwd_dq_kernel<D, MOD, BIAS><<<p.B * p.G * p.Hq * n_qt, kBwdThreads, C::SMEM_TOTAL, s>>>(p, maps, tdo, L.lse, L.ls, L.dvec, L.dq, L.dqs, L.dbias, L.dbs);
   return cudaGetLastError();
+}
+
+template <int D, int MOD>
+static cudaError_t launch_bwd_dm(const AttnParams& p, const TmaMaps& maps, const CUtensorMap& tdo, const BwdLaunch& L,
+                                 cudaStream_t s) {
+  return p.bias ? launch_bwd_dmb<D, MOD, true>(p, maps, tdo, L, s) : launch_bwd_dmb<D, MOD, false>(p, maps, tdo, L, s);
 }
 
 template <int D>
@@ -703,10 +743,11 @@ cudaError_t launch_bwd_prepass(const AttnParams& p, const void* dout, Strided5 d
   return cudaGetLastError();
 }
 
-cudaError_t launch_attn_bwd(const AttnParams& p, const TmaMaps& maps, const CUtensorMap& tdo, const float* lse,
+cudaError_t launch_attn_bwd(const AttnParams& p, const TmaMaps& maps, const CUtensorMap& tdo, const CUtensorMap& tq64,
+                            const CUtensorMap& tdo64, const float* lse,
                             Strided5 ls, const void* dout, Strided5 dos, float* dvec, void* dq, Strided5 dqs, void* dk,
                             Strided5 dks, void* dv, Strided5 dvs, float* dbias, Strided5 dbs, cudaStream_t s) {
-  BwdLaunch L{lse, ls, dbias, dbs, static_cast<const __nv_bfloat16*>(dout), dos, dvec, static_cast<__nv_bfloat16*>(dq),
+  BwdLaunch L{&tq64, &tdo64, lse, ls, dbias, dbs, static_cast<const __nv_bfloat16*>(dout), dos, dvec, static_cast<__nv_bfloat16*>(dq),
               static_cast<__nv_bfloat16*>(dk), static_cast<__nv_bfloat16*>(dv), dqs, dks, dvs};
   switch (p.Dqk) {
     case 128: return launch_bwd_d<128>(p, maps, tdo, L, s);

@@ -44,7 +44,8 @@ cudaError_t launch_sched_dump(const AttnParams& p, int32_t* out, int64_t out_wor
                               int32_t* max_tiles, cudaStream_t stream);
 cudaError_t launch_bwd_prepass(const AttnParams& p, const void* dout, Strided5 dos, float* dvec, void* da, void* dgate,
                                Strided5 dgs, cudaStream_t s);
-cudaError_t launch_attn_bwd(const AttnParams& p, const TmaMaps& maps, const CUtensorMap& tdo, const float* lse,
+cudaError_t launch_attn_bwd(const AttnParams& p, const TmaMaps& maps, const CUtensorMap& tdo, const CUtensorMap& tq64,
+                            const CUtensorMap& tdo64, const float* lse,
                             Strided5 ls, const void* dout, Strided5 dos, float* dvec, void* dq, Strided5 dqs, void* dk,
                             Strided5 dks, void* dv, Strided5 dvs, float* dbias, Strided5 dbs, cudaStream_t s);
 }  // namespace fl
@@ -822,9 +823,11 @@ fl_status fl_attn_bwd(const fl_attn_bwd_args* args) {
     vda.stride[1] = (int64_t)p.Hq * p.Sq * p.Dv;
     vda.stride[0] = (int64_t)p.G * p.Hq * p.Sq * p.Dv;
   }
-  CUtensorMap tdo;
+  CUtensorMap tdo, tq64, tdo64;
   int bg, bb;
   if ((s = encode_map(vda, ch, &tdo, &bg, &bb)) != FL_OK) return s;
+  if ((s = encode_map(vda, ch, &tdo64, &bg, &bb, 64)) != FL_OK) return s;
+  if ((s = encode_map(B.P.q, ch, &tq64, &bg, &bb, 64)) != FL_OK) return s;
   float* dvec = reinterpret_cast<float*>(ws);
   if (B.dbias.present) {
     e = cudaMemsetAsync(B.dbias.data, 0, (size_t)B.dbias_span * sizeof(float), stream);
@@ -833,7 +836,7 @@ fl_status fl_attn_bwd(const fl_attn_bwd_args* args) {
   e = launch_bwd_prepass(p, B.dout.data, strides_of(B.dout), dvec, da, B.dgate.data, strides_of(B.dgate), stream);
   ++g_launches;
   if (e != cudaSuccess) return cuda_fail(e, "backward pre-pass launch");
-  e = launch_attn_bwd(p, maps, tdo, static_cast<const float*>(B.P.lse.data), strides_of(B.P.lse), B.dout.data,
+  e = launch_attn_bwd(p, maps, tdo, tq64, tdo64, static_cast<const float*>(B.P.lse.data), strides_of(B.P.lse), B.dout.data,
                       strides_of(B.dout), dvec, B.dq.data, strides_of(B.dq), B.dk.data, strides_of(B.dk), B.dv.data,
                       strides_of(B.dv), static_cast<float*>(B.dbias.data), strides_of(B.dbias), stream);
   g_launches += 2;
