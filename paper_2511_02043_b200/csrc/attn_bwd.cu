@@ -469,8 +469,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 }
 
 // ================================================================ dQ
-// grid = B * Hq * n_qtile (query tile descending: causal's heaviest tiles first), 320 threads:
-// warps 0-7 compute (two warpgroups split the tile's 128 key columns), warp 8 TMA, warp 9 MMA + TMEM.
+// grid = B * G * Hq * n_qtile (query tile descending: causal's heaviest tiles first), 320 threads: warps 0-7
+// compute, warp 8 TMA, warp 9 MMA + TMEM.  Items are the 64-key halves of the tile's KV tiles; warpgroup w
+// takes items e = w (mod 2) in TMEM slot w (S [0, 64), dP [64, 128) of the slot, dS over S's upper half),
+// so the MMAs of one item run while the other warpgroup computes (as in the dK/dV kernel).
 template <int D, int MOD, bool BIAS>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     bwd_dq_kernel(const __grid_constant__ AttnParams p, const __grid_constant__ TmaMaps maps,
@@ -487,9 +489,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* q_full = bars;
   uint64_t* full = bars + 1;
   uint64_t* empty = full + C::NST;
-  uint64_t* s_full = empty + C::NST;
-  uint64_t* p_full = s_full + 1;
-  uint64_t* o_full = p_full + 1;
+  uint64_t* s_full = empty + C::NST;                 // [2] per slot / warpgroup
+  uint64_t* p_full = s_full + 2;                     // [2]
+  uint64_t* o_full = p_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
 
   const int n_qt = (p.Sq + 127) / 128;
@@ -509,8 +511,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(s_full, 1);
-    mbar_init(p_full, 256);
+    for (int w = 0; w < 2; ++w) {
+      mbar_init(&s_full[w], 1);
+      mbar_init(&p_full[w], 128);
+    }
     mbar_init(o_full, 1);
     fence_mbar_init();
   }
@@ -519,7 +523,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DQ = 256;
+  constexpr uint32_t COL_DQ = 256;
 
   if (warp == 8) {
     if (lane == 0) {
@@ -547,59 +551,69 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
   } else if (warp == 9) {
     if (lane == 0) {
+      // items = 64-key halves of the KV tiles, e = 2 (kt - kt_lo) + half, in TMEM slot e & 1 (warpgroup e & 1)
       const uint32_t qa = smem_u32(sQ), doa = smem_u32(sDO), ring = smem_u32(sRing);
+      const int n_items = 2 * (kt_hi - kt_lo);
       mbar_wait(q_full, 0);
-      for (int kt = kt_lo; kt < kt_hi; ++kt) {
-        const int e = kt - kt_lo, st = e % C::NST;
-        mbar_wait(&full[st], (e / C::NST) & 1);
+      auto issue_s = [&](int e) {                    // S = Q K_half^T, dP = dO V_half^T into slot e & 1
+        const int t = e >> 1, st = t % C::NST, sl = e & 1;
+        if ((e & 1) == 0) mbar_wait(&full[st], (t / C::NST) & 1);
         tc_fence_after();
-        const uint32_t ka = ring + st * 2 * C::TILE_BYTES, va = ka + C::TILE_BYTES;
+        const uint32_t ka = ring + st * 2 * C::TILE_BYTES + (e & 1) * 64 * C::SWB, va = ka + C::TILE_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)     // S = Q K^T
-          umma_ss(tmem + COL_S, kmajor_desc<D>(qa, kk), kmajor_desc<D>(ka, kk), C::IDESC_NN, kk > 0);
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_ss(tmem + sl * 128, kmajor_desc<D>(qa, kk), kmajor_desc_c<D>(ka, kk, C::CHUNK_BYTES), C::IDESC_N64, kk > 0);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)     // dP = dO V^T
-          umma_ss(tmem + COL_DP, kmajor_desc<D>(doa, kk), kmajor_desc<D>(va, kk), C::IDESC_NN, kk > 0);
-        umma_commit(s_full);
-        mbar_wait(p_full, e & 1);
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_ss(tmem + sl * 128 + 64, kmajor_desc<D>(doa, kk), kmajor_desc_c<D>(va, kk, C::CHUNK_BYTES), C::IDESC_N64,
+                  kk > 0);
+        umma_commit(&s_full[sl]);
+      };
+      if (n_items > 0) issue_s(0);
+      if (n_items > 1) issue_s(1);
+      for (int e = 0; e < n_items; ++e) {
+        const int t = e >> 1, st = t % C::NST, sl = e & 1;
+        mbar_wait(&p_full[sl], (e >> 1) & 1);
         tc_fence_after();
+        const uint32_t ka = ring + st * 2 * C::TILE_BYTES + (e & 1) * 64 * C::SWB;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)          // dQ += dS K   (dS bf16 in TMEM [64, 128))
-          umma_ts(tmem + COL_DQ, tmem + COL_S + 64 + kk * 8, mnmajor_desc<D>(ka, kk), C::IDESC_ND,
-                  (e > 0 || kk > 0) ? 1u : 0u);
-        umma_commit(&empty[st]);
+        for (int kk = 0; kk < 4; ++kk)          // dQ += dS K_half   (dS bf16 at slot + [32, 64))
+          umma_ts(tmem + COL_DQ, tmem + sl * 128 + 32 + kk * 8, mnmajor_desc_c<D>(ka, kk, C::CHUNK_BYTES),
+                  C::IDESC_ND, (e > 0 || kk > 0) ? 1u : 0u);
+        if (e & 1) umma_commit(&empty[st]);      // both halves of the K/V tile are done
+        if (e + 2 < n_items) issue_s(e + 2);    // slot sl again, after dQ(e) read its dS (in order)
       }
       umma_commit(o_full);
     }
   } else {
-    // warpgroup wg takes key columns [64 wg, 64 wg + 64) of each KV tile (same TMEM lanes = query rows)
-    const int wg = warp >> 2;
+    const int wg = warp >> 2;                       // warpgroup wg: items e = wg (mod 2), TMEM slot wg
     const int r = threadIdx.x & 127;
     const int q = q0 + r;
     const bool row_ok = q < p.Sq;
     const int q_abs = q + p.q_off;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    const int j0 = wg * 64;
+    const uint32_t col_s = wg * 128, col_dp = wg * 128 + 64;
     const float slope_l2 = MOD == MOD_ALIBI ? head_slope(p, h) : 0.f;
     const float lse_l2 =
         row_ok ? lse_g[(int64_t)b * ls.b + (int64_t)g * ls.g + (int64_t)h * ls.h + (int64_t)q * ls.s] * kBwdLog2e : INFINITY;
     const float dvr = row_ok ? dvec[(((int64_t)b * p.G + g) * p.Hq + h) * p.Sq + q] : 0.f;
     const uint32_t* kbits = p.keybits ? p.keybits + ((int64_t)b * p.G + g) * p.keybits_words : nullptr;
     const Interval iv = row_interval(p, b, q);
-    for (int kt = kt_lo; kt < kt_hi; ++kt) {
-      const int e = kt - kt_lo;
-      const int k0 = kt * 128;
-      const bool full_tile = tile_inside(iv, k0, p.Sk);
-      uint32_t kw0 = 0xFFFFFFFFu, kw1 = 0xFFFFFFFFu;     // key-mask words of this warpgroup's 64 keys
+    const int n_items = 2 * (kt_hi - kt_lo);
+    int ew = 0;
+    for (int e = wg; e < n_items; e += 2, ++ew) {
+      const int kh0 = kt_lo * 128 + e * 64;          // this item's first key
+      const bool full_tile = kh0 >= iv.lo && kh0 + 64 <= iv.hi && kh0 + 64 <= p.Sk;
+      uint32_t kw0 = 0xFFFFFFFFu, kw1 = 0xFFFFFFFFu; // key-mask words of the item's 64 keys
       if (kbits) {
-        kw0 = __ldg(kbits + ((k0 + j0) >> 5));
-        kw1 = __ldg(kbits + ((k0 + j0) >> 5) + 1);
+        kw0 = __ldg(kbits + (kh0 >> 5));
+        kw1 = __ldg(kbits + (kh0 >> 5) + 1);
       }
-      mbar_wait(s_full, e & 1);
+      mbar_wait(&s_full[wg], ew & 1);
       tc_fence_after();
       uint32_t sv[64];
-      tmem_ld32(tmem + lane_base + COL_S + j0, &sv[0]);
-      tmem_ld32(tmem + lane_base + COL_S + j0 + 32, &sv[32]);
+      tmem_ld32(tmem + lane_base + col_s, &sv[0]);
+      tmem_ld32(tmem + lane_base + col_s + 32, &sv[32]);
       tmem_wait_ld();
       uint32_t pk[32], fk[32];
 #pragma unroll
@@ -607,24 +621,22 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         float pr[2], f[2];
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
-          const int k = k0 + j0 + j + t;
+          const int k = kh0 + j + t;
           float ft;
           const bool kon = (((j + t) < 32 ? kw0 : kw1) >> ((j + t) & 31)) & 1u;
           const bool keep = kon && (full_tile || (k >= iv.lo && k < iv.hi && k < p.Sk));
           const float bv = (BIAS && keep) ? bias_at(p, b, g, h, q, k) : 0.f;
-          const float s = bwd_score<MOD>(p, __uint_as_float(sv[j + t]), slope_l2, k, q_abs, ft, bv);
-          pr[t] = keep ? ex2(fmaf(s, kBwdLog2e, -lse_l2)) : 0.f;
+          const float sc = bwd_score<MOD>(p, __uint_as_float(sv[j + t]), slope_l2, k, q_abs, ft, bv);
+          pr[t] = keep ? ex2(fmaf(sc, kBwdLog2e, -lse_l2)) : 0.f;
           f[t] = ft;
         }
         pk[j >> 1] = pack_bf16(pr[0], pr[1]);
         fk[j >> 1] = pack_bf16(f[0], f[1]);
       }
-      // both warpgroups have read their S columns before dS overwrites S's columns [64, 128)
-      named_bar_sync(1, 256);
 #pragma unroll
-      for (int c = 0; c < 64; c += 32) {            // dS = P (dP - Dvec) f -> TMEM [64 + (j0 + c)/2, ...)
+      for (int c = 0; c < 64; c += 32) {            // dS = P (dP - Dvec) f -> TMEM slot + [32 + c/2, ...)
         uint32_t dp[32];
-        tmem_ld32(tmem + lane_base + COL_DP + j0 + c, dp);
+        tmem_ld32(tmem + lane_base + col_dp + c, dp);
         tmem_wait_ld();
         uint32_t ds[16];
 #pragma unroll
@@ -638,17 +650,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
           ds[j >> 1] = pack_bf16(d0, d1);
           if (BIAS && dbias && row_ok) {            // dL/dbias = dS (fp32 atomics: broadcast dims accumulate)
-            const int k = k0 + j0 + c + j;
+            const int k = kh0 + c + j;
             const int64_t off = b * dbs.b + g * dbs.g + (int64_t)h * dbs.h + (int64_t)q * dbs.s + (int64_t)k * dbs.d;
             if (k < p.Sk && d0 != 0.f) atomicAdd(dbias + off, d0);
             if (k + 1 < p.Sk && d1 != 0.f) atomicAdd(dbias + off + dbs.d, d1);
           }
         }
-        tmem_st16(tmem + lane_base + COL_S + 64 + ((j0 + c) >> 1), ds);
+        tmem_st16(tmem + lane_base + col_s + 32 + (c >> 1), ds);
       }
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(p_full);
+      mbar_arrive(&p_full[wg]);
     }
     if (kt_hi > kt_lo) {
       mbar_wait(o_full, 0);
