@@ -127,6 +127,14 @@ def evoformer(case: dict):
     dt = DT[case.get("dtype", "bf16")]
     m = lambda t: synth.uniform((B, Ns, Nr, H, c), seed=seed, tensor=t, dtype=dt, lead=3)
     Q, K, V = m("q"), m("k"), m("v")
+    if case.get("dist") == "needle":                    # needle rows in the attention view (peaked softmax)
+        if case["kind"] == "row":                       # view rows: (b, s, h) x keys i
+            q, k = synth.needle((B * Ns, H, Nr, c), (B * Ns, H, Nr, c), seed=seed, dtype=dt)
+            to = lambda t: t.reshape(B, Ns, H, Nr, c).permute(0, 1, 3, 2, 4).contiguous()
+        else:                                           # view rows: (b, i, h) x keys s
+            q, k = synth.needle((B * Nr, H, Ns, c), (B * Nr, H, Ns, c), seed=seed, dtype=dt)
+            to = lambda t: t.reshape(B, Nr, H, Ns, c).permute(0, 3, 1, 2, 4).contiguous()
+        Q, K = to(q), to(k)
     Gt = synth.uniform((B, Ns, Nr, H, c), seed=seed, tensor="gate", dtype=torch.bfloat16 if dt == torch.bfloat16 else dt,
                        lo=-4, hi=4, lead=3)
     msa_mask = synth.key_mask((B, Ns, Nr), seed=seed, p_zero=case.get("p_zero", 0.0), lead=2)
