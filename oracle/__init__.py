@@ -89,6 +89,8 @@ def lib():
         dp = C.POINTER(C.c_double)
         _lib.flo_linear_ln.argtypes = [C.c_int64, C.c_int64, C.c_int64, dp, dp, dp, dp, dp, C.c_double, dp, dp]
         _lib.flo_linear_ln.restype = C.c_int
+        _lib.flo_ipa.argtypes = [C.c_int64] * 6 + [dp] * 14
+        _lib.flo_ipa.restype = C.c_int
     return _lib
 
 
@@ -345,3 +347,20 @@ def linear_ln(x, w, bias=None, ln_gamma=None, ln_beta=None, eps=1e-5, with_abs=F
     assert rc == 0, rc
     shp = tuple(np.shape(x)[:-1]) + (N,)
     return (y.reshape(shp), ya.reshape(shp)) if with_abs else y.reshape(shp)
+
+
+def ipa(q, k, v, qp, kp, vp, R, t, bias, z, gamma):
+    """NEXT-4 oracle (fl_oracle.c flo_ipa): the Invariant Point Attention core of AF2 Alg.22 (reading G23).
+    q, k, v [N, H, c]; qp, kp [N, H, Pq, 3]; vp [N, H, Pv, 3]; R [N, 3, 3]; t [N, 3]; bias [H, N, N];
+    z [N, N, cz]; gamma [H].  Returns (o [N, H, c], op [N, H, Pv, 3] in the local frames, opair [N, H, cz])."""
+    arr = lambda x: np.ascontiguousarray(torch.as_tensor(x).double().numpy(), dtype=np.float64)
+    ins = [arr(x) for x in (q, k, v, qp, kp, vp, R, t, bias, z, gamma)]
+    N, H, c = ins[0].shape
+    Pq, Pv, cz = ins[3].shape[2], ins[5].shape[2], ins[9].shape[2]
+    o = np.zeros((N, H, c))
+    op = np.zeros((N, H, Pv, 3))
+    opair = np.zeros((N, H, cz))
+    pp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
+    rc = lib().flo_ipa(N, H, c, Pq, Pv, cz, *[pp(a) for a in ins], pp(o), pp(op), pp(opair))
+    assert rc == 0, rc
+    return o, op, opair

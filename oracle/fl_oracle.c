@@ -528,3 +528,79 @@ int flo_linear_ln(int64_t M, int64_t N, int64_t K, const double* x, const double
   }
   return 0;
 }
+
+/* AlphaFold's Invariant Point Attention (IPA), named by the paper among the variants
+ * FlexAttention cannot express with 12 heads of dimension 16.  The paper
+ * gives no formula; this is AF2 (Jumper et al. 2021) Suppl. Alg.22 lines 7-10 (the attention core, after
+ * the linear projections), written out per (i, h) in fp64 (reading G23):
+ *   logit_ij = w_L ( c^-1/2 q_i . k_j + b_ij - (gamma_h w_C / 2) sum_p || T_i q_ip - T_j k_jp ||^2 ),
+ *   w_L = sqrt(1/3), w_C = sqrt(2 / (9 Pq)), T x = R x + t;
+ *   a_ij = softmax_j(logit_ij) (two-pass, Alg.1);
+ *   o_i = sum_j a_ij v_j;   opair_i = sum_j a_ij z_ij;   op_ip = T_i^-1 ( sum_j a_ij T_j v_jp ) = R_i^T (g - t_i).
+ * Layouts (contiguous fp64): q, k, v [N][H][c]; qp, kp [N][H][Pq][3]; vp [N][H][Pv][3]; R [N][3][3]
+ * (row-major, x_global = R x_local + t); t [N][3]; bias [H][N][N]; z [N][N][cz]; gamma [H];
+ * outputs o [N][H][c], op [N][H][Pv][3], opair [N][H][cz]. */
+int flo_ipa(int64_t N, int64_t H, int64_t c, int64_t Pq, int64_t Pv, int64_t cz, const double* q, const double* k,
+            const double* v, const double* qp, const double* kp, const double* vp, const double* R, const double* t,
+            const double* bias, const double* z, const double* gamma, double* o, double* op, double* opair) {
+  if (N < 1 || H < 1 || c < 1 || Pq < 0 || Pv < 0 || cz < 0) return -1;
+  const double wL = sqrt(1.0 / 3.0), wC = Pq > 0 ? sqrt(2.0 / (9.0 * (double)Pq)) : 0.0;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t task = 0; task < N * H; ++task) {
+    const int64_t i = task / H, h = task % H;
+    double* lg = (double*)malloc(sizeof(double) * N);
+    double* g = (double*)malloc(sizeof(double) * (Pv > 0 ? Pv * 3 : 1));
+    /* logits */
+    for (int64_t j = 0; j < N; ++j) {
+      double dot = 0.0;
+      for (int64_t d = 0; d < c; ++d) dot += q[(i * H + h) * c + d] * k[(j * H + h) * c + d];
+      double dist = 0.0;
+      for (int64_t pp = 0; pp < Pq; ++pp) {
+        double xi[3], yj[3];
+        for (int a = 0; a < 3; ++a) {
+          xi[a] = t[i * 3 + a];
+          yj[a] = t[j * 3 + a];
+          for (int bq = 0; bq < 3; ++bq) {
+            xi[a] += R[(i * 3 + a) * 3 + bq] * qp[((i * H + h) * Pq + pp) * 3 + bq];
+            yj[a] += R[(j * 3 + a) * 3 + bq] * kp[((j * H + h) * Pq + pp) * 3 + bq];
+          }
+        }
+        for (int a = 0; a < 3; ++a) dist += (xi[a] - yj[a]) * (xi[a] - yj[a]);
+      }
+      lg[j] = wL * (dot / sqrt((double)c) + bias[(h * N + i) * N + j] - gamma[h] * wC / 2.0 * dist);
+    }
+    /* softmax (two-pass) */
+    double m = -INFINITY, den = 0.0;
+    for (int64_t j = 0; j < N; ++j) m = lg[j] > m ? lg[j] : m;
+    for (int64_t j = 0; j < N; ++j) den += exp(lg[j] - m);
+    for (int64_t j = 0; j < N; ++j) lg[j] = exp(lg[j] - m) / den;
+    /* outputs */
+    for (int64_t d = 0; d < c; ++d) {
+      double acc = 0.0;
+      for (int64_t j = 0; j < N; ++j) acc += lg[j] * v[(j * H + h) * c + d];
+      o[(i * H + h) * c + d] = acc;
+    }
+    for (int64_t e = 0; e < cz; ++e) {
+      double acc = 0.0;
+      for (int64_t j = 0; j < N; ++j) acc += lg[j] * z[(i * N + j) * cz + e];
+      opair[(i * H + h) * cz + e] = acc;
+    }
+    for (int64_t pp = 0; pp < Pv; ++pp) {
+      for (int a = 0; a < 3; ++a) g[pp * 3 + a] = 0.0;
+      for (int64_t j = 0; j < N; ++j)
+        for (int a = 0; a < 3; ++a) {
+          double y = t[j * 3 + a];
+          for (int bq = 0; bq < 3; ++bq) y += R[(j * 3 + a) * 3 + bq] * vp[((j * H + h) * Pv + pp) * 3 + bq];
+          g[pp * 3 + a] += lg[j] * y;
+        }
+      for (int a = 0; a < 3; ++a) {                   /* R_i^T (g - t_i) */
+        double acc = 0.0;
+        for (int bq = 0; bq < 3; ++bq) acc += R[(i * 3 + bq) * 3 + a] * (g[pp * 3 + bq] - t[i * 3 + bq]);
+        op[((i * H + h) * Pv + pp) * 3 + a] = acc;
+      }
+    }
+    free(lg);
+    free(g);
+  }
+  return 0;
+}

@@ -115,4 +115,8 @@ int flo_num_threads(void);
 /* NEXT-2: y = [LayerNorm(x)] w^T + bias (see fl_oracle.c). */
 int flo_linear_ln(int64_t M, int64_t N, int64_t K, const double* x, const double* w, const double* bias,
                   const double* gamma, const double* beta, double eps, double* y, double* yabs);
+/* NEXT-4: Invariant Point Attention core (AF2 Alg.22 lines 7-10, reading G23; see fl_oracle.c). */
+int flo_ipa(int64_t N, int64_t H, int64_t c, int64_t Pq, int64_t Pv, int64_t cz, const double* q, const double* k,
+            const double* v, const double* qp, const double* kp, const double* vp, const double* R, const double* t,
+            const double* bias, const double* z, const double* gamma, double* o, double* op, double* opair);
 #endif

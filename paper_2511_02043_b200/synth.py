@@ -215,3 +215,31 @@ def key_mask(shape, *, seed=0, p_zero=0.1, lead=1):
         out[i] = (_rng(seed, "key_mask", i).random(tuple(inner)) >= p_zero).astype(np.uint8)
     return torch.from_numpy(out.reshape(shape))
 
+
+
+def ipa_inputs(N, H=12, c=16, Pq=4, Pv=8, cz=128, seed=0, dtype=torch.bfloat16):
+    """Invariant Point Attention inputs (reading G23; AF2 Alg.22 after its projections), protein-like:
+    frames with uniformly random rotations (normalised random quaternions) and translations on a centred
+    random walk of 3.8 A steps (C-alpha spacing); q, k, v, local points, pair bias and pair features
+    U(-1, 1) (points x 4 A); per-head gamma in (0.1, 1.1).  Random numbers only -- the method's arithmetic
+    lives in the kernels and the oracle.  Values are rounded to `dtype` (frames stay f32)."""
+    g = torch.Generator().manual_seed(seed)
+    u = lambda *s: torch.rand(*s, generator=g, dtype=torch.float64) * 2 - 1
+    quat = torch.randn(N, 4, generator=g, dtype=torch.float64)
+    quat = quat / quat.norm(dim=1, keepdim=True)
+    a, b, cc, d = quat.unbind(1)
+    R = torch.stack([
+        torch.stack([a * a + b * b - cc * cc - d * d, 2 * (b * cc - a * d), 2 * (b * d + a * cc)], -1),
+        torch.stack([2 * (b * cc + a * d), a * a - b * b + cc * cc - d * d, 2 * (cc * d - a * b)], -1),
+        torch.stack([2 * (b * d - a * cc), 2 * (cc * d + a * b), a * a - b * b - cc * cc + d * d], -1)], 1)
+    step = torch.randn(N, 3, generator=g, dtype=torch.float64)
+    step = 3.8 * step / step.norm(dim=1, keepdim=True)
+    t = torch.cumsum(step, 0)
+    t = t - t.mean(0)
+    out = dict(q=u(N, H, c), k=u(N, H, c), v=u(N, H, c), qp=4 * u(N, H, Pq, 3), kp=4 * u(N, H, Pq, 3),
+               vp=4 * u(N, H, Pv, 3), bias=u(H, N, N), z=u(N, N, cz),
+               gamma=0.1 + torch.rand(H, generator=g, dtype=torch.float64))
+    out = {k_: v_.to(dtype) for k_, v_ in out.items()}
+    out["gamma"] = out["gamma"].float()
+    out["R"], out["t"] = R.float(), t.float()
+    return out

@@ -701,3 +701,72 @@ def test_linear_ln_abs_scale():
     xp, wp = x.abs(), w.abs()
     y2, ya2 = oracle.linear_ln(xp, wp, with_abs=True)
     assert np.abs(y2 - ya2).max() < 1e-12
+
+
+# ---------------------------------------------------------------- NEXT-4: Invariant Point Attention (G23)
+def _ipa(N=7, H=2, c=4, Pq=2, Pv=3, cz=5, seed=4):
+    from paper_2511_02043_b200 import synth
+    return {k: v.double() for k, v in synth.ipa_inputs(N, H, c, Pq, Pv, cz, seed=seed, dtype=torch.float64).items()}
+
+
+def test_ipa_invariant_under_global_rigid_motion():
+    """IPA's defining property (AF2 Suppl. 1.8.2): a global rotation + translation of every frame leaves
+    the scalar, local-point and pair outputs unchanged."""
+    x = _ipa()
+    o, op, opair = oracle.ipa(**x)
+    g = torch.Generator().manual_seed(9)
+    qq = torch.randn(4, generator=g, dtype=torch.float64)
+    a, b, c, d = (qq / qq.norm()).tolist()
+    G = torch.tensor([[a * a + b * b - c * c - d * d, 2 * (b * c - a * d), 2 * (b * d + a * c)],
+                      [2 * (b * c + a * d), a * a - b * b + c * c - d * d, 2 * (c * d - a * b)],
+                      [2 * (b * d - a * c), 2 * (c * d + a * b), a * a - b * b - c * c + d * d]], dtype=torch.float64)
+    y = dict(x, R=G @ x["R"], t=x["t"] @ G.T + torch.tensor([5.0, -3.0, 11.0], dtype=torch.float64))
+    o2, op2, opair2 = oracle.ipa(**y)
+    np.testing.assert_allclose(o2, o, rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(op2, op, rtol=1e-10, atol=1e-10)
+    np.testing.assert_allclose(opair2, opair, rtol=1e-10, atol=1e-12)
+
+
+def test_ipa_without_points_is_biased_attention():
+    """gamma = 0 removes the point term: o = softmax(w_L (q.k / sqrt(c) + b)) v, i.e. the attention oracle
+    with scale w_L / sqrt(c) and additive bias w_L b (w_L = sqrt(1/3))."""
+    x = _ipa()
+    x["gamma"] = torch.zeros_like(x["gamma"])
+    o, _, _ = oracle.ipa(**x)
+    wl = math.sqrt(1 / 3)
+    q4 = x["q"].permute(1, 0, 2).unsqueeze(0)
+    k4 = x["k"].permute(1, 0, 2).unsqueeze(0)
+    v4 = x["v"].permute(1, 0, 2).unsqueeze(0)
+    ref, _ = oracle.attn(q4, k4, v4, scale=wl / math.sqrt(x["q"].shape[2]), bias=(wl * x["bias"]).unsqueeze(0))
+    np.testing.assert_allclose(o, np.asarray(ref).reshape(q4.shape).transpose(0, 2, 1, 3)[0], rtol=1e-12, atol=1e-13)
+
+
+def test_ipa_brute_force():
+    """Every output against a separate math.fsum transcription of AF2 Alg.22 lines 7-10 on a tiny case."""
+    x = _ipa(N=4, H=2, c=3, Pq=2, Pv=2, cz=3, seed=6)
+    o, op, opair = oracle.ipa(**x)
+    X = {k: v.numpy() for k, v in x.items()}
+    N, H, c = X["q"].shape
+    Pq, Pv = X["qp"].shape[2], X["vp"].shape[2]
+    wl, wc = math.sqrt(1 / 3), math.sqrt(2 / (9 * Pq))
+    glob = lambda i, pt: X["R"][i] @ pt + X["t"][i]
+    for i in range(N):
+        for h in range(H):
+            lg = []
+            for j in range(N):
+                dot = math.fsum(X["q"][i, h, d] * X["k"][j, h, d] for d in range(c))
+                dist = math.fsum(float(((glob(i, X["qp"][i, h, p]) - glob(j, X["kp"][j, h, p])) ** 2).sum())
+                                 for p in range(Pq))
+                lg.append(wl * (dot / math.sqrt(c) + X["bias"][h, i, j] - X["gamma"][h] * wc / 2 * dist))
+            m = max(lg)
+            e = [math.exp(v - m) for v in lg]
+            s = math.fsum(e)
+            a = [v / s for v in e]
+            for d in range(c):
+                assert abs(o[i, h, d] - math.fsum(a[j] * X["v"][j, h, d] for j in range(N))) < 1e-12
+            for f in range(X["z"].shape[2]):
+                assert abs(opair[i, h, f] - math.fsum(a[j] * X["z"][i, j, f] for j in range(N))) < 1e-12
+            for p in range(Pv):
+                gsum = sum(a[j] * glob(j, X["vp"][j, h, p]) for j in range(N))
+                loc = X["R"][i].T @ (gsum - X["t"][i])
+                np.testing.assert_allclose(op[i, h, p], loc, rtol=1e-10, atol=1e-12)
