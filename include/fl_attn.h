@@ -257,6 +257,29 @@ typedef struct {
 } fl_linear_args;
 fl_status fl_linear(const fl_linear_args* args);
 
+/* ---- Invariant Point Attention core (the paper names IPA among the variants
+ * FlexAttention cannot express, P:L47 / P:L443, with 12 heads of dimension 16; formula: reading
+ * G23 = AF2 Suppl. Alg.22 lines 7-10, after the linear projections) -------------------------------------
+ *   logit_ij^h = w_L ( c^-1/2 q_i.k_j + b_ij^h - (gamma_h w_C / 2) sum_p |T_i q_ip - T_j k_jp|^2 ),
+ *   w_L = sqrt(1/3), w_C = sqrt(2 / (9 Pq)), T x = R x + t,  a = softmax_j(logit),
+ *   o_i = sum_j a_ij v_j,  opair_i = sum_j a_ij z_ij,  op_ip = T_i^-1 sum_j a_ij T_j v_jp.
+ * Inputs (device, contiguous): q, k, v bf16 [N, H, c]; qp, kp bf16 [N, H, Pq, 3]; vp bf16 [N, H, Pv, 3];
+ * R f32 [N, 3, 3] (row-major, global = R local + t); t f32 [N, 3]; bias bf16 [H, N, N] (the projected pair
+ * bias b); z bf16 [N, N, cz]; gamma f32 [H] (already softplus'ed).  Outputs: o bf16 [N, H, c]; op f32
+ * [N, H, Pv, 3] (local frames); opair bf16 [N, H, cz].  Limits: c + 9 Pq + 2 <= 64, Pv <= 8, cz % 8 == 0, N <= 40000.  Launches: a prep kernel (the augmented 64-column Q' / K' of the point
+ * term's expansion, hi/lo bf16 pairs), a bias-scale kernel, the fused attention forward (tensor cores,
+ * softmax, o and the LSE), a finish kernel (pair and point outputs from the recomputed probabilities, fp32).
+ * Workspace: fl_ipa_workspace_size.  Asynchronous on `stream`. */
+typedef struct {
+  fl_tensor q, k, v, qp, kp, vp, R, t, bias, z, gamma;
+  fl_tensor o, op, opair;
+  void* stream;
+  void* workspace;
+  size_t workspace_bytes;
+} fl_ipa_args;
+fl_status fl_ipa_fwd(const fl_ipa_args* args);
+fl_status fl_ipa_workspace_size(const fl_ipa_args* args, size_t* bytes);
+
 /* Contiguous range [begin, end) of `units` independent work units owned by
  * `rank` of `world` (multi-GPU batch x head sharding; no collective). */
 void fl_shard_range(int64_t units, int32_t world, int32_t rank, int64_t* begin, int64_t* end);

@@ -18,7 +18,7 @@ EXPORTS = ["fl_attn_fwd", "fl_attn_workspace_size", "fl_attn_host_scratch_size",
            "fl_rsa_build_summaries", "fl_rsa_update_summaries", "fl_rsa_select", "fl_shard_range", "fl_diag_umma_gemm",
            "fl_diag_pipe_rate", "fl_debug_schedule", "fl_attn_args_size", "fl_attn_bwd",
            "fl_attn_bwd_workspace_size", "fl_status_string", "fl_last_error", "fl_abi_version", "fl_launch_count", "fl_debug_timing",
-           "fl_linear"]
+           "fl_linear", "fl_ipa_fwd", "fl_ipa_workspace_size"]
 
 
 class Tensor(C.Structure):
@@ -56,6 +56,12 @@ class BwdArgs(C.Structure):
 class LinearArgs(C.Structure):
     _fields_ = [("x", Tensor), ("w", Tensor), ("bias", Tensor), ("ln_gamma", Tensor), ("ln_beta", Tensor),
                 ("y", Tensor), ("ln_eps", C.c_float), ("stream", C.c_void_p)]
+
+
+class IpaArgs(C.Structure):
+    _fields_ = [(n, Tensor) for n in ("q", "k", "v", "qp", "kp", "vp", "R", "t", "bias", "z", "gamma", "o", "op",
+                                      "opair")] + [("stream", C.c_void_p), ("workspace", C.c_void_p),
+                                                   ("workspace_bytes", C.c_size_t)]
 
 
 class FlError(RuntimeError):
@@ -97,6 +103,10 @@ def lib():
         L.fl_debug_schedule.argtypes = [C.POINTER(AttnArgs), C.c_void_p, C.c_int64, C.POINTER(C.c_int64),
                                         C.POINTER(C.c_int32)]
         L.fl_debug_schedule.restype = C.c_int
+        L.fl_ipa_fwd.argtypes = [C.POINTER(IpaArgs)]
+        L.fl_ipa_fwd.restype = C.c_int
+        L.fl_ipa_workspace_size.argtypes = [C.POINTER(IpaArgs), C.POINTER(C.c_size_t)]
+        L.fl_ipa_workspace_size.restype = C.c_int
         L.fl_linear.argtypes = [C.POINTER(LinearArgs)]
         L.fl_linear.restype = C.c_int
         L.fl_attn_bwd.argtypes = [C.POINTER(BwdArgs)]

@@ -20,6 +20,8 @@
 namespace fl {
 cudaError_t launch_attn_simt(const AttnParams& p, cudaStream_t stream);
 cudaError_t launch_attn_tc(const AttnParams& p, const TmaMaps& maps, cudaStream_t stream);
+cudaError_t launch_ipa_prep(const IpaParams& p, cudaStream_t s);
+cudaError_t launch_ipa_finish(const IpaParams& p, const float* lse, void* opair, float* op, cudaStream_t s);
 cudaError_t launch_linear(const LinParams& p, const CUtensorMap& tx, const CUtensorMap& tw, const CUtensorMap& ty,
                           int y_tma, cudaStream_t stream);
 cudaError_t launch_pack_keymask(const unsigned char* km, int64_t sb, int64_t sg, int64_t sk, int B, int G, int Sk,
@@ -905,6 +907,139 @@ fl_status fl_linear(const fl_linear_args* a) {
   const cudaError_t e = launch_linear(p, tx, tw, ty, y_tma, static_cast<cudaStream_t>(a->stream));
   ++g_launches;
   return e == cudaSuccess ? FL_OK : cuda_fail(e, "linear launch");
+}
+
+namespace {
+struct IpaPrepared {
+  fl::IpaParams p;
+  int64_t N = 0, H = 0, c = 0, Pq = 0, Pv = 0, cz = 0;
+  size_t off_qa = 0, off_ka = 0, off_va = 0, off_gv = 0, off_bias = 0, off_o = 0, off_lse = 0, off_attn = 0,
+         total = 0;
+};
+
+bool dense(const fl_tensor& t, int rank, const int64_t* sizes, int dtype) {
+  if (!t.data || t.rank != rank || t.dtype != dtype) return false;
+  int64_t st = 1;
+  for (int d = rank - 1; d >= 0; --d) {
+    if (t.size[d] != sizes[d]) return false;
+    if (t.size[d] > 1 && t.stride[d] != st) return false;
+    st *= t.size[d];
+  }
+  return true;
+}
+
+fl_status prepare_ipa(const fl_ipa_args* a, IpaPrepared& P) {
+  if (!a) return fail(FL_ERR_INVALID_ARGUMENT, "args is NULL");
+  if (!a->q.data || a->q.rank != 3) return fail(FL_ERR_SHAPE_MISMATCH, "ipa: q [N, H, c]");
+  P.N = a->q.size[0]; P.H = a->q.size[1]; P.c = a->q.size[2];
+  if (!a->qp.data || a->qp.rank != 4 || !a->vp.data || a->vp.rank != 4 || !a->z.data || a->z.rank != 3)
+    return fail(FL_ERR_SHAPE_MISMATCH, "ipa: qp / kp [N, H, Pq, 3], vp [N, H, Pv, 3], z [N, N, cz]");
+  P.Pq = a->qp.size[2]; P.Pv = a->vp.size[2]; P.cz = a->z.size[2];
+  const int64_t N = P.N, H = P.H, c = P.c;
+  const int64_t s_nhc[3] = {N, H, c}, s_qp[4] = {N, H, P.Pq, 3}, s_vp[4] = {N, H, P.Pv, 3}, s_R[3] = {N, 3, 3},
+                s_t[2] = {N, 3}, s_b[3] = {H, N, N}, s_z[3] = {N, N, P.cz}, s_g[1] = {H}, s_opair[3] = {N, H, P.cz};
+  if (!dense(a->q, 3, s_nhc, FL_BF16) || !dense(a->k, 3, s_nhc, FL_BF16) || !dense(a->v, 3, s_nhc, FL_BF16) ||
+      !dense(a->qp, 4, s_qp, FL_BF16) || !dense(a->kp, 4, s_qp, FL_BF16) || !dense(a->vp, 4, s_vp, FL_BF16) ||
+      !dense(a->R, 3, s_R, FL_F32) || !dense(a->t, 2, s_t, FL_F32) || !dense(a->bias, 3, s_b, FL_BF16) ||
+      !dense(a->z, 3, s_z, FL_BF16) || !dense(a->gamma, 1, s_g, FL_F32) || !dense(a->o, 3, s_nhc, FL_BF16) ||
+      !dense(a->op, 4, s_vp, FL_F32) || !dense(a->opair, 3, s_opair, FL_BF16))
+    return fail(FL_ERR_SHAPE_MISMATCH, "ipa: tensors must be contiguous with the documented shapes and dtypes");
+  if (N < 1 || H < 1 || c < 1 || c + 9 * P.Pq + 2 > 64 || P.cz < 8 || P.cz % 8 != 0 || P.Pv < 0 || N > 40000 ||
+      3 * P.Pv > 24)
+    return fail(FL_ERR_UNSUPPORTED, "ipa: c + 9 Pq + 2 <= 64, Pv <= 8, cz % 8 == 0, N <= 40000");
+  for (const fl_tensor* t : {&a->q, &a->k, &a->v, &a->qp, &a->kp, &a->vp, &a->R, &a->t, &a->bias, &a->z, &a->gamma,
+                             &a->o, &a->op, &a->opair})
+    if (!on_device(t->data)) return fail(FL_ERR_INVALID_ARGUMENT, "ipa: pointers must be device memory");
+  auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
+  size_t off = 0;
+  P.off_qa = off; off += up(N * H * 64 * 2);
+  P.off_ka = off; off += up(N * H * 64 * 2);
+  P.off_va = off; off += up(N * H * 64 * 2);
+  P.off_gv = off; off += up(N * H * (P.Pv > 0 ? P.Pv : 1) * 3 * 4);
+  P.off_bias = off; off += up(H * N * N * 4);
+  P.off_o = off; off += up(N * H * 64 * 2);
+  P.off_lse = off; off += up(H * N * 4);
+  P.off_attn = off;
+  off += 1024 * 1024;                                // the attention call's workspace (ticket counter)
+  P.total = off;
+  fl::IpaParams& p = P.p;
+  p.N = (int)N; p.H = (int)H; p.c = (int)c; p.Pq = (int)P.Pq; p.Pv = (int)P.Pv; p.cz = (int)P.cz;
+  p.q = static_cast<const __nv_bfloat16*>(a->q.data); p.k = static_cast<const __nv_bfloat16*>(a->k.data);
+  p.qp = static_cast<const __nv_bfloat16*>(a->qp.data); p.kp = static_cast<const __nv_bfloat16*>(a->kp.data);
+  p.vp = static_cast<const __nv_bfloat16*>(a->vp.data); p.bias = static_cast<const __nv_bfloat16*>(a->bias.data);
+  p.z = static_cast<const __nv_bfloat16*>(a->z.data);
+  p.R = static_cast<const float*>(a->R.data); p.t = static_cast<const float*>(a->t.data);
+  p.gamma = static_cast<const float*>(a->gamma.data);
+  return FL_OK;
+}
+
+fl_tensor mk_tensor(void* data, int dtype, std::initializer_list<int64_t> sizes, std::initializer_list<int64_t> strides) {
+  fl_tensor t;
+  memset(&t, 0, sizeof t);
+  t.data = data; t.dtype = dtype; t.rank = (int)sizes.size();
+  int i = 0;
+  for (int64_t x : sizes) t.size[i++] = x;
+  i = 0;
+  for (int64_t x : strides) t.stride[i++] = x;
+  return t;
+}
+}  // namespace
+
+fl_status fl_ipa_workspace_size(const fl_ipa_args* args, size_t* bytes) {
+  if (!bytes) return fail(FL_ERR_INVALID_ARGUMENT, "bytes is NULL");
+  IpaPrepared P;
+  fl_status s = prepare_ipa(args, P);
+  if (s != FL_OK) return s;
+  *bytes = P.total;
+  return FL_OK;
+}
+
+fl_status fl_ipa_fwd(const fl_ipa_args* args) {
+  IpaPrepared P;
+  fl_status s = prepare_ipa(args, P);
+  if (s != FL_OK) return s;
+  if (!args->workspace || args->workspace_bytes < P.total)
+    return fail(FL_ERR_WORKSPACE, "ipa needs %zu bytes of workspace (fl_ipa_workspace_size)", P.total);
+  char* ws = static_cast<char*>(args->workspace);
+  cudaStream_t stream = static_cast<cudaStream_t>(args->stream);
+  fl::IpaParams& p = P.p;
+  p.qa = reinterpret_cast<__nv_bfloat16*>(ws + P.off_qa);
+  p.ka = reinterpret_cast<__nv_bfloat16*>(ws + P.off_ka);
+  p.gv = reinterpret_cast<float*>(ws + P.off_gv);
+  p.bias_s = reinterpret_cast<__nv_bfloat16*>(ws + P.off_bias);
+  const int64_t N = P.N, H = P.H, c = P.c;
+  // V' = [v | 0] (64 columns: the attention kernel's D_v = D_qk); its scalar output o = the first c columns
+  __nv_bfloat16* va = reinterpret_cast<__nv_bfloat16*>(ws + P.off_va);
+  cudaError_t e = cudaMemsetAsync(va, 0, N * H * 64 * 2, stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(va, 64 * 2, args->v.data, c * 2, c * 2, N * H, cudaMemcpyDeviceToDevice, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "ipa V' staging");
+  if ((e = launch_ipa_prep(p, stream)) != cudaSuccess) return cuda_fail(e, "ipa prep launch");
+  g_launches += 2;
+  // the fused attention forward over the augmented operands: [B=1, H, S=N, 64] views of [N, H, 64]
+  fl_attn_args at;
+  memset(&at, 0, sizeof at);
+  at.var.abi_version = FL_ABI_VERSION;
+  at.var.scale = 1.0f;
+  at.q = mk_tensor(p.qa, FL_BF16, {1, H, N, 64}, {N * H * 64, 64, H * 64, 1});
+  at.k = mk_tensor(p.ka, FL_BF16, {1, H, N, 64}, {N * H * 64, 64, H * 64, 1});
+  at.v = mk_tensor(va, FL_BF16, {1, H, N, 64}, {N * H * 64, 64, H * 64, 1});
+  void* o64 = ws + P.off_o;
+  at.o = mk_tensor(o64, FL_BF16, {1, H, N, 64}, {N * H * 64, 64, H * 64, 1});
+  float* lse = reinterpret_cast<float*>(ws + P.off_lse);
+  at.lse = mk_tensor(lse, FL_F32, {1, H, N}, {H * N, N, 1});
+  at.var.bias = mk_tensor(p.bias_s, FL_BF16, {1, H, N, N}, {H * N * N, N * N, N, 1});
+  at.stream = stream;
+  at.workspace = ws + P.off_attn;
+  at.workspace_bytes = P.total - P.off_attn;
+  if ((s = fl_attn_fwd(&at)) != FL_OK) return s;
+  // o = the first c columns of O'
+  e = cudaMemcpy2DAsync(args->o.data, c * 2, o64, 64 * 2, c * 2, N * H, cudaMemcpyDeviceToDevice, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "ipa o copy");
+  if ((e = launch_ipa_finish(p, lse, args->opair.data, static_cast<float*>(args->op.data), stream)) != cudaSuccess)
+    return cuda_fail(e, "ipa finish launch");
+  ++g_launches;
+  return FL_OK;
 }
 
 fl_status fl_diag_pipe_rate(int32_t op, int32_t iters, float* sink, int64_t* ops, void* stream) {

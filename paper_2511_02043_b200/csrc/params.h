@@ -4,6 +4,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda.h>
+#include <cuda_bf16.h>
 
 namespace fl {
 
@@ -104,6 +105,16 @@ struct LinParams {
   float eps;
   void* y;                   // bf16
   int64_t ys_m, ys_n;        // element strides of y
+};
+
+// Invariant Point Attention core (ipa.cu, NEXT-4), built by host.cu's fl_ipa_fwd.
+struct IpaParams {
+  int N, H, c, Pq, Pv, cz;
+  const __nv_bfloat16 *q, *k, *qp, *kp, *vp, *bias, *z;   // contiguous: [N,H,c], [N,H,P,3], [H,N,N], [N,N,cz]
+  const float *R, *t, *gamma;                              // [N,3,3] (x_global = R x + t), [N,3], [H]
+  __nv_bfloat16 *qa, *ka;                                  // augmented Q', K' [N,H,64]
+  float* gv;                                               // global value points T_j v_jp [N,H,Pv*3]
+  __nv_bfloat16* bias_s;                                   // w_L b [H,N,N] (bf16: the attention's vector bias path)
 };
 
 // RSA block selection (rsa.cu), built by host.cu's fl_rsa_select.

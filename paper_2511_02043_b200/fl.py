@@ -303,6 +303,30 @@ def linear(x: torch.Tensor, w: torch.Tensor, bias=None, ln_gamma=None, ln_beta=N
     return out
 
 
+def ipa_fwd(q, k, v, qp, kp, vp, R, t, bias, z, gamma, *, workspace=None, stream=None):
+    """Invariant Point Attention core (fl_ipa_fwd, NEXT-4, reading G23): q, k, v bf16 [N, H, c]; qp, kp bf16
+    [N, H, Pq, 3]; vp bf16 [N, H, Pv, 3]; R f32 [N, 3, 3]; t f32 [N, 3]; bias bf16 [H, N, N]; z bf16
+    [N, N, cz]; gamma f32 [H].  Returns (o bf16 [N, H, c], op f32 [N, H, Pv, 3], opair bf16 [N, H, cz])."""
+    N, H, c = q.shape
+    Pv, cz = vp.shape[2], z.shape[2]
+    o = torch.empty(N, H, c, device=q.device, dtype=torch.bfloat16)
+    op = torch.empty(N, H, Pv, 3, device=q.device, dtype=torch.float32)
+    opair = torch.empty(N, H, cz, device=q.device, dtype=torch.bfloat16)
+    a = _lib.IpaArgs()
+    for name, tt in (("q", q), ("k", k), ("v", v), ("qp", qp), ("kp", kp), ("vp", vp), ("R", R), ("t", t),
+                     ("bias", bias), ("z", z), ("gamma", gamma), ("o", o), ("op", op), ("opair", opair)):
+        setattr(a, name, tensor(tt))
+    a.stream = _stream_handle(q.device, stream)
+    need = C.c_size_t(0)
+    _lib.check(_lib.lib().fl_ipa_workspace_size(C.byref(a), C.byref(need)))
+    if workspace is None or workspace.numel() * workspace.element_size() < need.value:
+        workspace = torch.empty(need.value, dtype=torch.uint8, device=q.device)
+    a.workspace, a.workspace_bytes = workspace.data_ptr(), need.value
+    _lib.check(_lib.lib().fl_ipa_fwd(C.byref(a)))
+    _keep_alive_on(stream, [workspace])
+    return o, op, opair
+
+
 def diag_umma_gemm(a: torch.Tensor, b: torch.Tensor, n: int, k: int, b_mn_major=False, a_from_tmem=False):
     c = torch.empty(128, n, device=a.device, dtype=torch.float32)
     s = torch.cuda.current_stream(a.device).cuda_stream

@@ -219,6 +219,42 @@ def evo_block_grid(quick):
     return rows
 
 
+def ipa_grid(quick):
+    """NEXT-4: the Invariant Point Attention core (AF2 Alg.22 lines 7-10, reading G23; 12 heads x 16, P:L891;
+    4 query / 8 value points, c_z = 128) through fl_ipa_fwd vs the same core in PyTorch (fp32 points,
+    bf16 elsewhere) eager and under torch.compile."""
+    from paper_2511_02043_b200 import synth
+    wl = math.sqrt(1 / 3)
+
+    def torch_ipa(q, k, v, qp, kp, vp, R, t, bias, z, gamma):
+        N, H, c = q.shape
+        Pq = qp.shape[2]
+        wc = math.sqrt(2 / (9 * Pq))
+        glob = lambda pts: torch.einsum("nij,nhpj->nhpi", R, pts.float()) + t[:, None, None, :]
+        x, y, g = glob(qp), glob(kp), glob(vp)
+        d2 = ((x[:, None] - y[None, :]) ** 2).sum((-1, -2))                  # [i, j, h]
+        logit = wl * (torch.einsum("ihc,jhc->ijh", q.float(), k.float()) / math.sqrt(c) + bias.float().permute(1, 2, 0)
+                      - gamma * wc / 2 * d2)
+        a = torch.softmax(logit, dim=1)                                       # over j
+        o = torch.einsum("ijh,jhc->ihc", a, v.float())
+        opair = torch.einsum("ijh,ijc->ihc", a, z.float())
+        gs = torch.einsum("ijh,jhpx->ihpx", a, g) - t[:, None, None, :]
+        op = torch.einsum("nji,nhpj->nhpi", R, gs)
+        return o, op, opair
+    tc = torch.compile(torch_ipa)
+    rows = []
+    for N in ((256,) if quick else (128, 256, 384)):
+        x = {k_: v_.cuda() for k_, v_ in synth.ipa_inputs(N, seed=1).items()}
+        t_ours = timeit(lambda: fl.ipa_fwd(**x), graph=True)
+        t_tc = timeit(lambda: tc(**x))
+        t_eager = timeit(lambda: torch_ipa(**x))
+        H, c, Pq, Pv, cz = 12, 16, 4, 8, 128
+        flops = 2 * H * N * N * (64 + 64) + 2 * H * N * N * (cz + 3 * Pv)   # tensor-core logits + PV, outputs
+        rows.append(("ipa", "compile", N, 1, t_ours, t_tc, 0.0, flops / t_ours / 1e9))
+        rows.append(("ipa", "eager", N, 1, t_ours, t_eager, 0.0, flops / t_ours / 1e9))
+    return rows
+
+
 def main():
     import torch._dynamo
     torch._dynamo.config.recompile_limit = 100000        # every (shape, mod) recompiles flex_attention once
@@ -231,7 +267,7 @@ def main():
     print("| variant | heads | S (or N_seq) | B | ours ms | comparator ms | flex block-mask ms | ours TFLOP/s | "
           "speed-up vs comparator kernel | incl. mask |")
     print("|---|---|---|---|---|---|---|---|---|---|")
-    ap_rows = (evo_block_grid(a.quick),) if a.block_only else (flex_grid(a.quick), diff_grid(a.quick), evo_grid(a.quick), evo_block_grid(a.quick))
+    ap_rows = (evo_block_grid(a.quick), ipa_grid(a.quick)) if a.block_only else (flex_grid(a.quick), diff_grid(a.quick), evo_grid(a.quick), evo_block_grid(a.quick), ipa_grid(a.quick))
     for rows in ap_rows:
         for name, heads, S, B, to, tf, tm, tfl in rows:
             sp = tf / to if tf == tf else float("nan")
@@ -240,7 +276,8 @@ def main():
             sys.stdout.flush()
     print("\ncomparator: FlexAttention (torch.compile'd flex_attention) for the first block; torch.compile of "
           "Listing 4 for diff; torch.compile of the eager Evoformer row attention for evoformer_row; "
-          "for evoformer_block the whole AF2 Alg.7 block in PyTorch (cuBLAS + SDPA) under torch.compile / eager.")
+          "for evoformer_block the whole AF2 Alg.7 block in PyTorch (cuBLAS + SDPA) under torch.compile / eager; "
+          "for ipa the IPA core (AF2 Alg.22 lines 7-10) in PyTorch under torch.compile / eager.")
 
 
 if __name__ == "__main__":
