@@ -63,6 +63,10 @@ VARIANTS = {
     # configs[4]: Rectified Sparse Attention B=4 H=32 S=32768 D=128 (blocks 128, top-16 + sink + diagonal)
     "rsa": dict(rsa="prefill", B=4, H=32, S=32768, D=128, topk=16),
     "rsa_decode": dict(rsa="decode", B=4, H=32, S=32768, D=128, topk=16),
+    # SURVEY §8(f) NEXT-2 / NEXT-4 (not BASELINE lines): the whole Evoformer row-attention block (AF2 Alg.7)
+    # chained from this package's kernels, and the Invariant Point Attention core (12 heads x 16)
+    "evo_block": dict(special="evo_block", Ns=512, Nr=384),
+    "ipa": dict(special="ipa", N=384),
 }
 SUITES = {"flex": ["causal", "alibi", "sliding", "softcap", "document"]}
 VARIANT_KW = ("mod", "softcap", "mask", "window", "prefix", "diff", "lam")
@@ -626,10 +630,38 @@ def rsa_oracle_rate(cfg, q1, k1, v1, budget_s):
             f"(b=0,h=0): oracle selection in full + {nr} of {Sq} attention rows; rate of that head", t_sel + t_att)
 
 
+def special_job(variant, device):
+    """NEXT-2 / NEXT-4 workloads (single GPU, not sharded): one call each, flops as in tools/paper_grid.py."""
+    from paper_2511_02043_b200 import fl, synth
+    cfg = VARIANTS[variant]
+    if variant == "evo_block":
+        from paper_2511_02043_b200 import evoformer
+        H, c, cm, cz, Ns, Nr = 8, 32, 256, 128, cfg["Ns"], cfg["Nr"]
+        w = evoformer.synthetic_weights(c_m=cm, c_z=cz, H=H, c=c, seed=1, device=device)
+        m = (synth.uniform((Ns, Nr, cm), seed=2, tensor="q", lead=2) * 2).to(torch.bfloat16).to(device)
+        z = (synth.uniform((Nr, Nr, cz), seed=2, tensor="k", lead=2) * 2).to(torch.bfloat16).to(device)
+        blk = evoformer.RowAttnBlock(w, Ns, Nr, device=device)
+        flops = 2 * Ns * Nr * cm * 4 * H * c + 2 * Nr * Nr * cz * H + 4 * Ns * H * Nr * Nr * c + 2 * Ns * Nr * H * c * cm
+        job = Job(variant, f"evoformer_row_block_bf16_Nseq{Ns}_Nres{Nr}_cm{cm}_cz{cz}_H{H}_c{c}")
+        job.calls.append(Call("evo_block", lambda: blk(m, z), flops, 0, "tensor", kernel="attn_tc_kernel"))
+    else:
+        N = cfg["N"]
+        x = {k: v.to(device) for k, v in synth.ipa_inputs(N, seed=1).items()}
+        ws = torch.empty(64 << 20, dtype=torch.uint8, device=device)
+        flops = 2 * 12 * N * N * (64 + 64) + 2 * 12 * N * N * (128 + 24)
+        job = Job(variant, f"ipa_core_N{N}_H12_c16_Pq4_Pv8_cz128")
+        job.calls.append(Call("ipa", lambda: fl.ipa_fwd(**x, workspace=ws), flops, 0, "tensor", kernel="attn_tc_kernel"))
+    job.step_flops = job.calls[0].flops
+    job.units = "whole problem (not sharded)"
+    return job
+
+
 def make_job(variant, rank, world, device, with_host=True):
     if variant in SUITES:
         return dense_job(SUITES[variant], rank, world, device, with_host)
     cfg = VARIANTS[variant]
+    if cfg.get("special"):
+        return special_job(variant, device)
     if cfg.get("evo"):
         return evo_job(variant, rank, world, device, with_host)
     if cfg.get("rsa"):
@@ -715,6 +747,7 @@ def oracle_only_job(variant):
 
 
 EXTRA_CONFIGS = ["c1", "diff", "evo_row", "evo_col", "rsa", "rsa_decode"]   # BASELINE configs[0, 2, 3, 4]
+NEXT_EXTRAS = ["bwd_causal", "evo_block", "ipa"]     # SURVEY §8(f) rows, single-GPU runs only
 
 
 def time_job(job, steps, warmup, device, stream, use_graph=True, flush=None, clk=None):
@@ -948,6 +981,18 @@ def main():
             del xj
             torch.cuda.empty_cache()
 
+    # the §8(f) rows (backward, Evoformer block, IPA), one GPU only: timed the same way, reported apart
+    nexts = {}
+    if args.variant == "flex" and not args.no_extra and world == 1:
+        for name in NEXT_EXTRAS:
+            xj = make_job(name, rank, world, device, with_host=False)
+            xt = time_job(xj, 3, args.warmup, device, stream, flush=flush)
+            nexts[name] = {"workload": xj.workload, "value": xj.step_flops / (xt["ms_per_step"] * 1e-3) / 1e12,
+                           "unit": "TFLOP/s", "ms_per_step": xt["ms_per_step"],
+                           "gpu_launches_per_step": xt["launches"] // 3}
+            del xj
+            torch.cuda.empty_cache()
+
     if rank != 0:
         if world > 1:
             torch.distributed.barrier()
@@ -973,6 +1018,8 @@ def main():
         line["e2e"] = e2e
     if configs:
         line["configs"] = configs
+    if nexts:
+        line["next"] = nexts
     if not args.no_cpu_baseline and job.oracle is not None:
         v_cpu, cores, sample, _ = job.oracle(15.0)
         line["cpu_baseline"] = {"value": v_cpu, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample}
