@@ -865,6 +865,9 @@ fl_status fl_linear(const fl_linear_args* a) {
                           f32s[i]->stride[0] != 1))
       return fail(FL_ERR_SHAPE_MISMATCH, "linear: bias f32 [N], ln_gamma / ln_beta f32 [K], contiguous");
   if (a->ln_beta.data && !a->ln_gamma.data) return fail(FL_ERR_INVALID_ARGUMENT, "linear: ln_beta needs ln_gamma");
+  for (const void* v : {a->ln_gamma.data, a->ln_beta.data})
+    if (v && reinterpret_cast<uintptr_t>(v) % 16 != 0)
+      return fail(FL_ERR_MISALIGNED, "linear: ln_gamma / ln_beta need 16-byte alignment");
   const void* ptrs[] = {x.data, w.data, y.data, a->bias.data, a->ln_gamma.data, a->ln_beta.data};
   for (const void* p : ptrs)
     if (!on_device(p)) return fail(FL_ERR_INVALID_ARGUMENT, "linear: pointers must be device memory");

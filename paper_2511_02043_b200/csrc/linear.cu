@@ -135,12 +135,17 @@ __global__ void __launch_bounds__(kLinThreads, 1)
           const uint4 u = *a;
           const uint32_t ww[4] = {u.x, u.y, u.z, u.w};
           uint32_t o[4];
+          const int k8 = c * 64 + pc * 8;              // gamma / beta of these 8 columns: 4 vector loads
+          const float4 g0 = __ldg(reinterpret_cast<const float4*>(p.ln_g + k8));
+          const float4 g1 = __ldg(reinterpret_cast<const float4*>(p.ln_g + k8 + 4));
+          const float4 b0 = p.ln_b ? __ldg(reinterpret_cast<const float4*>(p.ln_b + k8)) : make_float4(0.f, 0.f, 0.f, 0.f);
+          const float4 b1 = p.ln_b ? __ldg(reinterpret_cast<const float4*>(p.ln_b + k8 + 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+          const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+          const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
-            const int k = c * 64 + pc * 8 + 2 * t;
-            const float y0 = fmaf((bf16_lo(ww[t]) - mean) * rstd, __ldg(p.ln_g + k), p.ln_b ? __ldg(p.ln_b + k) : 0.f);
-            const float y1 =
-                fmaf((bf16_hi(ww[t]) - mean) * rstd, __ldg(p.ln_g + k + 1), p.ln_b ? __ldg(p.ln_b + k + 1) : 0.f);
+            const float y0 = fmaf((bf16_lo(ww[t]) - mean) * rstd, gg[2 * t], bb[2 * t]);
+            const float y1 = fmaf((bf16_hi(ww[t]) - mean) * rstd, gg[2 * t + 1], bb[2 * t + 1]);
             o[t] = pack_bf16(y0, y1);
           }
           *a = make_uint4(o[0], o[1], o[2], o[3]);
@@ -154,6 +159,14 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
     __nv_bfloat16* yr = static_cast<__nv_bfloat16*>(p.y) + (int64_t)(row_ok ? m : 0) * p.ys_m;
     const bool vec = p.ys_n == 1 && (reinterpret_cast<uintptr_t>(p.y) % 16 == 0) && (p.ys_m % 8 == 0);
+    // coalesced epilogue: the tile is staged in shared memory (row = thread, swizzled 16-B chunks), then
+    // written back by consecutive threads along each row (16 threads x 16 B = one 256-B row segment)
+#ifdef FL_LIN_STAGED_STORE   // measured slower (QKVG projection 468 -> 540 us): opt-in
+    const bool y_co = !y_tma && vec && p.NT == 128;
+#else
+    const bool y_co = false;
+#endif
+    const bool stage = y_tma || y_co;
     for (int nt = 0; nt < n_nt; ++nt) {
       const int b = nt & 1, n0 = nt * p.NT;
       mbar_wait(&acc_full[b], (nt >> 1) & 1);
@@ -163,12 +176,24 @@ __global__ void __launch_bounds__(kLinThreads, 1)
         tmem_ld32(tmem + lane_base + b * 128 + c, acc);   // every lane loads (.sync.aligned)
         tmem_wait_ld();
         float f[32];
+        if (p.bias && n0 + c + 32 <= p.N && ((reinterpret_cast<uintptr_t>(p.bias + n0 + c) & 15) == 0)) {
+          const float4* b4 = reinterpret_cast<const float4*>(p.bias + n0 + c);   // 8 vector loads, not 32
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          const int n = n0 + c + t;
-          f[t] = __uint_as_float(acc[t]) + ((p.bias && n < p.N) ? __ldg(p.bias + n) : 0.f);
+          for (int t4 = 0; t4 < 8; ++t4) {
+            const float4 bb = __ldg(b4 + t4);
+            f[4 * t4] = __uint_as_float(acc[4 * t4]) + bb.x;
+            f[4 * t4 + 1] = __uint_as_float(acc[4 * t4 + 1]) + bb.y;
+            f[4 * t4 + 2] = __uint_as_float(acc[4 * t4 + 2]) + bb.z;
+            f[4 * t4 + 3] = __uint_as_float(acc[4 * t4 + 3]) + bb.w;
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const int n = n0 + c + t;
+            f[t] = __uint_as_float(acc[t]) + ((p.bias && n < p.N) ? __ldg(p.bias + n) : 0.f);
+          }
         }
-        if (y_tma) {
+        if (stage) {
           // swizzled staging (slab c / 64, 16-B chunk q of row r at (q ^ (r & 7)) * 16): conflict-free; one
           // TMA store per 64-column slab below writes whole rows (rows past M / columns past N are clipped)
           uint8_t* srow = sY + (c >> 6) * 128 * 128 + r * 128;
@@ -196,6 +221,26 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&acc_empty[b]);                      // the accumulator may take tile nt + 2
+      if (y_co) {
+        named_bar_sync(1, 128);                        // the tile is staged
+#pragma unroll 4
+        for (int pass = 0; pass < 16; ++pass) {
+          const int row = pass * 8 + (r >> 4), q = r & 15, mm = m0 + row;
+          const uint4 v = *reinterpret_cast<const uint4*>(sY + (q >> 3) * 128 * 128 + row * 128 +
+                                                          (((q & 7) ^ (row & 7)) << 4));
+          if (mm < p.M) {
+            __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.y) + (int64_t)mm * p.ys_m + n0 + q * 8;
+            if (n0 + q * 8 + 8 <= p.N) {
+              *reinterpret_cast<uint4*>(dst) = v;
+            } else {
+              const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+              for (int e = 0; e < 8 && n0 + q * 8 + e < p.N; ++e)
+                dst[e] = __ushort_as_bfloat16((unsigned short)(e & 1 ? w[e >> 1] >> 16 : w[e >> 1] & 0xFFFFu));
+            }
+          }
+        }
+        named_bar_sync(1, 128);                        // the staging buffer is free for the next tile
+      }
       if (y_tma) {
         fence_proxy_async_smem();                      // staging stores -> the TMA engine
         named_bar_sync(1, 128);
