@@ -954,7 +954,7 @@ def main():
         e2e_ms = max_over_ranks([a0.elapsed_time(a1) / n_e2e], device, world)[0]
         e2e = {"value": step_flops_all / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
-               "api": "fl_attn_fwd_host / pinned host buffers (H2D + kernel + D2H on one stream)"}
+               "api": "fl_attn_fwd_host / pinned host buffers (batch chunks: H2D, kernel, D2H pipelined on three streams)"}
     mufu = mufu_peaks(device) if rank == 0 else None
     pk, pk_src = peaks()
     prof = {}

@@ -191,7 +191,11 @@ fl_status fl_attn_workspace_size(const fl_attn_args* args, size_t* bytes);
  * memory (pinned for overlap).  `device_scratch` holds device copies laid out
  * by the library: size from fl_attn_host_scratch_size.  The call enqueues
  * H2D copies, the kernel and the D2H copy of o (and lse) on `stream`, and
- * returns without synchronising.  Host tensors must be contiguous. */
+ * returns without synchronising.  Host tensors must be contiguous.  With B >= 2
+ * and only q / k / v / doc_offsets batched (no bias, key mask, gate, block lists,
+ * paged KV), the batch is split into up to 4 chunks whose H2D (an internal copy-in
+ * stream), kernel (`stream`) and D2H (an internal copy-out stream) overlap; events
+ * order them after `stream`'s prior work and `stream` waits for the last D2H. */
 fl_status fl_attn_host_scratch_size(const fl_attn_args* args, size_t* bytes);
 fl_status fl_attn_fwd_host(const fl_attn_args* host_args, void* device_scratch, size_t scratch_bytes);
 

@@ -622,6 +622,74 @@ fl_status fl_attn_fwd_host(const fl_attn_args* host_args, void* scratch, size_t 
   }
   d.workspace = base + hp.total;
   d.workspace_bytes = P0.ws_bytes;
+  // Pipelined over batch chunks when only q / k / v (+ small per-call vectors) carry the batch: chunk c's
+  // H2D (copy-in stream), kernel (the caller's stream) and D2H (copy-out stream) overlap with the other
+  // chunks' transfers; events order them, and the caller's stream waits for the last D2H.
+  const int64_t B = host_args->q.rank >= 4 ? host_args->q.size[0] : 1;
+  const bool chunkable = B >= 2 && !d.var.bias.data && !d.var.key_mask.data && !d.var.gate.data &&
+                         !d.var.blk_idx.data && !d.var.kv_page_table.data && d.k.size[0] == B && d.v.size[0] == B &&
+                         d.o.size[0] == B && (!d.lse.data || d.lse.size[0] == B) &&
+                         (!d.var.doc_offsets.data || d.var.doc_offsets.size[0] == B);
+  if (chunkable) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static cudaStream_t s_in[16], s_out[16];
+    static std::once_flag once[16];
+    if (dev < 0 || dev >= 16) dev = 0;
+    std::call_once(once[dev], [&] {
+      cudaStreamCreateWithFlags(&s_in[dev], cudaStreamNonBlocking);
+      cudaStreamCreateWithFlags(&s_out[dev], cudaStreamNonBlocking);
+    });
+    const int nch = (int)std::min<int64_t>(B, 4);
+    cudaEvent_t ev[2 * 4 + 2];
+    for (auto& e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    cudaEventRecord(ev[0], stream);                  // the streams start after the caller's prior work
+    cudaStreamWaitEvent(s_in[dev], ev[0], 0);
+    cudaStreamWaitEvent(s_out[dev], ev[0], 0);
+    // small inputs (no batch dim) once, in full
+    for (int i = 0; i < hp.n; ++i) {
+      fl_tensor* t = hp.items[i].t;
+      if (hp.items[i].out || t == &d.q || t == &d.k || t == &d.v || t == &d.var.doc_offsets) continue;
+      cudaMemcpyAsync(t->data, host_ptr[i], hp.items[i].bytes, cudaMemcpyHostToDevice, s_in[dev]);
+    }
+    fl_status st = FL_OK;
+    for (int c = 0; c < nch && st == FL_OK; ++c) {
+      const int64_t b0 = B * c / nch, b1 = B * (c + 1) / nch, nb = b1 - b0;
+      fl_attn_args dc = d;
+      for (int i = 0; i < hp.n; ++i) {
+        fl_tensor* t = hp.items[i].t;
+        const bool batched = t == &d.q || t == &d.k || t == &d.v || t == &d.var.doc_offsets || t == &d.o || t == &d.lse;
+        if (!batched) continue;
+        const size_t row = hp.items[i].bytes / (size_t)B;    // bytes per batch entry (contiguous, batch-major)
+        char* dptr = static_cast<char*>(t->data) + row * b0;
+        // the chunk's view: same tensor, batch range [b0, b1)
+        fl_tensor* ct = t == &d.q ? &dc.q : t == &d.k ? &dc.k : t == &d.v ? &dc.v : t == &d.o ? &dc.o
+                      : t == &d.lse ? &dc.lse : &dc.var.doc_offsets;
+        ct->data = dptr;
+        ct->size[0] = nb;
+        if (!hp.items[i].out)
+          cudaMemcpyAsync(dptr, static_cast<char*>(host_ptr[i]) + row * b0, row * nb, cudaMemcpyHostToDevice, s_in[dev]);
+      }
+      cudaEventRecord(ev[1 + c], s_in[dev]);
+      cudaStreamWaitEvent(stream, ev[1 + c], 0);
+      Prepared Pc;
+      if ((st = prepare(&dc, Pc, true)) == FL_OK) st = launch_prepared(Pc, &dc);
+      cudaEventRecord(ev[1 + nch + c], stream);
+      cudaStreamWaitEvent(s_out[dev], ev[1 + nch + c], 0);
+      for (int i = 0; i < hp.n; ++i) {
+        if (!hp.items[i].out) continue;
+        const size_t row = hp.items[i].bytes / (size_t)B;
+        cudaMemcpyAsync(static_cast<char*>(host_ptr[i]) + row * b0, static_cast<char*>(hp.items[i].t->data) + row * b0,
+                        row * nb, cudaMemcpyDeviceToHost, s_out[dev]);
+      }
+    }
+    cudaEventRecord(ev[2 * nch + 1], s_out[dev]);
+    cudaStreamWaitEvent(stream, ev[2 * nch + 1], 0);   // the call's completion is visible on the caller's stream
+    for (auto& e : ev) cudaEventDestroy(e);          // deferred by the runtime until the events complete
+    if (st != FL_OK) return st;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? FL_OK : cuda_fail(e, "pipelined host call");
+  }
   Prepared P;
   if ((s = prepare(&d, P, true)) != FL_OK) return s;
   for (int i = 0; i < hp.n; ++i) {

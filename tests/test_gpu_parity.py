@@ -225,6 +225,23 @@ def test_host_entry_matches_device_entry(fl):
     assert torch.equal(out, dev.cpu())
 
 
+@pytest.mark.parametrize("case", [dict(B=4, S=300, D=128, mask="document", n_docs=3, Hq=2),
+                                  dict(B=3, S=200, D=64, mask="causal", mod="alibi")])
+def test_host_entry_pipelined_matches_device_entry(fl, case):
+    """B >= 2: fl_attn_fwd_host pipelines batch chunks (H2D / kernel / D2H on three streams); the result
+    (O and LSE) must equal the device entry's bit for bit."""
+    ins, gk, _ = cases.build(case)
+    dev, dlse = cases.run_gpu(fl, ins, gk, return_lse=True)
+    runner = fl.HostRunner()
+    out = torch.empty(dev.shape, dtype=dev.dtype).pin_memory()
+    lse = torch.empty(dlse.shape, dtype=torch.float32).pin_memory()
+    hk = {k: (v.pin_memory() if torch.is_tensor(v) else v) for k, v in gk.items()}
+    runner(ins["q"].pin_memory(), ins["k"].pin_memory(), ins["v"].pin_memory(), out, lse, **hk)
+    torch.cuda.synchronize()
+    assert torch.equal(out, dev.cpu())
+    assert torch.equal(lse, dlse.cpu())
+
+
 def test_errors_are_loud(fl):
     q = torch.zeros(1, 1, 8, 48, device="cuda", dtype=torch.bfloat16)
     with pytest.raises(fl.FlError, match="UNSUPPORTED"):
