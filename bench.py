@@ -341,6 +341,7 @@ class Job:
         self.oracle = None        # fn(budget_s) -> (tflops, threads, sample, secs)
         self.extra = {}
         self.parity = {}          # host inputs / outputs / oracle kwargs for the full-size parity tests
+        self.parity_result = {}   # per variant: GPU output vs the oracle on the cpu_baseline leg's rows
         self.units = ""           # this rank's shard, for the JSON line
         self.outputs = []         # (block, device output) of this rank's shard
 
@@ -442,8 +443,18 @@ def dense_job(names, rank, world, device, with_host=True):
             nr = int(min(total_rows, max(64, 64 * per_budget / max(dt, 1e-3))))
             rows = np.linspace(0, total_rows - 1, nr).astype(np.int64)
             t0 = time.perf_counter()
-            oracle.attn(host0["q"], host0["k"], host0["v"], rows=rows, **ok)
+            ref, _ = oracle.attn(host0["q"], host0["k"], host0["v"], rows=rows, **ok)
             dt = time.perf_counter() - t0
+            if (rank == 0 and torch.device(device).type == "cuda" and not cfg.get("bwd")
+                    and out0.numel() // out0.shape[-1] == total_rows):
+                # the same rows of this variant's GPU output at full size, re-run once outside the timing
+                next(c for c in job.calls if c.label == n).fn()
+                torch.cuda.synchronize()
+                D = out0.shape[-1]
+                got = out0.reshape(-1, D)[torch.as_tensor(rows, device=out0.device)].double().cpu().numpy()
+                err, tol = float(np.abs(got - ref).max()), 1e-5 if cfg.get("dtype") == "f32" else 2e-2
+                job.parity_result[n] = {"rows": int(nr), "max_abs": err, "max_ref": float(np.abs(ref).max()),
+                                        "tol": tol, "ok": err <= tol}
             tot_flops += bpairs * flops_per_pair(cfg) * (nr / total_rows)
             tot_s += dt
             n_rows += nr
@@ -500,8 +511,15 @@ def evo_job(name, rank, world, device, with_host=True):
         nr = int(min(total_rows, max(256, 256 * budget_s / max(dt, 1e-3))))
         rows = np.linspace(0, total_rows - 1, nr).astype(np.int64)
         t0 = time.perf_counter()
-        oracle.attn(hq, hk, hv, rows=rows, **okw)
+        ref, _ = oracle.attn(hq, hk, hv, rows=rows, **okw)
         dt = time.perf_counter() - t0
+        if rank == 0 and torch.device(device).type == "cuda":
+            job.calls[0].fn()
+            torch.cuda.synchronize()
+            got = out.reshape(-1, out.shape[-1])[torch.as_tensor(rows, device=out.device)].double().cpu().numpy()
+            err = float(np.abs(got - ref).max())
+            job.parity_result[name] = {"rows": int(nr), "max_abs": err, "max_ref": float(np.abs(ref).max()),
+                                       "tol": 2e-2, "ok": err <= 2e-2}
         return (flops * nr / total_rows / dt / 1e12, oracle.num_threads(),
                 f"{nr} of {total_rows} output rows (evenly spaced), useful flops scaled by row share", dt)
     job.oracle = oracle_fn
@@ -1023,6 +1041,9 @@ def main():
     if not args.no_cpu_baseline and job.oracle is not None:
         v_cpu, cores, sample, _ = job.oracle(15.0)
         line["cpu_baseline"] = {"value": v_cpu, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample}
+        if job.parity_result:
+            line["parity"] = {"vs": "fp64 oracle on the cpu_baseline rows (block 0 of the step, full size)",
+                              "variants": job.parity_result}
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.barrier()

@@ -640,8 +640,9 @@ fl_status fl_attn_fwd_host(const fl_attn_args* host_args, void* scratch, size_t 
       cudaStreamCreateWithFlags(&s_in[dev], cudaStreamNonBlocking);
       cudaStreamCreateWithFlags(&s_out[dev], cudaStreamNonBlocking);
     });
-    const int nch = (int)std::min<int64_t>(B, 4);
-    cudaEvent_t ev[2 * 4 + 2];
+    constexpr int kMaxChunks = 8;                    // finer chunks shorten the pipeline's fill and drain
+    const int nch = (int)std::min<int64_t>(B, kMaxChunks);
+    cudaEvent_t ev[2 * kMaxChunks + 2];
     for (auto& e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     cudaEventRecord(ev[0], stream);                  // the streams start after the caller's prior work
     cudaStreamWaitEvent(s_in[dev], ev[0], 0);
