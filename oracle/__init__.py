@@ -84,7 +84,7 @@ def lib():
         _lib.flo_keep_row.restype = C.c_int
         _lib.flo_attn_bwd.argtypes = [C.POINTER(_Problem), C.POINTER(_Tensor), C.POINTER(C.c_double),
                                       C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double),
-                                      C.POINTER(C.c_double)]
+                                      C.POINTER(C.c_double), C.POINTER(C.c_double)]
         _lib.flo_attn_bwd.restype = C.c_int
         dp = C.POINTER(C.c_double)
         _lib.flo_linear_ln.argtypes = [C.c_int64, C.c_int64, C.c_int64, dp, dp, dp, dp, dp, C.c_double, dp, dp]
@@ -179,10 +179,11 @@ def attn(q, k, v, *, scale=0.0, mod="none", softcap=0.0, alibi_slopes=None,
     return out, lse
 
 
-def attn_bwd(q, k, v, dout, with_dgate=False, with_dbias=False, **variant):
+def attn_bwd(q, k, v, dout, with_dgate=False, with_dbias=False, with_dlambda=False, **variant):
     """Gradients (dq, dk, dv) of L = sum(O * dout), fp64 numpy arrays shaped like q, k, v (NEXT-3); with
     with_dgate also dL/dgate (shaped like dout) for a gated variant, with with_dbias also dL/dbias as the
-    full logical [B, G, Hq, Sq, Sk] array (sum it over the dims the bias broadcasts)."""
+    full logical [B, G, Hq, Sq, Sk] array (sum it over the dims the bias broadcasts), with with_dlambda (diff)
+    also dL/dlambda_h [Hq] (sum it over h for a scalar lambda)."""
     keep: list = []
     p = _problem(q, k, v, keep, **variant)
     dt = _tensor(dout, keep)
@@ -195,11 +196,12 @@ def attn_bwd(q, k, v, dout, with_dgate=False, with_dbias=False, **variant):
     B, G, Hq, Sq = qs[0], qs[1], qs[2] // maps, qs[3]
     Sk = tuple(k.shape)[-2]
     db = np.zeros((B, G, Hq, Sq, Sk), dtype=np.float64) if with_dbias else None
+    dl = np.zeros(Hq, dtype=np.float64) if with_dlambda else None
     dpp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double)) if a is not None else None
-    rc = lib().flo_attn_bwd(C.byref(p), C.byref(dt), dpp(dq), dpp(dk), dpp(dv), dpp(dg), dpp(db))
+    rc = lib().flo_attn_bwd(C.byref(p), C.byref(dt), dpp(dq), dpp(dk), dpp(dv), dpp(dg), dpp(db), dpp(dl))
     if rc != 0:
         raise ValueError(f"flo_attn_bwd rejected the problem (code {rc})")
-    out = (dq, dk, dv) + ((dg,) if with_dgate else ()) + ((db,) if with_dbias else ())
+    out = (dq, dk, dv) + ((dg,) if with_dgate else ()) + ((db,) if with_dbias else ()) + ((dl,) if with_dlambda else ())
     return out
 
 

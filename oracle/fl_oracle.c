@@ -255,8 +255,11 @@ int flo_keep_row(const flo_problem* p, int64_t b, int64_t g, int64_t h, int64_t 
 /* dbias (optional, may be NULL): dL/dbias for the additive score bias of Eq.4 / G16 (s = scale q.k + bias
  * before the softcap), logical [B, G, Hq, Sq, Sk] contiguous: the score gradient dx of each kept (q, k) --
  * the caller sums it over the dims its bias broadcasts (e.g. the MSA rows s of the Evoformer pair bias). */
+/* dlambda (optional, may be NULL; diff only): dL/dlambda_h [Hq] of Listing 4's O = A_0 - lambda_h A_1 (P:L412-424,
+ * G8): -sum over (b, g, q, d) of dO * gate' * A_1 -- with lambda_qk the lambda the re-parameterisation yields
+ * (the caller chains into lambda_qk), with a scalar lambda the caller sums it over h. */
 int flo_attn_bwd(const flo_problem* p, const flo_tensor* dout, double* dq, double* dk, double* dv, double* dgate,
-                 double* dbias) {
+                 double* dbias, double* dlambda) {
   int64_t maps;
   int rc = check_problem(p, &maps);
   if (rc) return rc;
@@ -273,6 +276,8 @@ int flo_attn_bwd(const flo_problem* p, const flo_tensor* dout, double* dq, doubl
     for (int64_t i = 0; i < B * G * Hq * Sq * Dv; ++i) dgate[i] = 0.0;
   if (dbias)
     for (int64_t i = 0; i < B * G * Hq * Sq * Sk; ++i) dbias[i] = 0.0;
+  if (dlambda)
+    for (int64_t i = 0; i < Hq; ++i) dlambda[i] = 0.0;
   /* one task per (b, g, kv head): every write of the task stays inside it */
 #pragma omp parallel
   {
@@ -327,7 +332,7 @@ int flo_attn_bwd(const flo_problem* p, const flo_tensor* dout, double* dq, doubl
             }
             /* dA = dO * gate' * (1 or -lambda) */
             double coef = map == 0 ? 1.0 : -lam;
-            double dot_da_a = 0.0;
+            double dot_da_a = 0.0, dlam = 0.0;
             for (int64_t d = 0; d < Dv; ++d) {
               double gv = 1.0;
               if (p->gate_mode != FLO_GATE_NONE) {
@@ -336,12 +341,17 @@ int flo_attn_bwd(const flo_problem* p, const flo_tensor* dout, double* dq, doubl
               }
               da[d] = coef * gv * elem(dout, off5(dout, b, g, h, q, d));
               dot_da_a += da[d] * a[d];
+              if (map == 1) dlam -= gv * elem(dout, off5(dout, b, g, h, q, d)) * a[d];    /* dO/dlambda = -gate' A_1 */
               if (dgate && p->gate_mode != FLO_GATE_NONE) {
                 const double gl = elem(&p->gate, off5(&p->gate, b, g, h, q, d));
                 const double dgl = p->gate_mode == FLO_GATE_SIGMOID ? gv * (1.0 - gv) : 1.0;   /* gate'(g) */
                 (void)gl;
                 dgate[(((b * G + g) * Hq + h) * Sq + q) * Dv + d] += coef * a[d] * dgl * elem(dout, off5(dout, b, g, h, q, d));
               }
+            }
+            if (dlambda && map == 1) {
+#pragma omp atomic
+              dlambda[h] += dlam;                       /* heads of one group meet across the b, g tasks */
             }
             for (int64_t k = 0; k < Sk; ++k) {
               if (pr[k] == 0.0 && sc[k] == -INFINITY) continue;

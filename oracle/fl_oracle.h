@@ -103,9 +103,10 @@ int flo_rsa_select(const flo_tensor* q, const flo_tensor* k, int32_t blk_q, int3
 
 /* Backward: dQ, dK, dV (fp64, logical shapes of q, k, v, row-major) of
  * L = sum O * dO for the problem's forward, by the plain chain rule through the definition (see the
- * comment at the definition).  dout: logical [B,G,Hq,Sq,Dv].  -11 when diff_norm is set (not derived). */
+ * comment at the definition).  dout: logical [B,G,Hq,Sq,Dv].  -11 when diff_norm is set (not derived).
+ * dgate / dbias / dlambda: optional (NULL), see the definition's comment. */
 int flo_attn_bwd(const flo_problem* p, const flo_tensor* dout, double* dq, double* dk, double* dv, double* dgate,
-                 double* dbias);
+                 double* dbias, double* dlambda);
 
 int flo_num_threads(void);
 

@@ -632,6 +632,32 @@ def test_backward_matches_central_differences(kw):
         np.testing.assert_allclose(grad, num, rtol=1e-6, atol=1e-8)
 
 
+@pytest.mark.parametrize("gated", [False, True])
+def test_backward_dlambda_matches_central_differences(gated):
+    """dL/dlambda_h of Listing 4 (G8) against central differences of the oracle forward in the
+    per-head lambda_h and in the scalar lambda (whose gradient is the sum over heads), with and without the
+    sigmoid gate, causal, GQA 2:1."""
+    H, Hkv, S, D = 2, 1, 6, 4
+    q, k, v, do = rnd(1, 2 * H, S, D, seed=80), rnd(1, 2 * Hkv, S, D, seed=81), rnd(1, Hkv, S, D, seed=82), rnd(1, H, S, D, seed=83)
+    kw = dict(diff=True, mask="causal")
+    if gated:
+        kw.update(gate_mode="sigmoid", gate=rnd(1, H, S, D, seed=84, lo=-2, hi=2))
+    lh = np.array([0.3, -0.45])
+    dl = oracle.attn_bwd(q, k, v, do, with_dgate=gated, with_dlambda=True, lambda_h=torch.tensor(lh), **kw)[-1]
+    L = lambda **x: float((oracle.attn(q, k, v, **kw, **x)[0].reshape(do.shape) * do.numpy()).sum())
+    h = 1e-6
+    for i in range(H):
+        lp, lm = lh.copy(), lh.copy()
+        lp[i] += h
+        lm[i] -= h
+        num = (L(lambda_h=torch.tensor(lp)) - L(lambda_h=torch.tensor(lm))) / (2 * h)
+        assert abs(dl[i] - num) <= 1e-6 * max(1.0, abs(num)), (i, dl[i], num)
+    dl_s = oracle.attn_bwd(q, k, v, do, with_dgate=gated, with_dlambda=True, lam=0.25, **kw)[-1]
+    num = (L(lam=0.25 + h) - L(lam=0.25 - h)) / (2 * h)
+    assert abs(dl_s.sum() - num) <= 1e-6 * max(1.0, abs(num))
+    assert np.all(dl_s != 0.0)
+
+
 def test_backward_matches_torch_autograd_listing1():
     """Listing 1 executed eagerly in fp64 under torch.autograd, causal and GQA via repeats."""
     q, k, v, do = rnd(2, 4, 33, 8, seed=95), rnd(2, 2, 33, 8, seed=96), rnd(2, 2, 33, 8, seed=97), rnd(2, 4, 33, 8, seed=98)
