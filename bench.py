@@ -57,6 +57,7 @@ VARIANTS = {
     "c1": dict(B=1, H=1, S=128, D=64, mask="causal", dtype="f32"),
     # configs[2]: differential attention bf16 B=8 H=16 S=8192 D=64 (two maps, lambda)
     "diff": dict(B=8, H=16, S=8192, D=64, diff=True, lam=0.2),
+    "bwd_diff": dict(B=8, H=16, S=8192, D=64, diff=True, lam=0.2, bwd=True),   # NEXT-3 for configs[2]
     # configs[3]: Evoformer gated self-attention with pair bias, N_seq=512 N_res=384 H=8 c=32
     "evo_row": dict(evo="row", B=1, Ns=512, Nr=384, H=8, D=32),
     "evo_col": dict(evo="col", B=1, Ns=512, Nr=384, H=8, D=32),
@@ -390,10 +391,14 @@ def dense_job(names, rank, world, device, with_host=True):
             for (blk, host, q, k, v, out), f in zip(blocks, fns):
                 kw_b, _ = block_variant_kw(cfg, blk)
                 dkw = _dev_kw(kw_b, device)
-                o_b, lse_b = fl.attn_fwd(q, k, v, return_lse=True, **dkw)
+                if cfg.get("diff"):     # the diff backward recomputes both maps' outputs and LSEs itself
+                    o_b, lse_b = fl.attn_fwd(q, k, v, **dkw), None
+                else:
+                    o_b, lse_b = fl.attn_fwd(q, k, v, return_lse=True, **dkw)
                 do_b = torch.empty_like(o_b).uniform_(-1, 1)
                 g = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v))
-                wsb = torch.empty(4 * o_b.numel() // o_b.shape[-1] + 256, dtype=torch.uint8, device=device)
+                wsb = torch.empty(fl.attn_bwd_workspace_bytes(q, k, v, o_b, lse_b, do_b, **dkw), dtype=torch.uint8,
+                                  device=device)
                 bfns.append(lambda q=q, k=k, v=v, o_b=o_b, lse_b=lse_b, do_b=do_b, g=g, dkw=dkw, wsb=wsb:
                             fl.attn_bwd(q, k, v, o_b, lse_b, do_b, dq=g[0], dk=g[1], dv=g[2], workspace=wsb, **dkw))
             flops *= 2.5
@@ -765,7 +770,7 @@ def oracle_only_job(variant):
 
 
 EXTRA_CONFIGS = ["c1", "diff", "evo_row", "evo_col", "rsa", "rsa_decode"]   # BASELINE configs[0, 2, 3, 4]
-NEXT_EXTRAS = ["bwd_causal", "evo_block", "ipa"]     # SURVEY §8(f) rows, single-GPU runs only
+NEXT_EXTRAS = ["bwd_causal", "bwd_diff", "evo_block", "ipa"]     # SURVEY §8(f) rows, single-GPU runs only
 
 
 def time_job(job, steps, warmup, device, stream, use_graph=True, flush=None, clk=None):

@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define FL_ABI_VERSION 3
+#define FL_ABI_VERSION 4
 
 typedef enum {
   FL_OK = 0,
@@ -157,9 +157,14 @@ fl_status fl_attn_fwd(const fl_attn_args* args);
  * (a KV-tile-major dK/dV pass and a query-tile-major dQ pass, two compute warpgroups each, no atomics).
  * Supported (v3): bf16, rank-4 or rank-5 q/k/v (G), D_qk == D_v in {32, 64, 128}, GQA, masks none /
  * causal / sliding / prefix / document (either alignment), mods none / ALiBi / softcap, key_mask (MSA
- * mask), sigmoid gate (+ dgate), additive bias (+ dbias).  Not yet: diff, mul gate, block lists, paged KV, fp32
- * (FL_ERR_UNSUPPORTED).  Workspace (fl_attn_bwd_workspace_size): 4 B G Hq S_q bytes (Dvec) + the packed
- * key mask + 2 B G Hq S_q D_v bytes with a sigmoid gate, each 256-byte rounded. */
+ * mask), sigmoid gate (+ dgate), additive bias (+ dbias), differential attention (v4, Listing 4 P:L412-424,
+ * G8: lambda, lambda_h or lambda_qk; + dlambda).  Not yet: the diff_norm epilogue, dbias with diff, mul gate,
+ * block lists, paged KV, fp32 (FL_ERR_UNSUPPORTED).  Workspace (fl_attn_bwd_workspace_size): 4 B G Hq S_q
+ * bytes (Dvec) + the packed key mask + 2 B G Hq S_q D_v bytes with a sigmoid gate, each 256-byte rounded.
+ * Diff: the forward keeps neither map's output, so the call recomputes both maps (o_i, lse_i: the forward
+ * kernel per map), seeds map 1 with -lambda_h dO, runs the single-map backward per map and sums dV (and
+ * dgate) over the maps; lse must be absent, o (the diff output) is validated but not read, and the workspace
+ * holds o_0, o_1, lse_0, lse_1, dO_1, dV_1 (+ dgate_1) plus one forward and one backward workspace. */
 typedef struct {
   fl_tensor q, k, v, o;      /* the forward's inputs and output (bf16) */
   fl_tensor lse;             /* the forward's LSE, f32 [B, Hq, S_q] (required) */
@@ -173,6 +178,8 @@ typedef struct {
   fl_tensor dbias;           /* optional (with a bias): dL/dbias, f32, the bias's shape; dims the bias broadcasts
                                 (stride 0 or size 1) are summed over; must be compact -- the call zeroes it and
                                 accumulates with fp32 atomics (ABI v3) */
+  fl_tensor dlambda;         /* optional (diff): dL/dlambda_h, f32 [Hq] (sum it over h for a scalar lambda; with
+                                lambda_qk, the gradient of the lambda it yields); zeroed and accumulated (ABI v4) */
 } fl_attn_bwd_args;
 
 fl_status fl_attn_bwd(const fl_attn_bwd_args* args);
@@ -193,7 +200,7 @@ fl_status fl_attn_workspace_size(const fl_attn_args* args, size_t* bytes);
  * H2D copies, the kernel and the D2H copy of o (and lse) on `stream`, and
  * returns without synchronising.  Host tensors must be contiguous.  With B >= 2
  * and only q / k / v / doc_offsets batched (no bias, key mask, gate, block lists,
- * paged KV), the batch is split into up to 4 chunks whose H2D (an internal copy-in
+ * paged KV), the batch is split into up to 8 chunks whose H2D (an internal copy-in
  * stream), kernel (`stream`) and D2H (an internal copy-out stream) overlap; events
  * order them after `stream`'s prior work and `stream` waits for the last D2H. */
 fl_status fl_attn_host_scratch_size(const fl_attn_args* args, size_t* bytes);
@@ -324,6 +331,7 @@ const char* fl_last_error(void);   /* thread-local detail of the last non-OK sta
 int32_t fl_abi_version(void);
 /* sizeof(fl_attn_args) of this build: bindings compare it with their own mirror at load time. */
 size_t fl_attn_args_size(void);
+size_t fl_attn_bwd_args_size(void);      /* sizeof(fl_attn_bwd_args), for the same check (ABI v4) */
 /* Number of kernel launches enqueued by the calling thread since the last reset. */
 int64_t fl_launch_count(int32_t reset);
 

@@ -12,11 +12,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(HERE, "libfl_attn.so")
 
 FL_BF16, FL_F32, FL_U8, FL_I32 = 0, 1, 2, 3
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 EXPORTS = ["fl_attn_fwd", "fl_attn_workspace_size", "fl_attn_host_scratch_size", "fl_attn_fwd_host",
            "fl_rsa_build_summaries", "fl_rsa_update_summaries", "fl_rsa_select", "fl_shard_range", "fl_diag_umma_gemm",
-           "fl_diag_pipe_rate", "fl_debug_schedule", "fl_attn_args_size", "fl_attn_bwd",
+           "fl_diag_pipe_rate", "fl_debug_schedule", "fl_attn_args_size", "fl_attn_bwd_args_size", "fl_attn_bwd",
            "fl_attn_bwd_workspace_size", "fl_status_string", "fl_last_error", "fl_abi_version", "fl_launch_count", "fl_debug_timing",
            "fl_linear", "fl_ipa_fwd", "fl_ipa_workspace_size"]
 
@@ -50,7 +50,7 @@ class BwdArgs(C.Structure):
     _fields_ = [("q", Tensor), ("k", Tensor), ("v", Tensor), ("o", Tensor), ("lse", Tensor), ("dout", Tensor),
                 ("dq", Tensor), ("dk", Tensor), ("dv", Tensor), ("var", Variant), ("stream", C.c_void_p),
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t), ("dgate", Tensor),
-                ("dbias", Tensor)]
+                ("dbias", Tensor), ("dlambda", Tensor)]
 
 
 class LinearArgs(C.Structure):
@@ -130,6 +130,10 @@ def lib():
         if L.fl_attn_args_size() != C.sizeof(AttnArgs):
             raise RuntimeError(f"libfl_attn.so was built for a different fl_attn_args layout "
                                f"({L.fl_attn_args_size()} vs {C.sizeof(AttnArgs)} bytes): rebuild it")
+        L.fl_attn_bwd_args_size.restype = C.c_size_t
+        if L.fl_attn_bwd_args_size() != C.sizeof(BwdArgs):
+            raise RuntimeError(f"libfl_attn.so was built for a different fl_attn_bwd_args layout "
+                               f"({L.fl_attn_bwd_args_size()} vs {C.sizeof(BwdArgs)} bytes): rebuild it")
         _lib = L
     return _lib
 

@@ -96,11 +96,78 @@ __global__ void __launch_bounds__(256) bwd_gate_kernel(const AttnParams p, const
       pg[t] = pack_bf16(d0 * o0 * (1.f - s0), d1 * o1 * (1.f - s1));
     }
     *reinterpret_cast<uint4*>(dar + c) = make_uint4(pa[0], pa[1], pa[2], pa[3]);
-    if (dgr) *reinterpret_cast<uint4*>(dgr + c) = make_uint4(pg[0], pg[1], pg[2], pg[3]);
+    if (dgr && p.grad_accum) {                        // second diff map: add to the first map's dgate
+      const uint4 u = *reinterpret_cast<const uint4*>(dgr + c);
+      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float o0 = bf16_lo(wo[t]), o1 = bf16_hi(wo[t]), d0 = bf16_lo(wd[t]), d1 = bf16_hi(wd[t]);
+        const float s0 = 1.f / (1.f + __expf(-bf16_lo(wg[t]))), s1 = 1.f / (1.f + __expf(-bf16_hi(wg[t])));
+        pg[t] = pack_bf16(fmaf(d0 * o0, 1.f - s0, bf16_lo(w[t])), fmaf(d1 * o1, 1.f - s1, bf16_hi(w[t])));
+      }
+      *reinterpret_cast<uint4*>(dgr + c) = make_uint4(pg[0], pg[1], pg[2], pg[3]);
+    } else if (dgr) {
+      *reinterpret_cast<uint4*>(dgr + c) = make_uint4(pg[0], pg[1], pg[2], pg[3]);
+    }
   }
 #pragma unroll
   for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
   if (lane == 0) dvec[row] = acc;
+}
+
+// Differential attention (Listing 4; reading G8), O = A_0 - lambda_h A_1: the backward runs the
+// single-map kernels once per map (host.cu) with the map-1 seed dO_1 = -lambda_h dO; this kernel writes that
+// seed (contiguous, [rows, Dv]) and dL/dlambda_h = -sum_{b,g,q,d} dO * o_1, o_1 the recomputed map-1 output
+// (gated when the forward is: o_1 = gate' A_1).  One warp per row; the block's 8 rows share one head when
+// they lie in one (b, g, h) (S_q % 8 == 0), then one atomic per block.
+__global__ void __launch_bounds__(256) diff_bwd_seed_kernel(const AttnParams p, const __nv_bfloat16* __restrict__ dout,
+                                                           Strided5 dos, const __nv_bfloat16* __restrict__ o1,
+                                                           __nv_bfloat16* __restrict__ do1, float* __restrict__ dlambda) {
+  __shared__ float part[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 8 + warp;
+  const int64_t n_rows = (int64_t)p.B * p.G * p.Hq * p.Sq;
+  float acc = 0.f;
+  int h = 0;
+  if (row < n_rows) {
+    const int q = (int)(row % p.Sq);
+    const int64_t bgh = row / p.Sq;
+    h = (int)(bgh % p.Hq);
+    const int g = (int)((bgh / p.Hq) % p.G), b = (int)(bgh / ((int64_t)p.Hq * p.G));
+    const float c = -diff_lambda(p, h);
+    const __nv_bfloat16* d = dout + b * dos.b + g * dos.g + h * dos.h + q * dos.s;
+    const __nv_bfloat16* o = o1 + row * p.Dv;
+    __nv_bfloat16* out = do1 + row * p.Dv;
+    for (int col = lane * 8; col < p.Dv; col += 256) {
+      const uint4 ud = *reinterpret_cast<const uint4*>(d + col), uo = *reinterpret_cast<const uint4*>(o + col);
+      const uint32_t wd[4] = {ud.x, ud.y, ud.z, ud.w}, wo[4] = {uo.x, uo.y, uo.z, uo.w};
+      uint32_t pd[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float d0 = bf16_lo(wd[t]), d1 = bf16_hi(wd[t]);
+        acc = fmaf(d0, bf16_lo(wo[t]), fmaf(d1, bf16_hi(wo[t]), acc));
+        pd[t] = pack_bf16(c * d0, c * d1);
+      }
+      *reinterpret_cast<uint4*>(out + col) = make_uint4(pd[0], pd[1], pd[2], pd[3]);
+    }
+  }
+  if (!dlambda) return;
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+  const int64_t r0 = (int64_t)blockIdx.x * 8, r1 = r0 + 7;
+  const bool one_head = r1 < n_rows && r0 / p.Sq == r1 / p.Sq;
+  if (!one_head) {
+    if (lane == 0 && row < n_rows) atomicAdd(dlambda + h, -acc);
+    return;
+  }
+  if (lane == 0) part[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += part[w];
+    atomicAdd(dlambda + h, -t);
+  }
 }
 
 // ---------------------------------------------------------------- shared configuration
@@ -451,7 +518,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
           const float sc = which ? p.scale : 1.f;
           uint4* op = reinterpret_cast<uint4*>((which ? dkp : dvp) + c);
-          if (k_ok)
+          if (k_ok && !which && p.grad_accum) {        // dV of the second diff map: add to the first map's
+#pragma unroll
+            for (int t8 = 0; t8 < 4; ++t8) {
+              const uint4 u = op[t8];
+              const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+              uint32_t r[4];
+#pragma unroll
+              for (int t = 0; t < 4; ++t)
+                r[t] = pack_bf16(__uint_as_float(o[t8 * 8 + 2 * t]) + bf16_lo(w[t]),
+                                 __uint_as_float(o[t8 * 8 + 2 * t + 1]) + bf16_hi(w[t]));
+              op[t8] = make_uint4(r[0], r[1], r[2], r[3]);
+            }
+          } else if (k_ok)
 #pragma unroll
           for (int t8 = 0; t8 < 4; ++t8)
             op[t8] = make_uint4(pack_bf16(__uint_as_float(o[t8 * 8 + 0]) * sc, __uint_as_float(o[t8 * 8 + 1]) * sc),
@@ -752,6 +831,15 @@ cudaError_t launch_bwd_prepass(const AttnParams& p, const void* dout, Strided5 d
                                                                 static_cast<__nv_bfloat16*>(dgate), dgs, dvec);
   else
     bwd_dvec_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(p, static_cast<const __nv_bfloat16*>(dout), dos, dvec);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_diff_bwd_seed(const AttnParams& p, const void* dout, Strided5 dos, const void* o1, void* do1,
+                                 float* dlambda, cudaStream_t s) {
+  const int64_t rows = (int64_t)p.B * p.G * p.Hq * p.Sq;
+  diff_bwd_seed_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(
+      p, static_cast<const __nv_bfloat16*>(dout), dos, static_cast<const __nv_bfloat16*>(o1),
+      static_cast<__nv_bfloat16*>(do1), dlambda);
   return cudaGetLastError();
 }
 

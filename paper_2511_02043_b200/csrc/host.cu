@@ -46,6 +46,8 @@ cudaError_t launch_sched_dump(const AttnParams& p, int32_t* out, int64_t out_wor
                               int32_t* max_tiles, cudaStream_t stream);
 cudaError_t launch_bwd_prepass(const AttnParams& p, const void* dout, Strided5 dos, float* dvec, void* da, void* dgate,
                                Strided5 dgs, cudaStream_t s);
+cudaError_t launch_diff_bwd_seed(const AttnParams& p, const void* dout, Strided5 dos, const void* o1, void* do1,
+                                 float* dlambda, cudaStream_t s);
 cudaError_t launch_attn_bwd(const AttnParams& p, const TmaMaps& maps, const CUtensorMap& tdo, const CUtensorMap& tq64,
                             const CUtensorMap& tdo64, const float* lse,
                             Strided5 ls, const void* dout, Strided5 dos, float* dvec, void* dq, Strided5 dqs, void* dk,
@@ -782,7 +784,7 @@ fl_status prepare_bwd(const fl_attn_bwd_args* a, BwdPrepared& B, bool device_ptr
   if (!B.P.bf16) return fail(FL_ERR_UNSUPPORTED, "backward: bf16 q/k/v/o");
   if (p.Dqk != 32 && p.Dqk != 64 && p.Dqk != 128) return fail(FL_ERR_UNSUPPORTED, "backward: D in {32, 64, 128}");
   if (var.diff || var.kv_page_table.data || var.mask == FL_MASK_BLOCKLIST || var.gate_mode == FL_GATE_MUL)
-    return fail(FL_ERR_UNSUPPORTED, "backward: no diff / block list / paged KV / mul gate");
+    return fail(FL_ERR_UNSUPPORTED, "backward: no block list / paged KV / mul gate");
   if (!a->lse.data) return fail(FL_ERR_INVALID_ARGUMENT, "backward needs the forward's lse");
   const int R = B.P.q_rank;
   const fl_tensor* ts[4] = {&a->dout, &a->dq, &a->dk, &a->dv};
@@ -847,8 +849,163 @@ fl_status prepare_bwd(const fl_attn_bwd_args* a, BwdPrepared& B, bool device_ptr
 }
 }  // namespace
 
+namespace {
+fl_status bwd_single(const fl_attn_bwd_args* args, bool grad_accum = false);
+
+// ---- differential attention backward (Listing 4; reading G8): O = gate'(A_0 - lambda_h A_1) is
+// linear in the two maps, so the backward is the single-map backward of each map -- map 0 seeded with dO,
+// map 1 with dO_1 = -lambda_h dO -- on the maps' own outputs and LSEs, recomputed by the forward kernel
+// (the diff forward keeps neither), with dV (and dgate) summed over the maps:
+//   1. fwd(q_i, k_i, v) -> o_i, lse_i            (i = 0, 1; map i = heads [iH, (i+1)H) of q and k)
+//   2. dO_1 = -lambda_h dO;  dlambda_h = -sum dO * o_1                 (diff_bwd_seed_kernel)
+//   3. bwd(map 0, dO) -> dq[:, :H], dk[:, :Hkv], dv, dgate
+//   4. bwd(map 1, dO_1) -> dq[:, H:], dk[:, Hkv:]; dv += (fp32 add in the dK/dV epilogue), dgate += (pre-pass)
+fl_tensor head_slice(fl_tensor t, int64_t h0, int64_t nh) {
+  const int hd = t.rank - 3;
+  t.data = static_cast<char*>(t.data) + h0 * t.stride[hd] * elem_bytes(t.dtype);
+  t.size[hd] = nh;
+  return t;
+}
+
+fl_tensor dense_like(const fl_tensor& like, void* data, int dtype, int rank) {
+  fl_tensor t;
+  memset(&t, 0, sizeof t);
+  t.data = data; t.dtype = dtype; t.rank = rank;
+  int64_t st = 1;
+  for (int d = rank - 1; d >= 0; --d) {
+    t.size[d] = like.size[d];
+    t.stride[d] = st;
+    st *= like.size[d];
+  }
+  return t;
+}
+
+size_t up256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct DiffBwdPlan {
+  fl_attn_args fwd[2];
+  fl_attn_bwd_args bwd[2];
+  AttnParams seed;                  // shape and lambda for the seed kernel
+  char* base = nullptr;
+  size_t off_do1 = 0, ws = 0;
+  bool empty = false;
+};
+
+fl_status plan_diff_bwd(const fl_attn_bwd_args* a, DiffBwdPlan& D, bool device_ptrs) {
+  const fl_variant& var = a->var;
+  if (var.diff_norm) return fail(FL_ERR_UNSUPPORTED, "backward: diff_norm (the G8b RMSNorm epilogue) is not differentiated");
+  if (a->dbias.data) return fail(FL_ERR_UNSUPPORTED, "backward: dbias with diff");
+  if (var.kv_page_table.data || var.mask == FL_MASK_BLOCKLIST || var.gate_mode == FL_GATE_MUL)
+    return fail(FL_ERR_UNSUPPORTED, "backward: no block list / paged KV / mul gate");
+  if (a->lse.data) return fail(FL_ERR_INVALID_ARGUMENT, "diff backward: lse must be absent (the maps' LSEs are recomputed)");
+  fl_attn_args f;
+  memset(&f, 0, sizeof f);
+  f.q = a->q; f.k = a->k; f.v = a->v; f.o = a->o; f.var = var; f.stream = a->stream;
+  Prepared P;
+  fl_status s = prepare(&f, P, device_ptrs);        // validates the diff problem (lambda_h, lambda_qk, ...)
+  if (s != FL_OK) return s;
+  if (!P.bf16) return fail(FL_ERR_UNSUPPORTED, "backward: bf16 q/k/v/o");
+  const AttnParams& p = P.p;
+  D.seed = p;
+  D.empty = P.empty_work;
+  const int64_t Hq = p.Hq, Hkv = p.Hkv;
+  const int64_t rows = (int64_t)p.B * p.G * Hq * p.Sq;
+  if (p.Dv % 8) return fail(FL_ERR_UNSUPPORTED, "diff backward: D_v %% 8 == 0");
+  if (a->dlambda.data) {
+    const fl_tensor& t = a->dlambda;
+    if (t.dtype != FL_F32 || t.rank != 1 || t.size[0] != Hq || (Hq > 1 && t.stride[0] != 1))
+      return fail(FL_ERR_SHAPE_MISMATCH, "dlambda: f32 [Hq], contiguous");
+    if (device_ptrs && !on_device(t.data)) return fail(FL_ERR_INVALID_ARGUMENT, "dlambda must be device memory");
+  }
+  // workspace: o_0 | o_1 | lse_0 | lse_1 | dO_1 | forward workspace | backward workspace
+  D.base = device_ptrs ? static_cast<char*>(a->workspace) : reinterpret_cast<char*>(uintptr_t(1) << 12);
+  if (!D.base) D.base = reinterpret_cast<char*>(uintptr_t(1) << 12);   // sizes only (checked before running)
+  const size_t so = up256((size_t)rows * p.Dv * 2), sl = up256((size_t)rows * 4);
+  size_t off = 0;
+  const size_t off_o[2] = {0, so}, off_l[2] = {2 * so, 2 * so + sl};
+  off = 2 * so + 2 * sl;
+  D.off_do1 = off; off += so;
+  fl_tensor lse_like = a->o;                          // [B,(G,)Hq,Sq]: o's sizes without the head dim
+  lse_like.rank = a->o.rank - 1;
+  for (int m = 0; m < 2; ++m) {
+    fl_attn_args& fm = D.fwd[m];
+    fm = f;
+    fm.var.diff = 0;
+    memset(&fm.var.lambda_h, 0, sizeof fm.var.lambda_h);
+    memset(&fm.var.lambda_qk, 0, sizeof fm.var.lambda_qk);
+    fm.q = head_slice(a->q, m * Hq, Hq);
+    fm.k = head_slice(a->k, m * Hkv, Hkv);
+    fm.o = dense_like(a->o, D.base + off_o[m], FL_BF16, a->o.rank);
+    fm.lse = dense_like(lse_like, D.base + off_l[m], FL_F32, lse_like.rank);
+  }
+  size_t fws = 0;
+  if ((s = fl_attn_workspace_size(&D.fwd[0], &fws)) != FL_OK) return s;
+  const size_t off_fws = off;
+  off += up256(fws);
+  size_t bws = 0;
+  for (int m = 0; m < 2; ++m) {
+    fl_attn_bwd_args& bm = D.bwd[m];
+    memset(&bm, 0, sizeof bm);
+    bm.q = D.fwd[m].q; bm.k = D.fwd[m].k; bm.v = a->v; bm.o = D.fwd[m].o; bm.lse = D.fwd[m].lse;
+    bm.var = D.fwd[m].var;
+    bm.stream = a->stream;
+    bm.dq = head_slice(a->dq, m * Hq, Hq);
+    bm.dk = head_slice(a->dk, m * Hkv, Hkv);
+    bm.dout = m == 0 ? a->dout : dense_like(a->dout, D.base + D.off_do1, FL_BF16, a->dout.rank);
+    bm.dv = a->dv;
+    bm.dgate = a->dgate;
+    BwdPrepared B;
+    if ((s = prepare_bwd(&bm, B, false)) != FL_OK) return s;
+    bws = std::max(bws, B.ws);
+  }
+  const size_t off_bws = off;
+  off += up256(bws);
+  for (int m = 0; m < 2; ++m) {
+    D.fwd[m].workspace = D.base + off_fws; D.fwd[m].workspace_bytes = fws;
+    D.bwd[m].workspace = D.base + off_bws; D.bwd[m].workspace_bytes = bws;
+  }
+  D.ws = off;
+  return FL_OK;
+}
+
+fl_status bwd_diff(const fl_attn_bwd_args* a) {
+  DiffBwdPlan D;
+  fl_status s = plan_diff_bwd(a, D, true);
+  if (s != FL_OK) return s;
+  if (!a->workspace || a->workspace_bytes < D.ws)
+    return fail(FL_ERR_WORKSPACE, "the diff backward needs %zu bytes of workspace", D.ws);
+  cudaStream_t stream = static_cast<cudaStream_t>(a->stream);
+  if (a->dlambda.data) {
+    cudaError_t e = cudaMemsetAsync(a->dlambda.data, 0, (size_t)D.seed.Hq * sizeof(float), stream);
+    if (e != cudaSuccess) return cuda_fail(e, "dlambda reset");
+  }
+  if (D.empty) return FL_OK;
+  for (int m = 0; m < 2; ++m) {                      // 1. the maps' outputs and LSEs
+    Prepared P;
+    if ((s = prepare(&D.fwd[m], P, true)) != FL_OK) return s;
+    if ((s = launch_prepared(P, &D.fwd[m])) != FL_OK) return s;
+  }
+  View5 dov;                                          // 2. map-1 seed and dlambda
+  to_view(a->dout, a->q.rank, 0, dov);
+  cudaError_t e = launch_diff_bwd_seed(D.seed, a->dout.data, strides_of(dov), D.fwd[1].o.data,
+                                       D.base + D.off_do1, static_cast<float*>(a->dlambda.data), stream);
+  ++g_launches;
+  if (e != cudaSuccess) return cuda_fail(e, "diff seed launch");
+  for (int m = 0; m < 2; ++m)                         // 3, 4. the single-map backward of each map; the maps
+    if ((s = bwd_single(&D.bwd[m], m == 1)) != FL_OK) return s;   // share V (and the gate): map 1 accumulates
+  return FL_OK;
+}
+}  // namespace
+
 fl_status fl_attn_bwd_workspace_size(const fl_attn_bwd_args* args, size_t* bytes) {
   if (!bytes) return fail(FL_ERR_INVALID_ARGUMENT, "bytes is NULL");
+  if (args && args->var.diff) {
+    DiffBwdPlan D;
+    fl_status s = plan_diff_bwd(args, D, false);
+    if (s != FL_OK) return s;
+    *bytes = D.ws;
+    return FL_OK;
+  }
   BwdPrepared B;
   fl_status s = prepare_bwd(args, B, false);
   if (s != FL_OK) return s;
@@ -857,9 +1014,17 @@ fl_status fl_attn_bwd_workspace_size(const fl_attn_bwd_args* args, size_t* bytes
 }
 
 fl_status fl_attn_bwd(const fl_attn_bwd_args* args) {
+  if (args && args->var.diff) return bwd_diff(args);
+  if (args && args->dlambda.data) return fail(FL_ERR_INVALID_ARGUMENT, "dlambda needs diff");
+  return bwd_single(args);
+}
+
+namespace {
+fl_status bwd_single(const fl_attn_bwd_args* args, bool grad_accum) {
   BwdPrepared B;
   fl_status s = prepare_bwd(args, B, true);
   if (s != FL_OK) return s;
+  B.P.p.grad_accum = grad_accum ? 1 : 0;
   if (B.P.empty_work) return FL_OK;
   if (!args->workspace || args->workspace_bytes < B.ws)
     return fail(FL_ERR_WORKSPACE, "the backward needs %zu bytes of workspace", B.ws);
@@ -913,6 +1078,7 @@ fl_status fl_attn_bwd(const fl_attn_bwd_args* args) {
   g_launches += 2;
   return e == cudaSuccess ? FL_OK : cuda_fail(e, "backward launch");
 }
+}  // namespace
 
 fl_status fl_linear(const fl_linear_args* a) {
   if (!a) return fail(FL_ERR_INVALID_ARGUMENT, "args is NULL");
@@ -1254,6 +1420,7 @@ const char* fl_status_string(fl_status s) {
 }
 
 size_t fl_attn_args_size(void) { return sizeof(fl_attn_args); }
+size_t fl_attn_bwd_args_size(void) { return sizeof(fl_attn_bwd_args); }
 
 fl_status fl_debug_timing(uint64_t* out48, int32_t reset) {
   if (!out48) return fail(FL_ERR_INVALID_ARGUMENT, "out48 is NULL");

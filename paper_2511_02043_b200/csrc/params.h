@@ -53,6 +53,9 @@ struct AttnParams {
   // bf16 small heads (attn_tc.cuh): 0 = (b, g, h)-major units claimed by tickets; 1 = pair bias resident in
   // TMEM (Evoformer rows): (b, h, q-block) segments with the G pairs minor, static contiguous chunks per CTA
   int32_t unit_order;
+  // backward only: add this call's dV and dgate to the values already in dv / dgate (the second map of a
+  // differential attention: the maps share V and the gate) instead of overwriting them
+  int32_t grad_accum;
 };
 
 // lambda of head h (Listing 4's lambda_full, G8): re-parameterised from lambda_qk when given (NEXT-2:

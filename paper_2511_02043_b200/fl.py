@@ -177,16 +177,7 @@ def _keep_alive_on(stream, tensors):
             t.record_stream(stream)
 
 
-def attn_bwd(q, k, v, out, lse, dout, *, dq=None, dk=None, dv=None, dgate=None, dbias=None, workspace=None, **variant):
-    """Backward of attn_fwd (fl_attn_bwd, NEXT-3): returns (dq, dk, dv) of L = sum(out * dout), given the
-    forward's output and natural-log LSE (attn_fwd(..., return_lse=True)); with a sigmoid gate also dgate
-    (dL/dgate-logits): (dq, dk, dv, dgate)."""
-    dq = torch.empty_like(q) if dq is None else dq
-    dk = torch.empty_like(k) if dk is None else dk
-    dv = torch.empty_like(v) if dv is None else dv
-    gated = variant.get("gate_mode") == "sigmoid"
-    if gated and dgate is None:
-        dgate = torch.empty(out.shape, dtype=torch.bfloat16, device=q.device)
+def _bwd_args(q, k, v, out, lse, dout, dq, dk, dv, dgate, dbias, dlambda, variant):
     keep: list = []
     fa = make_args(q, k, v, out, lse, keep=keep, **variant)
     a = _lib.BwdArgs()
@@ -194,10 +185,35 @@ def attn_bwd(q, k, v, out, lse, dout, *, dq=None, dk=None, dv=None, dgate=None, 
     a.dout, a.dq, a.dk, a.dv = tensor(dout), tensor(dq), tensor(dk), tensor(dv)
     a.dgate = tensor(dgate)
     a.dbias = tensor(dbias)        # optional: pass an f32 tensor shaped like the bias to receive dL/dbias
+    a.dlambda = tensor(dlambda)
     a.var = fa.var
     a.stream = fa.stream
     need = C.c_size_t(0)
     _lib.check(_lib.lib().fl_attn_bwd_workspace_size(C.byref(a), C.byref(need)))
+    return a, keep, need
+
+
+def attn_bwd_workspace_bytes(q, k, v, out, lse, dout, **variant) -> int:
+    """fl_attn_bwd_workspace_size for these arguments (gradient buffers are not needed to size it)."""
+    gated = variant.get("gate_mode") == "sigmoid"
+    dg = torch.empty(out.shape, dtype=torch.bfloat16, device=q.device) if gated else None
+    return _bwd_args(q, k, v, out, lse, dout, torch.empty_like(q), torch.empty_like(k), torch.empty_like(v), dg,
+                     None, None, variant)[2].value
+
+
+def attn_bwd(q, k, v, out, lse, dout, *, dq=None, dk=None, dv=None, dgate=None, dbias=None, dlambda=None,
+             workspace=None, **variant):
+    """Backward of attn_fwd (fl_attn_bwd, NEXT-3): returns (dq, dk, dv) of L = sum(out * dout), given the
+    forward's output and natural-log LSE (attn_fwd(..., return_lse=True)); with a sigmoid gate also dgate
+    (dL/dgate-logits): (dq, dk, dv, dgate).  Differential attention (diff=True): lse=None (the call recomputes
+    the maps); pass an f32 [Hq] `dlambda` to receive dL/dlambda_h."""
+    dq = torch.empty_like(q) if dq is None else dq
+    dk = torch.empty_like(k) if dk is None else dk
+    dv = torch.empty_like(v) if dv is None else dv
+    gated = variant.get("gate_mode") == "sigmoid"
+    if gated and dgate is None:
+        dgate = torch.empty(out.shape, dtype=torch.bfloat16, device=q.device)
+    a, keep, need = _bwd_args(q, k, v, out, lse, dout, dq, dk, dv, dgate, dbias, dlambda, variant)
     if workspace is None or workspace.numel() * workspace.element_size() < need.value:
         workspace = torch.empty(max(need.value, 1), dtype=torch.uint8, device=q.device)
     keep.append(workspace)

@@ -36,7 +36,7 @@ def test_exports_every_declared_symbol(L):
 
 def test_abi_version_and_status_strings(L):
     from paper_2511_02043_b200 import _lib
-    assert L.fl_abi_version() == _lib.ABI_VERSION == 3
+    assert L.fl_abi_version() == _lib.ABI_VERSION == 4
     assert L.fl_status_string(0) == b"FL_OK"
     assert L.fl_status_string(2) == b"FL_ERR_UNSUPPORTED"
 

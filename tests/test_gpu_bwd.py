@@ -141,3 +141,74 @@ def test_backward_unsupported_is_loud(fl):
     od, ld = fl.attn_fwd(q2, q2, q, diff=True, lam=0.3), None
     with pytest.raises(fl.FlError):
         fl.attn_bwd(q2, q2, q, od, torch.zeros(1, 2, 128, device="cuda"), od.clone(), diff=True, lam=0.3)
+
+
+DIFF_BWD = [
+    dict(name="diff_needle_D64", Hq=2, S=300, D=64, diff=True, lam=0.7, dist="needle"),
+    dict(name="diff_lambda_h_causal_gqa_D128", Hq=4, Hkv=2, S=333, D=128, diff=True, lambda_h=True, mask="causal",
+         dist="needle"),
+    dict(name="diff_gate_causal_D32", Hq=2, S=260, D=32, diff=True, lam=0.5, gate_mode="sigmoid", mask="causal",
+         dist="needle"),
+    dict(name="diff_reparam_sliding_D64", Hq=2, S=200, D=64, diff=True, lambda_qk=True, lambda_init=0.8,
+         mask="sliding", window=64, dist="needle"),
+]
+_DIFF_KEYS = ("diff", "lam", "lambda_h", "lambda_qk", "lambda_init")
+
+
+@pytest.mark.parametrize("case", DIFF_BWD, ids=[c["name"] for c in DIFF_BWD])
+def test_backward_diff(fl, case):
+    """Differential attention (Listing 4, G8): dQ, dK (both maps), dV (summed over the maps),
+    dgate and dL/dlambda_h against the oracle's chain rule (pinned to central differences).  dlambda_h is a
+    sum of B S D terms dO * o_1: its bar is 8 x 2^-8 x sqrt(sum (dO o_1)^2) (bf16 rounding of o_1, independent
+    per element, 8 sigma), o_1 = the oracle's map-1 output."""
+    ins, gk, ok = cases.build(dict(case, dtype="bf16"))
+    q, k, v = (ins[n].cuda() for n in ("q", "k", "v"))
+    kw = {x: cases.to_dev(y, "cuda") for x, y in gk.items()}
+    out = fl.attn_fwd(q, k, v, **kw)
+    dout = synth.uniform(tuple(out.shape), seed=21, tensor="gate")
+    Hq = out.shape[-3]
+    dl = torch.empty(Hq, dtype=torch.float32, device="cuda")
+    gated = kw.get("gate_mode") == "sigmoid"
+    grads = fl.attn_bwd(q, k, v, out, None, dout.cuda(), dlambda=dl, **kw)
+    torch.cuda.synchronize()
+    refs = oracle.attn_bwd(ins["q"], ins["k"], ins["v"], dout, with_dgate=gated, with_dlambda=True, **ok)
+    names = ("dq", "dk", "dv", "dgate") if gated else ("dq", "dk", "dv")
+    # map 0 alone (lambda = 0): the value dV / dgate hold, rounded to bf16, before map 1 adds to them
+    ok0 = dict({x: y for x, y in ok.items() if x not in _DIFF_KEYS}, diff=True, lam=0.0)
+    refs0 = oracle.attn_bwd(ins["q"], ins["k"], ins["v"], dout, with_dgate=gated, **ok0)
+    for i, (name, got, ref) in enumerate(zip(names, grads, refs)):
+        g64 = got.cpu().double().numpy()
+        if name in ("dv", "dgate"):
+            # summed over the maps: the map-0 value is stored in bf16, map 1 adds in fp32 and the sum is
+            # rounded again -- up to 2^-9 (|map-0 value| + |sum|) on top of the 2e-2 bar (|dV| reaches ~8 with
+            # GQA over needle rows, where one bf16 ulp is 2^-5)
+            ref = ref.reshape(g64.shape)
+            err = np.abs(g64 - ref)
+            bound = 2e-2 + 2.0 ** -9 * (np.abs(refs0[i].reshape(g64.shape)) + np.abs(ref))
+            assert np.all(err <= bound), f"{case['name']} {name}: worst excess {(err - bound).max():.3e}"
+            assert np.abs(ref).max() >= 0.05 and err.max() <= 0.05 * np.abs(ref).max()
+            continue
+        r = check(g64, ref, 2e-2, what=f"{case['name']} {name}")
+        if r["max_ref"] >= 0.05:
+            assert r["max_abs"] <= 0.05 * r["max_ref"], f"{case['name']} {name}: {r}"
+    # dlambda: the map-1 output from the oracle (gate included), per head
+    ok1 = {x: y for x, y in ok.items() if x not in _DIFF_KEYS}
+    Hkv = ins["k"].shape[1] // 2
+    o1, _ = oracle.attn(ins["q"][:, Hq:], ins["k"][:, Hkv:], ins["v"], **ok1)
+    terms = dout.double().numpy() * o1.reshape(dout.shape)
+    ref_dl = refs[-1]
+    assert np.allclose(ref_dl, -terms.sum(axis=(0, 2, 3)), rtol=1e-9, atol=1e-9)     # the oracle agrees with itself
+    bar = 8 * 2.0 ** -8 * np.sqrt((terms ** 2).sum(axis=(0, 2, 3))) + 1e-3
+    err = np.abs(dl.cpu().double().numpy() - ref_dl)
+    assert np.all(err <= bar), (case["name"], err, bar, ref_dl)
+    assert np.abs(ref_dl).max() > 4 * bar.max(), "dlambda check not discriminating"
+
+
+def test_backward_diff_unsupported_is_loud(fl):
+    q = torch.zeros(1, 4, 128, 64, device="cuda", dtype=torch.bfloat16)
+    v = torch.zeros(1, 2, 128, 64, device="cuda", dtype=torch.bfloat16)
+    o = fl.attn_fwd(q, q, v, diff=True, lam=0.3)
+    with pytest.raises(fl.FlError, match="UNSUPPORTED"):
+        fl.attn_bwd(q, q, v, o, None, o.clone(), diff=True, lam=0.3, diff_norm=True, diff_norm_eps=1e-5)
+    with pytest.raises(fl.FlError):
+        fl.attn_bwd(q, q, v, o, torch.zeros(1, 2, 128, device="cuda"), o.clone(), diff=True, lam=0.3)
