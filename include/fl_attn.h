@@ -158,8 +158,9 @@ fl_status fl_attn_fwd(const fl_attn_args* args);
  * Supported (v3): bf16, rank-4 or rank-5 q/k/v (G), D_qk == D_v in {32, 64, 128}, GQA, masks none /
  * causal / sliding / prefix / document (either alignment), mods none / ALiBi / softcap, key_mask (MSA
  * mask), sigmoid gate (+ dgate), additive bias (+ dbias), differential attention (v4, Listing 4 P:L412-424,
- * G8: lambda, lambda_h or lambda_qk; + dlambda).  Not yet: the diff_norm epilogue, dbias with diff, mul gate,
- * block lists, paged KV, fp32 (FL_ERR_UNSUPPORTED).  Workspace (fl_attn_bwd_workspace_size): 4 B G Hq S_q
+ * G8: lambda, lambda_h or lambda_qk; + dlambda), mul gate (v4; + dgate = dO * A, A recomputed by the forward
+ * kernel without the gate into the workspace: 2 B G Hq S_q D_v bytes + that forward's workspace).  Not yet:
+ * the diff_norm epilogue, dbias or the mul gate with diff, block lists, paged KV, fp32 (FL_ERR_UNSUPPORTED).  Workspace (fl_attn_bwd_workspace_size): 4 B G Hq S_q
  * bytes (Dvec) + the packed key mask + 2 B G Hq S_q D_v bytes with a sigmoid gate, each 256-byte rounded.
  * Diff: the forward keeps neither map's output, so the call recomputes both maps (o_i, lse_i: the forward
  * kernel per map), seeds map 1 with -lambda_h dO, runs the single-map backward per map and sums dV (and
@@ -174,7 +175,7 @@ typedef struct {
   void* stream;
   void* workspace;
   size_t workspace_bytes;
-  fl_tensor dgate;           /* optional (gate_mode sigmoid): dL/dgate-logits, bf16, the gate's shape (ABI v3) */
+  fl_tensor dgate;           /* optional (a gate): dL/dgate (sigmoid: of the logits), bf16, the gate's shape (ABI v3) */
   fl_tensor dbias;           /* optional (with a bias): dL/dbias, f32, the bias's shape; dims the bias broadcasts
                                 (stride 0 or size 1) are summed over; must be compact -- the call zeroes it and
                                 accumulates with fp32 atomics (ABI v3) */

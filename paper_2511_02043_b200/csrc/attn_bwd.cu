@@ -65,10 +65,13 @@ __global__ void __launch_bounds__(256) bwd_dvec_kernel(const AttnParams p, const
 // out = s(g) * A:  dA = dO * s(g) (written as the dO the tcgen05 kernels read, contiguous [B,G,Hq,Sq,Dv]),
 // dg = dO * out * (1 - s(g))  (= dO * A * s (1 - s), no division by s), Dvec = rowsum(dA * A) = rowsum(dO * out).
 // One warp per output row, 8 elements per lane and step.
+// Mul gate (O = G * A): dA = dO * G, dg = dO * A with A the ungated output the host recomputed into `aun`
+// (contiguous [rows, Dv]; no division by G), Dvec = rowsum(dO * out) as above.
+template <bool MUL>
 __global__ void __launch_bounds__(256) bwd_gate_kernel(const AttnParams p, const __nv_bfloat16* __restrict__ dout,
                                                       Strided5 dos, __nv_bfloat16* __restrict__ da,
                                                       __nv_bfloat16* __restrict__ dgate, Strided5 dgs,
-                                                      float* __restrict__ dvec) {
+                                                      float* __restrict__ dvec, const __nv_bfloat16* __restrict__ aun) {
   const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   const int64_t n_rows = (int64_t)p.B * p.G * p.Hq * p.Sq;
@@ -87,6 +90,20 @@ __global__ void __launch_bounds__(256) bwd_gate_kernel(const AttnParams p, const
                 ug = *reinterpret_cast<const uint4*>(gl + c);
     const uint32_t wo[4] = {uo.x, uo.y, uo.z, uo.w}, wd[4] = {ud.x, ud.y, ud.z, ud.w}, wg[4] = {ug.x, ug.y, ug.z, ug.w};
     uint32_t pa[4], pg[4];
+    if constexpr (MUL) {
+      const uint4 ua = *reinterpret_cast<const uint4*>(aun + row * p.Dv + c);
+      const uint32_t wa[4] = {ua.x, ua.y, ua.z, ua.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float d0 = bf16_lo(wd[t]), d1 = bf16_hi(wd[t]);
+        acc = fmaf(bf16_lo(wo[t]), d0, fmaf(bf16_hi(wo[t]), d1, acc));
+        pa[t] = pack_bf16(d0 * bf16_lo(wg[t]), d1 * bf16_hi(wg[t]));
+        pg[t] = pack_bf16(d0 * bf16_lo(wa[t]), d1 * bf16_hi(wa[t]));
+      }
+      *reinterpret_cast<uint4*>(dar + c) = make_uint4(pa[0], pa[1], pa[2], pa[3]);
+      if (dgr) *reinterpret_cast<uint4*>(dgr + c) = make_uint4(pg[0], pg[1], pg[2], pg[3]);
+      continue;
+    }
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       const float o0 = bf16_lo(wo[t]), o1 = bf16_hi(wo[t]), d0 = bf16_lo(wd[t]), d1 = bf16_hi(wd[t]);
@@ -823,12 +840,16 @@ static cudaError_t launch_bwd_d(const AttnParams& p, const TmaMaps& maps, const 
 // The gate pre-pass (when p.gate_mode is sigmoid; `da` receives dO * s(g) and the caller's tdo map points
 // at it) or the plain Dvec pass.
 cudaError_t launch_bwd_prepass(const AttnParams& p, const void* dout, Strided5 dos, float* dvec, void* da, void* dgate,
-                               Strided5 dgs, cudaStream_t s) {
+                               Strided5 dgs, const void* aun, cudaStream_t s) {
   const int64_t rows = (int64_t)p.B * p.G * p.Hq * p.Sq;
   if (p.gate_mode == GATE_SIGMOID)
-    bwd_gate_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(p, static_cast<const __nv_bfloat16*>(dout), dos,
-                                                                static_cast<__nv_bfloat16*>(da),
-                                                                static_cast<__nv_bfloat16*>(dgate), dgs, dvec);
+    bwd_gate_kernel<false><<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(
+        p, static_cast<const __nv_bfloat16*>(dout), dos, static_cast<__nv_bfloat16*>(da),
+        static_cast<__nv_bfloat16*>(dgate), dgs, dvec, nullptr);
+  else if (p.gate_mode == GATE_MUL)
+    bwd_gate_kernel<true><<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(
+        p, static_cast<const __nv_bfloat16*>(dout), dos, static_cast<__nv_bfloat16*>(da),
+        static_cast<__nv_bfloat16*>(dgate), dgs, dvec, static_cast<const __nv_bfloat16*>(aun));
   else
     bwd_dvec_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(p, static_cast<const __nv_bfloat16*>(dout), dos, dvec);
   return cudaGetLastError();

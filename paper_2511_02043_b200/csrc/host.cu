@@ -45,7 +45,7 @@ cudaError_t launch_pipe_rate(int op, int iters, int n_sms, float* sink, cudaStre
 cudaError_t launch_sched_dump(const AttnParams& p, int32_t* out, int64_t out_words, int64_t* n_records,
                               int32_t* max_tiles, cudaStream_t stream);
 cudaError_t launch_bwd_prepass(const AttnParams& p, const void* dout, Strided5 dos, float* dvec, void* da, void* dgate,
-                               Strided5 dgs, cudaStream_t s);
+                               Strided5 dgs, const void* aun, cudaStream_t s);
 cudaError_t launch_diff_bwd_seed(const AttnParams& p, const void* dout, Strided5 dos, const void* o1, void* do1,
                                  float* dlambda, cudaStream_t s);
 cudaError_t launch_attn_bwd(const AttnParams& p, const TmaMaps& maps, const CUtensorMap& tdo, const CUtensorMap& tq64,
@@ -767,7 +767,8 @@ namespace {
 struct BwdPrepared {
   Prepared P;
   View5 dout, dq, dk, dv, dgate, dbias;
-  size_t ws = 0, off_bits = 0, off_da = 0;
+  size_t ws = 0, off_bits = 0, off_da = 0, off_aun = 0, off_fws = 0, fws = 0;
+  fl_attn_args fwd_ungated;         // mul gate: the forward without the gate, recomputing A into the workspace
   int64_t dbias_span = 0;
 };
 
@@ -783,8 +784,8 @@ fl_status prepare_bwd(const fl_attn_bwd_args* a, BwdPrepared& B, bool device_ptr
   const AttnParams& p = B.P.p;
   if (!B.P.bf16) return fail(FL_ERR_UNSUPPORTED, "backward: bf16 q/k/v/o");
   if (p.Dqk != 32 && p.Dqk != 64 && p.Dqk != 128) return fail(FL_ERR_UNSUPPORTED, "backward: D in {32, 64, 128}");
-  if (var.diff || var.kv_page_table.data || var.mask == FL_MASK_BLOCKLIST || var.gate_mode == FL_GATE_MUL)
-    return fail(FL_ERR_UNSUPPORTED, "backward: no block list / paged KV / mul gate");
+  if (var.diff || var.kv_page_table.data || var.mask == FL_MASK_BLOCKLIST)
+    return fail(FL_ERR_UNSUPPORTED, "backward: no block list / paged KV");
   if (!a->lse.data) return fail(FL_ERR_INVALID_ARGUMENT, "backward needs the forward's lse");
   const int R = B.P.q_rank;
   const fl_tensor* ts[4] = {&a->dout, &a->dq, &a->dk, &a->dv};
@@ -799,7 +800,7 @@ fl_status prepare_bwd(const fl_attn_bwd_args* a, BwdPrepared& B, bool device_ptr
   }
   // dgate (optional; sigmoid gate only): bf16, the gate's shape
   if (a->dgate.data) {
-    if (var.gate_mode != FL_GATE_SIGMOID) return fail(FL_ERR_INVALID_ARGUMENT, "dgate needs gate_mode sigmoid");
+    if (var.gate_mode == FL_GATE_NONE) return fail(FL_ERR_INVALID_ARGUMENT, "dgate needs a gate");
     if (a->dgate.dtype != FL_BF16 || !to_view(a->dgate, R, 0, B.dgate))
       return fail(FL_ERR_SHAPE_MISMATCH, "dgate: bf16 with q's rank");
     for (int d = 0; d < 5; ++d)
@@ -844,7 +845,25 @@ fl_status prepare_bwd(const fl_attn_bwd_args* a, BwdPrepared& B, bool device_ptr
   B.off_bits = B.ws;
   B.ws += (B.P.keybits_bytes + 255) & ~size_t(255);
   B.off_da = B.ws;
-  if (var.gate_mode == FL_GATE_SIGMOID) B.ws += ((size_t)p.B * p.G * p.Hq * p.Sq * p.Dv * 2 + 255) & ~size_t(255);
+  if (var.gate_mode != FL_GATE_NONE) B.ws += ((size_t)p.B * p.G * p.Hq * p.Sq * p.Dv * 2 + 255) & ~size_t(255);
+  if (var.gate_mode == FL_GATE_MUL) {
+    // | A = softmax(s) V without the gate (dgate = dO * A; O / G would divide by the gate) | its forward's workspace
+    if (p.Dv % 8) return fail(FL_ERR_UNSUPPORTED, "backward, mul gate: D_v %% 8 == 0");
+    B.off_aun = B.ws;
+    B.ws += ((size_t)p.B * p.G * p.Hq * p.Sq * p.Dv * 2 + 255) & ~size_t(255);
+    fl_attn_args& fu = B.fwd_ungated;
+    memset(&fu, 0, sizeof fu);
+    fu.q = a->q; fu.k = a->k; fu.v = a->v; fu.var = var; fu.stream = a->stream;
+    fu.var.gate_mode = FL_GATE_NONE;
+    memset(&fu.var.gate, 0, sizeof fu.var.gate);
+    fu.o = a->o;                                     // placeholder data for sizing; contiguous A at run time
+    fu.o.stride[fu.o.rank - 1] = 1;
+    for (int d = fu.o.rank - 2; d >= 0; --d) fu.o.stride[d] = fu.o.stride[d + 1] * fu.o.size[d + 1];
+    fl_status st = fl_attn_workspace_size(&fu, &B.fws);
+    if (st != FL_OK) return st;
+    B.off_fws = B.ws;
+    B.ws += (B.fws + 255) & ~size_t(255);
+  }
   return FL_OK;
 }
 }  // namespace
@@ -1047,10 +1066,22 @@ fl_status bwd_single(const fl_attn_bwd_args* args, bool grad_accum) {
     if (e != cudaSuccess) return cuda_fail(e, "pack_keymask launch");
     p.keybits = bits;
   }
-  // dO as the tcgen05 kernels read it: the caller's, or dO * s(g) from the gate pre-pass (contiguous)
+  // mul gate: A (the ungated output) for dgate = dO * A, recomputed by the forward kernel
+  void* aun = nullptr;
+  if (p.gate_mode == GATE_MUL) {
+    fl_attn_args fu = B.fwd_ungated;
+    aun = ws + B.off_aun;
+    fu.o.data = aun;
+    fu.workspace = ws + B.off_fws;
+    fu.workspace_bytes = B.fws;
+    Prepared PU;
+    if ((s = prepare(&fu, PU, true)) != FL_OK) return s;
+    if ((s = launch_prepared(PU, &fu)) != FL_OK) return s;
+  }
+  // dO as the tcgen05 kernels read it: the caller's, or dO * gate' from the gate pre-pass (contiguous)
   View5 vda = B.dout;
   void* da = nullptr;
-  if (p.gate_mode == GATE_SIGMOID) {
+  if (p.gate_mode != GATE_NONE) {
     da = ws + B.off_da;
     vda.data = da;
     vda.stride[4] = 1;
@@ -1069,7 +1100,7 @@ fl_status bwd_single(const fl_attn_bwd_args* args, bool grad_accum) {
     e = cudaMemsetAsync(B.dbias.data, 0, (size_t)B.dbias_span * sizeof(float), stream);
     if (e != cudaSuccess) return cuda_fail(e, "dbias reset");
   }
-  e = launch_bwd_prepass(p, B.dout.data, strides_of(B.dout), dvec, da, B.dgate.data, strides_of(B.dgate), stream);
+  e = launch_bwd_prepass(p, B.dout.data, strides_of(B.dout), dvec, da, B.dgate.data, strides_of(B.dgate), aun, stream);
   ++g_launches;
   if (e != cudaSuccess) return cuda_fail(e, "backward pre-pass launch");
   e = launch_attn_bwd(p, maps, tdo, tq64, tdo64, static_cast<const float*>(B.P.lse.data), strides_of(B.P.lse), B.dout.data,

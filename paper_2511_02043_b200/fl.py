@@ -195,7 +195,7 @@ def _bwd_args(q, k, v, out, lse, dout, dq, dk, dv, dgate, dbias, dlambda, varian
 
 def attn_bwd_workspace_bytes(q, k, v, out, lse, dout, **variant) -> int:
     """fl_attn_bwd_workspace_size for these arguments (gradient buffers are not needed to size it)."""
-    gated = variant.get("gate_mode") == "sigmoid"
+    gated = variant.get("gate_mode") in ("sigmoid", "mul")
     dg = torch.empty(out.shape, dtype=torch.bfloat16, device=q.device) if gated else None
     return _bwd_args(q, k, v, out, lse, dout, torch.empty_like(q), torch.empty_like(k), torch.empty_like(v), dg,
                      None, None, variant)[2].value
@@ -204,13 +204,13 @@ def attn_bwd_workspace_bytes(q, k, v, out, lse, dout, **variant) -> int:
 def attn_bwd(q, k, v, out, lse, dout, *, dq=None, dk=None, dv=None, dgate=None, dbias=None, dlambda=None,
              workspace=None, **variant):
     """Backward of attn_fwd (fl_attn_bwd, NEXT-3): returns (dq, dk, dv) of L = sum(out * dout), given the
-    forward's output and natural-log LSE (attn_fwd(..., return_lse=True)); with a sigmoid gate also dgate
-    (dL/dgate-logits): (dq, dk, dv, dgate).  Differential attention (diff=True): lse=None (the call recomputes
+    forward's output and natural-log LSE (attn_fwd(..., return_lse=True)); with a gate also dgate
+    (dL/dgate, of the logits for the sigmoid gate): (dq, dk, dv, dgate).  Differential attention (diff=True): lse=None (the call recomputes
     the maps); pass an f32 [Hq] `dlambda` to receive dL/dlambda_h."""
     dq = torch.empty_like(q) if dq is None else dq
     dk = torch.empty_like(k) if dk is None else dk
     dv = torch.empty_like(v) if dv is None else dv
-    gated = variant.get("gate_mode") == "sigmoid"
+    gated = variant.get("gate_mode") in ("sigmoid", "mul")
     if gated and dgate is None:
         dgate = torch.empty(out.shape, dtype=torch.bfloat16, device=q.device)
     a, keep, need = _bwd_args(q, k, v, out, lse, dout, dq, dk, dv, dgate, dbias, dlambda, variant)

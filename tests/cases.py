@@ -99,6 +99,8 @@ def build(case: dict):
             ok["diff_norm_w"] = w.astype(np.float64)
     if c.get("gate_mode"):
         g = synth.gate_logits((B, Hq, Sq, Dv), seed=seed, dtype=torch.bfloat16 if dt == torch.bfloat16 else dt)
+        if c.get("gate_unit"):          # a mul gate in [-1, 1] (exact: / 4), the |inputs| <= 1 regime of the bar
+            g = g / 4
         gk["gate_mode"] = ok["gate_mode"] = c["gate_mode"]
         gk["gate"] = g
         ok["gate"] = g

@@ -37,11 +37,13 @@ for D in (128, 64):
         dict(name=f"sq_lt_sk_D{D}", Sq=100, Sk=450, D=D, mask="causal"),
         dict(name=f"keymask_D{D}", Hq=2, S=300, D=D, key_mask=True, dist="needle"),
         dict(name=f"gate_sigmoid_D{D}", Hq=2, S=260, D=D, mask="causal", gate_mode="sigmoid", dist="needle"),
+        dict(name=f"gate_mul_D{D}", Hq=2, S=260, D=D, mask="causal", gate_mode="mul", gate_unit=True, dist="needle"),
     ]
 BWD += [
     dict(name="vanilla_D32", Hq=2, S=300, D=32),
     dict(name="causal_needle_D32", Hq=2, S=520, D=32, mask="causal", dist="needle"),
     dict(name="gate_keymask_D32", Hq=2, S=200, D=32, key_mask=True, gate_mode="sigmoid", dist="needle"),
+    dict(name="gate_mul_keymask_D32", Hq=2, S=200, D=32, key_mask=True, gate_mode="mul", gate_unit=True, dist="needle"),
 ]
 
 
@@ -56,7 +58,7 @@ def test_backward_vs_oracle(fl, case):
 
 
 def _compare(fl, name0, host_qkv, dev_qkv, out, lse, dout, kw, ok):
-    gated = kw.get("gate_mode") == "sigmoid"
+    gated = kw.get("gate_mode") in ("sigmoid", "mul")
     grads = fl.attn_bwd(*dev_qkv, out, lse, dout.cuda(), **kw)
     torch.cuda.synchronize()
     refs = oracle.attn_bwd(*host_qkv, dout, with_dgate=gated, **ok)
@@ -134,9 +136,6 @@ def test_backward_evoformer_row(fl, Nr):
 def test_backward_unsupported_is_loud(fl):
     q = torch.zeros(1, 2, 128, 64, device="cuda", dtype=torch.bfloat16)
     o, lse = fl.attn_fwd(q, q, q[:, :1].expand(1, 2, 128, 64).contiguous(), return_lse=True)
-    g = torch.ones_like(o)
-    with pytest.raises(fl.FlError, match="UNSUPPORTED"):
-        fl.attn_bwd(q, q, q, o, lse, o.clone(), gate_mode="mul", gate=g)
     q2 = torch.zeros(1, 4, 128, 64, device="cuda", dtype=torch.bfloat16)
     od, ld = fl.attn_fwd(q2, q2, q, diff=True, lam=0.3), None
     with pytest.raises(fl.FlError):
