@@ -85,15 +85,14 @@ __global__ void __launch_bounds__(kDecCompute + 32, 1)
                              float* __restrict__ part, int bps, int n_split, long long n_items) {
   using C = DecCfg<D>;
   constexpr int DG = D / 8;                 // 16-byte column groups
-  constexpr int KG = kDecCompute / DG;      // key groups for P V
-  constexpr int KPG = 128 / KG;             // keys per key group
   constexpr int NW = kDecCompute / 32;
+  constexpr int KPW = 128 / NW;             // keys per warp (16)
+  constexpr int CPL = D / 32;               // P V columns per lane
   extern __shared__ uint8_t dec_smem_raw[];
   uint8_t* ring = dec_smem_raw + ((1024u - (smem_u32(dec_smem_raw) & 1023u)) & 1023u);
   __shared__ __align__(16) float qs[D];
-  __shared__ float ps[128];
-  __shared__ float red[2][NW];
-  __shared__ __align__(16) float accs[KG][D];
+  __shared__ float wm_s[NW], wl_s[NW];
+  __shared__ __align__(16) float accs[NW][D];
   __shared__ uint64_t full[C::NST], empty[C::NST];
   __shared__ int kbinfo[C::NST];
 
@@ -177,8 +176,11 @@ __global__ void __launch_bounds__(kDecCompute + 32, 1)
   }
 
   // ============================== compute (256 threads) ==============================
-  const int dg = t % DG, kg = t / DG;
-  const int key = t >> 1, half = t & 1;               // Q K^T: thread pair (2k, 2k+1) splits key k's D
+  // Warp w owns keys [16 w, 16 w + 16) of every block and keeps its own online softmax (m, l, O over all
+  // D columns): lane pair (2k, 2k + 1) splits key k's Q K^T dot product, then lane j accumulates P V for
+  // columns [CPL j, CPL j + CPL) over the warp's 16 keys (P broadcast by shuffles).  No barrier per
+  // block -- the eight warps meet once per item, when their partials are merged (Alg.2's closed form).
+  const int key = warp * KPW + (lane >> 1), half = lane & 1;
   auto load_q = [&](long long it) -> unsigned short {  // element t of the item's query row
     int q, h, g, b;
     int64_t bgh;
@@ -187,6 +189,9 @@ __global__ void __launch_bounds__(kDecCompute + 32, 1)
   };
   unsigned short q_next = 0;
   if (t < D && blockIdx.x < n_items) q_next = load_q(blockIdx.x);
+  // lane's P V columns inside a 128-B swizzled V row: 16-B chunk cv, byte offset cb within it
+  constexpr int BPL = CPL * 2;
+  const int cv = lane * BPL / 16, cb = lane * BPL % 16;
   int e = 0;
   for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
     const int64_t row = it / n_split;
@@ -205,9 +210,9 @@ __global__ void __launch_bounds__(kDecCompute + 32, 1)
     named_bar_sync(1, kDecCompute);
     if (t < D && it + gridDim.x < n_items) q_next = load_q(it + gridDim.x);   // in flight during this item
 
-    float acc[8];
+    float acc[CPL];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+    for (int i = 0; i < CPL; ++i) acc[i] = 0.f;
     float m = -INFINITY, l = 0.f;
     for (int i = 0; i < bps; ++i, ++e) {
       const int s = e % C::NST;
@@ -250,59 +255,63 @@ __global__ void __launch_bounds__(kDecCompute + 32, 1)
         if (p.mod == MOD_ALIBI) sv += slope_l2 * (float)(k - q_abs);
         if (p.mod == MOD_SOFTCAP) sv = p.softcap * kDecLog2e * tanh_approx(dot * p.scale / p.softcap);
       }
-      float bm = dec_warp_max(sv);
-      if (lane == 0) red[0][warp] = bm;
-      named_bar_sync(1, kDecCompute);
-      bm = red[0][0];
-#pragma unroll
-      for (int w2 = 1; w2 < NW; ++w2) bm = fmaxf(bm, red[0][w2]);
-      const float m_new = fmaxf(m, bm);
-      if (m_new == -INFINITY) {                         // nothing kept so far (block-uniform)
+      const float m_new = fmaxf(m, dec_warp_max(sv));
+      if (m_new == -INFINITY) {                         // nothing kept by this warp so far (warp-uniform)
         mbar_arrive(&empty[s]);
-        named_bar_sync(1, kDecCompute);
         continue;
       }
       const float corr = ex2(m - m_new);                // 0 when m = -inf
       const float pe = sv == -INFINITY ? 0.f : ex2(sv - m_new);
-      if (half == 0) ps[key] = pe;
-      const float ws = dec_warp_sum(half == 0 ? pe : 0.f);
-      if (lane == 0) red[1][warp] = ws;
-      named_bar_sync(1, kDecCompute);
-      float bs = 0.f;
-#pragma unroll
-      for (int w2 = 0; w2 < NW; ++w2) bs += red[1][w2];
-      l = l * corr + bs;
+      l = l * corr + dec_warp_sum(half == 0 ? pe : 0.f);
       m = m_new;
 #pragma unroll
-      for (int i2 = 0; i2 < 8; ++i2) acc[i2] *= corr;
+      for (int i2 = 0; i2 < CPL; ++i2) acc[i2] *= corr;
 #pragma unroll
-      for (int t2 = 0; t2 < KPG; ++t2) {
-        const int kr = kg * KPG + t2;
-        const float pv = ps[kr];
-        const uint4 vv = *reinterpret_cast<const uint4*>(vs + (dg >> 3) * C::SLAB + kr * 128 + (((dg & 7) ^ (kr & 7)) << 4));
-        const uint32_t w4[4] = {vv.x, vv.y, vv.z, vv.w};
-#pragma unroll
-        for (int e2 = 0; e2 < 4; ++e2) {
-          acc[2 * e2] = fmaf(pv, bf16_lo(w4[e2]), acc[2 * e2]);
-          acc[2 * e2 + 1] = fmaf(pv, bf16_hi(w4[e2]), acc[2 * e2 + 1]);
+      for (int kk = 0; kk < KPW; ++kk) {
+        const int kr = warp * KPW + kk;
+        const float pv = __shfl_sync(0xffffffffu, pe, 2 * kk);
+        const uint8_t* vp = vs + (cv >> 3) * C::SLAB + kr * 128 + ((((cv & 7) ^ (kr & 7)) << 4) | cb);
+        if constexpr (CPL == 4) {
+          const uint2 vv = *reinterpret_cast<const uint2*>(vp);
+          acc[0] = fmaf(pv, bf16_lo(vv.x), acc[0]);
+          acc[1] = fmaf(pv, bf16_hi(vv.x), acc[1]);
+          acc[2] = fmaf(pv, bf16_lo(vv.y), acc[2]);
+          acc[3] = fmaf(pv, bf16_hi(vv.y), acc[3]);
+        } else {
+          const uint32_t vv = *reinterpret_cast<const uint32_t*>(vp);
+          acc[0] = fmaf(pv, bf16_lo(vv), acc[0]);
+          acc[1] = fmaf(pv, bf16_hi(vv), acc[1]);
         }
       }
       mbar_arrive(&empty[s]);                           // this thread is done with the stage
-      named_bar_sync(1, kDecCompute);                   // ps / red reuse
     }
+    // merge the eight warps' partials: O_s = sum_w O_w 2^(m_w - M), l_s = sum_w l_w 2^(m_w - M)
 #pragma unroll
-    for (int i2 = 0; i2 < 8; ++i2) accs[kg][dg * 8 + i2] = acc[i2];
+    for (int i2 = 0; i2 < CPL; ++i2) accs[warp][lane * CPL + i2] = acc[i2];
+    if (lane == 0) {
+      wm_s[warp] = m;
+      wl_s[warp] = l;
+    }
     named_bar_sync(1, kDecCompute);
     float* out = part + (row * n_split + split) * (D + 2);
     if (t < D) {
-      float o = 0.f;
+      float M = -INFINITY;
 #pragma unroll
-      for (int g2 = 0; g2 < KG; ++g2) o += accs[g2][t];
+      for (int w = 0; w < NW; ++w) M = fmaxf(M, wm_s[w]);
+      float o = 0.f, L = 0.f;
+      if (M != -INFINITY) {
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          const float f = wm_s[w] == -INFINITY ? 0.f : ex2(wm_s[w] - M);
+          o = fmaf(accs[w][t], f, o);
+          L = fmaf(wl_s[w], f, L);
+        }
+      }
       out[t] = o;
-    }
-    if (t == 0) {
-      out[D] = m;
-      out[D + 1] = l;
+      if (t == 0) {
+        out[D] = M;
+        out[D + 1] = L;
+      }
     }
   }
 }
