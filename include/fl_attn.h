@@ -278,9 +278,13 @@ fl_status fl_linear(const fl_linear_args* args);
  * Inputs (device, contiguous): q, k, v bf16 [N, H, c]; qp, kp bf16 [N, H, Pq, 3]; vp bf16 [N, H, Pv, 3];
  * R f32 [N, 3, 3] (row-major, global = R local + t); t f32 [N, 3]; bias bf16 [H, N, N] (the projected pair
  * bias b); z bf16 [N, N, cz]; gamma f32 [H] (already softplus'ed).  Outputs: o bf16 [N, H, c]; op f32
- * [N, H, Pv, 3] (local frames); opair bf16 [N, H, cz].  Limits: c + 9 Pq + 2 <= 64, Pv <= 8, cz % 8 == 0, N <= 40000.  Launches: a prep kernel (the augmented 64-column Q' / K' of the point
- * term's expansion, hi/lo bf16 pairs), a bias-scale kernel, the fused attention forward (tensor cores,
- * softmax, o and the LSE), a finish kernel (pair and point outputs from the recomputed probabilities, fp32).
+ * [N, H, Pv, 3] (local frames); opair bf16 [N, H, cz].  Limits: c + 9 Pq + 2 <= 64, Pv in {0, 4, 8},
+ * cz % 8 == 0, N <= 8600 (a row's probabilities for 6 heads staged in shared memory; FL_ERR_UNSUPPORTED
+ * otherwise).  Launches: a prep
+ * kernel (the augmented 64-column Q' / K' of the point term's expansion, hi/lo bf16 pairs), a bias-scale
+ * kernel, the fused attention forward (tensor cores, softmax, o and the LSE), a probabilities kernel
+ * (a_ij^h = exp(logit - LSE) in fp32, 16 query rows per CTA) and an output kernel (CTA per row i and group of
+ * 6 heads: z_i streamed once per group for the pair output, the point sums back-transformed by T_i^-1).
  * Workspace: fl_ipa_workspace_size.  Asynchronous on `stream`. */
 typedef struct {
   fl_tensor q, k, v, qp, kp, vp, R, t, bias, z, gamma;

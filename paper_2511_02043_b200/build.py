@@ -62,8 +62,8 @@ def build(verbose: bool = False, extra=None) -> str:
             if log:
                 print(f"== {os.path.basename(o)}\n{log}", file=sys.stderr)
     if _stale(SO, objs) or extra:
-        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", SO, *objs, "-lcuda"]
-        cmd = [c for c in cmd if c != "-lcuda"]
+        # --no-undefined: a symbol missing from the objects fails the link here, not the dlopen on the GPU box
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-Xlinker", "--no-undefined", "-o", SO, *objs]
         subprocess.check_call(cmd)
     return SO
 

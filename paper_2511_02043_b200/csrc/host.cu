@@ -21,7 +21,8 @@ namespace fl {
 cudaError_t launch_attn_simt(const AttnParams& p, cudaStream_t stream);
 cudaError_t launch_attn_tc(const AttnParams& p, const TmaMaps& maps, cudaStream_t stream);
 cudaError_t launch_ipa_prep(const IpaParams& p, cudaStream_t s);
-cudaError_t launch_ipa_finish(const IpaParams& p, const float* lse, void* opair, float* op, cudaStream_t s);
+cudaError_t launch_ipa_finish(const IpaParams& p, const float* lse, float* A, void* opair, float* op, cudaStream_t s);
+size_t ipa_out_smem(const IpaParams& p);
 cudaError_t launch_linear(const LinParams& p, const CUtensorMap& tx, const CUtensorMap& tw, const CUtensorMap& ty,
                           int y_tma, cudaStream_t stream);
 cudaError_t launch_pack_keymask(const unsigned char* km, int64_t sb, int64_t sg, int64_t sk, int B, int G, int Sk,
@@ -1182,8 +1183,8 @@ namespace {
 struct IpaPrepared {
   fl::IpaParams p;
   int64_t N = 0, H = 0, c = 0, Pq = 0, Pv = 0, cz = 0;
-  size_t off_qa = 0, off_ka = 0, off_va = 0, off_gv = 0, off_bias = 0, off_o = 0, off_lse = 0, off_attn = 0,
-         total = 0;
+  size_t off_qa = 0, off_ka = 0, off_va = 0, off_gv = 0, off_bias = 0, off_o = 0, off_lse = 0, off_a = 0,
+         off_attn = 0, total = 0;
 };
 
 bool dense(const fl_tensor& t, int rank, const int64_t* sizes, int dtype) {
@@ -1213,9 +1214,15 @@ fl_status prepare_ipa(const fl_ipa_args* a, IpaPrepared& P) {
       !dense(a->z, 3, s_z, FL_BF16) || !dense(a->gamma, 1, s_g, FL_F32) || !dense(a->o, 3, s_nhc, FL_BF16) ||
       !dense(a->op, 4, s_vp, FL_F32) || !dense(a->opair, 3, s_opair, FL_BF16))
     return fail(FL_ERR_SHAPE_MISMATCH, "ipa: tensors must be contiguous with the documented shapes and dtypes");
-  if (N < 1 || H < 1 || c < 1 || c + 9 * P.Pq + 2 > 64 || P.cz < 8 || P.cz % 8 != 0 || P.Pv < 0 || N > 40000 ||
+  if (N < 1 || H < 1 || c < 1 || c + 9 * P.Pq + 2 > 64 || P.cz < 8 || P.cz % 8 != 0 || P.Pv < 0 || P.Pv % 4 != 0 ||
       3 * P.Pv > 24)
-    return fail(FL_ERR_UNSUPPORTED, "ipa: c + 9 Pq + 2 <= 64, Pv <= 8, cz % 8 == 0, N <= 40000");
+    return fail(FL_ERR_UNSUPPORTED, "ipa: c + 9 Pq + 2 <= 64, Pv in {0, 4, 8}, cz %% 8 == 0");
+  {
+    fl::IpaParams ps;
+    ps.N = (int)N; ps.H = (int)H;
+    if (N > 65535 || ipa_out_smem(ps) > 227 * 1024)
+      return fail(FL_ERR_UNSUPPORTED, "ipa: N <= 8600 (a row's probabilities of 6 heads fit shared memory)");
+  }
   for (const fl_tensor* t : {&a->q, &a->k, &a->v, &a->qp, &a->kp, &a->vp, &a->R, &a->t, &a->bias, &a->z, &a->gamma,
                              &a->o, &a->op, &a->opair})
     if (!on_device(t->data)) return fail(FL_ERR_INVALID_ARGUMENT, "ipa: pointers must be device memory");
@@ -1228,6 +1235,7 @@ fl_status prepare_ipa(const fl_ipa_args* a, IpaPrepared& P) {
   P.off_bias = off; off += up(H * N * N * 4);
   P.off_o = off; off += up(N * H * 64 * 2);
   P.off_lse = off; off += up(H * N * 4);
+  P.off_a = off; off += up(H * N * N * 4);           // a_ij^h (fp32) for the pair and point outputs
   P.off_attn = off;
   off += 1024 * 1024;                                // the attention call's workspace (ticket counter)
   P.total = off;
@@ -1305,9 +1313,10 @@ fl_status fl_ipa_fwd(const fl_ipa_args* args) {
   // o = the first c columns of O'
   e = cudaMemcpy2DAsync(args->o.data, c * 2, o64, 64 * 2, c * 2, N * H, cudaMemcpyDeviceToDevice, stream);
   if (e != cudaSuccess) return cuda_fail(e, "ipa o copy");
-  if ((e = launch_ipa_finish(p, lse, args->opair.data, static_cast<float*>(args->op.data), stream)) != cudaSuccess)
+  if ((e = launch_ipa_finish(p, lse, reinterpret_cast<float*>(ws + P.off_a), args->opair.data,
+                             static_cast<float*>(args->op.data), stream)) != cudaSuccess)
     return cuda_fail(e, "ipa finish launch");
-  ++g_launches;
+  g_launches += 2;
   return FL_OK;
 }
 

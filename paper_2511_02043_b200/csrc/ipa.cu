@@ -47,7 +47,7 @@ __global__ void ipa_prep_kernel(const IpaParams p) {
     for (int f = 0; f < 3; ++f) y += R[e * 3 + f] * __bfloat162float(p.kp[((int64_t)w * p.Pq + pp) * 3 + f]);
     y2 += y * y;
   }
-  const int P3 = 3 * p.Pq, o1 = p.c, o2 = p.c + P3, o3 = p.c + 2 * P3, o4 = p.c + 3 * P3;
+  const int P3 = 3 * p.Pq, o1 = p.c, o4 = p.c + 3 * P3;   // column blocks: [o1, o1 + 3 P3) points, o4, o4 + 1 norms
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
     const int d = lane + 32 * half;
@@ -93,111 +93,208 @@ __global__ void ipa_bias_kernel(const IpaParams p) {
     p.bias_s[i] = __float2bfloat16_rn(wL * __bfloat162float(p.bias[i]));
 }
 
-// One CTA per (row i, head h), 128 threads (many small CTAs: the per-row loops are latency-bound, so the
-// kernel relies on occupancy): a_ij (recomputed from Q', K', w_L b and the forward's LSE, fp32), then
-// opair_i^h = sum_j a_ij z_ij (thread = feature) and the point output op_ip^h = R_i^T (sum_j a_ij g_jp^h - t_i)
-// (24 sums split over 5 j-partitions of the threads, reduced in shared memory).
-constexpr int kIpaThreads = 128;
-constexpr int kIpaParts = kIpaThreads / 24;        // 5 j-partitions for the (<= 24) point sums
-__global__ void __launch_bounds__(kIpaThreads) ipa_finish_kernel(const IpaParams p, const float* __restrict__ lse,
-                                                                 __nv_bfloat16* __restrict__ opair,
-                                                                 float* __restrict__ op) {
-  extern __shared__ float ipa_smem[];
-  float* a = ipa_smem;                             // [N]
-  float* qs = a + p.N;                             // [64]
-  float* gs = qs + kIpaD;                          // [kIpaParts][24]
-  const int i = blockIdx.x / p.H, h = blockIdx.x % p.H, tid = threadIdx.x;
-  if (tid < kIpaD) qs[tid] = __bfloat162float(p.qa[((int64_t)i * p.H + h) * kIpaD + tid]);
-  __syncthreads();
-  const float l = lse[(int64_t)h * p.N + i];      // lse [1, H, N] (natural log, G19)
-  // ---- a_ij
-  for (int j = tid; j < p.N; j += kIpaThreads) {
-    const uint4* kr = reinterpret_cast<const uint4*>(p.ka + ((int64_t)j * p.H + h) * kIpaD);
-    uint4 u[8];
+// a_ij^h = exp(Q'_i.K'_j + w_L b_ij - LSE_i) for a block of kProbRows query rows of one head, fp32 into
+// A [H, N, N] (for the pair output): thread = key j (its K' row of 64 bf16 in registers), the block's Q'
+// rows and LSEs in shared memory -- each K' row is read once per row block instead of once per row.  The
+// point output of the block's rows is summed here as well, over key chunks of kJC staged in shared memory
+// (the chunk's a_ij and global value points g_jp^h): thread (row, float4 of the <= 24 coordinates) --
+// op_ip^h = R_i^T (sum_j a_ij g_jp^h - t_i).
+constexpr int kProbRows = 16;
+constexpr int kProbThreads = 128;
+constexpr int kJC = 256;                           // keys per chunk
+size_t ipa_probs_smem() { return (size_t)(kProbRows * kJC + kJC * 24 + kProbRows * 24) * 4; }
+__global__ void __launch_bounds__(kProbThreads) ipa_probs_kernel(const IpaParams p, const float* __restrict__ lse,
+                                                                 float* __restrict__ A, float* __restrict__ op) {
+  __shared__ __align__(16) float qs[kProbRows][kIpaD];
+  __shared__ float ls[kProbRows];
+  extern __shared__ __align__(16) float pr_smem[];
+  float* as = pr_smem;                             // [kProbRows][kJC]
+  float* gs = as + kProbRows * kJC;                // [kJC][24]
+  float* gsum = gs + kJC * 24;                     // [kProbRows][24]
+  const int h = blockIdx.y, i0 = blockIdx.x * kProbRows, tid = threadIdx.x;
+  const int nr = min(kProbRows, p.N - i0);
+  const int PV3 = p.Pv * 3;
+  {                                                 // the rows' Q' (8 bf16 per thread and load, batched)
+    constexpr int kB = (kProbRows * kIpaD / 8 + kProbThreads - 1) / kProbThreads;
+    uint4 tmp[kB];
 #pragma unroll
-    for (int d = 0; d < 8; ++d) u[d] = __ldg(kr + d);
-    float s0 = 0.f, s1 = 0.f;
-#pragma unroll
-    for (int d = 0; d < 8; ++d) {
-      const uint32_t w[4] = {u[d].x, u[d].y, u[d].z, u[d].w};
-#pragma unroll
-      for (int x = 0; x < 4; ++x) {
-        s0 = fmaf(qs[d * 8 + 2 * x], bf16_lo(w[x]), s0);
-        s1 = fmaf(qs[d * 8 + 2 * x + 1], bf16_hi(w[x]), s1);
-      }
+    for (int k = 0; k < kB; ++k) {
+      const int e = tid + k * kProbThreads, r = e / (kIpaD / 8), d8 = e % (kIpaD / 8);
+      tmp[k] = make_uint4(0u, 0u, 0u, 0u);
+      if (r < nr) tmp[k] = __ldg(reinterpret_cast<const uint4*>(p.qa + ((int64_t)(i0 + r) * p.H + h) * kIpaD) + d8);
     }
-    const float s = s0 + s1 + __bfloat162float(p.bias_s[((int64_t)h * p.N + i) * p.N + j]);
-    a[j] = __expf(s - l);
-  }
-  __syncthreads();
-  // ---- pair output: thread -> 8 consecutive features (one 16-byte load of z per j) and a j-partition
-  // (8 partitions), reduced over the partitions in shared memory
-  const __nv_bfloat16* zi = p.z + (int64_t)i * p.N * p.cz;
-  float* red = ipa_smem + ((p.N + kIpaD + kIpaParts * 24 + 3) & ~3);   // [8][128], 16-byte aligned
-  for (int fb = 0; fb < p.cz; fb += 128) {
-    const int f8 = fb + (tid % 16) * 8, part = tid / 16;
-    float acc[8];
 #pragma unroll
-    for (int x = 0; x < 8; ++x) acc[x] = 0.f;
-    if (f8 < p.cz) {
-#pragma unroll 4
-      for (int j = part; j < p.N; j += 8) {
-        const uint4 zv = __ldg(reinterpret_cast<const uint4*>(zi + (int64_t)j * p.cz + f8));
-        const uint32_t w[4] = {zv.x, zv.y, zv.z, zv.w};
-        const float aj = a[j];
+    for (int k = 0; k < kB; ++k) {
+      const int e = tid + k * kProbThreads, r = e / (kIpaD / 8), d8 = e % (kIpaD / 8);
+      if (r < kProbRows) {
+        const uint32_t w[4] = {tmp[k].x, tmp[k].y, tmp[k].z, tmp[k].w};
 #pragma unroll
         for (int x = 0; x < 4; ++x) {
-          acc[2 * x] = fmaf(aj, bf16_lo(w[x]), acc[2 * x]);
-          acc[2 * x + 1] = fmaf(aj, bf16_hi(w[x]), acc[2 * x + 1]);
+          qs[r][d8 * 8 + 2 * x] = bf16_lo(w[x]);
+          qs[r][d8 * 8 + 2 * x + 1] = bf16_hi(w[x]);
         }
       }
     }
-#pragma unroll
-    for (int x = 0; x < 8; ++x) red[part * 128 + (tid % 16) * 8 + x] = acc[x];
-    __syncthreads();
-    if (fb + tid < p.cz) {
-      float v = 0.f;
-#pragma unroll
-      for (int q8 = 0; q8 < 8; ++q8) v += red[q8 * 128 + tid];
-      opair[((int64_t)i * p.H + h) * p.cz + fb + tid] = __float2bfloat16_rn(v);
-    }
-    __syncthreads();
   }
-  // ---- point output: thread -> (float4 of the <= 24 sums, j-partition), reduced in shared memory
-  const int PV3 = p.Pv * 3;
-  const int64_t jstride = (int64_t)p.H * PV3;
-  constexpr int kPtParts = kIpaThreads / 6;        // 21
-  if (tid < 6 * kPtParts) {
-    const int f4 = tid % 6, part = tid / 6;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (f4 * 4 < PV3) {
-      const float* gj = p.gv + (int64_t)h * PV3 + f4 * 4;
-#pragma unroll 4
-      for (int j = part; j < p.N; j += kPtParts) {
-        const float4 g4 = __ldg(reinterpret_cast<const float4*>(gj + (int64_t)j * jstride));
-        const float aj = a[j];
-        acc.x = fmaf(aj, g4.x, acc.x);
-        acc.y = fmaf(aj, g4.y, acc.y);
-        acc.z = fmaf(aj, g4.z, acc.z);
-        acc.w = fmaf(aj, g4.w, acc.w);
+  if (tid < kProbRows) ls[tid] = tid < nr ? lse[(int64_t)h * p.N + i0 + tid] : 0.f;   // lse [1, H, N] (G19)
+  const int pr_r = tid / 6, pr_f4 = tid % 6;       // point sums: threads < 96
+  const bool pt_on = tid < kProbRows * 6 && pr_r < nr && pr_f4 * 4 < PV3;
+  float4 pacc = make_float4(0.f, 0.f, 0.f, 0.f);
+  __syncthreads();
+  for (int j0 = 0; j0 < p.N; j0 += kJC) {
+    const int cnt = min(kJC, p.N - j0);
+    {                                               // the chunk's g_jp^h (<= 6 float4 per key), loads batched
+      constexpr int kB = kJC * 6 / kProbThreads;    // 12
+      const int nq = PV3 / 4, n4 = cnt * nq;
+      float4 tmp[kB];
+#pragma unroll
+      for (int k = 0; k < kB; ++k) {
+        const int e = tid + k * kProbThreads;
+        if (e < n4)
+          tmp[k] = __ldg(reinterpret_cast<const float4*>(p.gv + ((int64_t)(j0 + e / nq) * p.H + h) * PV3) + e % nq);
+      }
+#pragma unroll
+      for (int k = 0; k < kB; ++k) {
+        const int e = tid + k * kProbThreads;
+        if (e < n4) *reinterpret_cast<float4*>(gs + (e / nq) * 24 + (e % nq) * 4) = tmp[k];
       }
     }
-    reinterpret_cast<float4*>(red)[part * 6 + f4] = acc;
+    for (int jj = tid; jj < cnt; jj += kProbThreads) {
+      const int j = j0 + jj;
+      const uint4* kr = reinterpret_cast<const uint4*>(p.ka + ((int64_t)j * p.H + h) * kIpaD);
+      uint4 u[8];
+#pragma unroll
+      for (int d = 0; d < 8; ++d) u[d] = __ldg(kr + d);
+      float bv[kProbRows];                          // the rows' biases, all in flight at once
+#pragma unroll
+      for (int r = 0; r < kProbRows; ++r)
+        bv[r] = r < nr ? __bfloat162float(p.bias_s[((int64_t)h * p.N + i0 + r) * p.N + j]) : 0.f;
+#pragma unroll
+      for (int r = 0; r < kProbRows; ++r) {
+        float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {
+          const uint32_t w[4] = {u[d].x, u[d].y, u[d].z, u[d].w};
+          const float4 qa = *reinterpret_cast<const float4*>(&qs[r][d * 8]);
+          const float4 qb = *reinterpret_cast<const float4*>(&qs[r][d * 8 + 4]);
+          s0 = fmaf(qa.x, bf16_lo(w[0]), s0);
+          s1 = fmaf(qa.y, bf16_hi(w[0]), s1);
+          s0 = fmaf(qa.z, bf16_lo(w[1]), s0);
+          s1 = fmaf(qa.w, bf16_hi(w[1]), s1);
+          s0 = fmaf(qb.x, bf16_lo(w[2]), s0);
+          s1 = fmaf(qb.y, bf16_hi(w[2]), s1);
+          s0 = fmaf(qb.z, bf16_lo(w[3]), s0);
+          s1 = fmaf(qb.w, bf16_hi(w[3]), s1);
+        }
+        const float av = r < nr ? __expf(s0 + s1 + bv[r] - ls[r]) : 0.f;
+        as[r * kJC + jj] = av;
+        if (r < nr) A[((int64_t)h * p.N + i0 + r) * p.N + j] = av;
+      }
+    }
+    __syncthreads();
+    if (pt_on) {
+      const float* ar = as + pr_r * kJC;
+#pragma unroll 4
+      for (int jj = 0; jj < cnt; ++jj) {
+        const float aj = ar[jj];
+        const float4 g4 = *reinterpret_cast<const float4*>(gs + jj * 24 + pr_f4 * 4);
+        pacc.x = fmaf(aj, g4.x, pacc.x);
+        pacc.y = fmaf(aj, g4.y, pacc.y);
+        pacc.z = fmaf(aj, g4.z, pacc.z);
+        pacc.w = fmaf(aj, g4.w, pacc.w);
+      }
+    }
+    __syncthreads();
   }
+  if (PV3 == 0) return;
+  if (pt_on) *reinterpret_cast<float4*>(gsum + pr_r * 24 + pr_f4 * 4) = pacc;
   __syncthreads();
-  if (tid < PV3) {
-    float v = 0.f;
-    for (int part = 0; part < kPtParts; ++part) v += red[part * 24 + tid];
-    gs[tid] = v;
-  }
-  __syncthreads();
-  if (tid < p.Pv) {
-    const float* g = gs + tid * 3;
+  for (int e = tid; e < nr * p.Pv; e += kProbThreads) {
+    const int r = e / p.Pv, pp = e % p.Pv, i = i0 + r;
+    const float* g = gsum + r * 24 + pp * 3;
     const float* R = p.R + i * 9;
     const float* t = p.t + i * 3;
     for (int x = 0; x < 3; ++x)
-      op[(((int64_t)i * p.H + h) * p.Pv + tid) * 3 + x] =
+      op[(((int64_t)i * p.H + h) * p.Pv + pp) * 3 + x] =
           R[0 * 3 + x] * (g[0] - t[0]) + R[1 * 3 + x] * (g[1] - t[1]) + R[2 * 3 + x] * (g[2] - t[2]);
+  }
+}
+
+// One CTA per (row i, group of kOutHG heads): z_i (the row's N x c_z pair features) is streamed once for
+// the group's heads, opair_i^h = sum_j a_ij^h z_ij (thread = 8 consecutive features x one of 16
+// j-partitions).  The group's a_i^h [kOutHG][N] is staged in shared memory.
+constexpr int kOutThreads = 256;
+constexpr int kOutHG = 6;                          // heads per pass over z_i (6 x 8 accumulators)
+__global__ void __launch_bounds__(kOutThreads) ipa_out_kernel(const IpaParams p, const float* __restrict__ A,
+                                                              __nv_bfloat16* __restrict__ opair) {
+  extern __shared__ __align__(16) float ipa_smem[];
+  float* a = ipa_smem;                             // [kOutHG][N]
+  float* red = a + (((int64_t)kOutHG * p.N + 3) & ~3);   // [8 warps][kOutHG][128] / point partials
+  const int i = blockIdx.x, hg = blockIdx.y * kOutHG, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ng = min(kOutHG, p.H - hg);
+  for (int e0 = 0; e0 < ng * p.N; e0 += 8 * kOutThreads) {   // 8 loads in flight per thread
+    float tmp[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int e = e0 + tid + k * kOutThreads;
+      if (e < ng * p.N) tmp[k] = __ldg(A + ((int64_t)(hg + e / p.N) * p.N + i) * p.N + e % p.N);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int e = e0 + tid + k * kOutThreads;
+      if (e < ng * p.N) a[e] = tmp[k];
+    }
+  }
+  __syncthreads();
+  // ---- pair output
+  const __nv_bfloat16* zi = p.z + (int64_t)i * p.N * p.cz;
+  const int fl8 = (tid & 15) * 8, part = tid >> 4;   // 16 j-partitions; lanes l, l ^ 16 hold parts 2w, 2w + 1
+  for (int fb = 0; fb < p.cz; fb += 128) {
+    const int f8 = fb + fl8;
+    {
+      const int h0 = 0, nh = ng;                   // local head index; global head = hg + local
+      float acc[kOutHG][8];
+#pragma unroll
+      for (int hh = 0; hh < kOutHG; ++hh)
+#pragma unroll
+        for (int x = 0; x < 8; ++x) acc[hh][x] = 0.f;
+      if (f8 < p.cz) {
+#pragma unroll 6
+        for (int j = part; j < p.N; j += 16) {
+          const uint4 zv = __ldg(reinterpret_cast<const uint4*>(zi + (int64_t)j * p.cz + f8));
+          const uint32_t w[4] = {zv.x, zv.y, zv.z, zv.w};
+#pragma unroll
+          for (int hh = 0; hh < kOutHG; ++hh) {
+            const float aj = hh < nh ? a[(h0 + hh) * p.N + j] : 0.f;
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+              acc[hh][2 * x] = fmaf(aj, bf16_lo(w[x]), acc[hh][2 * x]);
+              acc[hh][2 * x + 1] = fmaf(aj, bf16_hi(w[x]), acc[hh][2 * x + 1]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int hh = 0; hh < kOutHG; ++hh)
+#pragma unroll
+        for (int x = 0; x < 8; ++x) acc[hh][x] += __shfl_xor_sync(0xffffffffu, acc[hh][x], 16);
+      if (lane < 16)
+#pragma unroll
+        for (int hh = 0; hh < kOutHG; ++hh)
+#pragma unroll
+          for (int x = 0; x < 8; ++x) red[(warp * kOutHG + hh) * 128 + fl8 + x] = acc[hh][x];
+      __syncthreads();
+      for (int e = tid; e < nh * 128; e += kOutThreads) {
+        const int hh = e / 128, f = e % 128;
+        if (fb + f < p.cz) {
+          float v = 0.f;
+#pragma unroll
+          for (int w2 = 0; w2 < kOutThreads / 32; ++w2) v += red[(w2 * kOutHG + hh) * 128 + f];
+          opair[((int64_t)i * p.H + hg + h0 + hh) * p.cz + fb + f] = __float2bfloat16_rn(v);
+        }
+      }
+      __syncthreads();
+    }
   }
 }
 
@@ -209,11 +306,23 @@ cudaError_t launch_ipa_prep(const IpaParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_ipa_finish(const IpaParams& p, const float* lse, void* opair, float* op, cudaStream_t s) {
-  const int smem = (((p.N + kIpaD + kIpaParts * 24 + 3) & ~3) + 8 * 128) * 4;
-  cudaError_t e = cudaFuncSetAttribute(ipa_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+size_t ipa_out_smem(const IpaParams& p) {
+  return ((((size_t)kOutHG * p.N + 3) & ~size_t(3)) + (size_t)(kOutThreads / 32) * kOutHG * 128) * 4;
+}
+
+cudaError_t launch_ipa_finish(const IpaParams& p, const float* lse, float* A, void* opair, float* op, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(ipa_probs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)ipa_probs_smem());
   if (e != cudaSuccess) return e;
-  ipa_finish_kernel<<<p.N * p.H, kIpaThreads, smem, s>>>(p, lse, static_cast<__nv_bfloat16*>(opair), op);
+  ipa_probs_kernel<<<dim3((p.N + kProbRows - 1) / kProbRows, p.H), kProbThreads, ipa_probs_smem(), s>>>(p, lse, A, op);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const size_t smem = ipa_out_smem(p);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  e = cudaFuncSetAttribute(ipa_out_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  ipa_out_kernel<<<dim3(p.N, (p.H + kOutHG - 1) / kOutHG), kOutThreads, smem, s>>>(
+      p, A, static_cast<__nv_bfloat16*>(opair));
   return cudaGetLastError();
 }
 
