@@ -18,12 +18,20 @@ from tests.parity import check
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("N", [100, 300])
-def test_ipa_vs_oracle(N):
+IPA_CASES = [dict(N=100), dict(N=300),
+             # ragged row block (77 % 16), one head group of 5, 4 value points, c_z = 64 (half the feature lanes)
+             dict(N=77, H=5, Pv=4, cz=64),
+             # three key chunks (520 = 2 x 256 + 8), head groups 6 + 1, c_z = 192 (two feature passes)
+             dict(N=520, H=7, cz=192)]
+
+
+@pytest.mark.parametrize("case", IPA_CASES, ids=lambda c: "_".join(f"{k}{v}" for k, v in c.items()))
+def test_ipa_vs_oracle(case):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2511_02043_b200 import fl
-    x = synth.ipa_inputs(N, seed=N)
+    N = case["N"]
+    x = synth.ipa_inputs(seed=N, **case)
     dev = {k: v.cuda() for k, v in x.items()}
     o, op, opair = fl.ipa_fwd(**dev)
     torch.cuda.synchronize()
@@ -50,3 +58,13 @@ def test_ipa_global_motion_invariance_on_gpu():
     assert (a[0].float() - b[0].float()).abs().max().item() < 2e-2
     assert (a[2].float() - b[2].float()).abs().max().item() < 2e-2
     assert (a[1] - b[1]).abs().max().item() < 2 ** -7 * (float(y["t"].abs().max()) + 7)
+
+
+def test_ipa_unsupported_is_loud():
+    """P_v outside {0, 4, 8} (the float4 point sums) is refused with FL_ERR_UNSUPPORTED, not computed wrongly."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2511_02043_b200 import fl
+    x = synth.ipa_inputs(40, Pv=3, seed=1)
+    with pytest.raises(fl.FlError, match="UNSUPPORTED"):
+        fl.ipa_fwd(**{k: v.cuda() for k, v in x.items()})
