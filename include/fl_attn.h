@@ -147,7 +147,8 @@ typedef struct {
  * Launches per call: 1 attention kernel (2 on the split-KV path), +1 key-mask pack kernel when a
  * key mask is given, + a 4-byte stream-ordered memset of the scheduler counter (bf16).
  * Empty work (B*G*Hq*S_q == 0) returns FL_OK without a launch; S_k == 0 gives O = 0,
- * lse = -inf (G7); a fully masked row likewise gives O = 0, lse = -inf. */
+ * lse = -inf (G7); a fully masked row likewise gives O = 0, lse = -inf.  A tensor with zero elements
+ * may carry data == NULL. */
 fl_status fl_attn_fwd(const fl_attn_args* args);
 
 /* ---- backward (the training half, §2.4) ------------------------------
@@ -165,7 +166,8 @@ fl_status fl_attn_fwd(const fl_attn_args* args);
  * Diff: the forward keeps neither map's output, so the call recomputes both maps (o_i, lse_i: the forward
  * kernel per map), seeds map 1 with -lambda_h dO, runs the single-map backward per map and sums dV (and
  * dgate) over the maps; lse must be absent, o (the diff output) is validated but not read, and the workspace
- * holds o_0, o_1, lse_0, lse_1, dO_1, dV_1 (+ dgate_1) plus one forward and one backward workspace. */
+ * holds o_0, o_1, lse_0, lse_1 and dO_1 plus one forward and one backward workspace.
+ * Degenerate shapes: no queries -> dK = dV = 0; no keys -> dQ = 0 and dgate = 0 (zero-fill launches). */
 typedef struct {
   fl_tensor q, k, v, o;      /* the forward's inputs and output (bf16) */
   fl_tensor lse;             /* the forward's LSE, f32 [B, Hq, S_q] (required) */

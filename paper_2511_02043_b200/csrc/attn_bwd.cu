@@ -187,6 +187,20 @@ __global__ void __launch_bounds__(256) diff_bwd_seed_kernel(const AttnParams p, 
   }
 }
 
+// Zero a strided [B, G, H, S, D] bf16 view (contiguous last dim): the gradients the kernels never visit
+// when the problem has no queries (dK, dV) or no keys (dQ, dgate).  One thread per 8 elements.
+__global__ void zero_rows_kernel(__nv_bfloat16* __restrict__ dst, Strided5 ds, int B, int G, int H, int S, int D) {
+  const int64_t n8 = (int64_t)B * G * H * S * (D / 8);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n8; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c8 = (int)(e % (D / 8));
+    const int64_t row = e / (D / 8);
+    const int q = (int)(row % S);
+    const int64_t bgh = row / S;
+    const int h = (int)(bgh % H), g = (int)((bgh / H) % G), b = (int)(bgh / ((int64_t)H * G));
+    *reinterpret_cast<uint4*>(dst + b * ds.b + g * ds.g + h * ds.h + q * ds.s + c8 * 8) = make_uint4(0u, 0u, 0u, 0u);
+  }
+}
+
 // ---------------------------------------------------------------- shared configuration
 template <int D>
 struct BwdCfg {
@@ -852,6 +866,14 @@ cudaError_t launch_bwd_prepass(const AttnParams& p, const void* dout, Strided5 d
         static_cast<__nv_bfloat16*>(dgate), dgs, dvec, static_cast<const __nv_bfloat16*>(aun));
   else
     bwd_dvec_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(p, static_cast<const __nv_bfloat16*>(dout), dos, dvec);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_zero_rows(void* dst, Strided5 ds, int B, int G, int H, int S, int D, cudaStream_t s) {
+  const int64_t n8 = (int64_t)B * G * H * S * (D / 8);
+  if (n8 == 0) return cudaSuccess;
+  zero_rows_kernel<<<(unsigned)std::min<int64_t>((n8 + 255) / 256, 4 * 148), 256, 0, s>>>(
+      static_cast<__nv_bfloat16*>(dst), ds, B, G, H, S, D);
   return cudaGetLastError();
 }
 

@@ -47,6 +47,7 @@ cudaError_t launch_sched_dump(const AttnParams& p, int32_t* out, int64_t out_wor
                               int32_t* max_tiles, cudaStream_t stream);
 cudaError_t launch_bwd_prepass(const AttnParams& p, const void* dout, Strided5 dos, float* dvec, void* da, void* dgate,
                                Strided5 dgs, const void* aun, cudaStream_t s);
+cudaError_t launch_zero_rows(void* dst, Strided5 ds, int B, int G, int H, int S, int D, cudaStream_t s);
 cudaError_t launch_diff_bwd_seed(const AttnParams& p, const void* dout, Strided5 dos, const void* o1, void* do1,
                                  float* dlambda, cudaStream_t s);
 cudaError_t launch_attn_bwd(const AttnParams& p, const TmaMaps& maps, const CUtensorMap& tdo, const CUtensorMap& tq64,
@@ -127,9 +128,18 @@ int elem_bytes(int dtype) { return dtype == FL_F32 || dtype == FL_I32 ? 4 : dtyp
 
 // Map a rank-(base) or rank-(base+1) tensor onto slots; `slots` lists the View5
 // slot of each dim of the rank-(base+1) form (the G dim is slot 1).
+// A tensor argument is given when it has data, or when it has no elements (torch hands out NULL for those).
+bool given(const fl_tensor& t) {
+  if (t.data) return true;
+  if (t.rank <= 0 || t.rank > 5) return false;
+  for (int d = 0; d < t.rank; ++d)
+    if (t.size[d] == 0) return true;
+  return false;
+}
+
 bool to_view(const fl_tensor& t, int q_rank, int rank_delta, View5& v) {
   v = View5();
-  if (!t.data) return true;
+  if (!given(t)) return true;                 // absent (an empty tensor with NULL data is present, 0 elements)
   if (t.rank != q_rank + rank_delta) return false;
   v.present = true;
   v.data = t.data;
@@ -259,7 +269,7 @@ fl_status prepare(const fl_attn_args* a, Prepared& P, bool device_ptrs) {
   const fl_variant& var = a->var;
   if (var.abi_version != FL_ABI_VERSION)
     return fail(FL_ERR_ABI_VERSION, "abi_version %u != %d", var.abi_version, FL_ABI_VERSION);
-  if (!a->q.data || !a->k.data || !a->v.data || !a->o.data)
+  if (!given(a->q) || !given(a->k) || !given(a->v) || !given(a->o))
     return fail(FL_ERR_INVALID_ARGUMENT, "q, k, v and o are required");
   const int R = a->q.rank;
   if (R != 4 && R != 5) return fail(FL_ERR_INVALID_ARGUMENT, "q rank must be 4 or 5");
@@ -787,13 +797,13 @@ fl_status prepare_bwd(const fl_attn_bwd_args* a, BwdPrepared& B, bool device_ptr
   if (p.Dqk != 32 && p.Dqk != 64 && p.Dqk != 128) return fail(FL_ERR_UNSUPPORTED, "backward: D in {32, 64, 128}");
   if (var.diff || var.kv_page_table.data || var.mask == FL_MASK_BLOCKLIST)
     return fail(FL_ERR_UNSUPPORTED, "backward: no block list / paged KV");
-  if (!a->lse.data) return fail(FL_ERR_INVALID_ARGUMENT, "backward needs the forward's lse");
+  if (!a->lse.data && !B.P.empty_work) return fail(FL_ERR_INVALID_ARGUMENT, "backward needs the forward's lse");
   const int R = B.P.q_rank;
   const fl_tensor* ts[4] = {&a->dout, &a->dq, &a->dk, &a->dv};
   View5* vs[4] = {&B.dout, &B.dq, &B.dk, &B.dv};
   const View5* like[4] = {&B.P.o, &B.P.q, &B.P.k, &B.P.v};
   for (int i = 0; i < 4; ++i) {
-    if (!ts[i]->data || ts[i]->dtype != FL_BF16) return fail(FL_ERR_INVALID_ARGUMENT, "dout / dq / dk / dv: bf16, required");
+    if (!given(*ts[i]) || ts[i]->dtype != FL_BF16) return fail(FL_ERR_INVALID_ARGUMENT, "dout / dq / dk / dv: bf16, required");
     if (!to_view(*ts[i], R, 0, *vs[i])) return fail(FL_ERR_SHAPE_MISMATCH, "dout / dq / dk / dv must have q's rank");
     for (int d = 0; d < 5; ++d)
       if (vs[i]->size[d] != like[i]->size[d]) return fail(FL_ERR_SHAPE_MISMATCH, "dout / dq / dk / dv shapes must match o / q / k / v");
@@ -882,7 +892,7 @@ fl_status bwd_single(const fl_attn_bwd_args* args, bool grad_accum = false);
 //   4. bwd(map 1, dO_1) -> dq[:, H:], dk[:, Hkv:]; dv += (fp32 add in the dK/dV epilogue), dgate += (pre-pass)
 fl_tensor head_slice(fl_tensor t, int64_t h0, int64_t nh) {
   const int hd = t.rank - 3;
-  t.data = static_cast<char*>(t.data) + h0 * t.stride[hd] * elem_bytes(t.dtype);
+  if (t.data) t.data = static_cast<char*>(t.data) + h0 * t.stride[hd] * elem_bytes(t.dtype);   // (NULL: empty)
   t.size[hd] = nh;
   return t;
 }
@@ -999,7 +1009,11 @@ fl_status bwd_diff(const fl_attn_bwd_args* a) {
     cudaError_t e = cudaMemsetAsync(a->dlambda.data, 0, (size_t)D.seed.Hq * sizeof(float), stream);
     if (e != cudaSuccess) return cuda_fail(e, "dlambda reset");
   }
-  if (D.empty) return FL_OK;
+  if (D.empty) {                                     // no queries: the per-map calls zero dK, dV
+    for (int m = 0; m < 2; ++m)
+      if ((s = bwd_single(&D.bwd[m], m == 1)) != FL_OK) return s;
+    return FL_OK;
+  }
   for (int m = 0; m < 2; ++m) {                      // 1. the maps' outputs and LSEs
     Prepared P;
     if ((s = prepare(&D.fwd[m], P, true)) != FL_OK) return s;
@@ -1045,10 +1059,28 @@ fl_status bwd_single(const fl_attn_bwd_args* args, bool grad_accum) {
   fl_status s = prepare_bwd(args, B, true);
   if (s != FL_OK) return s;
   B.P.p.grad_accum = grad_accum ? 1 : 0;
-  if (B.P.empty_work) return FL_OK;
+  cudaStream_t stream = static_cast<cudaStream_t>(args->stream);
+  if (B.P.empty_work || B.P.no_keys) {
+    // no queries: dK = dV = 0; no keys: O = 0 (G7), so dQ = 0 and dgate = 0 (dK, dV, dbias are empty)
+    const AttnParams& p = B.P.p;
+    cudaError_t e = cudaSuccess;
+    auto zero = [&](const View5& v, int H, int S, int D, bool shared) {   // shared: summed over diff maps
+      if (e == cudaSuccess && v.present && !(shared && grad_accum)) {
+        e = launch_zero_rows(v.data, strides_of(v), p.B, p.G, H, S, D, stream);
+        ++g_launches;
+      }
+    };
+    if (B.P.empty_work) {
+      zero(B.dk, p.Hkv, p.Sk, p.Dqk, false);
+      zero(B.dv, p.Hkv, p.Sk, p.Dv, true);
+    } else {
+      zero(B.dq, p.Hq, p.Sq, p.Dqk, false);
+      zero(B.dgate, p.Hq, p.Sq, p.Dv, true);
+    }
+    return e == cudaSuccess ? FL_OK : cuda_fail(e, "gradient zero fill");
+  }
   if (!args->workspace || args->workspace_bytes < B.ws)
     return fail(FL_ERR_WORKSPACE, "the backward needs %zu bytes of workspace", B.ws);
-  cudaStream_t stream = static_cast<cudaStream_t>(args->stream);
   char* ws = static_cast<char*>(args->workspace);
   AttnParams& p = B.P.p;
   TmaMaps maps;

@@ -211,3 +211,36 @@ def test_backward_diff_unsupported_is_loud(fl):
         fl.attn_bwd(q, q, v, o, None, o.clone(), diff=True, lam=0.3, diff_norm=True, diff_norm_eps=1e-5)
     with pytest.raises(fl.FlError):
         fl.attn_bwd(q, q, v, o, torch.zeros(1, 2, 128, device="cuda"), o.clone(), diff=True, lam=0.3)
+
+
+def test_backward_degenerate_shapes(fl):
+    """Edge cases of the definition: no queries -> dK = dV = 0; no keys -> O = 0 (G7), so dQ = 0 and dgate = 0.
+    The gradient buffers start as NaN so an unwritten gradient fails."""
+    bf = torch.bfloat16
+    nan = lambda *s: torch.full(s, float("nan"), device="cuda", dtype=bf)
+    # S_q = 0
+    q = torch.zeros(1, 2, 0, 64, device="cuda", dtype=bf)
+    k = torch.rand(1, 2, 50, 64, device="cuda", dtype=bf)
+    o, lse = fl.attn_fwd(q, k, k, return_lse=True)
+    dq, dk, dv = fl.attn_bwd(q, k, k, o, lse, o.clone(), dq=torch.empty_like(q), dk=nan(1, 2, 50, 64), dv=nan(1, 2, 50, 64))
+    torch.cuda.synchronize()
+    assert dk.abs().max().item() == 0 and dv.abs().max().item() == 0
+    # S_k = 0, sigmoid gate
+    q = torch.rand(1, 2, 40, 64, device="cuda", dtype=bf)
+    k = torch.zeros(1, 2, 0, 64, device="cuda", dtype=bf)
+    g = torch.rand(1, 2, 40, 64, device="cuda", dtype=bf)
+    o, lse = fl.attn_fwd(q, k, k, return_lse=True, gate_mode="sigmoid", gate=g)
+    assert o.abs().max().item() == 0
+    dq, dk, dv, dg = fl.attn_bwd(q, k, k, o, lse, torch.rand_like(o), dq=nan(1, 2, 40, 64), dgate=nan(1, 2, 40, 64),
+                                 gate_mode="sigmoid", gate=g)
+    torch.cuda.synchronize()
+    assert dq.abs().max().item() == 0 and dg.abs().max().item() == 0
+    # differential attention, S_q = 0: both maps' dK slices and the shared dV are zeroed
+    q = torch.zeros(1, 4, 0, 64, device="cuda", dtype=bf)
+    k = torch.rand(1, 4, 30, 64, device="cuda", dtype=bf)
+    v = torch.rand(1, 2, 30, 64, device="cuda", dtype=bf)
+    o = fl.attn_fwd(q, k, v, diff=True, lam=0.3)
+    dq, dk, dv = fl.attn_bwd(q, k, v, o, None, o.clone(), dq=torch.empty_like(q), dk=nan(1, 4, 30, 64),
+                             dv=nan(1, 2, 30, 64), diff=True, lam=0.3)
+    torch.cuda.synchronize()
+    assert dk.abs().max().item() == 0 and dv.abs().max().item() == 0
