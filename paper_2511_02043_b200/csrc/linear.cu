@@ -35,7 +35,8 @@ __global__ void __launch_bounds__(kLinThreads, 1)
   uint8_t* sX = smem;                                  // [nkc][128 rows x 128 B]
   uint8_t* sW = smem + nkc * 128 * 128;                // [2][nkc][kWSlab]
   uint8_t* sY = sW + 2 * nkc * kWSlab;                // output staging for the TMA store: 2 slabs of 128 x 64
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sY + 2 * 128 * 128);
+  float* sBias = reinterpret_cast<float*>(sY + 2 * 128 * 128);   // [2][128]: the bias of tile nt (parity nt & 1)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sBias + 2 * 128);
   uint64_t* x_full = bars;
   uint64_t* ln_done = bars + 1;
   uint64_t* w_full = bars + 2;                         // [2]
@@ -167,8 +168,15 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     const bool y_co = false;
 #endif
     const bool stage = y_tma || y_co;
+    // the tile's bias in shared memory: thread r fetches column r of tile nt + 1 while tile nt is processed
+    // (a per-chunk global load stalled the epilogue on its latency: 19 % of the samples)
+    auto bias_of = [&](int nt2) { const int n = nt2 * p.NT + r; return (p.bias && r < p.NT && n < p.N) ? __ldg(p.bias + n) : 0.f; };
+    sBias[r] = bias_of(0);
+    float bias_next = n_nt > 1 ? bias_of(1) : 0.f;
+    named_bar_sync(2, 128);
     for (int nt = 0; nt < n_nt; ++nt) {
       const int b = nt & 1, n0 = nt * p.NT;
+      const float* sb = sBias + b * 128;
       mbar_wait(&acc_full[b], (nt >> 1) & 1);
       tc_fence_after();
       for (int c = 0; c < p.NT; c += 32) {
@@ -176,22 +184,13 @@ __global__ void __launch_bounds__(kLinThreads, 1)
         tmem_ld32(tmem + lane_base + b * 128 + c, acc);   // every lane loads (.sync.aligned)
         tmem_wait_ld();
         float f[32];
-        if (p.bias && n0 + c + 32 <= p.N && ((reinterpret_cast<uintptr_t>(p.bias + n0 + c) & 15) == 0)) {
-          const float4* b4 = reinterpret_cast<const float4*>(p.bias + n0 + c);   // 8 vector loads, not 32
 #pragma unroll
-          for (int t4 = 0; t4 < 8; ++t4) {
-            const float4 bb = __ldg(b4 + t4);
-            f[4 * t4] = __uint_as_float(acc[4 * t4]) + bb.x;
-            f[4 * t4 + 1] = __uint_as_float(acc[4 * t4 + 1]) + bb.y;
-            f[4 * t4 + 2] = __uint_as_float(acc[4 * t4 + 2]) + bb.z;
-            f[4 * t4 + 3] = __uint_as_float(acc[4 * t4 + 3]) + bb.w;
-          }
-        } else {
-#pragma unroll
-          for (int t = 0; t < 32; ++t) {
-            const int n = n0 + c + t;
-            f[t] = __uint_as_float(acc[t]) + ((p.bias && n < p.N) ? __ldg(p.bias + n) : 0.f);
-          }
+        for (int t4 = 0; t4 < 8; ++t4) {
+          const float4 bb = *reinterpret_cast<const float4*>(sb + c + 4 * t4);   // broadcast
+          f[4 * t4] = __uint_as_float(acc[4 * t4]) + bb.x;
+          f[4 * t4 + 1] = __uint_as_float(acc[4 * t4 + 1]) + bb.y;
+          f[4 * t4 + 2] = __uint_as_float(acc[4 * t4 + 2]) + bb.z;
+          f[4 * t4 + 3] = __uint_as_float(acc[4 * t4 + 3]) + bb.w;
         }
         if (stage) {
           // swizzled staging (slab c / 64, 16-B chunk q of row r at (q ^ (r & 7)) * 16): conflict-free; one
@@ -221,6 +220,11 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&acc_empty[b]);                      // the accumulator may take tile nt + 2
+      if (nt + 1 < n_nt) {                             // publish tile nt + 1's bias, fetch tile nt + 2's
+        sBias[((nt + 1) & 1) * 128 + r] = bias_next;
+        bias_next = nt + 2 < n_nt ? bias_of(nt + 2) : 0.f;
+        named_bar_sync(2, 128);
+      }
       if (y_co) {
         named_bar_sync(1, 128);                        // the tile is staged
 #pragma unroll 4
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
   if (warp == 4) tmem_dealloc<256>(tmem);
 }
 
-int linear_smem_bytes(int K) { return (K / 64) * 128 * 128 * 3 + 2 * 128 * 128 + 128 + 1024; }
+int linear_smem_bytes(int K) { return (K / 64) * 128 * 128 * 3 + 2 * 128 * 128 + 2 * 128 * 4 + 128 + 1024; }
 
 cudaError_t launch_linear(const LinParams& p, const CUtensorMap& tx, const CUtensorMap& tw, const CUtensorMap& ty,
                           int y_tma, cudaStream_t stream) {
