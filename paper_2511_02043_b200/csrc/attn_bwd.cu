@@ -201,6 +201,11 @@ __global__ void zero_rows_kernel(__nv_bfloat16* __restrict__ dst, Strided5 ds, i
   }
 }
 
+template <bool B>
+struct BoolTag {
+  static constexpr bool value = B;
+};
+
 // ---------------------------------------------------------------- shared configuration
 template <int D>
 struct BwdCfg {
@@ -470,26 +475,34 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tmem_wait_ld();
         // P^T (bf16 pairs) and the softcap factor, query q0 + j = column j
         uint32_t pk[32], fk[32];
+        // mask-free items (every element kept) take a loop without the per-element interval test
+        auto p_loop = [&](auto fast_tag) {
+          constexpr bool kFast = decltype(fast_tag)::value;
 #pragma unroll
-        for (int j = 0; j < 64; j += 4) {
-          const float4 lse4 = *reinterpret_cast<const float4*>(rl + j);
-          const float lsev[4] = {lse4.x, lse4.y, lse4.z, lse4.w};
-          float pr[4], f[4];
+          for (int j = 0; j < 64; j += 4) {
+            const float4 lse4 = *reinterpret_cast<const float4*>(rl + j);
+            const float lsev[4] = {lse4.x, lse4.y, lse4.z, lse4.w};
+            float pr[4], f[4];
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int q = q0 + j + t;
-            float ft;
-            const bool keep = key_on && (full_tile || (k >= riv[j + t] && k < riv[64 + j + t]));   // hi <= S_k
-            const float bv = (BIAS && keep) ? bias_at(p, b, g, hh, q, k) : 0.f;
-            const float s = bwd_score<MOD>(p, __uint_as_float(sv[j + t]), slope_l2, k, q + p.q_off, ft, bv);
-            pr[t] = keep ? ex2(fmaf(s, kBwdLog2e, -lsev[t])) : 0.f;
-            f[t] = ft;
+            for (int t = 0; t < 4; ++t) {
+              const int q = q0 + j + t;
+              float ft;
+              const bool keep = kFast || (key_on && (full_tile || (k >= riv[j + t] && k < riv[64 + j + t])));   // hi <= S_k
+              const float bv = (BIAS && keep) ? bias_at(p, b, g, hh, q, k) : 0.f;
+              const float s = bwd_score<MOD>(p, __uint_as_float(sv[j + t]), slope_l2, k, q + p.q_off, ft, bv);
+              pr[t] = keep ? ex2(fmaf(s, kBwdLog2e, -lsev[t])) : 0.f;
+              f[t] = ft;
+            }
+            pk[j >> 1] = pack_bf16(pr[0], pr[1]);
+            pk[(j >> 1) + 1] = pack_bf16(pr[2], pr[3]);
+            fk[j >> 1] = pack_bf16(f[0], f[1]);
+            fk[(j >> 1) + 1] = pack_bf16(f[2], f[3]);
           }
-          pk[j >> 1] = pack_bf16(pr[0], pr[1]);
-          pk[(j >> 1) + 1] = pack_bf16(pr[2], pr[3]);
-          fk[j >> 1] = pack_bf16(f[0], f[1]);
-          fk[(j >> 1) + 1] = pack_bf16(f[2], f[3]);
-        }
+        };
+        if (full_tile && key_on)
+          p_loop(BoolTag<true>{});
+        else
+          p_loop(BoolTag<false>{});
         tmem_st32(tmem + lane_base + col_s + 32, &pk[0]);
         // dS^T = P^T (dP^T - Dvec) * f, 32 queries at a time, into slot + [0, 32) (S^T is consumed)
 #pragma unroll
@@ -726,23 +739,34 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tmem_ld32(tmem + lane_base + col_s + 32, &sv[32]);
       tmem_wait_ld();
       uint32_t pk[32], fk[32];
+      // mask-free items (full tile, no masked key) take a loop without the per-element key / interval tests
+      auto p_loop = [&](auto fast_tag) {
+        constexpr bool kFast = decltype(fast_tag)::value;
 #pragma unroll
-      for (int j = 0; j < 64; j += 2) {
-        float pr[2], f[2];
+        for (int j = 0; j < 64; j += 2) {
+          float pr[2], f[2];
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          const int k = kh0 + j + t;
-          float ft;
-          const bool kon = (((j + t) < 32 ? kw0 : kw1) >> ((j + t) & 31)) & 1u;
-          const bool keep = kon && (full_tile || (k >= iv.lo && k < iv.hi && k < p.Sk));
-          const float bv = (BIAS && keep) ? bias_at(p, b, g, h, q, k) : 0.f;
-          const float sc = bwd_score<MOD>(p, __uint_as_float(sv[j + t]), slope_l2, k, q_abs, ft, bv);
-          pr[t] = keep ? ex2(fmaf(sc, kBwdLog2e, -lse_l2)) : 0.f;
-          f[t] = ft;
+          for (int t = 0; t < 2; ++t) {
+            const int k = kh0 + j + t;
+            float ft;
+            bool keep = true;
+            if (!kFast) {
+              const bool kon = (((j + t) < 32 ? kw0 : kw1) >> ((j + t) & 31)) & 1u;
+              keep = kon && (full_tile || (k >= iv.lo && k < iv.hi && k < p.Sk));
+            }
+            const float bv = (BIAS && keep) ? bias_at(p, b, g, h, q, k) : 0.f;
+            const float sc = bwd_score<MOD>(p, __uint_as_float(sv[j + t]), slope_l2, k, q_abs, ft, bv);
+            pr[t] = keep ? ex2(fmaf(sc, kBwdLog2e, -lse_l2)) : 0.f;
+            f[t] = ft;
+          }
+          pk[j >> 1] = pack_bf16(pr[0], pr[1]);
+          fk[j >> 1] = pack_bf16(f[0], f[1]);
         }
-        pk[j >> 1] = pack_bf16(pr[0], pr[1]);
-        fk[j >> 1] = pack_bf16(f[0], f[1]);
-      }
+      };
+      if (full_tile && (kw0 & kw1) == 0xFFFFFFFFu)
+        p_loop(BoolTag<true>{});
+      else
+        p_loop(BoolTag<false>{});
 #pragma unroll
       for (int c = 0; c < 64; c += 32) {            // dS = P (dP - Dvec) f -> TMEM slot + [32 + c/2, ...)
         uint32_t dp[32];
