@@ -102,29 +102,29 @@ __global__ void __launch_bounds__(256) bwd_gate_kernel(const AttnParams p, const
       }
       *reinterpret_cast<uint4*>(dar + c) = make_uint4(pa[0], pa[1], pa[2], pa[3]);
       if (dgr) *reinterpret_cast<uint4*>(dgr + c) = make_uint4(pg[0], pg[1], pg[2], pg[3]);
-      continue;
-    }
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const float o0 = bf16_lo(wo[t]), o1 = bf16_hi(wo[t]), d0 = bf16_lo(wd[t]), d1 = bf16_hi(wd[t]);
-      const float s0 = 1.f / (1.f + __expf(-bf16_lo(wg[t]))), s1 = 1.f / (1.f + __expf(-bf16_hi(wg[t])));
-      acc = fmaf(o0, d0, fmaf(o1, d1, acc));
-      pa[t] = pack_bf16(d0 * s0, d1 * s1);
-      pg[t] = pack_bf16(d0 * o0 * (1.f - s0), d1 * o1 * (1.f - s1));
-    }
-    *reinterpret_cast<uint4*>(dar + c) = make_uint4(pa[0], pa[1], pa[2], pa[3]);
-    if (dgr && p.grad_accum) {                        // second diff map: add to the first map's dgate
-      const uint4 u = *reinterpret_cast<const uint4*>(dgr + c);
-      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    } else {
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         const float o0 = bf16_lo(wo[t]), o1 = bf16_hi(wo[t]), d0 = bf16_lo(wd[t]), d1 = bf16_hi(wd[t]);
         const float s0 = 1.f / (1.f + __expf(-bf16_lo(wg[t]))), s1 = 1.f / (1.f + __expf(-bf16_hi(wg[t])));
-        pg[t] = pack_bf16(fmaf(d0 * o0, 1.f - s0, bf16_lo(w[t])), fmaf(d1 * o1, 1.f - s1, bf16_hi(w[t])));
+        acc = fmaf(o0, d0, fmaf(o1, d1, acc));
+        pa[t] = pack_bf16(d0 * s0, d1 * s1);
+        pg[t] = pack_bf16(d0 * o0 * (1.f - s0), d1 * o1 * (1.f - s1));
       }
-      *reinterpret_cast<uint4*>(dgr + c) = make_uint4(pg[0], pg[1], pg[2], pg[3]);
-    } else if (dgr) {
-      *reinterpret_cast<uint4*>(dgr + c) = make_uint4(pg[0], pg[1], pg[2], pg[3]);
+      *reinterpret_cast<uint4*>(dar + c) = make_uint4(pa[0], pa[1], pa[2], pa[3]);
+      if (dgr && p.grad_accum) {                        // second diff map: add to the first map's dgate
+        const uint4 u = *reinterpret_cast<const uint4*>(dgr + c);
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float o0 = bf16_lo(wo[t]), o1 = bf16_hi(wo[t]), d0 = bf16_lo(wd[t]), d1 = bf16_hi(wd[t]);
+          const float s0 = 1.f / (1.f + __expf(-bf16_lo(wg[t]))), s1 = 1.f / (1.f + __expf(-bf16_hi(wg[t])));
+          pg[t] = pack_bf16(fmaf(d0 * o0, 1.f - s0, bf16_lo(w[t])), fmaf(d1 * o1, 1.f - s1, bf16_hi(w[t])));
+        }
+        *reinterpret_cast<uint4*>(dgr + c) = make_uint4(pg[0], pg[1], pg[2], pg[3]);
+      } else if (dgr) {
+        *reinterpret_cast<uint4*>(dgr + c) = make_uint4(pg[0], pg[1], pg[2], pg[3]);
+      }
     }
   }
 #pragma unroll
