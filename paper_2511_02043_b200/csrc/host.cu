@@ -23,6 +23,7 @@ cudaError_t launch_attn_tc(const AttnParams& p, const TmaMaps& maps, cudaStream_
 cudaError_t launch_ipa_prep(const IpaParams& p, cudaStream_t s);
 cudaError_t launch_ipa_finish(const IpaParams& p, const float* lse, float* A, void* opair, float* op, cudaStream_t s);
 size_t ipa_out_smem(const IpaParams& p);
+int linear_nt_max();
 cudaError_t launch_linear(const LinParams& p, const CUtensorMap& tx, const CUtensorMap& tw, const CUtensorMap& ty,
                           int y_tma, cudaStream_t stream);
 cudaError_t launch_pack_keymask(const unsigned char* km, int64_t sb, int64_t sg, int64_t sk, int B, int G, int Sk,
@@ -1182,10 +1183,10 @@ fl_status fl_linear(const fl_linear_args* a) {
   int bg, bb;
   fl_status s;
   if ((s = encode_map(vx, 64, &tx, &bg, &bb)) != FL_OK) return s;
-  if ((s = encode_map(vw, 64, &tw, &bg, &bb)) != FL_OK) return s;
+  if ((s = encode_map(vw, 64, &tw, &bg, &bb, linear_nt_max())) != FL_OK) return s;   // W box: one tile of rows
   LinParams p;
   p.M = (int)M; p.N = (int)N; p.K = (int)K;
-  p.NT = N >= 128 ? 128 : (int)((N + 15) / 16 * 16);
+  p.NT = N >= linear_nt_max() ? linear_nt_max() : (int)((N + 15) / 16 * 16);
   p.bias = static_cast<const float*>(a->bias.data);
   p.ln_g = static_cast<const float*>(a->ln_gamma.data);
   p.ln_b = static_cast<const float*>(a->ln_beta.data);

@@ -23,20 +23,26 @@
 
 namespace fl {
 
-constexpr int kLinThreads = 192;
+constexpr int kLinThreads = 320;     // warps 0-3: rows [0, 128), 4: TMA, 5: MMA, 6-9: rows [128, 256)
+constexpr int kLinNT = 64;           // output columns per tile (TMEM accumulator width)
 
+// One CTA per 256 rows of x (two 128-row halves: every W tile brought into shared memory serves both, so
+// W -- re-read from L2 by every CTA -- moves half as often as with 128-row CTAs), 64-column output tiles,
+// W double-buffered, two TMEM accumulators per half (the epilogue of tile n overlaps the MMAs of n + 1).
 __global__ void __launch_bounds__(kLinThreads, 1)
     linear_ln_kernel(const __grid_constant__ LinParams p, const __grid_constant__ CUtensorMap tx,
                      const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap ty, int y_tma) {
+  (void)ty;
+  (void)y_tma;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int nkc = p.K / 64;                            // 64-column slabs
-  constexpr int kWSlab = 128 * 128;                    // 128 W rows (rows past N: TMA zero fill) x 128 B
-  uint8_t* sX = smem;                                  // [nkc][128 rows x 128 B]
-  uint8_t* sW = smem + nkc * 128 * 128;                // [2][nkc][kWSlab]
-  uint8_t* sY = sW + 2 * nkc * kWSlab;                // output staging for the TMA store: 2 slabs of 128 x 64
-  float* sBias = reinterpret_cast<float*>(sY + 2 * 128 * 128);   // [2][128]: the bias of tile nt (parity nt & 1)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sBias + 2 * 128);
+  constexpr int kXSlab = 128 * 128;                    // 128 X rows x 128 B
+  constexpr int kWSlab = kLinNT * 128;                 // 64 W rows (rows past N: TMA zero fill) x 128 B
+  uint8_t* sX = smem;                                  // [2 halves][nkc][kXSlab]
+  uint8_t* sW = smem + 2 * nkc * kXSlab;               // [2][nkc][kWSlab]
+  float* sBias = reinterpret_cast<float*>(sW + 2 * nkc * kWSlab);   // [2][64]: the bias of tile nt (parity nt & 1)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sBias + 2 * kLinNT);
   uint64_t* x_full = bars;
   uint64_t* ln_done = bars + 1;
   uint64_t* w_full = bars + 2;                         // [2]
@@ -45,22 +51,22 @@ __global__ void __launch_bounds__(kLinThreads, 1)
   uint64_t* acc_empty = bars + 8;                      // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * 128;
+  const int m0 = blockIdx.x * 256;
   const int n_nt = (p.N + p.NT - 1) / p.NT;
   const bool ln = p.ln_g != nullptr;
 
   if (threadIdx.x == 0) {
     mbar_init(x_full, 1);
-    mbar_init(ln_done, 128);
+    mbar_init(ln_done, 256);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&w_full[i], 1);
       mbar_init(&w_empty[i], 1);
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 128);
+      mbar_init(&acc_empty[i], 256);
     }
     fence_mbar_init();
   }
-  if (warp == 4) tmem_alloc<256>(tmem_slot);
+  if (warp == 4) tmem_alloc<4 * kLinNT>(tmem_slot);    // accumulator (half h, buffer b) at (2 h + b) * 64
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -70,8 +76,10 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     if (lane == 0) {                                   // ---- TMA producer
       tma_prefetch_desc(&tx);
       tma_prefetch_desc(&tw);
-      mbar_arrive_expect_tx(x_full, nkc * 128 * 128);
-      for (int c = 0; c < nkc; ++c) tma_load_5d(sX + c * 128 * 128, &tx, x_full, c * 64, m0, 0, 0, 0);
+      mbar_arrive_expect_tx(x_full, 2 * nkc * kXSlab);
+      for (int hf = 0; hf < 2; ++hf)                   // rows past M: TMA zero fill
+        for (int c = 0; c < nkc; ++c)
+          tma_load_5d(sX + (hf * nkc + c) * kXSlab, &tx, x_full, c * 64, m0 + 128 * hf, 0, 0, 0);
       for (int nt = 0; nt < n_nt; ++nt) {
         const int b = nt & 1;
         if (nt >= 2) mbar_wait(&w_empty[b], ((nt >> 1) - 1) & 1);
@@ -81,7 +89,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       }
     }
   } else if (warp == 5) {
-    if (lane == 0) {                                   // ---- MMA issuer: A = X, B = W tile (both K-major)
+    if (lane == 0) {                                   // ---- MMA issuer: A = X half, B = W tile (both K-major)
       mbar_wait(ln ? ln_done : x_full, 0);
       tc_fence_after();
       const uint32_t idesc = idesc_bf16_f32(128, (uint32_t)p.NT, 0);
@@ -91,18 +99,21 @@ __global__ void __launch_bounds__(kLinThreads, 1)
         mbar_wait(&w_full[b], (nt >> 1) & 1);
         if (nt >= 2) mbar_wait(&acc_empty[b], ((nt >> 1) - 1) & 1);
         tc_fence_after();
-        for (int kk = 0; kk < p.K / 16; ++kk) {
-          const uint32_t cx = (kk >> 2) * 128 * 128 + (kk & 3) * 32;
-          const uint32_t cw = (b * nkc + (kk >> 2)) * kWSlab + (kk & 3) * 32;
-          umma_ss(tmem + b * 128, smem_desc(xa + cx, 16, 1024, kLayoutSW128),
-                  smem_desc(wa + cw, 16, 1024, kLayoutSW128), idesc, kk > 0);
-        }
+        for (int hf = 0; hf < 2; ++hf)
+          for (int kk = 0; kk < p.K / 16; ++kk) {
+            const uint32_t cx = (hf * nkc + (kk >> 2)) * kXSlab + (kk & 3) * 32;
+            const uint32_t cw = (b * nkc + (kk >> 2)) * kWSlab + (kk & 3) * 32;
+            umma_ss(tmem + (2 * hf + b) * kLinNT, smem_desc(xa + cx, 16, 1024, kLayoutSW128),
+                    smem_desc(wa + cw, 16, 1024, kLayoutSW128), idesc, kk > 0);
+          }
         umma_commit(&w_empty[b]);
         umma_commit(&acc_full[b]);
       }
     }
   } else {
-    const int r = threadIdx.x;                         // row within the tile == TMEM lane
+    const int hf = warp >= 6 ? 1 : 0;                  // row half
+    const int r = 32 * (warp & 3) + lane;              // row within the half == TMEM lane
+    uint8_t* sXh = sX + hf * nkc * kXSlab;
     if (ln) {
       // LayerNorm of row r in place: 16-B piece pc of slab c sits at (pc ^ (r & 7)) * 16 (128-B swizzle)
       mbar_wait(x_full, 0);
@@ -110,7 +121,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       for (int c = 0; c < nkc; ++c)
 #pragma unroll
         for (int pc = 0; pc < 8; ++pc) {
-          const uint4 u = *reinterpret_cast<const uint4*>(sX + c * 16384 + r * 128 + ((pc ^ (r & 7)) << 4));
+          const uint4 u = *reinterpret_cast<const uint4*>(sXh + c * kXSlab + r * 128 + ((pc ^ (r & 7)) << 4));
           const uint32_t ww[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
           for (int t = 0; t < 4; ++t) s1 += bf16_lo(ww[t]) + bf16_hi(ww[t]);
@@ -120,7 +131,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       for (int c = 0; c < nkc; ++c)
 #pragma unroll
         for (int pc = 0; pc < 8; ++pc) {
-          const uint4 u = *reinterpret_cast<const uint4*>(sX + c * 16384 + r * 128 + ((pc ^ (r & 7)) << 4));
+          const uint4 u = *reinterpret_cast<const uint4*>(sXh + c * kXSlab + r * 128 + ((pc ^ (r & 7)) << 4));
           const uint32_t ww[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
@@ -132,7 +143,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       for (int c = 0; c < nkc; ++c)
 #pragma unroll
         for (int pc = 0; pc < 8; ++pc) {
-          uint4* a = reinterpret_cast<uint4*>(sX + c * 16384 + r * 128 + ((pc ^ (r & 7)) << 4));
+          uint4* a = reinterpret_cast<uint4*>(sXh + c * kXSlab + r * 128 + ((pc ^ (r & 7)) << 4));
           const uint4 u = *a;
           const uint32_t ww[4] = {u.x, u.y, u.z, u.w};
           uint32_t o[4];
@@ -154,34 +165,30 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       fence_proxy_async_smem();                        // generic stores -> the tensor core's reads
       mbar_arrive(ln_done);
     }
-    // ---- epilogue per column tile: row m0 + r, columns [n0, n0 + NT)
-    const int m = m0 + r;
+    // ---- epilogue per column tile: row m0 + 128 hf + r, columns [n0, n0 + NT)
+    const int m = m0 + 128 * hf + r;
     const bool row_ok = m < p.M;
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     __nv_bfloat16* yr = static_cast<__nv_bfloat16*>(p.y) + (int64_t)(row_ok ? m : 0) * p.ys_m;
     const bool vec = p.ys_n == 1 && (reinterpret_cast<uintptr_t>(p.y) % 16 == 0) && (p.ys_m % 8 == 0);
-    // coalesced epilogue: the tile is staged in shared memory (row = thread, swizzled 16-B chunks), then
-    // written back by consecutive threads along each row (16 threads x 16 B = one 256-B row segment)
-#ifdef FL_LIN_STAGED_STORE   // measured slower (QKVG projection 468 -> 540 us): opt-in
-    const bool y_co = !y_tma && vec && p.NT == 128;
-#else
-    const bool y_co = false;
-#endif
-    const bool stage = y_tma || y_co;
-    // the tile's bias in shared memory: thread r fetches column r of tile nt + 1 while tile nt is processed
-    // (a per-chunk global load stalled the epilogue on its latency: 19 % of the samples)
-    auto bias_of = [&](int nt2) { const int n = nt2 * p.NT + r; return (p.bias && r < p.NT && n < p.N) ? __ldg(p.bias + n) : 0.f; };
-    sBias[r] = bias_of(0);
+    // the tile's bias in shared memory: thread r < 64 of the first half fetches column r of tile nt + 1 while
+    // tile nt is processed (a per-chunk global load stalled the epilogue on its latency: 19 % of the samples)
+    const bool bias_thread = hf == 0 && r < p.NT;
+    auto bias_of = [&](int nt2) {
+      const int n = nt2 * p.NT + r;
+      return (bias_thread && p.bias && n < p.N) ? __ldg(p.bias + n) : 0.f;
+    };
+    if (hf == 0 && r < kLinNT) sBias[r] = bias_of(0);
     float bias_next = n_nt > 1 ? bias_of(1) : 0.f;
-    named_bar_sync(2, 128);
+    named_bar_sync(2, 256);
     for (int nt = 0; nt < n_nt; ++nt) {
       const int b = nt & 1, n0 = nt * p.NT;
-      const float* sb = sBias + b * 128;
+      const float* sb = sBias + b * kLinNT;
       mbar_wait(&acc_full[b], (nt >> 1) & 1);
       tc_fence_after();
       for (int c = 0; c < p.NT; c += 32) {
         uint32_t acc[32];
-        tmem_ld32(tmem + lane_base + b * 128 + c, acc);   // every lane loads (.sync.aligned)
+        tmem_ld32(tmem + lane_base + (2 * hf + b) * kLinNT + c, acc);   // every lane loads (.sync.aligned)
         tmem_wait_ld();
         float f[32];
 #pragma unroll
@@ -191,19 +198,6 @@ __global__ void __launch_bounds__(kLinThreads, 1)
           f[4 * t4 + 1] = __uint_as_float(acc[4 * t4 + 1]) + bb.y;
           f[4 * t4 + 2] = __uint_as_float(acc[4 * t4 + 2]) + bb.z;
           f[4 * t4 + 3] = __uint_as_float(acc[4 * t4 + 3]) + bb.w;
-        }
-        if (stage) {
-          // swizzled staging (slab c / 64, 16-B chunk q of row r at (q ^ (r & 7)) * 16): conflict-free; one
-          // TMA store per 64-column slab below writes whole rows (rows past M / columns past N are clipped)
-          uint8_t* srow = sY + (c >> 6) * 128 * 128 + r * 128;
-#pragma unroll
-          for (int t8 = 0; t8 < 4; ++t8) {
-            const int q = ((c & 63) >> 3) + t8;
-            *reinterpret_cast<uint4*>(srow + ((q ^ (r & 7)) << 4)) =
-                make_uint4(pack_bf16(f[8 * t8], f[8 * t8 + 1]), pack_bf16(f[8 * t8 + 2], f[8 * t8 + 3]),
-                           pack_bf16(f[8 * t8 + 4], f[8 * t8 + 5]), pack_bf16(f[8 * t8 + 6], f[8 * t8 + 7]));
-          }
-          continue;
         }
         if (!row_ok) continue;
         if (vec && c + 32 <= p.NT && n0 + c + 32 <= p.N) {
@@ -221,58 +215,28 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       tc_fence_before();
       mbar_arrive(&acc_empty[b]);                      // the accumulator may take tile nt + 2
       if (nt + 1 < n_nt) {                             // publish tile nt + 1's bias, fetch tile nt + 2's
-        sBias[((nt + 1) & 1) * 128 + r] = bias_next;
+        if (hf == 0 && r < kLinNT) sBias[((nt + 1) & 1) * kLinNT + r] = bias_next;
         bias_next = nt + 2 < n_nt ? bias_of(nt + 2) : 0.f;
-        named_bar_sync(2, 128);
-      }
-      if (y_co) {
-        named_bar_sync(1, 128);                        // the tile is staged
-#pragma unroll 4
-        for (int pass = 0; pass < 16; ++pass) {
-          const int row = pass * 8 + (r >> 4), q = r & 15, mm = m0 + row;
-          const uint4 v = *reinterpret_cast<const uint4*>(sY + (q >> 3) * 128 * 128 + row * 128 +
-                                                          (((q & 7) ^ (row & 7)) << 4));
-          if (mm < p.M) {
-            __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.y) + (int64_t)mm * p.ys_m + n0 + q * 8;
-            if (n0 + q * 8 + 8 <= p.N) {
-              *reinterpret_cast<uint4*>(dst) = v;
-            } else {
-              const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-              for (int e = 0; e < 8 && n0 + q * 8 + e < p.N; ++e)
-                dst[e] = __ushort_as_bfloat16((unsigned short)(e & 1 ? w[e >> 1] >> 16 : w[e >> 1] & 0xFFFFu));
-            }
-          }
-        }
-        named_bar_sync(1, 128);                        // the staging buffer is free for the next tile
-      }
-      if (y_tma) {
-        fence_proxy_async_smem();                      // staging stores -> the TMA engine
-        named_bar_sync(1, 128);
-        if (r == 0) {
-          for (int sl = 0; sl < (p.NT + 63) / 64 && n0 + sl * 64 < p.N; ++sl)
-            tma_store_5d(&ty, sY + sl * 128 * 128, n0 + sl * 64, m0, 0, 0, 0);
-          bulk_commit();
-          bulk_wait_read0();                           // the staging buffer is free again
-        }
-        named_bar_sync(1, 128);
+        named_bar_sync(2, 256);
       }
     }
-    if (y_tma && r == 0) bulk_wait0();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 4) tmem_dealloc<256>(tmem);
+  if (warp == 4) tmem_dealloc<4 * kLinNT>(tmem);
 }
 
-int linear_smem_bytes(int K) { return (K / 64) * 128 * 128 * 3 + 2 * 128 * 128 + 2 * 128 * 4 + 128 + 1024; }
+int linear_smem_bytes(int K) { return 2 * (K / 64) * 128 * 128 + 2 * (K / 64) * kLinNT * 128 + 2 * kLinNT * 4 + 128 + 1024; }
+int linear_nt_max() { return kLinNT; }
+int linear_rows_per_cta() { return 256; }
 
 cudaError_t launch_linear(const LinParams& p, const CUtensorMap& tx, const CUtensorMap& tw, const CUtensorMap& ty,
                           int y_tma, cudaStream_t stream) {
   const int smem = linear_smem_bytes(p.K);
   cudaError_t e = cudaFuncSetAttribute(linear_ln_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  linear_ln_kernel<<<(unsigned)((p.M + 127) / 128), kLinThreads, smem, stream>>>(p, tx, tw, ty, y_tma);
+  linear_ln_kernel<<<(unsigned)((p.M + 255) / 256), kLinThreads, smem, stream>>>(p, tx, tw, ty, y_tma);
   return cudaGetLastError();
 }
 
