@@ -1193,20 +1193,9 @@ fl_status fl_linear(const fl_linear_args* a) {
   p.eps = a->ln_eps;
   p.y = y.data;
   p.ys_m = y.stride[0]; p.ys_n = y.stride[1];
-  // row-contiguous y with 16-byte aligned rows: the epilogue stages each tile and TMA-stores whole rows
-  CUtensorMap ty;
-  memset(&ty, 0, sizeof ty);
-  int y_tma = 0;
-#ifdef FL_LIN_TMA_STORE   // measured slower (Evoformer block 0.87 -> 1.11 ms at N_seq 512): the per-tile
-                          // wait for the bulk store to release the staging buffer serialises the epilogue
-  if (y.stride[1] == 1 && aligned16(vy)) {
-#else
-  if (false) {
-#endif
-    const std::string saved = g_err;
-    y_tma = encode_map(vy, 64, &ty, &bg, &bb) == FL_OK;
-    g_err = saved;
-  }
+  CUtensorMap ty;                                  // (unused: the epilogue stores rows directly; a TMA-store
+  memset(&ty, 0, sizeof ty);                       //  epilogue measured slower, profiles/r02_ab.md)
+  const int y_tma = 0;
   const cudaError_t e = launch_linear(p, tx, tw, ty, y_tma, static_cast<cudaStream_t>(a->stream));
   ++g_launches;
   return e == cudaSuccess ? FL_OK : cuda_fail(e, "linear launch");
